@@ -1,0 +1,172 @@
+/*
+ * desklm_cuda.h -- C ABI of the B200-native RNNLM training / scoring path.
+ *
+ * This is the drop-in boundary between the desklm host API (C++ Trainer /
+ * Traits / Adapter, /root/reference/proj/include/desklm) and the sm_100a
+ * kernels in libdesklm_cuda.so.  Plain pointers and sizes only; every host
+ * array is borrowed for the duration of the call; all device memory is owned
+ * by the opaque context.  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj/include/desklm).
+ *
+ * Status codes mirror the reference's error classes (util.hpp:32-48,
+ * tools/desklm.cpp:1382-1390):
+ *   DL_OK 0, DL_EINVAL 1 (std::invalid_argument, CLI exit 1),
+ *   DL_EDATA 2 (DataError, CLI exit 2), DL_EDEVICE 3 (CUDA/NCCL failure).
+ * dl_last_error() returns the message of the last failure on that context
+ * (or the last global failure when ctx is NULL).
+ *
+ * Threading: one context per (host thread, GPU); calls on a context are
+ * serialised on its CUDA stream; value-returning calls synchronise.
+ */
+#ifndef DESKLM_CUDA_H
+#define DESKLM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dl_ctx dl_ctx;
+
+enum { DL_OK = 0, DL_EINVAL = 1, DL_EDATA = 2, DL_EDEVICE = 3 };
+
+/* Arithmetic of the GEMMs.  DL_FP32: fp32 SIMT kernels (parity mode,
+ * reference tolerance 1e-4).  DL_BF16: tcgen05/TMEM tensor-core kernels with
+ * bf16 operands, fp32 accumulation, fp32 master weights (throughput mode). */
+enum { DL_FP32 = 0, DL_BF16 = 1 };
+
+/* Activation (rnn.hpp:35: enum class Activation { kSigmoid, kTanh }). */
+enum { DL_SIGMOID = 0, DL_TANH = 1 };
+
+const char* dl_last_error(const dl_ctx* ctx);
+const char* dl_version(void);
+
+/* ---- model / optimiser state ------------------------------------------ */
+
+/* Replaces the StandardAdapter view construction (rnn.hpp:187-189) and
+ * RnnParams<float> storage (rnn.hpp:61-84): V x H W_in, H x H W_rec,
+ * V x H word-major W_out live in HBM for the context's lifetime. */
+int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act,
+              int precision);
+int dl_destroy(dl_ctx* ctx);
+
+/* Upload / download RnnParams<float> (row-major, W_out word-major V x H as
+ * in memory, rnn.hpp:61-77).  Download is what write_params (rnn.hpp:263)
+ * serialises. */
+int dl_set_params(dl_ctx* ctx, const float* w_in, const float* w_rec,
+                  const float* w_out);
+int dl_get_params(dl_ctx* ctx, float* w_in, float* w_rec, float* w_out);
+
+/* RmspropState (rmsprop.hpp:37-59): m_rec H x H, m_in V, m_out V. */
+int dl_set_opt(dl_ctx* ctx, const float* m_rec, const float* m_in,
+               const float* m_out, double rho, double eps);
+int dl_get_opt(dl_ctx* ctx, float* m_rec, float* m_in, float* m_out);
+
+/* ---- one truncated-BPTT window ----------------------------------------- */
+
+/* bptt_run<StandardAdapter<float>> in softmax mode (backprop.hpp:76-222,
+ * BpttOptions backprop.hpp:52-61, WindowBatch backprop.hpp:36-50):
+ * t-major (index t*B+b) inputs/targets/weights, h0 B x H, optional h_final.
+ * With compute_grads the clipped gradients stay on the device for
+ * dl_rmsprop / dl_get_grads.  *loss = scaled summed loss, *positions =
+ * unmasked count (BpttResult, backprop.hpp:63-66). */
+int dl_window(dl_ctx* ctx, int64_t T, int64_t B, const uint32_t* inputs,
+              const uint32_t* targets, const uint8_t* weights,
+              const float* h0, float* h_final, double loss_scale, float clip,
+              int compute_grads, double* loss, uint64_t* positions);
+
+/* Dense copies of the last window's clipped gradients (tests; the
+ * reference's StandardGrads, rnn.hpp:147-172, with SparseRowGrads::to_dense
+ * for W_in).  Any pointer may be NULL. */
+int dl_get_grads(dl_ctx* ctx, float* g_in_dense, float* g_rec, float* g_out);
+
+/* Test hook: load externally computed (already clipped) gradients in the
+ * reference's StandardGrads form -- sparse W_in rows (n_in_rows rows of H,
+ * words in_words), dense W_rec, dense W_out -- so rmsprop parity can be
+ * checked on identical inputs. */
+int dl_set_grads(dl_ctx* ctx, int64_t n_in_rows, const uint32_t* in_words,
+                 const float* in_rows, const float* g_rec, const float* g_out);
+
+/* rmsprop_update (rmsprop.hpp:113-133) with the device-resident gradients
+ * of the last dl_window.  *applied = 0 mirrors the reference's `false`
+ * (non-finite gradient: parameters and accumulators untouched). */
+int dl_rmsprop(dl_ctx* ctx, double eta, int* applied);
+
+/* ---- scoring ------------------------------------------------------------ */
+
+/* Lock-step forward scorer over S streams for `steps` steps (the inner loop
+ * of sharded_perplexity, eval.hpp:176-220; rnn_perplexity eval.hpp:84-145;
+ * the RNN half of rescore_nbest eval.hpp:725-751).  in[j*S+s] is the input
+ * id, tgt[j*S+s] the target id or -1 (not scored).  h0 (S x H) may be NULL
+ * for act(0).  logp (steps x S, NaN where skipped) and h_final may be NULL.
+ * Sums are over scored positions in (j, s) order. */
+int dl_score(dl_ctx* ctx, int64_t S, int64_t steps, const uint32_t* in,
+             const int64_t* tgt, const float* h0, float* h_final, double* logp,
+             double* total_logprob, uint64_t* predicted);
+
+/* sharded_perplexity (eval.hpp:151-222) and rnn_perplexity
+ * (eval.hpp:84-145) with the reference's argument meaning and errors. */
+int dl_sharded_perplexity(dl_ctx* ctx, const uint32_t* ids, int64_t n,
+                          int shards, uint32_t bos_id, double* total_logprob,
+                          uint64_t* predicted, double* perplexity);
+int dl_rnn_perplexity(dl_ctx* ctx, const uint32_t* ids, int64_t n,
+                      uint32_t bos_id, double* total_logprob,
+                      uint64_t* predicted, double* perplexity);
+
+/* ---- device-resident trainer (Trainer<Traits>::run_epoch) -------------- */
+
+/* Uploads the training IdStream once and sets up the offset-stream schedule
+ * of trainer.hpp:188-198 / :350-410: N = noffset*minibatch streams with
+ * cursors floor(i*L/N), hidden = act(0).  With a communicator of G ranks
+ * (dl_comm_init) the global minibatch is G*minibatch and this rank owns
+ * streams [rank*minibatch, (rank+1)*minibatch) of every group. */
+int dl_trainer_init(dl_ctx* ctx, const uint32_t* ids, int64_t L, int noffset,
+                    int minibatch, int unroll, double clip, uint32_t bos_id);
+
+/* Runs windows [first, first+count) of the epoch schedule (window w is
+ * group w % noffset), each = window build + bptt_run + rmsprop_update +
+ * hidden carry + cursor advance with wrap reset, entirely on the device
+ * (captured in a CUDA graph).  Adds the windows' losses (sum over windows)
+ * and skipped updates to the outputs. */
+int dl_trainer_run(dl_ctx* ctx, int64_t first, int64_t count, double eta,
+                   double* loss_sum, uint64_t* skipped);
+
+/* Schedule state for checkpoints (RTRN cursors + hidden, trainer.hpp:286-288).
+ * Arrays cover this rank's streams (N/G of them, group-major). */
+int dl_trainer_get_state(dl_ctx* ctx, int64_t* cursors, float* hidden);
+int dl_trainer_set_state(dl_ctx* ctx, const int64_t* cursors,
+                         const float* hidden);
+
+/* ---- multi-GPU ----------------------------------------------------------- */
+
+/* NCCL communicator for data-parallel streams (gradient allreduce before
+ * clip).  Rank 0 calls dl_comm_unique_id and broadcasts the 128 bytes. */
+int dl_comm_unique_id(uint8_t id[128]);
+int dl_comm_init(dl_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+
+/* ---- instrumentation ----------------------------------------------------- */
+
+/* Test hook for the GEMM engine behind every matmul_* of mat.hpp:116-184:
+ * C[M x N] = A . B^T with A K-major [M x K] (a_major 0) or MN-major [K x M]
+ * (1), likewise B ([N x K] / [K x N]); fp32 host data (rounded to bf16 in
+ * DL_BF16 mode).  splits > 1 exercises split-K.  With tgt != NULL (DL_BF16)
+ * the online-LSE logits epilogue runs and Cout receives M*N bf16 logits
+ * (widened), then M log-probs of tgt, then M target logits. */
+int dl_test_gemm(dl_ctx* ctx, int M, int N, int K, int a_major, int b_major,
+                 const float* A, const float* B, float* Cout, int splits,
+                 const uint32_t* tgt);
+
+/* Kernel launches issued on the context's streams since creation. */
+uint64_t dl_launch_count(const dl_ctx* ctx);
+/* Average device time (ms) of the named kernel class over the last
+ * dl_trainer_run / dl_window when profiling is on ("logits", "dh", "dw_out",
+ * "recurrence", "rmsprop", ...); returns -1 if unknown. */
+int dl_set_profiling(dl_ctx* ctx, int on);
+double dl_kernel_ms(const dl_ctx* ctx, const char* name);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DESKLM_CUDA_H */

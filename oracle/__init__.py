@@ -1,0 +1,389 @@
+"""TEST INFRASTRUCTURE ONLY -- the CPU checker for the RNNLM hot path.
+
+Two interchangeable back ends with one numpy-facing API:
+
+* ``Orc``  -- ``oracle/liborc.so``: a plain-C restatement of the reference
+  algorithm (``oracle/desklm_oracle.c``, every function cites the reference
+  file:line it restates).
+* ``Ref``  -- ``oracle/_ref/libdesklm_ref.so``: the unmodified reference
+  headers (``/root/reference/proj/include``) compiled behind a C shim
+  (``oracle/ref_shim.cpp``).  Built here; the prebuilt ``.so`` travels to
+  the GPU box, where ``/root/reference`` itself does not exist.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+leg may import this package; the product library never calls it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+ORC_SO = os.path.join(_HERE, "liborc.so")
+REF_SO = os.path.join(_HERE, "_ref", "libdesklm_ref.so")
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+_i64 = C.c_int64
+_u64 = C.c_uint64
+
+
+class TrainConfig(C.Structure):
+    """Field order of the RTRN config echo (trainer.hpp:412-432); defaults
+    follow TrainConfig (trainer.hpp:43-63) except mode=softmax."""
+
+    _fields_ = [
+        ("nstate", C.c_int64), ("nproj", C.c_int64),
+        ("noffset", C.c_int32), ("minibatch", C.c_int32),
+        ("unroll", C.c_int32), ("mode", C.c_int32),
+        ("eta", C.c_double), ("rho", C.c_double), ("eps", C.c_double),
+        ("clip", C.c_double), ("nce_k", C.c_int32), ("max_epochs", C.c_int32),
+        ("noise_floor", C.c_double), ("seed", C.c_uint64),
+        ("act", C.c_int32), ("valid_shards", C.c_int32),
+        ("divergence_factor", C.c_double), ("valid_limit", C.c_int64),
+        ("init_range", C.c_double), ("threads", C.c_int32), ("pad_", C.c_int32),
+    ]
+
+    def __init__(self, **kw):
+        d = dict(nstate=256, nproj=0, noffset=128, minibatch=8, unroll=16,
+                 mode=1, eta=1e-3, rho=0.9995, eps=1e-6, clip=1.0, nce_k=64,
+                 max_epochs=20, noise_floor=1e-8, seed=1, act=0,
+                 valid_shards=8, divergence_factor=10.0, valid_limit=0,
+                 init_range=0.1, threads=1, pad_=0)
+        d.update(kw)
+        super().__init__(**d)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile liborc.so (and _ref when /root/reference is present)."""
+    out = subprocess.run(["make", "-C", _HERE], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+class _Backend:
+    prefix = ""
+    so_path = ""
+
+    def __init__(self):
+        if not os.path.exists(self.so_path):
+            raise FileNotFoundError(f"{self.so_path} not built (make -C oracle)")
+        self.lib = C.CDLL(self.so_path)
+        p = self.prefix
+        L = self.lib
+        self._bptt = getattr(L, p + "bptt")
+        self._bptt.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _i64, _i64,
+                               _u32p, _u32p, _u8p, _f32p, C.c_double, C.c_float,
+                               C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                               C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._rms = getattr(L, p + "rmsprop")
+        self._rms.argtypes = [_i64, _i64, _f32p, _f32p, _f32p, _f32p, _f32p, _f32p,
+                              C.c_double, C.c_double, C.c_double, _i64, _vp, _vp,
+                              _f32p, C.c_int, _i64, _vp, _vp, C.POINTER(C.c_int)]
+        self._init = getattr(L, p + "init_uniform")
+        self._init.argtypes = [_i64, _i64, _u64, C.c_double, _f32p, _f32p, _f32p]
+        self._rs = getattr(L, p + "random_stream")
+        self._rs.restype = C.c_int64
+        self._rs.argtypes = [_u64, _u64, _u64, _u64, _vp, _u64]
+        self._rsp = getattr(L, p + "random_stream_pair")
+        self._rsp.argtypes = [_u64, _u64, _u64, _u64, _vp, _u64, C.POINTER(C.c_int64),
+                              _vp, _u64, C.POINTER(C.c_int64)]
+        self._sppl = getattr(L, p + "sharded_ppl")
+        self._sppl.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64,
+                               C.c_int, C.c_uint32, C.c_int, C.POINTER(C.c_double),
+                               C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        self._rppl = getattr(L, p + "rnn_ppl")
+        self._rppl.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64,
+                               C.c_uint32, C.c_int, C.POINTER(C.c_double),
+                               C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = ""
+            if hasattr(self.lib, "ref_last_error"):
+                self.lib.ref_last_error.restype = C.c_char_p
+                msg = self.lib.ref_last_error().decode()
+            raise OracleError(rc, msg)
+
+    # ---- data helpers
+    def init_uniform(self, V, H, seed, rng=0.1):
+        w_in = np.empty((V, H), np.float32)
+        w_rec = np.empty((H, H), np.float32)
+        w_out = np.empty((V, H), np.float32)
+        self._check(self._init(V, H, seed, rng, w_in, w_rec, w_out))
+        return w_in, w_rec, w_out
+
+    def random_stream(self, seed, v, min_tokens, max_len=12):
+        n = self._rs(seed, v, min_tokens, max_len, None, 0)
+        out = np.empty(n, np.uint32)
+        self._rs(seed, v, min_tokens, max_len, out.ctypes.data, n)
+        return out
+
+    def random_stream_pair(self, seed, v, min_a, min_b):
+        la, lb = C.c_int64(), C.c_int64()
+        cap = 2 * (min_a + min_b) + 64
+        a = np.empty(cap, np.uint32)
+        b = np.empty(cap, np.uint32)
+        self._check(self._rsp(seed, v, min_a, min_b, a.ctypes.data, cap, C.byref(la),
+                              b.ctypes.data, cap, C.byref(lb)))
+        return a[: la.value].copy(), b[: lb.value].copy()
+
+    # ---- hot path
+    def bptt(self, params, act, inputs, targets, weights, h0, loss_scale=1.0,
+             clip=3.4028234663852886e38, compute_grads=True, threads=1):
+        """bptt_run softmax mode.  Returns dict(loss, positions, h_final,
+        g_in_words, g_in_rows (slot order), g_in_dense, g_rec, g_out)."""
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        T, B = inputs.shape
+        hf = np.empty((B, H), np.float32)
+        nrows = C.c_int64(0)
+        gw = np.zeros(T * B, np.uint32)
+        gd = np.zeros((T * B, H), np.float32)
+        grec = np.zeros((H, H), np.float32)
+        gout = np.zeros((V, H), np.float32)
+        loss, pos = C.c_double(), C.c_uint64()
+        self._check(self._bptt(V, H, act, w_in, w_rec, w_out, T, B,
+                               np.ascontiguousarray(inputs, np.uint32),
+                               np.ascontiguousarray(targets, np.uint32),
+                               np.ascontiguousarray(weights, np.uint8),
+                               np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                               int(compute_grads), threads, hf.ctypes.data,
+                               C.addressof(nrows), gw.ctypes.data, gd.ctypes.data,
+                               grec.ctypes.data, gout.ctypes.data, C.byref(loss),
+                               C.byref(pos)))
+        r = dict(loss=loss.value, positions=pos.value, h_final=hf)
+        if compute_grads:
+            n = nrows.value
+            dense = np.zeros((V, H), np.float32)
+            for s in range(n):
+                dense[gw[s]] += gd[s]
+            r.update(g_in_words=gw[:n].copy(), g_in_rows=gd[:n].copy(),
+                     g_in_dense=dense, g_rec=grec, g_out=gout)
+        return r
+
+    def rmsprop(self, params, state, grads, rho, eps, eta, out_dense=True):
+        """rmsprop_update in place on copies; returns (params, state, applied)."""
+        w_in, w_rec, w_out = [np.array(x, np.float32, copy=True) for x in params]
+        m_rec, m_in, m_out = [np.array(x, np.float32, copy=True) for x in state]
+        V, H = w_in.shape
+        words = np.ascontiguousarray(grads["g_in_words"], np.uint32)
+        rows = np.ascontiguousarray(grads["g_in_rows"], np.float32)
+        applied = C.c_int()
+        if out_dense:
+            gout = np.ascontiguousarray(grads["g_out"], np.float32)
+            ow, on = None, 0
+        else:
+            ow = np.ascontiguousarray(grads["g_out_words"], np.uint32)
+            gout = np.ascontiguousarray(grads["g_out_rows"], np.float32)
+            on = len(ow)
+        self._check(self._rms(V, H, w_in, w_rec, w_out, m_rec, m_in, m_out, rho, eps,
+                              eta, len(words), words.ctypes.data, rows.ctypes.data,
+                              np.ascontiguousarray(grads["g_rec"], np.float32),
+                              int(out_dense), on,
+                              None if ow is None else ow.ctypes.data,
+                              gout.ctypes.data, C.byref(applied)))
+        return (w_in, w_rec, w_out), (m_rec, m_in, m_out), bool(applied.value)
+
+    def sharded_ppl(self, params, act, ids, shards, bos=1):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        tl, pr, ppl = C.c_double(), C.c_uint64(), C.c_double()
+        ids = np.ascontiguousarray(ids, np.uint32)
+        self._check(self._sppl(V, H, act, w_in, w_rec, w_out, ids, len(ids), shards,
+                               bos, 1, C.byref(tl), C.byref(pr), C.byref(ppl)))
+        return dict(total_logprob=tl.value, predicted=pr.value, perplexity=ppl.value)
+
+    def rnn_ppl(self, params, act, ids, bos=1):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        tl, pr, ppl = C.c_double(), C.c_uint64(), C.c_double()
+        ids = np.ascontiguousarray(ids, np.uint32)
+        self._check(self._rppl(V, H, act, w_in, w_rec, w_out, ids, len(ids), bos, 1,
+                               C.byref(tl), C.byref(pr), C.byref(ppl)))
+        return dict(total_logprob=tl.value, predicted=pr.value, perplexity=ppl.value)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"oracle status {code}: {msg}")
+        self.code = code
+
+
+class Orc(_Backend):
+    """The C restatement (oracle/desklm_oracle.c)."""
+
+    prefix = "orc_"
+    so_path = ORC_SO
+
+    def __init__(self):
+        super().__init__()
+        L = self.lib
+        self._slp = L.orc_sharded_logprobs
+        self._slp.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64,
+                              C.c_int, C.c_uint32, _vp, _i64, C.POINTER(C.c_int64),
+                              C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                              C.POINTER(C.c_uint64)]
+        self._wb = L.orc_window_build
+        self._wb.argtypes = [_u32p, _i64, _i64p, _i64, _i64, _i64, C.c_uint32,
+                             _u32p, _u32p, _u8p]
+        self._train = L.orc_train
+        self._train.argtypes = [C.POINTER(TrainConfig), _i64, _f32p, _f32p, _f32p,
+                                _u32p, _i64, _u32p, _i64, C.c_int, _f32p, _f32p,
+                                _f32p, _i64p, _f32p, _f64p, C.POINTER(C.c_int),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)]
+
+    def sharded_logprobs(self, params, act, ids, shards, bos=1):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        ids = np.ascontiguousarray(ids, np.uint32)
+        S, steps = C.c_int64(), C.c_int64()
+        tl, pr = C.c_double(), C.c_uint64()
+        n = len(ids)
+        Smax = min(shards, n // 2)
+        cap = (n // max(Smax, 1) + 2) * max(Smax, 1)
+        out = np.empty(cap, np.float64)
+        self._check(self._slp(V, H, act, w_in, w_rec, w_out, ids, n, shards, bos,
+                              out.ctypes.data, cap, C.byref(S), C.byref(steps),
+                              C.byref(tl), C.byref(pr)))
+        return out[: S.value * steps.value].reshape(steps.value, S.value).copy()
+
+    def window_build(self, ids, cursors, s0, B, T, bos=1):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        cur = np.ascontiguousarray(cursors, np.int64)
+        x = np.empty((T, B), np.uint32)
+        y = np.empty((T, B), np.uint32)
+        w = np.empty((T, B), np.uint8)
+        self._wb(ids, len(ids), cur, s0, B, T, bos, x, y, w)
+        return x, y, w
+
+    def train(self, cfg: TrainConfig, params, train_ids, valid_ids, run=True):
+        w_in, w_rec, w_out = [np.array(x, np.float32, copy=True) for x in params]
+        V, H = w_in.shape
+        N = cfg.noffset * cfg.minibatch
+        m_rec = np.zeros((H, H), np.float32)
+        m_in = np.zeros(V, np.float32)
+        m_out = np.zeros(V, np.float32)
+        cur = np.zeros(N, np.int64)
+        hid = np.zeros((N, H), np.float32)
+        logs = np.zeros((max(cfg.max_epochs, 1), 7), np.float64)
+        nl, bad, ep = C.c_int(), C.c_int(), C.c_int()
+        ini, eta, best = C.c_double(), C.c_double(), C.c_double()
+        tr = np.ascontiguousarray(train_ids, np.uint32)
+        va = np.ascontiguousarray(valid_ids, np.uint32)
+        rc = self._train(C.byref(cfg), V, w_in, w_rec, w_out, tr, len(tr), va, len(va),
+                         int(run), m_rec, m_in, m_out, cur, hid, logs, C.byref(nl),
+                         C.byref(ini), C.byref(eta), C.byref(best), C.byref(bad),
+                         C.byref(ep))
+        if rc not in (0,):
+            raise OracleError(rc, "orc_train")
+        return dict(params=(w_in, w_rec, w_out), opt=(m_rec, m_in, m_out),
+                    cursors=cur, hidden=hid, logs=logs[: nl.value].copy(),
+                    initial_ppl=ini.value, eta=eta.value, best_ppl=best.value,
+                    bad_epochs=bad.value, epoch=ep.value)
+
+
+class Ref(_Backend):
+    """The reference itself (oracle/_ref/libdesklm_ref.so)."""
+
+    prefix = "ref_"
+    so_path = REF_SO
+
+    def __init__(self):
+        super().__init__()
+        L = self.lib
+        self._slp = L.ref_sharded_logprobs
+        self._slp.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64,
+                              C.c_int, C.c_uint32, _vp, _i64, C.POINTER(C.c_int64),
+                              C.POINTER(C.c_int64)]
+        self._train = L.ref_train
+        self._train.argtypes = [C.POINTER(TrainConfig), _i64, _f32p, _f32p, _f32p,
+                                _u32p, _i64, _u32p, _i64, C.c_int, _vp, _u64,
+                                C.POINTER(C.c_uint64), _f64p, C.POINTER(C.c_int),
+                                C.POINTER(C.c_double)]
+        self._wp = L.ref_write_params
+        self._wp.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _vp, _u64,
+                             C.POINTER(C.c_uint64)]
+        self._wr = L.ref_write_rmsprop
+        self._wr.argtypes = [_i64, _i64, C.c_double, C.c_double, _f32p, _f32p, _f32p,
+                             _vp, _u64, C.POINTER(C.c_uint64)]
+        self._rescore = L.ref_rescore
+        self._rescore.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p,
+                                  C.c_char_p, C.c_double, C.c_double, C.c_int, _vp,
+                                  _u64, C.POINTER(C.c_uint64)]
+
+    def sharded_logprobs(self, params, act, ids, shards, bos=1):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        ids = np.ascontiguousarray(ids, np.uint32)
+        n = len(ids)
+        Smax = min(shards, n // 2)
+        cap = (n // max(Smax, 1) + 2) * max(Smax, 1)
+        out = np.empty(cap, np.float64)
+        S, steps = C.c_int64(), C.c_int64()
+        self._check(self._slp(V, H, act, w_in, w_rec, w_out, ids, n, shards, bos,
+                              out.ctypes.data, cap, C.byref(S), C.byref(steps)))
+        return out[: S.value * steps.value].reshape(steps.value, S.value).copy()
+
+    def train(self, cfg: TrainConfig, params, train_ids, valid_ids, run=True):
+        """Returns (rtrn_bytes, logs[n,7], initial_ppl)."""
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        tr = np.ascontiguousarray(train_ids, np.uint32)
+        va = np.ascontiguousarray(valid_ids, np.uint32)
+        N = cfg.noffset * cfg.minibatch
+        cap = 4096 + 8 * N + 4 * N * H + 8 * (2 * V * H + H * H) + 64 * V + 8 * V
+        buf = np.zeros(cap, np.uint8)
+        ln = C.c_uint64()
+        logs = np.zeros((max(cfg.max_epochs, 1), 7), np.float64)
+        nl = C.c_int()
+        ini = C.c_double()
+        self._check(self._train(C.byref(cfg), V, w_in, w_rec, w_out, tr, len(tr), va,
+                                len(va), int(run), buf.ctypes.data, cap, C.byref(ln),
+                                logs, C.byref(nl), C.byref(ini)))
+        return bytes(buf[: ln.value]), logs[: nl.value].copy(), ini.value
+
+    def write_params(self, params, act=0):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        ln = C.c_uint64()
+        self._wp(V, H, act, w_in, w_rec, w_out, None, 0, C.byref(ln))
+        buf = np.zeros(ln.value, np.uint8)
+        self._check(self._wp(V, H, act, w_in, w_rec, w_out, buf.ctypes.data, ln.value,
+                             C.byref(ln)))
+        return bytes(buf)
+
+    def write_rmsprop(self, V, H, rho, eps, state):
+        m_rec, m_in, m_out = [np.ascontiguousarray(x, np.float32) for x in state]
+        ln = C.c_uint64()
+        self._wr(V, H, rho, eps, m_rec, m_in, m_out, None, 0, C.byref(ln))
+        buf = np.zeros(ln.value, np.uint8)
+        self._check(self._wr(V, H, rho, eps, m_rec, m_in, m_out, buf.ctypes.data,
+                             ln.value, C.byref(ln)))
+        return bytes(buf)
+
+    def rescore(self, params, act, nbest_text, lm_scale=1.0, wip=0.0, fast=False):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        cap = 4 * len(nbest_text) + 1 << 16
+        buf = C.create_string_buffer(cap)
+        ln = C.c_uint64()
+        self._check(self._rescore(V, H, act, w_in, w_rec, w_out, nbest_text.encode(),
+                                  lm_scale, wip, int(fast), C.addressof(buf), cap,
+                                  C.byref(ln)))
+        return buf.value.decode()
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)

@@ -1,0 +1,678 @@
+/*
+ * oracle/desklm_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference desklm algorithm for the RNNLM
+ * training/scoring hot path.  It is the *checker* the parity tests compare
+ * the CUDA path against (and the "port" CPU baseline); it is never linked
+ * into, called by, or used as a fallback for the product library
+ * (paper_1502_00512_b200/libdesklm_cuda.so).
+ *
+ * Pinning: every function here is checked bit-for-bit against the reference
+ * itself, compiled from /root/reference/proj/include into oracle/_ref
+ * (oracle/ref_shim.cpp) with the same flags (-O3 -ffp-contract=off), and
+ * against the committed golden vectors in tests/golden/ (tests/test_oracle.py).
+ *
+ * Reference anchors (all paths relative to /root/reference/proj/include/desklm):
+ *   mt19937_64 / uniform01 / uniform / uniform_index   rng.hpp:37-50
+ *   random_stream (test fixture)                       ../../tests/oracles/helpers.hpp:36-52
+ *   RnnParams::init_uniform                            rnn.hpp:79-83
+ *   activate / activate_deriv                          rnn.hpp:37-49
+ *   dot_acc (8 fixed double lanes + tail)              mat.hpp:59-78
+ *   matmul_nt / matmul_nn / matmul_tn_add              mat.hpp:116-184
+ *   bptt_run, softmax branch                           backprop.hpp:76-222
+ *   StandardGrads::clip / SparseRowGrads               rnn.hpp:89-162
+ *   rmsprop_update (+ sparse / dense row updates)      rmsprop.hpp:77-133
+ *   sharded_perplexity / lse_column                    eval.hpp:48-57, 151-222
+ *   rnn_perplexity                                     eval.hpp:84-145
+ *   Trainer ctor / train / run_epoch / validate        trainer.hpp:178-270, 350-410
+ *
+ * Status codes: 0 ok, 1 invalid argument, 2 data error.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ rng */
+/* std::mt19937_64 (fully specified by the C++ standard). */
+typedef struct {
+  uint64_t x[312];
+  int p;
+} orc_mt64;
+
+void orc_mt_seed(orc_mt64* m, uint64_t seed) {
+  m->x[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    m->x[i] = 6364136223846793005ULL * (m->x[i - 1] ^ (m->x[i - 1] >> 62)) +
+              (uint64_t)i;
+  m->p = 312;
+}
+
+static void mt_twist(orc_mt64* m) {
+  const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
+  const uint64_t MAT = 0xB5026F5AA96619E9ULL;
+  for (int i = 0; i < 312; ++i) {
+    const uint64_t y = (m->x[i] & UM) | (m->x[(i + 1) % 312] & LM);
+    m->x[i] = m->x[(i + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? MAT : 0ULL);
+  }
+  m->p = 0;
+}
+
+uint64_t orc_mt_next(orc_mt64* m) {
+  if (m->p >= 312) mt_twist(m);
+  uint64_t z = m->x[m->p++];
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  z ^= z >> 43;
+  return z;
+}
+
+/* rng.hpp:37-50 */
+static double uniform01(orc_mt64* m) {
+  return (double)(orc_mt_next(m) >> 11) * 0x1.0p-53;
+}
+static double uniform(orc_mt64* m, double lo, double hi) {
+  return lo + (hi - lo) * uniform01(m);
+}
+static uint64_t uniform_index(orc_mt64* m, uint64_t n) {
+  return (uint64_t)(uniform01(m) * (double)n);
+}
+
+/* rnn.hpp:79-83: one generator, w_in then w_rec then w_out, row-major. */
+int orc_init_uniform(int64_t V, int64_t H, uint64_t seed, double range,
+                     float* w_in, float* w_rec, float* w_out) {
+  if (V < 1 || H < 1) return 1;
+  orc_mt64 m;
+  orc_mt_seed(&m, seed);
+  for (int64_t i = 0; i < V * H; ++i) w_in[i] = (float)uniform(&m, -range, range);
+  for (int64_t i = 0; i < H * H; ++i) w_rec[i] = (float)uniform(&m, -range, range);
+  for (int64_t i = 0; i < V * H; ++i) w_out[i] = (float)uniform(&m, -range, range);
+  return 0;
+}
+
+/* helpers.hpp:36-52 on an existing generator.  Returns the length; writes at
+ * most cap ids. */
+static int64_t random_stream_rng(orc_mt64* m, uint64_t v, uint64_t min_tokens,
+                                 uint64_t max_len, uint32_t* out, uint64_t cap) {
+  const uint64_t body = v - 3;
+  uint64_t n = 0;
+#define PUSH(val)                     \
+  do {                                \
+    if (n < cap) out[n] = (val);      \
+    ++n;                              \
+  } while (0)
+  while (n < min_tokens) {
+    PUSH(1u);
+    const uint64_t len = 1 + uniform_index(m, max_len);
+    for (uint64_t i = 0; i < len; ++i) {
+      const uint32_t r1 = (uint32_t)uniform_index(m, body);
+      const uint32_t r2 = (uint32_t)uniform_index(m, body);
+      PUSH(3u + (r1 < r2 ? r1 : r2));
+    }
+    PUSH(2u);
+  }
+#undef PUSH
+  return (int64_t)n;
+}
+
+int64_t orc_random_stream(uint64_t seed, uint64_t v, uint64_t min_tokens,
+                          uint64_t max_len, uint32_t* out, uint64_t cap) {
+  orc_mt64 m;
+  orc_mt_seed(&m, seed);
+  return random_stream_rng(&m, v, min_tokens, max_len, out, cap);
+}
+
+int orc_random_stream_pair(uint64_t seed, uint64_t v, uint64_t min_a,
+                           uint64_t min_b, uint32_t* out_a, uint64_t cap_a,
+                           int64_t* len_a, uint32_t* out_b, uint64_t cap_b,
+                           int64_t* len_b) {
+  orc_mt64 m;
+  orc_mt_seed(&m, seed);
+  *len_a = random_stream_rng(&m, v, min_a, 12, out_a, cap_a);
+  *len_b = random_stream_rng(&m, v, min_b, 12, out_b, cap_b);
+  return 0;
+}
+
+/* ----------------------------------------------------------- dense math */
+/* mat.hpp:59-78 */
+static double dot_acc(const float* x, const float* y, int64_t n) {
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, s7 = 0;
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    s0 += (double)x[i + 0] * (double)y[i + 0];
+    s1 += (double)x[i + 1] * (double)y[i + 1];
+    s2 += (double)x[i + 2] * (double)y[i + 2];
+    s3 += (double)x[i + 3] * (double)y[i + 3];
+    s4 += (double)x[i + 4] * (double)y[i + 4];
+    s5 += (double)x[i + 5] * (double)y[i + 5];
+    s6 += (double)x[i + 6] * (double)y[i + 6];
+    s7 += (double)x[i + 7] * (double)y[i + 7];
+  }
+  double tail = 0;
+  for (; i < n; ++i) tail += (double)x[i] * (double)y[i];
+  return ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) + tail;
+}
+
+/* C[MxN] = A[MxK] . B[NxK]^T, rounded to float (mat.hpp:116-134). */
+static void matmul_nt(const float* A, const float* B, float* C, int64_t M,
+                      int64_t N, int64_t K) {
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < N; ++j) C[i * N + j] = (float)dot_acc(A + i * K, B + j * K, K);
+}
+
+/* C[MxN] (=|+=) A[MxK] . B[KxN] with a double row accumulator; zero A
+ * entries are skipped (mat.hpp:136-166). */
+static void matmul_nn(const float* A, const float* B, float* C, int64_t M,
+                      int64_t N, int64_t K, int accumulate, double* acc) {
+  for (int64_t i = 0; i < M; ++i) {
+    for (int64_t j = 0; j < N; ++j) acc[j] = accumulate ? (double)C[i * N + j] : 0.0;
+    for (int64_t k = 0; k < K; ++k) {
+      const double a = (double)A[i * K + k];
+      if (a == 0.0) continue;
+      const float* bk = B + k * N;
+      for (int64_t j = 0; j < N; ++j) acc[j] += a * (double)bk[j];
+    }
+    for (int64_t j = 0; j < N; ++j) C[i * N + j] = (float)acc[j];
+  }
+}
+
+/* C[MxN] += A[KxM]^T . B[KxN], float accumulate, k outer (mat.hpp:168-184). */
+static void matmul_tn_add(const float* A, const float* B, float* C, int64_t K,
+                          int64_t M, int64_t N) {
+  for (int64_t k = 0; k < K; ++k) {
+    const float* ak = A + k * M;
+    const float* bk = B + k * N;
+    for (int64_t i = 0; i < M; ++i) {
+      const float a = ak[i];
+      if (a == 0.0f) continue;
+      float* ci = C + i * N;
+      for (int64_t j = 0; j < N; ++j) ci[j] += a * bk[j];
+    }
+  }
+}
+
+/* rnn.hpp:37-49 (float instantiation) */
+static float act_f(int act, float x) {
+  if (act == 0) return 1.0f / (1.0f + expf(-x));
+  return tanhf(x);
+}
+static float act_deriv_f(int act, float y) {
+  if (act == 0) return y * (1.0f - y);
+  return 1.0f - y * y;
+}
+
+/* std::min(c, std::max(-c, x)) -- note a NaN becomes -c (rnn.hpp:131-134). */
+static float clip1(float x, float c) {
+  const float t = (-c < x) ? x : -c;
+  return (t < c) ? t : c;
+}
+
+/* ------------------------------------------------------------- bptt_run */
+/* Softmax-mode window (backprop.hpp:76-222).  Sparse W_in gradient is
+ * reported in slot (first-touch) order like SparseRowGrads; g_in_words and
+ * g_in_data must hold T*B rows. */
+int orc_bptt(int64_t V, int64_t H, int act, const float* w_in,
+             const float* w_rec, const float* w_out, int64_t T, int64_t B,
+             const uint32_t* inputs, const uint32_t* targets,
+             const uint8_t* weights, const float* h0, double loss_scale,
+             float clip, int compute_grads, int threads, float* h_final,
+             int64_t* g_in_rows, uint32_t* g_in_words, float* g_in_data,
+             float* g_rec, float* g_out, double* loss, uint64_t* positions) {
+  (void)threads;
+  if (T < 1 || B < 1) return 1;
+  const int64_t BH = B * H;
+  float* h = (float*)malloc(sizeof(float) * (T + 1) * BH);
+  float* pre = (float*)malloc(sizeof(float) * BH);
+  float* scores = (float*)malloc(sizeof(float) * B * V);
+  float* dsc = compute_grads ? (float*)calloc((size_t)(T * B * V), sizeof(float)) : NULL;
+  memcpy(h, h0, sizeof(float) * BH);
+  /* forward (backprop.hpp:97-115) */
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(h + t * BH, w_rec, pre, B, H, H);
+    for (int64_t b = 0; b < B; ++b) {
+      const float* e = w_in + (int64_t)inputs[t * B + b] * H;
+      for (int64_t i = 0; i < H; ++i) pre[b * H + i] += e[i];
+    }
+    for (int64_t i = 0; i < BH; ++i) h[(t + 1) * BH + i] = act_f(act, pre[i]);
+  }
+  if (h_final) memcpy(h_final, h + T * BH, sizeof(float) * BH);
+  /* softmax loss (backprop.hpp:157-189) */
+  double L = 0.0;
+  uint64_t pos = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(h + (t + 1) * BH, w_out, scores, B, V, H);
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t idx = t * B + b;
+      if (!weights[idx]) continue;
+      ++pos;
+      const float* s = scores + b * V;
+      double mx = (double)s[0];
+      for (int64_t w = 1; w < V; ++w) mx = (mx < (double)s[w]) ? (double)s[w] : mx;
+      double z = 0.0;
+      for (int64_t w = 0; w < V; ++w) z += exp((double)s[w] - mx);
+      const double lse = mx + log(z);
+      const uint32_t y = targets[idx];
+      L += loss_scale * (lse - (double)s[y]);
+      if (compute_grads) {
+        float* d = dsc + idx * V;
+        for (int64_t w = 0; w < V; ++w)
+          d[w] = (float)(loss_scale * exp((double)s[w] - lse));
+        d[y] -= (float)loss_scale;
+      }
+    }
+  }
+  *loss = L;
+  *positions = pos;
+  if (compute_grads) {
+    /* backward (backprop.hpp:193-220) */
+    float* dh = (float*)calloc((size_t)BH, sizeof(float));
+    float* dpre = (float*)malloc(sizeof(float) * BH);
+    double* acc = (double*)malloc(sizeof(double) * (V > H ? V : H));
+    int32_t* slot_of = (int32_t*)malloc(sizeof(int32_t) * V);
+    for (int64_t w = 0; w < V; ++w) slot_of[w] = -1;
+    int64_t nrows = 0;
+    memset(g_rec, 0, sizeof(float) * H * H);
+    memset(g_out, 0, sizeof(float) * V * H);
+    for (int64_t t = T - 1; t >= 0; --t) {
+      const float* dst = dsc + t * B * V;
+      const float* ht1 = h + (t + 1) * BH;
+      /* softmax_backward (rnn.hpp:253-258) */
+      matmul_tn_add(dst, ht1, g_out, B, V, H);
+      matmul_nn(dst, w_out, dh, B, H, V, 1, acc);
+      for (int64_t i = 0; i < BH; ++i) dpre[i] = dh[i] * act_deriv_f(act, ht1[i]);
+      matmul_tn_add(dpre, h + t * BH, g_rec, B, H, H);
+      /* input_backward -> SparseRowGrads::axpy_row (rnn.hpp:106-110, 218-222) */
+      for (int64_t b = 0; b < B; ++b) {
+        const uint32_t w = inputs[t * B + b];
+        if (slot_of[w] < 0) {
+          slot_of[w] = (int32_t)nrows;
+          g_in_words[nrows] = w;
+          memset(g_in_data + nrows * H, 0, sizeof(float) * H);
+          ++nrows;
+        }
+        float* r = g_in_data + (int64_t)slot_of[w] * H;
+        for (int64_t i = 0; i < H; ++i) r[i] += 1.0f * dpre[b * H + i];
+      }
+      if (t > 0) matmul_nn(dpre, w_rec, dh, B, H, H, 0, acc);
+    }
+    *g_in_rows = nrows;
+    /* StandardGrads::clip (rnn.hpp:155-162) */
+    for (int64_t i = 0; i < nrows * H; ++i) g_in_data[i] = clip1(g_in_data[i], clip);
+    for (int64_t i = 0; i < H * H; ++i) g_rec[i] = clip1(g_rec[i], clip);
+    for (int64_t i = 0; i < V * H; ++i) g_out[i] = clip1(g_out[i], clip);
+    free(dh);
+    free(dpre);
+    free(acc);
+    free(slot_of);
+  }
+  free(h);
+  free(pre);
+  free(scores);
+  free(dsc);
+  return 0;
+}
+
+/* -------------------------------------------------------------- rmsprop */
+static double mean_sq(const float* x, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += (double)x[i] * (double)x[i];
+  return s / (double)n;
+}
+
+static int all_finite(const float* x, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!isfinite((double)x[i])) return 0;
+  return 1;
+}
+
+/* rmsprop.hpp:77-92 */
+static void update_rows_sparse(float* w, int64_t H, int64_t nrows,
+                               const uint32_t* words, const float* data,
+                               float* m, int64_t V, double rho, double eps,
+                               double eta) {
+  for (int64_t i = 0; i < V; ++i) m[i] = (float)(rho * m[i]);
+  for (int64_t s = 0; s < nrows; ++s) {
+    const uint32_t word = words[s];
+    const float* row = data + s * H;
+    m[word] += (float)((1.0 - rho) * mean_sq(row, H));
+    const double denom = sqrt((double)m[word] + eps);
+    float* wr = w + (int64_t)word * H;
+    for (int64_t i = 0; i < H; ++i) wr[i] -= (float)(eta * (double)row[i] / denom);
+  }
+}
+
+/* rmsprop.hpp:94-107 */
+static void update_rows_dense(float* w, int64_t V, int64_t H, const float* g,
+                              float* m, double rho, double eps, double eta) {
+  for (int64_t word = 0; word < V; ++word) {
+    const float* row = g + word * H;
+    m[word] = (float)(rho * (double)m[word] + (1.0 - rho) * mean_sq(row, H));
+    const double denom = sqrt((double)m[word] + eps);
+    float* wr = w + word * H;
+    for (int64_t i = 0; i < H; ++i) wr[i] -= (float)(eta * (double)row[i] / denom);
+  }
+}
+
+/* rmsprop.hpp:113-133.  out_dense selects the dense W_out gradient (softmax
+ * mode) or sparse rows (NCE mode). */
+int orc_rmsprop(int64_t V, int64_t H, float* w_in, float* w_rec, float* w_out,
+                float* m_rec, float* m_in, float* m_out, double rho, double eps,
+                double eta, int64_t n_in_rows, const uint32_t* in_words,
+                const float* in_data, const float* g_rec, int out_dense,
+                int64_t n_out_rows, const uint32_t* out_words,
+                const float* out_data, int* applied) {
+  const int fin = all_finite(in_data, n_in_rows * H) && all_finite(g_rec, H * H) &&
+                  (out_dense ? all_finite(out_data, V * H)
+                             : all_finite(out_data, n_out_rows * H));
+  if (!fin) {
+    *applied = 0;
+    return 0;
+  }
+  for (int64_t i = 0; i < H * H; ++i) {
+    const double gi = (double)g_rec[i];
+    m_rec[i] = (float)(rho * (double)m_rec[i] + (1.0 - rho) * gi * gi);
+    w_rec[i] -= (float)(eta * gi / sqrt((double)m_rec[i] + eps));
+  }
+  update_rows_sparse(w_in, H, n_in_rows, in_words, in_data, m_in, V, rho, eps, eta);
+  if (out_dense)
+    update_rows_dense(w_out, V, H, out_data, m_out, rho, eps, eta);
+  else
+    update_rows_sparse(w_out, H, n_out_rows, out_words, out_data, m_out, V, rho,
+                       eps, eta);
+  *applied = 1;
+  return 0;
+}
+
+/* --------------------------------------------------------------- scoring */
+/* eval.hpp:48-57 over a contiguous score vector. */
+static double lse_vec(const float* s, int64_t n) {
+  double mx = -INFINITY;
+  for (int64_t w = 0; w < n; ++w) mx = (mx < (double)s[w]) ? (double)s[w] : mx;
+  double z = 0.0;
+  for (int64_t w = 0; w < n; ++w) z += exp((double)s[w] - mx);
+  return mx + log(z);
+}
+
+/* Per-token log-probs of the sharded walk (eval.hpp:151-222).  out[j*S+s]
+ * is ln p or NaN for skipped targets; totals mirror PerplexityResult. */
+int orc_sharded_logprobs(int64_t V, int64_t H, int act, const float* w_in,
+                         const float* w_rec, const float* w_out,
+                         const uint32_t* ids, int64_t n, int shards,
+                         uint32_t bos, double* out, int64_t cap, int64_t* S_out,
+                         int64_t* steps_out, double* total_logprob,
+                         uint64_t* predicted) {
+  if (n < 2 || shards < 1) return 1;
+  const int64_t S = shards < n / 2 ? shards : n / 2;
+  int64_t* begin = (int64_t*)malloc(sizeof(int64_t) * (S + 1));
+  for (int64_t s = 0; s <= S; ++s) begin[s] = s * n / S;
+  int64_t max_len = 0;
+  for (int64_t s = 0; s < S; ++s)
+    if (begin[s + 1] - begin[s] > max_len) max_len = begin[s + 1] - begin[s];
+  *S_out = S;
+  *steps_out = max_len - 1;
+  if (out && (max_len - 1) * S > cap) {
+    free(begin);
+    return 1;
+  }
+  const float a0 = act_f(act, 0.0f);
+  float* h = (float*)malloc(sizeof(float) * S * H);
+  float* pre = (float*)malloc(sizeof(float) * S * H);
+  float* sc = (float*)malloc(sizeof(float) * V);
+  uint32_t* in = (uint32_t*)malloc(sizeof(uint32_t) * S);
+  int64_t* tgt = (int64_t*)malloc(sizeof(int64_t) * S);
+  for (int64_t i = 0; i < S * H; ++i) h[i] = a0;
+  double total = 0.0;
+  uint64_t pred = 0;
+  int rc = 0;
+  for (int64_t j = 0; j + 1 < max_len; ++j) {
+    int any = 0;
+    for (int64_t s = 0; s < S; ++s) {
+      const int64_t len = begin[s + 1] - begin[s];
+      if (j + 1 < len) {
+        const uint32_t x = ids[begin[s] + j], y = ids[begin[s] + j + 1];
+        if (x >= (uint64_t)V || y >= (uint64_t)V) {
+          rc = 2;
+          goto done;
+        }
+        in[s] = x;
+        tgt[s] = (y == bos) ? -1 : (int64_t)y;
+      } else {
+        in[s] = 0;
+        tgt[s] = -1;
+      }
+      any = any || tgt[s] >= 0;
+    }
+    matmul_nt(h, w_rec, pre, S, H, H);
+    for (int64_t s = 0; s < S; ++s)
+      for (int64_t i = 0; i < H; ++i) {
+        const float p = pre[s * H + i] + w_in[(int64_t)in[s] * H + i];
+        h[s * H + i] = act_f(act, p);
+      }
+    for (int64_t s = 0; s < S; ++s) {
+      double v = NAN;
+      if (any && tgt[s] >= 0) {
+        /* scores_t column s: W_out . h_s (eval.hpp:207, rnn.hpp:248-251) */
+        for (int64_t w = 0; w < V; ++w) sc[w] = (float)dot_acc(w_out + w * H, h + s * H, H);
+        v = (double)sc[tgt[s]] - lse_vec(sc, V);
+        total += v;
+        ++pred;
+      }
+      if (out) out[j * S + s] = v;
+    }
+  }
+  *total_logprob = total;
+  *predicted = pred;
+  if (pred == 0) rc = 1;
+done:
+  free(begin);
+  free(h);
+  free(pre);
+  free(sc);
+  free(in);
+  free(tgt);
+  return rc;
+}
+
+int orc_sharded_ppl(int64_t V, int64_t H, int act, const float* w_in,
+                    const float* w_rec, const float* w_out, const uint32_t* ids,
+                    int64_t n, int shards, uint32_t bos, int threads,
+                    double* total_logprob, uint64_t* predicted, double* ppl) {
+  (void)threads;
+  int64_t S, steps;
+  const int rc = orc_sharded_logprobs(V, H, act, w_in, w_rec, w_out, ids, n,
+                                      shards, bos, NULL, 0, &S, &steps,
+                                      total_logprob, predicted);
+  if (rc) return rc;
+  *ppl = exp(-*total_logprob / (double)*predicted);
+  return 0;
+}
+
+/* eval.hpp:84-145: single stream, state never reset after the start; every
+ * non-bos target scored (banking does not change the numbers). */
+int orc_rnn_ppl(int64_t V, int64_t H, int act, const float* w_in,
+                const float* w_rec, const float* w_out, const uint32_t* ids,
+                int64_t n, uint32_t bos, int threads, double* total_logprob,
+                uint64_t* predicted, double* ppl) {
+  (void)threads;
+  if (n < 2) return 1;
+  float* h = (float*)malloc(sizeof(float) * H);
+  float* pre = (float*)malloc(sizeof(float) * H);
+  float* sc = (float*)malloc(sizeof(float) * V);
+  const float a0 = act_f(act, 0.0f);
+  for (int64_t i = 0; i < H; ++i) h[i] = a0;
+  double total = 0.0;
+  uint64_t pred = 0;
+  int rc = 0;
+  for (int64_t i = 0; i + 1 < n; ++i) {
+    if (ids[i] >= (uint64_t)V || ids[i + 1] >= (uint64_t)V) {
+      rc = 2;
+      break;
+    }
+    matmul_nt(h, w_rec, pre, 1, H, H);
+    for (int64_t j = 0; j < H; ++j) h[j] = act_f(act, pre[j] + w_in[(int64_t)ids[i] * H + j]);
+    const uint32_t y = ids[i + 1];
+    if (y == bos) continue;
+    for (int64_t w = 0; w < V; ++w) sc[w] = (float)dot_acc(w_out + w * H, h, H);
+    total += (double)sc[y] - lse_vec(sc, V);
+    ++pred;
+  }
+  free(h);
+  free(pre);
+  free(sc);
+  if (rc) return rc;
+  if (pred == 0) return 1;
+  *total_logprob = total;
+  *predicted = pred;
+  *ppl = exp(-total / (double)pred);
+  return 0;
+}
+
+/* -------------------------------------------------------------- trainer */
+/* Window construction for streams s0..s0+B-1 (trainer.hpp:376-387). */
+void orc_window_build(const uint32_t* ids, int64_t L, const int64_t* cursors,
+                      int64_t s0, int64_t B, int64_t T, uint32_t bos,
+                      uint32_t* inputs, uint32_t* targets, uint8_t* weights) {
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t pos = cursors[s0 + b] + t;
+      const uint32_t x = ids[pos % L];
+      const uint32_t y = ids[(pos + 1) % L];
+      inputs[t * B + b] = x;
+      targets[t * B + b] = y;
+      weights[t * B + b] = (y == bos) ? 0 : 1;
+    }
+}
+
+/* Mirrors the ref_train_config layout in oracle/ref_shim.cpp. */
+typedef struct {
+  int64_t nstate, nproj;
+  int32_t noffset, minibatch, unroll, mode;
+  double eta, rho, eps, clip;
+  int32_t nce_k, max_epochs;
+  double noise_floor;
+  uint64_t seed;
+  int32_t act, valid_shards;
+  double divergence_factor;
+  int64_t valid_limit;
+  double init_range;
+  int32_t threads, pad_;
+} orc_train_config;
+
+/* Trainer<StandardTraits> in softmax mode: constructor (trainer.hpp:178-212),
+ * train() (:233-270), run_epoch() (:350-410), validate() (:223-228).
+ * Params (inout), opt state (out), cursors (out, N), hidden (out, N*H),
+ * logs (7 doubles/epoch).  Returns 2 on divergence (DataError). */
+int orc_train(const orc_train_config* c, int64_t V, float* w_in, float* w_rec,
+              float* w_out, const uint32_t* ids, int64_t L,
+              const uint32_t* valid, int64_t n_valid, int run_epochs,
+              float* m_rec, float* m_in, float* m_out, int64_t* cursors,
+              float* hidden, double* logs, int* n_logs, double* initial_ppl,
+              double* eta_out, double* best_out, int* bad_out, int* epoch_out) {
+  const int64_t H = c->nstate, B = c->minibatch, T = c->unroll;
+  const int64_t N = (int64_t)c->noffset * B;
+  if (c->mode != 1) return 1; /* NCE is out of scope for this oracle */
+  if (L < N) return 1;
+  for (int64_t i = 0; i < N; ++i) cursors[i] = i * L / N;
+  const float a0 = act_f(c->act, 0.0f);
+  for (int64_t i = 0; i < N * H; ++i) hidden[i] = a0;
+  const int64_t nv = (c->valid_limit > 0 && n_valid > c->valid_limit) ? c->valid_limit : n_valid;
+  if (nv < 2) return 1;
+  memset(m_rec, 0, sizeof(float) * H * H);
+  memset(m_in, 0, sizeof(float) * V);
+  memset(m_out, 0, sizeof(float) * V);
+  double eta = c->eta, best = 0.0, initial = 0.0;
+  int bad = 0, epoch = 0;
+  *n_logs = 0;
+  int rc = 0;
+  uint32_t* xin = (uint32_t*)malloc(sizeof(uint32_t) * T * B);
+  uint32_t* yt = (uint32_t*)malloc(sizeof(uint32_t) * T * B);
+  uint8_t* wt = (uint8_t*)malloc(T * B);
+  float* h0 = (float*)malloc(sizeof(float) * B * H);
+  float* hf = (float*)malloc(sizeof(float) * B * H);
+  uint32_t* gw = (uint32_t*)malloc(sizeof(uint32_t) * T * B);
+  float* gd = (float*)malloc(sizeof(float) * T * B * H);
+  float* grec = (float*)malloc(sizeof(float) * H * H);
+  float* gout = (float*)malloc(sizeof(float) * V * H);
+  if (run_epochs) {
+    double tl;
+    uint64_t pr;
+    double ppl;
+    if (orc_sharded_ppl(V, H, c->act, w_in, w_rec, w_out, valid, nv, c->valid_shards, 1, 1, &tl, &pr, &ppl)) {
+      rc = 1;
+      goto done;
+    }
+    initial = best = ppl;
+    while (epoch < c->max_epochs && bad < 2) {
+      const int64_t rounds = (L + N * T - 1) / (N * T);
+      double loss_sum = 0.0;
+      int64_t windows = 0, skipped = 0;
+      for (int64_t r = 0; r < rounds; ++r)
+        for (int64_t g = 0; g < c->noffset; ++g) {
+          const int64_t s0 = g * B;
+          orc_window_build(ids, L, cursors, s0, B, T, 1, xin, yt, wt);
+          memcpy(h0, hidden + s0 * H, sizeof(float) * B * H);
+          double loss;
+          uint64_t pos;
+          int64_t nrows;
+          orc_bptt(V, H, c->act, w_in, w_rec, w_out, T, B, xin, yt, wt, h0,
+                   1.0 / (double)(B * T), (float)c->clip, 1, 1, hf, &nrows, gw,
+                   gd, grec, gout, &loss, &pos);
+          loss_sum += loss;
+          ++windows;
+          int applied;
+          orc_rmsprop(V, H, w_in, w_rec, w_out, m_rec, m_in, m_out, c->rho,
+                      c->eps, eta, nrows, gw, gd, grec, 1, 0, NULL, gout, &applied);
+          if (!applied) ++skipped;
+          for (int64_t b = 0; b < B; ++b) {
+            memcpy(hidden + (s0 + b) * H, hf + b * H, sizeof(float) * H);
+            cursors[s0 + b] += T;
+            if (cursors[s0 + b] >= L) {
+              cursors[s0 + b] -= L;
+              for (int64_t i = 0; i < H; ++i) hidden[(s0 + b) * H + i] = a0;
+            }
+          }
+        }
+      if (orc_sharded_ppl(V, H, c->act, w_in, w_rec, w_out, valid, nv, c->valid_shards, 1, 1, &tl, &pr, &ppl)) {
+        rc = 1;
+        goto done;
+      }
+      double* lg = logs + 7 * (*n_logs);
+      lg[0] = ++epoch;
+      lg[1] = windows > 0 ? loss_sum / (double)windows : 0.0;
+      lg[2] = ppl;
+      lg[3] = eta;
+      lg[4] = 0.0;
+      lg[5] = 0.0;
+      lg[6] = (double)skipped;
+      ++*n_logs;
+      if (ppl > c->divergence_factor * initial) {
+        rc = 2;
+        goto done;
+      }
+      if (ppl < best) {
+        best = ppl;
+        bad = 0;
+      } else {
+        ++bad;
+        eta *= 0.5;
+      }
+    }
+  }
+done:
+  *initial_ppl = initial;
+  *eta_out = eta;
+  *best_out = best;
+  *bad_out = bad;
+  *epoch_out = epoch;
+  free(xin);
+  free(yt);
+  free(wt);
+  free(h0);
+  free(hf);
+  free(gw);
+  free(gd);
+  free(grec);
+  free(gout);
+  return rc;
+}

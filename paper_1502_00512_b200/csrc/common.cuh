@@ -1,0 +1,93 @@
+// Shared internals of libdesklm_cuda.so (sm_100a only).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace dl {
+
+using bf16 = __nv_bfloat16;
+
+// Status-carrying exception used inside the runtime; mapped to DL_E* codes
+// at the C-ABI boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define DL_CUDA(x)                                                        \
+  do {                                                                    \
+    cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess)                                                \
+      throw ::dl::Error(3, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                               " at " __FILE__ ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define DL_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) throw ::dl::Error((code), (msg)); \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+// Operand storage order for the generic GEMMs.  A is M x K, B is N x K
+// logically; K_MAJOR means K is the contiguous index (row-major [M][K]),
+// MN_MAJOR means M (or N) is contiguous (row-major [K][M]).
+enum Major : int { K_MAJOR = 0, MN_MAJOR = 1 };
+
+__device__ __forceinline__ float act_f(int act, float x) {
+  // rnn.hpp:37-42 (float): 1/(1+exp(-x)) or tanh
+  return act == 0 ? 1.0f / (1.0f + expf(-x)) : tanhf(x);
+}
+__device__ __forceinline__ float act_deriv_f(int act, float y) {
+  // rnn.hpp:45-49, expressed through the output y
+  return act == 0 ? y * (1.0f - y) : 1.0f - y * y;
+}
+// std::min(c, std::max(-c, x)): NaN maps to -c exactly like the reference
+// (rnn.hpp:131-134 with std::max/min's comparison order).
+__device__ __forceinline__ float clip1(float x, float c) {
+  const float t = (-c < x) ? x : -c;
+  return (t < c) ? t : c;
+}
+
+// ---------------------------------------------------------------- launches
+// GEMM problem description shared by the SIMT (fp32) and tcgen05 (bf16)
+// kernels.  C (+ split * split_stride) receives fp32 results; for k_splits>1
+// the caller reduces the slices.
+struct GemmDesc {
+  int M, N, K;
+  int a_major, b_major;
+  const void* A;  // float* (fp32 path) or bf16* (tc path)
+  const void* B;
+  int64_t lda, ldb;  // elements between consecutive rows of the stored matrix
+  float* C;
+  int64_t ldc;
+  int64_t split_stride;
+  int k_splits;
+  // optional fused clip (only valid with k_splits == 1)
+  float clip;
+  int do_clip;
+  int* nonfinite;  // set to 1 if any clipped value is non-finite
+  // logits epilogue (tc path): per-row online (max, sum-exp) partials per
+  // N tile, the target logit and an optional bf16 copy of the logits.
+  int logits;
+  bf16* S;
+  int64_t lds;
+  float2* part;          // [n_tiles][M]
+  const uint32_t* tgt;   // [M] target column per row
+  float* tgt_logit;      // [M]
+  int raster;            // 0: M-tiles fastest, 1: N-tiles fastest
+};
+
+// gemm_simt.cu
+void gemm_f32(const GemmDesc& g, cudaStream_t st);
+// gemm_tc.cu  (returns the number of N-tiles used for logits partials)
+int gemm_tc(const GemmDesc& g, cudaStream_t st);
+int tc_n_tiles(int N);
+int tc_splits(int K, int desired);
+
+}  // namespace dl

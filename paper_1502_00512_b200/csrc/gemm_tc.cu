@@ -1,0 +1,442 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a (bf16 operands, fp32 accumulate).
+//
+// One persistent, warp-specialised kernel serves every dense contraction of
+// the RNNLM window, replacing mat.hpp:116-184:
+//   logits      S  = Hs . W_out^T    (A K-major, B K-major)  + online-LSE epilogue
+//   dh_out      dH = dS . W_out      (A K-major, B MN-major)
+//   dW_out      dW = dS^T . Hs       (A MN-major, B MN-major) + clip epilogue
+//   recurrence  h  . W_rec^T / dpre . W_rec                     (split-K slices)
+//   dW_rec      dW = dpre^T . Hprev  (A MN-major, B MN-major)   (split-K slices)
+//
+// Roles (192 threads): warp 0 = TMA producer (one elected lane), warp 1 =
+// MMA issuer (one lane issues tcgen05.mma for the whole CTA), warps 2-5 =
+// epilogue (tcgen05.ld TMEM -> registers; warp w owns TMEM lanes
+// 32*(w%4)..+31, i.e. one accumulator row per thread).  Tiles are 128 x BN
+// with BK = 64 (one 128-byte swizzle row of bf16); the accumulator is double
+// buffered in TMEM (2 x BN fp32 columns) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Operands arrive by TMA with SWIZZLE_128B into the
+// canonical UMMA layouts:
+//   K-major  tile: rows of 128 B, 8-row groups 1024 B apart (SBO = 1024)
+//   MN-major tile: 64-element (128 B) MN chunks 8 KB apart (LBO = 8192),
+//                  each chunk 64 K-rows of 128 B, 8-row groups (SBO = 1024)
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace dl {
+namespace tc {
+
+constexpr int BM = 128, BK = 64, UMMA_K = 16;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100)
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Sched {
+  int m_tiles, n_tiles, k_splits, kb_total, kbps, raster;
+  __device__ void decode(int u, int& mt, int& nt, int& kb0, int& kb1) const {
+    const int s = u % k_splits;
+    const int t = u / k_splits;
+    if (raster == 0) { mt = t % m_tiles; nt = t / m_tiles; }
+    else { nt = t % n_tiles; mt = t / n_tiles; }
+    kb0 = s * kbps;
+    kb1 = min(kb_total, kb0 + kbps);
+  }
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               GemmDesc g, Sched sc) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then tmem slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
+  auto tfull = [&](int a) { return smem_u32(&bars[2 * C::STAGES + a]); };
+  auto tempty = [&](int a) { return smem_u32(&bars[2 * C::STAGES + 2 + a]); };
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1);
+          const uint32_t a_s = sbase + stage * C::STAGE;
+          const uint32_t b_s = a_s + C::A_BYTES;
+          mbar_expect_tx(full(stage), C::STAGE);
+          if (!A_MN) {
+            tma_load_2d(a_s, &tmA, full(stage), kb * BK, mt * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(a_s + j * 8192, &tmA, full(stage), mt * BM + 64 * j, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_s, &tmB, full(stage), kb * BK, nt * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(b_s + j * 8192, &tmB, full(stage), nt * BN + 64 * j, kb * BK);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                 (static_cast<uint32_t>(A_MN) << 15) |
+                                 (static_cast<uint32_t>(B_MN) << 16) |
+                                 (static_cast<uint32_t>(BN >> 3) << 17) |
+                                 (static_cast<uint32_t>(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        mbar_wait(tempty(acc), acc_phase ^ 1);
+        fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(full(stage), phase);
+          fence_after();
+          const uint32_t a_s = sbase + stage * C::STAGE;
+          const uint32_t b_s = a_s + C::A_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            const uint64_t ad = A_MN ? make_desc(a_s + ks * 2048, 8192, 1024)
+                                     : make_desc(a_s + ks * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(b_s + ks * 2048, 8192, 1024)
+                                     : make_desc(b_s + ks * 32, 16, 1024);
+            mma_bf16(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+          }
+          mma_commit(empty(stage));
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5)
+    const int quarter = warp % 4;
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    bool bad = false;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      int mt, nt, kb0, kb1;
+      sc.decode(u, mt, nt, kb0, kb1);
+      const int split = u % sc.k_splits;
+      mbar_wait(tfull(acc), acc_phase);
+      fence_after();
+      const int m = mt * BM + row;
+      const bool mvalid = m < g.M;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if (!g.logits) {
+        float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const int n0 = nt * BN + c * 32;
+          if (g.do_clip) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] = clip1(v[j], g.clip);
+              bad |= mvalid && (n0 + j < g.N) && !isfinite(v[j]);
+            }
+          }
+          if (!mvalid) continue;
+          if (n0 + 32 <= g.N && (g.ldc % 4) == 0) {
+            float4* dst = reinterpret_cast<float4*>(Crow + n0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < g.N) Crow[n0 + j] = v[j];
+          }
+        }
+      } else {
+        const float kLog2e = 1.4426950408889634f;
+        float mrun = -INFINITY, srun = 0.f, tval = 0.f;
+        bool thit = false;
+        const int tg = mvalid ? static_cast<int>(g.tgt[m]) : -1;
+        bf16* Srow = g.S ? g.S + static_cast<int64_t>(m) * g.lds : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const int n0 = nt * BN + c * 32;
+          float cmax = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const bool ok = n0 + j < g.N;
+            if (ok) cmax = fmaxf(cmax, v[j]);
+            if (n0 + j == tg) { tval = v[j]; thit = true; }
+          }
+          if (cmax > mrun) {
+            srun *= exp2f((mrun - cmax) * kLog2e);
+            mrun = cmax;
+          }
+          const float mb = mrun * kLog2e;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (n0 + j < g.N) srun += exp2f(fmaf(v[j], kLog2e, -mb));
+          if (Srow && mvalid) {
+            if (n0 + 32 <= g.N && (g.lds % 8) == 0) {
+              uint4* dst = reinterpret_cast<uint4*>(Srow + n0);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 q;
+                __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * j + 0], v[8 * j + 1]);
+                __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+                __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+                __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+                q.x = *reinterpret_cast<uint32_t*>(&p0);
+                q.y = *reinterpret_cast<uint32_t*>(&p1);
+                q.z = *reinterpret_cast<uint32_t*>(&p2);
+                q.w = *reinterpret_cast<uint32_t*>(&p3);
+                dst[j] = q;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < g.N) Srow[n0 + j] = __float2bfloat16_rn(v[j]);
+            }
+          }
+        }
+        if (mvalid) {
+          g.part[static_cast<int64_t>(nt) * g.M + m] = make_float2(mrun, srun);
+          if (thit) g.tgt_logit[m] = tval;
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    DL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    DL_REQUIRE(p && q == cudaDriverEntryPointSuccess, 3, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows x cols] matrix with leading
+// dimension ld (elements), box {64 cols, box_rows}, 128-byte swizzle.
+CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  DL_REQUIRE((reinterpret_cast<uintptr_t>(base) % 16) == 0, 1, "tma: base not 16B aligned");
+  DL_REQUIRE((ld * 2) % 16 == 0, 1, "tma: leading dimension must be a multiple of 8 elements");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DL_REQUIRE(r == CUDA_SUCCESS, 3, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+void launch(const GemmDesc& g, cudaStream_t st) {
+  using C = Cfg<BN>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  });
+  const CUtensorMap ta = A_MN ? make_map(g.A, g.K, g.M, g.lda, 64) : make_map(g.A, g.M, g.K, g.lda, BM);
+  const CUtensorMap tb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64) : make_map(g.B, g.N, g.K, g.ldb, BN);
+  Sched sc;
+  sc.m_tiles = (g.M + BM - 1) / BM;
+  sc.n_tiles = (g.N + BN - 1) / BN;
+  sc.kb_total = (g.K + BK - 1) / BK;
+  sc.k_splits = tc_splits(g.K, g.k_splits);
+  sc.kbps = (sc.kb_total + sc.k_splits - 1) / sc.k_splits;
+  DL_REQUIRE(sc.k_splits == std::max(1, g.k_splits), 1,
+             "tc gemm: k_splits not normalised with tc_splits()");
+  sc.raster = g.raster;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+  const int grid = std::min(total, kNumSMs);
+  kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, g, sc);
+  DL_CUDA(cudaGetLastError());
+}
+
+}  // namespace tc
+
+// Number of K slices actually produced for a requested split count: every
+// slice gets ceil(kb_total / splits) k-blocks and none is empty.
+int tc_splits(int K, int desired) {
+  const int kb_total = (K + tc::BK - 1) / tc::BK;
+  const int s = std::max(1, std::min(desired, kb_total));
+  const int kbps = (kb_total + s - 1) / s;
+  return (kb_total + kbps - 1) / kbps;
+}
+
+int tc_n_tiles(int N) {
+  const int bn = N >= 256 ? 256 : (N >= 128 ? 128 : 64);
+  return (N + bn - 1) / bn;
+}
+
+int gemm_tc(const GemmDesc& g, cudaStream_t st) {
+  const int bn = g.N >= 256 ? 256 : (g.N >= 128 ? 128 : 64);
+  const bool am = g.a_major == MN_MAJOR, bm = g.b_major == MN_MAJOR;
+#define DL_TC_CASE(BN_)                                            \
+  if (bn == BN_) {                                                 \
+    if (!am && !bm) tc::launch<BN_, false, false>(g, st);          \
+    else if (!am && bm) tc::launch<BN_, false, true>(g, st);       \
+    else if (am && !bm) tc::launch<BN_, true, false>(g, st);       \
+    else tc::launch<BN_, true, true>(g, st);                       \
+    return (g.N + BN_ - 1) / BN_;                                  \
+  }
+  DL_TC_CASE(256)
+  DL_TC_CASE(128)
+  DL_TC_CASE(64)
+#undef DL_TC_CASE
+  return 0;
+}
+
+}  // namespace dl

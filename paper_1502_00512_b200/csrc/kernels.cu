@@ -1,0 +1,613 @@
+// Bandwidth-bound kernels of the RNNLM window: recurrence epilogues (split-K
+// reduction + embedding gather + activation), softmax/LSE rows, the sparse
+// embedding gradient, clip/finite, rmsprop and the device-side offset-stream
+// schedule.  Each kernel cites the reference code it replaces (paths
+// relative to /root/reference/proj/include/desklm).
+#include "kernels.cuh"
+
+namespace dl {
+namespace {
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide deterministic reductions (fixed tree for a fixed block size).
+template <int NT>
+__device__ double block_sum_d(double v, double* red) {
+  v = warp_sum_d(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < NT / 32 ? red[l] : 0.0;
+    v = warp_sum_d(v);
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+template <int NT>
+__device__ double block_max_d(double v, double* red) {
+  v = warp_max_d(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < NT / 32 ? red[l] : -INFINITY;
+    v = warp_max_d(v);
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// ---------------------------------------------------------------- casts
+__global__ void k_f32_to_bf16(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+__global__ void k_fill_f32(float* __restrict__ x, float v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+// ------------------------------------------------------- recurrence steps
+// Forward step epilogue (backprop.hpp:102-112, rnn.hpp:209-216):
+//   pre = sum_s partial[s] (fixed order), rounded to float;
+//   pre += W_in[x_b] (float);  h = act(pre)
+__global__ void k_rec_fwd(const float* __restrict__ part, int splits, int64_t split_stride,
+                          int64_t Bn, int64_t H, const float* __restrict__ w_in,
+                          const uint32_t* __restrict__ x, int act, float* __restrict__ h,
+                          bf16* __restrict__ hb) {
+  const int64_t n = Bn * H;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / H, j = i % H;
+    float pre = part[i];
+    for (int s = 1; s < splits; ++s) pre += part[s * split_stride + i];
+    pre += w_in[(int64_t)x[b] * H + j];
+    const float y = act_f(act, pre);
+    h[i] = y;
+    if (hb) hb[i] = __float2bfloat16_rn(y);
+  }
+}
+
+// Backward step epilogue (backprop.hpp:207-218):
+//   dh = dh_out_t (+ sum_s partial[s] = dpre_{t+1} . W_rec when chained)
+//   dpre = dh * act'(h_{t+1})
+__global__ void k_rec_bwd(const float* __restrict__ part, int splits, int64_t split_stride,
+                          int64_t n, const float* __restrict__ dh_out,
+                          const float* __restrict__ hnext, int act, float* __restrict__ dpre,
+                          bf16* __restrict__ dpreb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float dh = 0.f;
+    if (splits > 0) {
+      dh = part[i];
+      for (int s = 1; s < splits; ++s) dh += part[s * split_stride + i];
+    }
+    dh += dh_out[i];
+    const float d = dh * act_deriv_f(act, hnext[i]);
+    dpre[i] = d;
+    if (dpreb) dpreb[i] = __float2bfloat16_rn(d);
+  }
+}
+
+// Split-K reduction with optional clip and finite flag (dW_rec, dh_out).
+__global__ void k_reduce(const float* __restrict__ part, int splits, int64_t split_stride,
+                         int64_t n, float* __restrict__ out, float clip, int do_clip,
+                         int* nonfinite) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = part[i];
+    for (int s = 1; s < splits; ++s) v += part[s * split_stride + i];
+    if (do_clip) {
+      v = clip1(v, clip);
+      bad |= !isfinite(v);
+    }
+    out[i] = v;
+  }
+  if (do_clip && nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+}
+
+// ---------------------------------------------------------- softmax rows
+// fp32 path: S holds fp32 logits [M x V].  Per row (backprop.hpp:162-186):
+//   mx = max_w s (double), z = sum exp(s - mx) (double), lse = mx + log z
+//   loss_row = w ? scale*(lse - s_y) : 0 ;  logp_row = s_y - lse
+//   grads: dS = w ? float(scale*exp(s - lse)) - [w==y] float(scale) : 0
+constexpr int kRowThreads = 512;
+
+__global__ void __launch_bounds__(kRowThreads)
+k_softmax_rows_f32(float* __restrict__ S, int64_t V, const uint32_t* __restrict__ tgt,
+                   const uint8_t* __restrict__ wts, double scale, int grads,
+                   double* __restrict__ loss_row, double* __restrict__ logp_row) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  float* s = S + r * V;
+  const bool active = wts == nullptr || wts[r] != 0;
+  if (!active) {
+    if (loss_row) loss_row[r] = 0.0;
+    if (logp_row) logp_row[r] = NAN;
+    if (grads)
+      for (int64_t w = threadIdx.x; w < V; w += blockDim.x) s[w] = 0.f;
+    return;
+  }
+  double mx = -INFINITY;
+  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) mx = fmax(mx, (double)s[w]);
+  mx = block_max_d<kRowThreads>(mx, red);
+  double z = 0.0;
+  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) z += exp((double)s[w] - mx);
+  z = block_sum_d<kRowThreads>(z, red);
+  const double lse = mx + log(z);
+  const uint32_t y = tgt[r];
+  const double sy = (double)s[y];
+  if (threadIdx.x == 0) {
+    if (loss_row) loss_row[r] = scale * (lse - sy);
+    if (logp_row) logp_row[r] = sy - lse;
+  }
+  if (grads) {
+    __syncthreads();  // everyone has read s[y]
+    for (int64_t w = threadIdx.x; w < V; w += blockDim.x) {
+      float d = (float)(scale * exp((double)s[w] - lse));
+      if (w == y) d -= (float)scale;
+      s[w] = d;
+    }
+  }
+}
+
+// bf16 path: the tcgen05 logits epilogue left per-(N tile, row) partials
+// (max, sum-exp) and the fp32 target logit; combine them into lse, then
+// overwrite the bf16 logits with bf16 dS in place.
+__global__ void __launch_bounds__(kRowThreads)
+k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __restrict__ part,
+                    int n_tiles, const float* __restrict__ tgt_logit,
+                    const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ wts,
+                    double scale, int grads, double* __restrict__ loss_row,
+                    double* __restrict__ logp_row) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  bf16* s = S ? S + r * V : nullptr;
+  const bool active = wts == nullptr || wts[r] != 0;
+  if (!active) {
+    if (threadIdx.x == 0) {
+      if (loss_row) loss_row[r] = 0.0;
+      if (logp_row) logp_row[r] = NAN;
+    }
+    if (grads) {
+      const bf16 z = __float2bfloat16_rn(0.f);
+      for (int64_t w = threadIdx.x; w < V; w += blockDim.x) s[w] = z;
+    }
+    return;
+  }
+  double mx = -INFINITY;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+  mx = block_max_d<kRowThreads>(mx, red);
+  double z = 0.0;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const float2 p = part[(int64_t)t * M + r];
+    if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
+  }
+  z = block_sum_d<kRowThreads>(z, red);
+  const double lse = mx + log(z);
+  const double sy = (double)tgt_logit[r];
+  if (threadIdx.x == 0) {
+    if (loss_row) loss_row[r] = scale * (lse - sy);
+    if (logp_row) logp_row[r] = sy - lse;
+  }
+  if (grads) {
+    const uint32_t y = tgt[r];
+    const float lsef = (float)lse, scf = (float)scale;
+    const float kLog2e = 1.4426950408889634f;
+    if ((V % 8) == 0) {
+      uint4* s8 = reinterpret_cast<uint4*>(s);
+      for (int64_t q = threadIdx.x; q < V / 8; q += blockDim.x) {
+        uint4 u = s8[q];
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 f = __bfloat1622float2(h2[k]);
+          const int64_t w0 = q * 8 + 2 * k;
+          f.x = scf * exp2f((f.x - lsef) * kLog2e) - (w0 == y ? scf : 0.f);
+          f.y = scf * exp2f((f.y - lsef) * kLog2e) - (w0 + 1 == y ? scf : 0.f);
+          h2[k] = __float22bfloat162_rn(f);
+        }
+        s8[q] = u;
+      }
+    } else {
+      for (int64_t w = threadIdx.x; w < V; w += blockDim.x) {
+        const float f = __bfloat162float(s[w]);
+        s[w] = __float2bfloat16_rn(scf * exp2f((f - lsef) * kLog2e) - (w == y ? scf : 0.f));
+      }
+    }
+  }
+}
+
+// Deterministic sum of per-row losses (fixed order / fixed tree) and count
+// of scored rows; accumulates into acc[0] (loss) and cnt[0].
+__global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restrict__ wts,
+                           int64_t n, double* acc, unsigned long long* cnt) {
+  __shared__ double red[32];
+  double s = 0.0, c = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    s += v[i];
+    c += (wts == nullptr || wts[i]) ? 1.0 : 0.0;
+  }
+  s = block_sum_d<1024>(s, red);
+  c = block_sum_d<1024>(c, red);
+  if (threadIdx.x == 0) {
+    acc[0] += s;
+    if (cnt) cnt[0] += (unsigned long long)c;
+  }
+}
+
+// ------------------------------------------------------- embedding grads
+// SparseRowGrads for W_in (rnn.hpp:89-127, input_backward rnn.hpp:218-222):
+// positions are sorted by (word, processing order) where the processing
+// order of position (t, b) is (T-1-t)*B + b (the backward loop runs t
+// descending, b ascending), so every word's row is summed in exactly the
+// reference's float order.  One block, bitonic sort in shared memory.
+constexpr int kSortThreads = 1024;
+
+__global__ void __launch_bounds__(kSortThreads)
+k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int n_pow2,
+             int* __restrict__ seg_start, int* __restrict__ n_seg, int* __restrict__ order_pos,
+             uint32_t* __restrict__ seg_word) {
+  extern __shared__ unsigned long long keys[];
+  __shared__ int warp_cnt[32];
+  const int64_t n = T * B;
+  for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+    unsigned long long k = ~0ull;
+    if (i < n) {
+      const int64_t t = T - 1 - i / B, b = i % B;
+      k = ((unsigned long long)x[t * B + b] << 32) | (unsigned)i;
+    }
+    keys[i] = k;
+  }
+  __syncthreads();
+  for (int size = 2; size <= n_pow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n_pow2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long a = keys[lo], c = keys[hi];
+        if ((a > c) == up) { keys[lo] = c; keys[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  // segment heads + exclusive scan (chunked, fixed order)
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    int head = 0;
+    if (i < n) head = (i == 0) || ((keys[i] >> 32) != (keys[i - 1] >> 32));
+    const unsigned bal = __ballot_sync(0xffffffffu, head);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) warp_cnt[w] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += warp_cnt[k];
+    off += __popc(bal & ((1u << l) - 1));
+    if (i < n) {
+      const int ord = (int)(keys[i] & 0xffffffffu);
+      const int64_t t = T - 1 - ord / B, b = ord % B;
+      order_pos[i] = (int)(t * B + b);
+      if (head) {
+        seg_start[off] = i;
+        seg_word[off] = (uint32_t)(keys[i] >> 32);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < (int)(blockDim.x / 32); ++k) tot += warp_cnt[k];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *n_seg = base;
+    seg_start[base] = (int)n;
+  }
+}
+
+// Row sums per segment in processing order, then clip (rnn.hpp:155-162).
+__global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
+                             const int* __restrict__ seg_start, const int* __restrict__ n_seg,
+                             const int* __restrict__ order_pos, float* __restrict__ rows,
+                             float clip, int* nonfinite) {
+  const int slot = blockIdx.x;
+  if (slot >= *n_seg) return;
+  const int a = seg_start[slot], e = seg_start[slot + 1];
+  bool bad = false;
+  for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < H;
+       j += (int64_t)gridDim.y * blockDim.x) {
+    float acc = 0.f;
+    for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
+    acc = clip1(acc, clip);
+    bad |= !isfinite(acc);
+    rows[(int64_t)slot * H + j] = acc;
+  }
+  if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+}
+
+// Dense scatter of the compact rows (tests / dl_get_grads).
+__global__ void k_embed_dense(const float* __restrict__ rows, const uint32_t* __restrict__ words,
+                              const int* __restrict__ n_seg, int64_t H, float* __restrict__ dense) {
+  const int slot = blockIdx.x;
+  if (slot >= *n_seg) return;
+  for (int64_t j = threadIdx.x; j < H; j += blockDim.x)
+    dense[(int64_t)words[slot] * H + j] = rows[(int64_t)slot * H + j];
+}
+
+// --------------------------------------------------------------- rmsprop
+// rmsprop.hpp:118-124: per-element W_rec update in double, stored float.
+__global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                          const float* __restrict__ g, int64_t n, double rho, double eps,
+                          double eta, const int* __restrict__ nonfinite) {
+  if (*nonfinite) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = (double)g[i];
+    const float mi = (float)(rho * (double)m[i] + (1.0 - rho) * gi * gi);
+    m[i] = mi;
+    const float wi = w[i] - (float)(eta * gi / sqrt((double)mi + eps));
+    w[i] = wi;
+    if (wb) wb[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+// rmsprop.hpp:84 first loop: every W_in accumulator decays.
+__global__ void k_rms_decay(float* __restrict__ m, int64_t n, double rho,
+                            const int* __restrict__ nonfinite) {
+  if (*nonfinite) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m[i] = (float)(rho * (double)m[i]);
+}
+
+// rmsprop.hpp:85-91: touched rows add (1-rho)*mean(g^2) to the decayed
+// scalar, then divide the whole row's step by sqrt(m + eps).
+// rmsprop.hpp:94-107 (dense=1): m = float(rho*m + (1-rho)*mean(g^2)).
+// One warp per row.
+__global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                           const float* __restrict__ g, const uint32_t* __restrict__ words,
+                           const int* __restrict__ n_rows_dev, int64_t n_rows, int64_t H,
+                           double rho, double eps, double eta, int dense,
+                           const int* __restrict__ nonfinite) {
+  if (*nonfinite) return;
+  const int64_t rows = n_rows_dev ? (int64_t)*n_rows_dev : n_rows;
+  const int lane = threadIdx.x % 32;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float* gr = g + r * H;
+    const int64_t word = words ? (int64_t)words[r] : r;
+    double s = 0.0;
+    if ((H % 4) == 0) {
+      const float4* g4 = reinterpret_cast<const float4*>(gr);
+      for (int64_t j = lane; j < H / 4; j += 32) {
+        const float4 q = g4[j];
+        s += (double)q.x * (double)q.x + (double)q.y * (double)q.y +
+             (double)q.z * (double)q.z + (double)q.w * (double)q.w;
+      }
+    } else {
+      for (int64_t j = lane; j < H; j += 32) s += (double)gr[j] * (double)gr[j];
+    }
+    s = warp_sum_d(s);
+    const double ms = s / (double)H;
+    float mw;
+    if (dense) mw = (float)(rho * (double)m[word] + (1.0 - rho) * ms);
+    else mw = m[word] + (float)((1.0 - rho) * ms);
+    const double denom = sqrt((double)mw + eps);
+    float* wr = w + word * H;
+    bf16* wbr = wb ? wb + word * H : nullptr;
+    if ((H % 4) == 0) {
+      const float4* g4 = reinterpret_cast<const float4*>(gr);
+      float4* w4 = reinterpret_cast<float4*>(wr);
+      for (int64_t j = lane; j < H / 4; j += 32) {
+        const float4 q = g4[j];
+        float4 o = w4[j];
+        o.x -= (float)(eta * (double)q.x / denom);
+        o.y -= (float)(eta * (double)q.y / denom);
+        o.z -= (float)(eta * (double)q.z / denom);
+        o.w -= (float)(eta * (double)q.w / denom);
+        w4[j] = o;
+        if (wbr) {
+          __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wbr + 4 * j);
+          b2[0] = __floats2bfloat162_rn(o.x, o.y);
+          b2[1] = __floats2bfloat162_rn(o.z, o.w);
+        }
+      }
+    } else {
+      for (int64_t j = lane; j < H; j += 32) {
+        const float o = wr[j] - (float)(eta * (double)gr[j] / denom);
+        wr[j] = o;
+        if (wbr) wbr[j] = __float2bfloat16_rn(o);
+      }
+    }
+    if (lane == 0) m[word] = mw;
+  }
+}
+
+__global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long long* skipped) {
+  if (*nonfinite) skipped[0] += 1ull;
+}
+
+// ----------------------------------------------------- offset streams
+// Window build for group g = window % noffset (trainer.hpp:376-389): the
+// rank's streams are s = g*Bg + rank*B + b; pos = cursor[s] + t; x =
+// ids[pos % L], y = ids[(pos+1) % L], w = (y != bos).  Also gathers h0.
+__global__ void k_window_build(const uint32_t* __restrict__ ids, int64_t L,
+                               const int64_t* __restrict__ cursors, const float* __restrict__ hidden,
+                               const int64_t* __restrict__ win_counter, int noffset, int64_t B,
+                               int64_t T, int64_t H, uint32_t bos, uint32_t* __restrict__ x,
+                               uint32_t* __restrict__ y, uint8_t* __restrict__ w,
+                               float* __restrict__ h0) {
+  const int64_t g = *win_counter % noffset;
+  const int64_t s0 = g * B;  // cursors / hidden hold this rank's streams only
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < T * B; i += nthreads) {
+    const int64_t t = i / B, b = i % B;
+    const int64_t pos = cursors[s0 + b] + t;
+    const uint32_t xi = ids[pos % L];
+    const uint32_t yi = ids[(pos + 1) % L];
+    x[i] = xi;
+    y[i] = yi;
+    w[i] = yi == bos ? 0 : 1;
+  }
+  for (int64_t i = tid; i < B * H; i += nthreads) h0[i] = hidden[s0 * H + i];
+}
+
+// After the window (trainer.hpp:396-405): hidden <- h_final, cursor += T,
+// wrap -> cursor -= L and hidden = act(0).  Advances the window counter.
+__global__ void k_window_finish(int64_t* __restrict__ cursors, float* __restrict__ hidden,
+                                const float* __restrict__ h_final, int64_t* win_counter,
+                                int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0) {
+  const int64_t g = *win_counter % noffset;
+  const int64_t s0 = g * B;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < B * H; i += nthreads) {
+    const int64_t b = i / H;
+    const bool wrap = cursors[s0 + b] + T >= L;
+    hidden[s0 * H + i] = wrap ? a0 : h_final[i];
+  }
+  __syncthreads();
+  // single block updates the cursors after every thread has read them
+  if (blockIdx.x == 0) {
+    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+      int64_t c = cursors[s0 + b] + T;
+      if (c >= L) c -= L;
+      cursors[s0 + b] = c;
+    }
+  }
+}
+
+__global__ void k_counter_inc(int64_t* c) { c[0] += 1; }
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers
+static inline int grid_for(int64_t n, int tpb = 256, int cap = 148 * 16) {
+  int64_t g = (n + tpb - 1) / tpb;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st) {
+  k_f32_to_bf16<<<grid_for(n), 256, 0, st>>>(x, y, n);
+}
+void fill_f32(float* x, float v, int64_t n, cudaStream_t st) {
+  k_fill_f32<<<grid_for(n), 256, 0, st>>>(x, v, n);
+}
+void rec_fwd(const float* part, int splits, int64_t ss, int64_t Bn, int64_t H, const float* w_in,
+             const uint32_t* x, int act, float* h, bf16* hb, cudaStream_t st) {
+  k_rec_fwd<<<grid_for(Bn * H), 256, 0, st>>>(part, splits, ss, Bn, H, w_in, x, act, h, hb);
+}
+void rec_bwd(const float* part, int splits, int64_t ss, int64_t n, const float* dh_out,
+             const float* hnext, int act, float* dpre, bf16* dpreb, cudaStream_t st) {
+  k_rec_bwd<<<grid_for(n), 256, 0, st>>>(part, splits, ss, n, dh_out, hnext, act, dpre, dpreb);
+}
+void reduce_splits(const float* part, int splits, int64_t ss, int64_t n, float* out, float clip,
+                   int do_clip, int* nonfinite, cudaStream_t st) {
+  k_reduce<<<grid_for(n), 256, 0, st>>>(part, splits, ss, n, out, clip, do_clip, nonfinite);
+}
+void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const uint8_t* wts,
+                      double scale, int grads, double* loss_row, double* logp_row,
+                      cudaStream_t st) {
+  if (M <= 0) return;
+  k_softmax_rows_f32<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, tgt, wts, scale, grads, loss_row,
+                                                          logp_row);
+}
+void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_tiles,
+                       const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts,
+                       double scale, int grads, double* loss_row, double* logp_row,
+                       cudaStream_t st) {
+  if (M <= 0) return;
+  k_softmax_rows_bf16<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, M, part, n_tiles, tgt_logit, tgt,
+                                                           wts, scale, grads, loss_row, logp_row);
+}
+void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
+              unsigned long long* cnt, cudaStream_t st) {
+  k_sum_rows<<<1, 1024, 0, st>>>(v, wts, n, acc, cnt);
+}
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int64_t H,
+                 float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
+                 int* nonfinite, cudaStream_t st) {
+  const int64_t n = T * B;
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  const size_t smem = sizeof(unsigned long long) * p2;
+  static bool attr = false;
+  if (!attr) {
+    DL_CUDA(cudaFuncSetAttribute(k_embed_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    attr = true;
+  }
+  DL_REQUIRE(smem <= 200 * 1024, 1, "window too large for the embedding sort (T*B <= 16384)");
+  k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, p2, ws.seg_start, n_rows, ws.order_pos,
+                                               words);
+  dim3 grid((unsigned)n, (unsigned)((H + 255) / 256));
+  k_embed_rows<<<grid, 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows, clip,
+                                     nonfinite);
+}
+void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,
+                 int64_t H, float* dense, cudaStream_t st) {
+  if (max_rows <= 0) return;
+  k_embed_dense<<<(unsigned)max_rows, 256, 0, st>>>(rows, words, n_rows, H, dense);
+}
+void rms_rec(float* w, bf16* wb, float* m, const float* g, int64_t n, double rho, double eps,
+             double eta, const int* nonfinite, cudaStream_t st) {
+  k_rms_rec<<<grid_for(n), 256, 0, st>>>(w, wb, m, g, n, rho, eps, eta, nonfinite);
+}
+void rms_decay(float* m, int64_t n, double rho, const int* nonfinite, cudaStream_t st) {
+  k_rms_decay<<<grid_for(n), 256, 0, st>>>(m, n, rho, nonfinite);
+}
+void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* words,
+              const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
+              int dense, const int* nonfinite, cudaStream_t st) {
+  const int64_t warps = n_rows;
+  int blocks = (int)std::min<int64_t>((warps * 32 + 255) / 256, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  k_rms_rows<<<blocks, 256, 0, st>>>(w, wb, m, g, words, n_rows_dev, n_rows, H, rho, eps, eta,
+                                     dense, nonfinite);
+}
+void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st) {
+  k_count_skip<<<1, 1, 0, st>>>(nonfinite, skipped);
+}
+void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
+                  const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
+                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st) {
+  k_window_build<<<grid_for(std::max(T * B, B * H)), 256, 0, st>>>(
+      ids, L, cursors, hidden, win_counter, noffset, B, T, H, bos, x, y, w, h0);
+}
+void window_finish(int64_t* cursors, float* hidden, const float* h_final, int64_t* win_counter,
+                   int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0,
+                   cudaStream_t st) {
+  // one block: cursors must be read by every thread before the update
+  k_window_finish<<<1, 1024, 0, st>>>(cursors, hidden, h_final, win_counter, noffset, B, T, H, L,
+                                      a0);
+  k_counter_inc<<<1, 1, 0, st>>>(win_counter);
+}
+
+}  // namespace dl

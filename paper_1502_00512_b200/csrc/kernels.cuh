@@ -1,0 +1,51 @@
+// Launchers for the bandwidth-bound kernels (kernels.cu).
+#pragma once
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dl {
+
+struct EmbedWs {
+  int* seg_start;  // [T*B + 1]
+  int* order_pos;  // [T*B]
+};
+
+void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
+void fill_f32(float* x, float v, int64_t n, cudaStream_t st);
+void rec_fwd(const float* part, int splits, int64_t split_stride, int64_t Bn, int64_t H,
+             const float* w_in, const uint32_t* x, int act, float* h, bf16* hb, cudaStream_t st);
+void rec_bwd(const float* part, int splits, int64_t split_stride, int64_t n, const float* dh_out,
+             const float* hnext, int act, float* dpre, bf16* dpreb, cudaStream_t st);
+void reduce_splits(const float* part, int splits, int64_t split_stride, int64_t n, float* out,
+                   float clip, int do_clip, int* nonfinite, cudaStream_t st);
+void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const uint8_t* wts,
+                      double scale, int grads, double* loss_row, double* logp_row,
+                      cudaStream_t st);
+void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_tiles,
+                       const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts,
+                       double scale, int grads, double* loss_row, double* logp_row,
+                       cudaStream_t st);
+void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
+              unsigned long long* cnt, cudaStream_t st);
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int64_t H,
+                 float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
+                 int* nonfinite, cudaStream_t st);
+void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,
+                 int64_t H, float* dense, cudaStream_t st);
+void rms_rec(float* w, bf16* wb, float* m, const float* g, int64_t n, double rho, double eps,
+             double eta, const int* nonfinite, cudaStream_t st);
+void rms_decay(float* m, int64_t n, double rho, const int* nonfinite, cudaStream_t st);
+void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* words,
+              const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
+              int dense, const int* nonfinite, cudaStream_t st);
+void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st);
+void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
+                  const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
+                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st);
+void window_finish(int64_t* cursors, float* hidden, const float* h_final, int64_t* win_counter,
+                   int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0,
+                   cudaStream_t st);
+
+}  // namespace dl

@@ -1,0 +1,1077 @@
+// libdesklm_cuda.so runtime: the C ABI of include/desklm_cuda.h.
+//
+// Owns all device memory of one model on one GPU and sequences the kernels
+// of one truncated-BPTT window (backprop.hpp:76-222), the rmsprop update
+// (rmsprop.hpp:113-133), the forward scorers (eval.hpp:84-222) and the
+// offset-stream epoch schedule (trainer.hpp:350-410).  There is no CPU
+// compute path: every number is produced by a kernel in gemm_tc.cu,
+// gemm_simt.cu or kernels.cu.
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/desklm_cuda.h"
+#include "kernels.cuh"
+
+using namespace dl;
+
+namespace {
+thread_local std::string g_err;
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  DL_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+struct PhaseTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  size_t used = 0;
+  std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> open;
+};
+}  // namespace
+
+struct dl_ctx {
+  int device = 0;
+  int64_t V = 0, H = 0;
+  int act = 0, precision = DL_FP32;
+  cudaStream_t st = nullptr;
+  std::string err;
+  std::atomic<uint64_t> launches{0};
+
+  // parameters (fp32 masters, bf16 shadows for the tensor-core path)
+  float *w_in = nullptr, *w_rec = nullptr, *w_out = nullptr;
+  bf16 *w_rec_bf = nullptr, *w_out_bf = nullptr;
+  // optimiser
+  float *m_rec = nullptr, *m_in = nullptr, *m_out = nullptr;
+  double rho = 0.9995, eps = 1e-6;
+  // gradients of the last window
+  float *g_rec = nullptr, *g_out = nullptr, *g_in_rows = nullptr;
+  uint32_t* g_in_words = nullptr;
+  int* g_in_n = nullptr;
+  int* nonfinite = nullptr;
+  bool have_grads = false;
+
+  // window workspace
+  int64_t capT = 0, capB = 0;
+  float* htape = nullptr;  // (T+1) x B x H
+  bf16* htape_bf = nullptr;
+  uint32_t *x_d = nullptr, *y_d = nullptr;
+  uint8_t* w_d = nullptr;
+  void* S = nullptr;  // logits / dS: fp32 or bf16 [TB x V]
+  float2* part = nullptr;
+  int part_tiles = 0;
+  float* tgt_logit = nullptr;
+  double* loss_row = nullptr;
+  double* logp_row = nullptr;
+  float* dh_out = nullptr;
+  float* dpre = nullptr;
+  bf16* dpre_bf = nullptr;
+  float* splitws = nullptr;
+  size_t splitws_elems = 0;
+  EmbedWs ews{};
+  double* d_loss = nullptr;
+  unsigned long long* d_pos = nullptr;
+  unsigned long long* d_skipped = nullptr;
+  float* h0_d = nullptr;  // B x H staging for the trainer
+
+  // pinned staging for the host-buffer API
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  // trainer
+  uint32_t* ids = nullptr;
+  int64_t L = 0;
+  int noffset = 0, minibatch = 0, unroll = 0;
+  double clip = 1.0;
+  uint32_t bos = 1;
+  int64_t* cursors = nullptr;  // rank-local [noffset*minibatch]
+  float* hidden = nullptr;     // rank-local [noffset*minibatch x H]
+  int64_t* win_counter = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  double graph_eta = NAN;
+  bool use_graph = true;
+
+  // DP
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // profiling
+  bool profiling = false;
+  std::map<std::string, std::pair<double, int64_t>> prof;  // name -> (ms sum, count)
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+};
+
+namespace {
+
+int fail(dl_ctx* c, int code, const std::string& m) {
+  g_err = m;
+  if (c) c->err = m;
+  return code;
+}
+
+template <class F>
+int guarded(dl_ctx* c, F&& f) {
+  try {
+    if (c) DL_CUDA(cudaSetDevice(c->device));
+    f();
+    return DL_OK;
+  } catch (const Error& e) {
+    return fail(c, e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, DL_EDEVICE, e.what());
+  }
+}
+
+// ---------------------------------------------------------------- timing
+cudaEvent_t ev_get(dl_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    DL_CUDA(cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+struct Phase {
+  dl_ctx* c;
+  std::string name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Phase(dl_ctx* c_, const char* n) : c(c_), name(n) {
+    if (c->profiling) {
+      a = ev_get(c);
+      b = ev_get(c);
+      DL_CUDA(cudaEventRecord(a, c->st));
+    }
+  }
+  ~Phase() {
+    if (c->profiling) {
+      cudaEventRecord(b, c->st);
+      c->pending.push_back({name, {a, b}});
+    }
+  }
+};
+
+void prof_collect(dl_ctx* c) {
+  if (!c->profiling) return;
+  DL_CUDA(cudaStreamSynchronize(c->st));
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    DL_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+    auto& slot = c->prof[p.first];
+    slot.first += ms;
+    slot.second += 1;
+  }
+  c->pending.clear();
+  c->ev_used = 0;
+}
+
+// ----------------------------------------------------------- allocation
+void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
+  if (T <= c->capT && B <= c->capB && c->htape) return;
+  const int64_t nT = std::max(T, c->capT), nB = std::max(B, c->capB);
+  const int64_t TB = nT * nB, H = c->H, V = c->V;
+  auto fr = [](auto*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  fr(c->htape); fr(c->htape_bf); fr(c->x_d); fr(c->y_d); fr(c->w_d); fr(c->S); fr(c->part);
+  fr(c->tgt_logit); fr(c->loss_row); fr(c->logp_row); fr(c->dh_out); fr(c->dpre); fr(c->dpre_bf);
+  fr(c->g_in_rows); fr(c->g_in_words); fr(c->ews.seg_start); fr(c->ews.order_pos); fr(c->h0_d);
+  c->capT = nT;
+  c->capB = nB;
+  c->htape = dalloc<float>((nT + 1) * nB * H);
+  c->x_d = dalloc<uint32_t>(TB);
+  c->y_d = dalloc<uint32_t>(TB);
+  c->w_d = dalloc<uint8_t>(TB);
+  c->loss_row = dalloc<double>(TB);
+  c->logp_row = dalloc<double>(TB);
+  c->dh_out = dalloc<float>(TB * H);
+  c->dpre = dalloc<float>(TB * H);
+  c->g_in_rows = dalloc<float>(TB * H);
+  c->g_in_words = dalloc<uint32_t>(TB);
+  c->ews.seg_start = dalloc<int>(TB + 1);
+  c->ews.order_pos = dalloc<int>(TB);
+  c->h0_d = dalloc<float>(nB * H);
+  if (c->precision == DL_BF16) {
+    c->htape_bf = dalloc<bf16>((nT + 1) * nB * H);
+    c->dpre_bf = dalloc<bf16>(TB * H);
+    c->S = dalloc<bf16>(TB * V);
+    c->part_tiles = tc_n_tiles((int)V);
+    c->part = dalloc<float2>((size_t)c->part_tiles * TB);
+    c->tgt_logit = dalloc<float>(TB);
+  } else {
+    c->S = dalloc<float>(TB * V);
+  }
+}
+
+void ensure_splitws(dl_ctx* c, size_t elems) {
+  if (elems <= c->splitws_elems) return;
+  if (c->splitws) cudaFree(c->splitws);
+  c->splitws = dalloc<float>(elems);
+  c->splitws_elems = elems;
+}
+
+void* ensure_pinned(dl_ctx* c, size_t bytes) {
+  if (bytes <= c->pinned_bytes) return c->pinned;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  DL_CUDA(cudaMallocHost(&c->pinned, bytes));
+  c->pinned_bytes = bytes;
+  return c->pinned;
+}
+
+// ---------------------------------------------------------------- GEMMs
+bool tc(dl_ctx* c) { return c->precision == DL_BF16; }
+
+int pick_splits(dl_ctx* c, int M, int N, int K, int max_splits = 32) {
+  const int bn = tc(c) ? (N >= 256 ? 256 : (N >= 128 ? 128 : 64)) : 128;
+  const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  int s = std::max(1, std::min(max_splits, kNumSMs / std::max(1, tiles)));
+  if (tc(c)) s = tc_splits(K, s);
+  else s = std::max(1, std::min(s, (K + 63) / 64));
+  return s;
+}
+
+void gemm(dl_ctx* c, GemmDesc g) {
+  c->launches++;
+  if (tc(c)) gemm_tc(g, c->st);
+  else gemm_f32(g, c->st);
+}
+
+GemmDesc desc(int M, int N, int K, int am, const void* A, int64_t lda, int bm, const void* B,
+              int64_t ldb, float* C, int64_t ldc) {
+  GemmDesc g{};
+  g.M = M; g.N = N; g.K = K;
+  g.a_major = am; g.b_major = bm;
+  g.A = A; g.B = B; g.lda = lda; g.ldb = ldb;
+  g.C = C; g.ldc = ldc;
+  g.k_splits = 1;
+  g.split_stride = 0;
+  return g;
+}
+
+void refresh_shadows(dl_ctx* c) {
+  if (!tc(c)) return;
+  f32_to_bf16(c->w_rec, c->w_rec_bf, c->H * c->H, c->st);
+  f32_to_bf16(c->w_out, c->w_out_bf, c->V * c->H, c->st);
+  c->launches += 2;
+}
+
+// ------------------------------------------------ forward recurrence step
+// h_{t+1} = act(h_t . W_rec^T + W_in[x_t]) for Bn rows (backprop.hpp:102-112)
+void rec_step_fwd(dl_ctx* c, int64_t Bn, const float* h_prev, const bf16* h_prev_bf,
+                  const uint32_t* x, float* h_next, bf16* h_next_bf) {
+  const int64_t H = c->H;
+  const int s = pick_splits(c, (int)Bn, (int)H, (int)H);
+  ensure_splitws(c, (size_t)s * Bn * H);
+  GemmDesc g = tc(c) ? desc((int)Bn, (int)H, (int)H, K_MAJOR, h_prev_bf, H, K_MAJOR, c->w_rec_bf,
+                            H, c->splitws, H)
+                     : desc((int)Bn, (int)H, (int)H, K_MAJOR, h_prev, H, K_MAJOR, c->w_rec, H,
+                            c->splitws, H);
+  g.k_splits = s;
+  g.split_stride = Bn * H;
+  gemm(c, g);
+  rec_fwd(c->splitws, s, Bn * H, Bn, H, c->w_in, x, c->act, h_next, h_next_bf, c->st);
+  c->launches++;
+}
+
+// logits over M rows of `hs` with per-row targets; writes loss_row /
+// logp_row; with grads leaves dS in c->S.
+void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, const uint32_t* tgt,
+                  const uint8_t* wts, double scale, bool grads, double* loss_row,
+                  double* logp_row) {
+  const int64_t V = c->V, H = c->H;
+  if (tc(c)) {
+    GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs_bf, H, K_MAJOR, c->w_out_bf, H, nullptr, 0);
+    g.logits = 1;
+    g.S = grads ? static_cast<bf16*>(c->S) : nullptr;
+    g.lds = V;
+    g.part = c->part;
+    g.tgt = tgt;
+    g.tgt_logit = c->tgt_logit;
+    g.raster = 0;
+    {
+      Phase p(c, "logits");
+      gemm(c, g);
+    }
+    Phase p(c, "softmax");
+    softmax_rows_bf16(grads ? static_cast<bf16*>(c->S) : nullptr, M, V, c->part, c->part_tiles,
+                      c->tgt_logit, tgt, wts, scale, grads ? 1 : 0, loss_row, logp_row, c->st);
+    c->launches++;
+  } else {
+    GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs, H, K_MAJOR, c->w_out, H,
+                      static_cast<float*>(c->S), V);
+    {
+      Phase p(c, "logits");
+      gemm(c, g);
+    }
+    Phase p(c, "softmax");
+    softmax_rows_f32(static_cast<float*>(c->S), M, V, tgt, wts, scale, grads ? 1 : 0, loss_row,
+                     logp_row, c->st);
+    c->launches++;
+  }
+}
+
+// One window with device-resident inputs (x_d, y_d, w_d, htape[0]).
+// Accumulates loss into d_loss and scored positions into d_pos.
+void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool grads) {
+  const int64_t H = c->H, V = c->V, TB = T * B, BH = B * H;
+  cudaStream_t st = c->st;
+  if (tc(c)) {
+    f32_to_bf16(c->htape, c->htape_bf, BH, st);
+    c->launches++;
+  }
+  {
+    Phase p(c, "recurrence_fwd");
+    for (int64_t t = 0; t < T; ++t)
+      rec_step_fwd(c, B, c->htape + t * BH, tc(c) ? c->htape_bf + t * BH : nullptr,
+                   c->x_d + t * B, c->htape + (t + 1) * BH,
+                   tc(c) ? c->htape_bf + (t + 1) * BH : nullptr);
+  }
+  const float* Hs = c->htape + BH;
+  const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
+  output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
+  sum_rows(c->loss_row, c->w_d, TB, c->d_loss, c->d_pos, st);
+  c->launches++;
+  if (!grads) return;
+
+  DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
+  const bool dp = c->comm != nullptr;
+  // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
+  {
+    Phase p(c, "dh");
+    const int s = pick_splits(c, (int)TB, (int)H, (int)V, 8);
+    GemmDesc g = tc(c) ? desc((int)TB, (int)H, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->w_out_bf, H,
+                              c->dh_out, H)
+                       : desc((int)TB, (int)H, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->w_out, H,
+                              c->dh_out, H);
+    g.raster = 0;
+    if (s > 1) {
+      ensure_splitws(c, (size_t)s * TB * H);
+      g.C = c->splitws;
+      g.k_splits = s;
+      g.split_stride = TB * H;
+      gemm(c, g);
+      reduce_splits(c->splitws, s, TB * H, TB * H, c->dh_out, 0.f, 0, nullptr, st);
+      c->launches++;
+    } else {
+      gemm(c, g);
+    }
+  }
+  // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
+  {
+    Phase p(c, "dw_out");
+    GemmDesc g = tc(c) ? desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs_bf, H,
+                              c->g_out, H)
+                       : desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs, H,
+                              c->g_out, H);
+    g.raster = 1;
+    g.do_clip = dp ? 0 : 1;
+    g.clip = clip;
+    g.nonfinite = c->nonfinite;
+    gemm(c, g);
+  }
+  // backward recurrence (backprop.hpp:197-219)
+  {
+    Phase p(c, "recurrence_bwd");
+    for (int64_t t = T - 1; t >= 0; --t) {
+      float* dp_t = c->dpre + t * BH;
+      bf16* dpb_t = tc(c) ? c->dpre_bf + t * BH : nullptr;
+      int s = 0;
+      if (t < T - 1) {
+        s = pick_splits(c, (int)B, (int)H, (int)H);
+        ensure_splitws(c, (size_t)s * BH);
+        GemmDesc g = tc(c) ? desc((int)B, (int)H, (int)H, K_MAJOR, c->dpre_bf + (t + 1) * BH, H,
+                                  MN_MAJOR, c->w_rec_bf, H, c->splitws, H)
+                           : desc((int)B, (int)H, (int)H, K_MAJOR, c->dpre + (t + 1) * BH, H,
+                                  MN_MAJOR, c->w_rec, H, c->splitws, H);
+        g.k_splits = s;
+        g.split_stride = BH;
+        gemm(c, g);
+      }
+      rec_bwd(c->splitws, s, BH, BH, c->dh_out + t * BH, c->htape + (t + 1) * BH, c->act, dp_t,
+              dpb_t, st);
+      c->launches++;
+    }
+  }
+  // dW_rec = sum_t dpre_t^T . h_t  [H x H] (backprop.hpp:214)
+  {
+    Phase p(c, "dw_rec");
+    const int s = pick_splits(c, (int)H, (int)H, (int)TB, 16);
+    ensure_splitws(c, (size_t)s * H * H);
+    GemmDesc g = tc(c) ? desc((int)H, (int)H, (int)TB, MN_MAJOR, c->dpre_bf, H, MN_MAJOR,
+                              c->htape_bf, H, c->splitws, H)
+                       : desc((int)H, (int)H, (int)TB, MN_MAJOR, c->dpre, H, MN_MAJOR, c->htape, H,
+                              c->splitws, H);
+    g.k_splits = s;
+    g.split_stride = H * H;
+    gemm(c, g);
+    reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dp ? 0 : 1, c->nonfinite, st);
+    c->launches++;
+  }
+  // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped
+  {
+    Phase p(c, "embed_grad");
+    embed_grads(c->x_d, T, B, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words, c->g_in_n,
+                c->nonfinite, st);
+    c->launches += 2;
+  }
+  c->have_grads = true;
+}
+
+void run_rmsprop(dl_ctx* c, double eta, int64_t TB) {
+  Phase p(c, "rmsprop");
+  cudaStream_t st = c->st;
+  rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
+          c->eps, eta, c->nonfinite, st);
+  rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
+  rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
+           c->eps, eta, 0, c->nonfinite, st);
+  rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->V,
+           c->H, c->rho, c->eps, eta, 1, c->nonfinite, st);
+  count_skip(c->nonfinite, c->d_skipped, st);
+  c->launches += 5;
+}
+
+float act0(int act) { return act == 0 ? 0.5f : 0.0f; }
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* dl_last_error(const dl_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+const char* dl_version(void) { return "desklm-b200 0.1 (sm_100a)"; }
+
+int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int precision) {
+  if (!out) return fail(nullptr, DL_EINVAL, "dl_create: null out");
+  *out = nullptr;
+  if (V < 1 || H < 1) return fail(nullptr, DL_EINVAL, "RnnParams: V,H >= 1");
+  if (act != DL_SIGMOID && act != DL_TANH) return fail(nullptr, DL_EINVAL, "bad activation");
+  if (precision != DL_FP32 && precision != DL_BF16) return fail(nullptr, DL_EINVAL, "bad precision");
+  if (precision == DL_BF16 && ((H % 8) != 0 || (V % 8) != 0))
+    return fail(nullptr, DL_EINVAL, "bf16 tensor-core mode needs V and H multiples of 8 (TMA)");
+  dl_ctx* c = new dl_ctx();
+  c->device = device;
+  c->V = V;
+  c->H = H;
+  c->act = act;
+  c->precision = precision;
+  const int rc = guarded(c, [&] {
+    int n = 0;
+    DL_CUDA(cudaGetDeviceCount(&n));
+    DL_REQUIRE(device >= 0 && device < n, DL_EINVAL, "dl_create: no such device");
+    cudaDeviceProp prop;
+    DL_CUDA(cudaGetDeviceProperties(&prop, device));
+    DL_REQUIRE(prop.major == 10, DL_EDEVICE,
+               "libdesklm_cuda is built for sm_100a (B200); device is sm_" +
+                   std::to_string(prop.major * 10 + prop.minor));
+    DL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->w_in = dalloc<float>(V * H);
+    c->w_rec = dalloc<float>(H * H);
+    c->w_out = dalloc<float>(V * H);
+    c->m_rec = dalloc<float>(H * H);
+    c->m_in = dalloc<float>(V);
+    c->m_out = dalloc<float>(V);
+    c->g_rec = dalloc<float>(H * H);
+    c->g_out = dalloc<float>(V * H);
+    c->g_in_n = dalloc<int>(1);
+    c->nonfinite = dalloc<int>(1);
+    c->d_loss = dalloc<double>(1);
+    c->d_pos = dalloc<unsigned long long>(1);
+    c->d_skipped = dalloc<unsigned long long>(1);
+    c->win_counter = dalloc<int64_t>(1);
+    if (precision == DL_BF16) {
+      c->w_rec_bf = dalloc<bf16>(H * H);
+      c->w_out_bf = dalloc<bf16>(V * H);
+    }
+    DL_CUDA(cudaMemsetAsync(c->w_in, 0, V * H * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->w_rec, 0, H * H * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->w_out, 0, V * H * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->m_rec, 0, H * H * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->m_in, 0, V * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->m_out, 0, V * 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, 4, c->st));
+    DL_CUDA(cudaMemsetAsync(c->g_in_n, 0, 4, c->st));
+    refresh_shadows(c);
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+  if (rc != DL_OK) {
+    g_err = c->err;
+    dl_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return DL_OK;
+}
+
+int dl_destroy(dl_ctx* c) {
+  if (!c) return DL_OK;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->comm) ncclCommDestroy(c->comm);
+  void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->m_rec, c->m_in,
+                  c->m_out, c->g_rec, c->g_out, c->g_in_rows, c->g_in_words, c->g_in_n,
+                  c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
+                  c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
+                  c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
+                  c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return DL_OK;
+}
+
+int dl_set_params(dl_ctx* c, const float* w_in, const float* w_rec, const float* w_out) {
+  if (!c || !w_in || !w_rec || !w_out) return fail(c, DL_EINVAL, "dl_set_params: null argument");
+  return guarded(c, [&] {
+    DL_CUDA(cudaMemcpyAsync(c->w_in, w_in, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->w_rec, w_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->w_out, w_out, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    refresh_shadows(c);
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_get_params(dl_ctx* c, float* w_in, float* w_rec, float* w_out) {
+  if (!c) return fail(c, DL_EINVAL, "dl_get_params: null ctx");
+  return guarded(c, [&] {
+    if (w_in) DL_CUDA(cudaMemcpyAsync(w_in, c->w_in, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (w_rec) DL_CUDA(cudaMemcpyAsync(w_rec, c->w_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (w_out) DL_CUDA(cudaMemcpyAsync(w_out, c->w_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_set_opt(dl_ctx* c, const float* m_rec, const float* m_in, const float* m_out, double rho,
+               double eps) {
+  if (!c) return fail(c, DL_EINVAL, "dl_set_opt: null ctx");
+  if (!(rho > 0.0 && rho < 1.0)) return fail(c, DL_EINVAL, "rmsprop: rho must be in (0,1)");
+  if (!(eps > 0.0)) return fail(c, DL_EINVAL, "rmsprop: eps must be > 0");
+  return guarded(c, [&] {
+    c->rho = rho;
+    c->eps = eps;
+    if (m_rec) DL_CUDA(cudaMemcpyAsync(c->m_rec, m_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    if (m_in) DL_CUDA(cudaMemcpyAsync(c->m_in, m_in, c->V * 4, cudaMemcpyHostToDevice, c->st));
+    if (m_out) DL_CUDA(cudaMemcpyAsync(c->m_out, m_out, c->V * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  });
+}
+
+int dl_get_opt(dl_ctx* c, float* m_rec, float* m_in, float* m_out) {
+  if (!c) return fail(c, DL_EINVAL, "dl_get_opt: null ctx");
+  return guarded(c, [&] {
+    if (m_rec) DL_CUDA(cudaMemcpyAsync(m_rec, c->m_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (m_in) DL_CUDA(cudaMemcpyAsync(m_in, c->m_in, c->V * 4, cudaMemcpyDeviceToHost, c->st));
+    if (m_out) DL_CUDA(cudaMemcpyAsync(m_out, c->m_out, c->V * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_window(dl_ctx* c, int64_t T, int64_t B, const uint32_t* inputs, const uint32_t* targets,
+              const uint8_t* weights, const float* h0, float* h_final, double loss_scale,
+              float clip, int compute_grads, double* loss, uint64_t* positions) {
+  if (!c) return fail(c, DL_EINVAL, "dl_window: null ctx");
+  if (T < 1 || B < 1) return fail(c, DL_EINVAL, "bptt: empty window");
+  if (!inputs || !targets || !weights || !h0) return fail(c, DL_EINVAL, "bptt: null window arrays");
+  for (int64_t i = 0; i < T * B; ++i)
+    if (inputs[i] >= (uint64_t)c->V || targets[i] >= (uint64_t)c->V)
+      return fail(c, DL_EINVAL, "bptt: word id out of range");
+  return guarded(c, [&] {
+    ensure_window(c, T, B);
+    const int64_t TB = T * B, BH = B * c->H;
+    // one pinned staging copy of the window inputs, then async H2D
+    const size_t bytes = TB * 4 * 2 + TB + BH * 4 + 64;
+    uint8_t* pin = static_cast<uint8_t*>(ensure_pinned(c, std::max<size_t>(bytes, BH * 4 + 64)));
+    std::memcpy(pin, inputs, TB * 4);
+    std::memcpy(pin + TB * 4, targets, TB * 4);
+    std::memcpy(pin + TB * 8, weights, TB);
+    float* ph0 = reinterpret_cast<float*>(pin + ((TB * 9 + 15) / 16) * 16);
+    std::memcpy(ph0, h0, BH * 4);
+    DL_CUDA(cudaMemcpyAsync(c->x_d, pin, TB * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->y_d, pin + TB * 4, TB * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->w_d, pin + TB * 8, TB, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->htape, ph0, BH * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemsetAsync(c->d_loss, 0, 8, c->st));
+    DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
+    run_window(c, T, B, loss_scale, clip, compute_grads != 0);
+    struct { double l; unsigned long long p; } res;
+    DL_CUDA(cudaMemcpyAsync(&res.l, c->d_loss, 8, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaMemcpyAsync(&res.p, c->d_pos, 8, cudaMemcpyDeviceToHost, c->st));
+    if (h_final)
+      DL_CUDA(cudaMemcpyAsync(h_final, c->htape + T * BH, BH * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    if (loss) *loss = res.l;
+    if (positions) *positions = res.p;
+    c->capT = std::max(c->capT, T);
+  });
+}
+
+int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
+  if (!c) return fail(c, DL_EINVAL, "dl_get_grads: null ctx");
+  if (!c->have_grads) return fail(c, DL_EINVAL, "dl_get_grads: no gradients computed yet");
+  return guarded(c, [&] {
+    if (g_in_dense) {
+      float* dense = dalloc<float>(c->V * c->H);
+      DL_CUDA(cudaMemsetAsync(dense, 0, c->V * c->H * 4, c->st));
+      embed_dense(c->g_in_rows, c->g_in_words, c->g_in_n, c->capT * c->capB, c->H, dense, c->st);
+      DL_CUDA(cudaMemcpyAsync(g_in_dense, dense, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      cudaFree(dense);
+    }
+    if (g_rec) DL_CUDA(cudaMemcpyAsync(g_rec, c->g_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (g_out) DL_CUDA(cudaMemcpyAsync(g_out, c->g_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_set_grads(dl_ctx* c, int64_t n_in_rows, const uint32_t* in_words, const float* in_rows,
+                 const float* g_rec, const float* g_out) {
+  if (!c || !g_rec || !g_out || (n_in_rows > 0 && (!in_words || !in_rows)))
+    return fail(c, DL_EINVAL, "dl_set_grads: null argument");
+  if (n_in_rows < 0) return fail(c, DL_EINVAL, "dl_set_grads: bad row count");
+  for (int64_t i = 0; i < n_in_rows; ++i)
+    if (in_words[i] >= (uint64_t)c->V) return fail(c, DL_EINVAL, "dl_set_grads: word out of range");
+  return guarded(c, [&] {
+    if (n_in_rows > c->capT * c->capB) ensure_window(c, n_in_rows, 1);
+    const int n = (int)n_in_rows;
+    DL_CUDA(cudaMemcpyAsync(c->g_in_n, &n, 4, cudaMemcpyHostToDevice, c->st));
+    if (n_in_rows > 0) {
+      DL_CUDA(cudaMemcpyAsync(c->g_in_words, in_words, n_in_rows * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->g_in_rows, in_rows, n_in_rows * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    }
+    DL_CUDA(cudaMemcpyAsync(c->g_rec, g_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->g_out, g_out, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    // finite check of the injected gradients (rmsprop.hpp:116 / rnn.hpp:165-171)
+    int bad = 0;
+    auto fin = [&](const float* p, int64_t k) {
+      for (int64_t i = 0; i < k; ++i)
+        if (!std::isfinite(p[i])) return false;
+      return true;
+    };
+    bad = !(fin(g_rec, c->H * c->H) && fin(g_out, c->V * c->H) &&
+            (n_in_rows == 0 || fin(in_rows, n_in_rows * c->H)));
+    DL_CUDA(cudaMemcpyAsync(c->nonfinite, &bad, 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    c->have_grads = true;
+  });
+}
+
+int dl_rmsprop(dl_ctx* c, double eta, int* applied) {
+  if (!c) return fail(c, DL_EINVAL, "dl_rmsprop: null ctx");
+  if (!c->have_grads) return fail(c, DL_EINVAL, "dl_rmsprop: no gradients computed yet");
+  return guarded(c, [&] {
+    run_rmsprop(c, eta, c->capT * c->capB);
+    int bad = 0;
+    DL_CUDA(cudaMemcpyAsync(&bad, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    if (applied) *applied = bad ? 0 : 1;
+  });
+}
+
+int dl_score(dl_ctx* c, int64_t S, int64_t steps, const uint32_t* in, const int64_t* tgt,
+             const float* h0, float* h_final, double* logp, double* total_logprob,
+             uint64_t* predicted) {
+  if (!c) return fail(c, DL_EINVAL, "dl_score: null ctx");
+  if (S < 1 || steps < 0) return fail(c, DL_EINVAL, "dl_score: bad shape");
+  for (int64_t i = 0; i < S * steps; ++i) {
+    if (in[i] >= (uint64_t)c->V) return fail(c, DL_EDATA, "score: id out of vocabulary range");
+    if (tgt[i] >= c->V) return fail(c, DL_EDATA, "score: id out of vocabulary range");
+  }
+  return guarded(c, [&] {
+    const int64_t H = c->H, SH = S * H;
+    // bank several steps per logits GEMM (eval.hpp:45 kScoreBank idea)
+    int64_t bank = std::max<int64_t>(1, std::min<int64_t>(steps, 4096 / S));
+    if (bank < 1) bank = 1;
+    ensure_window(c, bank, S);
+    std::vector<double> lp(S * steps, NAN);
+    double* pin = static_cast<double*>(ensure_pinned(c, sizeof(double) * bank * S * 2 + 64));
+    // initial state
+    if (h0) DL_CUDA(cudaMemcpyAsync(c->htape, h0, SH * 4, cudaMemcpyHostToDevice, c->st));
+    else fill_f32(c->htape, act0(c->act), SH, c->st);
+    std::vector<uint32_t> ytmp(bank * S);
+    std::vector<uint8_t> wtmp(bank * S);
+    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
+      const int64_t nb = std::min(bank, steps - j0);
+      DL_CUDA(cudaMemcpyAsync(c->x_d, in + j0 * S, nb * S * 4, cudaMemcpyHostToDevice, c->st));
+      bool any = false;
+      for (int64_t i = 0; i < nb * S; ++i) {
+        const int64_t t = tgt[j0 * S + i];
+        ytmp[i] = t >= 0 ? (uint32_t)t : 0u;
+        wtmp[i] = t >= 0 ? 1 : 0;
+        any |= t >= 0;
+      }
+      DL_CUDA(cudaMemcpyAsync(c->y_d, ytmp.data(), nb * S * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->w_d, wtmp.data(), nb * S, cudaMemcpyHostToDevice, c->st));
+      if (tc(c)) f32_to_bf16(c->htape, c->htape_bf, SH, c->st);
+      {
+        Phase p(c, "recurrence_fwd");
+        for (int64_t t = 0; t < nb; ++t)
+          rec_step_fwd(c, S, c->htape + t * SH, tc(c) ? c->htape_bf + t * SH : nullptr,
+                       c->x_d + t * S, c->htape + (t + 1) * SH,
+                       tc(c) ? c->htape_bf + (t + 1) * SH : nullptr);
+      }
+      if (any)
+        output_layer(c, nb * S, c->htape + SH, tc(c) ? c->htape_bf + SH : nullptr, c->y_d, c->w_d,
+                     1.0, false, nullptr, c->logp_row);
+      // carry the last state to slot 0 for the next bank
+      DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * SH, SH * 4, cudaMemcpyDeviceToDevice, c->st));
+      if (any) {
+        DL_CUDA(cudaMemcpyAsync(pin, c->logp_row, nb * S * 8, cudaMemcpyDeviceToHost, c->st));
+        DL_CUDA(cudaStreamSynchronize(c->st));
+        for (int64_t i = 0; i < nb * S; ++i)
+          if (wtmp[i]) lp[j0 * S + i] = pin[i];
+      }
+      DL_CUDA(cudaStreamSynchronize(c->st));
+    }
+    if (h_final) DL_CUDA(cudaMemcpyAsync(h_final, c->htape, SH * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    double tot = 0.0;
+    uint64_t pred = 0;
+    for (int64_t i = 0; i < S * steps; ++i)
+      if (tgt[i] >= 0) {
+        tot += lp[i];
+        ++pred;
+      }
+    if (logp) std::memcpy(logp, lp.data(), sizeof(double) * S * steps);
+    if (total_logprob) *total_logprob = tot;
+    if (predicted) *predicted = pred;
+  });
+}
+
+int dl_sharded_perplexity(dl_ctx* c, const uint32_t* ids, int64_t n, int shards, uint32_t bos,
+                          double* total_logprob, uint64_t* predicted, double* perplexity) {
+  if (!c) return fail(c, DL_EINVAL, "dl_sharded_perplexity: null ctx");
+  if (n < 2) return fail(c, DL_EINVAL, "sharded perplexity: stream too short");
+  if (shards < 1) return fail(c, DL_EINVAL, "sharded perplexity: shards must be >= 1");
+  // eval.hpp:160-195: S = min(shards, n/2) slices begin = s*n/S walked cold
+  const int64_t S = std::min<int64_t>(shards, n / 2);
+  std::vector<int64_t> begin(S + 1);
+  for (int64_t s = 0; s <= S; ++s) begin[s] = s * n / S;
+  int64_t max_len = 0;
+  for (int64_t s = 0; s < S; ++s) max_len = std::max(max_len, begin[s + 1] - begin[s]);
+  const int64_t steps = std::max<int64_t>(0, max_len - 1);
+  std::vector<uint32_t> in(S * steps);
+  std::vector<int64_t> tg(S * steps);
+  for (int64_t j = 0; j < steps; ++j)
+    for (int64_t s = 0; s < S; ++s) {
+      const int64_t len = begin[s + 1] - begin[s];
+      if (j + 1 < len) {
+        const uint32_t x = ids[begin[s] + j], y = ids[begin[s] + j + 1];
+        if (x >= (uint64_t)c->V || y >= (uint64_t)c->V)
+          return fail(c, DL_EDATA, "sharded perplexity: id out of vocabulary range");
+        in[j * S + s] = x;
+        tg[j * S + s] = y == bos ? -1 : (int64_t)y;
+      } else {
+        in[j * S + s] = 0;
+        tg[j * S + s] = -1;
+      }
+    }
+  double tot = 0.0;
+  uint64_t pred = 0;
+  const int rc = dl_score(c, S, steps, in.data(), tg.data(), nullptr, nullptr, nullptr, &tot, &pred);
+  if (rc != DL_OK) return rc;
+  if (pred == 0) return fail(c, DL_EINVAL, "sharded perplexity: no predicted tokens");
+  if (total_logprob) *total_logprob = tot;
+  if (predicted) *predicted = pred;
+  if (perplexity) *perplexity = std::exp(-tot / (double)pred);
+  return DL_OK;
+}
+
+int dl_rnn_perplexity(dl_ctx* c, const uint32_t* ids, int64_t n, uint32_t bos,
+                      double* total_logprob, uint64_t* predicted, double* perplexity) {
+  if (!c) return fail(c, DL_EINVAL, "dl_rnn_perplexity: null ctx");
+  if (n < 2) return fail(c, DL_EINVAL, "rnn perplexity: stream too short");
+  // eval.hpp:123-137: one stream, every token is input; non-bos targets scored
+  std::vector<int64_t> tg(n - 1);
+  for (int64_t i = 0; i + 1 < n; ++i) {
+    if (ids[i] >= (uint64_t)c->V || ids[i + 1] >= (uint64_t)c->V)
+      return fail(c, DL_EDATA, "rnn perplexity: id out of vocabulary range");
+    tg[i] = ids[i + 1] == bos ? -1 : (int64_t)ids[i + 1];
+  }
+  double tot = 0.0;
+  uint64_t pred = 0;
+  const int rc = dl_score(c, 1, n - 1, ids, tg.data(), nullptr, nullptr, nullptr, &tot, &pred);
+  if (rc != DL_OK) return rc;
+  if (pred == 0) return fail(c, DL_EINVAL, "rnn perplexity: no predicted tokens");
+  if (total_logprob) *total_logprob = tot;
+  if (predicted) *predicted = pred;
+  if (perplexity) *perplexity = std::exp(-tot / (double)pred);
+  return DL_OK;
+}
+
+// ------------------------------------------------------------- trainer
+int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int minibatch,
+                    int unroll, double clip, uint32_t bos) {
+  if (!c) return fail(c, DL_EINVAL, "dl_trainer_init: null ctx");
+  if (noffset < 1 || minibatch < 1 || unroll < 1)
+    return fail(c, DL_EINVAL, "config: noffset, minibatch, unroll must be >= 1");
+  if (!(clip > 0.0)) return fail(c, DL_EINVAL, "config: clip must be > 0");
+  const int64_t Nglob = (int64_t)noffset * minibatch * c->nranks;
+  if (L < Nglob) return fail(c, DL_EINVAL, "trainer: training stream shorter than the stream count");
+  for (int64_t i = 0; i < L; ++i)
+    if (ids[i] >= (uint64_t)c->V) return fail(c, DL_EDATA, "trainer: id out of vocabulary range");
+  return guarded(c, [&] {
+    if (c->ids) cudaFree(c->ids);
+    if (c->cursors) cudaFree(c->cursors);
+    if (c->hidden) cudaFree(c->hidden);
+    c->L = L;
+    c->noffset = noffset;
+    c->minibatch = minibatch;
+    c->unroll = unroll;
+    c->clip = clip;
+    c->bos = bos;
+    c->ids = dalloc<uint32_t>(L);
+    DL_CUDA(cudaMemcpyAsync(c->ids, ids, L * 4, cudaMemcpyHostToDevice, c->st));
+    const int64_t Nl = (int64_t)noffset * minibatch;
+    c->cursors = dalloc<int64_t>(Nl);
+    c->hidden = dalloc<float>(Nl * c->H);
+    // trainer.hpp:194-198 with this rank's slice of every group
+    std::vector<int64_t> cur(Nl);
+    const int64_t Bg = (int64_t)minibatch * c->nranks;
+    for (int64_t g = 0; g < noffset; ++g)
+      for (int64_t b = 0; b < minibatch; ++b) {
+        const int64_t s = g * Bg + c->rank * minibatch + b;
+        cur[g * minibatch + b] = s * L / Nglob;
+      }
+    DL_CUDA(cudaMemcpyAsync(c->cursors, cur.data(), Nl * 8, cudaMemcpyHostToDevice, c->st));
+    fill_f32(c->hidden, act0(c->act), Nl * c->H, c->st);
+    ensure_window(c, unroll, minibatch);
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  });
+}
+
+int dl_trainer_get_state(dl_ctx* c, int64_t* cursors, float* hidden) {
+  if (!c || !c->cursors) return fail(c, DL_EINVAL, "trainer not initialised");
+  return guarded(c, [&] {
+    const int64_t Nl = (int64_t)c->noffset * c->minibatch;
+    if (cursors) DL_CUDA(cudaMemcpyAsync(cursors, c->cursors, Nl * 8, cudaMemcpyDeviceToHost, c->st));
+    if (hidden) DL_CUDA(cudaMemcpyAsync(hidden, c->hidden, Nl * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_trainer_set_state(dl_ctx* c, const int64_t* cursors, const float* hidden) {
+  if (!c || !c->cursors) return fail(c, DL_EINVAL, "trainer not initialised");
+  const int64_t Nl = (int64_t)c->noffset * c->minibatch;
+  if (cursors)
+    for (int64_t i = 0; i < Nl; ++i)
+      if (cursors[i] < 0 || cursors[i] >= c->L)
+        return fail(c, DL_EDATA, "trainer checkpoint: cursor out of range");
+  return guarded(c, [&] {
+    if (cursors) DL_CUDA(cudaMemcpyAsync(c->cursors, cursors, Nl * 8, cudaMemcpyHostToDevice, c->st));
+    if (hidden) DL_CUDA(cudaMemcpyAsync(c->hidden, hidden, Nl * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+namespace {
+// Size the split-K workspace for a T x B window before graph capture
+// (no allocation may happen inside a capture).
+void presize(dl_ctx* c, int64_t T, int64_t B) {
+  const int64_t H = c->H, V = c->V, TB = T * B;
+  size_t need = (size_t)pick_splits(c, (int)B, (int)H, (int)H) * B * H;
+  const int sdh = pick_splits(c, (int)TB, (int)H, (int)V, 8);
+  if (sdh > 1) need = std::max(need, (size_t)sdh * TB * H);
+  need = std::max(need, (size_t)pick_splits(c, (int)H, (int)H, (int)TB, 16) * H * H);
+  ensure_splitws(c, need);
+}
+
+// One device-resident window of the epoch schedule (trainer.hpp:376-405).
+void trainer_window(dl_ctx* c, double eta) {
+  const int64_t B = c->minibatch, T = c->unroll, H = c->H;
+  const double scale = 1.0 / (double)(B * c->nranks * T);
+  window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
+               c->x_d, c->y_d, c->w_d, c->htape, c->st);
+  c->launches++;
+  run_window(c, T, B, scale, (float)c->clip, true);
+  run_rmsprop(c, eta, T * B);
+  window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
+                c->L, act0(c->act), c->st);
+  c->launches += 2;
+}
+}  // namespace
+
+int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* loss_sum,
+                   uint64_t* skipped) {
+  if (!c || !c->ids) return fail(c, DL_EINVAL, "trainer not initialised");
+  if (!(eta > 0.0)) return fail(c, DL_EINVAL, "config: eta must be > 0");
+  return guarded(c, [&] {
+    DL_CUDA(cudaMemcpyAsync(c->win_counter, &first, 8, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemsetAsync(c->d_loss, 0, 8, c->st));
+    DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
+    DL_CUDA(cudaMemsetAsync(c->d_skipped, 0, 8, c->st));
+    const bool graphs = c->use_graph && !c->profiling && c->comm == nullptr;
+    presize(c, c->unroll, c->minibatch);
+    if (graphs) {
+      if (!c->graph || c->graph_eta != eta) {
+        if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+        // warm-up launch outside capture (lazy attribute setup, workspaces)
+        cudaGraph_t gph;
+        DL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        try {
+          trainer_window(c, eta);
+        } catch (...) {
+          cudaStreamEndCapture(c->st, &gph);
+          throw;
+        }
+        DL_CUDA(cudaStreamEndCapture(c->st, &gph));
+        DL_CUDA(cudaGraphInstantiate(&c->graph, gph, 0));
+        cudaGraphDestroy(gph);
+        c->graph_eta = eta;
+      }
+      for (int64_t i = 0; i < count; ++i) DL_CUDA(cudaGraphLaunch(c->graph, c->st));
+    } else {
+      for (int64_t i = 0; i < count; ++i) trainer_window(c, eta);
+    }
+    double l = 0.0;
+    unsigned long long sk = 0;
+    DL_CUDA(cudaMemcpyAsync(&l, c->d_loss, 8, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaMemcpyAsync(&sk, c->d_skipped, 8, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    prof_collect(c);
+    if (loss_sum) *loss_sum += l;
+    if (skipped) *skipped += sk;
+  });
+}
+
+// ---------------------------------------------------------------- comm
+int dl_comm_unique_id(uint8_t id[128]) {
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return fail(nullptr, DL_EDEVICE, "ncclGetUniqueId failed");
+  std::memcpy(id, &u, 128);
+  return DL_OK;
+}
+
+int dl_comm_init(dl_ctx* c, const uint8_t id[128], int nranks, int rank) {
+  if (!c) return fail(c, DL_EINVAL, "dl_comm_init: null ctx");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, DL_EINVAL, "dl_comm_init: bad rank");
+  return guarded(c, [&] {
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks == 1) return;
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    DL_REQUIRE(ncclCommInitRank(&c->comm, nranks, u, rank) == ncclSuccess, DL_EDEVICE,
+               "ncclCommInitRank failed");
+  });
+}
+
+// Test hook: C[M x N] = A . B^T through the context's GEMM engine, with A
+// stored K-major [M x K] or MN-major [K x M] (likewise B), fp32 host arrays
+// (rounded to bf16 on the device in DL_BF16 mode).  With tgt != NULL the
+// logits epilogue runs instead and C receives per-row (lse, target logit).
+int dl_test_gemm(dl_ctx* c, int M, int N, int K, int a_major, int b_major, const float* A,
+                 const float* B, float* Cout, int splits, const uint32_t* tgt) {
+  if (!c || M < 1 || N < 1 || K < 1) return fail(c, DL_EINVAL, "dl_test_gemm: bad shape");
+  return guarded(c, [&] {
+    const int64_t na = (int64_t)M * K, nb = (int64_t)N * K;
+    float *a32 = dalloc<float>(na), *b32 = dalloc<float>(nb);
+    DL_CUDA(cudaMemcpyAsync(a32, A, na * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(b32, B, nb * 4, cudaMemcpyHostToDevice, c->st));
+    bf16 *a16 = nullptr, *b16 = nullptr;
+    if (tc(c)) {
+      a16 = dalloc<bf16>(na);
+      b16 = dalloc<bf16>(nb);
+      f32_to_bf16(a32, a16, na, c->st);
+      f32_to_bf16(b32, b16, nb, c->st);
+    }
+    const int64_t lda = a_major == K_MAJOR ? K : M, ldb = b_major == K_MAJOR ? K : N;
+    const void* Ap = tc(c) ? (const void*)a16 : (const void*)a32;
+    const void* Bp = tc(c) ? (const void*)b16 : (const void*)b32;
+    if (tgt && tc(c)) {
+      const int nt = tc_n_tiles(N);
+      float2* part = dalloc<float2>((int64_t)nt * M);
+      float* tl = dalloc<float>(M);
+      uint32_t* tg = dalloc<uint32_t>(M);
+      bf16* S = dalloc<bf16>((int64_t)M * N);
+      double* lse = dalloc<double>(M);
+      DL_CUDA(cudaMemcpyAsync(tg, tgt, M * 4, cudaMemcpyHostToDevice, c->st));
+      GemmDesc g = desc(M, N, K, a_major, Ap, lda, b_major, Bp, ldb, nullptr, 0);
+      g.logits = 1;
+      g.S = S;
+      g.lds = N;
+      g.part = part;
+      g.tgt = tg;
+      g.tgt_logit = tl;
+      gemm(c, g);
+      // logp = s_y - lse per row via the softmax-rows kernel (grads off)
+      softmax_rows_bf16(nullptr, M, N, part, nt, tl, tg, nullptr, 1.0, 0, nullptr, lse, c->st);
+      std::vector<double> lp(M);
+      std::vector<float> t(M);
+      DL_CUDA(cudaMemcpyAsync(lp.data(), lse, M * 8, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaMemcpyAsync(t.data(), tl, M * 4, cudaMemcpyDeviceToHost, c->st));
+      std::vector<uint16_t> sb((size_t)M * N);
+      DL_CUDA(cudaMemcpyAsync(sb.data(), S, (size_t)M * N * 2, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      // Cout: [M x N] bf16 logits widened, then M logp, then M target logits
+      for (int64_t i = 0; i < (int64_t)M * N; ++i) {
+        uint32_t u = (uint32_t)sb[i] << 16;
+        std::memcpy(&Cout[i], &u, 4);
+      }
+      for (int i = 0; i < M; ++i) {
+        Cout[(int64_t)M * N + i] = (float)lp[i];
+        Cout[(int64_t)M * N + M + i] = t[i];
+      }
+      cudaFree(part); cudaFree(tl); cudaFree(tg); cudaFree(S); cudaFree(lse);
+    } else {
+      const int s = tc(c) ? tc_splits(K, std::max(1, splits)) : std::max(1, splits);
+      float* out = dalloc<float>((int64_t)s * M * N);
+      float* red = dalloc<float>((int64_t)M * N);
+      GemmDesc g = desc(M, N, K, a_major, Ap, lda, b_major, Bp, ldb, out, N);
+      g.k_splits = s;
+      g.split_stride = (int64_t)M * N;
+      gemm(c, g);
+      reduce_splits(out, s, (int64_t)M * N, (int64_t)M * N, red, 0.f, 0, nullptr, c->st);
+      DL_CUDA(cudaMemcpyAsync(Cout, red, (size_t)M * N * 4, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      cudaFree(out);
+      cudaFree(red);
+    }
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    cudaFree(a32); cudaFree(b32);
+    if (a16) cudaFree(a16);
+    if (b16) cudaFree(b16);
+  });
+}
+
+uint64_t dl_launch_count(const dl_ctx* c) { return c ? c->launches.load() : 0; }
+
+int dl_set_profiling(dl_ctx* c, int on) {
+  if (!c) return fail(c, DL_EINVAL, "null ctx");
+  c->profiling = on != 0;
+  c->prof.clear();
+  return DL_OK;
+}
+
+double dl_kernel_ms(const dl_ctx* c, const char* name) {
+  if (!c || !name) return -1.0;
+  auto it = c->prof.find(name);
+  if (it == c->prof.end() || it->second.second == 0) return -1.0;
+  return it->second.first / (double)it->second.second;
+}
+
+}  // extern "C"

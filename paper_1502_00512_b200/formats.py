@@ -1,0 +1,210 @@
+"""Byte-exact desklm file formats (little-endian), written fresh from the
+reference's documented layouts:
+
+* RNLM model     -- rnn.hpp:263-308   (W_out stored H x V, transposed from memory)
+* ROPT optimiser -- rmsprop.hpp:137-170 (40-byte header + m_rec, m_in, m_out)
+* RTRN trainer   -- trainer.hpp:274-341 + config echo :412-457
+* LE primitives  -- util.hpp:84-162
+"""
+from __future__ import annotations
+
+import io
+import struct
+
+import numpy as np
+
+from ._lib import DataError
+
+RNN_FORMAT_VERSION = 1
+RMSPROP_FORMAT_VERSION = 1
+TRAINER_FORMAT_VERSION = 1
+RMSPROP_HEADER_BYTES = 4 + 4 + 8 + 8 + 8 + 8
+
+
+# ------------------------------------------------------------ primitives
+class Reader:
+    def __init__(self, data: bytes):
+        self.b = memoryview(data)
+        self.i = 0
+
+    def take(self, n: int) -> bytes:
+        if self.i + n > len(self.b):
+            raise DataError("unexpected end of file")
+        out = bytes(self.b[self.i:self.i + n])
+        self.i += n
+        return out
+
+    def u8(self): return self.take(1)[0]
+    def u32(self): return struct.unpack("<I", self.take(4))[0]
+    def u64(self): return struct.unpack("<Q", self.take(8))[0]
+    def f64(self): return struct.unpack("<d", self.take(8))[0]
+
+    def f32s(self, n: int) -> np.ndarray:
+        return np.frombuffer(self.take(4 * n), dtype="<f4").astype(np.float32)
+
+    def string(self) -> str:
+        n = self.u64()
+        return self.take(n).decode("utf-8", errors="surrogateescape")
+
+    def magic(self, m: str, what: str):
+        if self.i + 4 > len(self.b) or bytes(self.b[self.i:self.i + 4]) != m.encode():
+            raise DataError(f"bad magic, not a {what} file")
+        self.i += 4
+
+
+def _u8(v): return struct.pack("<B", v)
+def _u32(v): return struct.pack("<I", v)
+def _u64(v): return struct.pack("<Q", v)
+def _f64(v): return struct.pack("<d", v)
+
+
+def _str(s: str) -> bytes:
+    b = s.encode("utf-8", errors="surrogateescape")
+    return _u64(len(b)) + b
+
+
+# ------------------------------------------------------------------ RNLM
+def write_params(params, vocab_words, act: int = 0) -> bytes:
+    """rnn.hpp:263-285."""
+    w_in, w_rec, w_out = params
+    V, H = w_in.shape
+    out = io.BytesIO()
+    out.write(b"RNLM" + _u32(RNN_FORMAT_VERSION) + _u64(V) + _u64(H) + _u8(act))
+    out.write(np.ascontiguousarray(w_in, "<f4").tobytes())
+    out.write(np.ascontiguousarray(w_rec, "<f4").tobytes())
+    out.write(np.ascontiguousarray(np.asarray(w_out).T, "<f4").tobytes())  # H x V on disk
+    out.write(_u64(len(vocab_words)))
+    for w in vocab_words:
+        out.write(_str(w))
+    return out.getvalue()
+
+
+def read_params(data_or_reader):
+    """rnn.hpp:287-308 -> ((w_in, w_rec, w_out), act, vocab_words)."""
+    r = data_or_reader if isinstance(data_or_reader, Reader) else Reader(data_or_reader)
+    r.magic("RNLM", "rnn checkpoint")
+    ver = r.u32()
+    if ver != RNN_FORMAT_VERSION:
+        raise DataError(f"rnn checkpoint: unsupported version {ver}")
+    V, H = r.u64(), r.u64()
+    if V < 1 or H < 1 or V > (1 << 26) or H > (1 << 20):
+        raise DataError("rnn checkpoint: implausible dimensions")
+    act = r.u8()
+    w_in = r.f32s(V * H).reshape(V, H)
+    w_rec = r.f32s(H * H).reshape(H, H)
+    w_out = np.ascontiguousarray(r.f32s(H * V).reshape(H, V).T)
+    n = r.u64()
+    if n != V:
+        raise DataError("rnn checkpoint: vocabulary size mismatch")
+    words = [r.string() for _ in range(n)]
+    return (w_in, w_rec, w_out), act, words
+
+
+# ------------------------------------------------------------------ ROPT
+def write_rmsprop(V, H, rho, eps, state) -> bytes:
+    """rmsprop.hpp:139-149."""
+    m_rec, m_in, m_out = state
+    return (b"ROPT" + _u32(RMSPROP_FORMAT_VERSION) + _u64(V) + _u64(H) + _f64(rho) +
+            _f64(eps) + np.ascontiguousarray(m_rec, "<f4").tobytes() +
+            np.ascontiguousarray(m_in, "<f4").tobytes() +
+            np.ascontiguousarray(m_out, "<f4").tobytes())
+
+
+def read_rmsprop(data_or_reader):
+    """rmsprop.hpp:151-166 -> (V, H, rho, eps, (m_rec, m_in, m_out))."""
+    r = data_or_reader if isinstance(data_or_reader, Reader) else Reader(data_or_reader)
+    r.magic("ROPT", "rmsprop state")
+    ver = r.u32()
+    if ver != RMSPROP_FORMAT_VERSION:
+        raise DataError(f"rmsprop state: unsupported version {ver}")
+    V, H = r.u64(), r.u64()
+    rho, eps = r.f64(), r.f64()
+    if not (0.0 < rho < 1.0):
+        raise ValueError("rmsprop: rho must be in (0,1)")
+    if not eps > 0.0:
+        raise ValueError("rmsprop: eps must be > 0")
+    m_rec = r.f32s(H * H).reshape(H, H)
+    m_in = r.f32s(V)
+    m_out = r.f32s(V)
+    return V, H, rho, eps, (m_rec, m_in, m_out)
+
+
+# ---------------------------------------------------------- mt19937_64 text
+def mt19937_64_text(seed: int) -> str:
+    """`os << std::mt19937_64(seed)` as libstdc++ prints it: the 312 state
+    words then the position index (312 right after seeding)."""
+    M = (1 << 64) - 1
+    x = [seed & M]
+    for i in range(1, 312):
+        x.append((6364136223846793005 * (x[-1] ^ (x[-1] >> 62)) + i) & M)
+    return " ".join(str(v) for v in x) + " 312"
+
+
+# ------------------------------------------------------------------ RTRN
+CONFIG_ECHO = (  # trainer.hpp:412-432 (name, kind)
+    ("nstate", "u64"), ("nproj", "u64"), ("noffset", "u32"), ("minibatch", "u32"),
+    ("unroll", "u32"), ("eta", "f64"), ("rho", "f64"), ("eps", "f64"), ("clip", "f64"),
+    ("mode", "u8"), ("nce_k", "u32"), ("noise_floor", "f64"), ("max_epochs", "u32"),
+    ("seed", "u64"), ("act", "u8"), ("divergence_factor", "f64"), ("valid_limit", "u64"),
+    ("valid_shards", "u32"), ("init_range", "f64"),
+)
+
+
+def write_config_echo(cfg) -> bytes:
+    pk = {"u64": _u64, "u32": _u32, "u8": _u8, "f64": _f64}
+    return b"".join(pk[k](getattr(cfg, n) if k == "f64" else int(getattr(cfg, n)))
+                    for n, k in CONFIG_ECHO)
+
+
+def check_config_echo(r: Reader, cfg):
+    rd = {"u64": r.u64, "u32": r.u32, "u8": r.u8, "f64": r.f64}
+    ok = True
+    for n, k in CONFIG_ECHO:
+        v = rd[k]()
+        if n == "max_epochs":  # only a stopping rule; a resumed run may raise it
+            continue
+        want = getattr(cfg, n)
+        ok = ok and (v == (want if k == "f64" else int(want)))
+    if not ok:
+        raise DataError("trainer checkpoint: configuration does not match this run")
+
+
+def write_trainer(cfg, epoch, eta, best, bad, initial, rng_text, cursors, hidden, params,
+                  vocab_words, opt_state) -> bytes:
+    """trainer.hpp:274-292."""
+    V, H = params[0].shape
+    out = io.BytesIO()
+    out.write(b"RTRN" + _u32(TRAINER_FORMAT_VERSION) + write_config_echo(cfg))
+    out.write(_u32(epoch) + _f64(eta) + _f64(best) + _u32(bad) + _f64(initial))
+    out.write(_str(rng_text))
+    out.write(_u64(len(cursors)))
+    out.write(np.ascontiguousarray(cursors, "<u8").tobytes())
+    out.write(np.ascontiguousarray(hidden, "<f4").tobytes())
+    out.write(write_params(params, vocab_words, cfg.act))
+    out.write(write_rmsprop(V, H, cfg.rho, cfg.eps, opt_state))
+    out.write(b"TEND")
+    return out.getvalue()
+
+
+def read_trainer(data: bytes, cfg, n_streams: int, hidden_size: int, L: int):
+    """trainer.hpp:300-336; returns a dict of the restored state."""
+    r = Reader(data)
+    r.magic("RTRN", "trainer checkpoint")
+    ver = r.u32()
+    if ver != TRAINER_FORMAT_VERSION:
+        raise DataError(f"trainer checkpoint: unsupported version {ver}")
+    check_config_echo(r, cfg)
+    st = dict(epoch=r.u32(), eta=r.f64(), best=r.f64(), bad=r.u32(), initial=r.f64())
+    st["rng_text"] = r.string()
+    n = r.u64()
+    if n != n_streams:
+        raise DataError("trainer checkpoint: cursor count mismatch")
+    cur = np.frombuffer(r.take(8 * n), dtype="<u8").astype(np.int64)
+    if np.any(cur < 0) or np.any(cur >= L):
+        raise DataError("trainer checkpoint: cursor out of range")
+    st["cursors"] = cur
+    st["hidden"] = r.f32s(n * hidden_size).reshape(n, hidden_size)
+    st["params"], st["act"], st["vocab"] = read_params(r)
+    _, _, _, _, st["opt"] = read_rmsprop(r)
+    r.magic("TEND", "trainer checkpoint trailer")
+    return st
