@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""RNNLM training throughput (words/sec, device-timed) on B200.
+
+Default workload (BASELINE.json configs[2], the north-star target shape):
+  C3 -- V = 64,000, H = 2,048, BPTT T = 16, B = 128 streams per GPU,
+        noffset = 8, exact softmax, rmsprop, bf16 tensor cores (fp32
+        masters); data-parallel over N GPUs with global minibatch 128*N.
+A "step" is one truncated-BPTT window of the offset-stream schedule
+(window build + forward + softmax + backward + rmsprop + hidden carry),
+B*T words per GPU, exactly what Trainer::run_epoch does per window
+(trainer.hpp:374-406).  Words include bos-target positions, as the
+reference's tokens_per_sec does (trainer.hpp:250, :409).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c1|c2|c3|c5]
+  python bench.py --impl reference ...   # the reference CPU trainer
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = {"hbm_gbs": 6533.2, "bf16_tflops": 1679.5, "bf16_tflops_sustained": 1414.1}
+try:
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        PEAKS.update(json.load(f))
+except Exception:
+    pass
+
+CONFIGS = {
+    # name: V, H, T, B(per GPU), noffset, L, data seed
+    "c1": dict(V=10000, H=128, T=8, B=8, noffset=128, L=1_000_000, seed=1001,
+               desc="RNNLM hidden=128, vocab=10K, BPTT=8, 1M-token stream"),
+    "c2": dict(V=64000, H=1024, T=16, B=128, noffset=8, L=1 << 24, seed=2001,
+               desc="RNNLM hidden=1024, vocab=64K full softmax, 128 streams"),
+    "c3": dict(V=64000, H=2048, T=16, B=128, noffset=8, L=1 << 25, seed=3001,
+               desc="RNNLM hidden=2048, vocab=64K, 128 streams/GPU, data-parallel"),
+}
+
+
+def synthetic_stream(seed: int, V: int, L: int) -> np.ndarray:
+    """Sentences <s> w.. </s> of 1..12 words, ids 3 + min(u1, u2) over [3, V)
+    -- the shape of the reference's random_stream fixture
+    (tests/oracles/helpers.hpp:36-52), generated vectorised."""
+    rng = np.random.default_rng(seed)
+    out = np.empty(L + 64, np.uint32)
+    n = 0
+    while n < L:
+        k = 65536
+        lens = rng.integers(1, 13, k)
+        tot = int(lens.sum()) + 2 * k
+        body = np.minimum(rng.integers(0, V - 3, tot), rng.integers(0, V - 3, tot)) + 3
+        ends = np.cumsum(lens + 2)
+        starts = ends - lens - 2
+        body[starts] = 1
+        body[ends - 1] = 2
+        take = min(tot, L + 64 - n)
+        out[n:n + take] = body[:take]
+        n += take
+    return out[:L]
+
+
+def flops_per_word(V, H):
+    """6*H*V + 6*H^2: forward logits + recurrence, dS.W_out + dW_out, the
+    recurrent backward and dW_rec."""
+    return 6 * H * V + 6 * H * H
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def run_reference(args, cfg):
+    """The reference's own CPU trainer (oracle/_ref = the unmodified
+    /root/reference headers compiled here) on a bounded sample of the same
+    workload: one window of B_s streams x T steps at full V and H
+    (bptt_run + rmsprop_update), all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cores = os.cpu_count() or 1
+    try:
+        ref = oracle.Ref()
+        kind = "reference"
+    except FileNotFoundError:
+        ref = oracle.Orc()
+        kind = "port"
+    V, H, T = cfg["V"], cfg["H"], cfg["T"]
+    Bs = min(cfg["B"], args.ref_streams)
+    Ts = min(T, args.ref_unroll)
+    ids = synthetic_stream(cfg["seed"], V, 1 << 16)
+    rng = np.random.default_rng(1)
+    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32) for s in ((V, H), (H, H), (V, H)))
+    state = (np.zeros((H, H), np.float32), np.zeros(V, np.float32), np.zeros(V, np.float32))
+    h0 = np.full((Bs, H), 0.5, np.float32)
+    times = []
+    for i in range(args.warmup + args.steps):
+        s0 = i * Bs * Ts
+        x = ids[s0:s0 + Ts * Bs].reshape(Ts, Bs)
+        y = ids[s0 + 1:s0 + 1 + Ts * Bs].reshape(Ts, Bs)
+        w = (y != 1).astype(np.uint8)
+        t0 = time.perf_counter()
+        g = ref.bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0, True, cores)
+        params, state, _ = ref.rmsprop(params, state, g, 0.9995, 1e-6, 0.05)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+        if sum(times) > args.ref_budget_s and len(times) >= 1:
+            break
+    words = Bs * Ts
+    value = words * len(times) / sum(times)
+    sample = (f"window-sampled: {len(times)} window(s) of B={Bs} streams x T={Ts} at "
+              f"V={V}, H={H} (bptt_run + rmsprop_update, softmax), threads={cores}")
+    out = {"metric": "training words/sec", "value": value, "unit": "words/s",
+           "impl": "reference", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+           "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
+           "data": "synthetic", "config": {"workload": cfg["name"], "desc": cfg["desc"],
+                                            "V": V, "H": H, "T": T, "B_per_gpu": cfg["B"]},
+           "cpu_baseline": {"value": value, "unit": "words/s", "cores": cores, "kind": kind,
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-streams", type=int, default=8)
+    ap.add_argument("--ref-unroll", type=int, default=4)
+    ap.add_argument("--ref-budget-s", type=float, default=25.0)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1502_00512_b200 as dl
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    V, H, T, B, noffset = cfg["V"], cfg["H"], cfg["T"], cfg["B"], cfg["noffset"]
+    L = cfg["L"]
+    ids = synthetic_stream(cfg["seed"], V, L)
+    rng = np.random.default_rng(7)  # random-init weights, init_uniform range 0.1
+    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                   for s in ((V, H), (H, H), (V, H)))
+    model = dl.GpuRnn(V, H, 0, args.precision, local)
+    if world > 1:
+        uid = [dl.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        model.comm_init(uid[0], world, rank)
+    model.set_params(*params)
+    model.set_opt(None, None, None, 0.9995, 1e-6)
+    model.trainer_init(ids, noffset, B, T, 1.0)
+    eta = 1e-3
+    stream = torch.cuda.ExternalStream(dl._lib.load().dl_cuda_stream(model.handle))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also captures the per-window CUDA graph)
+    model.trainer_run(0, args.warmup, eta)
+    torch.cuda.synchronize()
+    launches0 = model.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        loss_sum, skipped = model.trainer_run(args.warmup, args.steps, eta)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = model.launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    words = world * B * T * args.steps
+    value = words / (ms / 1000.0)
+    fpw = flops_per_word(V, H)
+
+    # per-kernel device times (eager launches + CUDA events on the library
+    # stream) -> roofline of the dominant kernel
+    model.set_profiling(True)
+    model.trainer_run(args.warmup + args.steps, args.profile_steps, eta)
+    phases = {}
+    for name in ("recurrence_fwd", "logits", "softmax", "dh", "dw_out", "recurrence_bwd",
+                 "dw_rec", "embed_grad", "rmsprop"):
+        v = model.kernel_ms(name)
+        if v >= 0:
+            phases[name] = v
+    model.set_profiling(False)
+    TB = T * B
+    gemm_flops = {"logits": 2.0 * TB * V * H, "dh": 2.0 * TB * V * H, "dw_out": 2.0 * TB * V * H}
+    dom = max(gemm_flops, key=lambda k: phases.get(k, 0.0))
+    dom_ms = phases.get(dom, float("nan"))
+    achieved = gemm_flops[dom] / (dom_ms / 1000.0) / 1e12
+    peak = PEAKS["bf16_tflops_sustained"]
+    step_ms = ms / args.steps
+    roofline = {"bound": "tensor", "kernel": f"tc_gemm[{dom}]", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_kind": "measured sustained (MEASURED_PEAKS.json bf16_tflops_sustained)",
+                "algorithmic_flops_per_launch": gemm_flops[dom],
+                "step_frac_of_peak": value / world * fpw / 1e12 / peak,
+                "phase_ms": phases}
+
+    # end-to-end through the public API with host buffers: dl_window (H2D of
+    # the window ids/targets/mask/h0 from host, D2H of loss + h_final) then
+    # dl_rmsprop, per step
+    e2e = None
+    if args.e2e_steps > 0:
+        wins = []
+        for i in range(args.e2e_steps + 1):
+            s0 = (i * TB * 7) % (L - TB - 2)
+            x = ids[s0:s0 + TB].reshape(T, B)
+            y = ids[s0 + 1:s0 + 1 + TB].reshape(T, B)
+            wins.append(dl.WindowBatch(x, y, (y != 1).astype(np.uint8)))
+        h0 = np.full((B, H), 0.5, np.float32)
+        dl.bptt_run(model, wins[0], h0, 1.0 / TB, 1.0)
+        dl.rmsprop_update(model, eta)
+        barrier()
+        t0 = time.perf_counter()
+        for wb in wins[1:]:
+            res, h0 = dl.bptt_run(model, wb, h0, 1.0 / TB, 1.0)
+            dl.rmsprop_update(model, eta)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * TB * args.e2e_steps / dt, "unit": "words/s",
+               "h2d_bytes_per_step": TB * 9 + B * H * 4, "d2h_bytes_per_step": B * H * 4 + 8 + 8 + 4,
+               "api": "dl_window + dl_rmsprop (host arrays)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                                "--config", args.config, "--steps", "1", "--warmup", "0"],
+                               capture_output=True, text=True, timeout=600)
+            line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+            cpu = json.loads(line)["cpu_baseline"]
+        except Exception as ex:  # report, never fake
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        out = {"metric": "training words/sec", "value": value, "unit": "words/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+               "config": {"workload": args.config, "desc": cfg["desc"], "V": V, "H": H,
+                          "T": T, "B_per_gpu": B, "global_minibatch": B * world,
+                          "noffset": noffset, "L": L, "loss": "exact softmax",
+                          "optimizer": "rmsprop (per-word W_in/W_out scalars)",
+                          "parallelism": f"dp{world}",
+                          "l2": "inputs larger than L2 (W_out bf16 262 MB + fp32 master 524 MB "
+                                "streamed every window)"},
+               "flops_per_word": fpw, "mean_window_loss": loss_sum / args.steps,
+               "skipped_updates": skipped, "gpu_launches": launches,
+               "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
+               "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

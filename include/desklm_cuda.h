@@ -157,8 +157,11 @@ int dl_test_gemm(dl_ctx* ctx, int M, int N, int K, int a_major, int b_major,
                  const float* A, const float* B, float* Cout, int splits,
                  const uint32_t* tgt);
 
-/* Kernel launches issued on the context's streams since creation. */
+/* Kernel launches issued on the context's streams since creation (graph
+ * replays count every kernel node). */
 uint64_t dl_launch_count(const dl_ctx* ctx);
+/* The context's cudaStream_t (as void*), for CUDA-event timing by callers. */
+void* dl_cuda_stream(const dl_ctx* ctx);
 /* Average device time (ms) of the named kernel class over the last
  * dl_trainer_run / dl_window when profiling is on ("logits", "dh", "dw_out",
  * "recurrence", "rmsprop", ...); returns -1 if unknown. */

@@ -343,7 +343,7 @@ class Ref(_Backend):
         tr = np.ascontiguousarray(train_ids, np.uint32)
         va = np.ascontiguousarray(valid_ids, np.uint32)
         N = cfg.noffset * cfg.minibatch
-        cap = 4096 + 8 * N + 4 * N * H + 8 * (2 * V * H + H * H) + 64 * V + 8 * V
+        cap = 16384 + 8 * N + 4 * N * H + 8 * (2 * V * H + H * H) + 64 * V + 8 * V
         buf = np.zeros(cap, np.uint8)
         ln = C.c_uint64()
         logs = np.zeros((max(cfg.max_epochs, 1), 7), np.float64)

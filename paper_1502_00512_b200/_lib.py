@@ -18,7 +18,7 @@ EXPORTS = (
     "dl_rmsprop", "dl_score", "dl_sharded_perplexity", "dl_rnn_perplexity",
     "dl_trainer_init", "dl_trainer_run", "dl_trainer_get_state",
     "dl_trainer_set_state", "dl_comm_unique_id", "dl_comm_init",
-    "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm",
+    "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -76,6 +76,7 @@ def load():
         "dl_test_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
                                    vp, C.c_int, vp]),
         "dl_launch_count": (u64, [vp]),
+        "dl_cuda_stream": (vp, [vp]),
         "dl_set_profiling": (C.c_int, [vp, C.c_int]),
         "dl_kernel_ms": (C.c_double, [vp, C.c_char_p]),
     }

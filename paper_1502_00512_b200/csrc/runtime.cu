@@ -102,6 +102,7 @@ struct dl_ctx {
   int64_t* win_counter = nullptr;
   cudaGraphExec_t graph = nullptr;
   double graph_eta = NAN;
+  uint64_t graph_launches = 0;
   bool use_graph = true;
 
   // DP
@@ -929,8 +930,8 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     if (graphs) {
       if (!c->graph || c->graph_eta != eta) {
         if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
-        // warm-up launch outside capture (lazy attribute setup, workspaces)
         cudaGraph_t gph;
+        const uint64_t before = c->launches.load();
         DL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
         try {
           trainer_window(c, eta);
@@ -942,8 +943,13 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
         DL_CUDA(cudaGraphInstantiate(&c->graph, gph, 0));
         cudaGraphDestroy(gph);
         c->graph_eta = eta;
+        c->graph_launches = c->launches.load() - before;
+        c->launches -= c->graph_launches;  // counted when replayed
       }
-      for (int64_t i = 0; i < count; ++i) DL_CUDA(cudaGraphLaunch(c->graph, c->st));
+      for (int64_t i = 0; i < count; ++i) {
+        DL_CUDA(cudaGraphLaunch(c->graph, c->st));
+        c->launches += c->graph_launches;
+      }
     } else {
       for (int64_t i = 0; i < count; ++i) trainer_window(c, eta);
     }
@@ -1059,6 +1065,8 @@ int dl_test_gemm(dl_ctx* c, int M, int N, int K, int a_major, int b_major, const
 }
 
 uint64_t dl_launch_count(const dl_ctx* c) { return c ? c->launches.load() : 0; }
+
+void* dl_cuda_stream(const dl_ctx* c) { return c ? static_cast<void*>(c->st) : nullptr; }
 
 int dl_set_profiling(dl_ctx* c, int on) {
   if (!c) return fail(c, DL_EINVAL, "null ctx");

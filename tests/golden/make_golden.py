@@ -1,0 +1,82 @@
+"""Generates tests/golden/*.npz from the reference itself (oracle/_ref, the
+unmodified /root/reference headers compiled behind oracle/ref_shim.cpp).
+
+Run here (where /root/reference exists):  python tests/golden/make_golden.py
+The fixtures pin the C oracle (tests/test_oracle.py) on machines without the
+reference, e.g. the GPU box.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import oracle  # noqa: E402
+
+
+def window_case(ref, V, H, T, B, act, mask, clip, seed):
+    rng = np.random.default_rng(seed)
+    params = ref.init_uniform(V, H, seed + 1)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(0, V - 1, (T, B)).astype(np.uint32)
+    y[y >= 1] += 1
+    w = (rng.random((T, B)) >= mask).astype(np.uint8)
+    h0 = rng.uniform(-0.5, 0.5, (B, H)).astype(np.float32)
+    r = ref.bptt(params, act, x, y, w, h0, 1.0 / (T * B), clip)
+    state = (rng.uniform(0, 0.01, (H, H)).astype(np.float32),
+             rng.uniform(0, 0.01, V).astype(np.float32),
+             rng.uniform(0, 0.01, V).astype(np.float32))
+    p2, s2, applied = ref.rmsprop(params, state, r, 0.9995, 1e-6, 0.05)
+    return dict(V=V, H=H, T=T, B=B, act=act, clip=clip, w_in=params[0], w_rec=params[1],
+                w_out=params[2], x=x, y=y, w=w, h0=h0, loss=r["loss"],
+                positions=r["positions"], h_final=r["h_final"], g_in_words=r["g_in_words"],
+                g_in_rows=r["g_in_rows"], g_rec=r["g_rec"], g_out=r["g_out"], m_rec=state[0],
+                m_in=state[1], m_out=state[2], u_w_in=p2[0], u_w_rec=p2[1], u_w_out=p2[2],
+                u_m_rec=s2[0], u_m_in=s2[1], u_m_out=s2[2], applied=applied)
+
+
+def main():
+    ref = oracle.Ref()
+    out = os.path.join(HERE)
+    # bptt windows: the pinned FD instance shape (test_backprop.cpp:185-231),
+    # a tanh one with active clipping, and a C1-like one
+    cases = [window_case(ref, 7, 5, 4, 2, 0, 0.15, 3.4e38, 101),
+             window_case(ref, 12, 6, 6, 3, 1, 0.0, 0.01, 139),
+             window_case(ref, 300, 32, 8, 8, 0, 0.1, 1.0, 7)]
+    for i, c in enumerate(cases):
+        np.savez_compressed(os.path.join(out, f"window_{i}.npz"), **c)
+    # scoring
+    V, H = 200, 16
+    params = ref.init_uniform(V, H, 5)
+    ids = ref.random_stream(77, V, 1500)
+    sl = ref.sharded_logprobs(params, 1, ids, 8)
+    sp = ref.sharded_ppl(params, 1, ids, 8)
+    rp = ref.rnn_ppl(params, 1, ids)
+    np.savez_compressed(os.path.join(out, "score.npz"), w_in=params[0], w_rec=params[1],
+                        w_out=params[2], ids=ids, act=1, shards=8, logprobs=sl,
+                        sharded=np.array([sp["total_logprob"], sp["predicted"], sp["perplexity"]]),
+                        rnn=np.array([rp["total_logprob"], rp["predicted"], rp["perplexity"]]))
+    # a full Trainer<StandardTraits> run (softmax, 3 epochs) and its RTRN bytes
+    V, H = 30, 8
+    tr, va = ref.random_stream_pair(77, V, 416, 120)
+    tr = tr[:400]
+    params = ref.init_uniform(V, H, 3)
+    cfg = oracle.TrainConfig(nstate=H, noffset=2, minibatch=2, unroll=5, eta=0.05,
+                             max_epochs=3, mode=1)
+    blob, logs, ini = ref.train(cfg, params, tr, va)
+    blob0, _, _ = ref.train(cfg, params, tr, va, run=False)
+    np.savez_compressed(os.path.join(out, "train.npz"), w_in=params[0], w_rec=params[1],
+                        w_out=params[2], train=tr, valid=va, logs=logs, initial=ini,
+                        rtrn=np.frombuffer(blob, np.uint8), rtrn0=np.frombuffer(blob0, np.uint8),
+                        rnlm=np.frombuffer(ref.write_params(params), np.uint8))
+    # known-answer vectors of the fixtures themselves
+    np.savez_compressed(os.path.join(out, "kat.npz"),
+                        stream_1001=ref.random_stream(1001, 10000, 200)[:200],
+                        init_11=np.concatenate([a.ravel()[:16] for a in ref.init_uniform(7, 5, 11)]))
+    print("golden fixtures written to", out)
+
+
+if __name__ == "__main__":
+    main()

@@ -79,8 +79,7 @@ def test_rescore_matches_reference(ref):
     for u in range(4):
         for h in range(5):
             n = int(rng.integers(0, 7))
-            ws = " ".join(words[int(rng.integers(3, V + 3)) % (V + 3)] if False else
-                          ("oov" if rng.random() < 0.1 else words[int(rng.integers(3, V))])
+            ws = " ".join("oov" if rng.random() < 0.1 else words[int(rng.integers(3, V))]
                           for _ in range(n))
             ac = float(rng.normal(-100, 5))
             lines.append(f"u{u}\t{ac:.3f}\t{-20.0:.3f}" + (f"\t{ws}" if n else ""))
