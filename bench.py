@@ -255,7 +255,7 @@ def main():
     model.trainer_run(args.warmup + args.steps, args.profile_steps, eta)
     phases = {}
     for name in ("recurrence_fwd", "logits", "softmax", "dh", "dw_out", "recurrence_bwd",
-                 "dw_rec", "embed_grad", "rmsprop"):
+                 "dw_rec", "embed_grad", "rmsprop", "rmsprop_out"):
         v = model.kernel_ms(name)
         if v >= 0:
             phases[name] = v

@@ -329,21 +329,22 @@ k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int n_pow2,
 }
 
 // Row sums per segment in processing order, then clip (rnn.hpp:155-162).
+// Grid-stride over slots; threads cover the H columns of one slot.
 __global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
                              const int* __restrict__ seg_start, const int* __restrict__ n_seg,
                              const int* __restrict__ order_pos, float* __restrict__ rows,
                              float clip, int* nonfinite) {
-  const int slot = blockIdx.x;
-  if (slot >= *n_seg) return;
-  const int a = seg_start[slot], e = seg_start[slot + 1];
+  const int ns = *n_seg;
   bool bad = false;
-  for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < H;
-       j += (int64_t)gridDim.y * blockDim.x) {
-    float acc = 0.f;
-    for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
-    acc = clip1(acc, clip);
-    bad |= !isfinite(acc);
-    rows[(int64_t)slot * H + j] = acc;
+  for (int slot = blockIdx.x; slot < ns; slot += gridDim.x) {
+    const int a = seg_start[slot], e = seg_start[slot + 1];
+    for (int64_t j = threadIdx.x; j < H; j += blockDim.x) {
+      float acc = 0.f;
+      for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
+      acc = clip1(acc, clip);
+      bad |= !isfinite(acc);
+      rows[(int64_t)slot * H + j] = acc;
+    }
   }
   if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
 }
@@ -451,6 +452,11 @@ __global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long lo
   if (*nonfinite) skipped[0] += 1ull;
 }
 
+// dst = src ? *src : value  (device-side flags inside graphs)
+__global__ void k_set_flag(int* dst, const int* src, int value) {
+  dst[0] = src ? src[0] : value;
+}
+
 // ----------------------------------------------------- offset streams
 // Window build for group g = window % noffset (trainer.hpp:376-389): the
 // rank's streams are s = g*Bg + rank*B + b; pos = cursor[s] + t; x =
@@ -479,30 +485,41 @@ __global__ void k_window_build(const uint32_t* __restrict__ ids, int64_t L,
 
 // After the window (trainer.hpp:396-405): hidden <- h_final, cursor += T,
 // wrap -> cursor -= L and hidden = act(0).  Advances the window counter.
-__global__ void k_window_finish(int64_t* __restrict__ cursors, float* __restrict__ hidden,
-                                const float* __restrict__ h_final, int64_t* win_counter,
-                                int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0) {
-  const int64_t g = *win_counter % noffset;
-  const int64_t s0 = g * B;
+__global__ void k_hidden_carry(const int64_t* __restrict__ cursors, float* __restrict__ hidden,
+                               const float* __restrict__ h_final,
+                               const int64_t* __restrict__ win_counter, int noffset, int64_t B,
+                               int64_t T, int64_t H, int64_t L, float a0) {
+  const int64_t s0 = (*win_counter % noffset) * B;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = tid; i < B * H; i += nthreads) {
-    const int64_t b = i / H;
-    const bool wrap = cursors[s0 + b] + T >= L;
-    hidden[s0 * H + i] = wrap ? a0 : h_final[i];
-  }
-  __syncthreads();
-  // single block updates the cursors after every thread has read them
-  if (blockIdx.x == 0) {
-    for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
-      int64_t c = cursors[s0 + b] + T;
-      if (c >= L) c -= L;
-      cursors[s0 + b] = c;
+  if ((H % 4) == 0) {
+    const float4* src = reinterpret_cast<const float4*>(h_final);
+    float4* dst = reinterpret_cast<float4*>(hidden + s0 * H);
+    for (int64_t i = tid; i < B * H / 4; i += nthreads) {
+      const bool wrap = cursors[s0 + (4 * i) / H] + T >= L;
+      dst[i] = wrap ? make_float4(a0, a0, a0, a0) : src[i];
+    }
+  } else {
+    for (int64_t i = tid; i < B * H; i += nthreads) {
+      const bool wrap = cursors[s0 + i / H] + T >= L;
+      hidden[s0 * H + i] = wrap ? a0 : h_final[i];
     }
   }
 }
 
-__global__ void k_counter_inc(int64_t* c) { c[0] += 1; }
+// Runs after k_hidden_carry (which reads the old cursors); advances the
+// window counter at the end.
+__global__ void k_cursor_advance(int64_t* __restrict__ cursors, int64_t* win_counter,
+                                 int noffset, int64_t B, int64_t T, int64_t L) {
+  const int64_t s0 = (*win_counter % noffset) * B;
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    int64_t c = cursors[s0 + b] + T;
+    if (c >= L) c -= L;
+    cursors[s0 + b] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) win_counter[0] += 1;
+}
 
 }  // namespace
 
@@ -567,7 +584,7 @@ void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int
   DL_REQUIRE(smem <= 200 * 1024, 1, "window too large for the embedding sort (T*B <= 16384)");
   k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, p2, ws.seg_start, n_rows, ws.order_pos,
                                                words);
-  dim3 grid((unsigned)n, (unsigned)((H + 255) / 256));
+  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 8);
   k_embed_rows<<<grid, 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows, clip,
                                      nonfinite);
 }
@@ -595,6 +612,9 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st) {
   k_count_skip<<<1, 1, 0, st>>>(nonfinite, skipped);
 }
+void set_flag(int* dst, const int* src, int value, cudaStream_t st) {
+  k_set_flag<<<1, 1, 0, st>>>(dst, src, value);
+}
 void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
                   const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
                   uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st) {
@@ -604,10 +624,9 @@ void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const 
 void window_finish(int64_t* cursors, float* hidden, const float* h_final, int64_t* win_counter,
                    int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0,
                    cudaStream_t st) {
-  // one block: cursors must be read by every thread before the update
-  k_window_finish<<<1, 1024, 0, st>>>(cursors, hidden, h_final, win_counter, noffset, B, T, H, L,
-                                      a0);
-  k_counter_inc<<<1, 1, 0, st>>>(win_counter);
+  k_hidden_carry<<<grid_for(B * H / 4), 256, 0, st>>>(cursors, hidden, h_final, win_counter,
+                                                       noffset, B, T, H, L, a0);
+  k_cursor_advance<<<1, 256, 0, st>>>(cursors, win_counter, noffset, B, T, L);
 }
 
 }  // namespace dl

@@ -41,6 +41,15 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st);
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st);
+
+// rec_tc.cu: one recurrence step, tcgen05 + split-K cluster/DSMEM reduction.
+// mode 0: out = act(A . W_rec^T + W_in[x]); mode 1: out = (A . W_rec +
+// dh_out) * act'(hnext).  A is [M x H] bf16, K-major.
+void rec_plan(int M, int H, int& bn, int& S);
+void rec_step_tc(int mode, int M, int H, int act, const bf16* A, const bf16* w_rec_bf,
+                 const float* w_in, const uint32_t* x, const float* dh_out, const float* hnext,
+                 float* out, bf16* outb, cudaStream_t st);
+void set_flag(int* dst, const int* src, int value, cudaStream_t st);
 void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
                   const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
                   uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st);

@@ -1,0 +1,271 @@
+// One recurrence step as a single tcgen05 kernel with a split-K cluster
+// reduction in distributed shared memory (sm_100a, bf16 operands).
+//
+// Replaces, per time step, matmul_nt(h_t, W_rec) + input_forward + activate
+// (backprop.hpp:102-112, rnn.hpp:209-216) in the forward direction and
+// matmul_nn(dpre_{t+1}, W_rec) + the dh_out add + activate_deriv
+// (backprop.hpp:204-218) in the backward direction.  The step is a small,
+// latency-bound contraction (M = B streams <= 128, N = K = H), so instead of
+// a split-K GEMM that round-trips S partial products through HBM, one
+// cluster of S CTAs owns each 128 x BN output tile:
+//   * CTA r of the cluster computes the partial product over K-slice r with
+//     tcgen05.mma into TMEM (operands staged by TMA, SWIZZLE_128B),
+//   * drains its fp32 partial to its own shared memory,
+//   * after a cluster barrier, reduces rows [r*128/S, (r+1)*128/S) across
+//     all S CTAs' shared memory (DSMEM) in fixed rank order -- deterministic --
+//     and applies the fused epilogue (W_in row gather + sigmoid/tanh, or
+//     + dh_out and * act'(h)), writing fp32 and bf16 copies.
+#include <cooperative_groups.h>
+
+#include <mutex>
+
+#include "tc_common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dl {
+namespace tc {
+
+constexpr int kRecThreads = 256;
+
+struct RecParams {
+  int M, N, K;          // rows (streams), H, H
+  int S, kbs;           // cluster size (K splits), k-blocks per split
+  int mode;             // 0 forward, 1 backward
+  int act;
+  const float* w_in;    // fwd: embedding rows
+  const uint32_t* x;    // fwd: input ids [M]
+  const float* dh_out;  // bwd: [M x N]
+  const float* hnext;   // bwd: h_{t+1} [M x N]
+  float* out;           // h_{t+1} or dpre_t  [M x N]
+  bf16* outb;           // bf16 copy (nullable)
+};
+
+template <int BN>
+struct RecCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int NST = (160 * 1024) / STAGE > 8 ? 8 : (160 * 1024) / STAGE;
+  static constexpr int PSTRIDE = BN + 4;  // fp32 partial row pitch (bank spread)
+  static constexpr int PART_BYTES = BM * PSTRIDE * 4;
+  static constexpr int RING = NST * STAGE;
+  static constexpr int BODY = RING > PART_BYTES ? RING : PART_BYTES;
+  static constexpr int SMEM = BODY + 1024 + 256;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+};
+
+template <int BN, bool B_MN>
+__global__ void __launch_bounds__(kRecThreads, 1)
+rec_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                RecParams p) {
+  using C = RecCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BODY);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::NST + 1);
+  float* part = reinterpret_cast<float*>(smem);  // aliases the ring after the MMAs
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nt = blockIdx.y, mt = blockIdx.z;
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[C::NST + s]); };
+  const uint32_t tfull = smem_u32(&bars[2 * C::NST]);
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < C::NST; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kb0 = rank * p.kbs;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < p.kbs; ++i) {
+      const int kb = kb0 + i;
+      mbar_wait(empty(stage), phase ^ 1);
+      const uint32_t a_s = sbase + stage * C::STAGE;
+      const uint32_t b_s = a_s + C::A_BYTES;
+      mbar_expect_tx(full(stage), C::STAGE);
+      tma_load_2d(a_s, &tmA, full(stage), kb * BK, mt * BM);
+      if (!B_MN) {
+        tma_load_2d(b_s, &tmB, full(stage), kb * BK, nt * BN);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j)
+          tma_load_2d(b_s + j * 8192, &tmB, full(stage), nt * BN + 64 * j, kb * BK);
+      }
+      if (++stage == C::NST) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                               (static_cast<uint32_t>(B_MN) << 16) |
+                               (static_cast<uint32_t>(BN >> 3) << 17) |
+                               (static_cast<uint32_t>(BM >> 4) << 24);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < p.kbs; ++i) {
+      mbar_wait(full(stage), phase);
+      fence_after();
+      const uint32_t a_s = sbase + stage * C::STAGE;
+      const uint32_t b_s = a_s + C::A_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+        const uint64_t ad = make_desc(a_s + ks * 32, 16, 1024);
+        const uint64_t bd = B_MN ? make_desc(b_s + ks * 2048, 8192, 1024)
+                                 : make_desc(b_s + ks * 32, 16, 1024);
+        mma_bf16(tmem, ad, bd, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+      }
+      mma_commit(empty(stage));
+      if (++stage == C::NST) { stage = 0; phase ^= 1; }
+    }
+    mma_commit(tfull);
+  }
+  __syncwarp();
+
+  // ---- drain TMEM -> own shared memory (fp32 partial of this K slice)
+  mbar_wait(tfull, 0);
+  fence_after();
+  {
+    const int quarter = warp % 4;
+    const int half = warp / 4;  // 8 warps: two column halves per lane quarter
+    const int row = quarter * 32 + lane;
+    float* prow = part + row * C::PSTRIDE;
+#pragma unroll 1
+    for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(prow + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  }
+  fence_before();
+  cluster.sync();  // every CTA's partial is visible cluster-wide
+
+  // ---- reduce my row slice across the cluster (rank order), fused epilogue
+  const int rows = BM / p.S;
+  const int r0 = rank * rows;
+  for (int idx = threadIdx.x; idx < rows * BN; idx += kRecThreads) {
+    const int row = r0 + idx / BN, col = idx % BN;
+    const int m = mt * BM + row, n = nt * BN + col;
+    if (m >= p.M || n >= p.N) continue;
+    float acc = 0.f;
+    for (int q = 0; q < p.S; ++q) {
+      const float* peer = cluster.map_shared_rank(part, q);
+      acc += peer[row * C::PSTRIDE + col];
+    }
+    const int64_t o = static_cast<int64_t>(m) * p.N + n;
+    float y;
+    if (p.mode == 0) {
+      acc += p.w_in[static_cast<int64_t>(p.x[m]) * p.N + n];
+      y = act_f(p.act, acc);
+    } else {
+      y = (acc + p.dh_out[o]) * act_deriv_f(p.act, p.hnext[o]);
+    }
+    p.out[o] = y;
+    if (p.outb) p.outb[o] = __float2bfloat16_rn(y);
+  }
+  cluster.sync();  // peers are done reading my shared memory
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+template <int BN, bool B_MN>
+void rec_launch(const void* A, const void* Bw, RecParams p, cudaStream_t st) {
+  using Cf = RecCfg<BN>;
+  auto kern = rec_step_kernel<BN, B_MN>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  const CUtensorMap ta = make_map(A, p.M, p.K, p.K, BM);
+  const CUtensorMap tb = B_MN ? make_map(Bw, p.K, p.N, p.N, 64) : make_map(Bw, p.N, p.K, p.K, BN);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.S, (p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
+  cfg.blockDim = dim3(kRecThreads);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+}
+
+}  // namespace tc
+
+// Tile choice for a recurrence step: BN in {64,128,256} and S in {1,2,4,8}
+// K-slices (each >= one 64-wide k-block) to put ~128 CTAs on the 148 SMs.
+void rec_plan(int M, int H, int& bn, int& S) {
+  const int kb_total = (H + 63) / 64;
+  const int m_tiles = (M + 127) / 128;
+  int best = -1;
+  double best_score = 1e30;
+  const int bns[3] = {256, 128, 64};
+  for (int bi = 0; bi < 3; ++bi)
+    for (int s = 8; s >= 1; s >>= 1) {
+      const int b = bns[bi];
+      if (s > kb_total || (kb_total % s) != 0) continue;
+      if (b > 64 && H < b) continue;
+      const int ctas = m_tiles * ((H + b - 1) / b) * s;
+      if (ctas > 148) continue;
+      // prefer ~128 CTAs, then fewer K slices (less DSMEM traffic)
+      const double score = std::abs(128 - ctas) + 0.5 * s;
+      if (score < best_score) { best_score = score; best = bi * 16 + s; }
+    }
+  if (best < 0) { bn = 64; S = 1; return; }
+  bn = bns[best / 16];
+  S = best % 16;
+}
+
+void rec_step_tc(int mode, int M, int H, int act, const bf16* A, const bf16* w_rec_bf,
+                 const float* w_in, const uint32_t* x, const float* dh_out, const float* hnext,
+                 float* out, bf16* outb, cudaStream_t st) {
+  int bn, S;
+  rec_plan(M, H, bn, S);
+  tc::RecParams p{};
+  p.M = M; p.N = H; p.K = H;
+  p.S = S;
+  p.kbs = ((H + 63) / 64) / S;
+  p.mode = mode;
+  p.act = act;
+  p.w_in = w_in; p.x = x; p.dh_out = dh_out; p.hnext = hnext;
+  p.out = out; p.outb = outb;
+  const bool bmn = mode == 1;  // backward contracts over the first index of W_rec
+#define DL_REC_CASE(BN_)                                           \
+  if (bn == BN_) {                                                 \
+    if (bmn) tc::rec_launch<BN_, true>(A, w_rec_bf, p, st);        \
+    else tc::rec_launch<BN_, false>(A, w_rec_bf, p, st);           \
+    return;                                                        \
+  }
+  DL_REC_CASE(256)
+  DL_REC_CASE(128)
+  DL_REC_CASE(64)
+#undef DL_REC_CASE
+}
+
+}  // namespace dl

@@ -1,0 +1,103 @@
+"""Tensor-core (DL_BF16) mode: bf16 operands, fp32 accumulation and fp32
+master weights.  The north star's bar for this mode is "validation
+perplexity after N steps within 1% of the reference"; per-window numbers
+are checked with bf16-scale tolerances, and the cluster recurrence kernel
+(rec_tc.cu) is cross-checked against the split-K GEMM path."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def cos(a, b):
+    a, b = np.ravel(a).astype(np.float64), np.ravel(b).astype(np.float64)
+    return float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b) + 1e-300))
+
+
+def window_inputs(rng, V, T, B):
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.1).astype(np.uint8)
+    return x, y, w
+
+
+@pytest.mark.parametrize("V,H,T,B,act", [(1000, 128, 8, 8, 0), (4096, 512, 8, 64, 1),
+                                         (8000, 1024, 4, 128, 0)])
+def test_bf16_window_close_to_oracle(orc, V, H, T, B, act):
+    import paper_1502_00512_b200 as dl
+    rng = np.random.default_rng(V + H)
+    params = orc.init_uniform(V, H, 3)
+    x, y, w = window_inputs(rng, V, T, B)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    want = orc.bptt(params, act, x, y, w, h0, 1.0 / (T * B), 1.0)
+    m = dl.GpuRnn(V, H, act, "bf16")
+    m.set_params(*params)
+    res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
+    assert res.positions == want["positions"]
+    assert res.loss == pytest.approx(want["loss"], rel=1e-2)
+    assert np.abs(hf - want["h_final"]).max() < 2e-2
+    g_in, g_rec, g_out = m.grads()
+    assert cos(g_out, want["g_out"]) > 0.995
+    assert cos(g_rec, want["g_rec"]) > 0.98
+    assert cos(g_in, want["g_in_dense"]) > 0.98
+
+
+def test_cluster_recurrence_matches_splitk_path(orc):
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 2048, 2048, 6, 128
+    rng = np.random.default_rng(11)
+    params = orc.init_uniform(V, H, 5)
+    x, y, w = window_inputs(rng, V, T, B)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    out = []
+    for flag in ("1", "0"):
+        os.environ["DL_REC_CLUSTER"] = flag
+        try:
+            m = dl.GpuRnn(V, H, 0, "bf16")
+        finally:
+            os.environ.pop("DL_REC_CLUSTER", None)
+        m.set_params(*params)
+        res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
+        out.append((res.loss, hf, m.grads()))
+        m.close()
+    (l1, h1, g1), (l2, h2, g2) = out
+    assert l1 == pytest.approx(l2, rel=1e-4)
+    assert np.abs(h1 - h2).max() < 2e-3
+    for a, b in zip(g1, g2):
+        assert cos(a, b) > 0.999
+
+
+def test_bf16_scorer_ppl_within_one_percent(orc):
+    import paper_1502_00512_b200 as dl
+    V, H = 10000, 256
+    params = orc.init_uniform(V, H, 8)
+    ids = orc.random_stream(21, V, 6000)
+    want = orc.sharded_ppl(params, 0, ids, 64)
+    m = dl.GpuRnn(V, H, 0, "bf16")
+    m.set_params(*params)
+    r = dl.sharded_perplexity(m, ids, 64)
+    assert r.predicted == want["predicted"]
+    assert r.perplexity == pytest.approx(want["perplexity"], rel=1e-2)
+
+
+def test_bf16_training_ppl_within_one_percent_of_reference(orc):
+    """PPL match: same corpus, seed and init; validation
+    perplexity after one epoch of windows within 1% of the fp32 reference
+    trainer."""
+    import paper_1502_00512_b200 as dl
+    V, H = 2000, 128
+    tr, va = orc.random_stream_pair(555, V, 24016, 4000)
+    tr = tr[:24000]
+    params = orc.init_uniform(V, H, 1)
+    kw = dict(nstate=H, noffset=16, minibatch=8, unroll=8, eta=0.05, max_epochs=1, mode=1)
+    want = orc.train(oracle.TrainConfig(**kw), params, tr, va)
+    t = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, "bf16")
+    t.train()
+    assert t.initial_ppl == pytest.approx(want["initial_ppl"], rel=1e-2)
+    assert t.logs[0].valid_ppl == pytest.approx(want["logs"][0][2], rel=1e-2)
+    cur, _ = t.model.trainer_state()
+    assert np.array_equal(cur, want["cursors"])
