@@ -338,9 +338,20 @@ __global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
   bool bad = false;
   for (int slot = blockIdx.x; slot < ns; slot += gridDim.x) {
     const int a = seg_start[slot], e = seg_start[slot + 1];
-    for (int64_t j = threadIdx.x; j < H; j += blockDim.x) {
+    for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < H;
+         j += (int64_t)gridDim.y * blockDim.x) {
+      // frequent words (bos/eos) own long segments: issue 8 independent
+      // loads per batch, then add them in the reference's order
       float acc = 0.f;
-      for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
+      for (int i = a; i < e; i += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = i + u < e ? dpre[(int64_t)order_pos[i + u] * H + j] : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i + u < e) acc += 1.0f * v[u];
+      }
       acc = clip1(acc, clip);
       bad |= !isfinite(acc);
       rows[(int64_t)slot * H + j] = acc;
@@ -584,9 +595,10 @@ void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int
   DL_REQUIRE(smem <= 200 * 1024, 1, "window too large for the embedding sort (T*B <= 16384)");
   k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, p2, ws.seg_start, n_rows, ws.order_pos,
                                                words);
-  const unsigned grid = (unsigned)std::min<int64_t>(n, 148 * 8);
-  k_embed_rows<<<grid, 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows, clip,
-                                     nonfinite);
+  const unsigned gy = (unsigned)((H + 255) / 256);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (148 * 16) / gy));
+  k_embed_rows<<<dim3(gx, gy), 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows,
+                                             clip, nonfinite);
 }
 void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,
                  int64_t H, float* dense, cudaStream_t st) {

@@ -161,27 +161,39 @@ rec_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   cluster.sync();  // every CTA's partial is visible cluster-wide
 
   // ---- reduce my row slice across the cluster (rank order), fused epilogue
+  // 16-byte DSMEM loads: each thread owns 4 consecutive columns (N % 8 == 0
+  // in bf16 mode, so a 4-column group never straddles the N edge)
   const int rows = BM / p.S;
   const int r0 = rank * rows;
-  for (int idx = threadIdx.x; idx < rows * BN; idx += kRecThreads) {
-    const int row = r0 + idx / BN, col = idx % BN;
+  constexpr int Q = BN / 4;
+  for (int idx = threadIdx.x; idx < rows * Q; idx += kRecThreads) {
+    const int row = r0 + idx / Q, col = 4 * (idx % Q);
     const int m = mt * BM + row, n = nt * BN + col;
     if (m >= p.M || n >= p.N) continue;
-    float acc = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int q = 0; q < p.S; ++q) {
       const float* peer = cluster.map_shared_rank(part, q);
-      acc += peer[row * C::PSTRIDE + col];
+      const float4 v = *reinterpret_cast<const float4*>(peer + row * C::PSTRIDE + col);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     const int64_t o = static_cast<int64_t>(m) * p.N + n;
-    float y;
+    float4 y;
     if (p.mode == 0) {
-      acc += p.w_in[static_cast<int64_t>(p.x[m]) * p.N + n];
-      y = act_f(p.act, acc);
+      const float4 e = *reinterpret_cast<const float4*>(p.w_in + static_cast<int64_t>(p.x[m]) * p.N + n);
+      y = make_float4(act_f(p.act, acc.x + e.x), act_f(p.act, acc.y + e.y),
+                      act_f(p.act, acc.z + e.z), act_f(p.act, acc.w + e.w));
     } else {
-      y = (acc + p.dh_out[o]) * act_deriv_f(p.act, p.hnext[o]);
+      const float4 d = *reinterpret_cast<const float4*>(p.dh_out + o);
+      const float4 h = *reinterpret_cast<const float4*>(p.hnext + o);
+      y = make_float4((acc.x + d.x) * act_deriv_f(p.act, h.x), (acc.y + d.y) * act_deriv_f(p.act, h.y),
+                      (acc.z + d.z) * act_deriv_f(p.act, h.z), (acc.w + d.w) * act_deriv_f(p.act, h.w));
     }
-    p.out[o] = y;
-    if (p.outb) p.outb[o] = __float2bfloat16_rn(y);
+    *reinterpret_cast<float4*>(p.out + o) = y;
+    if (p.outb) {
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.outb + o);
+      ob[0] = __floats2bfloat162_rn(y.x, y.y);
+      ob[1] = __floats2bfloat162_rn(y.z, y.w);
+    }
   }
   cluster.sync();  // peers are done reading my shared memory
   if (warp == 0) {
