@@ -343,13 +343,13 @@ __global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
       // frequent words (bos/eos) own long segments: issue 8 independent
       // loads per batch, then add them in the reference's order
       float acc = 0.f;
-      for (int i = a; i < e; i += 8) {
-        float v[8];
+      for (int i = a; i < e; i += 32) {
+        float v[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 32; ++u)
           v[u] = i + u < e ? dpre[(int64_t)order_pos[i + u] * H + j] : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 32; ++u)
           if (i + u < e) acc += 1.0f * v[u];
       }
       acc = clip1(acc, clip);
@@ -374,7 +374,7 @@ __global__ void k_embed_dense(const float* __restrict__ rows, const uint32_t* __
 __global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
                           const float* __restrict__ g, int64_t n, double rho, double eps,
                           double eta, const int* __restrict__ nonfinite) {
-  if (*nonfinite) return;
+  if (nonfinite && *nonfinite) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double gi = (double)g[i];
@@ -389,7 +389,7 @@ __global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* _
 // rmsprop.hpp:84 first loop: every W_in accumulator decays.
 __global__ void k_rms_decay(float* __restrict__ m, int64_t n, double rho,
                             const int* __restrict__ nonfinite) {
-  if (*nonfinite) return;
+  if (nonfinite && *nonfinite) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     m[i] = (float)(rho * (double)m[i]);
@@ -404,7 +404,7 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
                            const int* __restrict__ n_rows_dev, int64_t n_rows, int64_t H,
                            double rho, double eps, double eta, int dense,
                            const int* __restrict__ nonfinite) {
-  if (*nonfinite) return;
+  if (nonfinite && *nonfinite) return;
   const int64_t rows = n_rows_dev ? (int64_t)*n_rows_dev : n_rows;
   const int lane = threadIdx.x % 32;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;

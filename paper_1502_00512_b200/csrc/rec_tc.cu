@@ -17,6 +17,7 @@
 //     + dh_out and * act'(h)), writing fp32 and bf16 copies.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tc_common.cuh"
@@ -252,6 +253,15 @@ void rec_plan(int M, int H, int& bn, int& S) {
   if (best < 0) { bn = 64; S = 1; return; }
   bn = bns[best / 16];
   S = best % 16;
+  // tuning overrides (bench sweeps): DL_REC_BN, DL_REC_S
+  if (const char* e = std::getenv("DL_REC_BN")) {
+    const int v = std::atoi(e);
+    if ((v == 64 || v == 128 || v == 256) && H >= v) bn = v;
+  }
+  if (const char* e = std::getenv("DL_REC_S")) {
+    const int v = std::atoi(e);
+    if ((v == 1 || v == 2 || v == 4 || v == 8) && kb_total % v == 0) S = v;
+  }
 }
 
 void rec_step_tc(int mode, int M, int H, int act, const bf16* A, const bf16* w_rec_bf,

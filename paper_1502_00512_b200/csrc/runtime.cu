@@ -63,9 +63,8 @@ struct dl_ctx {
   uint32_t* g_in_words = nullptr;
   int* g_in_n = nullptr;
   int* nonfinite = nullptr;
-  int* out_guard = nullptr;  // deferred W_out update: 0 = apply, 1 = none
   bool have_grads = false;
-  cudaStream_t st2 = nullptr;  // side stream (deferred W_out update)
+  cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // window workspace
@@ -342,8 +341,10 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
 
 // One window with device-resident inputs (x_d, y_d, w_d, htape[0]).
 // Accumulates loss into d_loss and scored positions into d_pos.
+// fork_out_eta > 0: apply the dense W_out rmsprop with that eta on the side
+// stream as soon as dW_out is final (caller joins ev_join).
 void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool grads,
-                cudaEvent_t join_before_logits = nullptr) {
+                double fork_out_eta = 0.0) {
   const int64_t H = c->H, V = c->V, TB = T * B, BH = B * H;
   cudaStream_t st = c->st;
   if (tc(c)) {
@@ -357,9 +358,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                    c->x_d + t * B, c->htape + (t + 1) * BH,
                    tc(c) ? c->htape_bf + (t + 1) * BH : nullptr);
   }
-  // the previous window's deferred W_out update (side stream) must land
-  // before W_out is read again
-  if (join_before_logits) DL_CUDA(cudaStreamWaitEvent(st, join_before_logits, 0));
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
   output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
@@ -402,6 +400,28 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     g.clip = clip;
     g.nonfinite = c->nonfinite;
     gemm(c, g);
+  }
+  // With a finite clip bound every clipped component is finite (clip1 maps
+  // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
+  // cannot fail and the dense W_out update -- HBM-bound -- may start now on
+  // the side stream, overlapping the latency-bound backward recurrence.
+  if (fork_out_eta > 0.0) {
+    DL_CUDA(cudaEventRecord(c->ev_fork, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) {
+      a = ev_get(c);
+      b = ev_get(c);
+      DL_CUDA(cudaEventRecord(a, c->st2));
+    }
+    rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, V, H,
+             c->rho, c->eps, fork_out_eta, 1, nullptr, c->st2);
+    c->launches++;
+    if (c->profiling) {
+      DL_CUDA(cudaEventRecord(b, c->st2));
+      c->pending.push_back({"rmsprop_out", {a, b}});
+    }
+    DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
   }
   // backward recurrence (backprop.hpp:197-219)
   {
@@ -457,11 +477,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   c->have_grads = true;
 }
 
-// rmsprop_update (rmsprop.hpp:113-133).  With defer_out the dense W_out part
-// is left pending (out_guard = this window's non-finite flag) and is applied
-// by apply_deferred_out() -- in the trainer at the start of the next window,
-// concurrently with its forward recurrence, which never reads W_out.
-void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool defer_out = false) {
+// rmsprop_update (rmsprop.hpp:113-133).  skip_out: the dense W_out part was
+// already issued on the side stream by run_window (fork_out_eta).
+void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   Phase p(c, "rmsprop");
   cudaStream_t st = c->st;
   rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
@@ -469,23 +487,11 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool defer_out = false) {
   rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
-  if (defer_out) {
-    set_flag(c->out_guard, c->nonfinite, 0, st);
-  } else {
+  if (!skip_out)
     rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->V,
              c->H, c->rho, c->eps, eta, 1, c->nonfinite, st);
-  }
   count_skip(c->nonfinite, c->d_skipped, st);
-  c->launches += 5;
-}
-
-// The pending dense W_out update of the previous window (guarded by
-// out_guard: 0 = apply, 1 = nothing pending / rejected), then clear it.
-void apply_deferred_out(dl_ctx* c, double eta, cudaStream_t st) {
-  rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->V,
-           c->H, c->rho, c->eps, eta, 1, c->out_guard, st);
-  set_flag(c->out_guard, nullptr, 1, st);
-  c->launches += 2;
+  c->launches += 4;
 }
 
 float act0(int act) { return act == 0 ? 0.5f : 0.0f; }
@@ -526,8 +532,6 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    c->out_guard = dalloc<int>(1);
-    set_flag(c->out_guard, nullptr, 1, c->st);
     c->w_in = dalloc<float>(V * H);
     c->w_rec = dalloc<float>(H * H);
     c->w_out = dalloc<float>(V * H);
@@ -577,8 +581,7 @@ int dl_destroy(dl_ctx* c) {
                   c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
-                  c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
-                  c->out_guard};
+                  c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -955,32 +958,18 @@ void presize(dl_ctx* c, int64_t T, int64_t B) {
 void trainer_window(dl_ctx* c, double eta) {
   const int64_t B = c->minibatch, T = c->unroll, H = c->H;
   const double scale = 1.0 / (double)(B * c->nranks * T);
-  // fork: the previous window's dense W_out rmsprop runs on the side stream
-  // while this window builds its batch and runs the forward recurrence
-  DL_CUDA(cudaEventRecord(c->ev_fork, c->st));
-  DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-  {
-    cudaEvent_t a = nullptr, b = nullptr;
-    if (c->profiling) {
-      a = ev_get(c);
-      b = ev_get(c);
-      DL_CUDA(cudaEventRecord(a, c->st2));
-    }
-    apply_deferred_out(c, eta, c->st2);
-    if (c->profiling) {
-      DL_CUDA(cudaEventRecord(b, c->st2));
-      c->pending.push_back({"rmsprop_out", {a, b}});
-    }
-  }
-  DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
   window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
                c->x_d, c->y_d, c->w_d, c->htape, c->st);
   c->launches++;
-  run_window(c, T, B, scale, (float)c->clip, true, c->ev_join);
-  run_rmsprop(c, eta, T * B, /*defer_out=*/true);
+  // the dense W_out update overlaps the backward recurrence when it cannot
+  // be rejected (finite clip, see run_window) and no allreduce is pending
+  const bool fork = std::isfinite((float)c->clip) && c->comm == nullptr;
+  run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0);
+  run_rmsprop(c, eta, T * B, /*skip_out=*/fork);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
                 c->L, act0(c->act), c->st);
   c->launches += 2;
+  if (fork) DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
 }
 }  // namespace
 
@@ -1021,8 +1010,6 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     } else {
       for (int64_t i = 0; i < count; ++i) trainer_window(c, eta);
     }
-    // flush the last window's pending W_out update
-    apply_deferred_out(c, eta, c->st);
     double l = 0.0;
     unsigned long long sk = 0;
     DL_CUDA(cudaMemcpyAsync(&l, c->d_loss, 8, cudaMemcpyDeviceToHost, c->st));
