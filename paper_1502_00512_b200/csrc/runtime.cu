@@ -55,6 +55,10 @@ struct dl_ctx {
   // parameters (fp32 masters, bf16 shadows for the tensor-core path)
   float *w_in = nullptr, *w_rec = nullptr, *w_out = nullptr;
   bf16 *w_rec_bf = nullptr, *w_out_bf = nullptr;
+  // second W_out shadow: a forked update writes it while the dh GEMM still
+  // reads w_out_bf; swap_shadow() flips them (par tracks the flip parity)
+  bf16* w_out_bf_next = nullptr;
+  int par = 0;
   // optimiser
   float *m_rec = nullptr, *m_in = nullptr, *m_out = nullptr;
   double rho = 0.9995, eps = 1e-6;
@@ -104,6 +108,8 @@ struct dl_ctx {
   float* hidden = nullptr;     // rank-local [noffset*minibatch x H]
   int64_t* win_counter = nullptr;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};  // indexed by shadow parity
+  int graph_par0 = -1;
   double graph_eta = NAN;
   uint64_t graph_launches = 0;
   bool use_graph = true;
@@ -142,6 +148,15 @@ int guarded(dl_ctx* c, F&& f) {
   } catch (const std::exception& e) {
     return fail(c, DL_EDEVICE, e.what());
   }
+}
+
+void drop_graphs(dl_ctx* c) {
+  for (int v = 0; v < 2; ++v)
+    if (c->graphs[v]) {
+      cudaGraphExecDestroy(c->graphs[v]);
+      c->graphs[v] = nullptr;
+    }
+  c->graph = nullptr;
 }
 
 // ---------------------------------------------------------------- timing
@@ -367,6 +382,44 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
 
   DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
   const bool dp = c->comm != nullptr;
+  // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
+  {
+    Phase p(c, "dw_out");
+    GemmDesc g = tc(c) ? desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs_bf, H,
+                              c->g_out, H)
+                       : desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs, H,
+                              c->g_out, H);
+    g.raster = 1;
+    g.do_clip = dp ? 0 : 1;
+    g.clip = clip;
+    g.nonfinite = c->nonfinite;
+    gemm(c, g);
+  }
+  // With a finite clip bound every clipped component is finite (clip1 maps
+  // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
+  // cannot fail and the dense W_out update -- HBM-bound -- may start as soon
+  // as dW_out is final, on the side stream, concurrently with the
+  // tensor-bound dh GEMM below.  It writes the fp32 master and the *other*
+  // bf16 shadow, so dh keeps reading this window's W_out; the caller joins
+  // ev_join and flips the shadows (swap_shadow).
+  if (fork_out_eta > 0.0) {
+    DL_CUDA(cudaEventRecord(c->ev_fork, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) {
+      a = ev_get(c);
+      b = ev_get(c);
+      DL_CUDA(cudaEventRecord(a, c->st2));
+    }
+    rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, V, H, c->rho,
+             c->eps, fork_out_eta, 1, nullptr, c->st2);
+    c->launches++;
+    if (c->profiling) {
+      DL_CUDA(cudaEventRecord(b, c->st2));
+      c->pending.push_back({"rmsprop_out", {a, b}});
+    }
+    DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
+  }
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
   {
     Phase p(c, "dh");
@@ -387,41 +440,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     } else {
       gemm(c, g);
     }
-  }
-  // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
-  {
-    Phase p(c, "dw_out");
-    GemmDesc g = tc(c) ? desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs_bf, H,
-                              c->g_out, H)
-                       : desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs, H,
-                              c->g_out, H);
-    g.raster = 1;
-    g.do_clip = dp ? 0 : 1;
-    g.clip = clip;
-    g.nonfinite = c->nonfinite;
-    gemm(c, g);
-  }
-  // With a finite clip bound every clipped component is finite (clip1 maps
-  // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
-  // cannot fail and the dense W_out update -- HBM-bound -- may start now on
-  // the side stream, overlapping the latency-bound backward recurrence.
-  if (fork_out_eta > 0.0) {
-    DL_CUDA(cudaEventRecord(c->ev_fork, st));
-    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    cudaEvent_t a = nullptr, b = nullptr;
-    if (c->profiling) {
-      a = ev_get(c);
-      b = ev_get(c);
-      DL_CUDA(cudaEventRecord(a, c->st2));
-    }
-    rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, V, H,
-             c->rho, c->eps, fork_out_eta, 1, nullptr, c->st2);
-    c->launches++;
-    if (c->profiling) {
-      DL_CUDA(cudaEventRecord(b, c->st2));
-      c->pending.push_back({"rmsprop_out", {a, b}});
-    }
-    DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
   }
   // backward recurrence (backprop.hpp:197-219)
   {
@@ -549,6 +567,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     if (precision == DL_BF16) {
       c->w_rec_bf = dalloc<bf16>(H * H);
       c->w_out_bf = dalloc<bf16>(V * H);
+      c->w_out_bf_next = dalloc<bf16>(V * H);
     }
     DL_CUDA(cudaMemsetAsync(c->w_in, 0, V * H * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->w_rec, 0, H * H * 4, c->st));
@@ -574,9 +593,9 @@ int dl_destroy(dl_ctx* c) {
   if (!c) return DL_OK;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  if (c->graph) cudaGraphExecDestroy(c->graph);
+  drop_graphs(c);
   if (c->comm) ncclCommDestroy(c->comm);
-  void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->m_rec, c->m_in,
+  void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->w_out_bf_next, c->m_rec, c->m_in,
                   c->m_out, c->g_rec, c->g_out, c->g_in_rows, c->g_in_words, c->g_in_n,
                   c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
@@ -627,7 +646,7 @@ int dl_set_opt(dl_ctx* c, const float* m_rec, const float* m_in, const float* m_
     if (m_in) DL_CUDA(cudaMemcpyAsync(c->m_in, m_in, c->V * 4, cudaMemcpyHostToDevice, c->st));
     if (m_out) DL_CUDA(cudaMemcpyAsync(c->m_out, m_out, c->V * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
-    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+    drop_graphs(c);
   });
 }
 
@@ -914,7 +933,7 @@ int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int 
     fill_f32(c->hidden, act0(c->act), Nl * c->H, c->st);
     ensure_window(c, unroll, minibatch);
     DL_CUDA(cudaStreamSynchronize(c->st));
-    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+    drop_graphs(c);
   });
 }
 
@@ -943,6 +962,15 @@ int dl_trainer_set_state(dl_ctx* c, const int64_t* cursors, const float* hidden)
 }
 
 namespace {
+bool fork_ok(dl_ctx* c) {
+  return tc(c) && c->w_out_bf_next && std::isfinite((float)c->clip) && c->comm == nullptr;
+}
+
+void swap_shadow(dl_ctx* c) {
+  std::swap(c->w_out_bf, c->w_out_bf_next);
+  c->par ^= 1;
+}
+
 // Size the split-K workspace for a T x B window before graph capture
 // (no allocation may happen inside a capture).
 void presize(dl_ctx* c, int64_t T, int64_t B) {
@@ -961,15 +989,19 @@ void trainer_window(dl_ctx* c, double eta) {
   window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
                c->x_d, c->y_d, c->w_d, c->htape, c->st);
   c->launches++;
-  // the dense W_out update overlaps the backward recurrence when it cannot
-  // be rejected (finite clip, see run_window) and no allreduce is pending
-  const bool fork = std::isfinite((float)c->clip) && c->comm == nullptr;
+  // the dense W_out update overlaps the dh GEMM when it cannot be rejected
+  // (finite clip, see run_window), a second bf16 shadow exists and no
+  // allreduce is pending
+  const bool fork = fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0);
   run_rmsprop(c, eta, T * B, /*skip_out=*/fork);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
                 c->L, act0(c->act), c->st);
   c->launches += 2;
-  if (fork) DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+  if (fork) {
+    DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    swap_shadow(c);
+  }
 }
 }  // namespace
 
@@ -985,26 +1017,35 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     const bool graphs = c->use_graph && !c->profiling && c->comm == nullptr;
     presize(c, c->unroll, c->minibatch);
     if (graphs) {
+      // one graph per W_out-shadow parity (the forked update writes the
+      // other shadow, so consecutive windows alternate between two graphs)
+      const int nvar = fork_ok(c) ? 2 : 1;
       if (!c->graph || c->graph_eta != eta) {
-        if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
-        cudaGraph_t gph;
-        const uint64_t before = c->launches.load();
-        DL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-        try {
-          trainer_window(c, eta);
-        } catch (...) {
-          cudaStreamEndCapture(c->st, &gph);
-          throw;
+        drop_graphs(c);
+        c->graph_par0 = c->par;
+        for (int v = 0; v < nvar; ++v) {
+          cudaGraph_t gph;
+          const uint64_t before = c->launches.load();
+          DL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+          try {
+            trainer_window(c, eta);  // host side flips the shadows when forking
+          } catch (...) {
+            cudaStreamEndCapture(c->st, &gph);
+            throw;
+          }
+          DL_CUDA(cudaStreamEndCapture(c->st, &gph));
+          DL_CUDA(cudaGraphInstantiate(&c->graphs[(c->graph_par0 + v) & 1], gph, 0));
+          cudaGraphDestroy(gph);
+          c->graph_launches = c->launches.load() - before;
+          c->launches -= c->graph_launches;  // counted when replayed
         }
-        DL_CUDA(cudaStreamEndCapture(c->st, &gph));
-        DL_CUDA(cudaGraphInstantiate(&c->graph, gph, 0));
-        cudaGraphDestroy(gph);
+        if (nvar == 2 && c->par != c->graph_par0) swap_shadow(c);  // (never: 2 flips)
+        c->graph = c->graphs[c->graph_par0];
         c->graph_eta = eta;
-        c->graph_launches = c->launches.load() - before;
-        c->launches -= c->graph_launches;  // counted when replayed
       }
       for (int64_t i = 0; i < count; ++i) {
-        DL_CUDA(cudaGraphLaunch(c->graph, c->st));
+        DL_CUDA(cudaGraphLaunch(nvar == 2 ? c->graphs[c->par] : c->graph, c->st));
+        if (nvar == 2) swap_shadow(c);
         c->launches += c->graph_launches;
       }
     } else {
