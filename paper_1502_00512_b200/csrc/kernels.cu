@@ -459,6 +459,54 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
   }
 }
 
+// Dense W_out rows (rmsprop.hpp:94-107) for H = 128*NV4: one warp per row,
+// the gradient row held in registers (each lane: NV4 float4), so every load
+// of a row is issued before the first use -- enough bytes in flight to run
+// at HBM speed from only one 256-thread block per SM, which co-resides with
+// the tensor-core GEMM it overlaps.
+template <int NV4>
+__global__ void __launch_bounds__(256)
+k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                 const float* __restrict__ g, int64_t V, double rho, double eps, double eta,
+                 const int* __restrict__ nonfinite) {
+  if (nonfinite && *nonfinite) return;
+  constexpr int64_t H = 128 * NV4;
+  const int lane = threadIdx.x % 32;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp0; r < V; r += nwarps) {
+    const float4* g4 = reinterpret_cast<const float4*>(g + r * H);
+    float4* w4 = reinterpret_cast<float4*>(w + r * H);
+    float4 q[NV4], o[NV4];
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) q[k] = __ldcs(g4 + lane + 32 * k);
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) o[k] = w4[lane + 32 * k];
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k)
+      s += (double)q[k].x * (double)q[k].x + (double)q[k].y * (double)q[k].y +
+           (double)q[k].z * (double)q[k].z + (double)q[k].w * (double)q[k].w;
+    s = warp_sum_d(s);
+    const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
+    const double denom = sqrt((double)mw + eps);
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      o[k].x -= (float)(eta * (double)q[k].x / denom);
+      o[k].y -= (float)(eta * (double)q[k].y / denom);
+      o[k].z -= (float)(eta * (double)q[k].z / denom);
+      o[k].w -= (float)(eta * (double)q[k].w / denom);
+      w4[lane + 32 * k] = o[k];
+      if (wb) {
+        __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + r * H + 4 * (lane + 32 * k));
+        b2[0] = __floats2bfloat162_rn(o[k].x, o[k].y);
+        b2[1] = __floats2bfloat162_rn(o[k].z, o[k].w);
+      }
+    }
+    if (lane == 0) m[r] = mw;
+  }
+}
+
 __global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long long* skipped) {
   if (*nonfinite) skipped[0] += 1ull;
 }
@@ -615,6 +663,14 @@ void rms_decay(float* m, int64_t n, double rho, const int* nonfinite, cudaStream
 void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* words,
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st) {
+  if (dense && !words && !n_rows_dev && (H == 1024 || H == 2048)) {
+    const int blocks = 148 * 2;
+    if (H == 1024)
+      k_rms_dense_rows<8><<<blocks, 256, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
+    else
+      k_rms_dense_rows<16><<<blocks, 256, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
+    return;
+  }
   const int64_t warps = n_rows;
   int blocks = (int)std::min<int64_t>((warps * 32 + 255) / 256, 148 * 8);
   if (blocks < 1) blocks = 1;

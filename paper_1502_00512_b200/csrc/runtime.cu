@@ -546,8 +546,12 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_REQUIRE(prop.major == 10, DL_EDEVICE,
                "libdesklm_cuda is built for sm_100a (B200); device is sm_" +
                    std::to_string(prop.major * 10 + prop.minor));
-    DL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-    DL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    // main stream at the highest priority so the tensor-core GEMMs claim SMs
+    // first; the side stream (bandwidth-bound W_out update) fills in
+    int prio_lo = 0, prio_hi = 0;
+    DL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    DL_CUDA(cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_hi));
+    DL_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_lo));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->w_in = dalloc<float>(V * H);
