@@ -132,6 +132,12 @@ int dl_trainer_init(dl_ctx* ctx, const uint32_t* ids, int64_t L, int noffset,
 int dl_trainer_run(dl_ctx* ctx, int64_t first, int64_t count, double eta,
                    double* loss_sum, uint64_t* skipped);
 
+/* Host-only: this rank's initial cursors (noffset*minibatch of them,
+ * group-major) -- floor(i*L/N) of trainer.hpp:194-195 over the global
+ * stream index i = g*G*minibatch + rank*minibatch + b. */
+int dl_rank_cursors(int64_t L, int noffset, int minibatch, int nranks, int rank,
+                    int64_t* out);
+
 /* Schedule state for checkpoints (RTRN cursors + hidden, trainer.hpp:286-288).
  * Arrays cover this rank's streams (N/G of them, group-major). */
 int dl_trainer_get_state(dl_ctx* ctx, int64_t* cursors, float* hidden);
@@ -156,6 +162,14 @@ int dl_comm_init(dl_ctx* ctx, const uint8_t id[128], int nranks, int rank);
 int dl_test_gemm(dl_ctx* ctx, int M, int N, int K, int a_major, int b_major,
                  const float* A, const float* B, float* Cout, int splits,
                  const uint32_t* tgt);
+
+/* Test hook for the data-parallel W_in gradient (SparseRowGrads over the
+ * gathered window, rnn.hpp:89-127): G rank-blocked windows x_all [G][T][B]
+ * and dpre_all [G][T][B][H] -> clipped dense g_in [V x H], each word's row
+ * summed in the reference's order (t descending, global stream ascending). */
+int dl_test_embed(dl_ctx* ctx, int G, int64_t T, int64_t B,
+                  const uint32_t* x_all, const float* dpre_all, float clip,
+                  float* g_in_dense);
 
 /* Kernel launches issued on the context's streams since creation (graph
  * replays count every kernel node). */

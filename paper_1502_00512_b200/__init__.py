@@ -183,6 +183,15 @@ class GpuRnn:
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
 
 
+def rank_cursors(L: int, noffset: int, minibatch: int, nranks: int = 1, rank: int = 0):
+    """This rank's initial stream cursors (host-only C-ABI call): the
+    reference's floor(i*L/N) (trainer.hpp:194-195) over global streams
+    i = g*nranks*minibatch + rank*minibatch + b, group-major."""
+    out = np.empty(noffset * minibatch, np.int64)
+    check(load().dl_rank_cursors(L, noffset, minibatch, nranks, rank, out.ctypes.data))
+    return out
+
+
 def comm_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     check(load().dl_comm_unique_id(C.addressof(buf)))

@@ -260,21 +260,27 @@ __global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restri
 // order of position (t, b) is (T-1-t)*B + b (the backward loop runs t
 // descending, b ascending), so every word's row is summed in exactly the
 // reference's float order.  One block, bitonic sort in shared memory.
+// With G data-parallel ranks the gathered window is rank-blocked ([G][T][B])
+// and the global stream index is r*B + b, so processing order i maps to
+// t = T-1 - i/(G*B), r = (i % (G*B)) / B, b = i % B.
 constexpr int kSortThreads = 1024;
 
+__device__ __forceinline__ int64_t gathered_pos(int64_t i, int64_t T, int64_t B, int64_t G) {
+  const int64_t GB = G * B;
+  const int64_t t = T - 1 - i / GB, bg = i % GB;
+  return (bg / B) * T * B + t * B + (bg % B);
+}
+
 __global__ void __launch_bounds__(kSortThreads)
-k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int n_pow2,
+k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, int n_pow2,
              int* __restrict__ seg_start, int* __restrict__ n_seg, int* __restrict__ order_pos,
              uint32_t* __restrict__ seg_word) {
   extern __shared__ unsigned long long keys[];
   __shared__ int warp_cnt[32];
-  const int64_t n = T * B;
+  const int64_t n = G * T * B;
   for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
     unsigned long long k = ~0ull;
-    if (i < n) {
-      const int64_t t = T - 1 - i / B, b = i % B;
-      k = ((unsigned long long)x[t * B + b] << 32) | (unsigned)i;
-    }
+    if (i < n) k = ((unsigned long long)x[gathered_pos(i, T, B, G)] << 32) | (unsigned)i;
     keys[i] = k;
   }
   __syncthreads();
@@ -307,8 +313,7 @@ k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int n_pow2,
     off += __popc(bal & ((1u << l) - 1));
     if (i < n) {
       const int ord = (int)(keys[i] & 0xffffffffu);
-      const int64_t t = T - 1 - ord / B, b = ord % B;
-      order_pos[i] = (int)(t * B + b);
+      order_pos[i] = (int)gathered_pos(ord, T, B, G);
       if (head) {
         seg_start[off] = i;
         seg_word[off] = (uint32_t)(keys[i] >> 32);
@@ -511,6 +516,12 @@ __global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long lo
   if (*nonfinite) skipped[0] += 1ull;
 }
 
+__global__ void k_accum_loss(double* acc, const double* v, unsigned long long* cnt,
+                             const unsigned long long* vc) {
+  acc[0] += v[0];
+  cnt[0] += vc[0];
+}
+
 // dst = src ? *src : value  (device-side flags inside graphs)
 __global__ void k_set_flag(int* dst, const int* src, int value) {
   dst[0] = src ? src[0] : value;
@@ -627,10 +638,10 @@ void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st) {
   k_sum_rows<<<1, 1024, 0, st>>>(v, wts, n, acc, cnt);
 }
-void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int64_t H,
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st) {
-  const int64_t n = T * B;
+  const int64_t n = G * T * B;
   int p2 = 1;
   while (p2 < n) p2 <<= 1;
   const size_t smem = sizeof(unsigned long long) * p2;
@@ -641,8 +652,8 @@ void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int
     attr = true;
   }
   DL_REQUIRE(smem <= 200 * 1024, 1, "window too large for the embedding sort (T*B <= 16384)");
-  k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, p2, ws.seg_start, n_rows, ws.order_pos,
-                                               words);
+  k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, G, p2, ws.seg_start, n_rows,
+                                               ws.order_pos, words);
   const unsigned gy = (unsigned)((H + 255) / 256);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (148 * 16) / gy));
   k_embed_rows<<<dim3(gx, gy), 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows,
@@ -679,6 +690,10 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
 }
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st) {
   k_count_skip<<<1, 1, 0, st>>>(nonfinite, skipped);
+}
+void accum_loss(double* acc, const double* v, unsigned long long* cnt,
+                const unsigned long long* vc, cudaStream_t st) {
+  k_accum_loss<<<1, 1, 0, st>>>(acc, v, cnt, vc);
 }
 void set_flag(int* dst, const int* src, int value, cudaStream_t st) {
   k_set_flag<<<1, 1, 0, st>>>(dst, src, value);

@@ -29,7 +29,8 @@ void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_
                        cudaStream_t st);
 void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st);
-void embed_grads(const uint32_t* x, int64_t T, int64_t B, const float* dpre, int64_t H,
+// x / dpre: G rank-blocked windows [G][T][B] (G = 1 on one GPU)
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st);
 void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,
@@ -50,6 +51,8 @@ void rec_step_tc(int mode, int M, int H, int act, const bf16* A, const bf16* w_r
                  const float* w_in, const uint32_t* x, const float* dh_out, const float* hnext,
                  float* out, bf16* outb, cudaStream_t st);
 void set_flag(int* dst, const int* src, int value, cudaStream_t st);
+void accum_loss(double* acc, const double* v, unsigned long long* cnt,
+                const unsigned long long* vc, cudaStream_t st);
 void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
                   const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
                   uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st);

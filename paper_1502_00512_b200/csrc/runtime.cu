@@ -116,10 +116,17 @@ struct dl_ctx {
   // recurrence steps as one cluster kernel each (rec_tc.cu); DL_REC_CLUSTER=0
   // falls back to split-K GEMM + reduction kernels (both are sm_100a CUDA)
   bool rec_cluster = true;
+  // DL_FORK_OUT=1: run the dense W_out update concurrently with the dh GEMM
+  // (measured neutral on B200: both contend for L2/HBM bandwidth)
+  bool fork_out = false;
 
   // DP
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  uint32_t* x_all = nullptr;  // [G][T][B] gathered window ids
+  float* dpre_all = nullptr;  // [G][T][B][H] gathered dpre
+  double* win_loss = nullptr;  // [loss, positions(u64)] of one window
+  unsigned long long* win_pos = nullptr;
 
   // profiling
   bool profiling = false;
@@ -214,8 +221,10 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->htape); fr(c->htape_bf); fr(c->x_d); fr(c->y_d); fr(c->w_d); fr(c->S); fr(c->part);
   fr(c->tgt_logit); fr(c->loss_row); fr(c->logp_row); fr(c->dh_out); fr(c->dpre); fr(c->dpre_bf);
   fr(c->g_in_rows); fr(c->g_in_words); fr(c->ews.seg_start); fr(c->ews.order_pos); fr(c->h0_d);
+  fr(c->x_all); fr(c->dpre_all);
   c->capT = nT;
   c->capB = nB;
+  const int64_t G = c->nranks;  // W_in gradient rows cover the gathered window
   c->htape = dalloc<float>((nT + 1) * nB * H);
   c->x_d = dalloc<uint32_t>(TB);
   c->y_d = dalloc<uint32_t>(TB);
@@ -224,11 +233,15 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   c->logp_row = dalloc<double>(TB);
   c->dh_out = dalloc<float>(TB * H);
   c->dpre = dalloc<float>(TB * H);
-  c->g_in_rows = dalloc<float>(TB * H);
-  c->g_in_words = dalloc<uint32_t>(TB);
-  c->ews.seg_start = dalloc<int>(TB + 1);
-  c->ews.order_pos = dalloc<int>(TB);
+  c->g_in_rows = dalloc<float>(G * TB * H);
+  c->g_in_words = dalloc<uint32_t>(G * TB);
+  c->ews.seg_start = dalloc<int>(G * TB + 1);
+  c->ews.order_pos = dalloc<int>(G * TB);
   c->h0_d = dalloc<float>(nB * H);
+  if (G > 1) {
+    c->x_all = dalloc<uint32_t>(G * TB);
+    c->dpre_all = dalloc<float>(G * TB * H);
+  }
   if (c->precision == DL_BF16) {
     c->htape_bf = dalloc<bf16>((nT + 1) * nB * H);
     c->dpre_bf = dalloc<bf16>(TB * H);
@@ -284,6 +297,11 @@ GemmDesc desc(int M, int N, int K, int am, const void* A, int64_t lda, int bm, c
   g.k_splits = 1;
   g.split_stride = 0;
   return g;
+}
+
+void nccl_check(ncclResult_t r) {
+  if (r != ncclSuccess)
+    throw Error(DL_EDEVICE, std::string("NCCL: ") + ncclGetErrorString(r));
 }
 
 void refresh_shadows(dl_ctx* c) {
@@ -376,12 +394,22 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
   output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
-  sum_rows(c->loss_row, c->w_d, TB, c->d_loss, c->d_pos, st);
-  c->launches++;
+  const bool dp = c->comm != nullptr;
+  if (dp) {
+    // the window's loss is the sum over all ranks' streams
+    DL_CUDA(cudaMemsetAsync(c->win_loss, 0, 16, st));
+    sum_rows(c->loss_row, c->w_d, TB, c->win_loss, c->win_pos, st);
+    nccl_check(ncclAllReduce(c->win_loss, c->win_loss, 1, ncclDouble, ncclSum, c->comm, st));
+    nccl_check(ncclAllReduce(c->win_pos, c->win_pos, 1, ncclUint64, ncclSum, c->comm, st));
+    accum_loss(c->d_loss, c->win_loss, c->d_pos, c->win_pos, st);
+    c->launches += 2;
+  } else {
+    sum_rows(c->loss_row, c->w_d, TB, c->d_loss, c->d_pos, st);
+    c->launches++;
+  }
   if (!grads) return;
 
   DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
-  const bool dp = c->comm != nullptr;
   // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
   {
     Phase p(c, "dw_out");
@@ -394,6 +422,17 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     g.clip = clip;
     g.nonfinite = c->nonfinite;
     gemm(c, g);
+  }
+  if (dp) {
+    // data parallel: sum dW_out over ranks, then clip --
+    // on the communication stream, overlapping dh and the backward
+    // recurrence; joined before the update
+    DL_CUDA(cudaEventRecord(c->ev_fork, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    nccl_check(ncclAllReduce(c->g_out, c->g_out, (size_t)(V * H), ncclFloat, ncclSum, c->comm,
+                             c->st2));
+    reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
+    c->launches++;
   }
   // With a finite clip bound every clipped component is finite (clip1 maps
   // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
@@ -485,11 +524,30 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dp ? 0 : 1, c->nonfinite, st);
     c->launches++;
   }
-  // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped
-  {
+  if (dp) {
+    // dW_rec: allreduce + clip.  W_in: allgather every rank's (ids, dpre) so
+    // all ranks run the identical segmented sum over the global window in
+    // the reference's order (t descending, global stream ascending).
+    const int G = c->nranks;
+    DL_CUDA(cudaEventRecord(c->ev_fork, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    nccl_check(ncclAllReduce(c->g_rec, c->g_rec, (size_t)(H * H), ncclFloat, ncclSum, c->comm,
+                             c->st2));
+    reduce_splits(c->g_rec, 1, 0, H * H, c->g_rec, clip, 1, c->nonfinite, c->st2);
+    nccl_check(ncclAllGather(c->x_d, c->x_all, (size_t)TB, ncclUint32, c->comm, c->st2));
+    nccl_check(ncclAllGather(c->dpre, c->dpre_all, (size_t)(TB * H), ncclFloat, c->comm, c->st2));
+    DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
+    DL_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+    c->launches++;
     Phase p(c, "embed_grad");
-    embed_grads(c->x_d, T, B, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words, c->g_in_n,
-                c->nonfinite, st);
+    embed_grads(c->x_all, T, B, G, c->dpre_all, H, clip, c->ews, c->g_in_rows, c->g_in_words,
+                c->g_in_n, c->nonfinite, st);
+    c->launches += 2;
+  } else {
+    // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped
+    Phase p(c, "embed_grad");
+    embed_grads(c->x_d, T, B, 1, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words,
+                c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   }
   c->have_grads = true;
@@ -537,6 +595,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   c->act = act;
   c->precision = precision;
   if (const char* e = std::getenv("DL_REC_CLUSTER")) c->rec_cluster = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_FORK_OUT")) c->fork_out = std::atoi(e) != 0;
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
@@ -567,6 +626,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->d_loss = dalloc<double>(1);
     c->d_pos = dalloc<unsigned long long>(1);
     c->d_skipped = dalloc<unsigned long long>(1);
+    c->win_loss = dalloc<double>(2);
+    c->win_pos = reinterpret_cast<unsigned long long*>(c->win_loss + 1);
     c->win_counter = dalloc<int64_t>(1);
     if (precision == DL_BF16) {
       c->w_rec_bf = dalloc<bf16>(H * H);
@@ -604,7 +665,8 @@ int dl_destroy(dl_ctx* c) {
                   c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
-                  c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter};
+                  c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
+                  c->win_loss, c->x_all, c->dpre_all};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -758,7 +820,7 @@ int dl_rmsprop(dl_ctx* c, double eta, int* applied) {
   if (!c) return fail(c, DL_EINVAL, "dl_rmsprop: null ctx");
   if (!c->have_grads) return fail(c, DL_EINVAL, "dl_rmsprop: no gradients computed yet");
   return guarded(c, [&] {
-    run_rmsprop(c, eta, c->capT * c->capB);
+    run_rmsprop(c, eta, c->capT * c->capB * c->nranks);
     int bad = 0;
     DL_CUDA(cudaMemcpyAsync(&bad, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
@@ -900,6 +962,23 @@ int dl_rnn_perplexity(dl_ctx* c, const uint32_t* ids, int64_t n, uint32_t bos,
 }
 
 // ------------------------------------------------------------- trainer
+// trainer.hpp:194-195 (cursor_i = floor(i*L/N)) for this rank's slice of
+// every group: with G ranks the global minibatch is G*minibatch and rank r
+// owns global streams g*G*minibatch + r*minibatch + b.  Pure host code.
+int dl_rank_cursors(int64_t L, int noffset, int minibatch, int nranks, int rank,
+                    int64_t* out) {
+  if (L < 1 || noffset < 1 || minibatch < 1 || nranks < 1 || rank < 0 || rank >= nranks || !out)
+    return fail(nullptr, DL_EINVAL, "dl_rank_cursors: bad arguments");
+  const int64_t Bg = (int64_t)minibatch * nranks;
+  const int64_t Nglob = (int64_t)noffset * Bg;
+  for (int64_t g = 0; g < noffset; ++g)
+    for (int64_t b = 0; b < minibatch; ++b) {
+      const int64_t s = g * Bg + (int64_t)rank * minibatch + b;
+      out[g * minibatch + b] = s * L / Nglob;
+    }
+  return DL_OK;
+}
+
 int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int minibatch,
                     int unroll, double clip, uint32_t bos) {
   if (!c) return fail(c, DL_EINVAL, "dl_trainer_init: null ctx");
@@ -925,14 +1004,8 @@ int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int 
     const int64_t Nl = (int64_t)noffset * minibatch;
     c->cursors = dalloc<int64_t>(Nl);
     c->hidden = dalloc<float>(Nl * c->H);
-    // trainer.hpp:194-198 with this rank's slice of every group
     std::vector<int64_t> cur(Nl);
-    const int64_t Bg = (int64_t)minibatch * c->nranks;
-    for (int64_t g = 0; g < noffset; ++g)
-      for (int64_t b = 0; b < minibatch; ++b) {
-        const int64_t s = g * Bg + c->rank * minibatch + b;
-        cur[g * minibatch + b] = s * L / Nglob;
-      }
+    dl_rank_cursors(L, noffset, minibatch, c->nranks, c->rank, cur.data());
     DL_CUDA(cudaMemcpyAsync(c->cursors, cur.data(), Nl * 8, cudaMemcpyHostToDevice, c->st));
     fill_f32(c->hidden, act0(c->act), Nl * c->H, c->st);
     ensure_window(c, unroll, minibatch);
@@ -967,7 +1040,8 @@ int dl_trainer_set_state(dl_ctx* c, const int64_t* cursors, const float* hidden)
 
 namespace {
 bool fork_ok(dl_ctx* c) {
-  return tc(c) && c->w_out_bf_next && std::isfinite((float)c->clip) && c->comm == nullptr;
+  return c->fork_out && tc(c) && c->w_out_bf_next && std::isfinite((float)c->clip) &&
+         c->comm == nullptr;
 }
 
 void swap_shadow(dl_ctx* c) {
@@ -998,7 +1072,7 @@ void trainer_window(dl_ctx* c, double eta) {
   // allreduce is pending
   const bool fork = fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0);
-  run_rmsprop(c, eta, T * B, /*skip_out=*/fork);
+  run_rmsprop(c, eta, T * B * c->nranks, /*skip_out=*/fork);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
                 c->L, act0(c->act), c->st);
   c->launches += 2;
@@ -1080,11 +1154,42 @@ int dl_comm_init(dl_ctx* c, const uint8_t id[128], int nranks, int rank) {
   return guarded(c, [&] {
     c->nranks = nranks;
     c->rank = rank;
+    c->capT = c->capB = 0;  // window buffers are re-sized for the gathered window
+    drop_graphs(c);
     if (nranks == 1) return;
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
     DL_REQUIRE(ncclCommInitRank(&c->comm, nranks, u, rank) == ncclSuccess, DL_EDEVICE,
                "ncclCommInitRank failed");
+  });
+}
+
+// Test hook for the data-parallel W_in gradient: G rank-blocked windows
+// x_all [G][T][B], dpre_all [G][T][B][H] -> clipped dense g_in [V x H],
+// summed per word in the reference's processing order over the global
+// window (t descending, global stream r*B+b ascending).
+int dl_test_embed(dl_ctx* c, int G, int64_t T, int64_t B, const uint32_t* x_all,
+                  const float* dpre_all, float clip, float* g_in_dense) {
+  if (!c || G < 1 || T < 1 || B < 1) return fail(c, DL_EINVAL, "dl_test_embed: bad shape");
+  return guarded(c, [&] {
+    const int64_t n = G * T * B, H = c->H;
+    uint32_t* x = dalloc<uint32_t>(n);
+    float* d = dalloc<float>(n * H);
+    float* rows = dalloc<float>(n * H);
+    uint32_t* words = dalloc<uint32_t>(n);
+    int* nr = dalloc<int>(1);
+    EmbedWs ws{dalloc<int>(n + 1), dalloc<int>(n)};
+    float* dense = dalloc<float>(c->V * H);
+    DL_CUDA(cudaMemcpyAsync(x, x_all, n * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(d, dpre_all, n * H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemsetAsync(dense, 0, c->V * H * 4, c->st));
+    embed_grads(x, T, B, G, d, H, clip, ws, rows, words, nr, nullptr, c->st);
+    embed_dense(rows, words, nr, n, H, dense, c->st);
+    DL_CUDA(cudaMemcpyAsync(g_in_dense, dense, c->V * H * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    for (void* p : {(void*)x, (void*)d, (void*)rows, (void*)words, (void*)nr, (void*)ws.seg_start,
+                    (void*)ws.order_pos, (void*)dense})
+      cudaFree(p);
   });
 }
 
