@@ -3,6 +3,9 @@
 // embedding gradient, clip/finite, rmsprop and the device-side offset-stream
 // schedule.  Each kernel cites the reference code it replaces (paths
 // relative to /root/reference/proj/include/desklm).
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+
 #include "kernels.cuh"
 
 namespace dl {
@@ -333,6 +336,71 @@ k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, in
   }
 }
 
+// Same contract as k_embed_sort, by a stable block radix sort on the word id
+// (values = processing index, so equal words keep processing order), for
+// n <= 1024 * IPT positions.
+template <int IPT>
+struct EmbedRadix {
+  using Sort = cub::BlockRadixSort<uint32_t, kSortThreads, IPT, int>;
+  using Scan = cub::BlockScan<int, kSortThreads>;
+  struct Smem {
+    union {
+      typename Sort::TempStorage sort;
+      typename Scan::TempStorage scan;
+    } u;
+    uint32_t last[kSortThreads];
+  };
+};
+
+template <int IPT>
+__global__ void __launch_bounds__(kSortThreads)
+k_embed_radix(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, int end_bit,
+              int* __restrict__ seg_start, int* __restrict__ n_seg, int* __restrict__ order_pos,
+              uint32_t* __restrict__ seg_word) {
+  using R = EmbedRadix<IPT>;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  typename R::Smem& sm = *reinterpret_cast<typename R::Smem*>(sm_raw);
+  const int n = (int)(G * T * B);
+  const uint32_t pad = (1u << end_bit) - 1u;  // > every word id
+  uint32_t key[IPT];
+  int val[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = threadIdx.x * IPT + k;
+    key[k] = i < n ? x[gathered_pos(i, T, B, G)] : pad;
+    val[k] = i;
+  }
+  typename R::Sort(sm.u.sort).Sort(key, val, 0, end_bit);
+  sm.last[threadIdx.x] = key[IPT - 1];
+  __syncthreads();
+  int head[IPT], cnt = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = threadIdx.x * IPT + k;
+    const uint32_t prev = k > 0 ? key[k - 1] : (threadIdx.x > 0 ? sm.last[threadIdx.x - 1] : ~0u);
+    head[k] = (i < n) && key[k] != prev;
+    cnt += head[k];
+  }
+  int off, total;
+  typename R::Scan(sm.u.scan).ExclusiveSum(cnt, off, total);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = threadIdx.x * IPT + k;
+    if (i < n) {
+      order_pos[i] = (int)gathered_pos(val[k], T, B, G);
+      if (head[k]) {
+        seg_start[off] = i;
+        seg_word[off] = key[k];
+        ++off;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    *n_seg = total;
+    seg_start[total] = n;
+  }
+}
+
 // Row sums per segment in processing order, then clip (rnn.hpp:155-162).
 // Grid-stride over slots; threads cover the H columns of one slot.
 __global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
@@ -470,7 +538,7 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
 // at HBM speed from only one 256-thread block per SM, which co-resides with
 // the tensor-core GEMM it overlaps.
 template <int NV4>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128, NV4 > 8 ? 3 : 4)
 k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
                  const float* __restrict__ g, int64_t V, double rho, double eps, double eta,
                  const int* __restrict__ nonfinite) {
@@ -482,11 +550,9 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
   for (int64_t r = warp0; r < V; r += nwarps) {
     const float4* g4 = reinterpret_cast<const float4*>(g + r * H);
     float4* w4 = reinterpret_cast<float4*>(w + r * H);
-    float4 q[NV4], o[NV4];
+    float4 q[NV4];
 #pragma unroll
     for (int k = 0; k < NV4; ++k) q[k] = __ldcs(g4 + lane + 32 * k);
-#pragma unroll
-    for (int k = 0; k < NV4; ++k) o[k] = w4[lane + 32 * k];
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < NV4; ++k)
@@ -497,15 +563,16 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
     const double denom = sqrt((double)mw + eps);
 #pragma unroll
     for (int k = 0; k < NV4; ++k) {
-      o[k].x -= (float)(eta * (double)q[k].x / denom);
-      o[k].y -= (float)(eta * (double)q[k].y / denom);
-      o[k].z -= (float)(eta * (double)q[k].z / denom);
-      o[k].w -= (float)(eta * (double)q[k].w / denom);
-      w4[lane + 32 * k] = o[k];
+      float4 o = w4[lane + 32 * k];
+      o.x -= (float)(eta * (double)q[k].x / denom);
+      o.y -= (float)(eta * (double)q[k].y / denom);
+      o.z -= (float)(eta * (double)q[k].z / denom);
+      o.w -= (float)(eta * (double)q[k].w / denom);
+      w4[lane + 32 * k] = o;
       if (wb) {
         __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + r * H + 4 * (lane + 32 * k));
-        b2[0] = __floats2bfloat162_rn(o[k].x, o[k].y);
-        b2[1] = __floats2bfloat162_rn(o[k].z, o[k].w);
+        b2[0] = __floats2bfloat162_rn(o.x, o.y);
+        b2[1] = __floats2bfloat162_rn(o.z, o.w);
       }
     }
     if (lane == 0) m[r] = mw;
@@ -638,22 +705,27 @@ void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st) {
   k_sum_rows<<<1, 1024, 0, st>>>(v, wts, n, acc, cnt);
 }
-void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, const float* dpre, int64_t H,
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st) {
   const int64_t n = G * T * B;
-  int p2 = 1;
-  while (p2 < n) p2 <<= 1;
-  const size_t smem = sizeof(unsigned long long) * p2;
-  static bool attr = false;
-  if (!attr) {
-    DL_CUDA(cudaFuncSetAttribute(k_embed_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    attr = true;
-  }
-  DL_REQUIRE(smem <= 200 * 1024, 1, "window too large for the embedding sort (T*B <= 16384)");
-  k_embed_sort<<<1, kSortThreads, smem, st>>>(x, T, B, G, p2, ws.seg_start, n_rows,
-                                               ws.order_pos, words);
+  DL_REQUIRE(n <= 16 * kSortThreads, 1, "window too large for the embedding sort (G*T*B <= 16384)");
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) <= V) ++end_bit;  // 2^end_bit - 1 >= V pads past every id
+#define DL_RADIX(IPT)                                                                          \
+  if (n <= (IPT) * kSortThreads) {                                                             \
+    static bool attr = false;                                                                  \
+    const size_t smem = sizeof(typename EmbedRadix<IPT>::Smem);                                \
+    if (!attr) {                                                                               \
+      DL_CUDA(cudaFuncSetAttribute(k_embed_radix<IPT>,                                         \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+      attr = true;                                                                             \
+    }                                                                                          \
+    k_embed_radix<IPT><<<1, kSortThreads, smem, st>>>(x, T, B, G, end_bit, ws.seg_start,       \
+                                                      n_rows, ws.order_pos, words);            \
+  } else
+  DL_RADIX(2) DL_RADIX(4) DL_RADIX(8) DL_RADIX(16) {}
+#undef DL_RADIX
   const unsigned gy = (unsigned)((H + 255) / 256);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (148 * 16) / gy));
   k_embed_rows<<<dim3(gx, gy), 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows,
@@ -675,11 +747,11 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st) {
   if (dense && !words && !n_rows_dev && (H == 1024 || H == 2048)) {
-    const int blocks = 148 * 2;
+    const int blocks = 148 * (H == 1024 ? 4 : 3);
     if (H == 1024)
-      k_rms_dense_rows<8><<<blocks, 256, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
+      k_rms_dense_rows<8><<<blocks, 128, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
     else
-      k_rms_dense_rows<16><<<blocks, 256, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
+      k_rms_dense_rows<16><<<blocks, 128, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
     return;
   }
   const int64_t warps = n_rows;

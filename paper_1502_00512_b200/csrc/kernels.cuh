@@ -30,7 +30,7 @@ void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_
 void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st);
 // x / dpre: G rank-blocked windows [G][T][B] (G = 1 on one GPU)
-void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, const float* dpre, int64_t H,
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st);
 void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,

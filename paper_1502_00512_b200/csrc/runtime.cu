@@ -540,13 +540,13 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     DL_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
     c->launches++;
     Phase p(c, "embed_grad");
-    embed_grads(c->x_all, T, B, G, c->dpre_all, H, clip, c->ews, c->g_in_rows, c->g_in_words,
+    embed_grads(c->x_all, T, B, G, V, c->dpre_all, H, clip, c->ews, c->g_in_rows, c->g_in_words,
                 c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   } else {
     // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped
     Phase p(c, "embed_grad");
-    embed_grads(c->x_d, T, B, 1, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words,
+    embed_grads(c->x_d, T, B, 1, V, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words,
                 c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   }
@@ -1183,7 +1183,7 @@ int dl_test_embed(dl_ctx* c, int G, int64_t T, int64_t B, const uint32_t* x_all,
     DL_CUDA(cudaMemcpyAsync(x, x_all, n * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaMemcpyAsync(d, dpre_all, n * H * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaMemsetAsync(dense, 0, c->V * H * 4, c->st));
-    embed_grads(x, T, B, G, d, H, clip, ws, rows, words, nr, nullptr, c->st);
+    embed_grads(x, T, B, G, c->V, d, H, clip, ws, rows, words, nr, nullptr, c->st);
     embed_dense(rows, words, nr, n, H, dense, c->st);
     DL_CUDA(cudaMemcpyAsync(g_in_dense, dense, c->V * H * 4, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
