@@ -6,6 +6,8 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace dl {
@@ -459,6 +461,27 @@ __global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* _
   }
 }
 
+// float(eta * g / denom) exactly as the reference computes it (double
+// multiply, IEEE double divide, round to float), with one reciprocal per row
+// instead of a divide per element: q*inv is within 1.5 double ulps of the
+// correctly rounded quotient, so rounding it to float gives the same float
+// unless the quotient lies within a few double ulps of a float rounding
+// midpoint -- only then is the exact division performed.
+__device__ __forceinline__ float rms_step(double eta, float g, double denom, double inv) {
+  const double q = eta * (double)g;
+  const double r = q * inv;
+  const float f = (float)r;
+  const float af = fabsf(f);
+  if (!(af < 3.0e38f) || af < 1.0e-30f) return (float)(q / denom);  // inf/NaN/tiny: exact
+  const double up = (double)__int_as_float(__float_as_int(af) + 1) - (double)af;
+  const double dn = (double)af - (double)__int_as_float(__float_as_int(af) - 1);
+  const double ar = fabs(r), fd = (double)af;
+  const double tol = ar * 0x1p-49;
+  if (fabs(ar - (fd + 0.5 * up)) <= tol || fabs(ar - (fd - 0.5 * dn)) <= tol)
+    return (float)(q / denom);
+  return f;
+}
+
 // rmsprop.hpp:84 first loop: every W_in accumulator decays.
 __global__ void k_rms_decay(float* __restrict__ m, int64_t n, double rho,
                             const int* __restrict__ nonfinite) {
@@ -502,6 +525,7 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
     if (dense) mw = (float)(rho * (double)m[word] + (1.0 - rho) * ms);
     else mw = m[word] + (float)((1.0 - rho) * ms);
     const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
     float* wr = w + word * H;
     bf16* wbr = wb ? wb + word * H : nullptr;
     if ((H % 4) == 0) {
@@ -510,10 +534,10 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
       for (int64_t j = lane; j < H / 4; j += 32) {
         const float4 q = g4[j];
         float4 o = w4[j];
-        o.x -= (float)(eta * (double)q.x / denom);
-        o.y -= (float)(eta * (double)q.y / denom);
-        o.z -= (float)(eta * (double)q.z / denom);
-        o.w -= (float)(eta * (double)q.w / denom);
+        o.x -= rms_step(eta, q.x, denom, inv);
+        o.y -= rms_step(eta, q.y, denom, inv);
+        o.z -= rms_step(eta, q.z, denom, inv);
+        o.w -= rms_step(eta, q.w, denom, inv);
         w4[j] = o;
         if (wbr) {
           __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wbr + 4 * j);
@@ -523,7 +547,7 @@ __global__ void k_rms_rows(float* __restrict__ w, bf16* __restrict__ wb, float* 
       }
     } else {
       for (int64_t j = lane; j < H; j += 32) {
-        const float o = wr[j] - (float)(eta * (double)gr[j] / denom);
+        const float o = wr[j] - rms_step(eta, gr[j], denom, inv);
         wr[j] = o;
         if (wbr) wbr[j] = __float2bfloat16_rn(o);
       }
@@ -561,13 +585,14 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
     s = warp_sum_d(s);
     const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
     const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
 #pragma unroll
     for (int k = 0; k < NV4; ++k) {
       float4 o = w4[lane + 32 * k];
-      o.x -= (float)(eta * (double)q[k].x / denom);
-      o.y -= (float)(eta * (double)q[k].y / denom);
-      o.z -= (float)(eta * (double)q[k].z / denom);
-      o.w -= (float)(eta * (double)q[k].w / denom);
+      o.x -= rms_step(eta, q[k].x, denom, inv);
+      o.y -= rms_step(eta, q[k].y, denom, inv);
+      o.z -= rms_step(eta, q[k].z, denom, inv);
+      o.w -= rms_step(eta, q[k].w, denom, inv);
       w4[lane + 32 * k] = o;
       if (wb) {
         __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + r * H + 4 * (lane + 32 * k));
@@ -743,10 +768,17 @@ void rms_rec(float* w, bf16* wb, float* m, const float* g, int64_t n, double rho
 void rms_decay(float* m, int64_t n, double rho, const int* nonfinite, cudaStream_t st) {
   k_rms_decay<<<grid_for(n), 256, 0, st>>>(m, n, rho, nonfinite);
 }
+// DL_DENSE_ROWS=1 selects the register-resident one-warp-per-row W_out
+// kernel (fewer warps; measured slower than k_rms_rows on B200).
+static const bool use_dense_rows_kernel = [] {
+  const char* e = std::getenv("DL_DENSE_ROWS");
+  return e && std::atoi(e) != 0;
+}();
+
 void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* words,
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st) {
-  if (dense && !words && !n_rows_dev && (H == 1024 || H == 2048)) {
+  if (use_dense_rows_kernel && dense && !words && !n_rows_dev && (H == 1024 || H == 2048)) {
     const int blocks = 148 * (H == 1024 ? 4 : 3);
     if (H == 1024)
       k_rms_dense_rows<8><<<blocks, 128, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
