@@ -47,6 +47,15 @@ void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t 
 // mode 0: out = act(A . W_rec^T + W_in[x]); mode 1: out = (A . W_rec +
 // dh_out) * act'(hnext).  A is [M x H] bf16, K-major.
 void rec_plan(int M, int H, int& bn, int& S);
+// All T steps in one persistent cluster launch (W_rec slice resident in
+// shared memory, grid barrier per step).  mode 0: A tape = h (bf16) rows
+// [(T+1) x M]; writes htape[s+1].  mode 1: A tape = dpre (bf16) [T x M];
+// writes dpre[s] for s = T-1..0.  Returns false if it cannot run (caller
+// falls back to rec_step_tc per step).
+bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, int64_t a_rows,
+                   const bf16* w_rec_bf, const float* w_in, const uint32_t* x,
+                   const float* dh_out, const float* htape, float* out, bf16* outb,
+                   unsigned* counter, cudaStream_t st);
 void rec_step_tc(int mode, int M, int H, int act, const bf16* A, const bf16* w_rec_bf,
                  const float* w_in, const uint32_t* x, const float* dh_out, const float* hnext,
                  float* out, bf16* outb, cudaStream_t st);

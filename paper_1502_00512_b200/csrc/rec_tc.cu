@@ -229,7 +229,294 @@ void rec_launch(const void* A, const void* Bw, RecParams p, cudaStream_t st) {
   DL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
 }
 
+// --------------------------------------------------------------------------
+// Persistent variant: ONE launch runs all T steps of the forward (or
+// backward) recurrence of a window.  Each CTA keeps its W_rec slice
+// (BN x K/S bf16) resident in shared memory for the whole window and only
+// streams its K-slice of h_t (or dpre_{t+1}) per step; steps are separated
+// by a grid-wide barrier on a global arrival counter (all CTAs co-resident:
+// cooperative cluster launch).  Per step: TMA A -> tcgen05.mma -> TMEM ->
+// shared fp32 partial -> cluster barrier -> DSMEM rank-ordered reduction +
+// fused epilogue -> global h_{t+1} / dpre_t (fp32 + bf16) -> arrive.
+struct PersistParams {
+  int M, N, K, S, kbs, T, mode, act;
+  int64_t MN;
+  const float* w_in;
+  const uint32_t* x;      // fwd: ids of step s at x + s*M
+  const float* dh_out;    // bwd: [T][M][N]
+  const float* htape;     // bwd: h tape [T+1][M][N] (act' argument)
+  float* out;             // fwd: htape (writes step s+1); bwd: dpre (writes step s)
+  bf16* outb;
+  unsigned* counter;      // zeroed before the launch
+};
+
+template <int BN>
+struct PersistCfg {
+  static constexpr int A_BLK = BM * BK * 2;  // 16 KB
+  static constexpr int B_BLK = BN * BK * 2;
+  static constexpr int PSTRIDE = BN + 4;
+  static constexpr int PART = BM * PSTRIDE * 4;
+  static constexpr int MAXKB = 4;  // k-blocks per CTA (K/S <= 256)
+  static constexpr int SMEM = MAXKB * (A_BLK + B_BLK) + PART + 1024 + 256;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int BN, bool B_MN>
+__global__ void __launch_bounds__(kRecThreads, 1)
+rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   PersistParams p) {
+  using C = PersistCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;                                 // kbs x 16 KB
+  uint8_t* sB = smem + C::MAXKB * C::A_BLK;           // kbs x B_BLK
+  float* part = reinterpret_cast<float*>(sB + C::MAXKB * C::B_BLK);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(part) + C::PART);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t barA = smem_u32(&bars[0]), barB = smem_u32(&bars[1]), tfull = smem_u32(&bars[2]);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nt = blockIdx.y;
+  const unsigned nctas = gridDim.x * gridDim.y;
+
+  if (threadIdx.x == 32) {
+    mbar_init(barA, 1);
+    mbar_init(barB, 1);
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kb0 = rank * p.kbs;
+  const int rows = BM / p.S, r0 = rank * rows;
+  constexpr int Q = BN / 4;
+
+  // resident W_rec slice, loaded once
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    mbar_expect_tx(barB, p.kbs * C::B_BLK);
+    for (int i = 0; i < p.kbs; ++i) {
+      const uint32_t b_s = smem_u32(sB + i * C::B_BLK);
+      if (!B_MN) {
+        tma_load_2d(b_s, &tmB, barB, (kb0 + i) * BK, nt * BN);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j)
+          tma_load_2d(b_s + j * 8192, &tmB, barB, nt * BN + 64 * j, (kb0 + i) * BK);
+      }
+    }
+  }
+
+  for (int j = 0; j < p.T; ++j) {
+    const int s = p.mode == 0 ? j : p.T - 1 - j;   // time step written this iteration
+    const bool gemm = p.mode == 0 || j > 0;        // bwd t = T-1 has no recurrent term
+    const uint32_t ph = (p.mode == 0 ? j : j - 1) & 1;
+    if (gemm) {
+      if (warp == 0 && lane == 0) {
+        // wait until every CTA has published the previous step
+        if (j > 0) {
+          const unsigned target = nctas * (unsigned)j;
+          long spins = 0;
+          while (ld_acquire(p.counter) < target) {
+            __nanosleep(20);
+            if (++spins > (1l << 26)) __trap();  // never hang the GPU
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        const int arow = p.mode == 0 ? s * p.M : (s + 1) * p.M;
+        mbar_expect_tx(barA, p.kbs * C::A_BLK);
+        for (int i = 0; i < p.kbs; ++i)
+          tma_load_2d(smem_u32(sA + i * C::A_BLK), &tmA, barA, (kb0 + i) * BK, arow);
+      } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                   (static_cast<uint32_t>(B_MN) << 16) |
+                                   (static_cast<uint32_t>(BN >> 3) << 17) |
+                                   (static_cast<uint32_t>(BM >> 4) << 24);
+        if (j == (p.mode == 0 ? 0 : 1)) mbar_wait(barB, 0);
+        mbar_wait(barA, ph);
+        fence_after();
+        for (int i = 0; i < p.kbs; ++i) {
+          const uint32_t a_s = smem_u32(sA + i * C::A_BLK);
+          const uint32_t b_s = smem_u32(sB + i * C::B_BLK);
+#pragma unroll
+          for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            const uint64_t ad = make_desc(a_s + ks * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(b_s + ks * 2048, 8192, 1024)
+                                     : make_desc(b_s + ks * 32, 16, 1024);
+            mma_bf16(tmem, ad, bd, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(tfull);
+      }
+      __syncwarp();
+      mbar_wait(tfull, ph);
+      fence_after();
+      {
+        const int quarter = warp % 4, half = warp / 4;
+        float* prow = part + (quarter * 32 + lane) * C::PSTRIDE;
+#pragma unroll 1
+        for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+          float v[32];
+          tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            *reinterpret_cast<float4*>(prow + c * 32 + q) =
+                make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+      }
+      fence_before();
+      cluster.sync();
+    }
+    // reduce my row slice over the cluster (rank order) + fused epilogue
+    for (int idx = threadIdx.x; idx < rows * Q; idx += kRecThreads) {
+      const int row = r0 + idx / Q, col = 4 * (idx % Q);
+      const int m = row, n = nt * BN + col;
+      if (m >= p.M || n >= p.N) continue;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gemm)
+        for (int q = 0; q < p.S; ++q) {
+          const float* peer = cluster.map_shared_rank(part, q);
+          const float4 v = *reinterpret_cast<const float4*>(peer + row * C::PSTRIDE + col);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      const int64_t o = static_cast<int64_t>(m) * p.N + n;
+      float4 y;
+      int64_t oo;
+      if (p.mode == 0) {
+        const float4 e = *reinterpret_cast<const float4*>(
+            p.w_in + static_cast<int64_t>(p.x[s * p.M + m]) * p.N + n);
+        y = make_float4(act_f(p.act, acc.x + e.x), act_f(p.act, acc.y + e.y),
+                        act_f(p.act, acc.z + e.z), act_f(p.act, acc.w + e.w));
+        oo = (s + 1) * p.MN + o;
+      } else {
+        const float4 d = *reinterpret_cast<const float4*>(p.dh_out + s * p.MN + o);
+        const float4 h = *reinterpret_cast<const float4*>(p.htape + (s + 1) * p.MN + o);
+        y = make_float4((acc.x + d.x) * act_deriv_f(p.act, h.x),
+                        (acc.y + d.y) * act_deriv_f(p.act, h.y),
+                        (acc.z + d.z) * act_deriv_f(p.act, h.z),
+                        (acc.w + d.w) * act_deriv_f(p.act, h.w));
+        oo = s * p.MN + o;
+      }
+      *reinterpret_cast<float4*>(p.out + oo) = y;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.outb + oo);
+      ob[0] = __floats2bfloat162_rn(y.x, y.y);
+      ob[1] = __floats2bfloat162_rn(y.z, y.w);
+    }
+    // publish this step (generic stores -> visible to the next step's TMA)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(p.counter, 1u);
+  }
+  cluster.sync();  // peers are done reading my shared memory
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(BN < 32 ? 32 : BN));
+  }
+}
+
+template <int BN, bool B_MN>
+bool persist_launch(const void* A_tape, int64_t a_rows, const void* Bw, PersistParams p,
+                    cudaStream_t st) {
+  using Cf = PersistCfg<BN>;
+  auto kern = rec_persist_kernel<BN, B_MN>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  const CUtensorMap ta = make_map(A_tape, a_rows, p.K, p.K, BM);
+  const CUtensorMap tb = B_MN ? make_map(Bw, p.K, p.N, p.N, 64) : make_map(Bw, p.N, p.K, p.K, BN);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.S, (p.N + BN - 1) / BN, 1);
+  cfg.blockDim = dim3(kRecThreads);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // The grid barrier needs every CTA resident at once: only launch when the
+  // device can host all clusters simultaneously (then nothing can starve
+  // them: other work on the GPU is finite and never waits on this kernel).
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    max_clusters = n;
+  }
+  const int need = (int)(cfg.gridDim.x * cfg.gridDim.y / p.S);
+  if (max_clusters < need) return false;
+  DL_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned), st));
+  DL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  return true;
+}
+
 }  // namespace tc
+
+// All T steps of a window's recurrence in one persistent launch; returns
+// false (nothing launched) when the shape or the device cannot host it, in
+// which case the caller uses the per-step kernels.
+bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, int64_t a_rows,
+                   const bf16* w_rec_bf, const float* w_in, const uint32_t* x,
+                   const float* dh_out, const float* htape, float* out, bf16* outb,
+                   unsigned* counter, cudaStream_t st) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("DL_REC_PERSIST");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!enabled || M > tc::BM || T < 1) return false;
+  const int kb_total = (H + 63) / 64;
+  int bn = 0, S = 0;
+  const int bns[2] = {128, 64};  // BN = 256 does not fit resident W_rec + partials
+  for (int bi = 0; bi < 2 && !bn; ++bi)
+    for (int s = 8; s >= 1; s >>= 1) {
+      const int b = bns[bi];
+      if (H % b || kb_total % s || kb_total / s > 4) continue;
+      if ((H / b) * s > 148) continue;
+      bn = b;
+      S = s;
+      break;
+    }
+  if (!bn) return false;
+  tc::PersistParams p{};
+  p.M = M; p.N = H; p.K = H; p.S = S; p.kbs = kb_total / S; p.T = T; p.mode = mode; p.act = act;
+  p.MN = (int64_t)M * H;
+  p.w_in = w_in; p.x = x; p.dh_out = dh_out; p.htape = htape;
+  p.out = out; p.outb = outb; p.counter = counter;
+  const bool bmn = mode == 1;
+  bool ok = false;
+#define DL_P_CASE(BN_)                                                            \
+  if (bn == BN_)                                                                  \
+    ok = bmn ? tc::persist_launch<BN_, true>(a_tape, a_rows, w_rec_bf, p, st)     \
+             : tc::persist_launch<BN_, false>(a_tape, a_rows, w_rec_bf, p, st);
+  DL_P_CASE(128)
+  DL_P_CASE(64)
+#undef DL_P_CASE
+  if (!ok) cudaGetLastError();  // clear a refused launch; caller falls back
+  return ok;
+}
 
 // Tile choice for a recurrence step: BN in {64,128,256} and S in {1,2,4,8}
 // K-slices (each >= one 64-wide k-block) to put ~128 CTAs on the 148 SMs.

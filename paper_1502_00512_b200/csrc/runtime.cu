@@ -126,6 +126,7 @@ struct dl_ctx {
   uint32_t* x_all = nullptr;  // [G][T][B] gathered window ids
   float* dpre_all = nullptr;  // [G][T][B][H] gathered dpre
   double* win_loss = nullptr;  // [loss, positions(u64)] of one window
+  unsigned* bar_counter = nullptr;  // grid barrier of the persistent recurrence
   unsigned long long* win_pos = nullptr;
 
   // profiling
@@ -386,10 +387,18 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   }
   {
     Phase p(c, "recurrence_fwd");
-    for (int64_t t = 0; t < T; ++t)
-      rec_step_fwd(c, B, c->htape + t * BH, tc(c) ? c->htape_bf + t * BH : nullptr,
-                   c->x_d + t * B, c->htape + (t + 1) * BH,
-                   tc(c) ? c->htape_bf + (t + 1) * BH : nullptr);
+    const bool persist = tc(c) && c->rec_cluster &&
+                         rec_window_tc(0, (int)T, (int)B, (int)H, c->act, c->htape_bf, (T + 1) * B,
+                                       c->w_rec_bf, c->w_in, c->x_d, nullptr, nullptr, c->htape,
+                                       c->htape_bf, c->bar_counter, st);
+    if (persist) {
+      c->launches++;
+    } else {
+      for (int64_t t = 0; t < T; ++t)
+        rec_step_fwd(c, B, c->htape + t * BH, tc(c) ? c->htape_bf + t * BH : nullptr,
+                     c->x_d + t * B, c->htape + (t + 1) * BH,
+                     tc(c) ? c->htape_bf + (t + 1) * BH : nullptr);
+    }
   }
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
@@ -483,7 +492,12 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // backward recurrence (backprop.hpp:197-219)
   {
     Phase p(c, "recurrence_bwd");
-    for (int64_t t = T - 1; t >= 0; --t) {
+    const bool persist = tc(c) && c->rec_cluster &&
+                         rec_window_tc(1, (int)T, (int)B, (int)H, c->act, c->dpre_bf, T * B,
+                                       c->w_rec_bf, nullptr, nullptr, c->dh_out, c->htape,
+                                       c->dpre, c->dpre_bf, c->bar_counter, st);
+    if (persist) c->launches++;
+    for (int64_t t = persist ? -1 : T - 1; t >= 0; --t) {
       float* dp_t = c->dpre + t * BH;
       bf16* dpb_t = tc(c) ? c->dpre_bf + t * BH : nullptr;
       int s = 0;
@@ -626,6 +640,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->d_loss = dalloc<double>(1);
     c->d_pos = dalloc<unsigned long long>(1);
     c->d_skipped = dalloc<unsigned long long>(1);
+    c->bar_counter = dalloc<unsigned>(1);
     c->win_loss = dalloc<double>(2);
     c->win_pos = reinterpret_cast<unsigned long long*>(c->win_loss + 1);
     c->win_counter = dalloc<int64_t>(1);
@@ -666,7 +681,7 @@ int dl_destroy(dl_ctx* c) {
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
-                  c->win_loss, c->x_all, c->dpre_all};
+                  c->win_loss, c->x_all, c->dpre_all, c->bar_counter};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
