@@ -17,6 +17,7 @@
 //     + dh_out and * act'(h)), writing fp32 and bf16 copies.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -256,8 +257,9 @@ struct PersistCfg {
   static constexpr int B_BLK = BN * BK * 2;
   static constexpr int PSTRIDE = BN + 4;
   static constexpr int PART = BM * PSTRIDE * 4;
-  static constexpr int MAXKB = 4;  // k-blocks per CTA (K/S <= 256)
-  static constexpr int SMEM = MAXKB * (A_BLK + B_BLK) + PART + 1024 + 256;
+  static constexpr int MAXKB = BN <= 64 ? 8 : 4;  // resident W_rec k-blocks per CTA
+  static constexpr int NA = 4;                    // A ring stages (streamed per step)
+  static constexpr int SMEM = NA * A_BLK + MAXKB * B_BLK + PART + 1024 + 256;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -274,12 +276,15 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sA = smem;                                 // kbs x 16 KB
-  uint8_t* sB = smem + C::MAXKB * C::A_BLK;           // kbs x B_BLK
+  uint8_t* sA = smem;                                 // NA-stage ring of 16 KB
+  uint8_t* sB = smem + C::NA * C::A_BLK;              // kbs x B_BLK, resident
   float* part = reinterpret_cast<float*>(sB + C::MAXKB * C::B_BLK);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(part) + C::PART);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const uint32_t barA = smem_u32(&bars[0]), barB = smem_u32(&bars[1]), tfull = smem_u32(&bars[2]);
+  // bars: full[NA], empty[NA], barB, tfull
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::NA + 2);
+  auto fullA = [&](int s) { return smem_u32(&bars[s]); };
+  auto emptyA = [&](int s) { return smem_u32(&bars[C::NA + s]); };
+  const uint32_t barB = smem_u32(&bars[2 * C::NA]), tfull = smem_u32(&bars[2 * C::NA + 1]);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -287,11 +292,13 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const unsigned nctas = gridDim.x * gridDim.y;
 
   if (threadIdx.x == 32) {
-    mbar_init(barA, 1);
+    for (int s = 0; s < C::NA; ++s) { mbar_init(fullA(s), 1); mbar_init(emptyA(s), 1); }
     mbar_init(barB, 1);
     mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  int a_stage = 0;       // A ring position, persistent across steps
+  uint32_t a_phase = 0;  // (producer and MMA lanes advance identical copies)
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -339,19 +346,23 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         const int arow = p.mode == 0 ? s * p.M : (s + 1) * p.M;
-        mbar_expect_tx(barA, p.kbs * C::A_BLK);
-        for (int i = 0; i < p.kbs; ++i)
-          tma_load_2d(smem_u32(sA + i * C::A_BLK), &tmA, barA, (kb0 + i) * BK, arow);
+        for (int i = 0; i < p.kbs; ++i) {
+          mbar_wait(emptyA(a_stage), a_phase ^ 1);
+          mbar_expect_tx(fullA(a_stage), C::A_BLK);
+          tma_load_2d(smem_u32(sA + a_stage * C::A_BLK), &tmA, fullA(a_stage), (kb0 + i) * BK,
+                      arow);
+          if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
+        }
       } else if (warp == 1 && lane == 0) {
         constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                    (static_cast<uint32_t>(B_MN) << 16) |
                                    (static_cast<uint32_t>(BN >> 3) << 17) |
                                    (static_cast<uint32_t>(BM >> 4) << 24);
         if (j == (p.mode == 0 ? 0 : 1)) mbar_wait(barB, 0);
-        mbar_wait(barA, ph);
-        fence_after();
         for (int i = 0; i < p.kbs; ++i) {
-          const uint32_t a_s = smem_u32(sA + i * C::A_BLK);
+          mbar_wait(fullA(a_stage), a_phase);
+          fence_after();
+          const uint32_t a_s = smem_u32(sA + a_stage * C::A_BLK);
           const uint32_t b_s = smem_u32(sB + i * C::B_BLK);
 #pragma unroll
           for (int ks = 0; ks < BK / UMMA_K; ++ks) {
@@ -360,6 +371,8 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                                      : make_desc(b_s + ks * 32, 16, 1024);
             mma_bf16(tmem, ad, bd, idesc, (i > 0 || ks > 0) ? 1u : 0u);
           }
+          mma_commit(emptyA(a_stage));
+          if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
         }
         mma_commit(tfull);
       }
@@ -457,17 +470,18 @@ bool persist_launch(const void* A_tape, int64_t a_rows, const void* Bw, PersistP
   // The grid barrier needs every CTA resident at once: only launch when the
   // device can host all clusters simultaneously (then nothing can starve
   // them: other work on the GPU is finite and never waits on this kernel).
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
+  static int max_clusters[4] = {-1, -1, -1, -1};  // per cluster size 1, 2, 4, 8
+  const int si = p.S == 1 ? 0 : p.S == 2 ? 1 : p.S == 4 ? 2 : 3;
+  if (max_clusters[si] < 0) {
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
-    max_clusters = n;
+    max_clusters[si] = n;
   }
   const int need = (int)(cfg.gridDim.x * cfg.gridDim.y / p.S);
-  if (max_clusters < need) return false;
+  if (max_clusters[si] < need) return false;
   DL_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned), st));
   DL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return true;
@@ -488,33 +502,35 @@ bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, i
   }();
   if (!enabled || M > tc::BM || T < 1) return false;
   const int kb_total = (H + 63) / 64;
-  int bn = 0, S = 0;
-  const int bns[2] = {128, 64};  // BN = 256 does not fit resident W_rec + partials
-  for (int bi = 0; bi < 2 && !bn; ++bi)
-    for (int s = 8; s >= 1; s >>= 1) {
-      const int b = bns[bi];
-      if (H % b || kb_total % s || kb_total / s > 4) continue;
-      if ((H / b) * s > 148) continue;
-      bn = b;
-      S = s;
-      break;
-    }
-  if (!bn) return false;
+  // candidates in preference order (BN = 256 cannot keep W_rec + partials
+  // resident); the first whose clusters all fit on the device launches
+  const int cand[8][2] = {{64, 4}, {128, 8}, {64, 8}, {128, 4}, {64, 2}, {128, 2}, {64, 1},
+                          {128, 1}};
   tc::PersistParams p{};
-  p.M = M; p.N = H; p.K = H; p.S = S; p.kbs = kb_total / S; p.T = T; p.mode = mode; p.act = act;
+  p.M = M; p.N = H; p.K = H; p.T = T; p.mode = mode; p.act = act;
   p.MN = (int64_t)M * H;
   p.w_in = w_in; p.x = x; p.dh_out = dh_out; p.htape = htape;
   p.out = out; p.outb = outb; p.counter = counter;
   const bool bmn = mode == 1;
   bool ok = false;
-#define DL_P_CASE(BN_)                                                            \
-  if (bn == BN_)                                                                  \
-    ok = bmn ? tc::persist_launch<BN_, true>(a_tape, a_rows, w_rec_bf, p, st)     \
-             : tc::persist_launch<BN_, false>(a_tape, a_rows, w_rec_bf, p, st);
-  DL_P_CASE(128)
-  DL_P_CASE(64)
-#undef DL_P_CASE
-  if (!ok) cudaGetLastError();  // clear a refused launch; caller falls back
+  int bn = 0, S = 0;
+  for (int ci = 0; ci < 8 && !ok; ++ci) {
+    bn = cand[ci][0];
+    S = cand[ci][1];
+    const int maxkb = bn <= 64 ? tc::PersistCfg<64>::MAXKB : tc::PersistCfg<128>::MAXKB;
+    if (H % bn || kb_total % S || kb_total / S > maxkb || (H / bn) * S > 148) continue;
+    p.S = S;
+    p.kbs = kb_total / S;
+    if (bn == 64)
+      ok = bmn ? tc::persist_launch<64, true>(a_tape, a_rows, w_rec_bf, p, st)
+               : tc::persist_launch<64, false>(a_tape, a_rows, w_rec_bf, p, st);
+    else
+      ok = bmn ? tc::persist_launch<128, true>(a_tape, a_rows, w_rec_bf, p, st)
+               : tc::persist_launch<128, false>(a_tape, a_rows, w_rec_bf, p, st);
+  }
+  if (std::getenv("DL_DEBUG"))
+    fprintf(stderr, "[desklm] persistent recurrence mode=%d T=%d M=%d H=%d BN=%d S=%d -> %s\n",
+            mode, T, M, H, bn, S, ok ? "launched" : "fallback");
   return ok;
 }
 

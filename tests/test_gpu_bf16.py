@@ -66,7 +66,9 @@ def test_cluster_recurrence_matches_splitk_path(orc):
         m.close()
     (l1, h1, g1), (l2, h2, g2) = out
     assert l1 == pytest.approx(l2, rel=1e-4)
-    assert np.abs(h1 - h2).max() < 2e-3
+    # bf16 h tapes: different (deterministic) summation orders move a value
+    # across a bf16 rounding boundary now and then; that propagates
+    assert np.abs(h1 - h2).max() < 1e-2
     for a, b in zip(g1, g2):
         assert cos(a, b) > 0.999
 
