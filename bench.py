@@ -86,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -177,7 +177,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
@@ -226,12 +226,14 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # warm-up (also captures the per-window CUDA graph)
-    model.trainer_run(0, args.warmup, eta)
-    torch.cuda.synchronize()
-    launches0 = model.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # clocks are sampled from before the warm-up through the timed region
+    # (nvidia-smi's 100 ms period would otherwise miss a short timed region)
     with ClockSampler(local) as clk:
+        # warm-up (also captures the per-window CUDA graphs)
+        model.trainer_run(0, args.warmup, eta)
+        torch.cuda.synchronize()
+        launches0 = model.launch_count()
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
@@ -239,6 +241,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
+        time.sleep(0.25)
     ms = e0.elapsed_time(e1)
     launches = model.launch_count() - launches0
     if world > 1:
@@ -267,8 +270,16 @@ def main():
     achieved = gemm_flops[dom] / (dom_ms / 1000.0) / 1e12
     peak = PEAKS["bf16_tflops_sustained"]
     step_ms = ms / args.steps
+    traffic = None  # dram bytes per launch of that kernel from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as f:
+            s = json.load(f)["dominant_kernel_for_bench_roofline"]
+        if s["kernel"] == f"tc_gemm[{dom}]" and args.config == "c3":
+            traffic = s["traffic_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": f"tc_gemm[{dom}]", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_kind": "measured sustained (MEASURED_PEAKS.json bf16_tflops_sustained)",
                 "algorithmic_flops_per_launch": gemm_flops[dom],
                 "step_frac_of_peak": value / world * fpw / 1e12 / peak,
