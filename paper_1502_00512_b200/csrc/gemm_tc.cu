@@ -21,6 +21,7 @@
 //                  each chunk 64 K-rows of 128 B, 8-row groups (SBO = 1024)
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tc_common.cuh"
@@ -51,6 +52,10 @@ struct Sched {
     kb1 = min(kb_total, kb0 + kbps);
   }
 };
+
+template <int BN>
+__device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, int m, int nt,
+                                             int split, bool& bad);
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -171,8 +176,230 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_wait(tfull(acc), acc_phase);
       fence_after();
       const int m = mt * BM + row;
-      const bool mvalid = m < g.M;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      epilogue_row<BN>(g, taddr, m, nt, split, bad);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// --------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs on one TPC
+// computes a 256 x 256 tile with M = 256 MMAs issued by the even CTA.  Each
+// CTA stages its own 128 rows of A and half (128 columns) of B, so every
+// CTA moves 32 KB per 64-deep k-block instead of 48 KB for the same tensor
+// work (1/3 less L2->SM traffic) and fits a 6-deep pipeline.  Both CTAs'
+// TMA transactions complete on the even CTA's full barrier; its MMA commits
+// multicast to both CTAs' empty / tmem-full barriers; both epilogues drain
+// their own TMEM half (128 rows x 256 columns) and arrive remotely on the
+// even CTA's tmem-empty barrier.
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;   // 128 rows of A
+  static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 columns of B
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int TMEM_COLS = 512;         // 2 accumulator stages x 256 columns
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t bar, int c0, int c1) {
+  // completes on the even CTA's barrier (peer bit cleared), as CUTLASS's
+  // SM100_TMA_2SM_LOAD does
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_rank0(uint32_t bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(0));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                GemmDesc g, Sched sc) {
+  using C = Cfg2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
+  auto tfull = [&](int a) { return smem_u32(&bars[2 * C::STAGES + a]); };
+  auto tempty = [&](int a) { return smem_u32(&bars[2 * C::STAGES + 2 + a]); };
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        const int m0 = mt * 256 + (int)rank * 128;
+        const int n0 = nt * 256 + (int)rank * 128;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1);
+          const uint32_t a_s = sbase + stage * C::STAGE;
+          const uint32_t b_s = a_s + C::A_BYTES;
+          if (leader) mbar_expect_tx(full(stage), 2 * C::STAGE);
+          if (!A_MN) {
+            tma_load_2d_pair(a_s, &tmA, full(stage), kb * BK, m0);
+          } else {
+            tma_load_2d_pair(a_s, &tmA, full(stage), m0, kb * BK);
+            tma_load_2d_pair(a_s + 8192, &tmA, full(stage), m0 + 64, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(b_s, &tmB, full(stage), kb * BK, n0);
+          } else {
+            tma_load_2d_pair(b_s, &tmB, full(stage), n0, kb * BK);
+            tma_load_2d_pair(b_s + 8192, &tmB, full(stage), n0 + 64, kb * BK);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                 (static_cast<uint32_t>(A_MN) << 15) |
+                                 (static_cast<uint32_t>(B_MN) << 16) |
+                                 (static_cast<uint32_t>(256 >> 3) << 17) |
+                                 (static_cast<uint32_t>(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < total; u += npairs) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        mbar_wait(tempty(acc), acc_phase ^ 1);
+        fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(full(stage), phase);
+          fence_after();
+          const uint32_t a_s = sbase + stage * C::STAGE;
+          const uint32_t b_s = a_s + C::A_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            const uint64_t ad = A_MN ? make_desc(a_s + ks * 2048, 8192, 1024)
+                                     : make_desc(a_s + ks * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(b_s + ks * 2048, 8192, 1024)
+                                     : make_desc(b_s + ks * 32, 16, 1024);
+            mma_bf16_pair(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+          }
+          mma_commit_pair(empty(stage));
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(tfull(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int quarter = warp % 4;
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    bool bad = false;
+    for (int u = pair; u < total; u += npairs) {
+      int mt, nt, kb0, kb1;
+      sc.decode(u, mt, nt, kb0, kb1);
+      const int split = u % sc.k_splits;
+      mbar_wait(tfull(acc), acc_phase);
+      fence_after();
+      const int m = mt * 256 + (int)rank * 128 + row;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256;
+      epilogue_row<256>(g, taddr, m, nt, split, bad);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_rank0(tempty(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// Epilogue of one accumulator row (this thread's TMEM lane) of a 128 x BN
+// tile: fp32 store (+ clip / finite flag, split-K slice) or the logits
+// epilogue (online max / sum-exp over the tile's columns, target-logit
+// capture, optional bf16 logits).
+template <int BN>
+__device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, int m, int nt,
+                                             int split, bool& bad) {
+      const bool mvalid = m < g.M;
       if (!g.logits) {
         float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
 #pragma unroll 1
@@ -253,20 +480,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (thit) g.tgt_logit[m] = tval;
         }
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty(acc));
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
-    if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(C::TMEM_COLS));
-  }
 }
 
 // ------------------------------------------------------------------- host
@@ -326,6 +539,31 @@ void launch(const GemmDesc& g, cudaStream_t st) {
   DL_CUDA(cudaGetLastError());
 }
 
+template <bool A_MN, bool B_MN>
+void launch2(const GemmDesc& g, cudaStream_t st) {
+  using C = Cfg2;
+  auto kern = tc_gemm2_kernel<A_MN, B_MN>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  });
+  const CUtensorMap ta = A_MN ? make_map(g.A, g.K, g.M, g.lda, 64) : make_map(g.A, g.M, g.K, g.lda, BM);
+  const CUtensorMap tb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64) : make_map(g.B, g.N, g.K, g.ldb, 128);
+  Sched sc;
+  sc.m_tiles = (g.M + 255) / 256;
+  sc.n_tiles = (g.N + 255) / 256;
+  sc.kb_total = (g.K + BK - 1) / BK;
+  sc.k_splits = tc_splits(g.K, g.k_splits);
+  sc.kbps = (sc.kb_total + sc.k_splits - 1) / sc.k_splits;
+  DL_REQUIRE(sc.k_splits == std::max(1, g.k_splits), 1,
+             "tc gemm: k_splits not normalised with tc_splits()");
+  sc.raster = g.raster;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+  const int pairs = std::min(total, kNumSMs / 2);
+  kern<<<2 * pairs, kThreads, C::SMEM, st>>>(ta, tb, g, sc);
+  DL_CUDA(cudaGetLastError());
+}
+
 }  // namespace tc
 
 // Number of K slices actually produced for a requested split count: every
@@ -345,6 +583,17 @@ int tc_n_tiles(int N) {
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
   const int bn = g.N >= 256 ? 256 : (g.N >= 128 ? 128 : 64);
   const bool am = g.a_major == MN_MAJOR, bm = g.b_major == MN_MAJOR;
+  static const bool pair_ok = [] {
+    const char* e = std::getenv("DL_GEMM_2CTA");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (pair_ok && bn == 256 && g.M >= 256) {
+    if (!am && !bm) tc::launch2<false, false>(g, st);
+    else if (!am && bm) tc::launch2<false, true>(g, st);
+    else if (am && !bm) tc::launch2<true, false>(g, st);
+    else tc::launch2<true, true>(g, st);
+    return (g.N + 255) / 256;
+  }
 #define DL_TC_CASE(BN_)                                            \
   if (bn == BN_) {                                                 \
     if (!am && !bm) tc::launch<BN_, false, false>(g, st);          \
