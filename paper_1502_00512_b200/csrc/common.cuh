@@ -81,6 +81,7 @@ struct GemmDesc {
   const uint32_t* tgt;   // [M] target column per row
   float* tgt_logit;      // [M]
   int raster;            // 0: M-tiles fastest, 1: N-tiles fastest
+  int no_pair;           // 1: keep the single-CTA kernel (no cta_group::2 tiles)
 };
 
 // gemm_simt.cu

@@ -587,7 +587,7 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     const char* e = std::getenv("DL_GEMM_2CTA");
     return !(e && std::atoi(e) == 0);
   }();
-  if (pair_ok && bn == 256 && g.M >= 256) {
+  if (pair_ok && !g.no_pair && bn == 256 && g.M >= 256) {
     if (!am && !bm) tc::launch2<false, false>(g, st);
     else if (!am && bm) tc::launch2<false, true>(g, st);
     else if (am && !bm) tc::launch2<true, false>(g, st);
