@@ -29,7 +29,10 @@
 namespace dl {
 namespace tc {
 
-constexpr int kThreads = 192;
+// warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 epilogue: two warps
+// per TMEM lane quarter, each draining half of the tile's columns
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 template <int BN>
 struct Cfg {
@@ -55,7 +58,15 @@ struct Sched {
 
 template <int BN>
 __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, int m, int nt,
-                                             int split, bool& bad);
+                                             int split, bool& bad, int c0, int c1, int sub);
+
+// 2^x on the SFU (ex2.approx, flush-to-zero): the online-LSE epilogue's
+// exponentials never need the denormal range
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -76,7 +87,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (threadIdx.x == 32) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -164,7 +175,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else {
     // ---------------- epilogue (warps 2..5)
-    const int quarter = warp % 4;
+    const int quarter = warp % 4, half = (warp - 2) / 4;
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -177,7 +188,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       fence_after();
       const int m = mt * BM + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      epilogue_row<BN>(g, taddr, m, nt, split, bad);
+      epilogue_row<BN>(g, taddr, m, nt, split, bad, half * (BN / 64), (half + 1) * (BN / 64),
+                       2 * nt + half);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(acc));
@@ -274,7 +286,7 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
   if (threadIdx.x == 32) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 8); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 2 * kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -361,7 +373,7 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else {
-    const int quarter = warp % 4;
+    const int quarter = warp % 4, half = (warp - 2) / 4;
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -374,7 +386,7 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       fence_after();
       const int m = mt * 256 + (int)rank * 128 + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256;
-      epilogue_row<256>(g, taddr, m, nt, split, bad);
+      epilogue_row<256>(g, taddr, m, nt, split, bad, half * 4, half * 4 + 4, 2 * nt + half);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_rank0(tempty(acc));
@@ -398,12 +410,12 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // capture, optional bf16 logits).
 template <int BN>
 __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, int m, int nt,
-                                             int split, bool& bad) {
+                                             int split, bool& bad, int c0, int c1, int sub) {
       const bool mvalid = m < g.M;
       if (!g.logits) {
         float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = c0; c < c1; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           const int n0 = nt * BN + c * 32;
@@ -433,25 +445,41 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
         const int tg = mvalid ? static_cast<int>(g.tgt[m]) : -1;
         bf16* Srow = g.S ? g.S + static_cast<int64_t>(m) * g.lds : nullptr;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = c0; c < c1; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           const int n0 = nt * BN + c * 32;
           float cmax = -INFINITY;
+          const bool whole = n0 + 32 <= g.N;
+          if (whole) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const bool ok = n0 + j < g.N;
-            if (ok) cmax = fmaxf(cmax, v[j]);
-            if (n0 + j == tg) { tval = v[j]; thit = true; }
+            for (int j = 0; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < g.N) cmax = fmaxf(cmax, v[j]);
+          }
+          if (static_cast<unsigned>(tg - n0) < 32u) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j == tg) tval = v[j];
+            thit = true;
           }
           if (cmax > mrun) {
-            srun *= exp2f((mrun - cmax) * kLog2e);
+            srun *= fast_exp2((mrun - cmax) * kLog2e);
             mrun = cmax;
           }
           const float mb = mrun * kLog2e;
+          float part_sum = 0.f;
+          if (whole) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (n0 + j < g.N) srun += exp2f(fmaf(v[j], kLog2e, -mb));
+            for (int j = 0; j < 32; ++j) part_sum += fast_exp2(fmaf(v[j], kLog2e, -mb));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < g.N) part_sum += fast_exp2(fmaf(v[j], kLog2e, -mb));
+          }
+          srun += part_sum;
           if (Srow && mvalid) {
             if (n0 + 32 <= g.N && (g.lds % 8) == 0) {
               uint4* dst = reinterpret_cast<uint4*>(Srow + n0);
@@ -476,7 +504,7 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
           }
         }
         if (mvalid) {
-          g.part[static_cast<int64_t>(nt) * g.M + m] = make_float2(mrun, srun);
+          g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(mrun, srun);
           if (thit) g.tgt_logit[m] = tval;
         }
       }
@@ -575,9 +603,11 @@ int tc_splits(int K, int desired) {
   return (kb_total + kbps - 1) / kbps;
 }
 
+// Number of (max, sum-exp) partials per row the logits epilogue writes: one
+// per half N-tile (two epilogue warps per TMEM lane quarter).
 int tc_n_tiles(int N) {
   const int bn = N >= 256 ? 256 : (N >= 128 ? 128 : 64);
-  return (N + bn - 1) / bn;
+  return 2 * ((N + bn - 1) / bn);
 }
 
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
