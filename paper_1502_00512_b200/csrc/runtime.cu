@@ -119,7 +119,7 @@ struct dl_ctx {
   // DL_FORK_OUT=1: run the dense W_out update concurrently with the dh GEMM
   // (measured neutral on B200: both contend for L2/HBM bandwidth)
   bool fork_out = false;
-  bool logits_pair = false;  // DL_LOGITS_2CTA=1: CTA-pair tiles for the logits GEMM too
+  bool logits_pair = true;  // DL_LOGITS_2CTA=0: single-CTA tiles for the logits GEMM
 
   // DP
   ncclComm_t comm = nullptr;
@@ -352,8 +352,8 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     g.tgt = tgt;
     g.tgt_logit = c->tgt_logit;
     g.raster = 0;
-    // measured: the epilogue-heavy logits GEMM is faster on single-CTA tiles
-    // (0.42 vs 0.45 ms at C3); dh / dW_out gain 6-11% from CTA pairs
+    // with the 8-warp epilogue the logits GEMM gains most from CTA pairs
+    // (C3: 0.352 vs 0.404 ms single-CTA)
     g.no_pair = c->logits_pair ? 0 : 1;
     {
       Phase p(c, "logits");

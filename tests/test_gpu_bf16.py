@@ -92,8 +92,21 @@ def test_bf16_training_ppl_within_one_percent_of_reference(orc):
     trainer."""
     import paper_1502_00512_b200 as dl
     V, H = 2000, 128
-    tr, va = orc.random_stream_pair(555, V, 24016, 4000)
-    tr = tr[:24000]
+    # a learnable corpus (sparse bigram chain with sentence markers) so the
+    # comparison measures trained models rather than noise around ln V
+    rng = np.random.default_rng(555)
+    succ = rng.integers(3, V, (V, 4))
+    ids = [1]
+    w = 3
+    while len(ids) < 28100:
+        if rng.random() < 0.1:
+            ids += [2, 1]
+            w = int(rng.integers(3, V))
+        else:
+            w = int(succ[w, rng.integers(0, 4)])
+        ids.append(w)
+    ids = np.array(ids, np.uint32)
+    tr, va = ids[:24000], ids[24000:28000]
     params = orc.init_uniform(V, H, 1)
     kw = dict(nstate=H, noffset=16, minibatch=8, unroll=8, eta=0.05, max_epochs=1, mode=1)
     want = orc.train(oracle.TrainConfig(**kw), params, tr, va)
