@@ -82,6 +82,11 @@ struct GemmDesc {
   float* tgt_logit;      // [M]
   int raster;            // 0: M-tiles fastest, 1: N-tiles fastest
   int no_pair;           // 1: keep the single-CTA kernel (no cta_group::2 tiles)
+  // bf16 gradient epilogue (dW_out in throughput mode): clipped values to Cb
+  // (ld = ldc) and per-(half N tile, row) sums of squares to rowsq
+  // [2*n_tiles][M] (double), for the dense rmsprop's mean_sq
+  bf16* Cb;
+  double* rowsq;
 };
 
 // gemm_simt.cu

@@ -412,7 +412,47 @@ template <int BN>
 __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, int m, int nt,
                                              int split, bool& bad, int c0, int c1, int sub) {
       const bool mvalid = m < g.M;
-      if (!g.logits) {
+      if (!g.logits && g.Cb) {
+        // bf16 gradient rows + per-(half tile, row) partial sum of squares of
+        // the clipped fp32 values (the dense rmsprop's mean_sq, rmsprop.hpp:100)
+        bf16* Brow = g.Cb + static_cast<int64_t>(m) * g.ldc;
+        double sq = 0.0;
+#pragma unroll 1
+        for (int c = c0; c < c1; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const int n0 = nt * BN + c * 32;
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = clip1(v[j], g.clip);
+            if (n0 + j < g.N) s = fmaf(v[j], v[j], s);
+          }
+          sq += (double)s;
+          if (!mvalid) continue;
+          if (n0 + 32 <= g.N && (g.ldc % 8) == 0) {
+            uint4* dst = reinterpret_cast<uint4*>(Brow + n0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 q;
+              __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * j + 0], v[8 * j + 1]);
+              __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+              __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+              q.x = *reinterpret_cast<uint32_t*>(&p0);
+              q.y = *reinterpret_cast<uint32_t*>(&p1);
+              q.z = *reinterpret_cast<uint32_t*>(&p2);
+              q.w = *reinterpret_cast<uint32_t*>(&p3);
+              dst[j] = q;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < g.N) Brow[n0 + j] = __float2bfloat16_rn(v[j]);
+          }
+        }
+        if (mvalid) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
+      } else if (!g.logits) {
         float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
 #pragma unroll 1
         for (int c = c0; c < c1; ++c) {

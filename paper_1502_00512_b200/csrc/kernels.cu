@@ -604,6 +604,56 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
   }
 }
 
+// Dense W_out rmsprop (rmsprop.hpp:94-107) from the bf16 gradient the dW_out
+// GEMM epilogue wrote, with mean_sq assembled from its per-(half tile, row)
+// partial sums of squares (fixed order): one pass over the row, 12 B/elem
+// (g 2, w 4+4, shadow 2).  One warp per row.
+__global__ void __launch_bounds__(256)
+k_rms_dense_g16(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                const bf16* __restrict__ g, const double* __restrict__ rowsq, int nsub,
+                int64_t V, int64_t H, double rho, double eps, double eta) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp0; r < V; r += nwarps) {
+    double s = 0.0;
+    for (int k = 0; k < nsub; ++k) s += rowsq[(int64_t)k * V + r];
+    const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
+    const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
+    const uint4* g8 = reinterpret_cast<const uint4*>(g + r * H);
+    float4* w4 = reinterpret_cast<float4*>(w + r * H);
+    uint4* b8 = reinterpret_cast<uint4*>(wb + r * H);
+#pragma unroll 2
+    for (int64_t j = lane; j < H / 8; j += 32) {
+      const uint4 q = __ldcs(g8 + j);
+      float4 o0 = w4[2 * j], o1 = w4[2 * j + 1];
+      const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+      const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
+      const float2 c = __bfloat1622float2(q2[2]), d = __bfloat1622float2(q2[3]);
+      o0.x -= rms_step(eta, a.x, denom, inv);
+      o0.y -= rms_step(eta, a.y, denom, inv);
+      o0.z -= rms_step(eta, b.x, denom, inv);
+      o0.w -= rms_step(eta, b.y, denom, inv);
+      o1.x -= rms_step(eta, c.x, denom, inv);
+      o1.y -= rms_step(eta, c.y, denom, inv);
+      o1.z -= rms_step(eta, d.x, denom, inv);
+      o1.w -= rms_step(eta, d.y, denom, inv);
+      w4[2 * j] = o0;
+      w4[2 * j + 1] = o1;
+      uint4 ob;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(o0.x, o0.y), p1 = __floats2bfloat162_rn(o0.z, o0.w);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(o1.x, o1.y), p3 = __floats2bfloat162_rn(o1.z, o1.w);
+      ob.x = *reinterpret_cast<uint32_t*>(&p0);
+      ob.y = *reinterpret_cast<uint32_t*>(&p1);
+      ob.z = *reinterpret_cast<uint32_t*>(&p2);
+      ob.w = *reinterpret_cast<uint32_t*>(&p3);
+      b8[j] = ob;
+    }
+    if (lane == 0) m[r] = mw;
+  }
+}
+
 __global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long long* skipped) {
   if (*nonfinite) skipped[0] += 1ull;
 }
@@ -794,6 +844,11 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
 }
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st) {
   k_count_skip<<<1, 1, 0, st>>>(nonfinite, skipped);
+}
+void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
+                   int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>((V * 32 + 255) / 256, 148 * 8);
+  k_rms_dense_g16<<<blocks, 256, 0, st>>>(w, wb, m, g, rowsq, nsub, V, H, rho, eps, eta);
 }
 void accum_loss(double* acc, const double* v, unsigned long long* cnt,
                 const unsigned long long* vc, cudaStream_t st) {

@@ -42,6 +42,10 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st);
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st);
+// dense W_out rmsprop from bf16 gradients + per-(half tile, row) sums of
+// squares [nsub][V] (H % 8 == 0)
+void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
+                   int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st);
 
 // rec_tc.cu: one recurrence step, tcgen05 + split-K cluster/DSMEM reduction.
 // mode 0: out = act(A . W_rec^T + W_in[x]); mode 1: out = (A . W_rec +

@@ -68,6 +68,12 @@ struct dl_ctx {
   int* g_in_n = nullptr;
   int* nonfinite = nullptr;
   bool have_grads = false;
+  // bf16 mode: dW_out as bf16 + row sums of squares from the GEMM epilogue
+  // (DL_G16=0 keeps the fp32 gradient); g16_valid = the last window used it
+  bf16* g_out_bf = nullptr;
+  double* rowsq = nullptr;
+  int rowsq_n = 0;
+  bool g16 = true, g16_valid = false;
   cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
@@ -434,6 +440,14 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     g.do_clip = dp ? 0 : 1;
     g.clip = clip;
     g.nonfinite = c->nonfinite;
+    // throughput mode: bf16 clipped dW_out + row sums of squares (halves the
+    // gradient's HBM traffic); needs a finite clip (no non-finite check) and
+    // no allreduce between the GEMM and the update
+    c->g16_valid = tc(c) && c->g16 && !dp && std::isfinite(clip);
+    if (c->g16_valid) {
+      g.Cb = c->g_out_bf;
+      g.rowsq = c->rowsq;
+    }
     gemm(c, g);
   }
   if (dp) {
@@ -463,8 +477,12 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       b = ev_get(c);
       DL_CUDA(cudaEventRecord(a, c->st2));
     }
-    rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, V, H, c->rho,
-             c->eps, fork_out_eta, 1, nullptr, c->st2);
+    if (c->g16_valid)
+      rms_dense_g16(c->w_out, c->w_out_bf_next, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, V, H,
+                    c->rho, c->eps, fork_out_eta, c->st2);
+    else
+      rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, V, H, c->rho,
+               c->eps, fork_out_eta, 1, nullptr, c->st2);
     c->launches++;
     if (c->profiling) {
       DL_CUDA(cudaEventRecord(b, c->st2));
@@ -581,7 +599,10 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
-  if (!skip_out)
+  if (!skip_out && c->g16_valid)
+    rms_dense_g16(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, c->V, c->H,
+                  c->rho, c->eps, eta, st);
+  else if (!skip_out)
     rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->V,
              c->H, c->rho, c->eps, eta, 1, c->nonfinite, st);
   count_skip(c->nonfinite, c->d_skipped, st);
@@ -615,6 +636,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_REC_CLUSTER")) c->rec_cluster = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_FORK_OUT")) c->fork_out = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_LOGITS_2CTA")) c->logits_pair = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_G16")) c->g16 = std::atoi(e) != 0;
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
@@ -653,6 +675,9 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
       c->w_rec_bf = dalloc<bf16>(H * H);
       c->w_out_bf = dalloc<bf16>(V * H);
       c->w_out_bf_next = dalloc<bf16>(V * H);
+      c->g_out_bf = dalloc<bf16>(V * H);
+      c->rowsq_n = tc_n_tiles((int)H);
+      c->rowsq = dalloc<double>((size_t)c->rowsq_n * V);
     }
     DL_CUDA(cudaMemsetAsync(c->w_in, 0, V * H * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->w_rec, 0, H * H * 4, c->st));
@@ -686,7 +711,8 @@ int dl_destroy(dl_ctx* c) {
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
-                  c->win_loss, c->x_all, c->dpre_all, c->bar_counter};
+                  c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
+                  c->rowsq};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -799,7 +825,19 @@ int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
       cudaFree(dense);
     }
     if (g_rec) DL_CUDA(cudaMemcpyAsync(g_rec, c->g_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
-    if (g_out) DL_CUDA(cudaMemcpyAsync(g_out, c->g_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (g_out && c->g16_valid) {
+      // bf16 gradient of the throughput path, widened on the host
+      std::vector<uint16_t> tmp((size_t)(c->V * c->H));
+      DL_CUDA(cudaMemcpyAsync(tmp.data(), c->g_out_bf, tmp.size() * 2, cudaMemcpyDeviceToHost,
+                              c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      for (size_t i = 0; i < tmp.size(); ++i) {
+        const uint32_t u = (uint32_t)tmp[i] << 16;
+        std::memcpy(&g_out[i], &u, 4);
+      }
+    } else if (g_out) {
+      DL_CUDA(cudaMemcpyAsync(g_out, c->g_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    }
     DL_CUDA(cudaStreamSynchronize(c->st));
   });
 }
@@ -833,6 +871,7 @@ int dl_set_grads(dl_ctx* c, int64_t n_in_rows, const uint32_t* in_words, const f
     DL_CUDA(cudaMemcpyAsync(c->nonfinite, &bad, 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
     c->have_grads = true;
+    c->g16_valid = false;  // injected gradients are fp32
   });
 }
 
