@@ -58,6 +58,12 @@ int dl_set_params(dl_ctx* ctx, const float* w_in, const float* w_rec,
                   const float* w_out);
 int dl_get_params(dl_ctx* ctx, float* w_in, float* w_rec, float* w_out);
 
+/* Host-only: RnnParams<float>::init_uniform (rnn.hpp:79-83) -- one
+ * std::mt19937_64(seed) drawn over w_in, w_rec, w_out in order, uniform in
+ * [-range, range) exactly as rng.hpp:37-44; bit-identical to the reference. */
+int dl_init_uniform(int64_t V, int64_t H, uint64_t seed, double range,
+                    float* w_in, float* w_rec, float* w_out);
+
 /* RmspropState (rmsprop.hpp:37-59): m_rec H x H, m_in V, m_out V. */
 int dl_set_opt(dl_ctx* ctx, const float* m_rec, const float* m_in,
                const float* m_out, double rho, double eps);

@@ -183,6 +183,17 @@ class GpuRnn:
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
 
 
+def init_uniform(V: int, H: int, seed: int, init_range: float = 0.1):
+    """RnnParams<float>::init_uniform (rnn.hpp:79-83), bit-identical (host
+    C-ABI call, std::mt19937_64).  Returns (w_in, w_rec, w_out)."""
+    w_in = np.empty((V, H), np.float32)
+    w_rec = np.empty((H, H), np.float32)
+    w_out = np.empty((V, H), np.float32)
+    check(load().dl_init_uniform(V, H, seed, init_range, w_in.ctypes.data, w_rec.ctypes.data,
+                                 w_out.ctypes.data))
+    return w_in, w_rec, w_out
+
+
 def rank_cursors(L: int, noffset: int, minibatch: int, nranks: int = 1, rank: int = 0):
     """This rank's initial stream cursors (host-only C-ABI call): the
     reference's floor(i*L/N) (trainer.hpp:194-195) over global streams

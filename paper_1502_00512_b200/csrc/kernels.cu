@@ -415,17 +415,23 @@ __global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
     const int a = seg_start[slot], e = seg_start[slot + 1];
     for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < H;
          j += (int64_t)gridDim.y * blockDim.x) {
-      // frequent words (bos/eos) own long segments: issue 8 independent
-      // loads per batch, then add them in the reference's order
       float acc = 0.f;
-      for (int i = a; i < e; i += 32) {
-        float v[32];
+      if (e - a <= 2) {
+        // most words occur once or twice per window
+        acc += 1.0f * dpre[(int64_t)order_pos[a] * H + j];
+        if (e - a == 2) acc += 1.0f * dpre[(int64_t)order_pos[a + 1] * H + j];
+      } else {
+        // frequent words (bos/eos) own long segments: issue 16 independent
+        // loads per batch, then add them in the reference's order
+        for (int i = a; i < e; i += 16) {
+          float v[16];
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
-          v[u] = i + u < e ? dpre[(int64_t)order_pos[i + u] * H + j] : 0.f;
+          for (int u = 0; u < 16; ++u)
+            v[u] = i + u < e ? dpre[(int64_t)order_pos[i + u] * H + j] : 0.f;
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
-          if (i + u < e) acc += 1.0f * v[u];
+          for (int u = 0; u < 16; ++u)
+            if (i + u < e) acc += 1.0f * v[u];
+        }
       }
       acc = clip1(acc, clip);
       bad |= !isfinite(acc);

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -1017,6 +1018,25 @@ int dl_rnn_perplexity(dl_ctx* c, const uint32_t* ids, int64_t n, uint32_t bos,
   if (total_logprob) *total_logprob = tot;
   if (predicted) *predicted = pred;
   if (perplexity) *perplexity = std::exp(-tot / (double)pred);
+  return DL_OK;
+}
+
+// RnnParams::init_uniform (rnn.hpp:79-83): one std::mt19937_64(seed), w_in
+// then w_rec then w_out, each element float(lo + (hi - lo) * u) with
+// u = (rng() >> 11) * 2^-53 (rng.hpp:37-44).  Pure host code; bit-exact.
+int dl_init_uniform(int64_t V, int64_t H, uint64_t seed, double range, float* w_in,
+                    float* w_rec, float* w_out) {
+  if (V < 1 || H < 1) return fail(nullptr, DL_EINVAL, "RnnParams: V,H >= 1");
+  if (!w_in || !w_rec || !w_out) return fail(nullptr, DL_EINVAL, "dl_init_uniform: null output");
+  std::mt19937_64 rng(seed);
+  const double lo = -range, hi = range;
+  auto fill = [&](float* p, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+      p[i] = static_cast<float>(lo + (hi - lo) * (static_cast<double>(rng() >> 11) * 0x1.0p-53));
+  };
+  fill(w_in, V * H);
+  fill(w_rec, H * H);
+  fill(w_out, V * H);
   return DL_OK;
 }
 

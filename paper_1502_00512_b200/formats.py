@@ -63,6 +63,50 @@ def _str(s: str) -> bytes:
     return _u64(len(b)) + b
 
 
+# ------------------------------------------------- vocabulary / id streams
+SPECIALS = ("<unk>", "<s>", "</s>")  # ids 0, 1, 2 (corpus.hpp:54-74)
+
+
+def read_vocab(text: str):
+    """Vocabulary::read (corpus.hpp:96-104): one word per line (a trailing
+    CR is dropped); must start with <unk>, <s>, </s>."""
+    words = text.split("\n")
+    if words and words[-1] == "":
+        words.pop()
+    words = [w[:-1] if w.endswith("\r") else w for w in words]
+    if len(words) < 3 or tuple(words[:3]) != SPECIALS:
+        raise DataError("vocabulary must start with <unk>, <s>, </s>")
+    return words
+
+
+def write_vocab(words) -> str:
+    """Vocabulary::write (corpus.hpp:92-94)."""
+    return "".join(w + "\n" for w in words)
+
+
+def read_id_stream(text: str, vocab_size: int) -> np.ndarray:
+    """read_id_stream (corpus.hpp:264-279): whitespace-separated decimal ids,
+    each < vocab_size."""
+    out = []
+    line = 1
+    for tok in text.split():
+        try:
+            v = int(tok)
+            if v < 0:
+                raise ValueError
+        except ValueError:
+            raise DataError(f"id stream: not a number: {tok} (line {line})")
+        if v >= vocab_size:
+            raise DataError(f"id stream: id out of range: {tok}")
+        out.append(v)
+    return np.array(out, np.uint32)
+
+
+def write_id_stream(ids, eos_id: int = 2) -> str:
+    """write_id_stream (corpus.hpp:256-262): one sentence per line."""
+    return "".join(f"{int(i)}{chr(10) if int(i) == eos_id else ' '}" for i in ids)
+
+
 # ------------------------------------------------------------------ RNLM
 def write_params(params, vocab_words, act: int = 0) -> bytes:
     """rnn.hpp:263-285."""

@@ -89,3 +89,29 @@ def test_rng_text_matches_reference(ref):
         pcfg = TrainConfig(nstate=H, noffset=1, minibatch=1, unroll=2, seed=seed)
         st = formats.read_trainer(blob, pcfg, 1, H, len(tr))
         assert st["rng_text"] == formats.mt19937_64_text(seed)
+
+
+def test_init_uniform_is_bit_identical_to_reference():
+    """dl_init_uniform (host C ABI) vs the reference's init_uniform fixture."""
+    import paper_1502_00512_b200 as dl
+    g = np.load(os.path.join(GOLD, "kat.npz"))
+    got = np.concatenate([a.ravel()[:16] for a in dl.init_uniform(7, 5, 11)])
+    assert np.array_equal(got, g["init_11"])
+    t = np.load(os.path.join(GOLD, "train.npz"))
+    for a, b in zip(dl.init_uniform(30, 8, 3), (t["w_in"], t["w_rec"], t["w_out"])):
+        assert np.array_equal(a, b)
+
+
+def test_id_stream_and_vocab_text_formats():
+    words = make_vocab(6)
+    assert formats.read_vocab(formats.write_vocab(words)) == words
+    with pytest.raises(DataError):
+        formats.read_vocab("a\nb\nc\n")
+    ids = np.array([1, 4, 3, 2, 1, 5, 2], np.uint32)
+    text = formats.write_id_stream(ids)
+    assert text == "1 4 3 2\n1 5 2\n"
+    assert np.array_equal(formats.read_id_stream(text, 6), ids)
+    with pytest.raises(DataError):
+        formats.read_id_stream("1 9 2", 6)
+    with pytest.raises(DataError):
+        formats.read_id_stream("1 x 2", 6)
