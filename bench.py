@@ -44,7 +44,59 @@ CONFIGS = {
                desc="RNNLM hidden=1024, vocab=64K full softmax, 128 streams"),
     "c3": dict(V=64000, H=2048, T=16, B=128, noffset=8, L=1 << 25, seed=3001,
                desc="RNNLM hidden=2048, vocab=64K, 128 streams/GPU, data-parallel"),
+    # forward-only scoring (sharded_perplexity / n-best): a step = one
+    # lock-step scoring step over S streams
+    "c5": dict(V=64000, H=2048, T=1, B=1024, noffset=1, L=1 << 22, seed=5001, score=True,
+               desc="perplexity scoring forward pass, hidden=2048, vocab=64K, 1024 streams"),
 }
+
+
+def run_scoring(args, cfg):
+    """C5: sharded-perplexity scoring words/s (eval.hpp:151-222 lock-step walk
+    over S streams, exact softmax), device-timed on the library stream."""
+    import torch
+
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200._lib import load
+    V, H, S = cfg["V"], cfg["H"], cfg["B"]
+    ids = synthetic_stream(cfg["seed"], V, cfg["L"])
+    rng = np.random.default_rng(7)
+    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32) for s in ((V, H), (H, H), (V, H)))
+    model = dl.GpuRnn(V, H, 0, args.precision, 0)
+    model.set_params(*params)
+    steps = args.steps + args.warmup
+    n = len(ids) // S
+    begin = np.arange(S) * n
+    j = np.arange(steps)[:, None]
+    x = ids[begin[None, :] + j].astype(np.uint32)
+    y = ids[begin[None, :] + j + 1].astype(np.int64)
+    t = np.where(y == 1, -1, y)
+    stream = torch.cuda.ExternalStream(load().dl_cuda_stream(model.handle))
+    dl.score(model, x[: args.warmup], t[: args.warmup])  # warm-up (tile setup)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        lp, tot, pred, _ = dl.score(model, x[args.warmup:], t[args.warmup:])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.25)
+    ms = e0.elapsed_time(e1)
+    words = S * args.steps
+    value = words / (ms / 1000.0)
+    fpw = 2 * H * V + 2 * H * H
+    peak = PEAKS["bf16_tflops_sustained"]
+    print(json.dumps({
+        "metric": "scoring words/sec", "value": value, "unit": "words/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": "c5", "desc": cfg["desc"], "V": V, "H": H, "streams": S},
+        "flops_per_word": fpw, "mean_logprob": tot / max(pred, 1),
+        "clocks": clk.summary(),
+        "roofline": {"bound": "tensor", "kernel": "whole scoring step", "unit": "TFLOP/s",
+                     "achieved": value * fpw / 1e12, "peak": peak,
+                     "frac": value * fpw / 1e12 / peak, "traffic": None}}), flush=True)
 
 
 def synthetic_stream(seed: int, V: int, L: int) -> np.ndarray:
@@ -136,6 +188,28 @@ def run_reference(args, cfg):
         ref = oracle.Orc()
         kind = "port"
     V, H, T = cfg["V"], cfg["H"], cfg["T"]
+    if cfg.get("score"):
+        # sharded_perplexity over S = 64 slices of a short stream (a bounded
+        # sample of the 1024-stream scoring workload)
+        ids = synthetic_stream(cfg["seed"], V, 64 * 4 + 1)
+        rng = np.random.default_rng(1)
+        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                       for s in ((V, H), (H, H), (V, H)))
+        t0 = time.perf_counter()
+        r = ref.sharded_ppl(params, 0, ids, 64)
+        dt = time.perf_counter() - t0
+        value = 64 * 3 / dt
+        print(json.dumps({
+            "metric": "scoring words/sec", "value": value, "unit": "words/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": 3, "warmup": 0,
+            "ms_per_step": 1000 * dt / 3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (f64 accumulate)", "data": "synthetic",
+            "config": {"workload": "c5", "V": V, "H": H},
+            "cpu_baseline": {"value": value, "unit": "words/s", "cores": cores, "kind": kind,
+                             "sample": "sharded_perplexity, 64 slices x 3 steps, threads=1"},
+            "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
     Bs = min(cfg["B"], args.ref_streams)
     Ts = min(T, args.ref_unroll)
     ids = synthetic_stream(cfg["seed"], V, 1 << 16)
@@ -192,6 +266,9 @@ def main():
     cfg = dict(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         run_reference(args, cfg)
+        return
+    if cfg.get("score"):
+        run_scoring(args, cfg)
         return
 
     import torch
