@@ -157,6 +157,14 @@ int dl_trainer_set_state(dl_ctx* ctx, const int64_t* cursors,
 int dl_comm_unique_id(uint8_t id[128]);
 int dl_comm_init(dl_ctx* ctx, const uint8_t id[128], int nranks, int rank);
 
+/* In-process rank groups: G contexts on ONE device act as G ranks (one host
+ * thread per context, collectives through device memory with a host
+ * barrier) so the multi-rank paths can be exercised on a single GPU.  Same
+ * semantics as dl_comm_init otherwise. */
+int dl_local_group_create(int G, void** group);
+int dl_local_group_destroy(void* group);
+int dl_comm_init_local(dl_ctx* ctx, void* group, int rank);
+
 /* ---- instrumentation ----------------------------------------------------- */
 
 /* Test hook for the GEMM engine behind every matmul_* of mat.hpp:116-184:

@@ -178,6 +178,11 @@ class GpuRnn:
         hid = np.ascontiguousarray(hidden, np.float32)
         self._chk(load().dl_trainer_set_state(self._h, cur.ctypes.data, hid.ctypes.data))
 
+    def comm_init_local(self, group: "LocalGroup", rank: int):
+        """Join an in-process rank group (single-device multi-rank runs)."""
+        self._chk(load().dl_comm_init_local(self._h, group.handle, rank))
+        self._group = group  # keep the group alive as long as the model
+
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
@@ -201,6 +206,25 @@ def rank_cursors(L: int, noffset: int, minibatch: int, nranks: int = 1, rank: in
     out = np.empty(noffset * minibatch, np.int64)
     check(load().dl_rank_cursors(L, noffset, minibatch, nranks, rank, out.ctypes.data))
     return out
+
+
+class LocalGroup:
+    """G contexts on one device acting as G ranks (dl_local_group_create);
+    drive each rank's calls from its own thread (collectives synchronise the
+    host threads)."""
+
+    def __init__(self, G: int):
+        h = C.c_void_p()
+        check(load().dl_local_group_create(G, C.byref(h)))
+        self.handle, self.G = h, G
+
+    def __del__(self):
+        try:
+            if self.handle:
+                load().dl_local_group_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
 
 def comm_unique_id() -> bytes:
@@ -495,7 +519,10 @@ class Trainer:
         if L < N:
             raise ValueError("trainer: training stream shorter than the stream count")
         self.model = GpuRnn(V, H, cfg.act, precision, device)
-        if comm is not None:
+        # comm: (nccl_unique_id, nranks, rank) or (LocalGroup, nranks, rank)
+        if comm is not None and isinstance(comm[0], LocalGroup):
+            self.model.comm_init_local(comm[0], comm[2])
+        elif comm is not None:
             self.model.comm_init(comm[0], comm[1], comm[2])
         self.model.set_params(w_in, w_rec, w_out)
         self.model.set_opt(None, None, None, cfg.rho, cfg.eps)

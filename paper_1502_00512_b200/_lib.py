@@ -19,7 +19,8 @@ EXPORTS = (
     "dl_trainer_init", "dl_trainer_run", "dl_trainer_get_state",
     "dl_trainer_set_state", "dl_comm_unique_id", "dl_comm_init",
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
-    "dl_test_embed", "dl_rank_cursors", "dl_init_uniform",
+    "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
+    "dl_local_group_destroy", "dl_comm_init_local",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -79,6 +80,9 @@ def load():
         "dl_test_embed": (C.c_int, [vp, C.c_int, i64, i64, vp, vp, C.c_float, vp]),
         "dl_rank_cursors": (C.c_int, [i64, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
         "dl_init_uniform": (C.c_int, [i64, i64, u64, C.c_double, vp, vp, vp]),
+        "dl_local_group_create": (C.c_int, [C.c_int, P(vp)]),
+        "dl_local_group_destroy": (C.c_int, [vp]),
+        "dl_comm_init_local": (C.c_int, [vp, vp, C.c_int]),
         "dl_launch_count": (u64, [vp]),
         "dl_cuda_stream": (vp, [vp]),
         "dl_set_profiling": (C.c_int, [vp, C.c_int]),

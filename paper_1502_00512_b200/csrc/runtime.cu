@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/desklm_cuda.h"
+#include "comm.cuh"
 #include "kernels.cuh"
 
 using namespace dl;
@@ -129,7 +130,7 @@ struct dl_ctx {
   bool logits_pair = true;  // DL_LOGITS_2CTA=0: single-CTA tiles for the logits GEMM
 
   // DP
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;  // NcclComm (production) or LocalComm (single-device tests)
   int nranks = 1, rank = 0;
   uint32_t* x_all = nullptr;  // [G][T][B] gathered window ids
   float* dpre_all = nullptr;  // [G][T][B][H] gathered dpre
@@ -419,8 +420,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // the window's loss is the sum over all ranks' streams
     DL_CUDA(cudaMemsetAsync(c->win_loss, 0, 16, st));
     sum_rows(c->loss_row, c->w_d, TB, c->win_loss, c->win_pos, st);
-    nccl_check(ncclAllReduce(c->win_loss, c->win_loss, 1, ncclDouble, ncclSum, c->comm, st));
-    nccl_check(ncclAllReduce(c->win_pos, c->win_pos, 1, ncclUint64, ncclSum, c->comm, st));
+    c->comm->allreduce_sum(c->win_loss, 1, DType::F64, st);
+    c->comm->allreduce_sum(c->win_pos, 1, DType::U64, st);
     accum_loss(c->d_loss, c->win_loss, c->d_pos, c->win_pos, st);
     c->launches += 2;
   } else {
@@ -457,8 +458,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // recurrence; joined before the update
     DL_CUDA(cudaEventRecord(c->ev_fork, st));
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    nccl_check(ncclAllReduce(c->g_out, c->g_out, (size_t)(V * H), ncclFloat, ncclSum, c->comm,
-                             c->st2));
+    c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
     reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
     c->launches++;
   }
@@ -568,11 +568,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     const int G = c->nranks;
     DL_CUDA(cudaEventRecord(c->ev_fork, st));
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    nccl_check(ncclAllReduce(c->g_rec, c->g_rec, (size_t)(H * H), ncclFloat, ncclSum, c->comm,
-                             c->st2));
+    c->comm->allreduce_sum(c->g_rec, (size_t)(H * H), DType::F32, c->st2);
     reduce_splits(c->g_rec, 1, 0, H * H, c->g_rec, clip, 1, c->nonfinite, c->st2);
-    nccl_check(ncclAllGather(c->x_d, c->x_all, (size_t)TB, ncclUint32, c->comm, c->st2));
-    nccl_check(ncclAllGather(c->dpre, c->dpre_all, (size_t)(TB * H), ncclFloat, c->comm, c->st2));
+    c->comm->allgather(c->x_d, c->x_all, (size_t)TB, DType::U32, c->st2);
+    c->comm->allgather(c->dpre, c->dpre_all, (size_t)(TB * H), DType::F32, c->st2);
     DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
     DL_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
     c->launches++;
@@ -705,7 +704,7 @@ int dl_destroy(dl_ctx* c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
-  if (c->comm) ncclCommDestroy(c->comm);
+  delete c->comm;
   void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->w_out_bf_next, c->m_rec, c->m_in,
                   c->m_out, c->g_rec, c->g_out, c->g_in_rows, c->g_in_words, c->g_in_n,
                   c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
@@ -1235,11 +1234,38 @@ int dl_comm_init(dl_ctx* c, const uint8_t id[128], int nranks, int rank) {
     c->rank = rank;
     c->capT = c->capB = 0;  // window buffers are re-sized for the gathered window
     drop_graphs(c);
+    delete c->comm;
+    c->comm = nullptr;
     if (nranks == 1) return;
-    ncclUniqueId u;
-    std::memcpy(&u, id, 128);
-    DL_REQUIRE(ncclCommInitRank(&c->comm, nranks, u, rank) == ncclSuccess, DL_EDEVICE,
-               "ncclCommInitRank failed");
+    c->comm = new NcclComm(id, nranks, rank);
+  });
+}
+
+// In-process groups: G contexts on one device behave as G ranks (one host
+// thread per context).  Used to run the multi-rank code paths -- data
+// parallel and vocabulary sharded -- on a single GPU.
+int dl_local_group_create(int G, void** group) {
+  if (G < 1 || G > 16 || !group) return fail(nullptr, DL_EINVAL, "dl_local_group_create: 1..16");
+  *group = new LocalGroup(G);
+  return DL_OK;
+}
+
+int dl_local_group_destroy(void* group) {
+  delete static_cast<LocalGroup*>(group);
+  return DL_OK;
+}
+
+int dl_comm_init_local(dl_ctx* c, void* group, int rank) {
+  if (!c || !group) return fail(c, DL_EINVAL, "dl_comm_init_local: null argument");
+  LocalGroup* g = static_cast<LocalGroup*>(group);
+  if (rank < 0 || rank >= g->G) return fail(c, DL_EINVAL, "dl_comm_init_local: bad rank");
+  return guarded(c, [&] {
+    c->nranks = g->G;
+    c->rank = rank;
+    c->capT = c->capB = 0;
+    drop_graphs(c);
+    delete c->comm;
+    c->comm = g->G > 1 ? new LocalComm(g, rank) : nullptr;
   });
 }
 

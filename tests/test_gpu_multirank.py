@@ -1,0 +1,104 @@
+"""The multi-rank code paths run on ONE GPU: G contexts in one process form
+an in-process rank group (dl_local_group_create / dl_comm_init_local, the
+same collective interface the NCCL path implements), one host thread per
+rank.  Data parallel: every rank trains its slice of the
+global minibatch; gradients are summed before clip + rmsprop, so replicas
+must stay bit-identical and equal a single context training the whole
+global minibatch (to fp32 summation-order tolerance)."""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def close(a, b, rel=1e-4):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.all(np.abs(a - b) <= rel * np.abs(b) + 1e-4 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("G,precision", [(2, "fp32"), (4, "fp32"), (2, "bf16")])
+def test_dp_window_matches_global_window(orc, G, precision):
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 512, 64, 6, 8
+    Bg = G * B
+    rng = np.random.default_rng(G)
+    params = orc.init_uniform(V, H, 21)
+    x = rng.integers(0, V, (T, Bg)).astype(np.uint32)
+    y = rng.integers(2, V, (T, Bg)).astype(np.uint32)
+    w = (rng.random((T, Bg)) > 0.1).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (Bg, H)).astype(np.float32)
+    scale = 1.0 / (Bg * T)
+    single = dl.GpuRnn(V, H, 0, precision)
+    single.set_params(*params)
+    r1, hf1 = dl.bptt_run(single, dl.WindowBatch(x, y, w), h0, scale, 1.0)
+    assert dl.rmsprop_update(single, 0.05)
+    want = single.params() + single.opt()
+
+    group = dl.LocalGroup(G)
+    ranks = []
+    for r in range(G):
+        m = dl.GpuRnn(V, H, 0, precision)
+        m.comm_init_local(group, r)
+        m.set_params(*params)
+        ranks.append(m)
+
+    def run(r):
+        sl = slice(r * B, (r + 1) * B)
+        wb = dl.WindowBatch(np.ascontiguousarray(x[:, sl]), np.ascontiguousarray(y[:, sl]),
+                            np.ascontiguousarray(w[:, sl]))
+        res, hf = dl.bptt_run(ranks[r], wb, np.ascontiguousarray(h0[sl]), scale, 1.0)
+        ok = dl.rmsprop_update(ranks[r], 0.05)
+        return res, hf, ok
+
+    with ThreadPoolExecutor(G) as ex:
+        outs = list(ex.map(run, range(G)))
+    for r, (res, hf, ok) in enumerate(outs):
+        assert ok
+        assert res.loss == pytest.approx(r1.loss, rel=1e-6)  # global (allreduced) loss
+        assert res.positions == r1.positions
+        assert np.allclose(hf, hf1[r * B:(r + 1) * B], atol=1e-6 if precision == "fp32" else 2e-2)
+    got = [m.params() + m.opt() for m in ranks]
+    for r in range(1, G):  # replicas are bit-identical
+        for a, b in zip(got[0], got[r]):
+            assert np.array_equal(a, b)
+    if precision == "fp32":
+        for a, b in zip(got[0], want):
+            assert close(a, b)
+
+
+def test_dp_trainer_matches_global_minibatch(orc):
+    """Two ranks x minibatch 4 == one trainer with minibatch 8 (same
+    schedule: rank r owns streams g*8 + r*4 + b)."""
+    import paper_1502_00512_b200 as dl
+    V, H, G = 80, 32, 2
+    tr, va = orc.random_stream_pair(17, V, 4016, 600)
+    tr = tr[:4000]
+    params = orc.init_uniform(V, H, 9)
+    kw = dict(nstate=H, noffset=3, unroll=5, eta=0.02, max_epochs=2, mode=1)
+    single = dl.Trainer(dl.TrainConfig(minibatch=G * 4, **kw), params, dl.make_vocab(V), tr, va,
+                        "fp32")
+    single.train()
+    group = dl.LocalGroup(G)
+    trainers = [dl.Trainer(dl.TrainConfig(minibatch=4, **kw), params, dl.make_vocab(V), tr, va,
+                           "fp32", comm=(group, G, r)) for r in range(G)]
+    with ThreadPoolExecutor(G) as ex:
+        list(ex.map(lambda t: t.train(), trainers))
+    for t in trainers:
+        assert len(t.logs) == len(single.logs)
+        for a, b in zip(t.logs, single.logs):
+            assert a.train_loss == pytest.approx(b.train_loss, rel=1e-4)
+            assert a.valid_ppl == pytest.approx(b.valid_ppl, rel=1e-3)
+    # cursors: rank r's group-major slice interleaves into the global layout
+    cs, _ = single.model.trainer_state()
+    Bg, nof = G * 4, 3
+    for r, t in enumerate(trainers):
+        c, _ = t.model.trainer_state()
+        for g in range(nof):
+            assert np.array_equal(c[g * 4:(g + 1) * 4], cs[g * Bg + r * 4:g * Bg + (r + 1) * 4])
+    for a, b in zip(trainers[0].params(), trainers[1].params()):
+        assert np.array_equal(a, b)
