@@ -165,6 +165,19 @@ int dl_local_group_create(int G, void** group);
 int dl_local_group_destroy(void* group);
 int dl_comm_init_local(dl_ctx* ctx, void* group, int rank);
 
+/* Vocabulary-sharded softmax (no reference counterpart: the reference's
+ * output layer, rnn.hpp:245-258 / backprop.hpp:162-186, is one V x H
+ * matrix).  With on != 0, after dl_comm_init(_local) with G ranks, rank r
+ * holds only W_out / m_out rows [r*V/G, (r+1)*V/G); every rank runs the same
+ * windows (identical inputs, no minibatch split).  Per window the ranks
+ * exchange G x TB block log-sum-exps and the target logits (forward) and sum
+ * dh = dS . W_out (backward); W_in / W_rec stay replicated and bit-identical.
+ * dl_set_params / dl_set_opt read, and dl_get_params / dl_get_opt /
+ * dl_get_grads write, only this rank's W_out / m_out rows of the full V-row
+ * host arrays.  Resets W_out and m_out to zero: call before dl_set_params.
+ * dl_comm_init(_local) turns sharding off again. */
+int dl_set_vocab_shard(dl_ctx* ctx, int on);
+
 /* ---- instrumentation ----------------------------------------------------- */
 
 /* Test hook for the GEMM engine behind every matmul_* of mat.hpp:116-184:

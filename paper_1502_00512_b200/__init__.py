@@ -109,7 +109,7 @@ class GpuRnn:
     def params(self):
         w_in = np.empty((self.V, self.H), np.float32)
         w_rec = np.empty((self.H, self.H), np.float32)
-        w_out = np.empty((self.V, self.H), np.float32)
+        w_out = np.zeros((self.V, self.H), np.float32)  # vocab-sharded: own rows only
         self._chk(load().dl_get_params(self._h, w_in.ctypes.data, w_rec.ctypes.data,
                                        w_out.ctypes.data))
         return w_in, w_rec, w_out
@@ -123,7 +123,7 @@ class GpuRnn:
     def opt(self):
         m_rec = np.empty((self.H, self.H), np.float32)
         m_in = np.empty(self.V, np.float32)
-        m_out = np.empty(self.V, np.float32)
+        m_out = np.zeros(self.V, np.float32)
         self._chk(load().dl_get_opt(self._h, m_rec.ctypes.data, m_in.ctypes.data,
                                     m_out.ctypes.data))
         return m_rec, m_in, m_out
@@ -132,7 +132,7 @@ class GpuRnn:
         """Dense clipped gradients of the last window: (g_in, g_rec, g_out)."""
         g_in = np.empty((self.V, self.H), np.float32)
         g_rec = np.empty((self.H, self.H), np.float32)
-        g_out = np.empty((self.V, self.H), np.float32)
+        g_out = np.zeros((self.V, self.H), np.float32)
         self._chk(load().dl_get_grads(self._h, g_in.ctypes.data, g_rec.ctypes.data,
                                       g_out.ctypes.data))
         return g_in, g_rec, g_out
@@ -186,6 +186,12 @@ class GpuRnn:
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
+
+    def set_vocab_shard(self, on: bool = True):
+        """Vocabulary-sharded softmax over the communicator's ranks
+        (dl_set_vocab_shard): this rank keeps W_out rows [r*V/G, (r+1)*V/G).
+        Zeroes W_out / m_out -- call before set_params."""
+        self._chk(load().dl_set_vocab_shard(self._h, int(on)))
 
 
 def init_uniform(V: int, H: int, seed: int, init_range: float = 0.1):
@@ -496,7 +502,8 @@ class Trainer:
     window).  Validation is the device sharded scorer."""
 
     def __init__(self, cfg: TrainConfig, params, vocab_words: Sequence[str], train_ids,
-                 valid_ids, precision: str = "fp32", device: int = 0, comm=None):
+                 valid_ids, precision: str = "fp32", device: int = 0, comm=None,
+                 vocab_shard: bool = False):
         cfg.validate()
         self.cfg = cfg
         self.vocab = list(vocab_words)
@@ -514,8 +521,11 @@ class Trainer:
             raise ValueError("trainer: validation stream too short")
         self.valid = valid
         self.nranks, self.rank = (1, 0) if comm is None else (comm[1], comm[2])
+        # vocabulary-sharded ranks all run the same streams; data-parallel
+        # ranks split the global minibatch
+        self.dp_ranks = 1 if vocab_shard else self.nranks
         L = len(self.train_ids)
-        N = cfg.noffset * cfg.minibatch * self.nranks
+        N = cfg.noffset * cfg.minibatch * self.dp_ranks
         if L < N:
             raise ValueError("trainer: training stream shorter than the stream count")
         self.model = GpuRnn(V, H, cfg.act, precision, device)
@@ -524,6 +534,8 @@ class Trainer:
             self.model.comm_init_local(comm[0], comm[2])
         elif comm is not None:
             self.model.comm_init(comm[0], comm[1], comm[2])
+        if vocab_shard:
+            self.model.set_vocab_shard(True)
         self.model.set_params(w_in, w_rec, w_out)
         self.model.set_opt(None, None, None, cfg.rho, cfg.eps)
         self.model.trainer_init(self.train_ids, cfg.noffset, cfg.minibatch, cfg.unroll,
@@ -545,7 +557,7 @@ class Trainer:
         """trainer.hpp:350-410 -> (mean window loss, skipped, tokens)."""
         cfg = self.cfg
         L = len(self.train_ids)
-        N = cfg.noffset * cfg.minibatch * self.nranks
+        N = cfg.noffset * cfg.minibatch * self.dp_ranks
         T = cfg.unroll
         rounds = (L + N * T - 1) // (N * T)
         windows = rounds * cfg.noffset

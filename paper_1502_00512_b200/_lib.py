@@ -20,7 +20,7 @@ EXPORTS = (
     "dl_trainer_set_state", "dl_comm_unique_id", "dl_comm_init",
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
     "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
-    "dl_local_group_destroy", "dl_comm_init_local",
+    "dl_local_group_destroy", "dl_comm_init_local", "dl_set_vocab_shard",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -83,6 +83,7 @@ def load():
         "dl_local_group_create": (C.c_int, [C.c_int, P(vp)]),
         "dl_local_group_destroy": (C.c_int, [vp]),
         "dl_comm_init_local": (C.c_int, [vp, vp, C.c_int]),
+        "dl_set_vocab_shard": (C.c_int, [vp, C.c_int]),
         "dl_launch_count": (u64, [vp]),
         "dl_cuda_stream": (vp, [vp]),
         "dl_set_profiling": (C.c_int, [vp, C.c_int]),

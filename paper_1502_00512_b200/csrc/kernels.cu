@@ -136,10 +136,24 @@ __global__ void k_reduce(const float* __restrict__ part, int splits, int64_t spl
 //   grads: dS = w ? float(scale*exp(s - lse)) - [w==y] float(scale) : 0
 constexpr int kRowThreads = 512;
 
+// Vocabulary-sharded rows: every rank holds a V/G column
+// block of the logits.  lse over the full vocabulary is the log-sum-exp of
+// the G block lse values (gathered, rank order); the target logit was summed
+// over ranks (only its owner contributes).
+__device__ __forceinline__ double lse_of_blocks(const double* __restrict__ lse_all, int G,
+                                                int64_t M, int64_t r) {
+  double mx = -INFINITY;
+  for (int g = 0; g < G; ++g) mx = fmax(mx, lse_all[g * M + r]);
+  double z = 0.0;
+  for (int g = 0; g < G; ++g) z += exp(lse_all[g * M + r] - mx);
+  return mx + log(z);
+}
+
 __global__ void __launch_bounds__(kRowThreads)
-k_softmax_rows_f32(float* __restrict__ S, int64_t V, const uint32_t* __restrict__ tgt,
+k_softmax_rows_f32(float* __restrict__ S, int64_t V, int64_t M, const uint32_t* __restrict__ tgt,
                    const uint8_t* __restrict__ wts, double scale, int grads,
-                   double* __restrict__ loss_row, double* __restrict__ logp_row) {
+                   double* __restrict__ loss_row, double* __restrict__ logp_row,
+                   const double* __restrict__ lse_all, int G, const float* __restrict__ tgt_logit) {
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
   float* s = S + r * V;
@@ -151,15 +165,20 @@ k_softmax_rows_f32(float* __restrict__ S, int64_t V, const uint32_t* __restrict_
       for (int64_t w = threadIdx.x; w < V; w += blockDim.x) s[w] = 0.f;
     return;
   }
-  double mx = -INFINITY;
-  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) mx = fmax(mx, (double)s[w]);
-  mx = block_max_d<kRowThreads>(mx, red);
-  double z = 0.0;
-  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) z += exp((double)s[w] - mx);
-  z = block_sum_d<kRowThreads>(z, red);
-  const double lse = mx + log(z);
-  const uint32_t y = tgt[r];
-  const double sy = (double)s[y];
+  double lse;
+  if (lse_all) {
+    lse = lse_of_blocks(lse_all, G, M, r);
+  } else {
+    double mx = -INFINITY;
+    for (int64_t w = threadIdx.x; w < V; w += blockDim.x) mx = fmax(mx, (double)s[w]);
+    mx = block_max_d<kRowThreads>(mx, red);
+    double z = 0.0;
+    for (int64_t w = threadIdx.x; w < V; w += blockDim.x) z += exp((double)s[w] - mx);
+    z = block_sum_d<kRowThreads>(z, red);
+    lse = mx + log(z);
+  }
+  const uint32_t y = tgt[r];  // sharded: column inside this block, or ~0u
+  const double sy = lse_all ? (double)tgt_logit[r] : (double)s[y];
   if (threadIdx.x == 0) {
     if (loss_row) loss_row[r] = scale * (lse - sy);
     if (logp_row) logp_row[r] = sy - lse;
@@ -182,7 +201,7 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
                     int n_tiles, const float* __restrict__ tgt_logit,
                     const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ wts,
                     double scale, int grads, double* __restrict__ loss_row,
-                    double* __restrict__ logp_row) {
+                    double* __restrict__ logp_row, const double* __restrict__ lse_all, int G) {
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
   bf16* s = S ? S + r * V : nullptr;
@@ -198,16 +217,22 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
     }
     return;
   }
-  double mx = -INFINITY;
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
-  mx = block_max_d<kRowThreads>(mx, red);
-  double z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const float2 p = part[(int64_t)t * M + r];
-    if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
+  double lse;
+  if (lse_all) {
+    lse = lse_of_blocks(lse_all, G, M, r);
+  } else {
+    double mx = -INFINITY;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+      mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+    mx = block_max_d<kRowThreads>(mx, red);
+    double z = 0.0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+      const float2 p = part[(int64_t)t * M + r];
+      if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
+    }
+    z = block_sum_d<kRowThreads>(z, red);
+    lse = mx + log(z);
   }
-  z = block_sum_d<kRowThreads>(z, red);
-  const double lse = mx + log(z);
   const double sy = (double)tgt_logit[r];
   if (threadIdx.x == 0) {
     if (loss_row) loss_row[r] = scale * (lse - sy);
@@ -241,6 +266,57 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
   }
 }
 
+// Sharded output layer helpers.  Targets inside [v0, v0 + Vo) become local
+// columns, all others ~0u (matches no column).
+__global__ void k_shard_targets(const uint32_t* __restrict__ y, int64_t M, int64_t v0, int64_t Vo,
+                                uint32_t* __restrict__ loc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = (int64_t)y[i] - v0;
+    loc[i] = (l >= 0 && l < Vo) ? (uint32_t)l : ~0u;
+  }
+}
+
+// Block log-sum-exp of one row from the tcgen05 epilogue's partials.
+__global__ void __launch_bounds__(256)
+k_block_lse_bf16(const float2* __restrict__ part, int n_tiles, int64_t M,
+                 double* __restrict__ lse) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  double mx = -INFINITY;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+    mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+  mx = block_max_d<256>(mx, red);
+  double z = 0.0;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const float2 p = part[(int64_t)t * M + r];
+    if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
+  }
+  z = block_sum_d<256>(z, red);
+  if (threadIdx.x == 0) lse[r] = mx + log(z);
+}
+
+// fp32: block log-sum-exp in double over the row's Vo logits, plus the
+// target logit (0 when the target is not in this block).
+__global__ void __launch_bounds__(kRowThreads)
+k_block_lse_f32(const float* __restrict__ S, int64_t V, const uint32_t* __restrict__ loc,
+                double* __restrict__ lse, float* __restrict__ tgt_logit) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  const float* s = S + r * V;
+  double mx = -INFINITY;
+  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) mx = fmax(mx, (double)s[w]);
+  mx = block_max_d<kRowThreads>(mx, red);
+  double z = 0.0;
+  for (int64_t w = threadIdx.x; w < V; w += blockDim.x) z += exp((double)s[w] - mx);
+  z = block_sum_d<kRowThreads>(z, red);
+  if (threadIdx.x == 0) {
+    lse[r] = mx + log(z);
+    const uint32_t y = loc[r];
+    tgt_logit[r] = y < V ? s[y] : 0.f;
+  }
+}
+
 // Deterministic sum of per-row losses (fixed order / fixed tree) and count
 // of scored rows; accumulates into acc[0] (loss) and cnt[0].
 __global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restrict__ wts,
@@ -264,7 +340,7 @@ __global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restri
 // positions are sorted by (word, processing order) where the processing
 // order of position (t, b) is (T-1-t)*B + b (the backward loop runs t
 // descending, b ascending), so every word's row is summed in exactly the
-// reference's float order.  One block, bitonic sort in shared memory.
+// reference's float order.
 // With G data-parallel ranks the gathered window is rank-blocked ([G][T][B])
 // and the global stream index is r*B + b, so processing order i maps to
 // t = T-1 - i/(G*B), r = (i % (G*B)) / B, b = i % B.
@@ -276,71 +352,9 @@ __device__ __forceinline__ int64_t gathered_pos(int64_t i, int64_t T, int64_t B,
   return (bg / B) * T * B + t * B + (bg % B);
 }
 
-__global__ void __launch_bounds__(kSortThreads)
-k_embed_sort(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, int n_pow2,
-             int* __restrict__ seg_start, int* __restrict__ n_seg, int* __restrict__ order_pos,
-             uint32_t* __restrict__ seg_word) {
-  extern __shared__ unsigned long long keys[];
-  __shared__ int warp_cnt[32];
-  const int64_t n = G * T * B;
-  for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
-    unsigned long long k = ~0ull;
-    if (i < n) k = ((unsigned long long)x[gathered_pos(i, T, B, G)] << 32) | (unsigned)i;
-    keys[i] = k;
-  }
-  __syncthreads();
-  for (int size = 2; size <= n_pow2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n_pow2 / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long a = keys[lo], c = keys[hi];
-        if ((a > c) == up) { keys[lo] = c; keys[hi] = a; }
-      }
-      __syncthreads();
-    }
-  }
-  // segment heads + exclusive scan (chunked, fixed order)
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
-  __syncthreads();
-  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
-    const int i = c0 + threadIdx.x;
-    int head = 0;
-    if (i < n) head = (i == 0) || ((keys[i] >> 32) != (keys[i - 1] >> 32));
-    const unsigned bal = __ballot_sync(0xffffffffu, head);
-    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-    if (l == 0) warp_cnt[w] = __popc(bal);
-    __syncthreads();
-    int off = base;
-    for (int k = 0; k < w; ++k) off += warp_cnt[k];
-    off += __popc(bal & ((1u << l) - 1));
-    if (i < n) {
-      const int ord = (int)(keys[i] & 0xffffffffu);
-      order_pos[i] = (int)gathered_pos(ord, T, B, G);
-      if (head) {
-        seg_start[off] = i;
-        seg_word[off] = (uint32_t)(keys[i] >> 32);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int k = 0; k < (int)(blockDim.x / 32); ++k) tot += warp_cnt[k];
-      base += tot;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    *n_seg = base;
-    seg_start[base] = (int)n;
-  }
-}
-
-// Same contract as k_embed_sort, by a stable block radix sort on the word id
-// (values = processing index, so equal words keep processing order), for
-// n <= 1024 * IPT positions.
+// Sort by a stable block radix sort on the word id (values = processing
+// index, so equal words keep processing order), for n <= 1024 * IPT
+// positions; emits segment heads, words and the position order.
 template <int IPT>
 struct EmbedRadix {
   using Sort = cub::BlockRadixSort<uint32_t, kSortThreads, IPT, int>;
@@ -769,18 +783,34 @@ void reduce_splits(const float* part, int splits, int64_t ss, int64_t n, float* 
 }
 void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const uint8_t* wts,
                       double scale, int grads, double* loss_row, double* logp_row,
-                      cudaStream_t st) {
+                      cudaStream_t st, const double* lse_all, int G, const float* tgt_logit) {
   if (M <= 0) return;
-  k_softmax_rows_f32<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, tgt, wts, scale, grads, loss_row,
-                                                          logp_row);
+  k_softmax_rows_f32<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, M, tgt, wts, scale, grads,
+                                                          loss_row, logp_row, lse_all, G,
+                                                          tgt_logit);
 }
 void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_tiles,
                        const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts,
                        double scale, int grads, double* loss_row, double* logp_row,
-                       cudaStream_t st) {
+                       cudaStream_t st, const double* lse_all, int G) {
   if (M <= 0) return;
   k_softmax_rows_bf16<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, M, part, n_tiles, tgt_logit, tgt,
-                                                           wts, scale, grads, loss_row, logp_row);
+                                                           wts, scale, grads, loss_row, logp_row,
+                                                           lse_all, G);
+}
+void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
+                   cudaStream_t st) {
+  if (M <= 0) return;
+  k_shard_targets<<<grid_for(M), 256, 0, st>>>(y, M, v0, Vo, loc);
+}
+void block_lse_bf16(const float2* part, int n_tiles, int64_t M, double* lse, cudaStream_t st) {
+  if (M <= 0) return;
+  k_block_lse_bf16<<<(unsigned)M, 256, 0, st>>>(part, n_tiles, M, lse);
+}
+void block_lse_f32(const float* S, int64_t M, int64_t V, const uint32_t* loc, double* lse,
+                   float* tgt_logit, cudaStream_t st) {
+  if (M <= 0) return;
+  k_block_lse_f32<<<(unsigned)M, kRowThreads, 0, st>>>(S, V, loc, lse, tgt_logit);
 }
 void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st) {

@@ -20,13 +20,21 @@ void rec_bwd(const float* part, int splits, int64_t split_stride, int64_t n, con
              const float* hnext, int act, float* dpre, bf16* dpreb, cudaStream_t st);
 void reduce_splits(const float* part, int splits, int64_t split_stride, int64_t n, float* out,
                    float clip, int do_clip, int* nonfinite, cudaStream_t st);
+// lse_all != nullptr: vocabulary-sharded rows -- lse from the G gathered
+// block values [G][M], target logit from tgt_logit, tgt = local columns.
 void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const uint8_t* wts,
                       double scale, int grads, double* loss_row, double* logp_row,
-                      cudaStream_t st);
+                      cudaStream_t st, const double* lse_all = nullptr, int G = 0,
+                      const float* tgt_logit = nullptr);
 void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_tiles,
                        const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts,
                        double scale, int grads, double* loss_row, double* logp_row,
-                       cudaStream_t st);
+                       cudaStream_t st, const double* lse_all = nullptr, int G = 0);
+void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
+                   cudaStream_t st);
+void block_lse_bf16(const float2* part, int n_tiles, int64_t M, double* lse, cudaStream_t st);
+void block_lse_f32(const float* S, int64_t M, int64_t V, const uint32_t* loc, double* lse,
+                   float* tgt_logit, cudaStream_t st);
 void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st);
 // x / dpre: G rank-blocked windows [G][T][B] (G = 1 on one GPU)

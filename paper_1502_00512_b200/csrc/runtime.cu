@@ -131,6 +131,13 @@ struct dl_ctx {
 
   // DP
   Comm* comm = nullptr;  // NcclComm (production) or LocalComm (single-device tests)
+  // vocabulary-sharded output layer: this rank owns W_out
+  // rows [v0, v0 + Vo); W_in / W_rec and the recurrence are replicated
+  bool vshard = false;
+  int64_t Vo = 0, v0 = 0;
+  uint32_t* tgt_loc = nullptr;  // [TB] target column inside this rank's block, or ~0
+  double* lse_loc = nullptr;    // [TB] this rank's log-sum-exp over its block
+  double* lse_all = nullptr;    // [G x TB] gathered
   int nranks = 1, rank = 0;
   uint32_t* x_all = nullptr;  // [G][T][B] gathered window ids
   float* dpre_all = nullptr;  // [G][T][B][H] gathered dpre
@@ -166,6 +173,11 @@ int guarded(dl_ctx* c, F&& f) {
     return fail(c, DL_EDEVICE, e.what());
   }
 }
+
+// Ranks that split the minibatch (data parallel).  A vocabulary-sharded
+// group runs the same streams on every rank.
+int64_t dp_ranks(const dl_ctx* c) { return c->vshard ? 1 : c->nranks; }
+int dp_rank(const dl_ctx* c) { return c->vshard ? 0 : c->rank; }
 
 void drop_graphs(dl_ctx* c) {
   for (int v = 0; v < 2; ++v)
@@ -234,7 +246,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->x_all); fr(c->dpre_all);
   c->capT = nT;
   c->capB = nB;
-  const int64_t G = c->nranks;  // W_in gradient rows cover the gathered window
+  const int64_t G = dp_ranks(c);  // W_in gradient rows cover the gathered window
   c->htape = dalloc<float>((nT + 1) * nB * H);
   c->x_d = dalloc<uint32_t>(TB);
   c->y_d = dalloc<uint32_t>(TB);
@@ -252,15 +264,24 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
     c->x_all = dalloc<uint32_t>(G * TB);
     c->dpre_all = dalloc<float>(G * TB * H);
   }
+  const int64_t Vo = c->Vo;  // output rows held by this context
+  (void)V;
   if (c->precision == DL_BF16) {
     c->htape_bf = dalloc<bf16>((nT + 1) * nB * H);
     c->dpre_bf = dalloc<bf16>(TB * H);
-    c->S = dalloc<bf16>(TB * V);
-    c->part_tiles = tc_n_tiles((int)V);
+    c->S = dalloc<bf16>(TB * Vo);
+    c->part_tiles = tc_n_tiles((int)Vo);
     c->part = dalloc<float2>((size_t)c->part_tiles * TB);
     c->tgt_logit = dalloc<float>(TB);
   } else {
-    c->S = dalloc<float>(TB * V);
+    c->S = dalloc<float>(TB * Vo);
+  }
+  fr(c->tgt_loc); fr(c->lse_loc); fr(c->lse_all);
+  if (c->vshard) {
+    c->tgt_loc = dalloc<uint32_t>(TB);
+    c->lse_loc = dalloc<double>(TB);
+    c->lse_all = dalloc<double>((int64_t)c->nranks * TB);
+    if (!c->tgt_logit) c->tgt_logit = dalloc<float>(TB);
   }
 }
 
@@ -309,15 +330,10 @@ GemmDesc desc(int M, int N, int K, int am, const void* A, int64_t lda, int bm, c
   return g;
 }
 
-void nccl_check(ncclResult_t r) {
-  if (r != ncclSuccess)
-    throw Error(DL_EDEVICE, std::string("NCCL: ") + ncclGetErrorString(r));
-}
-
 void refresh_shadows(dl_ctx* c) {
   if (!tc(c)) return;
   f32_to_bf16(c->w_rec, c->w_rec_bf, c->H * c->H, c->st);
-  f32_to_bf16(c->w_out, c->w_out_bf, c->V * c->H, c->st);
+  f32_to_bf16(c->w_out, c->w_out_bf, c->Vo * c->H, c->st);
   c->launches += 2;
 }
 
@@ -350,7 +366,16 @@ void rec_step_fwd(dl_ctx* c, int64_t Bn, const float* h_prev, const bf16* h_prev
 void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, const uint32_t* tgt,
                   const uint8_t* wts, double scale, bool grads, double* loss_row,
                   double* logp_row) {
-  const int64_t V = c->V, H = c->H;
+  const int64_t V = c->Vo, H = c->H;  // this context's vocabulary rows
+  // Vocabulary-sharded: logits over the local block, the
+  // per-row block lse gathered from every rank (G x M doubles) and the target
+  // logit summed from its owner -- the only exchange of the forward pass.
+  const bool vs = c->vshard && c->comm;
+  if (vs) {
+    shard_targets(tgt, M, c->v0, V, c->tgt_loc, c->st);
+    c->launches++;
+    tgt = c->tgt_loc;
+  }
   if (tc(c)) {
     GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs_bf, H, K_MAJOR, c->w_out_bf, H, nullptr, 0);
     g.logits = 1;
@@ -363,13 +388,22 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     // with the 8-warp epilogue the logits GEMM gains most from CTA pairs
     // (C3: 0.352 vs 0.404 ms single-CTA)
     g.no_pair = c->logits_pair ? 0 : 1;
+    if (vs) DL_CUDA(cudaMemsetAsync(c->tgt_logit, 0, M * sizeof(float), c->st));
     {
       Phase p(c, "logits");
       gemm(c, g);
     }
+    if (vs) {
+      Phase p(c, "vocab_exchange");
+      block_lse_bf16(c->part, c->part_tiles, M, c->lse_loc, c->st);
+      c->launches++;
+      c->comm->allgather(c->lse_loc, c->lse_all, (size_t)M, DType::F64, c->st);
+      c->comm->allreduce_sum(c->tgt_logit, (size_t)M, DType::F32, c->st);
+    }
     Phase p(c, "softmax");
     softmax_rows_bf16(grads ? static_cast<bf16*>(c->S) : nullptr, M, V, c->part, c->part_tiles,
-                      c->tgt_logit, tgt, wts, scale, grads ? 1 : 0, loss_row, logp_row, c->st);
+                      c->tgt_logit, tgt, wts, scale, grads ? 1 : 0, loss_row, logp_row, c->st,
+                      vs ? c->lse_all : nullptr, c->nranks);
     c->launches++;
   } else {
     GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs, H, K_MAJOR, c->w_out, H,
@@ -378,9 +412,16 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
       Phase p(c, "logits");
       gemm(c, g);
     }
+    if (vs) {
+      Phase p(c, "vocab_exchange");
+      block_lse_f32(static_cast<float*>(c->S), M, V, tgt, c->lse_loc, c->tgt_logit, c->st);
+      c->launches++;
+      c->comm->allgather(c->lse_loc, c->lse_all, (size_t)M, DType::F64, c->st);
+      c->comm->allreduce_sum(c->tgt_logit, (size_t)M, DType::F32, c->st);
+    }
     Phase p(c, "softmax");
     softmax_rows_f32(static_cast<float*>(c->S), M, V, tgt, wts, scale, grads ? 1 : 0, loss_row,
-                     logp_row, c->st);
+                     logp_row, c->st, vs ? c->lse_all : nullptr, c->nranks, c->tgt_logit);
     c->launches++;
   }
 }
@@ -391,7 +432,9 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
 // stream as soon as dW_out is final (caller joins ev_join).
 void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool grads,
                 double fork_out_eta = 0.0) {
-  const int64_t H = c->H, V = c->V, TB = T * B, BH = B * H;
+  // V: input vocabulary (W_in rows); Vo: output rows held here (V / G when
+  // the softmax is vocabulary-sharded)
+  const int64_t H = c->H, V = c->V, Vo = c->Vo, TB = T * B, BH = B * H;
   cudaStream_t st = c->st;
   if (tc(c)) {
     f32_to_bf16(c->htape, c->htape_bf, BH, st);
@@ -415,7 +458,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
   output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
-  const bool dp = c->comm != nullptr;
+  const bool dp = c->comm != nullptr && !c->vshard;
+  const bool vs = c->comm != nullptr && c->vshard;
   if (dp) {
     // the window's loss is the sum over all ranks' streams
     DL_CUDA(cudaMemsetAsync(c->win_loss, 0, 16, st));
@@ -434,9 +478,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
   {
     Phase p(c, "dw_out");
-    GemmDesc g = tc(c) ? desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs_bf, H,
+    GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
                               c->g_out, H)
-                       : desc((int)V, (int)H, (int)TB, MN_MAJOR, c->S, V, MN_MAJOR, Hs, H,
+                       : desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
                               c->g_out, H);
     g.raster = 1;
     g.do_clip = dp ? 0 : 1;
@@ -479,10 +523,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       DL_CUDA(cudaEventRecord(a, c->st2));
     }
     if (c->g16_valid)
-      rms_dense_g16(c->w_out, c->w_out_bf_next, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, V, H,
+      rms_dense_g16(c->w_out, c->w_out_bf_next, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, Vo, H,
                     c->rho, c->eps, fork_out_eta, c->st2);
     else
-      rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, V, H, c->rho,
+      rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, Vo, H, c->rho,
                c->eps, fork_out_eta, 1, nullptr, c->st2);
     c->launches++;
     if (c->profiling) {
@@ -494,10 +538,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
   {
     Phase p(c, "dh");
-    const int s = pick_splits(c, (int)TB, (int)H, (int)V, 8);
-    GemmDesc g = tc(c) ? desc((int)TB, (int)H, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->w_out_bf, H,
-                              c->dh_out, H)
-                       : desc((int)TB, (int)H, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->w_out, H,
+    const int s = pick_splits(c, (int)TB, (int)H, (int)Vo, 8);
+    GemmDesc g = tc(c) ? desc((int)TB, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out_bf,
+                              H, c->dh_out, H)
+                       : desc((int)TB, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out, H,
                               c->dh_out, H);
     g.raster = 0;
     if (s > 1) {
@@ -511,6 +555,13 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     } else {
       gemm(c, g);
     }
+  }
+  if (vs) {
+    // each rank contracted its vocabulary block: dh_out = sum over ranks.
+    // After this the backward recurrence, dW_rec and the W_in rows are
+    // replicated computations on identical inputs.
+    Phase p(c, "vocab_exchange");
+    c->comm->allreduce_sum(c->dh_out, (size_t)(TB * H), DType::F32, st);
   }
   // backward recurrence (backprop.hpp:197-219)
   {
@@ -586,6 +637,12 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                 c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   }
+  // a non-finite dW_out block on one rank must skip the update everywhere
+  // (only reachable with an infinite clip bound)
+  if (vs && !std::isfinite(clip)) {
+    if (fork_out_eta > 0.0) DL_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+    c->comm->allreduce_sum(c->nonfinite, 1, DType::U32, st);
+  }
   c->have_grads = true;
 }
 
@@ -600,16 +657,55 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
   if (!skip_out && c->g16_valid)
-    rms_dense_g16(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, c->V, c->H,
+    rms_dense_g16(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, c->Vo, c->H,
                   c->rho, c->eps, eta, st);
   else if (!skip_out)
-    rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->V,
+    rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->Vo,
              c->H, c->rho, c->eps, eta, 1, c->nonfinite, st);
   count_skip(c->nonfinite, c->d_skipped, st);
   c->launches += 4;
 }
 
 float act0(int act) { return act == 0 ? 0.5f : 0.0f; }
+
+// (Re)allocates the output-layer state for this context's Vo vocabulary
+// rows: W_out and its shadows, m_out, dW_out (+ bf16 copy and row sums of
+// squares), all zeroed.  Window buffers sized by Vo are dropped too.
+void alloc_output(dl_ctx* c) {
+  auto fr = [](auto*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  fr(c->w_out); fr(c->m_out); fr(c->g_out); fr(c->w_out_bf); fr(c->w_out_bf_next);
+  fr(c->g_out_bf); fr(c->rowsq);
+  const int64_t Vo = c->Vo, H = c->H;
+  c->w_out = dalloc<float>(Vo * H);
+  c->m_out = dalloc<float>(Vo);
+  c->g_out = dalloc<float>(Vo * H);
+  DL_CUDA(cudaMemsetAsync(c->w_out, 0, Vo * H * 4, c->st));
+  DL_CUDA(cudaMemsetAsync(c->m_out, 0, Vo * 4, c->st));
+  if (c->precision == DL_BF16) {
+    c->w_out_bf = dalloc<bf16>(Vo * H);
+    c->w_out_bf_next = dalloc<bf16>(Vo * H);
+    c->g_out_bf = dalloc<bf16>(Vo * H);
+    c->rowsq_n = tc_n_tiles((int)H);
+    c->rowsq = dalloc<double>((size_t)c->rowsq_n * Vo);
+  }
+  c->capT = c->capB = 0;  // window buffers re-size on the next call
+  fr(c->htape);
+  c->have_grads = false;
+  drop_graphs(c);
+}
+
+// Back to the full output layer (W_out zeroed: set the parameters again).
+void reset_vshard(dl_ctx* c) {
+  if (!c->vshard) return;
+  c->vshard = false;
+  c->Vo = c->V;
+  c->v0 = 0;
+  alloc_output(c);
+  refresh_shadows(c);
+}
 
 }  // namespace
 
@@ -656,12 +752,12 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->w_in = dalloc<float>(V * H);
     c->w_rec = dalloc<float>(H * H);
-    c->w_out = dalloc<float>(V * H);
     c->m_rec = dalloc<float>(H * H);
     c->m_in = dalloc<float>(V);
-    c->m_out = dalloc<float>(V);
     c->g_rec = dalloc<float>(H * H);
-    c->g_out = dalloc<float>(V * H);
+    c->Vo = V;
+    c->v0 = 0;
+    alloc_output(c);
     c->g_in_n = dalloc<int>(1);
     c->nonfinite = dalloc<int>(1);
     c->d_loss = dalloc<double>(1);
@@ -671,20 +767,11 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->win_loss = dalloc<double>(2);
     c->win_pos = reinterpret_cast<unsigned long long*>(c->win_loss + 1);
     c->win_counter = dalloc<int64_t>(1);
-    if (precision == DL_BF16) {
-      c->w_rec_bf = dalloc<bf16>(H * H);
-      c->w_out_bf = dalloc<bf16>(V * H);
-      c->w_out_bf_next = dalloc<bf16>(V * H);
-      c->g_out_bf = dalloc<bf16>(V * H);
-      c->rowsq_n = tc_n_tiles((int)H);
-      c->rowsq = dalloc<double>((size_t)c->rowsq_n * V);
-    }
+    if (precision == DL_BF16) c->w_rec_bf = dalloc<bf16>(H * H);
     DL_CUDA(cudaMemsetAsync(c->w_in, 0, V * H * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->w_rec, 0, H * H * 4, c->st));
-    DL_CUDA(cudaMemsetAsync(c->w_out, 0, V * H * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->m_rec, 0, H * H * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->m_in, 0, V * 4, c->st));
-    DL_CUDA(cudaMemsetAsync(c->m_out, 0, V * 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, 4, c->st));
     DL_CUDA(cudaMemsetAsync(c->g_in_n, 0, 4, c->st));
     refresh_shadows(c);
@@ -712,7 +799,7 @@ int dl_destroy(dl_ctx* c) {
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
                   c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
-                  c->rowsq};
+                  c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -730,7 +817,8 @@ int dl_set_params(dl_ctx* c, const float* w_in, const float* w_rec, const float*
   return guarded(c, [&] {
     DL_CUDA(cudaMemcpyAsync(c->w_in, w_in, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaMemcpyAsync(c->w_rec, w_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->w_out, w_out, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->w_out, w_out + c->v0 * c->H, c->Vo * c->H * 4,
+                            cudaMemcpyHostToDevice, c->st));
     refresh_shadows(c);
     DL_CUDA(cudaStreamSynchronize(c->st));
   });
@@ -741,7 +829,9 @@ int dl_get_params(dl_ctx* c, float* w_in, float* w_rec, float* w_out) {
   return guarded(c, [&] {
     if (w_in) DL_CUDA(cudaMemcpyAsync(w_in, c->w_in, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
     if (w_rec) DL_CUDA(cudaMemcpyAsync(w_rec, c->w_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
-    if (w_out) DL_CUDA(cudaMemcpyAsync(w_out, c->w_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    if (w_out)
+      DL_CUDA(cudaMemcpyAsync(w_out + c->v0 * c->H, c->w_out, c->Vo * c->H * 4,
+                              cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
   });
 }
@@ -756,7 +846,8 @@ int dl_set_opt(dl_ctx* c, const float* m_rec, const float* m_in, const float* m_
     c->eps = eps;
     if (m_rec) DL_CUDA(cudaMemcpyAsync(c->m_rec, m_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
     if (m_in) DL_CUDA(cudaMemcpyAsync(c->m_in, m_in, c->V * 4, cudaMemcpyHostToDevice, c->st));
-    if (m_out) DL_CUDA(cudaMemcpyAsync(c->m_out, m_out, c->V * 4, cudaMemcpyHostToDevice, c->st));
+    if (m_out)
+      DL_CUDA(cudaMemcpyAsync(c->m_out, m_out + c->v0, c->Vo * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
     drop_graphs(c);
   });
@@ -767,7 +858,8 @@ int dl_get_opt(dl_ctx* c, float* m_rec, float* m_in, float* m_out) {
   return guarded(c, [&] {
     if (m_rec) DL_CUDA(cudaMemcpyAsync(m_rec, c->m_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
     if (m_in) DL_CUDA(cudaMemcpyAsync(m_in, c->m_in, c->V * 4, cudaMemcpyDeviceToHost, c->st));
-    if (m_out) DL_CUDA(cudaMemcpyAsync(m_out, c->m_out, c->V * 4, cudaMemcpyDeviceToHost, c->st));
+    if (m_out)
+      DL_CUDA(cudaMemcpyAsync(m_out + c->v0, c->m_out, c->Vo * 4, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
   });
 }
@@ -827,16 +919,18 @@ int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
     if (g_rec) DL_CUDA(cudaMemcpyAsync(g_rec, c->g_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
     if (g_out && c->g16_valid) {
       // bf16 gradient of the throughput path, widened on the host
-      std::vector<uint16_t> tmp((size_t)(c->V * c->H));
+      std::vector<uint16_t> tmp((size_t)(c->Vo * c->H));
       DL_CUDA(cudaMemcpyAsync(tmp.data(), c->g_out_bf, tmp.size() * 2, cudaMemcpyDeviceToHost,
                               c->st));
       DL_CUDA(cudaStreamSynchronize(c->st));
+      float* dst = g_out + c->v0 * c->H;
       for (size_t i = 0; i < tmp.size(); ++i) {
         const uint32_t u = (uint32_t)tmp[i] << 16;
-        std::memcpy(&g_out[i], &u, 4);
+        std::memcpy(&dst[i], &u, 4);
       }
     } else if (g_out) {
-      DL_CUDA(cudaMemcpyAsync(g_out, c->g_out, c->V * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaMemcpyAsync(g_out + c->v0 * c->H, c->g_out, c->Vo * c->H * 4,
+                              cudaMemcpyDeviceToHost, c->st));
     }
     DL_CUDA(cudaStreamSynchronize(c->st));
   });
@@ -858,7 +952,8 @@ int dl_set_grads(dl_ctx* c, int64_t n_in_rows, const uint32_t* in_words, const f
       DL_CUDA(cudaMemcpyAsync(c->g_in_rows, in_rows, n_in_rows * c->H * 4, cudaMemcpyHostToDevice, c->st));
     }
     DL_CUDA(cudaMemcpyAsync(c->g_rec, g_rec, c->H * c->H * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->g_out, g_out, c->V * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->g_out, g_out + c->v0 * c->H, c->Vo * c->H * 4,
+                            cudaMemcpyHostToDevice, c->st));
     // finite check of the injected gradients (rmsprop.hpp:116 / rnn.hpp:165-171)
     int bad = 0;
     auto fin = [&](const float* p, int64_t k) {
@@ -879,7 +974,7 @@ int dl_rmsprop(dl_ctx* c, double eta, int* applied) {
   if (!c) return fail(c, DL_EINVAL, "dl_rmsprop: null ctx");
   if (!c->have_grads) return fail(c, DL_EINVAL, "dl_rmsprop: no gradients computed yet");
   return guarded(c, [&] {
-    run_rmsprop(c, eta, c->capT * c->capB * c->nranks);
+    run_rmsprop(c, eta, c->capT * c->capB * dp_ranks(c));
     int bad = 0;
     DL_CUDA(cudaMemcpyAsync(&bad, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
@@ -1063,7 +1158,7 @@ int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int 
   if (noffset < 1 || minibatch < 1 || unroll < 1)
     return fail(c, DL_EINVAL, "config: noffset, minibatch, unroll must be >= 1");
   if (!(clip > 0.0)) return fail(c, DL_EINVAL, "config: clip must be > 0");
-  const int64_t Nglob = (int64_t)noffset * minibatch * c->nranks;
+  const int64_t Nglob = (int64_t)noffset * minibatch * dp_ranks(c);
   if (L < Nglob) return fail(c, DL_EINVAL, "trainer: training stream shorter than the stream count");
   for (int64_t i = 0; i < L; ++i)
     if (ids[i] >= (uint64_t)c->V) return fail(c, DL_EDATA, "trainer: id out of vocabulary range");
@@ -1083,7 +1178,7 @@ int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int 
     c->cursors = dalloc<int64_t>(Nl);
     c->hidden = dalloc<float>(Nl * c->H);
     std::vector<int64_t> cur(Nl);
-    dl_rank_cursors(L, noffset, minibatch, c->nranks, c->rank, cur.data());
+    dl_rank_cursors(L, noffset, minibatch, (int)dp_ranks(c), dp_rank(c), cur.data());
     DL_CUDA(cudaMemcpyAsync(c->cursors, cur.data(), Nl * 8, cudaMemcpyHostToDevice, c->st));
     fill_f32(c->hidden, act0(c->act), Nl * c->H, c->st);
     ensure_window(c, unroll, minibatch);
@@ -1130,9 +1225,9 @@ void swap_shadow(dl_ctx* c) {
 // Size the split-K workspace for a T x B window before graph capture
 // (no allocation may happen inside a capture).
 void presize(dl_ctx* c, int64_t T, int64_t B) {
-  const int64_t H = c->H, V = c->V, TB = T * B;
+  const int64_t H = c->H, Vo = c->Vo, TB = T * B;
   size_t need = (size_t)pick_splits(c, (int)B, (int)H, (int)H) * B * H;
-  const int sdh = pick_splits(c, (int)TB, (int)H, (int)V, 8);
+  const int sdh = pick_splits(c, (int)TB, (int)H, (int)Vo, 8);
   if (sdh > 1) need = std::max(need, (size_t)sdh * TB * H);
   need = std::max(need, (size_t)pick_splits(c, (int)H, (int)H, (int)TB, 16) * H * H);
   ensure_splitws(c, need);
@@ -1141,7 +1236,7 @@ void presize(dl_ctx* c, int64_t T, int64_t B) {
 // One device-resident window of the epoch schedule (trainer.hpp:376-405).
 void trainer_window(dl_ctx* c, double eta) {
   const int64_t B = c->minibatch, T = c->unroll, H = c->H;
-  const double scale = 1.0 / (double)(B * c->nranks * T);
+  const double scale = 1.0 / (double)(B * dp_ranks(c) * T);
   window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
                c->x_d, c->y_d, c->w_d, c->htape, c->st);
   c->launches++;
@@ -1150,7 +1245,7 @@ void trainer_window(dl_ctx* c, double eta) {
   // allreduce is pending
   const bool fork = fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0);
-  run_rmsprop(c, eta, T * B * c->nranks, /*skip_out=*/fork);
+  run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
                 c->L, act0(c->act), c->st);
   c->launches += 2;
@@ -1230,6 +1325,7 @@ int dl_comm_init(dl_ctx* c, const uint8_t id[128], int nranks, int rank) {
   if (!c) return fail(c, DL_EINVAL, "dl_comm_init: null ctx");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, DL_EINVAL, "dl_comm_init: bad rank");
   return guarded(c, [&] {
+    reset_vshard(c);
     c->nranks = nranks;
     c->rank = rank;
     c->capT = c->capB = 0;  // window buffers are re-sized for the gathered window
@@ -1260,12 +1356,37 @@ int dl_comm_init_local(dl_ctx* c, void* group, int rank) {
   LocalGroup* g = static_cast<LocalGroup*>(group);
   if (rank < 0 || rank >= g->G) return fail(c, DL_EINVAL, "dl_comm_init_local: bad rank");
   return guarded(c, [&] {
+    reset_vshard(c);
     c->nranks = g->G;
     c->rank = rank;
     c->capT = c->capB = 0;
     drop_graphs(c);
     delete c->comm;
     c->comm = g->G > 1 ? new LocalComm(g, rank) : nullptr;
+  });
+}
+
+int dl_set_vocab_shard(dl_ctx* c, int on) {
+  if (!c) return fail(c, DL_EINVAL, "dl_set_vocab_shard: null ctx");
+  if (on) {
+    if (!c->comm || c->nranks < 2)
+      return fail(c, DL_EINVAL, "dl_set_vocab_shard: needs a communicator of >= 2 ranks");
+    if (c->V % c->nranks != 0)
+      return fail(c, DL_EINVAL, "dl_set_vocab_shard: V must be a multiple of the rank count");
+    if (c->precision == DL_BF16 && ((c->V / c->nranks) % 8) != 0)
+      return fail(c, DL_EINVAL, "dl_set_vocab_shard: bf16 mode needs V/G a multiple of 8 (TMA)");
+  }
+  return guarded(c, [&] {
+    if (!on) {
+      reset_vshard(c);
+      return;
+    }
+    c->vshard = true;
+    c->Vo = c->V / c->nranks;
+    c->v0 = (int64_t)c->rank * c->Vo;
+    alloc_output(c);
+    refresh_shadows(c);
+    DL_CUDA(cudaStreamSynchronize(c->st));
   });
 }
 

@@ -71,6 +71,123 @@ def test_dp_window_matches_global_window(orc, G, precision):
             assert close(a, b)
 
 
+def _vshard_ranks(dl, G, V, H, precision, params):
+    group = dl.LocalGroup(G)
+    ranks = []
+    for r in range(G):
+        m = dl.GpuRnn(V, H, 0, precision)
+        m.comm_init_local(group, r)
+        m.set_vocab_shard(True)
+        m.set_params(*params)
+        ranks.append(m)
+    return ranks
+
+
+def _assemble(parts, G):
+    """Row block r of the vocabulary-sharded arrays comes from rank r."""
+    V = parts[0].shape[0]
+    out = np.zeros_like(parts[0])
+    for r in range(G):
+        out[r * V // G:(r + 1) * V // G] = parts[r][r * V // G:(r + 1) * V // G]
+    return out
+
+
+@pytest.mark.parametrize("G,precision", [(2, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])
+def test_vocab_shard_window_matches_full_softmax(orc, G, precision):
+    """G ranks each own V/G rows of W_out; loss, h_final,
+    gradients and the updated parameters equal one context holding the whole
+    output layer (fp32: 1e-5, the two-level log-sum-exp is the only change;
+    bf16: the same tensor-core tiles over a narrower N)."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 1024, 64, 6, 16
+    rng = np.random.default_rng(7 + G)
+    params = orc.init_uniform(V, H, 31)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.1).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    scale = 1.0 / (B * T)
+    wb = dl.WindowBatch(x, y, w)
+    single = dl.GpuRnn(V, H, 0, precision)
+    single.set_params(*params)
+    r1, hf1 = dl.bptt_run(single, wb, h0, scale, 1.0)
+    g1 = single.grads()
+    assert dl.rmsprop_update(single, 0.05)
+    want = single.params() + single.opt()
+
+    ranks = _vshard_ranks(dl, G, V, H, precision, params)
+
+    def run(r):
+        res, hf = dl.bptt_run(ranks[r], wb, h0, scale, 1.0)
+        g = ranks[r].grads()
+        ok = dl.rmsprop_update(ranks[r], 0.05)
+        return res, hf, g, ok
+
+    with ThreadPoolExecutor(G) as ex:
+        outs = list(ex.map(run, range(G)))
+    tol = 1e-5 if precision == "fp32" else 2e-3
+    for res, hf, g, ok in outs:
+        assert ok
+        assert res.positions == r1.positions
+        assert res.loss == pytest.approx(r1.loss, rel=tol)
+        assert np.allclose(hf, hf1, atol=1e-6)  # forward recurrence is replicated
+        assert res.loss == outs[0][0].loss  # every rank reports the same loss
+    # replicated state (W_in, W_rec, their grads) is bit-identical across ranks
+    got = [m.params() + m.opt() for m in ranks]
+    for r in range(1, G):
+        for k in (0, 1, 3, 4):
+            assert np.array_equal(got[0][k], got[r][k])
+        for k in (0, 1):
+            assert np.array_equal(outs[0][2][k], outs[r][2][k])
+    g_out = _assemble([o[2][2] for o in outs], G)
+    w_out = _assemble([gr[2] for gr in got], G)
+    m_out = _assemble([gr[5][:, None] for gr in got], G)[:, 0]
+    if precision == "fp32":
+        for a, b in zip(outs[0][2][:2] + (g_out,), g1):
+            assert close(a, b, 1e-5)
+        for a, b in zip(got[0][:2] + (w_out,) + got[0][3:5] + (m_out,), want):
+            assert close(a, b, 1e-5)
+    else:
+        # bf16: dW_out within bf16 rounding of the single-context gradient
+        assert np.abs(g_out - g1[2]).max() <= 2e-2 * np.abs(g1[2]).max()
+        assert np.abs(w_out - want[2]).max() <= 1e-3
+
+
+def test_vocab_shard_scoring_and_trainer(orc):
+    """Sharded scoring equals full scoring; a vocab-sharded trainer tracks
+    the single-context trainer (same streams on every rank)."""
+    import paper_1502_00512_b200 as dl
+    V, H, G = 96, 32, 2
+    tr, va = orc.random_stream_pair(23, V, 3016, 600)
+    tr = tr[:3000]
+    params = orc.init_uniform(V, H, 5)
+    single = dl.GpuRnn(V, H, 0, "fp32")
+    single.set_params(*params)
+    want = dl.sharded_perplexity(single, va, 4)
+    ranks = _vshard_ranks(dl, G, V, H, "fp32", params)
+    with ThreadPoolExecutor(G) as ex:
+        got = list(ex.map(lambda m: dl.sharded_perplexity(m, va, 4), ranks))
+    for p in got:
+        assert p.predicted == want.predicted
+        assert p.total_logprob == pytest.approx(want.total_logprob, rel=1e-9)
+
+    kw = dict(nstate=H, noffset=2, minibatch=4, unroll=5, eta=0.02, max_epochs=2, mode=1)
+    ref = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, "fp32")
+    ref.train()
+    group = dl.LocalGroup(G)
+    trainers = [dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, "fp32",
+                           comm=(group, G, r), vocab_shard=True) for r in range(G)]
+    with ThreadPoolExecutor(G) as ex:
+        list(ex.map(lambda t: t.train(), trainers))
+    for t in trainers:
+        assert len(t.logs) == len(ref.logs)
+        for a, b in zip(t.logs, ref.logs):
+            assert a.train_loss == pytest.approx(b.train_loss, rel=1e-4)
+            assert a.valid_ppl == pytest.approx(b.valid_ppl, rel=1e-3)
+    w_out = _assemble([t.params()[2] for t in trainers], G)
+    assert close(w_out, ref.params()[2], 1e-2)
+
+
 def test_dp_trainer_matches_global_minibatch(orc):
     """Two ranks x minibatch 4 == one trainer with minibatch 8 (same
     schedule: rank r owns streams g*8 + r*4 + b)."""
