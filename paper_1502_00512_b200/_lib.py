@@ -10,6 +10,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdesklm_cuda.so")
+# tuning experiments (scripts/build_variant.sh) may point at another build
+LIB_PATH = os.environ.get("DL_LIB_PATH", LIB_PATH)
 
 # Every symbol include/desklm_cuda.h declares (checked by tests/test_abi.py).
 EXPORTS = (

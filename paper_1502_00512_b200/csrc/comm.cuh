@@ -29,6 +29,10 @@ struct Comm {
   virtual void allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) = 0;
   // recv[r*n .. r*n+n) = rank r's send[0..n)
   virtual void allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) = 0;
+  // true when other ranks' kernels run concurrently on this rank's device:
+  // kernels that need the whole GPU co-resident (spin-waiting across CTAs)
+  // must not be used then
+  virtual bool shares_device() const { return false; }
 };
 
 struct NcclComm : Comm {
@@ -60,6 +64,7 @@ struct LocalComm : Comm {
   ~LocalComm() override;
   void allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) override;
   void allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) override;
+  bool shares_device() const override { return true; }
 
  private:
   void publish(const void* p, cudaStream_t st);  // ptr + ready event, then barrier + wait all

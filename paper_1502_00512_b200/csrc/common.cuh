@@ -54,6 +54,27 @@ __device__ __forceinline__ float clip1(float x, float c) {
   return (t < c) ? t : c;
 }
 
+// float(eta * g / denom) exactly as the reference computes it (double
+// multiply, IEEE double divide, round to float), with one reciprocal per row
+// instead of a divide per element: q*inv is within 1.5 double ulps of the
+// correctly rounded quotient, so rounding it to float gives the same float
+// unless the quotient lies within a few double ulps of a float rounding
+// midpoint -- only then is the exact division performed.
+__device__ __forceinline__ float rms_step(double eta, float g, double denom, double inv) {
+  const double q = eta * (double)g;
+  const double r = q * inv;
+  const float f = (float)r;
+  const float af = fabsf(f);
+  if (!(af < 3.0e38f) || af < 1.0e-30f) return (float)(q / denom);  // inf/NaN/tiny: exact
+  const double up = (double)__int_as_float(__float_as_int(af) + 1) - (double)af;
+  const double dn = (double)af - (double)__int_as_float(__float_as_int(af) - 1);
+  const double ar = fabs(r), fd = (double)af;
+  const double tol = ar * 0x1p-49;
+  if (fabs(ar - (fd + 0.5 * up)) <= tol || fabs(ar - (fd - 0.5 * dn)) <= tol)
+    return (float)(q / denom);
+  return f;
+}
+
 // ---------------------------------------------------------------- launches
 // GEMM problem description shared by the SIMT (fp32) and tcgen05 (bf16)
 // kernels.  C (+ split * split_stride) receives fp32 results; for k_splits>1
@@ -87,6 +108,17 @@ struct GemmDesc {
   // [2*n_tiles][M] (double), for the dense rmsprop's mean_sq
   bf16* Cb;
   double* rowsq;
+  // fused dense rmsprop (dW_out, bf16 trainer path; rmsprop.hpp:94-107):
+  // the epilogue clips, publishes per-(half N tile, row) sums of squares to
+  // rowsq, waits on rms_cnt[M block] until every N tile of its rows has
+  // published, then updates the fp32 master rms_w, the bf16 shadow rms_wb
+  // and m_out rms_m in place.  The gradient is never stored.
+  int rms;
+  float* rms_w;
+  bf16* rms_wb;
+  float* rms_m;
+  unsigned* rms_cnt;  // [ceil(M / 256)], zero at launch
+  double rho, eps, eta;
 };
 
 // gemm_simt.cu
@@ -95,5 +127,6 @@ void gemm_f32(const GemmDesc& g, cudaStream_t st);
 int gemm_tc(const GemmDesc& g, cudaStream_t st);
 int tc_n_tiles(int N);
 int tc_splits(int K, int desired);
+bool tc_rms_fusable(int M, int N);
 
 }  // namespace dl

@@ -216,14 +216,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 // multicast to both CTAs' empty / tmem-full barriers; both epilogues drain
 // their own TMEM half (128 rows x 256 columns) and arrive remotely on the
 // even CTA's tmem-empty barrier.
+// RMS: the fused-rmsprop variant gives one k-stage to a per-epilogue-warp
+// ring of two 32 x 32 fp32 master chunks (4 KB each, 16-byte units XOR
+// swizzled by row) filled by cp.async.
+template <bool RMS>
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2;   // 128 rows of A
   static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = RMS ? 5 : 6;
   static constexpr int TMEM_COLS = 512;         // 2 accumulator stages x 256 columns
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int EPI_OFF = STAGES * STAGE + 256;
+  static constexpr int EPI_CHUNK_BYTES = 32 * 32 * 4;
+  static constexpr int EPI_WARP_BYTES = RMS ? 2 * EPI_CHUNK_BYTES : 0;
+  static constexpr int SMEM = EPI_OFF + kEpiWarps * EPI_WARP_BYTES + 1024;
 };
+static_assert(Cfg2<true>::SMEM <= 227 * 1024 && Cfg2<false>::SMEM <= 227 * 1024,
+              "pair kernel shared memory");
 
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map,
                                                  uint32_t bar, int c0, int c1) {
@@ -265,11 +274,179 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <bool A_MN, bool B_MN>
+// relaxed poll (an acquire load would invalidate L1 on every iteration);
+// the caller fences once after the condition holds
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+// byte offset of 16-byte unit u (0..7) of row r in a 32 x 32 fp32 chunk: the
+// unit index is XOR-swizzled by r % 8, so both a row per thread and eight
+// threads per row touch eight distinct bank groups per quarter warp
+__device__ __forceinline__ uint32_t chunk_off(int r, int u) {
+  return static_cast<uint32_t>(r * 128 + ((u ^ (r & 7)) << 4));
+}
+
+// Fused dense W_out rmsprop epilogue (rmsprop.hpp:94-107) for one
+// accumulator row of a 256 x 256 pair tile: this warp drains columns
+// [c0, c0 + 128) of its TMEM lane quarter (32 rows, thread = row).
+//   pass 1: clip (rnn.hpp:158-159), partial sum of squares -> rowsq[sub][m];
+//           the warp arrives on its M block's counter, then waits until all
+//           2 * 8 * n_tiles warps of the block have arrived;
+//   pass 2: mean_sq over the row's partials in fixed order,
+//           m = float(rho m + (1-rho) mean_sq) exactly as the reference, and
+//           w -= s * g with s = float(eta / sqrt(m + eps)) in fp32 (the bf16
+//           mode's update; the reference rounds eta*g/denom once instead),
+//           then the bf16 shadow.
+// The fp32 master streams through a two-chunk cp.async ring in shared memory
+// (issued before pass 1, so the first loads overlap the sums and the block
+// sync): read coalesced (eight lanes per 128-byte row), updated a row per
+// thread against the TMEM accumulator, stored coalesced.
+// The old m is read before arriving; the nt == 0, half 0 warp writes the new
+// m after every warp of the block has arrived, so no reader sees it early.
+constexpr int kRmsChunks = 4;  // 32-column chunks per epilogue warp (half of 256)
+//   DL_RMS_DIAG  timing diagnostics only (wrong results): 1 no block sync,
+//                2 no pass 2, 4 no pass 1 tmem loads
+#ifndef DL_RMS_DIAG
+#define DL_RMS_DIAG 0
+#endif
+
+__device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, int m, int mt,
+                                             int nt, int half, int c0, int nsub, unsigned target,
+                                             uint32_t ring) {
+  const int lane = threadIdx.x % 32;
+  const bool mvalid = m < g.M;
+  const int sub = 2 * nt + half;
+  const int rbase = m - lane;
+  const float m_old = mvalid ? g.rms_m[m] : 0.f;
+  // coalesced role: lane -> rows 4i + lane/8, 16-byte unit lane % 8
+  const int cr = lane >> 3, cu = lane & 7;
+  const int64_t col0 = static_cast<int64_t>(nt) * 256 + c0 * 32 + 4 * cu;
+  auto issue = [&](int k, uint32_t buf) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = 4 * i + cr;
+      if (!(DL_RMS_DIAG & 16) && rbase + rr < g.M)
+        cp_async16(buf + chunk_off(rr, cu),
+                   g.rms_w + static_cast<int64_t>(rbase + rr) * g.ldc + col0 + k * 32);
+    }
+    cp_async_commit();
+  };
+  issue(0, ring);
+  issue(1, ring + 4096);
+
+  double sq = 0.0;
+#pragma unroll 1
+  for (int c = c0; c < ((DL_RMS_DIAG & 4) ? c0 : c0 + kRmsChunks); ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = clip1(v[j], g.clip);
+      s = fmaf(x, x, s);
+    }
+    sq += (double)s;
+  }
+  if (mvalid) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(g.rms_cnt + mt, 1u);
+#if !(DL_RMS_DIAG & 1)
+    while (ld_relaxed(g.rms_cnt + mt) < target) __nanosleep(32);
+#endif
+    __threadfence();
+  }
+  __syncwarp();
+  float step = 0.f, mw = 0.f;
+  if (mvalid) {
+    double tot = 0.0;
+    for (int k = 0; k < nsub; ++k) tot += __ldcg(g.rowsq + static_cast<int64_t>(k) * g.M + m);
+    mw = (float)(g.rho * (double)m_old + (1.0 - g.rho) * (tot / (double)g.N));
+    step = (float)(g.eta / sqrt((double)mw + g.eps));
+  }
+#pragma unroll 1
+  for (int k = 0; k < ((DL_RMS_DIAG & 2) ? 0 : kRmsChunks); ++k) {
+    const uint32_t buf = ring + (k & 1) * 4096;
+    if (k + 1 < kRmsChunks) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncwarp();
+    // row per thread: w -= step * clip(g) in place
+    float v[32];
+    tmem_ld32(taddr + (c0 + k) * 32, v);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t a = buf + chunk_off(lane, u);
+      float4 w = ld_shared_v4(a);
+      w.x -= step * clip1(v[4 * u + 0], g.clip);
+      w.y -= step * clip1(v[4 * u + 1], g.clip);
+      w.z -= step * clip1(v[4 * u + 2], g.clip);
+      w.w -= step * clip1(v[4 * u + 3], g.clip);
+      st_shared_v4(a, w);
+    }
+    __syncwarp();
+    // coalesced stores of the master and its bf16 shadow
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = 4 * i + cr;
+      const float4 w = ld_shared_v4(buf + chunk_off(rr, cu));
+      if (!(DL_RMS_DIAG & 8) && rbase + rr < g.M) {
+        const int64_t off = static_cast<int64_t>(rbase + rr) * g.ldc + col0 + k * 32;
+        *reinterpret_cast<float4*>(g.rms_w + off) = w;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(w.x, w.y);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(w.z, w.w);
+        uint2 q;
+        q.x = *reinterpret_cast<uint32_t*>(&p0);
+        q.y = *reinterpret_cast<uint32_t*>(&p1);
+        *reinterpret_cast<uint2*>(g.rms_wb + off) = q;
+      }
+    }
+    __syncwarp();
+    if (k + 2 < kRmsChunks) issue(k + 2, buf);
+  }
+  if (DL_RMS_DIAG & 2) cp_async_wait<0>();
+  if (mvalid && nt == 0 && half == 0) g.rms_m[m] = mw;
+}
+
+template <bool A_MN, bool B_MN, bool RMS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 GemmDesc g, Sched sc) {
-  using C = Cfg2;
+  using C = Cfg2<RMS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -386,7 +563,11 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       fence_after();
       const int m = mt * 256 + (int)rank * 128 + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256;
-      epilogue_row<256>(g, taddr, m, nt, split, bad, half * 4, half * 4 + 4, 2 * nt + half);
+      if constexpr (RMS)
+        epilogue_rms(g, taddr, m, mt, nt, half, half * 4, 2 * sc.n_tiles, 16u * sc.n_tiles,
+                     sbase + C::EPI_OFF + (warp - 2) * C::EPI_WARP_BYTES);
+      else
+        epilogue_row<256>(g, taddr, m, nt, split, bad, half * 4, half * 4 + 4, 2 * nt + half);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_rank0(tempty(acc));
@@ -607,10 +788,28 @@ void launch(const GemmDesc& g, cudaStream_t st) {
   DL_CUDA(cudaGetLastError());
 }
 
-template <bool A_MN, bool B_MN>
+// Co-resident CTA pairs of the pair kernel (queried once per variant).
+template <bool A_MN, bool B_MN, bool RMS>
+int max_pairs() {
+  static const int n = [] {
+    auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS>;
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg2<RMS>::SMEM));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kNumSMs, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = Cfg2<RMS>::SMEM;
+    int k = 0;
+    DL_CUDA(cudaOccupancyMaxActiveClusters(&k, kern, &cfg));
+    return k;
+  }();
+  return n;
+}
+
+template <bool A_MN, bool B_MN, bool RMS>
 void launch2(const GemmDesc& g, cudaStream_t st) {
-  using C = Cfg2;
-  auto kern = tc_gemm2_kernel<A_MN, B_MN>;
+  using C = Cfg2<RMS>;
+  auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS>;
   static std::once_flag once;
   std::call_once(once, [&] {
     DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -627,7 +826,18 @@ void launch2(const GemmDesc& g, cudaStream_t st) {
              "tc gemm: k_splits not normalised with tc_splits()");
   sc.raster = g.raster;
   const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
-  const int pairs = std::min(total, kNumSMs / 2);
+  int pairs = std::min(total, kNumSMs / 2);
+  DL_REQUIRE(RMS == (g.rms != 0), 1, "pair kernel variant mismatch");
+  if (RMS) {
+    // every N tile of an M block in the same round (N-fastest raster, a
+    // multiple of n_tiles pairs), all pairs co-resident: the blocks'
+    // row-sum exchange spins on the other pairs
+    DL_REQUIRE(sc.raster == 1 && sc.k_splits == 1 && g.N % 256 == 0, 1,
+               "fused rmsprop epilogue: raster 1, no split-K, N % 256 == 0");
+    pairs = std::min((kNumSMs / 2 / sc.n_tiles) * sc.n_tiles, total);
+    DL_REQUIRE(pairs > 0 && (kNumSMs / 2 / sc.n_tiles) * sc.n_tiles <= (max_pairs<A_MN, B_MN, true>()),
+               1, "fused rmsprop epilogue: not enough co-resident CTA pairs");
+  }
   kern<<<2 * pairs, kThreads, C::SMEM, st>>>(ta, tb, g, sc);
   DL_CUDA(cudaGetLastError());
 }
@@ -650,6 +860,17 @@ int tc_n_tiles(int N) {
   return 2 * ((N + bn - 1) / bn);
 }
 
+// Whether the fused dW_out + dense rmsprop epilogue can run for an M x N
+// gradient (pair tiles, N a multiple of 256, enough co-resident pairs).
+// Queries occupancy: call outside stream capture.
+bool tc_rms_fusable(int M, int N) {
+  const char* e = std::getenv("DL_GEMM_2CTA");
+  if ((e && std::atoi(e) == 0) || N % 256 != 0 || M < 256) return false;
+  const int nt = N / 256;
+  const int pairs = (kNumSMs / 2 / nt) * nt;
+  return pairs > 0 && pairs <= tc::max_pairs<true, true, true>();
+}
+
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
   const int bn = g.N >= 256 ? 256 : (g.N >= 128 ? 128 : 64);
   const bool am = g.a_major == MN_MAJOR, bm = g.b_major == MN_MAJOR;
@@ -658,10 +879,13 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     return !(e && std::atoi(e) == 0);
   }();
   if (pair_ok && !g.no_pair && bn == 256 && g.M >= 256) {
-    if (!am && !bm) tc::launch2<false, false>(g, st);
-    else if (!am && bm) tc::launch2<false, true>(g, st);
-    else if (am && !bm) tc::launch2<true, false>(g, st);
-    else tc::launch2<true, true>(g, st);
+    if (g.rms) {
+      DL_REQUIRE(am && bm, 1, "fused rmsprop epilogue: dW_out operands are MN-major");
+      tc::launch2<true, true, true>(g, st);
+    } else if (!am && !bm) tc::launch2<false, false, false>(g, st);
+    else if (!am && bm) tc::launch2<false, true, false>(g, st);
+    else if (am && !bm) tc::launch2<true, false, false>(g, st);
+    else tc::launch2<true, true, false>(g, st);
     return (g.N + 255) / 256;
   }
 #define DL_TC_CASE(BN_)                                            \

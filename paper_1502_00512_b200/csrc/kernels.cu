@@ -481,27 +481,6 @@ __global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* _
   }
 }
 
-// float(eta * g / denom) exactly as the reference computes it (double
-// multiply, IEEE double divide, round to float), with one reciprocal per row
-// instead of a divide per element: q*inv is within 1.5 double ulps of the
-// correctly rounded quotient, so rounding it to float gives the same float
-// unless the quotient lies within a few double ulps of a float rounding
-// midpoint -- only then is the exact division performed.
-__device__ __forceinline__ float rms_step(double eta, float g, double denom, double inv) {
-  const double q = eta * (double)g;
-  const double r = q * inv;
-  const float f = (float)r;
-  const float af = fabsf(f);
-  if (!(af < 3.0e38f) || af < 1.0e-30f) return (float)(q / denom);  // inf/NaN/tiny: exact
-  const double up = (double)__int_as_float(__float_as_int(af) + 1) - (double)af;
-  const double dn = (double)af - (double)__int_as_float(__float_as_int(af) - 1);
-  const double ar = fabs(r), fd = (double)af;
-  const double tol = ar * 0x1p-49;
-  if (fabs(ar - (fd + 0.5 * up)) <= tol || fabs(ar - (fd - 0.5 * dn)) <= tol)
-    return (float)(q / denom);
-  return f;
-}
-
 // rmsprop.hpp:84 first loop: every W_in accumulator decays.
 __global__ void k_rms_decay(float* __restrict__ m, int64_t n, double rho,
                             const int* __restrict__ nonfinite) {

@@ -128,6 +128,13 @@ struct dl_ctx {
   // (measured neutral on B200: both contend for L2/HBM bandwidth)
   bool fork_out = false;
   bool logits_pair = true;  // DL_LOGITS_2CTA=0: single-CTA tiles for the logits GEMM
+  // trainer path: the dense W_out rmsprop runs inside the dW_out GEMM's
+  // epilogue (gemm_tc.cu epilogue_rms); DL_FUSE_OUT=0 keeps the separate
+  // kernel.  fuse_cap: -1 unknown, else whether the device can run it.
+  bool fuse_out = true;
+  bool fork_late = false;  // DL_FORK_LATE=1 (run_window late_eta)
+  int fuse_cap = -1;
+  unsigned* rms_cnt = nullptr;  // [ceil(Vo / 256)] per-M-block arrival counters
 
   // DP
   Comm* comm = nullptr;  // NcclComm (production) or LocalComm (single-device tests)
@@ -430,8 +437,11 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
 // Accumulates loss into d_loss and scored positions into d_pos.
 // fork_out_eta > 0: apply the dense W_out rmsprop with that eta on the side
 // stream as soon as dW_out is final (caller joins ev_join).
+// fuse_eta > 0: the dense W_out rmsprop with that eta runs inside the dW_out
+// GEMM's epilogue (fuse_ok); dh then runs first, as it reads this window's
+// W_out shadow, which the fused update overwrites in place.
 void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool grads,
-                double fork_out_eta = 0.0) {
+                double fork_out_eta = 0.0, double fuse_eta = 0.0, double late_eta = 0.0) {
   // V: input vocabulary (W_in rows); Vo: output rows held here (V / G when
   // the softmax is vocabulary-sharded)
   const int64_t H = c->H, V = c->V, Vo = c->Vo, TB = T * B, BH = B * H;
@@ -475,9 +485,34 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   if (!grads) return;
 
   DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
+  const bool fused = fuse_eta > 0.0;
+  // late fork: dh, then dW_out, then the dense update on the side stream
+  // (in place: dh has consumed this window's shadow), overlapping the
+  // latency-bound backward recurrence, dW_rec and the W_in rows
+  const bool late = late_eta > 0.0;
   // dW_out = dS^T . Hs  [V x H], clipped (rnn.hpp:256 matmul_tn_add; rnn.hpp:158-159)
-  {
+  auto dw_out = [&] {
     Phase p(c, "dw_out");
+    if (fused) {
+      // + the dense rmsprop of every row (rmsprop.hpp:94-107) in the epilogue
+      GemmDesc g = desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
+                        nullptr, H);
+      g.raster = 1;
+      g.clip = clip;
+      g.rowsq = c->rowsq;
+      g.rms = 1;
+      g.rms_w = c->w_out;
+      g.rms_wb = c->w_out_bf;
+      g.rms_m = c->m_out;
+      g.rms_cnt = c->rms_cnt;
+      g.rho = c->rho;
+      g.eps = c->eps;
+      g.eta = fuse_eta;
+      DL_CUDA(cudaMemsetAsync(c->rms_cnt, 0, ((Vo + 255) / 256) * sizeof(unsigned), st));
+      c->g16_valid = false;
+      gemm(c, g);
+      return;
+    }
     GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
                               c->g_out, H)
                        : desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
@@ -495,7 +530,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       g.rowsq = c->rowsq;
     }
     gemm(c, g);
-  }
+  };
+  if (!fused && !late) dw_out();
   if (dp) {
     // data parallel: sum dW_out over ranks, then clip --
     // on the communication stream, overlapping dh and the backward
@@ -513,7 +549,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // tensor-bound dh GEMM below.  It writes the fp32 master and the *other*
   // bf16 shadow, so dh keeps reading this window's W_out; the caller joins
   // ev_join and flips the shadows (swap_shadow).
-  if (fork_out_eta > 0.0) {
+  auto fork_update = [&](double eta, bf16* shadow) {
     DL_CUDA(cudaEventRecord(c->ev_fork, st));
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
     cudaEvent_t a = nullptr, b = nullptr;
@@ -523,20 +559,21 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       DL_CUDA(cudaEventRecord(a, c->st2));
     }
     if (c->g16_valid)
-      rms_dense_g16(c->w_out, c->w_out_bf_next, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, Vo, H,
-                    c->rho, c->eps, fork_out_eta, c->st2);
+      rms_dense_g16(c->w_out, shadow, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, Vo, H, c->rho,
+                    c->eps, eta, c->st2);
     else
-      rms_rows(c->w_out, c->w_out_bf_next, c->m_out, c->g_out, nullptr, nullptr, Vo, H, c->rho,
-               c->eps, fork_out_eta, 1, nullptr, c->st2);
+      rms_rows(c->w_out, shadow, c->m_out, c->g_out, nullptr, nullptr, Vo, H, c->rho, c->eps,
+               eta, 1, nullptr, c->st2);
     c->launches++;
     if (c->profiling) {
       DL_CUDA(cudaEventRecord(b, c->st2));
       c->pending.push_back({"rmsprop_out", {a, b}});
     }
     DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
-  }
+  };
+  if (fork_out_eta > 0.0) fork_update(fork_out_eta, c->w_out_bf_next);
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
-  {
+  auto dh = [&] {
     Phase p(c, "dh");
     const int s = pick_splits(c, (int)TB, (int)H, (int)Vo, 8);
     GemmDesc g = tc(c) ? desc((int)TB, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out_bf,
@@ -555,7 +592,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     } else {
       gemm(c, g);
     }
-  }
+  };
+  dh();
+  if (fused || late) dw_out();
+  if (late) fork_update(late_eta, c->w_out_bf);
   if (vs) {
     // each rank contracted its vocabulary block: dh_out = sum over ranks.
     // After this the backward recurrence, dW_rec and the W_in rows are
@@ -677,7 +717,7 @@ void alloc_output(dl_ctx* c) {
     p = nullptr;
   };
   fr(c->w_out); fr(c->m_out); fr(c->g_out); fr(c->w_out_bf); fr(c->w_out_bf_next);
-  fr(c->g_out_bf); fr(c->rowsq);
+  fr(c->g_out_bf); fr(c->rowsq); fr(c->rms_cnt);
   const int64_t Vo = c->Vo, H = c->H;
   c->w_out = dalloc<float>(Vo * H);
   c->m_out = dalloc<float>(Vo);
@@ -690,7 +730,9 @@ void alloc_output(dl_ctx* c) {
     c->g_out_bf = dalloc<bf16>(Vo * H);
     c->rowsq_n = tc_n_tiles((int)H);
     c->rowsq = dalloc<double>((size_t)c->rowsq_n * Vo);
+    c->rms_cnt = dalloc<unsigned>((Vo + 255) / 256);
   }
+  c->fuse_cap = -1;
   c->capT = c->capB = 0;  // window buffers re-size on the next call
   fr(c->htape);
   c->have_grads = false;
@@ -733,6 +775,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_FORK_OUT")) c->fork_out = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_LOGITS_2CTA")) c->logits_pair = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_G16")) c->g16 = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_FUSE_OUT")) c->fuse_out = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_FORK_LATE")) c->fork_late = std::atoi(e) != 0;
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
@@ -799,7 +843,7 @@ int dl_destroy(dl_ctx* c) {
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
                   c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
-                  c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all};
+                  c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1212,6 +1256,21 @@ int dl_trainer_set_state(dl_ctx* c, const int64_t* cursors, const float* hidden)
 }
 
 namespace {
+// The dense W_out update can run inside the dW_out epilogue when it cannot be
+// rejected (finite clip: every clipped component is finite), no dW_out
+// allreduce sits between the GEMM and the update (single GPU or vocabulary
+// shards) and the pair kernel has the whole device to itself.
+bool fuse_ok(dl_ctx* c) {
+  if (!(c->fuse_out && tc(c) && std::isfinite((float)c->clip))) return false;
+  if (c->comm && (!c->vshard || c->comm->shares_device())) return false;
+  if (c->fuse_cap < 0) c->fuse_cap = tc_rms_fusable((int)c->Vo, (int)c->H) ? 1 : 0;
+  return c->fuse_cap == 1;
+}
+
+bool late_ok(dl_ctx* c) {
+  return c->fork_late && tc(c) && std::isfinite((float)c->clip) && c->comm == nullptr;
+}
+
 bool fork_ok(dl_ctx* c) {
   return c->fork_out && tc(c) && c->w_out_bf_next && std::isfinite((float)c->clip) &&
          c->comm == nullptr;
@@ -1243,16 +1302,17 @@ void trainer_window(dl_ctx* c, double eta) {
   // the dense W_out update overlaps the dh GEMM when it cannot be rejected
   // (finite clip, see run_window), a second bf16 shadow exists and no
   // allreduce is pending
-  const bool fork = fork_ok(c);
-  run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0);
-  run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork);
+  const bool fuse = fuse_ok(c);
+  const bool late = !fuse && late_ok(c);
+  const bool fork = !fuse && !late && fork_ok(c);
+  run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0, fuse ? eta : 0.0,
+             late ? eta : 0.0);
+  run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork || fuse || late);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
                 c->L, act0(c->act), c->st);
   c->launches += 2;
-  if (fork) {
-    DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
-    swap_shadow(c);
-  }
+  if (fork || late) DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+  if (fork) swap_shadow(c);
 }
 }  // namespace
 
@@ -1270,7 +1330,7 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     if (graphs) {
       // one graph per W_out-shadow parity (the forked update writes the
       // other shadow, so consecutive windows alternate between two graphs)
-      const int nvar = fork_ok(c) ? 2 : 1;
+      const int nvar = !fuse_ok(c) && !late_ok(c) && fork_ok(c) ? 2 : 1;
       if (!c->graph || c->graph_eta != eta) {
         drop_graphs(c);
         c->graph_par0 = c->par;

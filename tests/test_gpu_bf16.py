@@ -116,3 +116,37 @@ def test_bf16_training_ppl_within_one_percent_of_reference(orc):
     assert t.logs[0].valid_ppl == pytest.approx(want["logs"][0][2], rel=1e-2)
     cur, _ = t.model.trainer_state()
     assert np.array_equal(cur, want["cursors"])
+
+
+@pytest.mark.parametrize("V,H", [(4000, 512), (1000, 256)])
+def test_fused_wout_rmsprop_matches_separate_kernel(orc, V, H):
+    """Trainer path: the dense W_out rmsprop inside the dW_out GEMM epilogue
+    (cross-tile row sums of squares, M tail) equals the separate fp32-gradient
+    update kernel to within summation-order rounding."""
+    import paper_1502_00512_b200 as dl
+    params = orc.init_uniform(V, H, 4)
+    ids = orc.random_stream(9, V, 40000)
+    out = []
+    for fuse in ("1", "0"):
+        os.environ["DL_FUSE_OUT"] = fuse
+        os.environ["DL_G16"] = "0"
+        try:
+            m = dl.GpuRnn(V, H, 0, "bf16")
+        finally:
+            os.environ.pop("DL_FUSE_OUT", None)
+            os.environ.pop("DL_G16", None)
+        m.set_params(*params)
+        m.set_opt(None, None, None, 0.9995, 1e-6)
+        m.trainer_init(ids, 4, 64, 8, 1.0)
+        loss, skipped = m.trainer_run(0, 3, 0.01)
+        out.append((loss, skipped, m.params(), m.opt()))
+        m.close()
+    (l1, s1, p1, o1), (l2, s2, p2, o2) = out
+    assert s1 == s2 == 0
+    assert l1 == pytest.approx(l2, rel=1e-4)
+    for a, b in zip(p1, p2):
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-6)
+    for a, b in zip(o1, o2):
+        np.testing.assert_allclose(a, b, rtol=1e-3, atol=1e-9)
+    # the update moved every W_out row (dense rmsprop)
+    assert np.all(np.abs(p1[2] - params[2]).max(axis=1) > 0)
