@@ -30,6 +30,7 @@ namespace dl {
 namespace tc {
 
 constexpr int kRecThreads = 256;
+constexpr int kRecCounters = 256;  // per-column-tile step counters (PersistParams::counter)
 
 struct RecParams {
   int M, N, K;          // rows (streams), H, H
@@ -248,7 +249,7 @@ struct PersistParams {
   const float* htape;     // bwd: h tape [T+1][M][N] (act' argument)
   float* out;             // fwd: htape (writes step s+1); bwd: dpre (writes step s)
   bf16* outb;
-  unsigned* counter;      // zeroed before the launch
+  unsigned* counter;      // [kRecCounters] per column-tile cluster, zeroed before the launch
 };
 
 template <int BN>
@@ -258,16 +259,27 @@ struct PersistCfg {
   static constexpr int PSTRIDE = BN + 4;
   static constexpr int PART = BM * PSTRIDE * 4;
   static constexpr int MAXKB = BN <= 64 ? 8 : 4;  // resident W_rec k-blocks per CTA
-  static constexpr int NA = 4;                    // A ring stages (streamed per step)
-  static constexpr int SMEM = NA * A_BLK + MAXKB * B_BLK + PART + 1024 + 256;
+  // A ring: every k-block of the CTA's K-slice in flight at once; the fp32
+  // partial reuses it once the step's MMAs have completed (peers read it
+  // before anyone passes the next step's dependency wait)
+  static constexpr int NA = MAXKB;
+  static constexpr int RING = NA * A_BLK > PART ? NA * A_BLK : PART;
+  static constexpr int SMEM = RING + MAXKB * B_BLK + 1024 + 256;
+  static constexpr int NPRE = 4;  // epilogue float4 operands prefetched per thread
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+__device__ __forceinline__ unsigned rec_ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
+// Step dependencies are tracked per producing cluster: counter[c] counts
+// the CTAs of column-tile cluster c that have published a step (S per
+// step).  The k-block of A holding columns [64 kb, 64 kb + 64) was written
+// by cluster 64 kb / BN, so each A load waits only for its own producers
+// -- no grid-wide barrier -- and the TMA stream starts as soon as the first
+// needed tile is out.
 template <int BN, bool B_MN>
 __global__ void __launch_bounds__(kRecThreads, 1)
 rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -277,9 +289,9 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;                                 // NA-stage ring of 16 KB
-  uint8_t* sB = smem + C::NA * C::A_BLK;              // kbs x B_BLK, resident
-  float* part = reinterpret_cast<float*>(sB + C::MAXKB * C::B_BLK);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(part) + C::PART);
+  uint8_t* sB = smem + C::RING;                       // kbs x B_BLK, resident
+  float* part = reinterpret_cast<float*>(sA);         // fp32 partial (after the MMAs)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::MAXKB * C::B_BLK);
   // bars: full[NA], empty[NA], barB, tfull
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::NA + 2);
   auto fullA = [&](int s) { return smem_u32(&bars[s]); };
@@ -289,7 +301,6 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const int rank = (int)cluster.block_rank();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nt = blockIdx.y;
-  const unsigned nctas = gridDim.x * gridDim.y;
 
   if (threadIdx.x == 32) {
     for (int s = 0; s < C::NA; ++s) { mbar_init(fullA(s), 1); mbar_init(emptyA(s), 1); }
@@ -312,6 +323,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const int kb0 = rank * p.kbs;
   const int rows = BM / p.S, r0 = rank * rows;
   constexpr int Q = BN / 4;
+  const int nwork = rows * Q;  // float4 outputs of this CTA per step
 
   // resident W_rec slice, loaded once
   if (warp == 0 && lane == 0) {
@@ -333,25 +345,54 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int s = p.mode == 0 ? j : p.T - 1 - j;   // time step written this iteration
     const bool gemm = p.mode == 0 || j > 0;        // bwd t = T-1 has no recurrent term
     const uint32_t ph = (p.mode == 0 ? j : j - 1) & 1;
+    // epilogue operands do not depend on the recurrence: issue their loads
+    // now so they land while this step waits for its inputs
+    float4 pre_a[C::NPRE], pre_b[C::NPRE];
+#pragma unroll
+    for (int k = 0; k < C::NPRE; ++k) {
+      const int idx = threadIdx.x + k * kRecThreads;
+      if (idx >= nwork) break;
+      const int m = r0 + idx / Q, n = nt * BN + 4 * (idx % Q);
+      if (m >= p.M || n >= p.N) continue;
+      const int64_t o = static_cast<int64_t>(m) * p.N + n;
+      if (p.mode == 0) {
+        pre_a[k] = *reinterpret_cast<const float4*>(
+            p.w_in + static_cast<int64_t>(p.x[s * p.M + m]) * p.N + n);
+      } else {
+        pre_a[k] = *reinterpret_cast<const float4*>(p.dh_out + s * p.MN + o);
+        pre_b[k] = *reinterpret_cast<const float4*>(p.htape + (s + 1) * p.MN + o);
+      }
+    }
     if (gemm) {
-      if (warp == 0 && lane == 0) {
-        // wait until every CTA has published the previous step
-        if (j > 0) {
-          const unsigned target = nctas * (unsigned)j;
-          long spins = 0;
-          while (ld_acquire(p.counter) < target) {
-            __nanosleep(20);
-            if (++spins > (1l << 26)) __trap();  // never hang the GPU
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
+      if (warp == 0) {
         const int arow = p.mode == 0 ? s * p.M : (s + 1) * p.M;
-        for (int i = 0; i < p.kbs; ++i) {
-          mbar_wait(emptyA(a_stage), a_phase ^ 1);
-          mbar_expect_tx(fullA(a_stage), C::A_BLK);
-          tma_load_2d(smem_u32(sA + a_stage * C::A_BLK), &tmA, fullA(a_stage), (kb0 + i) * BK,
-                      arow);
-          if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
+        const unsigned target = (unsigned)p.S * (unsigned)j;
+        if (j > 0) {
+          // wait for (a) my cluster peers -- they have finished reading my
+          // partial, which lives in the A ring these loads overwrite -- and
+          // (b) the producers of each k-block of my K-slice.  Lane i < kbs
+          // polls k-block i's producer counter, lane kbs my own cluster's,
+          // all in parallel (acquire loads: a fence would also wait for the
+          // in-flight epilogue prefetches)
+          const unsigned* cnt = lane < p.kbs ? p.counter + ((kb0 + lane) * BK) / BN
+                                             : p.counter + nt;
+          long spins = 0;
+          bool ok = lane > p.kbs;
+          while (!__all_sync(0xffffffffu, ok)) {
+            if (!ok) ok = rec_ld_acquire(cnt) >= target;
+            if (++spins > (1l << 28)) __trap();
+          }
+          __syncwarp();  // order lane 0's loads after every lane's acquire
+        }
+        if (lane == 0) {
+          if (j > 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+          for (int i = 0; i < p.kbs; ++i) {
+            mbar_wait(emptyA(a_stage), a_phase ^ 1);
+            mbar_expect_tx(fullA(a_stage), C::A_BLK);
+            tma_load_2d(smem_u32(sA + a_stage * C::A_BLK), &tmA, fullA(a_stage), (kb0 + i) * BK,
+                        arow);
+            if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
+          }
         }
       } else if (warp == 1 && lane == 0) {
         constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
@@ -380,6 +421,8 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       mbar_wait(tfull, ph);
       fence_after();
       {
+        // the A ring is idle now (all MMAs of the step completed): drain the
+        // accumulator into it as this CTA's fp32 partial
         const int quarter = warp % 4, half = warp / 4;
         float* prow = part + (quarter * 32 + lane) * C::PSTRIDE;
 #pragma unroll 1
@@ -396,7 +439,10 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       cluster.sync();
     }
     // reduce my row slice over the cluster (rank order) + fused epilogue
-    for (int idx = threadIdx.x; idx < rows * Q; idx += kRecThreads) {
+#pragma unroll 1
+    for (int k = 0; k * kRecThreads < nwork; ++k) {
+      const int idx = threadIdx.x + k * kRecThreads;
+      if (idx >= nwork) break;
       const int row = r0 + idx / Q, col = 4 * (idx % Q);
       const int m = row, n = nt * BN + col;
       if (m >= p.M || n >= p.N) continue;
@@ -408,21 +454,30 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
       const int64_t o = static_cast<int64_t>(m) * p.N + n;
+      float4 ea, eb;
+      if (k < C::NPRE) {
+        // (k is uniform, the prefetch arrays are indexed by a constant)
+#pragma unroll
+        for (int kk = 0; kk < C::NPRE; ++kk)
+          if (kk == k) { ea = pre_a[kk]; eb = pre_b[kk]; }
+      } else if (p.mode == 0) {
+        ea = *reinterpret_cast<const float4*>(
+            p.w_in + static_cast<int64_t>(p.x[s * p.M + m]) * p.N + n);
+      } else {
+        ea = *reinterpret_cast<const float4*>(p.dh_out + s * p.MN + o);
+        eb = *reinterpret_cast<const float4*>(p.htape + (s + 1) * p.MN + o);
+      }
       float4 y;
       int64_t oo;
       if (p.mode == 0) {
-        const float4 e = *reinterpret_cast<const float4*>(
-            p.w_in + static_cast<int64_t>(p.x[s * p.M + m]) * p.N + n);
-        y = make_float4(act_f(p.act, acc.x + e.x), act_f(p.act, acc.y + e.y),
-                        act_f(p.act, acc.z + e.z), act_f(p.act, acc.w + e.w));
+        y = make_float4(act_f(p.act, acc.x + ea.x), act_f(p.act, acc.y + ea.y),
+                        act_f(p.act, acc.z + ea.z), act_f(p.act, acc.w + ea.w));
         oo = (s + 1) * p.MN + o;
       } else {
-        const float4 d = *reinterpret_cast<const float4*>(p.dh_out + s * p.MN + o);
-        const float4 h = *reinterpret_cast<const float4*>(p.htape + (s + 1) * p.MN + o);
-        y = make_float4((acc.x + d.x) * act_deriv_f(p.act, h.x),
-                        (acc.y + d.y) * act_deriv_f(p.act, h.y),
-                        (acc.z + d.z) * act_deriv_f(p.act, h.z),
-                        (acc.w + d.w) * act_deriv_f(p.act, h.w));
+        y = make_float4((acc.x + ea.x) * act_deriv_f(p.act, eb.x),
+                        (acc.y + ea.y) * act_deriv_f(p.act, eb.y),
+                        (acc.z + ea.z) * act_deriv_f(p.act, eb.z),
+                        (acc.w + ea.w) * act_deriv_f(p.act, eb.w));
         oo = s * p.MN + o;
       }
       *reinterpret_cast<float4*>(p.out + oo) = y;
@@ -430,11 +485,12 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       ob[0] = __floats2bfloat162_rn(y.x, y.y);
       ob[1] = __floats2bfloat162_rn(y.z, y.w);
     }
-    // publish this step (generic stores -> visible to the next step's TMA)
+    // publish this step to the consumers of this column tile (generic
+    // stores -> visible to their TMA loads)
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(p.counter, 1u);
+    if (threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counter + nt) : "memory");
   }
   cluster.sync();  // peers are done reading my shared memory
   if (warp == 0) {
@@ -482,7 +538,8 @@ bool persist_launch(const void* A_tape, int64_t a_rows, const void* Bw, PersistP
   }
   const int need = (int)(cfg.gridDim.x * cfg.gridDim.y / p.S);
   if (max_clusters[si] < need) return false;
-  DL_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned), st));
+  DL_REQUIRE((p.N + BN - 1) / BN <= kRecCounters, 1, "recurrence: too many column tiles");
+  DL_CUDA(cudaMemsetAsync(p.counter, 0, kRecCounters * sizeof(unsigned), st));
   DL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return true;
 }

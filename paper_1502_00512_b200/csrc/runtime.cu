@@ -807,7 +807,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->d_loss = dalloc<double>(1);
     c->d_pos = dalloc<unsigned long long>(1);
     c->d_skipped = dalloc<unsigned long long>(1);
-    c->bar_counter = dalloc<unsigned>(1);
+    c->bar_counter = dalloc<unsigned>(256);  // rec_tc.cu kRecCounters
     c->win_loss = dalloc<double>(2);
     c->win_pos = reinterpret_cast<unsigned long long*>(c->win_loss + 1);
     c->win_counter = dalloc<int64_t>(1);
