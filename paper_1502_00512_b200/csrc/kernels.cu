@@ -345,6 +345,7 @@ __global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restri
 // and the global stream index is r*B + b, so processing order i maps to
 // t = T-1 - i/(G*B), r = (i % (G*B)) / B, b = i % B.
 constexpr int kSortThreads = 1024;
+constexpr int kEmbedShort = 8;  // segments up to this many rows: k_embed_short
 
 __device__ __forceinline__ int64_t gathered_pos(int64_t i, int64_t T, int64_t B, int64_t G) {
   const int64_t GB = G * B;
@@ -372,7 +373,8 @@ template <int IPT>
 __global__ void __launch_bounds__(kSortThreads)
 k_embed_radix(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, int end_bit,
               int* __restrict__ seg_start, int* __restrict__ n_seg, int* __restrict__ order_pos,
-              uint32_t* __restrict__ seg_word) {
+              uint32_t* __restrict__ seg_word, int* __restrict__ long_list,
+              int* __restrict__ n_long) {
   using R = EmbedRadix<IPT>;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   typename R::Smem& sm = *reinterpret_cast<typename R::Smem*>(sm_raw);
@@ -415,38 +417,121 @@ k_embed_radix(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, i
     *n_seg = total;
     seg_start[total] = n;
   }
+  // the segments longer than kEmbedShort rows, for k_embed_long (any order)
+  __shared__ int n_long_sm;
+  if (threadIdx.x == 0) n_long_sm = 0;
+  __syncthreads();
+  for (int sl = threadIdx.x; sl < total; sl += kSortThreads)
+    if (seg_start[sl + 1] - seg_start[sl] > kEmbedShort) long_list[atomicAdd(&n_long_sm, 1)] = sl;
+  __syncthreads();
+  if (threadIdx.x == 0) *n_long = n_long_sm;
 }
 
-// Row sums per segment in processing order, then clip (rnn.hpp:155-162).
-// Grid-stride over slots; threads cover the H columns of one slot.
-__global__ void k_embed_rows(const float* __restrict__ dpre, int64_t H,
-                             const int* __restrict__ seg_start, const int* __restrict__ n_seg,
-                             const int* __restrict__ order_pos, float* __restrict__ rows,
-                             float clip, int* nonfinite) {
-  const int ns = *n_seg;
+// Row sums per segment in processing order, then clip (rnn.hpp:155-162),
+// in two kernels by segment length:
+//   k_embed_short: a warp per (segment of <= kEmbedShort rows, 1024-column
+//     chunk), grid-stride; each row's columns are 8 float4 loads per lane,
+//     all in flight, rows added in order;
+//   k_embed_long: a block per (long segment, 32-column chunk); the block's 8
+//     warps stage up to 256 rows x 32 columns in shared memory with every
+//     load in flight (lane = column), then warp 0 adds them in order.
+// Both sum every word's rows in exactly the reference's float order.
+constexpr int kShortWarps = 8;     // warps per k_embed_short block
+constexpr int kLongRows = 256;     // rows staged per pass in k_embed_long
+
+__global__ void __launch_bounds__(32 * kShortWarps)
+k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__ seg_start,
+              const int* __restrict__ n_seg, const int* __restrict__ order_pos,
+              float* __restrict__ rows, float clip, int* nonfinite) {
+  const int ns = __ldg(n_seg);
+  const int lane = threadIdx.x % 32;
+  const int64_t nchunk = (H + 1023) / 1024;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
   bool bad = false;
-  for (int slot = blockIdx.x; slot < ns; slot += gridDim.x) {
-    const int a = seg_start[slot], e = seg_start[slot + 1];
-    for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < H;
-         j += (int64_t)gridDim.y * blockDim.x) {
-      float acc = 0.f;
-      if (e - a <= 2) {
-        // most words occur once or twice per window
-        acc += 1.0f * dpre[(int64_t)order_pos[a] * H + j];
-        if (e - a == 2) acc += 1.0f * dpre[(int64_t)order_pos[a + 1] * H + j];
-      } else {
-        // frequent words (bos/eos) own long segments: issue 16 independent
-        // loads per batch, then add them in the reference's order
-        for (int i = a; i < e; i += 16) {
-          float v[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u)
-            v[u] = i + u < e ? dpre[(int64_t)order_pos[i + u] * H + j] : 0.f;
-#pragma unroll
-          for (int u = 0; u < 16; ++u)
-            if (i + u < e) acc += 1.0f * v[u];
-        }
+  for (int64_t w = gw; w < ns * nchunk; w += nw) {
+    const int slot = (int)(w / nchunk);
+    const int64_t c0 = (w % nchunk) * 1024;
+    const int a = __ldg(seg_start + slot), e = __ldg(seg_start + slot + 1);
+    if (e - a > kEmbedShort) continue;  // k_embed_long
+    if ((H % 4) != 0) {
+      // unaligned rows: one column per lane
+      for (int64_t j = c0 + lane; j < min(H, c0 + 1024); j += 32) {
+        float acc = 0.f;
+        for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
+        acc = clip1(acc, clip);
+        bad |= !isfinite(acc);
+        rows[(int64_t)slot * H + j] = acc;
       }
+      continue;
+    }
+    float4 acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = a; i < e; ++i) {
+      const float* src = dpre + (int64_t)__ldg(order_pos + i) * H;
+      float4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t j = c0 + 4 * (lane + 32 * q);
+        if (j < H) v[q] = __ldg(reinterpret_cast<const float4*>(src + j));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        acc[q].x += 1.0f * v[q].x;
+        acc[q].y += 1.0f * v[q].y;
+        acc[q].z += 1.0f * v[q].z;
+        acc[q].w += 1.0f * v[q].w;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = c0 + 4 * (lane + 32 * q);
+      if (j >= H) continue;
+      const float4 o = make_float4(clip1(acc[q].x, clip), clip1(acc[q].y, clip),
+                                   clip1(acc[q].z, clip), clip1(acc[q].w, clip));
+      bad |= !isfinite(o.x) || !isfinite(o.y) || !isfinite(o.z) || !isfinite(o.w);
+      *reinterpret_cast<float4*>(rows + (int64_t)slot * H + j) = o;
+    }
+  }
+  if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+}
+
+__global__ void __launch_bounds__(256)
+k_embed_long(const float* __restrict__ dpre, int64_t H, const int* __restrict__ seg_start,
+             const int* __restrict__ long_list, const int* __restrict__ n_long,
+             const int* __restrict__ order_pos, float* __restrict__ rows, float clip,
+             int* nonfinite) {
+  __shared__ float tile[kLongRows][32];
+  __shared__ int spos[kLongRows];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t nchunk = (H + 31) / 32;
+  const int64_t items = (int64_t)__ldg(n_long) * nchunk;
+  bool bad = false;
+  // grid-stride over (long segment, 32-column chunk)
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int slot = __ldg(long_list + it / nchunk);
+    const int64_t j = (it % nchunk) * 32 + lane;
+    const int a = __ldg(seg_start + slot), e = __ldg(seg_start + slot + 1);
+    float acc = 0.f;
+    for (int base = a; base < e; base += kLongRows) {
+      const int cnt = min(kLongRows, e - base);
+      if (threadIdx.x < cnt) spos[threadIdx.x] = __ldg(order_pos + base + threadIdx.x);
+      __syncthreads();
+      float v[kLongRows / 8];
+#pragma unroll
+      for (int u = 0; u < kLongRows / 8; ++u) {
+        const int r = warp + 8 * u;
+        v[u] = (r < cnt && j < H) ? __ldg(dpre + (int64_t)spos[r] * H + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kLongRows / 8; ++u) tile[warp + 8 * u][lane] = v[u];
+      __syncthreads();
+      if (warp == 0)
+        for (int r = 0; r < cnt; ++r) acc += 1.0f * tile[r][lane];
+      __syncthreads();
+    }
+    if (warp == 0 && j < H) {
       acc = clip1(acc, clip);
       bad |= !isfinite(acc);
       rows[(int64_t)slot * H + j] = acc;
@@ -470,12 +555,35 @@ __global__ void k_rms_rec(float* __restrict__ w, bf16* __restrict__ wb, float* _
                           const float* __restrict__ g, int64_t n, double rho, double eps,
                           double eta, const int* __restrict__ nonfinite) {
   if (nonfinite && *nonfinite) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double gi = (double)g[i];
-    const float mi = (float)(rho * (double)m[i] + (1.0 - rho) * gi * gi);
+  auto one = [&](float& wi, float& mi, float gf) {
+    const double gi = (double)gf;
+    mi = (float)(rho * (double)mi + (1.0 - rho) * gi * gi);
+    wi = wi - (float)(eta * gi / sqrt((double)mi + eps));
+  };
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = (n % 4) == 0 ? n / 4 : 0;
+  // four independent elements per thread (float4), all loads issued first
+  for (int64_t i = tid; i < n4; i += nth) {
+    const float4 gq = reinterpret_cast<const float4*>(g)[i];
+    float4 mq = reinterpret_cast<float4*>(m)[i];
+    float4 wq = reinterpret_cast<float4*>(w)[i];
+    one(wq.x, mq.x, gq.x);
+    one(wq.y, mq.y, gq.y);
+    one(wq.z, mq.z, gq.z);
+    one(wq.w, mq.w, gq.w);
+    reinterpret_cast<float4*>(m)[i] = mq;
+    reinterpret_cast<float4*>(w)[i] = wq;
+    if (wb) {
+      __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + 4 * i);
+      b2[0] = __floats2bfloat162_rn(wq.x, wq.y);
+      b2[1] = __floats2bfloat162_rn(wq.z, wq.w);
+    }
+  }
+  for (int64_t i = 4 * n4 + tid; i < n; i += nth) {
+    float wi = w[i], mi = m[i];
+    one(wi, mi, g[i]);
     m[i] = mi;
-    const float wi = w[i] - (float)(eta * gi / sqrt((double)mi + eps));
     w[i] = wi;
     if (wb) wb[i] = __float2bfloat16_rn(wi);
   }
@@ -795,9 +903,8 @@ void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st) {
   k_sum_rows<<<1, 1024, 0, st>>>(v, wts, n, acc, cnt);
 }
-void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre, int64_t H,
-                 float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
-                 int* nonfinite, cudaStream_t st) {
+void embed_sort(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, EmbedWs& ws,
+                uint32_t* words, int* n_rows, cudaStream_t st) {
   const int64_t n = G * T * B;
   DL_REQUIRE(n <= 16 * kSortThreads, 1, "window too large for the embedding sort (G*T*B <= 16384)");
   int end_bit = 1;
@@ -812,14 +919,27 @@ void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, 
       attr = true;                                                                             \
     }                                                                                          \
     k_embed_radix<IPT><<<1, kSortThreads, smem, st>>>(x, T, B, G, end_bit, ws.seg_start,       \
-                                                      n_rows, ws.order_pos, words);            \
+                                                      n_rows, ws.order_pos, words,             \
+                                                      ws.long_list(), ws.n_long());            \
   } else
   DL_RADIX(2) DL_RADIX(4) DL_RADIX(8) DL_RADIX(16) {}
 #undef DL_RADIX
-  const unsigned gy = (unsigned)((H + 255) / 256);
-  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (148 * 16) / gy));
-  k_embed_rows<<<dim3(gx, gy), 256, 0, st>>>(dpre, H, ws.seg_start, n_rows, ws.order_pos, rows,
-                                             clip, nonfinite);
+}
+void embed_rows(int64_t n, const float* dpre, int64_t H, float clip, EmbedWs& ws, float* rows,
+                int* n_rows, int* nonfinite, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t nchunk = (H + 1023) / 1024;
+  const int64_t warps = std::min<int64_t>(n * nchunk, 148 * 64);
+  k_embed_short<<<(unsigned)((warps + kShortWarps - 1) / kShortWarps), 32 * kShortWarps, 0, st>>>(
+      dpre, H, ws.seg_start, n_rows, ws.order_pos, rows, clip, nonfinite);
+  k_embed_long<<<148 * 2, 256, 0, st>>>(
+      dpre, H, ws.seg_start, ws.long_list(), ws.n_long(), ws.order_pos, rows, clip, nonfinite);
+}
+void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre,
+                 int64_t H, float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
+                 int* nonfinite, cudaStream_t st) {
+  embed_sort(x, T, B, G, V, ws, words, n_rows, st);
+  embed_rows(G * T * B, dpre, H, clip, ws, rows, n_rows, nonfinite, st);
 }
 void embed_dense(const float* rows, const uint32_t* words, const int* n_rows, int64_t max_rows,
                  int64_t H, float* dense, cudaStream_t st) {

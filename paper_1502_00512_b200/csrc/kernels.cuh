@@ -8,8 +8,11 @@
 namespace dl {
 
 struct EmbedWs {
-  int* seg_start;  // [T*B + 1]
+  int* seg_start;  // [T*B + 1] segment heads, then [T*B] long-segment slots, then their count
   int* order_pos;  // [T*B]
+  int* long_list() const { return seg_start + cap + 1; }
+  int* n_long() const { return seg_start + 2 * cap + 1; }
+  int64_t cap;     // T*B (positions the buffers hold)
 };
 
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
@@ -38,6 +41,13 @@ void block_lse_f32(const float* S, int64_t M, int64_t V, const uint32_t* loc, do
 void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
               unsigned long long* cnt, cudaStream_t st);
 // x / dpre: G rank-blocked windows [G][T][B] (G = 1 on one GPU)
+// W_in gradient rows: embed_sort (stable radix sort of the window's ids,
+// depends on x only) then embed_rows (segmented sums of dpre + clip);
+// embed_grads = both
+void embed_sort(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, EmbedWs& ws,
+                uint32_t* words, int* n_rows, cudaStream_t st);
+void embed_rows(int64_t n, const float* dpre, int64_t H, float clip, EmbedWs& ws, float* rows,
+                int* n_rows, int* nonfinite, cudaStream_t st);
 void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st);

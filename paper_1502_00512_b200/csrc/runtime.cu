@@ -78,6 +78,7 @@ struct dl_ctx {
   bool g16 = true, g16_valid = false;
   cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_sort_fork = nullptr, ev_sort_join = nullptr;  // W_in id sort on st2
 
   // window workspace
   int64_t capT = 0, capB = 0;
@@ -264,8 +265,9 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   c->dpre = dalloc<float>(TB * H);
   c->g_in_rows = dalloc<float>(G * TB * H);
   c->g_in_words = dalloc<uint32_t>(G * TB);
-  c->ews.seg_start = dalloc<int>(G * TB + 1);
+  c->ews.seg_start = dalloc<int>(2 * G * TB + 2);
   c->ews.order_pos = dalloc<int>(G * TB);
+  c->ews.cap = G * TB;
   c->h0_d = dalloc<float>(nB * H);
   if (G > 1) {
     c->x_all = dalloc<uint32_t>(G * TB);
@@ -446,6 +448,15 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // the softmax is vocabulary-sharded)
   const int64_t H = c->H, V = c->V, Vo = c->Vo, TB = T * B, BH = B * H;
   cudaStream_t st = c->st;
+  if (grads && !(c->comm != nullptr && !c->vshard)) {
+    // the W_in gradient's id sort depends on x only: run it on the side
+    // stream under the forward recurrence (which leaves SMs free) (joined before embed_rows)
+    DL_CUDA(cudaEventRecord(c->ev_sort_fork, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_sort_fork, 0));
+    embed_sort(c->x_d, T, B, 1, V, c->ews, c->g_in_words, c->g_in_n, c->st2);
+    c->launches++;
+    DL_CUDA(cudaEventRecord(c->ev_sort_join, c->st2));
+  }
   if (tc(c)) {
     f32_to_bf16(c->htape, c->htape_bf, BH, st);
     c->launches++;
@@ -669,12 +680,13 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     Phase p(c, "embed_grad");
     embed_grads(c->x_all, T, B, G, V, c->dpre_all, H, clip, c->ews, c->g_in_rows, c->g_in_words,
                 c->g_in_n, c->nonfinite, st);
-    c->launches += 2;
+    c->launches += 3;
   } else {
-    // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped
+    // W_in rows (rnn.hpp:218-222) -- deterministic segmented sum, clipped;
+    // the id sort was forked at the start of the window
+    DL_CUDA(cudaStreamWaitEvent(st, c->ev_sort_join, 0));
     Phase p(c, "embed_grad");
-    embed_grads(c->x_d, T, B, 1, V, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_words,
-                c->g_in_n, c->nonfinite, st);
+    embed_rows(TB, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   }
   // a non-finite dW_out block on one rank must skip the update everywhere
@@ -794,6 +806,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_lo));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_fork, cudaEventDisableTiming));
+    DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_join, cudaEventDisableTiming));
     c->w_in = dalloc<float>(V * H);
     c->w_rec = dalloc<float>(H * H);
     c->m_rec = dalloc<float>(H * H);
@@ -848,6 +862,8 @@ int dl_destroy(dl_ctx* c) {
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
+  if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->st2) cudaStreamDestroy(c->st2);
@@ -1464,7 +1480,7 @@ int dl_test_embed(dl_ctx* c, int G, int64_t T, int64_t B, const uint32_t* x_all,
     float* rows = dalloc<float>(n * H);
     uint32_t* words = dalloc<uint32_t>(n);
     int* nr = dalloc<int>(1);
-    EmbedWs ws{dalloc<int>(n + 1), dalloc<int>(n)};
+    EmbedWs ws{dalloc<int>(2 * n + 2), dalloc<int>(n), n};
     float* dense = dalloc<float>(c->V * H);
     DL_CUDA(cudaMemcpyAsync(x, x_all, n * 4, cudaMemcpyHostToDevice, c->st));
     DL_CUDA(cudaMemcpyAsync(d, dpre_all, n * H * 4, cudaMemcpyHostToDevice, c->st));
