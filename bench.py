@@ -372,25 +372,33 @@ def main():
         roofline["note"] = ("dW_out GEMM with the dense W_out rmsprop fused into its epilogue "
                             "(+10 B/elem of W_out: fp32 master read+write, bf16 shadow write)")
 
-    # end-to-end through the public API with host buffers: dl_window (H2D of
-    # the window ids/targets/mask/h0 from host, D2H of loss + h_final) then
-    # dl_rmsprop, per step
+    # end-to-end through the public API with host buffers: dl_train_window
+    # per step (H2D of the window ids/targets/mask/h0 from host, bptt_run +
+    # rmsprop_update, D2H of loss, positions, applied and h_final)
     e2e = None
     if args.e2e_steps > 0:
+        def pinned(shape, dtype):
+            return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+        # each step's window and the carried hidden state live in page-locked
+        # host memory (the copies themselves are inside the timed region)
         wins = []
         for i in range(args.e2e_steps + 1):
             s0 = (i * TB * 7) % (L - TB - 2)
-            x = ids[s0:s0 + TB].reshape(T, B)
-            y = ids[s0 + 1:s0 + 1 + TB].reshape(T, B)
-            wins.append(dl.WindowBatch(x, y, (y != 1).astype(np.uint8)))
-        h0 = np.full((B, H), 0.5, np.float32)
-        dl.bptt_run(model, wins[0], h0, 1.0 / TB, 1.0)
-        dl.rmsprop_update(model, eta)
+            x, y, w = pinned((T, B), torch.int32), pinned((T, B), torch.int32), \
+                pinned((T, B), torch.uint8)
+            x[:] = ids[s0:s0 + TB].reshape(T, B)
+            y[:] = ids[s0 + 1:s0 + 1 + TB].reshape(T, B)
+            w[:] = y != 1
+            wins.append(dl.WindowBatch(x.view(np.uint32), y.view(np.uint32), w))
+        hbuf = [pinned((B, H), torch.float32) for _ in range(2)]
+        hbuf[0][:] = 0.5
+        dl.train_window(model, wins[0], hbuf[0], 1.0 / TB, 1.0, eta, h_final=hbuf[1])
         barrier()
         t0 = time.perf_counter()
-        for wb in wins[1:]:
-            res, h0 = dl.bptt_run(model, wb, h0, 1.0 / TB, 1.0)
-            dl.rmsprop_update(model, eta)
+        for i, wb in enumerate(wins[1:]):
+            dl.train_window(model, wb, hbuf[(i + 1) % 2], 1.0 / TB, 1.0, eta,
+                            h_final=hbuf[i % 2])
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device="cuda")
@@ -398,7 +406,7 @@ def main():
             dt = float(t.item())
         e2e = {"value": world * TB * args.e2e_steps / dt, "unit": "words/s",
                "h2d_bytes_per_step": TB * 9 + B * H * 4, "d2h_bytes_per_step": B * H * 4 + 8 + 8 + 4,
-               "api": "dl_window + dl_rmsprop (host arrays)"}
+               "api": "dl_train_window (bptt_run + rmsprop_update), page-locked host arrays"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -99,6 +99,17 @@ int dl_set_grads(dl_ctx* ctx, int64_t n_in_rows, const uint32_t* in_words,
  * (non-finite gradient: parameters and accumulators untouched). */
 int dl_rmsprop(dl_ctx* ctx, double eta, int* applied);
 
+/* One training step of Trainer::run_epoch (trainer.hpp:391-397): bptt_run on
+ * the window (as dl_window with compute_grads = 1) followed by
+ * Traits::update = rmsprop_update (rmsprop.hpp:113-133) with eta.  Same
+ * results as dl_window + dl_rmsprop; in DL_BF16 mode with a finite clip the
+ * dense W_out update runs inside the dW_out GEMM's epilogue (the gradient is
+ * never stored).  *applied as for dl_rmsprop. */
+int dl_train_window(dl_ctx* ctx, int64_t T, int64_t B, const uint32_t* inputs,
+                    const uint32_t* targets, const uint8_t* weights,
+                    const float* h0, float* h_final, double loss_scale, float clip,
+                    double eta, double* loss, uint64_t* positions, int* applied);
+
 /* ---- scoring ------------------------------------------------------------ */
 
 /* Lock-step forward scorer over S streams for `steps` steps (the inner loop

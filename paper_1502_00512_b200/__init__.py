@@ -39,7 +39,7 @@ from ._lib import DL_BF16, DL_FP32, DataError, DeviceError, check, load
 
 __all__ = [
     "GpuRnn", "WindowBatch", "BpttResult", "PerplexityResult", "bptt_run",
-    "rmsprop_update", "sharded_perplexity", "rnn_perplexity", "score",
+    "rmsprop_update", "train_window", "sharded_perplexity", "rnn_perplexity", "score",
     "TrainConfig", "EpochLog", "Trainer", "DataError", "DeviceError", "formats",
     "param_count", "make_vocab", "KSIGMOID", "KTANH", "rescore_nbest",
     "read_nbest", "write_nbest", "NBestHyp", "NBestUtt",
@@ -288,6 +288,32 @@ def bptt_run(model: GpuRnn, wb: WindowBatch, h0, loss_scale: float = 1.0,
                                 float(loss_scale), float(clip), int(compute_grads),
                                 C.byref(loss), C.byref(pos)))
     return BpttResult(loss.value, pos.value), hf
+
+
+def train_window(model: GpuRnn, wb: WindowBatch, h0, loss_scale: float, clip: float,
+                 eta: float, h_final=None):
+    """One Trainer::run_epoch step (trainer.hpp:391-397): bptt_run then
+    rmsprop_update in one call (dl_train_window); returns (BpttResult,
+    h_final, applied).  h_final: optional float32 [B, H] output buffer
+    (page-locked buffers -- inputs too -- are DMA'd without staging)."""
+    x = np.ascontiguousarray(wb.inputs, np.uint32)
+    y = np.ascontiguousarray(wb.targets, np.uint32)
+    w = np.ascontiguousarray(wb.weights, np.uint8)
+    if x.shape != y.shape or x.shape != w.shape or x.ndim != 2:
+        raise ValueError("bptt: window size mismatch")
+    T, B = x.shape
+    h0 = np.ascontiguousarray(h0, np.float32)
+    if h0.shape != (B, model.H):
+        raise ValueError("bptt: initial state shape mismatch")
+    hf = np.empty((B, model.H), np.float32) if h_final is None else h_final
+    if hf.shape != (B, model.H) or hf.dtype != np.float32 or not hf.flags.c_contiguous:
+        raise ValueError("h_final: float32 [B, H] C-contiguous buffer expected")
+    loss, pos, applied = C.c_double(), C.c_uint64(), C.c_int()
+    model._chk(load().dl_train_window(model.handle, T, B, x.ctypes.data, y.ctypes.data,
+                                      w.ctypes.data, h0.ctypes.data, hf.ctypes.data,
+                                      float(loss_scale), float(clip), float(eta),
+                                      C.byref(loss), C.byref(pos), C.byref(applied)))
+    return BpttResult(loss.value, pos.value), hf, bool(applied.value)
 
 
 def rmsprop_update(model: GpuRnn, eta: float) -> bool:

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("DL_LIB_PATH", LIB_PATH)
 EXPORTS = (
     "dl_last_error", "dl_version", "dl_create", "dl_destroy", "dl_set_params",
     "dl_get_params", "dl_set_opt", "dl_get_opt", "dl_window", "dl_get_grads", "dl_set_grads",
-    "dl_rmsprop", "dl_score", "dl_sharded_perplexity", "dl_rnn_perplexity",
+    "dl_rmsprop", "dl_train_window", "dl_score", "dl_sharded_perplexity", "dl_rnn_perplexity",
     "dl_trainer_init", "dl_trainer_run", "dl_trainer_get_state",
     "dl_trainer_set_state", "dl_comm_unique_id", "dl_comm_init",
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
@@ -63,6 +63,8 @@ def load():
         "dl_get_grads": (C.c_int, [vp, vp, vp, vp]),
         "dl_set_grads": (C.c_int, [vp, i64, vp, vp, vp, vp]),
         "dl_rmsprop": (C.c_int, [vp, C.c_double, P(C.c_int)]),
+        "dl_train_window": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, C.c_double, C.c_float,
+                                      C.c_double, P(C.c_double), P(C.c_uint64), P(C.c_int)]),
         "dl_score": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, P(C.c_double),
                                P(C.c_uint64)]),
         "dl_sharded_perplexity": (C.c_int, [vp, vp, i64, C.c_int, C.c_uint32,

@@ -79,6 +79,7 @@ struct dl_ctx {
   cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sort_fork = nullptr, ev_sort_join = nullptr;  // W_in id sort on st2
+  cudaEvent_t ev_hfinal = nullptr;  // forward recurrence done (h_final readable)
 
   // window workspace
   int64_t capT = 0, capB = 0;
@@ -301,6 +302,15 @@ void ensure_splitws(dl_ctx* c, size_t elems) {
   c->splitws_elems = elems;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 void* ensure_pinned(dl_ctx* c, size_t bytes) {
   if (bytes <= c->pinned_bytes) return c->pinned;
   if (c->pinned) cudaFreeHost(c->pinned);
@@ -476,6 +486,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                      tc(c) ? c->htape_bf + (t + 1) * BH : nullptr);
     }
   }
+  DL_CUDA(cudaEventRecord(c->ev_hfinal, st));  // h_T final (window_call's D2H)
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
   output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
@@ -808,6 +819,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_join, cudaEventDisableTiming));
+    DL_CUDA(cudaEventCreateWithFlags(&c->ev_hfinal, cudaEventDisableTiming));
     c->w_in = dalloc<float>(V * H);
     c->w_rec = dalloc<float>(H * H);
     c->m_rec = dalloc<float>(H * H);
@@ -864,6 +876,7 @@ int dl_destroy(dl_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
+  if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->st2) cudaStreamDestroy(c->st2);
@@ -924,44 +937,92 @@ int dl_get_opt(dl_ctx* c, float* m_rec, float* m_in, float* m_out) {
   });
 }
 
-int dl_window(dl_ctx* c, int64_t T, int64_t B, const uint32_t* inputs, const uint32_t* targets,
-              const uint8_t* weights, const float* h0, float* h_final, double loss_scale,
-              float clip, int compute_grads, double* loss, uint64_t* positions) {
-  if (!c) return fail(c, DL_EINVAL, "dl_window: null ctx");
+namespace {
+bool fuse_ok(dl_ctx* c, double clip);
+}
+
+namespace {
+// dl_window / dl_train_window: validate, stage the window's host arrays
+// through pinned memory, run the window (+ the update when eta > 0), read
+// back loss, positions, h_final and the update's verdict.
+int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t* inputs,
+                const uint32_t* targets, const uint8_t* weights, const float* h0,
+                float* h_final, double loss_scale, float clip, bool grads, double eta,
+                double* loss, uint64_t* positions, int* applied) {
+  if (!c) return fail(c, DL_EINVAL, std::string(who) + ": null ctx");
   if (T < 1 || B < 1) return fail(c, DL_EINVAL, "bptt: empty window");
   if (!inputs || !targets || !weights || !h0) return fail(c, DL_EINVAL, "bptt: null window arrays");
+  if (eta > 0.0 || applied) {
+    if (!(eta > 0.0)) return fail(c, DL_EINVAL, "config: eta must be > 0");
+  }
   for (int64_t i = 0; i < T * B; ++i)
     if (inputs[i] >= (uint64_t)c->V || targets[i] >= (uint64_t)c->V)
       return fail(c, DL_EINVAL, "bptt: word id out of range");
   return guarded(c, [&] {
     ensure_window(c, T, B);
     const int64_t TB = T * B, BH = B * c->H;
-    // one pinned staging copy of the window inputs, then async H2D
+    // H2D of the window: page-locked caller buffers are copied from directly,
+    // pageable ones through one pinned staging buffer
     const size_t bytes = TB * 4 * 2 + TB + BH * 4 + 64;
     uint8_t* pin = static_cast<uint8_t*>(ensure_pinned(c, std::max<size_t>(bytes, BH * 4 + 64)));
-    std::memcpy(pin, inputs, TB * 4);
-    std::memcpy(pin + TB * 4, targets, TB * 4);
-    std::memcpy(pin + TB * 8, weights, TB);
-    float* ph0 = reinterpret_cast<float*>(pin + ((TB * 9 + 15) / 16) * 16);
-    std::memcpy(ph0, h0, BH * 4);
-    DL_CUDA(cudaMemcpyAsync(c->x_d, pin, TB * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->y_d, pin + TB * 4, TB * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->w_d, pin + TB * 8, TB, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->htape, ph0, BH * 4, cudaMemcpyHostToDevice, c->st));
+    auto h2d = [&](void* dst, const void* src, size_t n, size_t off) {
+      if (!is_pinned(src)) {
+        std::memcpy(pin + off, src, n);
+        src = pin + off;
+      }
+      DL_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->st));
+    };
+    h2d(c->x_d, inputs, TB * 4, 0);
+    h2d(c->y_d, targets, TB * 4, TB * 4);
+    h2d(c->w_d, weights, TB, TB * 8);
+    h2d(c->htape, h0, BH * 4, ((TB * 9 + 15) / 16) * 16);
     DL_CUDA(cudaMemsetAsync(c->d_loss, 0, 8, c->st));
     DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
-    run_window(c, T, B, loss_scale, clip, compute_grads != 0);
-    struct { double l; unsigned long long p; } res;
+    if (eta > 0.0) {
+      // Trainer::run_epoch's bptt_run + update (trainer.hpp:391-397)
+      const bool fuse = fuse_ok(c, clip);
+      run_window(c, T, B, loss_scale, clip, true, 0.0, fuse ? eta : 0.0);
+      run_rmsprop(c, eta, TB * dp_ranks(c), /*skip_out=*/fuse);
+    } else {
+      run_window(c, T, B, loss_scale, clip, grads);
+    }
+    struct { double l; unsigned long long p; int bad; } res;
     DL_CUDA(cudaMemcpyAsync(&res.l, c->d_loss, 8, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaMemcpyAsync(&res.p, c->d_pos, 8, cudaMemcpyDeviceToHost, c->st));
-    if (h_final)
-      DL_CUDA(cudaMemcpyAsync(h_final, c->htape + T * BH, BH * 4, cudaMemcpyDeviceToHost, c->st));
+    if (eta > 0.0)
+      DL_CUDA(cudaMemcpyAsync(&res.bad, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->st));
+    // h_final is final after the forward recurrence: its D2H runs on the
+    // side stream, under the rest of the window
+    if (h_final) {
+      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_hfinal, 0));
+      DL_CUDA(cudaMemcpyAsync(h_final, c->htape + T * BH, BH * 4, cudaMemcpyDeviceToHost,
+                              c->st2));
+    }
     DL_CUDA(cudaStreamSynchronize(c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st2));
     prof_collect(c);
     if (loss) *loss = res.l;
     if (positions) *positions = res.p;
+    if (applied) *applied = res.bad ? 0 : 1;
     c->capT = std::max(c->capT, T);
   });
+}
+}  // namespace
+
+int dl_window(dl_ctx* c, int64_t T, int64_t B, const uint32_t* inputs, const uint32_t* targets,
+              const uint8_t* weights, const float* h0, float* h_final, double loss_scale,
+              float clip, int compute_grads, double* loss, uint64_t* positions) {
+  return window_call(c, "dl_window", T, B, inputs, targets, weights, h0, h_final, loss_scale,
+                     clip, compute_grads != 0, 0.0, loss, positions, nullptr);
+}
+
+int dl_train_window(dl_ctx* c, int64_t T, int64_t B, const uint32_t* inputs,
+                    const uint32_t* targets, const uint8_t* weights, const float* h0,
+                    float* h_final, double loss_scale, float clip, double eta, double* loss,
+                    uint64_t* positions, int* applied) {
+  if (!(eta > 0.0)) return fail(c, DL_EINVAL, "config: eta must be > 0");
+  return window_call(c, "dl_train_window", T, B, inputs, targets, weights, h0, h_final,
+                     loss_scale, clip, true, eta, loss, positions, applied);
 }
 
 int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
@@ -1276,8 +1337,8 @@ namespace {
 // rejected (finite clip: every clipped component is finite), no dW_out
 // allreduce sits between the GEMM and the update (single GPU or vocabulary
 // shards) and the pair kernel has the whole device to itself.
-bool fuse_ok(dl_ctx* c) {
-  if (!(c->fuse_out && tc(c) && std::isfinite((float)c->clip))) return false;
+bool fuse_ok(dl_ctx* c, double clip) {
+  if (!(c->fuse_out && tc(c) && std::isfinite((float)clip))) return false;
   if (c->comm && (!c->vshard || c->comm->shares_device())) return false;
   if (c->fuse_cap < 0) c->fuse_cap = tc_rms_fusable((int)c->Vo, (int)c->H) ? 1 : 0;
   return c->fuse_cap == 1;
@@ -1318,7 +1379,7 @@ void trainer_window(dl_ctx* c, double eta) {
   // the dense W_out update overlaps the dh GEMM when it cannot be rejected
   // (finite clip, see run_window), a second bf16 shadow exists and no
   // allreduce is pending
-  const bool fuse = fuse_ok(c);
+  const bool fuse = fuse_ok(c, c->clip);
   const bool late = !fuse && late_ok(c);
   const bool fork = !fuse && !late && fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0, fuse ? eta : 0.0,
@@ -1346,7 +1407,7 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     if (graphs) {
       // one graph per W_out-shadow parity (the forked update writes the
       // other shadow, so consecutive windows alternate between two graphs)
-      const int nvar = !fuse_ok(c) && !late_ok(c) && fork_ok(c) ? 2 : 1;
+      const int nvar = !fuse_ok(c, c->clip) && !late_ok(c) && fork_ok(c) ? 2 : 1;
       if (!c->graph || c->graph_eta != eta) {
         drop_graphs(c);
         c->graph_par0 = c->par;

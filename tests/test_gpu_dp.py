@@ -43,10 +43,12 @@ def test_concurrent_wout_update_is_bitexact(orc):
     res = []
     for flag in ("0", "1"):
         os.environ["DL_FORK_OUT"] = flag
+        os.environ["DL_FUSE_OUT"] = "0"  # (the fused epilogue update takes precedence)
         try:
             t = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr[:40000], va, "bf16")
         finally:
             os.environ.pop("DL_FORK_OUT", None)
+            os.environ.pop("DL_FUSE_OUT", None)
         t.model.trainer_run(0, 5, 0.01)
         res.append((t.model.params(), t.model.opt()))
         t.model.close()

@@ -7,6 +7,8 @@ Tolerances (north star): fp32 mode -- loss / h_final / gradients within
 near-cancelling gradient sums; rmsprop bit-exact given identical gradients
 (<= 1 float ulp where a double sum of squares lands on a rounding tie).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -192,3 +194,51 @@ def test_window_then_update_matches_oracle_step(orc):
     for got, want in zip(m.params(), p2):
         ok, e = close(got, want, rel=1e-4, floor_frac=1e-4)
         assert ok, e
+
+
+@pytest.mark.parametrize("precision,V,H", [("fp32", 300, 40), ("bf16", 1000, 256),
+                                           ("bf16", 4000, 512)])
+def test_train_window_equals_window_then_rmsprop(orc, precision, V, H):
+    """dl_train_window = dl_window + dl_rmsprop (Trainer::run_epoch's pair,
+    trainer.hpp:391-397): identical in fp32; in bf16 the W_out update runs in
+    the dW_out epilogue (fp32 step arithmetic), so W_out / m_out agree to
+    rounding."""
+    import paper_1502_00512_b200 as dl
+    rng = np.random.default_rng(V)
+    T, B = 6, 64
+    params = orc.init_uniform(V, H, 2)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.1).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    wb = dl.WindowBatch(x, y, w)
+    out = []
+    for fused_call in (False, True):
+        # the separate path with the fp32 dW_out (DL_G16=0), as the fused
+        # epilogue updates from the fp32 accumulator
+        os.environ["DL_G16"] = "0"
+        try:
+            m = dl.GpuRnn(V, H, 0, precision)
+        finally:
+            os.environ.pop("DL_G16", None)
+        m.set_params(*params)
+        if fused_call:
+            res, hf, ok = dl.train_window(m, wb, h0, 1.0 / (T * B), 1.0, 0.05)
+        else:
+            res, hf = dl.bptt_run(m, wb, h0, 1.0 / (T * B), 1.0)
+            ok = dl.rmsprop_update(m, 0.05)
+        assert ok
+        out.append((res, hf, m.params(), m.opt()))
+        m.close()
+    (r1, h1, p1, o1), (r2, h2, p2, o2) = out
+    assert r1.positions == r2.positions
+    assert r1.loss == r2.loss
+    assert np.array_equal(h1, h2)
+    if precision == "fp32":
+        for a, b in zip(p1 + o1, p2 + o2):
+            assert np.array_equal(a, b)
+    else:
+        for a, b in zip(p1, p2):
+            np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-7)
+        for a, b in zip(o1, o2):
+            np.testing.assert_allclose(a, b, rtol=1e-3, atol=1e-12)
