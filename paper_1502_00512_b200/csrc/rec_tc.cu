@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "tc_common.cuh"
 #include "kernels.cuh"
@@ -250,7 +251,14 @@ struct PersistParams {
   float* out;             // fwd: htape (writes step s+1); bwd: dpre (writes step s)
   bf16* outb;
   unsigned* counter;      // [kRecCounters] per column-tile cluster, zeroed before the launch
+  unsigned long long* trace;  // DL_REC_TRACE: [4 CTAs][T][5] %globaltimer stamps, or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int BN>
 struct PersistCfg {
@@ -341,10 +349,14 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     }
   }
 
+  // trace: CTAs (rank 0, column tiles 0, 8, 16, 24)
+  unsigned long long* tr =
+      (p.trace && rank == 0 && nt % 8 == 0 && nt < 32) ? p.trace + (nt / 8) * p.T * 5 : nullptr;
   for (int j = 0; j < p.T; ++j) {
     const int s = p.mode == 0 ? j : p.T - 1 - j;   // time step written this iteration
     const bool gemm = p.mode == 0 || j > 0;        // bwd t = T-1 has no recurrent term
     const uint32_t ph = (p.mode == 0 ? j : j - 1) & 1;
+    if (tr && threadIdx.x == 0) tr[j * 5 + 0] = gtimer();
     // epilogue operands do not depend on the recurrence: issue their loads
     // now so they land while this step waits for its inputs
     float4 pre_a[C::NPRE], pre_b[C::NPRE];
@@ -385,6 +397,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           __syncwarp();  // order lane 0's loads after every lane's acquire
         }
         if (lane == 0) {
+          if (tr) tr[j * 5 + 1] = gtimer();
           if (j > 0) asm volatile("fence.proxy.async.global;" ::: "memory");
           for (int i = 0; i < p.kbs; ++i) {
             mbar_wait(emptyA(a_stage), a_phase ^ 1);
@@ -420,9 +433,12 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       __syncwarp();
       mbar_wait(tfull, ph);
       fence_after();
+      if (tr && threadIdx.x == 64) tr[j * 5 + 2] = gtimer();
       {
         // the A ring is idle now (all MMAs of the step completed): drain the
-        // accumulator into it as this CTA's fp32 partial
+        // accumulator into it as this CTA's fp32 partial (peers pull their
+        // row slices from it; pushing instead -- DSMEM stores -- measured
+        // slower: the cluster barrier then waits for the remote stores)
         const int quarter = warp % 4, half = warp / 4;
         float* prow = part + (quarter * 32 + lane) * C::PSTRIDE;
 #pragma unroll 1
@@ -437,8 +453,15 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       fence_before();
       cluster.sync();
+      if (tr && threadIdx.x == 64) tr[j * 5 + 3] = gtimer();
     }
-    // reduce my row slice over the cluster (rank order) + fused epilogue
+    // reduce my row slice over the cluster (rank order) + fused epilogue.
+    // Only the bf16 copy feeds the next step (its TMA loads): it is stored
+    // and published first, the fp32 copy (read by later kernels) after.
+    float4 ys[C::NPRE];
+    int64_t yo[C::NPRE];
+#pragma unroll
+    for (int k = 0; k < C::NPRE; ++k) yo[k] = -1;
 #pragma unroll 1
     for (int k = 0; k * kRecThreads < nwork; ++k) {
       const int idx = threadIdx.x + k * kRecThreads;
@@ -480,17 +503,25 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                         (acc.w + ea.w) * act_deriv_f(p.act, eb.w));
         oo = s * p.MN + o;
       }
-      *reinterpret_cast<float4*>(p.out + oo) = y;
       __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.outb + oo);
       ob[0] = __floats2bfloat162_rn(y.x, y.y);
       ob[1] = __floats2bfloat162_rn(y.z, y.w);
+      bool kept = false;
+#pragma unroll
+      for (int kk = 0; kk < C::NPRE; ++kk)
+        if (kk == k) { ys[kk] = y; yo[kk] = oo; kept = true; }
+      if (!kept) *reinterpret_cast<float4*>(p.out + oo) = y;
     }
     // publish this step to the consumers of this column tile (generic
     // stores -> visible to their TMA loads)
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[j * 5 + 4] = gtimer();
     if (threadIdx.x == 0)
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counter + nt) : "memory");
+#pragma unroll
+    for (int k = 0; k < C::NPRE; ++k)
+      if (yo[k] >= 0) *reinterpret_cast<float4*>(p.out + yo[k]) = ys[k];
   }
   cluster.sync();  // peers are done reading my shared memory
   if (warp == 0) {
@@ -561,13 +592,23 @@ bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, i
   const int kb_total = (H + 63) / 64;
   // candidates in preference order (BN = 256 cannot keep W_rec + partials
   // resident); the first whose clusters all fit on the device launches
-  const int cand[8][2] = {{64, 4}, {128, 8}, {64, 8}, {128, 4}, {64, 2}, {128, 2}, {64, 1},
-                          {128, 1}};
+  int cand[8][2] = {{64, 4}, {128, 8}, {64, 8}, {128, 4}, {64, 2}, {128, 2}, {64, 1}, {128, 1}};
+  if (const char* e = std::getenv("DL_REC_PCAND")) {  // tuning: "BN,S" tried first
+    int b = 0, k = 0;
+    if (std::sscanf(e, "%d,%d", &b, &k) == 2) { cand[0][0] = b; cand[0][1] = k; }
+  }
   tc::PersistParams p{};
   p.M = M; p.N = H; p.K = H; p.T = T; p.mode = mode; p.act = act;
   p.MN = (int64_t)M * H;
   p.w_in = w_in; p.x = x; p.dh_out = dh_out; p.htape = htape;
   p.out = out; p.outb = outb; p.counter = counter;
+  static unsigned long long* trace = nullptr;
+  static const bool tracing = std::getenv("DL_REC_TRACE") != nullptr;
+  if (tracing) {
+    if (!trace) DL_CUDA(cudaMalloc(&trace, 4 * 64 * 5 * sizeof(unsigned long long)));
+    DL_CUDA(cudaMemsetAsync(trace, 0, 4 * 64 * 5 * sizeof(unsigned long long), st));
+    p.trace = T <= 64 ? trace : nullptr;
+  }
   const bool bmn = mode == 1;
   bool ok = false;
   int bn = 0, S = 0;
@@ -588,6 +629,31 @@ bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, i
   if (std::getenv("DL_DEBUG"))
     fprintf(stderr, "[desklm] persistent recurrence mode=%d T=%d M=%d H=%d BN=%d S=%d -> %s\n",
             mode, T, M, H, bn, S, ok ? "launched" : "fallback");
+  if (ok && p.trace) {
+    // per-step phase durations (ns, CTA-averaged): wait, load+mma, reduce
+    // (drain + cluster sync), epilogue+publish; and step-to-step period
+    std::vector<unsigned long long> h(4 * T * 5);
+    DL_CUDA(cudaStreamSynchronize(st));
+    DL_CUDA(cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    double ph[5] = {0, 0, 0, 0, 0};
+    int n = 0;
+    for (int c = 0; c < 4; ++c)
+      for (int j = 1; j + 1 < T; ++j) {
+        const unsigned long long* r = &h[(c * T + j) * 5];
+        const unsigned long long* q = &h[(c * T + j + 1) * 5];
+        if (!r[0] || !r[4] || !q[0]) continue;
+        ph[0] += (double)(r[1] - r[0]);
+        ph[1] += (double)(r[2] - r[1]);
+        ph[2] += (double)(r[3] - r[2]);
+        ph[3] += (double)(r[4] - r[3]);
+        ph[4] += (double)(q[0] - r[0]);
+        ++n;
+      }
+    if (n)
+      fprintf(stderr, "[desklm] rec trace mode=%d: wait %.0f  load+mma %.0f  drain+sync %.0f  "
+              "epilogue %.0f  period %.0f ns\n", mode, ph[0] / n, ph[1] / n, ph[2] / n,
+              ph[3] / n, ph[4] / n);
+  }
   return ok;
 }
 
