@@ -11,6 +11,7 @@ size_t dtype_size(DType t) {
     case DType::U32: return 4;
     case DType::F64: return 8;
     case DType::U64: return 8;
+    case DType::BF16: return 2;
   }
   return 4;
 }
@@ -21,6 +22,7 @@ static ncclDataType_t nccl_type(DType t) {
     case DType::F64: return ncclDouble;
     case DType::U64: return ncclUint64;
     case DType::U32: return ncclUint32;
+    case DType::BF16: return ncclBfloat16;
   }
   return ncclFloat;
 }
@@ -88,6 +90,16 @@ struct Ptrs {
   const void* p[16];
 };
 
+// bf16: summed in fp32 in rank order, rounded once
+__global__ void k_sum_ranks_bf16(bf16* out, Ptrs in, int G, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float s = __bfloat162float(static_cast<const bf16*>(in.p[0])[i]);
+    for (int r = 1; r < G; ++r) s += __bfloat162float(static_cast<const bf16*>(in.p[r])[i]);
+    out[i] = __float2bfloat16_rn(s);
+  }
+}
+
 template <class T>
 __global__ void k_sum_ranks(T* out, Ptrs in, int G, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
@@ -119,6 +131,7 @@ void LocalComm::allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) {
         k_sum_ranks<unsigned long long><<<grid, 256, 0, st>>>((unsigned long long*)tmp, ps, nranks, n);
         break;
       case DType::U32: k_sum_ranks<unsigned><<<grid, 256, 0, st>>>((unsigned*)tmp, ps, nranks, n); break;
+      case DType::BF16: k_sum_ranks_bf16<<<grid, 256, 0, st>>>((bf16*)tmp, ps, nranks, n); break;
     }
     DL_CUDA(cudaGetLastError());
   }

@@ -20,7 +20,7 @@
 
 namespace dl {
 
-enum class DType { F32, F64, U64, U32 };
+enum class DType { F32, F64, U64, U32, BF16 };
 
 struct Comm {
   int nranks = 1, rank = 0;

@@ -632,7 +632,7 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
               if (n0 + j < g.N) Brow[n0 + j] = __float2bfloat16_rn(v[j]);
           }
         }
-        if (mvalid) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
+        if (mvalid && g.rowsq) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
       } else if (!g.logits) {
         float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
 #pragma unroll 1

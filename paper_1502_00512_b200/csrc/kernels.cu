@@ -761,6 +761,70 @@ k_rms_dense_g16(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict_
   }
 }
 
+// Dense W_out rmsprop (rmsprop.hpp:94-107) from an unclipped bf16 gradient
+// (the data-parallel path: dW_out summed over ranks in bf16): clip
+// (rnn.hpp:158-159), mean_sq in fp64, then the row's update -- two passes
+// over the row's gradient (the second from L1/L2).  One warp per row.
+__global__ void __launch_bounds__(256)
+k_rms_dense_g16c(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                 const bf16* __restrict__ g, int64_t V, int64_t H, float clip, double rho,
+                 double eps, double eta) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp0; r < V; r += nwarps) {
+    const uint4* g8 = reinterpret_cast<const uint4*>(g + r * H);
+    double s = 0.0;
+    for (int64_t j = lane; j < H / 8; j += 32) {
+      const uint4 q = __ldg(g8 + j);
+      const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(q2[k]);
+        const float a = clip1(f.x, clip), b = clip1(f.y, clip);
+        s += (double)a * (double)a + (double)b * (double)b;
+      }
+    }
+    s = warp_sum_d(s);
+    const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
+    const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
+    float4* w4 = reinterpret_cast<float4*>(w + r * H);
+    uint4* b8 = reinterpret_cast<uint4*>(wb + r * H);
+    for (int64_t j = lane; j < H / 8; j += 32) {
+      const uint4 q = __ldg(g8 + j);
+      const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+      float gg[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(q2[k]);
+        gg[2 * k] = clip1(f.x, clip);
+        gg[2 * k + 1] = clip1(f.y, clip);
+      }
+      float4 o0 = w4[2 * j], o1 = w4[2 * j + 1];
+      o0.x -= rms_step(eta, gg[0], denom, inv);
+      o0.y -= rms_step(eta, gg[1], denom, inv);
+      o0.z -= rms_step(eta, gg[2], denom, inv);
+      o0.w -= rms_step(eta, gg[3], denom, inv);
+      o1.x -= rms_step(eta, gg[4], denom, inv);
+      o1.y -= rms_step(eta, gg[5], denom, inv);
+      o1.z -= rms_step(eta, gg[6], denom, inv);
+      o1.w -= rms_step(eta, gg[7], denom, inv);
+      w4[2 * j] = o0;
+      w4[2 * j + 1] = o1;
+      uint4 ob;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(o0.x, o0.y), p1 = __floats2bfloat162_rn(o0.z, o0.w);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(o1.x, o1.y), p3 = __floats2bfloat162_rn(o1.z, o1.w);
+      ob.x = *reinterpret_cast<uint32_t*>(&p0);
+      ob.y = *reinterpret_cast<uint32_t*>(&p1);
+      ob.z = *reinterpret_cast<uint32_t*>(&p2);
+      ob.w = *reinterpret_cast<uint32_t*>(&p3);
+      b8[j] = ob;
+    }
+    if (lane == 0) m[r] = mw;
+  }
+}
+
 __global__ void k_count_skip(const int* __restrict__ nonfinite, unsigned long long* skipped) {
   if (*nonfinite) skipped[0] += 1ull;
 }
@@ -979,6 +1043,12 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
 }
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st) {
   k_count_skip<<<1, 1, 0, st>>>(nonfinite, skipped);
+}
+void rms_dense_g16c(float* w, bf16* wb, float* m, const bf16* g, int64_t V, int64_t H,
+                    float clip, double rho, double eps, double eta, cudaStream_t st) {
+  if (V <= 0) return;
+  const int blocks = (int)std::min<int64_t>((V + 7) / 8, 148 * 8);
+  k_rms_dense_g16c<<<blocks, 256, 0, st>>>(w, wb, m, g, V, H, clip, rho, eps, eta);
 }
 void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
                    int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st) {

@@ -62,6 +62,9 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
 void count_skip(const int* nonfinite, unsigned long long* skipped, cudaStream_t st);
 // dense W_out rmsprop from bf16 gradients + per-(half tile, row) sums of
 // squares [nsub][V] (H % 8 == 0)
+// data-parallel bf16 path: unclipped summed bf16 gradient, clip + update (H % 8 == 0)
+void rms_dense_g16c(float* w, bf16* wb, float* m, const bf16* g, int64_t V, int64_t H,
+                    float clip, double rho, double eps, double eta, cudaStream_t st);
 void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
                    int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st);
 

@@ -76,6 +76,10 @@ struct dl_ctx {
   double* rowsq = nullptr;
   int rowsq_n = 0;
   bool g16 = true, g16_valid = false;
+  // data parallel, bf16 mode, finite clip: dW_out is produced and summed over
+  // ranks in bf16 (unclipped), then clip + the dense update in one kernel
+  bool dp16 = false;
+  float dp16_clip = 1.f;
   cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sort_fork = nullptr, ev_sort_join = nullptr;  // W_in id sort on st2
@@ -532,6 +536,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       g.eta = fuse_eta;
       DL_CUDA(cudaMemsetAsync(c->rms_cnt, 0, ((Vo + 255) / 256) * sizeof(unsigned), st));
       c->g16_valid = false;
+      c->dp16 = false;
       gemm(c, g);
       return;
     }
@@ -547,9 +552,15 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // gradient's HBM traffic); needs a finite clip (no non-finite check) and
     // no allreduce between the GEMM and the update
     c->g16_valid = tc(c) && c->g16 && !dp && std::isfinite(clip);
+    c->dp16 = tc(c) && dp && std::isfinite(clip) && (H % 8) == 0;
+    c->dp16_clip = clip;
     if (c->g16_valid) {
       g.Cb = c->g_out_bf;
       g.rowsq = c->rowsq;
+    } else if (c->dp16) {
+      // per-rank partial, unclipped (the sum is clipped): bf16, no row sums
+      g.Cb = c->g_out_bf;
+      g.clip = INFINITY;
     }
     gemm(c, g);
   };
@@ -560,9 +571,15 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // recurrence; joined before the update
     DL_CUDA(cudaEventRecord(c->ev_fork, st));
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
-    reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
-    c->launches++;
+    if (c->dp16) {
+      // bf16 on the wire: half the NVLink bytes of the fp32 gradient; clip
+      // and the update follow in rms_dense_g16c
+      c->comm->allreduce_sum(c->g_out_bf, (size_t)(V * H), DType::BF16, c->st2);
+    } else {
+      c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
+      reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
+      c->launches++;
+    }
   }
   // With a finite clip bound every clipped component is finite (clip1 maps
   // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
@@ -719,7 +736,10 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
-  if (!skip_out && c->g16_valid)
+  if (!skip_out && c->dp16)
+    rms_dense_g16c(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->Vo, c->H, c->dp16_clip,
+                   c->rho, c->eps, eta, st);
+  else if (!skip_out && c->g16_valid)
     rms_dense_g16(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->rowsq, c->rowsq_n, c->Vo, c->H,
                   c->rho, c->eps, eta, st);
   else if (!skip_out)
@@ -1038,8 +1058,10 @@ int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
       cudaFree(dense);
     }
     if (g_rec) DL_CUDA(cudaMemcpyAsync(g_rec, c->g_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
-    if (g_out && c->g16_valid) {
-      // bf16 gradient of the throughput path, widened on the host
+    if (g_out && (c->g16_valid || c->dp16)) {
+      // bf16 gradient of the throughput path, widened on the host (the
+      // data-parallel one is the unclipped rank sum: clipped here as the
+      // update kernel does, rnn.hpp:131-134)
       std::vector<uint16_t> tmp((size_t)(c->Vo * c->H));
       DL_CUDA(cudaMemcpyAsync(tmp.data(), c->g_out_bf, tmp.size() * 2, cudaMemcpyDeviceToHost,
                               c->st));
@@ -1048,6 +1070,7 @@ int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
       for (size_t i = 0; i < tmp.size(); ++i) {
         const uint32_t u = (uint32_t)tmp[i] << 16;
         std::memcpy(&dst[i], &u, 4);
+        if (c->dp16) dst[i] = std::min(c->dp16_clip, std::max(-c->dp16_clip, dst[i]));
       }
     } else if (g_out) {
       DL_CUDA(cudaMemcpyAsync(g_out + c->v0 * c->H, c->g_out, c->Vo * c->H * 4,
@@ -1088,6 +1111,7 @@ int dl_set_grads(dl_ctx* c, int64_t n_in_rows, const uint32_t* in_words, const f
     DL_CUDA(cudaStreamSynchronize(c->st));
     c->have_grads = true;
     c->g16_valid = false;  // injected gradients are fp32
+    c->dp16 = false;
   });
 }
 

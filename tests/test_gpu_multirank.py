@@ -69,6 +69,11 @@ def test_dp_window_matches_global_window(orc, G, precision):
     if precision == "fp32":
         for a, b in zip(got[0], want):
             assert close(a, b)
+    else:
+        # bf16: dW_out is summed over ranks in bf16 before clip + update
+        for a, b in zip(got[0][:3], want[:3]):
+            d = np.asarray(a, np.float64) - np.asarray(b, np.float64)
+            assert np.abs(d).max() <= 2e-2 * max(1.0, np.abs(b).max())
 
 
 def _vshard_ranks(dl, G, V, H, precision, params):
