@@ -44,6 +44,10 @@ CONFIGS = {
                desc="RNNLM hidden=1024, vocab=64K full softmax, 128 streams"),
     "c3": dict(V=64000, H=2048, T=16, B=128, noffset=8, L=1 << 25, seed=3001,
                desc="RNNLM hidden=2048, vocab=64K, 128 streams/GPU, data-parallel"),
+    # vocabulary-sharded output layer over the N GPUs (strong scaling: the
+    # same B*T words per step, W_out rows split V/N per rank)
+    "c4": dict(V=256000, H=4096, T=16, B=128, noffset=8, L=1 << 25, seed=4001, vshard=True,
+               desc="RNNLM hidden=4096, vocab=256K, output softmax vocab-sharded over the GPUs"),
     # forward-only scoring (sharded_perplexity / n-best): a step = one
     # lock-step scoring step over S streams
     "c5": dict(V=64000, H=2048, T=1, B=1024, noffset=1, L=1 << 22, seed=5001, score=True,
@@ -293,6 +297,8 @@ def main():
         uid = [dl.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         model.comm_init(uid[0], world, rank)
+        if cfg.get("vshard"):
+            model.set_vocab_shard(True)
     model.set_params(*params)
     model.set_opt(None, None, None, 0.9995, 1e-6)
     model.trainer_init(ids, noffset, B, T, 1.0)
@@ -325,7 +331,10 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    words = world * B * T * args.steps
+    vshard = bool(cfg.get("vshard"))
+    # data parallel: every rank trains its own B streams; vocabulary-sharded:
+    # all ranks cooperate on the same B streams
+    words = (1 if vshard else world) * B * T * args.steps
     value = words / (ms / 1000.0)
     fpw = flops_per_word(V, H)
 
@@ -341,7 +350,9 @@ def main():
             phases[name] = v
     model.set_profiling(False)
     TB = T * B
-    gemm_flops = {"logits": 2.0 * TB * V * H, "dh": 2.0 * TB * V * H, "dw_out": 2.0 * TB * V * H}
+    Vloc = V // world if vshard else V  # W_out rows on this GPU
+    gemm_flops = {"logits": 2.0 * TB * Vloc * H, "dh": 2.0 * TB * Vloc * H,
+                  "dw_out": 2.0 * TB * Vloc * H}
     dom = max(gemm_flops, key=lambda k: phases.get(k, 0.0))
     dom_ms = phases.get(dom, float("nan"))
     achieved = gemm_flops[dom] / (dom_ms / 1000.0) / 1e12
@@ -422,13 +433,15 @@ def main():
     if rank == 0:
         out = {"metric": "training words/sec", "value": value, "unit": "words/s",
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+               "ms_per_step": step_ms, "higher_is_better": True,
+               "scaling": "strong" if vshard else "weak",
                "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
                "config": {"workload": args.config, "desc": cfg["desc"], "V": V, "H": H,
-                          "T": T, "B_per_gpu": B, "global_minibatch": B * world,
+                          "T": T, "B_per_gpu": B,
+                          "global_minibatch": B if vshard else B * world,
                           "noffset": noffset, "L": L, "loss": "exact softmax",
                           "optimizer": "rmsprop (per-word W_in/W_out scalars)",
-                          "parallelism": f"dp{world}",
+                          "parallelism": f"vocab{world}" if vshard else f"dp{world}",
                           "l2": "inputs larger than L2 (W_out bf16 262 MB + fp32 master 524 MB "
                                 "streamed every window)"},
                "flops_per_word": fpw, "mean_window_loss": loss_sum / args.steps,

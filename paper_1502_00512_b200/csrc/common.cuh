@@ -119,6 +119,8 @@ struct GemmDesc {
   float* rms_m;
   unsigned* rms_cnt;  // [ceil(M / 256)], zero at launch
   double rho, eps, eta;
+  unsigned long long* trace;  // DL_GEMM_TRACE diagnostics (fused kernel), or null
+  int trace_warps;            // DL_GEMM_TRACE_WARPS: trace three warps of one CTA
 };
 
 // gemm_simt.cu

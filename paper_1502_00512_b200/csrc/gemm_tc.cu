@@ -281,6 +281,11 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
@@ -290,6 +295,11 @@ __device__ __forceinline__ float ld_shared_f32(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -346,7 +356,8 @@ constexpr int kRmsChunks = 4;  // 32-column chunks per epilogue warp (half of 25
 
 __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, int m, int mt,
                                              int nt, int half, int c0, int nsub, unsigned target,
-                                             uint32_t ring) {
+                                             uint32_t ring, unsigned long long* tr = nullptr,
+                                             unsigned long long* arrt = nullptr) {
   const int lane = threadIdx.x % 32;
   const bool mvalid = m < g.M;
   const int sub = 2 * nt + half;
@@ -365,9 +376,6 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
     }
     cp_async_commit();
   };
-  issue(0, ring);
-  issue(1, ring + 4096);
-
   double sq = 0.0;
 #pragma unroll 1
   for (int c = c0; c < ((DL_RMS_DIAG & 4) ? c0 : c0 + kRmsChunks); ++c) {
@@ -384,12 +392,22 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
   if (mvalid) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
   __syncwarp();
   if (lane == 0) {
+    if (tr) tr[1] = gtimer_ns();
+    // release the partials (before any cp.async is in flight: a fence
+    // would wait for those loads too)
     __threadfence();
     atomicAdd(g.rms_cnt + mt, 1u);
+    if (arrt) *arrt = gtimer_ns();
+  }
+  // the master's first chunks load while the block's other warps publish
+  issue(0, ring);
+  issue(1, ring + 4096);
+  if (lane == 0) {
 #if !(DL_RMS_DIAG & 1)
     while (ld_relaxed(g.rms_cnt + mt) < target) __nanosleep(32);
 #endif
-    __threadfence();
+    ld_acquire_u32(g.rms_cnt + mt);  // acquire without waiting for the loads
+    if (tr) tr[2] = gtimer_ns();
   }
   __syncwarp();
   float step = 0.f, mw = 0.f;
@@ -440,6 +458,7 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
   }
   if (DL_RMS_DIAG & 2) cp_async_wait<0>();
   if (mvalid && nt == 0 && half == 0) g.rms_m[m] = mw;
+  if (tr && lane == 0) tr[3] = gtimer_ns();
 }
 
 template <bool A_MN, bool B_MN, bool RMS>
@@ -555,17 +574,34 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int acc = 0;
     uint32_t acc_phase = 0;
     bool bad = false;
-    for (int u = pair; u < total; u += npairs) {
+    // trace (g.trace): pairs 0, 1, 35, warp 2 -- per tile: tfull observed,
+    // pass 1 done, block sync done, pass 2 done (%globaltimer ns)
+    const int trace_slot = (blockIdx.x == 0) ? 0 : (blockIdx.x == 2) ? 1 : (blockIdx.x == 70) ? 2 : -1;
+    // (and every pair's pass-1 arrival time per tile at g.trace + 3*64*4)
+    unsigned long long* arr = (g.trace && lane == 0 && !g.trace_warps)
+                                  ? g.trace + 3 * 64 * 4 + (blockIdx.x * 8 + (warp - 2)) * 32
+                                  : nullptr;
+    int it = 0;
+    for (int u = pair; u < total; u += npairs, ++it) {
       int mt, nt, kb0, kb1;
       sc.decode(u, mt, nt, kb0, kb1);
       const int split = u % sc.k_splits;
       mbar_wait(tfull(acc), acc_phase);
       fence_after();
+      // (slots 0..2: warp 2 of pairs 0, 1, 35; with DL_GEMM_TRACE_WARPS the
+      // three slots are warps 2, 5 and 9 of pair 0)
+      const int tslot = g.trace_warps ? (blockIdx.x == 0 && (warp == 2 || warp == 5 || warp == 9)
+                                             ? (warp == 2 ? 0 : warp == 5 ? 1 : 2) : -1)
+                                      : (warp == 2 ? trace_slot : -1);
+      unsigned long long* tr = (g.trace && tslot >= 0 && it < 64)
+                                   ? g.trace + (tslot * 64 + it) * 4 : nullptr;
+      if (tr && lane == 0) tr[0] = gtimer_ns();
       const int m = mt * 256 + (int)rank * 128 + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256;
       if constexpr (RMS)
         epilogue_rms(g, taddr, m, mt, nt, half, half * 4, 2 * sc.n_tiles, 16u * sc.n_tiles,
-                     sbase + C::EPI_OFF + (warp - 2) * C::EPI_WARP_BYTES);
+                     sbase + C::EPI_OFF + (warp - 2) * C::EPI_WARP_BYTES, tr,
+                     (arr && it < 32) ? arr + it : nullptr);
       else
         epilogue_row<256>(g, taddr, m, nt, split, bad, half * 4, half * 4 + 4, 2 * nt + half);
       fence_before();

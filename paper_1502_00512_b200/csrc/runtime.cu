@@ -537,7 +537,66 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       DL_CUDA(cudaMemsetAsync(c->rms_cnt, 0, ((Vo + 255) / 256) * sizeof(unsigned), st));
       c->g16_valid = false;
       c->dp16 = false;
+      static const bool tracing = std::getenv("DL_GEMM_TRACE") != nullptr;
+      static unsigned long long* trace = nullptr;
+      if (tracing && !c->profiling) {
+        if (!trace) DL_CUDA(cudaMalloc(&trace, (3 * 64 * 4 + 148 * 8 * 32) * 8));
+        DL_CUDA(cudaMemsetAsync(trace, 0, (3 * 64 * 4 + 148 * 8 * 32) * 8, st));
+        g.trace = trace;
+        g.trace_warps = std::getenv("DL_GEMM_TRACE_WARPS") != nullptr;
+      }
       gemm(c, g);
+      if (g.trace) {
+        // per-tile epilogue phases of three pairs (diagnostics)
+        static unsigned long long h[3 * 64 * 4 + 148 * 8 * 32];
+        DL_CUDA(cudaStreamSynchronize(st));
+        DL_CUDA(cudaMemcpy(h, g.trace, sizeof h, cudaMemcpyDeviceToHost));
+        {
+          // arrival time of every epilogue warp per round: within each M
+          // block (8 pairs = 16 CTAs x 8 warps), the spread and who is last
+          const unsigned long long* a = h + 3 * 64 * 4;
+          double spread = 0;
+          int ns = 0;
+          std::vector<int> last_w(8, 0), last_c(144, 0);
+          for (int it = 1; it < 26; ++it)
+            for (int b = 0; b < 9; ++b) {
+              unsigned long long mn = ~0ull, mx = 0;
+              int aw = -1, ac = -1;
+              for (int cta = b * 16; cta < b * 16 + 16; ++cta)
+                for (int w = 0; w < 8; ++w) {
+                  const unsigned long long v = a[(cta * 8 + w) * 32 + it];
+                  if (!v) continue;
+                  mn = std::min(mn, v);
+                  if (v > mx) { mx = v; aw = w; ac = cta; }
+                }
+              if (aw >= 0) { spread += (double)(mx - mn); ++ns; last_w[aw]++; last_c[ac]++; }
+            }
+          fprintf(stderr, "[desklm] fused dW_out: mean arrival spread within an M block %.0f ns; "
+                  "last warp (2..9):", ns ? spread / ns : 0.0);
+          for (int w = 0; w < 8; ++w) fprintf(stderr, " %d", last_w[w]);
+          fprintf(stderr, "; last CTA parity even/odd: ");
+          int ev = 0, od = 0;
+          for (int cta = 0; cta < 144; ++cta) (cta % 2 ? od : ev) += last_c[cta];
+          fprintf(stderr, "%d/%d\n", ev, od);
+        }
+        for (int p = 0; p < 3; ++p) {
+          double a = 0, b = 0, cc = 0, per = 0;
+          int n = 0;
+          for (int i = 1; i + 1 < 64; ++i) {
+            const unsigned long long* r = h + (p * 64 + i) * 4;
+            const unsigned long long* q = h + (p * 64 + i + 1) * 4;
+            if (!r[0] || !r[3] || !q[0]) break;
+            a += (double)(r[1] - r[0]);
+            b += (double)(r[2] - r[1]);
+            cc += (double)(r[3] - r[2]);
+            per += (double)(q[0] - r[0]);
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[desklm] fused dW_out pair-slot %d: pass1 %.0f  sync %.0f  pass2 %.0f  "
+                    "tile period %.0f ns (%d tiles)\n", p, a / n, b / n, cc / n, per / n, n);
+        }
+      }
       return;
     }
     GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
