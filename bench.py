@@ -260,6 +260,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--dp-mode", default="vocab", choices=["vocab", "dense"],
+                    help="N>1 data parallel: vocabulary-parallel output layer (default) or "
+                         "the dense dW_out allreduce")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -299,6 +302,10 @@ def main():
         model.comm_init(uid[0], world, rank)
         if cfg.get("vshard"):
             model.set_vocab_shard(True)
+        elif args.dp_mode == "vocab":
+            # data-parallel streams, vocabulary-parallel output layer: no
+            # V x H gradient on the links, the W_out update split N ways
+            model.set_vocab_shard("dp")
     model.set_params(*params)
     model.set_opt(None, None, None, 0.9995, 1e-6)
     model.trainer_init(ids, noffset, B, T, 1.0)
@@ -350,9 +357,12 @@ def main():
             phases[name] = v
     model.set_profiling(False)
     TB = T * B
-    Vloc = V // world if vshard else V  # W_out rows on this GPU
-    gemm_flops = {"logits": 2.0 * TB * Vloc * H, "dh": 2.0 * TB * Vloc * H,
-                  "dw_out": 2.0 * TB * Vloc * H}
+    # W_out rows on this GPU; with the vocabulary-parallel DP output layer
+    # each GPU scores world x TB rows against V / world
+    Vloc = V // world if (vshard or (world > 1 and args.dp_mode == "vocab")) else V
+    TBo = TB * world if (world > 1 and args.dp_mode == "vocab" and not vshard) else TB
+    gemm_flops = {"logits": 2.0 * TBo * Vloc * H, "dh": 2.0 * TBo * Vloc * H,
+                  "dw_out": 2.0 * TBo * Vloc * H}
     dom = max(gemm_flops, key=lambda k: phases.get(k, 0.0))
     dom_ms = phases.get(dom, float("nan"))
     achieved = gemm_flops[dom] / (dom_ms / 1000.0) / 1e12
@@ -441,7 +451,10 @@ def main():
                           "global_minibatch": B if vshard else B * world,
                           "noffset": noffset, "L": L, "loss": "exact softmax",
                           "optimizer": "rmsprop (per-word W_in/W_out scalars)",
-                          "parallelism": f"vocab{world}" if vshard else f"dp{world}",
+                          "parallelism": (f"vocab{world}" if vshard else
+                                          f"dp{world}+vocab-parallel-output"
+                                          if world > 1 and args.dp_mode == "vocab"
+                                          else f"dp{world}"),
                           "l2": "inputs larger than L2 (W_out bf16 262 MB + fp32 master 524 MB "
                                 "streamed every window)"},
                "flops_per_word": fpw, "mean_window_loss": loss_sum / args.steps,

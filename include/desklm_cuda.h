@@ -186,7 +186,17 @@ int dl_comm_init_local(dl_ctx* ctx, void* group, int rank);
  * dl_set_params / dl_set_opt read, and dl_get_params / dl_get_opt /
  * dl_get_grads write, only this rank's W_out / m_out rows of the full V-row
  * host arrays.  Resets W_out and m_out to zero: call before dl_set_params.
- * dl_comm_init(_local) turns sharding off again. */
+ * dl_comm_init(_local) turns sharding off again.
+ * on == 2: data-parallel streams with a vocabulary-parallel output layer --
+ * every rank trains its own B streams (global minibatch G*B, as without
+ * sharding) and keeps W_out rows [r*V/G, (r+1)*V/G).  Per window the hidden
+ * states, targets and weights of all ranks are all-gathered, each rank
+ * scores the whole global window against its block (the same G x rows
+ * log-sum-exp exchange), the partial dh is reduce-scattered back to the
+ * rank owning the rows, and W_rec / W_in are summed as in plain data
+ * parallel: no V x H gradient crosses the links and the dense W_out update
+ * is split G ways.  Scoring calls keep the on == 1 semantics (identical
+ * inputs on every rank). */
 int dl_set_vocab_shard(dl_ctx* ctx, int on);
 
 /* ---- instrumentation ----------------------------------------------------- */

@@ -187,11 +187,14 @@ class GpuRnn:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
 
-    def set_vocab_shard(self, on: bool = True):
+    def set_vocab_shard(self, on=True):
         """Vocabulary-sharded softmax over the communicator's ranks
         (dl_set_vocab_shard): this rank keeps W_out rows [r*V/G, (r+1)*V/G).
-        Zeroes W_out / m_out -- call before set_params."""
-        self._chk(load().dl_set_vocab_shard(self._h, int(on)))
+        on=True / 1: every rank runs the same streams; on="dp" / 2: data-
+        parallel streams with a vocabulary-parallel output layer over the
+        gathered window.  Zeroes W_out / m_out -- call before set_params."""
+        mode = 2 if on == "dp" else int(on)
+        self._chk(load().dl_set_vocab_shard(self._h, mode))
 
 
 def init_uniform(V: int, H: int, seed: int, init_range: float = 0.1):
@@ -529,7 +532,7 @@ class Trainer:
 
     def __init__(self, cfg: TrainConfig, params, vocab_words: Sequence[str], train_ids,
                  valid_ids, precision: str = "fp32", device: int = 0, comm=None,
-                 vocab_shard: bool = False):
+                 vocab_shard=False):
         cfg.validate()
         self.cfg = cfg
         self.vocab = list(vocab_words)
@@ -547,9 +550,10 @@ class Trainer:
             raise ValueError("trainer: validation stream too short")
         self.valid = valid
         self.nranks, self.rank = (1, 0) if comm is None else (comm[1], comm[2])
-        # vocabulary-sharded ranks all run the same streams; data-parallel
-        # ranks split the global minibatch
-        self.dp_ranks = 1 if vocab_shard else self.nranks
+        # vocabulary-sharded ranks (vocab_shard=True) all run the same
+        # streams; data-parallel ranks -- plain, or with the vocabulary-
+        # parallel output layer (vocab_shard="dp") -- split the global minibatch
+        self.dp_ranks = 1 if vocab_shard is True else self.nranks
         L = len(self.train_ids)
         N = cfg.noffset * cfg.minibatch * self.dp_ranks
         if L < N:
@@ -561,7 +565,7 @@ class Trainer:
         elif comm is not None:
             self.model.comm_init(comm[0], comm[1], comm[2])
         if vocab_shard:
-            self.model.set_vocab_shard(True)
+            self.model.set_vocab_shard(vocab_shard)
         self.model.set_params(w_in, w_rec, w_out)
         self.model.set_opt(None, None, None, cfg.rho, cfg.eps)
         self.model.trainer_init(self.train_ids, cfg.noffset, cfg.minibatch, cfg.unroll,

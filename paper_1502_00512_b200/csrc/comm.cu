@@ -12,6 +12,7 @@ size_t dtype_size(DType t) {
     case DType::F64: return 8;
     case DType::U64: return 8;
     case DType::BF16: return 2;
+    case DType::U8: return 1;
   }
   return 4;
 }
@@ -23,6 +24,7 @@ static ncclDataType_t nccl_type(DType t) {
     case DType::U64: return ncclUint64;
     case DType::U32: return ncclUint32;
     case DType::BF16: return ncclBfloat16;
+    case DType::U8: return ncclUint8;
   }
   return ncclFloat;
 }
@@ -49,6 +51,11 @@ void NcclComm::allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) {
 
 void NcclComm::allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) {
   nccl_ok(ncclAllGather(send, recv, n, nccl_type(t), comm, st));
+}
+
+void NcclComm::reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
+                                  cudaStream_t st) {
+  nccl_ok(ncclReduceScatter(send, recv, n, nccl_type(t), ncclSum, comm, st));
 }
 
 // ------------------------------------------------------------- LocalComm
@@ -143,6 +150,28 @@ void LocalComm::allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) {
   for (int r = 0; r < nranks; ++r) DL_CUDA(cudaStreamWaitEvent(st, group->ev[r], 0));
   group->barrier();
   if (bytes) DL_CUDA(cudaMemcpyAsync(buf, tmp, bytes, cudaMemcpyDeviceToDevice, st));
+}
+
+void LocalComm::reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
+                                   cudaStream_t st) {
+  DL_REQUIRE(nranks <= 16, 1, "LocalComm: at most 16 ranks");
+  DL_REQUIRE(t == DType::F32, 1, "LocalComm: reduce_scatter supports f32");
+  publish(send, st);
+  Ptrs ps{};
+  for (int r = 0; r < nranks; ++r)
+    ps.p[r] = static_cast<const float*>(group->ptr[r]) + (size_t)rank * n;
+  const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+  if (n > 0) {
+    k_sum_ranks<float><<<grid, 256, 0, st>>>(static_cast<float*>(recv), ps, nranks, n);
+    DL_CUDA(cudaGetLastError());
+  }
+  // every rank has read every buffer before anyone reuses its own
+  DL_CUDA(cudaEventRecord(ev_b, st));
+  group->barrier();
+  group->ev[rank] = ev_b;
+  group->barrier();
+  for (int r = 0; r < nranks; ++r) DL_CUDA(cudaStreamWaitEvent(st, group->ev[r], 0));
+  group->barrier();
 }
 
 void LocalComm::allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) {

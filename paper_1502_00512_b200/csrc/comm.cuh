@@ -20,7 +20,7 @@
 
 namespace dl {
 
-enum class DType { F32, F64, U64, U32, BF16 };
+enum class DType { F32, F64, U64, U32, BF16, U8 };
 
 struct Comm {
   int nranks = 1, rank = 0;
@@ -29,6 +29,9 @@ struct Comm {
   virtual void allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) = 0;
   // recv[r*n .. r*n+n) = rank r's send[0..n)
   virtual void allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) = 0;
+  // recv[0..n) = sum over ranks of their send[rank*n .. rank*n+n)
+  virtual void reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
+                                  cudaStream_t st) = 0;
   // true when other ranks' kernels run concurrently on this rank's device:
   // kernels that need the whole GPU co-resident (spin-waiting across CTAs)
   // must not be used then
@@ -41,6 +44,8 @@ struct NcclComm : Comm {
   ~NcclComm() override;
   void allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) override;
   void allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) override;
+  void reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
+                          cudaStream_t st) override;
 };
 
 struct LocalGroup {
@@ -64,6 +69,8 @@ struct LocalComm : Comm {
   ~LocalComm() override;
   void allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) override;
   void allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) override;
+  void reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
+                          cudaStream_t st) override;
   bool shares_device() const override { return true; }
 
  private:

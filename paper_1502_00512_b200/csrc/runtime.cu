@@ -147,6 +147,18 @@ struct dl_ctx {
   // vocabulary-sharded output layer: this rank owns W_out
   // rows [v0, v0 + Vo); W_in / W_rec and the recurrence are replicated
   bool vshard = false;
+  // dpv: data-parallel streams (each rank its own B) AND a vocabulary-
+  // parallel output layer over the gathered global window: hidden states,
+  // targets and weights are all-gathered, each rank scores every row of the
+  // global window against its W_out block, dh is reduce-scattered back.
+  // No V x H gradient crosses the links and the dense W_out update is
+  // sharded.  (vshard is set too: W_out rows are sharded.)
+  bool dpv = false;
+  bf16* hs_all_bf = nullptr;  // dpv: [G*TB x H] gathered hidden states (bf16 mode)
+  float* hs_all = nullptr;    // dpv: [G*TB x H] (fp32 mode)
+  uint32_t* y_all = nullptr;  // dpv: [G*TB] gathered targets
+  uint8_t* w_all = nullptr;   // dpv: [G*TB] gathered weights
+  float* dh_all = nullptr;    // dpv: [G*TB x H] partial dh over the local W_out block
   int64_t Vo = 0, v0 = 0;
   uint32_t* tgt_loc = nullptr;  // [TB] target column inside this rank's block, or ~0
   double* lse_loc = nullptr;    // [TB] this rank's log-sum-exp over its block
@@ -189,8 +201,10 @@ int guarded(dl_ctx* c, F&& f) {
 
 // Ranks that split the minibatch (data parallel).  A vocabulary-sharded
 // group runs the same streams on every rank.
-int64_t dp_ranks(const dl_ctx* c) { return c->vshard ? 1 : c->nranks; }
-int dp_rank(const dl_ctx* c) { return c->vshard ? 0 : c->rank; }
+int64_t dp_ranks(const dl_ctx* c) { return c->vshard && !c->dpv ? 1 : c->nranks; }
+int dp_rank(const dl_ctx* c) { return c->vshard && !c->dpv ? 0 : c->rank; }
+// rows the output layer processes per window, as a multiple of T*B
+int64_t out_ranks(const dl_ctx* c) { return c->dpv ? c->nranks : 1; }
 
 void drop_graphs(dl_ctx* c) {
   for (int v = 0; v < 2; ++v)
@@ -257,6 +271,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->tgt_logit); fr(c->loss_row); fr(c->logp_row); fr(c->dh_out); fr(c->dpre); fr(c->dpre_bf);
   fr(c->g_in_rows); fr(c->g_in_words); fr(c->ews.seg_start); fr(c->ews.order_pos); fr(c->h0_d);
   fr(c->x_all); fr(c->dpre_all);
+  fr(c->hs_all_bf); fr(c->hs_all); fr(c->y_all); fr(c->w_all); fr(c->dh_all);
   c->capT = nT;
   c->capB = nB;
   const int64_t G = dp_ranks(c);  // W_in gradient rows cover the gathered window
@@ -264,8 +279,16 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   c->x_d = dalloc<uint32_t>(TB);
   c->y_d = dalloc<uint32_t>(TB);
   c->w_d = dalloc<uint8_t>(TB);
-  c->loss_row = dalloc<double>(TB);
-  c->logp_row = dalloc<double>(TB);
+  const int64_t MO = out_ranks(c) * TB;  // output-layer rows
+  c->loss_row = dalloc<double>(MO);
+  c->logp_row = dalloc<double>(MO);
+  if (c->dpv) {
+    if (c->precision == DL_BF16) c->hs_all_bf = dalloc<bf16>(MO * H);
+    else c->hs_all = dalloc<float>(MO * H);
+    c->y_all = dalloc<uint32_t>(MO);
+    c->w_all = dalloc<uint8_t>(MO);
+    c->dh_all = dalloc<float>(MO * H);
+  }
   c->dh_out = dalloc<float>(TB * H);
   c->dpre = dalloc<float>(TB * H);
   c->g_in_rows = dalloc<float>(G * TB * H);
@@ -283,19 +306,19 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   if (c->precision == DL_BF16) {
     c->htape_bf = dalloc<bf16>((nT + 1) * nB * H);
     c->dpre_bf = dalloc<bf16>(TB * H);
-    c->S = dalloc<bf16>(TB * Vo);
+    c->S = dalloc<bf16>(MO * Vo);
     c->part_tiles = tc_n_tiles((int)Vo);
-    c->part = dalloc<float2>((size_t)c->part_tiles * TB);
-    c->tgt_logit = dalloc<float>(TB);
+    c->part = dalloc<float2>((size_t)c->part_tiles * MO);
+    c->tgt_logit = dalloc<float>(MO);
   } else {
-    c->S = dalloc<float>(TB * Vo);
+    c->S = dalloc<float>(MO * Vo);
   }
   fr(c->tgt_loc); fr(c->lse_loc); fr(c->lse_all);
   if (c->vshard) {
-    c->tgt_loc = dalloc<uint32_t>(TB);
-    c->lse_loc = dalloc<double>(TB);
-    c->lse_all = dalloc<double>((int64_t)c->nranks * TB);
-    if (!c->tgt_logit) c->tgt_logit = dalloc<float>(TB);
+    c->tgt_loc = dalloc<uint32_t>(MO);
+    c->lse_loc = dalloc<double>(MO);
+    c->lse_all = dalloc<double>((int64_t)c->nranks * MO);
+    if (!c->tgt_logit) c->tgt_logit = dalloc<float>(MO);
   }
 }
 
@@ -462,7 +485,16 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // the softmax is vocabulary-sharded)
   const int64_t H = c->H, V = c->V, Vo = c->Vo, TB = T * B, BH = B * H;
   cudaStream_t st = c->st;
-  if (grads && !(c->comm != nullptr && !c->vshard)) {
+  // dp: dense dW_out summed over ranks; dprec: the recurrence side (W_rec,
+  // W_in) is data parallel; vs: replicated streams, vocabulary-sharded
+  // output (dh summed); dpv: data-parallel streams with a vocabulary-
+  // parallel output layer over the gathered window (dh reduce-scattered)
+  const bool dp = c->comm != nullptr && !c->vshard;
+  const bool dpv = c->comm != nullptr && c->dpv;
+  const bool dprec = dp || dpv;
+  const bool vs = c->comm != nullptr && c->vshard && !dpv;
+  const int64_t MO = dpv ? c->nranks * TB : TB;  // output-layer rows
+  if (grads && !dprec) {
     // the W_in gradient's id sort depends on x only: run it on the side
     // stream under the forward recurrence (which leaves SMs free) (joined before embed_rows)
     DL_CUDA(cudaEventRecord(c->ev_sort_fork, st));
@@ -493,9 +525,26 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   DL_CUDA(cudaEventRecord(c->ev_hfinal, st));  // h_T final (window_call's D2H)
   const float* Hs = c->htape + BH;
   const bf16* Hs_bf = tc(c) ? c->htape_bf + BH : nullptr;
-  output_layer(c, TB, Hs, Hs_bf, c->y_d, c->w_d, scale, grads, c->loss_row, nullptr);
-  const bool dp = c->comm != nullptr && !c->vshard;
-  const bool vs = c->comm != nullptr && c->vshard;
+  const uint32_t* yo = c->y_d;
+  const uint8_t* wo = c->w_d;
+  if (dpv) {
+    // gather the global window's hidden states, targets and weights
+    // (rank-blocked rows r*TB + t*B + b): every rank scores all of them
+    // against its W_out block
+    Phase p(c, "vocab_exchange");
+    if (tc(c)) {
+      c->comm->allgather(Hs_bf, c->hs_all_bf, (size_t)(TB * H), DType::BF16, st);
+      Hs_bf = c->hs_all_bf;
+    } else {
+      c->comm->allgather(Hs, c->hs_all, (size_t)(TB * H), DType::F32, st);
+      Hs = c->hs_all;
+    }
+    c->comm->allgather(c->y_d, c->y_all, (size_t)TB, DType::U32, st);
+    c->comm->allgather(c->w_d, c->w_all, (size_t)TB, DType::U8, st);
+    yo = c->y_all;
+    wo = c->w_all;
+  }
+  output_layer(c, MO, Hs, Hs_bf, yo, wo, scale, grads, c->loss_row, nullptr);
   if (dp) {
     // the window's loss is the sum over all ranks' streams
     DL_CUDA(cudaMemsetAsync(c->win_loss, 0, 16, st));
@@ -505,7 +554,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     accum_loss(c->d_loss, c->win_loss, c->d_pos, c->win_pos, st);
     c->launches += 2;
   } else {
-    sum_rows(c->loss_row, c->w_d, TB, c->d_loss, c->d_pos, st);
+    // (dpv: the gathered rows are the global window on every rank)
+    sum_rows(c->loss_row, wo, MO, c->d_loss, c->d_pos, st);
     c->launches++;
   }
   if (!grads) return;
@@ -521,7 +571,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     Phase p(c, "dw_out");
     if (fused) {
       // + the dense rmsprop of every row (rmsprop.hpp:94-107) in the epilogue
-      GemmDesc g = desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
+      GemmDesc g = desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
                         nullptr, H);
       g.raster = 1;
       g.clip = clip;
@@ -599,9 +649,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       }
       return;
     }
-    GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
+    GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
                               c->g_out, H)
-                       : desc((int)Vo, (int)H, (int)TB, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
+                       : desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
                               c->g_out, H);
     g.raster = 1;
     g.do_clip = dp ? 0 : 1;
@@ -673,19 +723,20 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
   auto dh = [&] {
     Phase p(c, "dh");
-    const int s = pick_splits(c, (int)TB, (int)H, (int)Vo, 8);
-    GemmDesc g = tc(c) ? desc((int)TB, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out_bf,
-                              H, c->dh_out, H)
-                       : desc((int)TB, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out, H,
-                              c->dh_out, H);
+    float* dst = dpv ? c->dh_all : c->dh_out;
+    const int s = pick_splits(c, (int)MO, (int)H, (int)Vo, 8);
+    GemmDesc g = tc(c) ? desc((int)MO, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out_bf,
+                              H, dst, H)
+                       : desc((int)MO, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out, H,
+                              dst, H);
     g.raster = 0;
     if (s > 1) {
-      ensure_splitws(c, (size_t)s * TB * H);
+      ensure_splitws(c, (size_t)s * MO * H);
       g.C = c->splitws;
       g.k_splits = s;
-      g.split_stride = TB * H;
+      g.split_stride = MO * H;
       gemm(c, g);
-      reduce_splits(c->splitws, s, TB * H, TB * H, c->dh_out, 0.f, 0, nullptr, st);
+      reduce_splits(c->splitws, s, MO * H, MO * H, dst, 0.f, 0, nullptr, st);
       c->launches++;
     } else {
       gemm(c, g);
@@ -700,6 +751,11 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // replicated computations on identical inputs.
     Phase p(c, "vocab_exchange");
     c->comm->allreduce_sum(c->dh_out, (size_t)(TB * H), DType::F32, st);
+  } else if (dpv) {
+    // every rank's partial dh over the global window, summed over ranks and
+    // scattered: this rank keeps its own TB rows
+    Phase p(c, "vocab_exchange");
+    c->comm->reduce_scatter_sum(c->dh_all, c->dh_out, (size_t)(TB * H), DType::F32, st);
   }
   // backward recurrence (backprop.hpp:197-219)
   {
@@ -747,10 +803,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     g.k_splits = s;
     g.split_stride = H * H;
     gemm(c, g);
-    reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dp ? 0 : 1, c->nonfinite, st);
+    reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dprec ? 0 : 1, c->nonfinite, st);
     c->launches++;
   }
-  if (dp) {
+  if (dprec) {
     // dW_rec: allreduce + clip.  W_in: allgather every rank's (ids, dpre) so
     // all ranks run the identical segmented sum over the global window in
     // the reference's order (t descending, global stream ascending).
@@ -778,7 +834,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   }
   // a non-finite dW_out block on one rank must skip the update everywhere
   // (only reachable with an infinite clip bound)
-  if (vs && !std::isfinite(clip)) {
+  if ((vs || dpv) && !std::isfinite(clip)) {
     if (fork_out_eta > 0.0) DL_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
     c->comm->allreduce_sum(c->nonfinite, 1, DType::U32, st);
   }
@@ -845,6 +901,7 @@ void alloc_output(dl_ctx* c) {
 void reset_vshard(dl_ctx* c) {
   if (!c->vshard) return;
   c->vshard = false;
+  c->dpv = false;
   c->Vo = c->V;
   c->v0 = 0;
   alloc_output(c);
@@ -948,6 +1005,7 @@ int dl_destroy(dl_ctx* c) {
                   c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
                   c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
+                  c->hs_all_bf, c->hs_all, c->y_all, c->w_all, c->dh_all,
                   c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1446,8 +1504,9 @@ void swap_shadow(dl_ctx* c) {
 void presize(dl_ctx* c, int64_t T, int64_t B) {
   const int64_t H = c->H, Vo = c->Vo, TB = T * B;
   size_t need = (size_t)pick_splits(c, (int)B, (int)H, (int)H) * B * H;
-  const int sdh = pick_splits(c, (int)TB, (int)H, (int)Vo, 8);
-  if (sdh > 1) need = std::max(need, (size_t)sdh * TB * H);
+  const int64_t MO = out_ranks(c) * TB;
+  const int sdh = pick_splits(c, (int)MO, (int)H, (int)Vo, 8);
+  if (sdh > 1) need = std::max(need, (size_t)sdh * MO * H);
   need = std::max(need, (size_t)pick_splits(c, (int)H, (int)H, (int)TB, 16) * H * H);
   ensure_splitws(c, need);
 }
@@ -1596,12 +1655,16 @@ int dl_set_vocab_shard(dl_ctx* c, int on) {
     if (c->precision == DL_BF16 && ((c->V / c->nranks) % 8) != 0)
       return fail(c, DL_EINVAL, "dl_set_vocab_shard: bf16 mode needs V/G a multiple of 8 (TMA)");
   }
+  if (on != 0 && on != 1 && on != 2)
+    return fail(c, DL_EINVAL, "dl_set_vocab_shard: mode must be 0, 1 or 2");
   return guarded(c, [&] {
     if (!on) {
       reset_vshard(c);
       return;
     }
     c->vshard = true;
+    c->dpv = on == 2;
+    c->capT = c->capB = 0;  // window buffers re-size for the gathered rows
     c->Vo = c->V / c->nranks;
     c->v0 = (int64_t)c->rank * c->Vo;
     alloc_output(c);

@@ -224,3 +224,100 @@ def test_dp_trainer_matches_global_minibatch(orc):
             assert np.array_equal(c[g * 4:(g + 1) * 4], cs[g * Bg + r * 4:g * Bg + (r + 1) * 4])
     for a, b in zip(trainers[0].params(), trainers[1].params()):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("G,precision", [(2, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])
+def test_dp_vocab_parallel_window_matches_global_window(orc, G, precision):
+    """Data-parallel streams + vocabulary-parallel output layer
+    (dl_set_vocab_shard mode 2): rank r trains streams [r*B, (r+1)*B) of the
+    global window, holds W_out rows [r*V/G, (r+1)*V/G); the hidden states are
+    gathered and dh reduce-scattered.  Equals one context training the global
+    minibatch (fp32: summation-order tolerance), W_in / W_rec bit-identical
+    across ranks."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 1024, 64, 6, 8
+    Bg = G * B
+    rng = np.random.default_rng(40 + G)
+    params = orc.init_uniform(V, H, 23)
+    x = rng.integers(0, V, (T, Bg)).astype(np.uint32)
+    y = rng.integers(2, V, (T, Bg)).astype(np.uint32)
+    w = (rng.random((T, Bg)) > 0.1).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (Bg, H)).astype(np.float32)
+    scale = 1.0 / (Bg * T)
+    single = dl.GpuRnn(V, H, 0, precision)
+    single.set_params(*params)
+    r1, hf1 = dl.bptt_run(single, dl.WindowBatch(x, y, w), h0, scale, 1.0)
+    g1 = single.grads()
+    assert dl.rmsprop_update(single, 0.05)
+    want = single.params() + single.opt()
+
+    group = dl.LocalGroup(G)
+    ranks = []
+    for r in range(G):
+        m = dl.GpuRnn(V, H, 0, precision)
+        m.comm_init_local(group, r)
+        m.set_vocab_shard("dp")
+        m.set_params(*params)
+        ranks.append(m)
+
+    def run(r):
+        sl = slice(r * B, (r + 1) * B)
+        wb = dl.WindowBatch(np.ascontiguousarray(x[:, sl]), np.ascontiguousarray(y[:, sl]),
+                            np.ascontiguousarray(w[:, sl]))
+        res, hf = dl.bptt_run(ranks[r], wb, np.ascontiguousarray(h0[sl]), scale, 1.0)
+        g = ranks[r].grads()
+        ok = dl.rmsprop_update(ranks[r], 0.05)
+        return res, hf, g, ok
+
+    with ThreadPoolExecutor(G) as ex:
+        outs = list(ex.map(run, range(G)))
+    tol = 1e-4 if precision == "fp32" else 2e-2
+    for r, (res, hf, g, ok) in enumerate(outs):
+        assert ok
+        assert res.positions == r1.positions
+        assert res.loss == pytest.approx(r1.loss, rel=1e-5 if precision == "fp32" else 1e-3)
+        assert np.allclose(hf, hf1[r * B:(r + 1) * B], atol=1e-6 if precision == "fp32" else 2e-2)
+    got = [m.params() + m.opt() for m in ranks]
+    for r in range(1, G):  # W_in, W_rec and their state replicate bit-identically
+        for k in (0, 1, 3, 4):
+            assert np.array_equal(got[0][k], got[r][k])
+    # the full W_out / m_out / dW_out are the rank blocks
+    w_out = _assemble([got[r][2] for r in range(G)], G)
+    m_out = _assemble([got[r][5] for r in range(G)], G)
+    g_out = _assemble([outs[r][2][2] for r in range(G)], G)
+    if precision == "fp32":
+        assert close(g_out, g1[2])
+        for a, b in zip(got[0][:2] + (w_out,) + got[0][3:5] + (m_out,), want):
+            assert close(a, b)
+    else:
+        d = np.abs(w_out.astype(np.float64) - want[2])
+        assert d.max() <= 2e-2 * max(1.0, np.abs(want[2]).max())
+        cosv = float(np.dot(g_out.ravel(), g1[2].ravel()) /
+                     (np.linalg.norm(g_out) * np.linalg.norm(g1[2]) + 1e-30))
+        assert cosv > 0.99
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_dp_vocab_parallel_trainer_matches_global_minibatch(orc, precision):
+    """Two ranks x minibatch 4 with the vocabulary-parallel output layer ==
+    one trainer with minibatch 8 (epoch losses and validation perplexities)."""
+    import paper_1502_00512_b200 as dl
+    V, H, G = 96, 64, 2
+    tr, va = orc.random_stream_pair(19, V, 4016, 600)
+    tr = tr[:4000]
+    params = orc.init_uniform(V, H, 11)
+    kw = dict(nstate=H, noffset=3, unroll=5, eta=0.02, max_epochs=2, mode=1)
+    single = dl.Trainer(dl.TrainConfig(minibatch=G * 4, **kw), params, dl.make_vocab(V), tr, va,
+                        precision)
+    single.train()
+    group = dl.LocalGroup(G)
+    trainers = [dl.Trainer(dl.TrainConfig(minibatch=4, **kw), params, dl.make_vocab(V), tr, va,
+                           precision, comm=(group, G, r), vocab_shard="dp") for r in range(G)]
+    with ThreadPoolExecutor(G) as ex:
+        list(ex.map(lambda t: t.train(), trainers))
+    rel = 1e-4 if precision == "fp32" else 1e-2
+    for t in trainers:
+        assert len(t.logs) == len(single.logs)
+        for a, b in zip(t.logs, single.logs):
+            assert a.train_loss == pytest.approx(b.train_loss, rel=rel)
+            assert a.valid_ppl == pytest.approx(b.valid_ppl, rel=10 * rel)
