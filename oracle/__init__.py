@@ -171,6 +171,28 @@ class _Backend:
                      g_in_dense=dense, g_rec=grec, g_out=gout)
         return r
 
+    def _nce_result(self, V, H, T, B, K1, compute_grads, hf, loss, pos, nin, giw, gid,
+                    grec, nout, gow, god):
+        r = dict(loss=loss.value, positions=pos.value, h_final=hf)
+        if compute_grads:
+            n, m = nin.value, nout.value
+            din = np.zeros((V, H), np.float32)
+            for s_ in range(n):
+                din[giw[s_]] += gid[s_]
+            dout = np.zeros((V, H), np.float32)
+            for s_ in range(m):
+                dout[gow[s_]] += god[s_]
+            r.update(g_in_words=giw[:n].copy(), g_in_rows=gid[:n].copy(), g_in_dense=din,
+                     g_rec=grec, g_out_words=gow[:m].copy(), g_out_rows=god[:m].copy(),
+                     g_out=dout)
+        return r
+
+    def mt_state(self, seed):
+        """std::mt19937_64(seed) state: 312 words + position (uint64[313])."""
+        st = np.zeros(313, np.uint64)
+        getattr(self.lib, self.prefix + "mt_state")(C.c_uint64(seed), st.ctypes.data_as(_vp))
+        return st
+
     def rmsprop(self, params, state, grads, rho, eps, eta, out_dense=True):
         """rmsprop_update in place on copies; returns (params, state, applied)."""
         w_in, w_rec, w_out = [np.array(x, np.float32, copy=True) for x in params]
@@ -294,6 +316,66 @@ class Orc(_Backend):
                     bad_epochs=bad.value, epoch=ep.value)
 
 
+    def noise_build(self, counts, k, floor=1e-8):
+        """NoiseModel + AliasSampler tables (nce.hpp:41-66, rng.hpp:54-89)."""
+        counts = np.ascontiguousarray(counts, np.float64)
+        V = len(counts)
+        q, lnkq, prob = (np.empty(V, np.float64) for _ in range(3))
+        alias = np.empty(V, np.uint32)
+        f = self.lib.orc_noise_build
+        f.argtypes = [_i64, _vp, C.c_int, C.c_double, _vp, _vp, _vp, _vp]
+        self._check(f(V, counts.ctypes.data, int(k), float(floor), q.ctypes.data,
+                      lnkq.ctypes.data, prob.ctypes.data, alias.ctypes.data))
+        return dict(k=int(k), q=q, ln_kq=lnkq, prob=prob, alias=alias)
+
+    def noise_sample(self, noise, rng, n):
+        out = np.empty(n, np.uint32)
+        f = self.lib.orc_noise_sample
+        f.argtypes = [_i64, _vp, _vp, _vp, _i64, _vp]
+        self._check(f(len(noise["prob"]), noise["prob"].ctypes.data, noise["alias"].ctypes.data,
+                      rng.ctypes.data, n, out.ctypes.data))
+        return out
+
+    def bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, noise, rng,
+                 compute_grads=True):
+        """bptt_run NCE mode (backprop.hpp:126-156); rng (uint64[313]) is
+        advanced in place.  Returns the bptt dict plus g_out_words /
+        g_out_rows (sparse, slot order) and the draws."""
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        T, B = inputs.shape
+        k = noise["k"]
+        K1 = k + 1
+        hf = np.empty((B, H), np.float32)
+        nin, nout = C.c_int64(0), C.c_int64(0)
+        giw = np.zeros(T * B, np.uint32)
+        gid = np.zeros((T * B, H), np.float32)
+        grec = np.zeros((H, H), np.float32)
+        gow = np.zeros(T * B * K1, np.uint32)
+        god = np.zeros((T * B * K1, H), np.float32)
+        draws = np.zeros(T * B * k, np.uint32)
+        loss, pos = C.c_double(), C.c_uint64()
+        f = self.lib.orc_bptt_nce
+        f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _i64, _i64, _u32p, _u32p,
+                      _u8p, _f32p, C.c_double, C.c_float, C.c_int, C.c_int, _vp, _vp, _vp,
+                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                      C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._check(f(V, H, act, w_in, w_rec, w_out, T, B,
+                      np.ascontiguousarray(inputs, np.uint32),
+                      np.ascontiguousarray(targets, np.uint32),
+                      np.ascontiguousarray(weights, np.uint8),
+                      np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                      int(compute_grads), k, noise["ln_kq"].ctypes.data,
+                      noise["prob"].ctypes.data, noise["alias"].ctypes.data, rng.ctypes.data,
+                      hf.ctypes.data, C.addressof(nin), giw.ctypes.data, gid.ctypes.data,
+                      grec.ctypes.data, C.addressof(nout), gow.ctypes.data, god.ctypes.data,
+                      draws.ctypes.data, C.byref(loss), C.byref(pos)))
+        r = self._nce_result(V, H, T, B, K1, compute_grads, hf, loss, pos, nin, giw, gid, grec,
+                             nout, gow, god)
+        r["noise"] = draws[:r["positions"] * k].copy()
+        return r
+
+
 class Ref(_Backend):
     """The reference itself (oracle/_ref/libdesklm_ref.so)."""
 
@@ -383,6 +465,52 @@ class Ref(_Backend):
                                   lm_scale, wip, int(fast), C.addressof(buf), cap,
                                   C.byref(ln)))
         return buf.value.decode()
+
+
+    def noise_sample(self, counts, k, floor, rng, n):
+        """n draws of NoiseModel(counts, k, floor).sample (rng advanced in
+        place) and its ln(k q) table."""
+        counts = np.ascontiguousarray(counts, np.float64)
+        V = len(counts)
+        out = np.empty(n, np.uint32)
+        lnkq = np.empty(V, np.float64)
+        f = self.lib.ref_noise_sample
+        f.argtypes = [_i64, _vp, C.c_int, C.c_double, _vp, _i64, _vp, _vp]
+        self._check(f(V, counts.ctypes.data, int(k), float(floor), rng.ctypes.data, n,
+                      out.ctypes.data, lnkq.ctypes.data))
+        return out, lnkq
+
+    def bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, counts, k,
+                 floor, rng, compute_grads=True):
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        T, B = inputs.shape
+        K1 = k + 1
+        counts = np.ascontiguousarray(counts, np.float64)
+        hf = np.empty((B, H), np.float32)
+        nin, nout = C.c_int64(0), C.c_int64(0)
+        giw = np.zeros(T * B, np.uint32)
+        gid = np.zeros((T * B, H), np.float32)
+        grec = np.zeros((H, H), np.float32)
+        gow = np.zeros(T * B * K1, np.uint32)
+        god = np.zeros((T * B * K1, H), np.float32)
+        loss, pos = C.c_double(), C.c_uint64()
+        f = self.lib.ref_bptt_nce
+        f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _i64, _i64, _u32p, _u32p,
+                      _u8p, _f32p, C.c_double, C.c_float, C.c_int, _vp, C.c_int, C.c_double,
+                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                      C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._check(f(V, H, act, w_in, w_rec, w_out, T, B,
+                      np.ascontiguousarray(inputs, np.uint32),
+                      np.ascontiguousarray(targets, np.uint32),
+                      np.ascontiguousarray(weights, np.uint8),
+                      np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                      int(compute_grads), counts.ctypes.data, int(k), float(floor),
+                      rng.ctypes.data, hf.ctypes.data, C.addressof(nin), giw.ctypes.data,
+                      gid.ctypes.data, grec.ctypes.data, C.addressof(nout), gow.ctypes.data,
+                      god.ctypes.data, C.byref(loss), C.byref(pos)))
+        return self._nce_result(V, H, T, B, K1, compute_grads, hf, loss, pos, nin, giw, gid,
+                                grec, nout, gow, god)
 
 
 def have_ref() -> bool:

@@ -20,6 +20,8 @@
  *   dot_acc (8 fixed double lanes + tail)              mat.hpp:59-78
  *   matmul_nt / matmul_nn / matmul_tn_add              mat.hpp:116-184
  *   bptt_run, softmax branch                           backprop.hpp:76-222
+ *   bptt_run, NCE branch; NoiseModel; AliasSampler    backprop.hpp:126-156, 193-203;
+ *                                                      nce.hpp:31-93; rng.hpp:54-101
  *   StandardGrads::clip / SparseRowGrads               rnn.hpp:89-162
  *   rmsprop_update (+ sparse / dense row updates)      rmsprop.hpp:77-133
  *   sharded_perplexity / lse_column                    eval.hpp:48-57, 151-222
@@ -310,6 +312,226 @@ int orc_bptt(int64_t V, int64_t H, int act, const float* w_in,
   free(pre);
   free(scores);
   free(dsc);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ NCE */
+/* NoiseModel (nce.hpp:41-66): q = max(count/total, floor) renormalised,
+ * ln_kq = log(k q); AliasSampler (rng.hpp:54-89) built from q with the same
+ * small/large stack discipline, so sampling is bit-identical. */
+int orc_noise_build(int64_t V, const double* counts, int k, double floor, double* q,
+                    double* ln_kq, double* prob, uint32_t* alias) {
+  if (k < 1 || V < 1) return 1;
+  double total = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    if (counts[w] < 0.0) return 1;
+    total += counts[w];
+  }
+  if (total <= 0.0) return 1;
+  double qsum = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    const double v = counts[w] / total;
+    q[w] = v > floor ? v : floor;  /* std::max(count/total, floor) */
+    qsum += q[w];
+  }
+  for (int64_t w = 0; w < V; ++w) {
+    q[w] /= qsum;
+    ln_kq[w] = log((double)k * q[w]);
+  }
+  /* AliasSampler(q) */
+  double tw = 0.0;
+  for (int64_t w = 0; w < V; ++w) tw += q[w];
+  double* scaled = (double*)malloc(sizeof(double) * V);
+  uint32_t* small = (uint32_t*)malloc(sizeof(uint32_t) * V);
+  uint32_t* large = (uint32_t*)malloc(sizeof(uint32_t) * V);
+  int64_t ns = 0, nl = 0;
+  for (int64_t i = 0; i < V; ++i) {
+    prob[i] = 0.0;
+    alias[i] = 0;
+    scaled[i] = q[i] * (double)V / tw;
+    if (scaled[i] < 1.0) small[ns++] = (uint32_t)i;
+    else large[nl++] = (uint32_t)i;
+  }
+  while (ns > 0 && nl > 0) {
+    const uint32_t sm = small[--ns];
+    const uint32_t lg = large[--nl];
+    prob[sm] = scaled[sm];
+    alias[sm] = lg;
+    scaled[lg] = (scaled[lg] + scaled[sm]) - 1.0;
+    if (scaled[lg] < 1.0) small[ns++] = lg;
+    else large[nl++] = lg;
+  }
+  for (int64_t i = 0; i < nl; ++i) prob[large[i]] = 1.0;
+  for (int64_t i = 0; i < ns; ++i) prob[small[i]] = 1.0;
+  free(scaled);
+  free(small);
+  free(large);
+  return 0;
+}
+
+/* AliasSampler::sample (rng.hpp:91-94) */
+static uint32_t alias_sample(orc_mt64* m, int64_t V, const double* prob, const uint32_t* alias) {
+  const uint64_t i = uniform_index(m, (uint64_t)V);
+  return uniform01(m) < prob[i] ? (uint32_t)i : alias[i];
+}
+
+/* the mt19937_64 state crosses the C boundary as 312 words + position */
+static void mt_load(orc_mt64* m, const uint64_t* st) {
+  memcpy(m->x, st, sizeof(uint64_t) * 312);
+  m->p = (int)st[312];
+}
+static void mt_store(const orc_mt64* m, uint64_t* st) {
+  memcpy(st, m->x, sizeof(uint64_t) * 312);
+  st[312] = (uint64_t)m->p;
+}
+void orc_mt_state(uint64_t seed, uint64_t* st) {
+  orc_mt64 m;
+  orc_mt_seed(&m, seed);
+  mt_store(&m, st);
+}
+int orc_noise_sample(int64_t V, const double* prob, const uint32_t* alias, uint64_t* rng,
+                     int64_t n, uint32_t* out) {
+  orc_mt64 m;
+  mt_load(&m, rng);
+  for (int64_t i = 0; i < n; ++i) out[i] = alias_sample(&m, V, prob, alias);
+  mt_store(&m, rng);
+  return 0;
+}
+
+/* nce.hpp:31-36 */
+static double softplus(double x) {
+  if (x > 0) return x + log1p(exp(-x));
+  return log1p(exp(x));
+}
+static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+/* NCE-mode window (backprop.hpp:76-156, 193-222).  rng: 313-word state, in
+ * and out (draws: t, then b, then sample; masked positions draw nothing).
+ * The sparse W_out gradient comes back in slot (first-touch) order like the
+ * W_in rows: g_out_words / g_out_data must hold T*B*(k+1) rows; noise_out
+ * (optional) receives the k draws of every unmasked position in order. */
+int orc_bptt_nce(int64_t V, int64_t H, int act, const float* w_in, const float* w_rec,
+                 const float* w_out, int64_t T, int64_t B, const uint32_t* inputs,
+                 const uint32_t* targets, const uint8_t* weights, const float* h0,
+                 double loss_scale, float clip, int compute_grads, int k, const double* ln_kq,
+                 const double* prob, const uint32_t* alias, uint64_t* rng, float* h_final,
+                 int64_t* g_in_rows, uint32_t* g_in_words, float* g_in_data, float* g_rec,
+                 int64_t* g_out_rows, uint32_t* g_out_words, float* g_out_data,
+                 uint32_t* noise_out, double* loss, uint64_t* positions) {
+  if (T < 1 || B < 1 || k < 1) return 1;
+  const int64_t BH = B * H, K1 = k + 1;
+  orc_mt64 m;
+  mt_load(&m, rng);
+  float* h = (float*)malloc(sizeof(float) * (T + 1) * BH);
+  float* pre = (float*)malloc(sizeof(float) * BH);
+  /* per (t, b): k+1 records (word, ds); n_rec[t*B+b] = 0 when masked */
+  uint32_t* rw = (uint32_t*)malloc(sizeof(uint32_t) * T * B * K1);
+  float* rds = (float*)malloc(sizeof(float) * T * B * K1);
+  int* has = (int*)calloc((size_t)(T * B), sizeof(int));
+  memcpy(h, h0, sizeof(float) * BH);
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(h + t * BH, w_rec, pre, B, H, H);
+    for (int64_t b = 0; b < B; ++b) {
+      const float* e = w_in + (int64_t)inputs[t * B + b] * H;
+      for (int64_t i = 0; i < H; ++i) pre[b * H + i] += e[i];
+    }
+    for (int64_t i = 0; i < BH; ++i) h[(t + 1) * BH + i] = act_f(act, pre[i]);
+  }
+  if (h_final) memcpy(h_final, h + T * BH, sizeof(float) * BH);
+  double L = 0.0;
+  uint64_t pos = 0, nd = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    const float* ht = h + (t + 1) * BH;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t idx = t * B + b;
+      if (!weights[idx]) continue;
+      ++pos;
+      has[idx] = 1;
+      const uint32_t y = targets[idx];
+      /* StandardAdapter::score: float(dot_acc<double>) (rnn.hpp:246-249) */
+      const double st = (double)(float)dot_acc(ht + b * H, w_out + (int64_t)y * H, H);
+      const double at = st - ln_kq[y];
+      L += loss_scale * softplus(-at);
+      rw[idx * K1] = y;
+      rds[idx * K1] = (float)(-loss_scale * sigmoid(-at));
+      for (int j = 0; j < k; ++j) {
+        const uint32_t w = alias_sample(&m, V, prob, alias);
+        if (noise_out) noise_out[nd++] = w;
+        const double s = (double)(float)dot_acc(ht + b * H, w_out + (int64_t)w * H, H);
+        const double a = s - ln_kq[w];
+        L += loss_scale * softplus(a);
+        rw[idx * K1 + 1 + j] = w;
+        rds[idx * K1 + 1 + j] = (float)(loss_scale * sigmoid(a));
+      }
+    }
+  }
+  mt_store(&m, rng);
+  *loss = L;
+  *positions = pos;
+  if (compute_grads) {
+    float* dh = (float*)calloc((size_t)BH, sizeof(float));
+    float* dpre = (float*)malloc(sizeof(float) * BH);
+    double* acc = (double*)malloc(sizeof(double) * H);
+    int32_t* slot_in = (int32_t*)malloc(sizeof(int32_t) * V);
+    int32_t* slot_out = (int32_t*)malloc(sizeof(int32_t) * V);
+    for (int64_t w = 0; w < V; ++w) slot_in[w] = slot_out[w] = -1;
+    int64_t nin = 0, nout = 0;
+    memset(g_rec, 0, sizeof(float) * H * H);
+    for (int64_t t = T - 1; t >= 0; --t) {
+      const float* ht1 = h + (t + 1) * BH;
+      /* score_backward per record (rnn.hpp:251-255): sparse row axpy, then
+       * dh[b] += ds * W_out[w] (float axpy) */
+      for (int64_t b = 0; b < B; ++b) {
+        const int64_t idx = t * B + b;
+        if (!has[idx]) continue;
+        for (int64_t r = 0; r < K1; ++r) {
+          const uint32_t w = rw[idx * K1 + r];
+          const float ds = rds[idx * K1 + r];
+          if (slot_out[w] < 0) {
+            slot_out[w] = (int32_t)nout;
+            g_out_words[nout] = w;
+            memset(g_out_data + nout * H, 0, sizeof(float) * H);
+            ++nout;
+          }
+          float* gr = g_out_data + (int64_t)slot_out[w] * H;
+          const float* hb = ht1 + b * H;
+          const float* wr = w_out + (int64_t)w * H;
+          float* db = dh + b * H;
+          for (int64_t i = 0; i < H; ++i) gr[i] += ds * hb[i];
+          for (int64_t i = 0; i < H; ++i) db[i] += ds * wr[i];
+        }
+      }
+      for (int64_t i = 0; i < BH; ++i) dpre[i] = dh[i] * act_deriv_f(act, ht1[i]);
+      matmul_tn_add(dpre, h + t * BH, g_rec, B, H, H);
+      for (int64_t b = 0; b < B; ++b) {
+        const uint32_t w = inputs[t * B + b];
+        if (slot_in[w] < 0) {
+          slot_in[w] = (int32_t)nin;
+          g_in_words[nin] = w;
+          memset(g_in_data + nin * H, 0, sizeof(float) * H);
+          ++nin;
+        }
+        float* r = g_in_data + (int64_t)slot_in[w] * H;
+        for (int64_t i = 0; i < H; ++i) r[i] += 1.0f * dpre[b * H + i];
+      }
+      if (t > 0) matmul_nn(dpre, w_rec, dh, B, H, H, 0, acc);
+    }
+    *g_in_rows = nin;
+    *g_out_rows = nout;
+    for (int64_t i = 0; i < nin * H; ++i) g_in_data[i] = clip1(g_in_data[i], clip);
+    for (int64_t i = 0; i < H * H; ++i) g_rec[i] = clip1(g_rec[i], clip);
+    for (int64_t i = 0; i < nout * H; ++i) g_out_data[i] = clip1(g_out_data[i], clip);
+    free(dh);
+    free(dpre);
+    free(acc);
+    free(slot_in);
+    free(slot_out);
+  }
+  free(h);
+  free(pre);
+  free(rw);
+  free(rds);
+  free(has);
   return 0;
 }
 

@@ -150,6 +150,87 @@ int ref_random_stream_pair(std::uint64_t seed, std::uint64_t v,
   });
 }
 
+// mt19937_64 state as 312 words + position (the libstdc++ stream order).
+static std::mt19937_64 rng_from(const std::uint64_t* st) {
+  std::stringstream ss;
+  for (int i = 0; i < 313; ++i) ss << st[i] << ' ';
+  std::mt19937_64 r;
+  ss >> r;
+  return r;
+}
+static void rng_to(const std::mt19937_64& r, std::uint64_t* st) {
+  std::stringstream ss;
+  ss << r;
+  for (int i = 0; i < 313; ++i) ss >> st[i];
+}
+
+void ref_mt_state(std::uint64_t seed, std::uint64_t* st) { rng_to(std::mt19937_64(seed), st); }
+
+// NoiseModel(counts, k, floor) (nce.hpp:41-66): ln(k q) per word and n draws
+// of its alias sampler from the given rng state (state updated in place).
+int ref_noise_sample(std::int64_t V, const double* counts, int k, double floor,
+                     std::uint64_t* rng, std::int64_t n, std::uint32_t* out,
+                     double* ln_kq) {
+  return guarded([&] {
+    NoiseModel nm(std::vector<double>(counts, counts + V), k, floor);
+    std::mt19937_64 r = rng_from(rng);
+    for (std::int64_t i = 0; i < n; ++i) out[i] = nm.sample(r);
+    for (std::int64_t w = 0; w < V; ++w) ln_kq[w] = nm.ln_kq(static_cast<WordId>(w));
+    rng_to(r, rng);
+  });
+}
+
+// One NCE-mode window (backprop.hpp:126-156).  The sparse W_out gradient
+// rows come back in slot order like W_in's (g_out_words/g_out_data hold
+// T*B*(k+1) rows).
+int ref_bptt_nce(std::int64_t V, std::int64_t H, int act, const float* w_in,
+                 const float* w_rec, const float* w_out, std::int64_t T, std::int64_t B,
+                 const std::uint32_t* inputs, const std::uint32_t* targets,
+                 const std::uint8_t* weights, const float* h0, double loss_scale, float clip,
+                 int compute_grads, const double* counts, int k, double floor,
+                 std::uint64_t* rng, float* h_final, std::int64_t* g_in_rows,
+                 std::uint32_t* g_in_words, float* g_in_data, float* g_rec,
+                 std::int64_t* g_out_rows, std::uint32_t* g_out_words, float* g_out_data,
+                 double* loss, std::uint64_t* positions) {
+  return guarded([&] {
+    const RnnParams<float> p = make_params(V, H, act, w_in, w_rec, w_out);
+    WindowBatch wb;
+    wb.resize(T, B);
+    std::memcpy(wb.inputs.data(), inputs, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.targets.data(), targets, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.weights.data(), weights, T * B);
+    Mat<float> h0m(B, H);
+    std::memcpy(h0m.a.data(), h0, sizeof(float) * B * H);
+    StandardAdapter<float> a(p);
+    NoiseModel nm(std::vector<double>(counts, counts + V), k, floor);
+    std::mt19937_64 r = rng_from(rng);
+    BpttOptions<float> opt;
+    opt.mode = LossMode::kNce;
+    opt.noise = &nm;
+    opt.rng = &r;
+    opt.loss_scale = loss_scale;
+    opt.clip = clip;
+    opt.compute_grads = compute_grads != 0;
+    StandardGrads<float> g;
+    Mat<float> hf;
+    const BpttResult res = bptt_run(a, wb, h0m, compute_grads ? &g : nullptr,
+                                    h_final ? &hf : nullptr, opt);
+    rng_to(r, rng);
+    *loss = res.loss;
+    *positions = res.positions;
+    if (h_final) std::memcpy(h_final, hf.a.data(), sizeof(float) * B * H);
+    if (compute_grads) {
+      *g_in_rows = static_cast<std::int64_t>(g.w_in.rows());
+      for (std::size_t s2 = 0; s2 < g.w_in.rows(); ++s2) g_in_words[s2] = g.w_in.words[s2];
+      std::memcpy(g_in_data, g.w_in.data.data(), sizeof(float) * g.w_in.data.size());
+      std::memcpy(g_rec, g.w_rec.a.data(), sizeof(float) * H * H);
+      *g_out_rows = static_cast<std::int64_t>(g.w_out_sp.rows());
+      for (std::size_t s2 = 0; s2 < g.w_out_sp.rows(); ++s2) g_out_words[s2] = g.w_out_sp.words[s2];
+      std::memcpy(g_out_data, g.w_out_sp.data.data(), sizeof(float) * g.w_out_sp.data.size());
+    }
+  });
+}
+
 // One softmax-mode window.  Sparse W_in gradient is exported in the
 // reference's slot order (first touch, t descending then b ascending).
 // g_in_words/g_in_data must hold T*B rows; *g_in_rows receives the count.

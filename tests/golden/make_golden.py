@@ -37,6 +37,38 @@ def window_case(ref, V, H, T, B, act, mask, clip, seed):
                 u_m_rec=s2[0], u_m_in=s2[1], u_m_out=s2[2], applied=applied)
 
 
+def nce_case(ref, V, H, T, B, k, floor, seed):
+    """One NCE-mode window (backprop.hpp:126-156) + the sparse-W_out rmsprop
+    step; the noise model is built from a unigram count vector."""
+    rng = np.random.default_rng(seed)
+    params = ref.init_uniform(V, H, seed + 1)
+    counts = rng.integers(0, 40, V).astype(np.float64)
+    counts[1] = 0.0  # bos is never a target
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.15).astype(np.uint8)
+    h0 = rng.uniform(-0.5, 0.5, (B, H)).astype(np.float32)
+    st0 = ref.mt_state(seed + 2)
+    st = st0.copy()
+    r = ref.bptt_nce(params, 0, x, y, w, h0, 1.0 / (T * B), 1.0, counts, k, floor, st)
+    state = (rng.uniform(0, 0.01, (H, H)).astype(np.float32),
+             rng.uniform(0, 0.01, V).astype(np.float32),
+             rng.uniform(0, 0.01, V).astype(np.float32))
+    p2, s2, applied = ref.rmsprop(params, state, r, 0.9995, 1e-6, 0.05, out_dense=False)
+    return dict(V=V, H=H, T=T, B=B, k=k, floor=floor, counts=counts, w_in=params[0],
+                w_rec=params[1], w_out=params[2], x=x, y=y, w=w, h0=h0, rng0=st0, rng1=st,
+                loss=r["loss"], positions=r["positions"], h_final=r["h_final"],
+                g_in_words=r["g_in_words"], g_in_rows=r["g_in_rows"], g_rec=r["g_rec"],
+                g_out_words=r["g_out_words"], g_out_rows=r["g_out_rows"], m_rec=state[0],
+                m_in=state[1], m_out=state[2], u_w_in=p2[0], u_w_rec=p2[1], u_w_out=p2[2],
+                u_m_rec=s2[0], u_m_in=s2[1], u_m_out=s2[2], applied=applied)
+
+
+def write_nce(ref, out):
+    for i, args in enumerate([(60, 12, 5, 4, 5, 1e-3, 301), (400, 32, 6, 8, 16, 1e-8, 333)]):
+        np.savez_compressed(os.path.join(out, f"nce_{i}.npz"), **nce_case(ref, *args))
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -75,6 +107,7 @@ def main():
     np.savez_compressed(os.path.join(out, "kat.npz"),
                         stream_1001=ref.random_stream(1001, 10000, 200)[:200],
                         init_11=np.concatenate([a.ravel()[:16] for a in ref.init_uniform(7, 5, 11)]))
+    write_nce(ref, out)
     print("golden fixtures written to", out)
 
 

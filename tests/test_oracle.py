@@ -184,3 +184,50 @@ def test_trainer_vs_reference(orc, ref, H, noffset, B, T, L, act):
     assert np.array_equal(st["cursors"], r["cursors"])
     for u, v in zip(st["params"] + st["opt"], r["params"] + r["opt"]):
         assert np.array_equal(u, v)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "nce_*.npz"))))
+def test_nce_golden_bitexact(orc, path):
+    """NCE window (backprop.hpp:126-156): noise model, alias draws from the
+    fixture's mt19937_64 state, loss, sparse W_out / W_in rows, W_rec and the
+    sparse-W_out rmsprop step all equal the reference's fixture."""
+    g = np.load(path)
+    params = (g["w_in"], g["w_rec"], g["w_out"])
+    noise = orc.noise_build(g["counts"], int(g["k"]), float(g["floor"]))
+    st = g["rng0"].copy()
+    T, B = g["x"].shape
+    r = orc.bptt_nce(params, 0, g["x"], g["y"], g["w"], g["h0"], 1.0 / (T * B), 1.0, noise, st)
+    assert np.array_equal(st, g["rng1"])
+    assert r["loss"] == float(g["loss"]) and r["positions"] == int(g["positions"])
+    for key in ("h_final", "g_in_words", "g_in_rows", "g_rec", "g_out_words", "g_out_rows"):
+        assert np.array_equal(r[key], g[key]), key
+    state = (g["m_rec"], g["m_in"], g["m_out"])
+    p2, s2, ok = orc.rmsprop(params, state, r, 0.9995, 1e-6, 0.05, out_dense=False)
+    assert ok == bool(g["applied"])
+    for a, key in zip(p2 + s2, ("u_w_in", "u_w_rec", "u_w_out", "u_m_rec", "u_m_in", "u_m_out")):
+        assert np.array_equal(a, g[key]), key
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_nce_random_configs_vs_reference(orc, ref, seed):
+    rng = np.random.default_rng(seed)
+    V, H = int(rng.integers(20, 500)), int(rng.integers(3, 40))
+    T, B, k = int(rng.integers(1, 7)), int(rng.integers(1, 6)), int(rng.integers(1, 20))
+    act = int(rng.integers(0, 2))
+    floor = [1e-8, 1e-3][seed % 2]
+    counts = rng.integers(0, 30, V).astype(np.float64)
+    counts[1] = 0
+    params = orc.init_uniform(V, H, seed)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.2).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    noise = orc.noise_build(counts, k, floor)
+    s1, s2 = orc.mt_state(seed), ref.mt_state(seed)
+    assert np.array_equal(s1, s2)
+    a = orc.bptt_nce(params, act, x, y, w, h0, 0.1, 0.5, noise, s1)
+    b = ref.bptt_nce(params, act, x, y, w, h0, 0.1, 0.5, counts, k, floor, s2)
+    assert np.array_equal(s1, s2)
+    assert a["loss"] == b["loss"] and a["positions"] == b["positions"]
+    for key in ("h_final", "g_in_dense", "g_rec", "g_out_words", "g_out_rows"):
+        assert np.array_equal(a[key], b[key]), key
