@@ -176,6 +176,28 @@ int dl_local_group_create(int G, void** group);
 int dl_local_group_destroy(void* group);
 int dl_comm_init_local(dl_ctx* ctx, void* group, int rank);
 
+/* ---- NCE (LossMode::kNce, the reference's default training mode) ------- */
+
+/* Loss mode of the following windows: 0 = NCE (backprop.hpp:126-156), 1 =
+ * exact softmax (the default of a fresh context).  TrainConfig::mode,
+ * trainer.hpp:53. */
+int dl_set_loss_mode(dl_ctx* ctx, int mode);
+
+/* NoiseModel(counts, k, floor) (nce.hpp:41-66): unigram counts of the
+ * training stream (NoiseModel::from_stream counts every non-bos token),
+ * k noise samples per position.  Sampling uses the AliasSampler of
+ * rng.hpp:54-94 on the host, the ln(k q) table lives on the device. */
+int dl_set_noise(dl_ctx* ctx, const double* counts, int64_t V, int k, double floor);
+
+/* The std::mt19937_64 the noise draws come from (BpttOptions::rng,
+ * backprop.hpp:52-61; Trainer::rng_, trainer.hpp:184, :284, :314): 312 state
+ * words then the position, as the libstdc++ stream operators write them.
+ * Every NCE window advances it by 2 draws per noise sample. */
+int dl_set_rng_state(dl_ctx* ctx, const uint64_t state[313]);
+int dl_get_rng_state(const dl_ctx* ctx, uint64_t state[313]);
+/* state of std::mt19937_64(seed) (host helper) */
+int dl_rng_seed_state(uint64_t seed, uint64_t state[313]);
+
 /* Vocabulary-sharded softmax (no reference counterpart: the reference's
  * output layer, rnn.hpp:245-258 / backprop.hpp:162-186, is one V x H
  * matrix).  With on != 0, after dl_comm_init(_local) with G ranks, rank r

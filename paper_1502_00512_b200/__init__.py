@@ -39,7 +39,7 @@ from ._lib import DL_BF16, DL_FP32, DataError, DeviceError, check, load
 
 __all__ = [
     "GpuRnn", "WindowBatch", "BpttResult", "PerplexityResult", "bptt_run",
-    "rmsprop_update", "train_window", "sharded_perplexity", "rnn_perplexity", "score",
+    "rmsprop_update", "train_window", "sharded_perplexity", "rng_seed_state", "rnn_perplexity", "score",
     "TrainConfig", "EpochLog", "Trainer", "DataError", "DeviceError", "formats",
     "param_count", "make_vocab", "KSIGMOID", "KTANH", "rescore_nbest",
     "read_nbest", "write_nbest", "NBestHyp", "NBestUtt",
@@ -187,6 +187,26 @@ class GpuRnn:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self._chk(load().dl_comm_init(self._h, C.addressof(buf), nranks, rank))
 
+    def set_loss_mode(self, mode: int):
+        """0 = NCE (LossMode::kNce), 1 = exact softmax (dl_set_loss_mode)."""
+        self._chk(load().dl_set_loss_mode(self._h, int(mode)))
+
+    def set_noise(self, counts, k: int, floor: float = 1e-8):
+        """NoiseModel(counts, k, floor) (nce.hpp:41-66) for NCE windows."""
+        c = np.ascontiguousarray(counts, np.float64)
+        self._chk(load().dl_set_noise(self._h, c.ctypes.data, len(c), int(k), float(floor)))
+
+    def set_rng_state(self, state):
+        st = np.ascontiguousarray(state, np.uint64)
+        if st.shape != (313,):
+            raise ValueError("rng state: 313 uint64 (312 words + position)")
+        self._chk(load().dl_set_rng_state(self._h, st.ctypes.data))
+
+    def rng_state(self):
+        st = np.zeros(313, np.uint64)
+        self._chk(load().dl_get_rng_state(self._h, st.ctypes.data))
+        return st
+
     def set_vocab_shard(self, on=True):
         """Vocabulary-sharded softmax over the communicator's ranks
         (dl_set_vocab_shard): this rank keeps W_out rows [r*V/G, (r+1)*V/G).
@@ -195,6 +215,13 @@ class GpuRnn:
         gathered window.  Zeroes W_out / m_out -- call before set_params."""
         mode = 2 if on == "dp" else int(on)
         self._chk(load().dl_set_vocab_shard(self._h, mode))
+
+
+def rng_seed_state(seed: int):
+    """std::mt19937_64(seed) as 312 state words + position (uint64[313])."""
+    st = np.zeros(313, np.uint64)
+    check(load().dl_rng_seed_state(int(seed), st.ctypes.data))
+    return st
 
 
 def init_uniform(V: int, H: int, seed: int, init_range: float = 0.1):

@@ -23,6 +23,8 @@ EXPORTS = (
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
     "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
     "dl_local_group_destroy", "dl_comm_init_local", "dl_set_vocab_shard",
+    "dl_set_loss_mode", "dl_set_noise", "dl_set_rng_state", "dl_get_rng_state",
+    "dl_rng_seed_state",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -88,6 +90,11 @@ def load():
         "dl_local_group_destroy": (C.c_int, [vp]),
         "dl_comm_init_local": (C.c_int, [vp, vp, C.c_int]),
         "dl_set_vocab_shard": (C.c_int, [vp, C.c_int]),
+        "dl_set_loss_mode": (C.c_int, [vp, C.c_int]),
+        "dl_set_noise": (C.c_int, [vp, vp, i64, C.c_int, C.c_double]),
+        "dl_set_rng_state": (C.c_int, [vp, vp]),
+        "dl_get_rng_state": (C.c_int, [vp, vp]),
+        "dl_rng_seed_state": (C.c_int, [u64, vp]),
         "dl_launch_count": (u64, [vp]),
         "dl_cuda_stream": (vp, [vp]),
         "dl_set_profiling": (C.c_int, [vp, C.c_int]),

@@ -442,7 +442,8 @@ constexpr int kLongRows = 256;     // rows staged per pass in k_embed_long
 __global__ void __launch_bounds__(32 * kShortWarps)
 k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__ seg_start,
               const int* __restrict__ n_seg, const int* __restrict__ order_pos,
-              float* __restrict__ rows, float clip, int* nonfinite) {
+              const float* __restrict__ order_scale, float* __restrict__ rows, float clip,
+              int* nonfinite) {
   const int ns = __ldg(n_seg);
   const int lane = threadIdx.x % 32;
   const int64_t nchunk = (H + 1023) / 1024;
@@ -458,7 +459,10 @@ k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__
       // unaligned rows: one column per lane
       for (int64_t j = c0 + lane; j < min(H, c0 + 1024); j += 32) {
         float acc = 0.f;
-        for (int i = a; i < e; ++i) acc += 1.0f * dpre[(int64_t)order_pos[i] * H + j];
+        for (int i = a; i < e; ++i) {
+          const float v = dpre[(int64_t)order_pos[i] * H + j];
+          acc = __fadd_rn(acc, order_scale ? __fmul_rn(order_scale[i], v) : v);
+        }
         acc = clip1(acc, clip);
         bad |= !isfinite(acc);
         rows[(int64_t)slot * H + j] = acc;
@@ -470,18 +474,20 @@ k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__
     for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = a; i < e; ++i) {
       const float* src = dpre + (int64_t)__ldg(order_pos + i) * H;
+      const float sc = order_scale ? __ldg(order_scale + i) : 1.0f;
       float4 v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int64_t j = c0 + 4 * (lane + 32 * q);
         if (j < H) v[q] = __ldg(reinterpret_cast<const float4*>(src + j));
       }
+      // (a scaled row is the reference's axpy_row: acc += s * x, two roundings)
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        acc[q].x += 1.0f * v[q].x;
-        acc[q].y += 1.0f * v[q].y;
-        acc[q].z += 1.0f * v[q].z;
-        acc[q].w += 1.0f * v[q].w;
+        acc[q].x = __fadd_rn(acc[q].x, __fmul_rn(sc, v[q].x));
+        acc[q].y = __fadd_rn(acc[q].y, __fmul_rn(sc, v[q].y));
+        acc[q].z = __fadd_rn(acc[q].z, __fmul_rn(sc, v[q].z));
+        acc[q].w = __fadd_rn(acc[q].w, __fmul_rn(sc, v[q].w));
       }
     }
 #pragma unroll
@@ -500,10 +506,11 @@ k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__
 __global__ void __launch_bounds__(256)
 k_embed_long(const float* __restrict__ dpre, int64_t H, const int* __restrict__ seg_start,
              const int* __restrict__ long_list, const int* __restrict__ n_long,
-             const int* __restrict__ order_pos, float* __restrict__ rows, float clip,
-             int* nonfinite) {
+             const int* __restrict__ order_pos, const float* __restrict__ order_scale,
+             float* __restrict__ rows, float clip, int* nonfinite) {
   __shared__ float tile[kLongRows][32];
   __shared__ int spos[kLongRows];
+  __shared__ float sscale[kLongRows];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t nchunk = (H + 31) / 32;
   const int64_t items = (int64_t)__ldg(n_long) * nchunk;
@@ -516,19 +523,23 @@ k_embed_long(const float* __restrict__ dpre, int64_t H, const int* __restrict__ 
     float acc = 0.f;
     for (int base = a; base < e; base += kLongRows) {
       const int cnt = min(kLongRows, e - base);
-      if (threadIdx.x < cnt) spos[threadIdx.x] = __ldg(order_pos + base + threadIdx.x);
+      if (threadIdx.x < cnt) {
+        spos[threadIdx.x] = __ldg(order_pos + base + threadIdx.x);
+        sscale[threadIdx.x] = order_scale ? __ldg(order_scale + base + threadIdx.x) : 1.0f;
+      }
       __syncthreads();
       float v[kLongRows / 8];
 #pragma unroll
       for (int u = 0; u < kLongRows / 8; ++u) {
         const int r = warp + 8 * u;
-        v[u] = (r < cnt && j < H) ? __ldg(dpre + (int64_t)spos[r] * H + j) : 0.f;
+        v[u] = (r < cnt && j < H) ? __fmul_rn(sscale[r], __ldg(dpre + (int64_t)spos[r] * H + j))
+                                  : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kLongRows / 8; ++u) tile[warp + 8 * u][lane] = v[u];
       __syncthreads();
       if (warp == 0)
-        for (int r = 0; r < cnt; ++r) acc += 1.0f * tile[r][lane];
+        for (int r = 0; r < cnt; ++r) acc = __fadd_rn(acc, tile[r][lane]);
       __syncthreads();
     }
     if (warp == 0 && j < H) {
@@ -989,15 +1000,18 @@ void embed_sort(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, E
   DL_RADIX(2) DL_RADIX(4) DL_RADIX(8) DL_RADIX(16) {}
 #undef DL_RADIX
 }
+int embed_short_max() { return kEmbedShort; }
+
 void embed_rows(int64_t n, const float* dpre, int64_t H, float clip, EmbedWs& ws, float* rows,
-                int* n_rows, int* nonfinite, cudaStream_t st) {
+                int* n_rows, int* nonfinite, cudaStream_t st, const float* order_scale) {
   if (n <= 0) return;
   const int64_t nchunk = (H + 1023) / 1024;
   const int64_t warps = std::min<int64_t>(n * nchunk, 148 * 64);
   k_embed_short<<<(unsigned)((warps + kShortWarps - 1) / kShortWarps), 32 * kShortWarps, 0, st>>>(
-      dpre, H, ws.seg_start, n_rows, ws.order_pos, rows, clip, nonfinite);
+      dpre, H, ws.seg_start, n_rows, ws.order_pos, order_scale, rows, clip, nonfinite);
   k_embed_long<<<148 * 2, 256, 0, st>>>(
-      dpre, H, ws.seg_start, ws.long_list(), ws.n_long(), ws.order_pos, rows, clip, nonfinite);
+      dpre, H, ws.seg_start, ws.long_list(), ws.n_long(), ws.order_pos, order_scale, rows, clip,
+      nonfinite);
 }
 void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre,
                  int64_t H, float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,

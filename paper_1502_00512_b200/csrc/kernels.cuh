@@ -15,6 +15,33 @@ struct EmbedWs {
   int64_t cap;     // T*B (positions the buffers hold)
 };
 
+// NCE records of one window (nce.cu): forward-order words / h rows / ds,
+// the processing-order -> forward map, and sort scratch
+struct NceRecs {
+  const uint32_t* rec_word;  // [N] forward order r = p*(k+1) + j
+  const uint32_t* rec_row;   // [N] t*B + b of the record's position
+  const uint32_t* proc_r;    // [N] processing order q -> r
+  const float* ds;           // [N] dloss/dscore, forward order
+  uint32_t *keys_in, *vals_in, *keys_out, *vals_out;
+  int *head, *slot;
+  void* temp;
+  size_t temp_bytes;
+};
+
+void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
+                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st);
+void nce_loss(const float* score, const uint32_t* rec_word, const double* ln_kq, int64_t P,
+              int K1, double scale, double* loss_pos, float* ds, cudaStream_t st);
+void nce_dh(const float* w_out, int64_t H, const uint32_t* rec_word, const uint32_t* rec_row,
+            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st);
+size_t nce_sort_temp_bytes(int64_t N);
+// sparse W_out gradient rows (slot order = by word), clipped: rows / words /
+// *n_rows on the device
+void nce_out_rows(const NceRecs& R, int64_t N, int64_t V, const float* h, int64_t H, float clip,
+                  struct EmbedWs& ws, float* order_scale, float* rows, uint32_t* words,
+                  int* n_rows, int* nonfinite, cudaStream_t st);
+int embed_short_max();
+
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
 void fill_f32(float* x, float v, int64_t n, cudaStream_t st);
 void rec_fwd(const float* part, int splits, int64_t split_stride, int64_t Bn, int64_t H,
@@ -46,8 +73,10 @@ void sum_rows(const double* v, const uint8_t* wts, int64_t n, double* acc,
 // embed_grads = both
 void embed_sort(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, EmbedWs& ws,
                 uint32_t* words, int* n_rows, cudaStream_t st);
+// (order_scale: optional per-sorted-record factor -- the NCE W_out rows sum
+// ds * h, SparseRowGrads::axpy_row rnn.hpp:113-116)
 void embed_rows(int64_t n, const float* dpre, int64_t H, float clip, EmbedWs& ws, float* rows,
-                int* n_rows, int* nonfinite, cudaStream_t st);
+                int* n_rows, int* nonfinite, cudaStream_t st, const float* order_scale = nullptr);
 void embed_grads(const uint32_t* x, int64_t T, int64_t B, int64_t G, int64_t V, const float* dpre, int64_t H,
                  float clip, EmbedWs& ws, float* rows, uint32_t* words, int* n_rows,
                  int* nonfinite, cudaStream_t st);

@@ -1,0 +1,204 @@
+// NCE output layer of the RNNLM window (LossMode::kNce, the reference's
+// default training mode): backprop.hpp:126-156 (loss), :193-203 (backward);
+// StandardAdapter::score / score_backward rnn.hpp:246-255; nce.hpp:31-36,
+// 103-129 (softplus / sigmoid / the loss); SparseRowGrads rnn.hpp:89-127.
+//
+// The noise ids are drawn on the host with the reference's mt19937_64 +
+// AliasSampler (runtime.cu), in the reference's order (t, then b, then the
+// sample; masked positions draw nothing), and arrive as records:
+//   forward order   r = p * (k+1) + j   (p = the p-th unmasked position in
+//                   t-major order, j = 0 the target, 1..k the noise words)
+//   processing order q (t descending, b ascending, j ascending) -- the order
+//                   score_backward visits them, hence the float summation
+//                   order of every sparse W_out row.
+// Kernels:
+//   k_nce_scores  score[r] = float(dot_acc<double>(h_row, W_out[w]))  -- the
+//                 reference's 8 fixed double lanes (mat.hpp:59-78), no FMA
+//   k_nce_loss    per position: a = s - ln(k q(w)); loss terms softplus;
+//                 ds = float(-scale*sigmoid(-a_t)) / float(scale*sigmoid(a))
+//   k_nce_dh      dh[row] = sum over the position's records of ds * W_out[w]
+//                 (float axpy order, mat.hpp:80-84)
+//   W_out rows    records stably radix-sorted by word (cub), segment heads,
+//                 then the segmented ds * h sums of kernels.cu (embed_rows).
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace dl {
+namespace {
+
+// one record per 8 threads: thread q owns the reference's lane q
+__global__ void k_nce_scores(const float* __restrict__ h, const float* __restrict__ w_out,
+                             int64_t H, const uint32_t* __restrict__ rec_word,
+                             const uint32_t* __restrict__ rec_row, int64_t N,
+                             float* __restrict__ score) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = gt / 8;
+  const int q = (int)(gt % 8);
+  const bool valid = r < N;
+  double s = 0.0;
+  const float* x = nullptr;
+  const float* y = nullptr;
+  const int64_t H8 = (H / 8) * 8;
+  if (valid) {
+    x = h + (int64_t)rec_row[r] * H;
+    y = w_out + (int64_t)rec_word[r] * H;
+    for (int64_t i = 0; i < H8; i += 8)
+      s = __dadd_rn(s, __dmul_rn((double)x[i + q], (double)y[i + q]));
+  }
+  // ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) + tail
+  const int base = (threadIdx.x % 32) & ~7;
+  double l[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) l[k] = __shfl_sync(0xffffffffu, s, base + k);
+  if (valid && q == 0) {
+    double tail = 0.0;
+    for (int64_t i = H8; i < H; ++i) tail = __dadd_rn(tail, __dmul_rn((double)x[i], (double)y[i]));
+    const double tot = __dadd_rn(__dadd_rn(__dadd_rn(l[0], l[1]), __dadd_rn(l[2], l[3])),
+                                 __dadd_rn(__dadd_rn(l[4], l[5]), __dadd_rn(l[6], l[7])));
+    score[r] = (float)__dadd_rn(tot, tail);
+  }
+}
+
+__device__ __forceinline__ double softplus_d(double x) {
+  return x > 0 ? x + log1p(exp(-x)) : log1p(exp(x));
+}
+__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+__global__ void k_nce_loss(const float* __restrict__ score, const uint32_t* __restrict__ rec_word,
+                           const double* __restrict__ ln_kq, int64_t P, int K1, double scale,
+                           double* __restrict__ loss_pos, float* __restrict__ ds) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int64_t r0 = p * K1;
+  const double at = (double)score[r0] - ln_kq[rec_word[r0]];
+  double L = scale * softplus_d(-at);
+  ds[r0] = (float)(-scale * sigmoid_d(-at));
+  for (int j = 1; j < K1; ++j) {
+    const double a = (double)score[r0 + j] - ln_kq[rec_word[r0 + j]];
+    L += scale * softplus_d(a);
+    ds[r0 + j] = (float)(scale * sigmoid_d(a));
+  }
+  loss_pos[p] = L;
+}
+
+// dh[row] = sum_j ds_j * W_out[w_j] in record order (float, two roundings)
+__global__ void k_nce_dh(const float* __restrict__ w_out, int64_t H,
+                         const uint32_t* __restrict__ rec_word, const uint32_t* __restrict__ rec_row,
+                         const float* __restrict__ ds, int K1, float* __restrict__ dh) {
+  const int64_t p = blockIdx.x;
+  const int64_t r0 = p * K1;
+  float* out = dh + (int64_t)rec_row[r0] * H;
+  for (int64_t i = threadIdx.x; i < H; i += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < K1; ++j)
+      acc = __fadd_rn(acc, __fmul_rn(ds[r0 + j], w_out[(int64_t)rec_word[r0 + j] * H + i]));
+    out[i] = acc;
+  }
+}
+
+// sort input in processing order: key = word, value = q
+__global__ void k_nce_sort_in(const uint32_t* __restrict__ proc_r,
+                              const uint32_t* __restrict__ rec_word, int64_t N,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  keys[q] = rec_word[proc_r[q]];
+  vals[q] = (uint32_t)q;
+}
+
+// after the stable sort: segment-head flags, and the rows / factors of the
+// segmented sums in sorted order
+__global__ void k_nce_sorted(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                             const uint32_t* __restrict__ proc_r,
+                             const uint32_t* __restrict__ rec_row, const float* __restrict__ ds,
+                             int64_t N, int* __restrict__ head, int* __restrict__ order_pos,
+                             float* __restrict__ order_scale) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+  const uint32_t r = proc_r[vals[i]];
+  order_pos[i] = (int)rec_row[r];
+  order_scale[i] = ds[r];
+}
+
+__global__ void k_nce_heads(const uint32_t* __restrict__ keys, const int* __restrict__ head,
+                            const int* __restrict__ slot, int64_t N, int* __restrict__ seg_start,
+                            uint32_t* __restrict__ words, int* __restrict__ n_seg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  if (head[i]) {
+    seg_start[slot[i]] = (int)i;
+    words[slot[i]] = keys[i];
+  }
+  if (i == N - 1) {
+    const int total = slot[i] + head[i];
+    *n_seg = total;
+    seg_start[total] = (int)N;
+  }
+}
+
+__global__ void k_nce_long(const int* __restrict__ seg_start, const int* __restrict__ n_seg,
+                           int short_max, int* __restrict__ long_list, int* __restrict__ n_long) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= *n_seg) return;
+  if (seg_start[s + 1] - seg_start[s] > short_max) long_list[atomicAdd(n_long, 1)] = s;
+}
+
+}  // namespace
+
+void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
+                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st) {
+  if (N <= 0) return;
+  const int64_t threads = N * 8;
+  k_nce_scores<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(h, w_out, H, rec_word, rec_row,
+                                                                  N, score);
+}
+
+void nce_loss(const float* score, const uint32_t* rec_word, const double* ln_kq, int64_t P,
+              int K1, double scale, double* loss_pos, float* ds, cudaStream_t st) {
+  if (P <= 0) return;
+  k_nce_loss<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(score, rec_word, ln_kq, P, K1, scale,
+                                                          loss_pos, ds);
+}
+
+void nce_dh(const float* w_out, int64_t H, const uint32_t* rec_word, const uint32_t* rec_row,
+            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st) {
+  if (P <= 0) return;
+  k_nce_dh<<<(unsigned)P, 256, 0, st>>>(w_out, H, rec_word, rec_row, ds, K1, dh);
+}
+
+size_t nce_sort_temp_bytes(int64_t N) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)N);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int*)nullptr, (int*)nullptr, (int)N);
+  return std::max(a, b);
+}
+
+void nce_out_rows(const NceRecs& R, int64_t N, int64_t V, const float* h, int64_t H, float clip,
+                  EmbedWs& ws, float* order_scale, float* rows, uint32_t* words, int* n_rows,
+                  int* nonfinite, cudaStream_t st) {
+  if (N <= 0) {
+    DL_CUDA(cudaMemsetAsync(n_rows, 0, sizeof(int), st));
+    return;
+  }
+  const unsigned g = (unsigned)((N + 255) / 256);
+  k_nce_sort_in<<<g, 256, 0, st>>>(R.proc_r, R.rec_word, N, R.keys_in, R.vals_in);
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) <= V) ++end_bit;
+  size_t tb = R.temp_bytes;
+  DL_CUDA(cub::DeviceRadixSort::SortPairs(R.temp, tb, R.keys_in, R.keys_out, R.vals_in,
+                                          R.vals_out, (int)N, 0, end_bit, st));
+  k_nce_sorted<<<g, 256, 0, st>>>(R.keys_out, R.vals_out, R.proc_r, R.rec_row, R.ds, N, R.head,
+                                  ws.order_pos, order_scale);
+  tb = R.temp_bytes;
+  DL_CUDA(cub::DeviceScan::ExclusiveSum(R.temp, tb, R.head, R.slot, (int)N, st));
+  k_nce_heads<<<g, 256, 0, st>>>(R.keys_out, R.head, R.slot, N, ws.seg_start, words, n_rows);
+  DL_CUDA(cudaMemsetAsync(ws.n_long(), 0, sizeof(int), st));
+  k_nce_long<<<g, 256, 0, st>>>(ws.seg_start, n_rows, embed_short_max(), ws.long_list(),
+                                ws.n_long());
+  embed_rows(N, h, H, clip, ws, rows, n_rows, nonfinite, st, order_scale);
+}
+
+}  // namespace dl

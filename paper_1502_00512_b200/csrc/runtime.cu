@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -169,6 +170,33 @@ struct dl_ctx {
   double* win_loss = nullptr;  // [loss, positions(u64)] of one window
   unsigned* bar_counter = nullptr;  // grid barrier of the persistent recurrence
   unsigned long long* win_pos = nullptr;
+
+  // NCE output layer (LossMode::kNce, trainer.hpp:53): noise model tables
+  // (host: alias sampler; device: ln(k q)), the bptt / trainer rng whose
+  // draws pick the noise words (host, std::mt19937_64 as the reference), and
+  // one window's records
+  int loss_mode = 1;  // 0 NCE, 1 exact softmax (LossMode order)
+  int nce_k = 0;
+  std::vector<double> nz_prob;
+  std::vector<uint32_t> nz_alias;
+  double* ln_kq_d = nullptr;
+  std::mt19937_64 rng{0};
+  bool out_sparse = false;  // the last window's dW_out is sparse rows (g_out compact)
+  int64_t nce_cap = 0, nce_P = 0, nce_N = 0;
+  uint32_t *rec_word_d = nullptr, *rec_row_d = nullptr, *proc_r_d = nullptr;
+  float *score_d = nullptr, *ds_d = nullptr, *nce_scale = nullptr;
+  double* loss_pos_d = nullptr;
+  uint32_t *sort_keys_in = nullptr, *sort_vals_in = nullptr, *sort_keys_out = nullptr,
+           *sort_vals_out = nullptr;
+  int *sort_head = nullptr, *sort_slot = nullptr;
+  void* sort_temp = nullptr;
+  size_t sort_temp_bytes = 0;
+  EmbedWs nce_ws{};
+  uint32_t* g_out_words = nullptr;  // [Vo] words of the compact sparse rows
+  int* g_out_n = nullptr;
+  std::vector<uint32_t> h_rec;  // host staging: rec_word | rec_row | proc_r
+  void* nce_pin = nullptr;      // pinned copy of h_rec for the H2D
+  size_t nce_pin_bytes = 0;
 
   // profiling
   bool profiling = false;
@@ -472,6 +500,147 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
   }
 }
 
+// ------------------------------------------------------------------ NCE
+// NoiseModel (nce.hpp:41-66) + AliasSampler (rng.hpp:54-89), host side.
+void nce_build(dl_ctx* c, const double* counts, int64_t V, int k, double floor) {
+  double total = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    DL_REQUIRE(counts[w] >= 0.0, 1, "NoiseModel: negative count");
+    total += counts[w];
+  }
+  DL_REQUIRE(total > 0.0, 1, "NoiseModel: zero total");
+  std::vector<double> q(V), lnkq(V);
+  double qsum = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    q[w] = std::max(counts[w] / total, floor);
+    qsum += q[w];
+  }
+  for (int64_t w = 0; w < V; ++w) {
+    q[w] /= qsum;
+    lnkq[w] = std::log(static_cast<double>(k) * q[w]);
+  }
+  double tw = 0.0;
+  for (double v : q) tw += v;
+  std::vector<double> prob(V, 0.0), scaled(V);
+  std::vector<uint32_t> alias(V, 0), small, large;
+  small.reserve(V);
+  large.reserve(V);
+  for (int64_t i = 0; i < V; ++i) {
+    scaled[i] = q[i] * static_cast<double>(V) / tw;
+    (scaled[i] < 1.0 ? small : large).push_back(static_cast<uint32_t>(i));
+  }
+  while (!small.empty() && !large.empty()) {
+    const uint32_t sm = small.back();
+    small.pop_back();
+    const uint32_t lg = large.back();
+    large.pop_back();
+    prob[sm] = scaled[sm];
+    alias[sm] = lg;
+    scaled[lg] = (scaled[lg] + scaled[sm]) - 1.0;
+    (scaled[lg] < 1.0 ? small : large).push_back(lg);
+  }
+  for (uint32_t i : large) prob[i] = 1.0;
+  for (uint32_t i : small) prob[i] = 1.0;
+  c->nz_prob = std::move(prob);
+  c->nz_alias = std::move(alias);
+  c->nce_k = k;
+  if (!c->ln_kq_d) c->ln_kq_d = dalloc<double>(V);
+  DL_CUDA(cudaMemcpy(c->ln_kq_d, lnkq.data(), V * 8, cudaMemcpyHostToDevice));
+}
+
+// AliasSampler::sample with uniform_index / uniform01 (rng.hpp:37-50, 91-94)
+inline uint32_t nce_draw(dl_ctx* c) {
+  const double u1 = static_cast<double>(c->rng() >> 11) * 0x1.0p-53;
+  const uint64_t i = static_cast<uint64_t>(u1 * static_cast<double>(c->nz_prob.size()));
+  const double u2 = static_cast<double>(c->rng() >> 11) * 0x1.0p-53;
+  return u2 < c->nz_prob[i] ? static_cast<uint32_t>(i) : c->nz_alias[i];
+}
+
+void nce_reserve(dl_ctx* c, int64_t N) {
+  if (N <= c->nce_cap) return;
+  auto fr = [](auto*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  fr(c->rec_word_d); fr(c->rec_row_d); fr(c->proc_r_d); fr(c->score_d); fr(c->ds_d);
+  fr(c->nce_scale); fr(c->loss_pos_d); fr(c->sort_keys_in); fr(c->sort_vals_in);
+  fr(c->sort_keys_out); fr(c->sort_vals_out); fr(c->sort_head); fr(c->sort_slot);
+  fr(c->sort_temp); fr(c->nce_ws.seg_start); fr(c->nce_ws.order_pos);
+  c->rec_word_d = dalloc<uint32_t>(N);
+  c->rec_row_d = dalloc<uint32_t>(N);
+  c->proc_r_d = dalloc<uint32_t>(N);
+  c->score_d = dalloc<float>(N);
+  c->ds_d = dalloc<float>(N);
+  c->nce_scale = dalloc<float>(N);
+  c->loss_pos_d = dalloc<double>(N);
+  c->sort_keys_in = dalloc<uint32_t>(N);
+  c->sort_vals_in = dalloc<uint32_t>(N);
+  c->sort_keys_out = dalloc<uint32_t>(N);
+  c->sort_vals_out = dalloc<uint32_t>(N);
+  c->sort_head = dalloc<int>(N);
+  c->sort_slot = dalloc<int>(N);
+  c->sort_temp_bytes = nce_sort_temp_bytes(N);
+  c->sort_temp = dalloc<uint8_t>(c->sort_temp_bytes);
+  c->nce_ws.seg_start = dalloc<int>(2 * N + 2);
+  c->nce_ws.order_pos = dalloc<int>(N);
+  c->nce_ws.cap = N;
+  c->nce_cap = N;
+}
+
+// The window's noise draws (backprop.hpp:126-156 order: t, b, then sample;
+// masked positions draw nothing) and its records in forward and processing
+// order, uploaded on the context stream.  targets / weights: host arrays.
+void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint32_t* targets,
+                 const uint8_t* weights) {
+  DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
+             "bptt: NCE mode needs noise model and rng (dl_set_noise)");
+  const int K1 = c->nce_k + 1;
+  int64_t P = 0;
+  for (int64_t i = 0; i < T * B; ++i) P += weights[i] ? 1 : 0;
+  const int64_t N = P * K1;
+  nce_reserve(c, std::max<int64_t>(N, 1));
+  c->h_rec.resize(3 * std::max<int64_t>(N, 1));
+  uint32_t* word = c->h_rec.data();
+  uint32_t* row = word + N;
+  uint32_t* proc = row + N;
+  std::vector<int64_t> first(T + 1, 0);  // forward index of row t's first position
+  int64_t p = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    first[t] = p;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t idx = t * B + b;
+      if (!weights[idx]) continue;
+      const int64_t r0 = p * K1;
+      word[r0] = targets[idx];
+      for (int j = 1; j < K1; ++j) word[r0 + j] = nce_draw(c);
+      for (int j = 0; j < K1; ++j) row[r0 + j] = static_cast<uint32_t>(idx);
+      ++p;
+    }
+  }
+  first[T] = p;
+  // processing order: t descending, b ascending, record ascending
+  int64_t q = 0;
+  for (int64_t t = T - 1; t >= 0; --t)
+    for (int64_t pp = first[t]; pp < first[t + 1]; ++pp)
+      for (int j = 0; j < K1; ++j) proc[q++] = static_cast<uint32_t>(pp * K1 + j);
+  c->nce_P = P;
+  c->nce_N = N;
+  if (N > 0) {
+    if (c->nce_pin_bytes < (size_t)(3 * N * 4)) {
+      if (c->nce_pin) cudaFreeHost(c->nce_pin);
+      DL_CUDA(cudaMallocHost(&c->nce_pin, 3 * N * 4));
+      c->nce_pin_bytes = 3 * N * 4;
+    }
+    uint32_t* pin = static_cast<uint32_t*>(c->nce_pin);
+    std::memcpy(pin, word, 3 * N * 4);
+    DL_CUDA(cudaMemcpyAsync(c->rec_word_d, pin, N * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->rec_row_d, pin + N, N * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaMemcpyAsync(c->proc_r_d, pin + 2 * N, N * 4, cudaMemcpyHostToDevice, c->st));
+    // (the staging buffer is reused by the next H2D only after this stream
+    // has consumed it: window_call synchronises every call)
+  }
+}
+
 // One window with device-resident inputs (x_d, y_d, w_d, htape[0]).
 // Accumulates loss into d_loss and scored positions into d_pos.
 // fork_out_eta > 0: apply the dense W_out rmsprop with that eta on the side
@@ -544,8 +713,21 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     yo = c->y_all;
     wo = c->w_all;
   }
-  output_layer(c, MO, Hs, Hs_bf, yo, wo, scale, grads, c->loss_row, nullptr);
-  if (dp) {
+  const bool nce = c->loss_mode == 0;
+  if (nce) {
+    // NCE loss over the window's records (backprop.hpp:126-156)
+    Phase p(c, "nce_loss");
+    const int K1 = c->nce_k + 1;
+    nce_scores(Hs, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st);
+    nce_loss(c->score_d, c->rec_word_d, c->ln_kq_d, c->nce_P, K1, scale, c->loss_pos_d, c->ds_d,
+             st);
+    sum_rows(c->loss_pos_d, nullptr, c->nce_P, c->d_loss, c->d_pos, st);
+    c->launches += 3;
+  } else {
+    output_layer(c, MO, Hs, Hs_bf, yo, wo, scale, grads, c->loss_row, nullptr);
+  }
+  if (nce) {
+  } else if (dp) {
     // the window's loss is the sum over all ranks' streams
     DL_CUDA(cudaMemsetAsync(c->win_loss, 0, 16, st));
     sum_rows(c->loss_row, c->w_d, TB, c->win_loss, c->win_pos, st);
@@ -561,7 +743,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   if (!grads) return;
 
   DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
-  const bool fused = fuse_eta > 0.0;
+  c->out_sparse = nce;
+  const bool fused = fuse_eta > 0.0 && !nce;
   // late fork: dh, then dW_out, then the dense update on the side stream
   // (in place: dh has consumed this window's shadow), overlapping the
   // latency-bound backward recurrence, dW_rec and the W_in rows
@@ -673,7 +856,16 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     }
     gemm(c, g);
   };
-  if (!fused && !late) dw_out();
+  if (nce) {
+    // score_backward of every record: dh[t][b] = sum ds * W_out[w]
+    // (rnn.hpp:251-255); masked positions contribute nothing
+    Phase p(c, "nce_dh");
+    DL_CUDA(cudaMemsetAsync(c->dh_out, 0, TB * H * sizeof(float), st));
+    nce_dh(c->w_out, H, c->rec_word_d, c->rec_row_d, c->ds_d, c->nce_P, c->nce_k + 1,
+           c->dh_out, st);
+    c->launches++;
+  }
+  if (!fused && !late && !nce) dw_out();
   if (dp) {
     // data parallel: sum dW_out over ranks, then clip --
     // on the communication stream, overlapping dh and the backward
@@ -742,7 +934,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       gemm(c, g);
     }
   };
-  dh();
+  if (!nce) dh();
   if (fused || late) dw_out();
   if (late) fork_update(late_eta, c->w_out_bf);
   if (vs) {
@@ -832,6 +1024,17 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     embed_rows(TB, c->dpre, H, clip, c->ews, c->g_in_rows, c->g_in_n, c->nonfinite, st);
     c->launches += 2;
   }
+  if (nce) {
+    // sparse W_out rows: records by word in processing order, sum of
+    // ds * h[t+1][b], clipped (SparseRowGrads, rnn.hpp:89-127, 155-162)
+    Phase p(c, "nce_out_rows");
+    NceRecs R{c->rec_word_d, c->rec_row_d, c->proc_r_d, c->ds_d, c->sort_keys_in,
+              c->sort_vals_in, c->sort_keys_out, c->sort_vals_out, c->sort_head,
+              c->sort_slot, c->sort_temp, c->sort_temp_bytes};
+    nce_out_rows(R, c->nce_N, Vo, Hs, H, clip, c->nce_ws, c->nce_scale, c->g_out,
+                 c->g_out_words, c->g_out_n, c->nonfinite, st);
+    c->launches += 8;
+  }
   // a non-finite dW_out block on one rank must skip the update everywhere
   // (only reachable with an infinite clip bound)
   if ((vs || dpv) && !std::isfinite(clip)) {
@@ -851,7 +1054,13 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
-  if (!skip_out && c->dp16)
+  if (!skip_out && c->out_sparse) {
+    // NCE: per-word-averaged sparse update of W_out (rmsprop.hpp:77-92, :129)
+    rms_decay(c->m_out, c->Vo, c->rho, c->nonfinite, st);
+    rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, c->g_out_words,
+             c->g_out_n, c->Vo, c->H, c->rho, c->eps, eta, 0, c->nonfinite, st);
+    c->launches += 2;
+  } else if (!skip_out && c->dp16)
     rms_dense_g16c(c->w_out, c->w_out_bf, c->m_out, c->g_out_bf, c->Vo, c->H, c->dp16_clip,
                    c->rho, c->eps, eta, st);
   else if (!skip_out && c->g16_valid)
@@ -875,11 +1084,13 @@ void alloc_output(dl_ctx* c) {
     p = nullptr;
   };
   fr(c->w_out); fr(c->m_out); fr(c->g_out); fr(c->w_out_bf); fr(c->w_out_bf_next);
-  fr(c->g_out_bf); fr(c->rowsq); fr(c->rms_cnt);
+  fr(c->g_out_bf); fr(c->rowsq); fr(c->rms_cnt); fr(c->g_out_words); fr(c->g_out_n);
   const int64_t Vo = c->Vo, H = c->H;
   c->w_out = dalloc<float>(Vo * H);
   c->m_out = dalloc<float>(Vo);
   c->g_out = dalloc<float>(Vo * H);
+  c->g_out_words = dalloc<uint32_t>(Vo);
+  c->g_out_n = dalloc<int>(1);
   DL_CUDA(cudaMemsetAsync(c->w_out, 0, Vo * H * 4, c->st));
   DL_CUDA(cudaMemsetAsync(c->m_out, 0, Vo * 4, c->st));
   if (c->precision == DL_BF16) {
@@ -1006,6 +1217,10 @@ int dl_destroy(dl_ctx* c) {
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
                   c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
                   c->hs_all_bf, c->hs_all, c->y_all, c->w_all, c->dh_all,
+                  c->ln_kq_d, c->rec_word_d, c->rec_row_d, c->proc_r_d, c->score_d, c->ds_d,
+                  c->nce_scale, c->loss_pos_d, c->sort_keys_in, c->sort_vals_in,
+                  c->sort_keys_out, c->sort_vals_out, c->sort_head, c->sort_slot, c->sort_temp,
+                  c->nce_ws.seg_start, c->nce_ws.order_pos, c->g_out_words, c->g_out_n,
                   c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1014,6 +1229,7 @@ int dl_destroy(dl_ctx* c) {
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
+  if (c->nce_pin) cudaFreeHost(c->nce_pin);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->st2) cudaStreamDestroy(c->st2);
@@ -1095,8 +1311,11 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
   for (int64_t i = 0; i < T * B; ++i)
     if (inputs[i] >= (uint64_t)c->V || targets[i] >= (uint64_t)c->V)
       return fail(c, DL_EINVAL, "bptt: word id out of range");
+  if (c->loss_mode == 0 && c->comm)
+    return fail(c, DL_EINVAL, "NCE mode: multi-rank windows are not supported");
   return guarded(c, [&] {
     ensure_window(c, T, B);
+    if (c->loss_mode == 0) nce_prepare(c, T, B, targets, weights);
     const int64_t TB = T * B, BH = B * c->H;
     // H2D of the window: page-locked caller buffers are copied from directly,
     // pageable ones through one pinned staging buffer
@@ -1117,7 +1336,7 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
     DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
     if (eta > 0.0) {
       // Trainer::run_epoch's bptt_run + update (trainer.hpp:391-397)
-      const bool fuse = fuse_ok(c, clip);
+      const bool fuse = c->loss_mode != 0 && fuse_ok(c, clip);
       run_window(c, T, B, loss_scale, clip, true, 0.0, fuse ? eta : 0.0);
       run_rmsprop(c, eta, TB * dp_ranks(c), /*skip_out=*/fuse);
     } else {
@@ -1175,7 +1394,16 @@ int dl_get_grads(dl_ctx* c, float* g_in_dense, float* g_rec, float* g_out) {
       cudaFree(dense);
     }
     if (g_rec) DL_CUDA(cudaMemcpyAsync(g_rec, c->g_rec, c->H * c->H * 4, cudaMemcpyDeviceToHost, c->st));
-    if (g_out && (c->g16_valid || c->dp16)) {
+    if (g_out && c->out_sparse) {
+      // NCE: the sparse rows scattered into the dense layout (to_dense)
+      float* dense = dalloc<float>(c->Vo * c->H);
+      DL_CUDA(cudaMemsetAsync(dense, 0, c->Vo * c->H * 4, c->st));
+      embed_dense(c->g_out, c->g_out_words, c->g_out_n, c->Vo, c->H, dense, c->st);
+      DL_CUDA(cudaMemcpyAsync(g_out + c->v0 * c->H, dense, c->Vo * c->H * 4,
+                              cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      cudaFree(dense);
+    } else if (g_out && (c->g16_valid || c->dp16)) {
       // bf16 gradient of the throughput path, widened on the host (the
       // data-parallel one is the unclipped rank sum: clipped here as the
       // update kernel does, rnn.hpp:131-134)
@@ -1643,6 +1871,49 @@ int dl_comm_init_local(dl_ctx* c, void* group, int rank) {
     delete c->comm;
     c->comm = g->G > 1 ? new LocalComm(g, rank) : nullptr;
   });
+}
+
+int dl_set_loss_mode(dl_ctx* c, int mode) {
+  if (!c) return fail(c, DL_EINVAL, "dl_set_loss_mode: null ctx");
+  if (mode != 0 && mode != 1) return fail(c, DL_EINVAL, "dl_set_loss_mode: 0 (NCE) or 1 (softmax)");
+  c->loss_mode = mode;
+  c->have_grads = false;
+  drop_graphs(c);
+  return DL_OK;
+}
+
+int dl_set_noise(dl_ctx* c, const double* counts, int64_t V, int k, double floor) {
+  if (!c || !counts) return fail(c, DL_EINVAL, "dl_set_noise: null argument");
+  if (V != c->V) return fail(c, DL_EINVAL, "NoiseModel: vocabulary size mismatch");
+  if (k < 1) return fail(c, DL_EINVAL, "NoiseModel: k must be >= 1");
+  if (!(floor > 0.0)) return fail(c, DL_EINVAL, "config: noise_floor must be > 0");
+  return guarded(c, [&] { nce_build(c, counts, V, k, floor); });
+}
+
+int dl_set_rng_state(dl_ctx* c, const uint64_t state[313]) {
+  if (!c || !state) return fail(c, DL_EINVAL, "dl_set_rng_state: null argument");
+  std::stringstream ss;
+  for (int i = 0; i < 313; ++i) ss << state[i] << ' ';
+  ss >> c->rng;
+  if (!ss) return fail(c, DL_EINVAL, "dl_set_rng_state: bad state");
+  drop_graphs(c);
+  return DL_OK;
+}
+
+int dl_get_rng_state(const dl_ctx* c, uint64_t state[313]) {
+  if (!c || !state) return fail(nullptr, DL_EINVAL, "dl_get_rng_state: null argument");
+  std::stringstream ss;
+  ss << c->rng;
+  for (int i = 0; i < 313; ++i) ss >> state[i];
+  return DL_OK;
+}
+
+int dl_rng_seed_state(uint64_t seed, uint64_t state[313]) {
+  if (!state) return fail(nullptr, DL_EINVAL, "dl_rng_seed_state: null argument");
+  std::stringstream ss;
+  ss << std::mt19937_64(seed);
+  for (int i = 0; i < 313; ++i) ss >> state[i];
+  return DL_OK;
 }
 
 int dl_set_vocab_shard(dl_ctx* c, int on) {
