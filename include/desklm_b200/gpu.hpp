@@ -243,12 +243,22 @@ class Trainer {
         model_(params.v, params.h, static_cast<int>(params.act), prec, device),
         rng_(cfg.seed) {
     cfg_.validate();
-    if (static_cast<int>(cfg_.mode) != 1)
-      throw std::invalid_argument("b200 trainer: only the exact-softmax loss is on the GPU path");
+    const int mode = static_cast<int>(cfg_.mode);  // LossMode: 0 NCE, 1 softmax
     if (static_cast<std::int64_t>(vocab_.size()) != params.v)
       throw std::invalid_argument("trainer: vocabulary/model size mismatch");
     model_.upload(params);
     model_.set_opt(nullptr, nullptr, nullptr, cfg_.rho, cfg_.eps);
+    if (mode == 0) {
+      // NoiseModel::from_stream (nce.hpp:69-76, trainer.hpp:207-209); the
+      // noise draws come from rng_ (seeded with cfg.seed, trainer.hpp:184)
+      std::vector<double> counts(static_cast<std::size_t>(params.v), 0.0);
+      for (std::uint32_t id : train_)
+        if (id != 1u) counts.at(id) += 1.0;
+      check(dl_set_loss_mode(model_.get(), 0), model_.get());
+      check(dl_set_noise(model_.get(), counts.data(), params.v, cfg_.nce_k, cfg_.noise_floor),
+            model_.get());
+      put_rng();
+    }
     if (cfg_.valid_limit > 0 && static_cast<std::int64_t>(valid.ids.size()) > cfg_.valid_limit)
       valid_.assign(valid.ids.begin(), valid.ids.begin() + cfg_.valid_limit);
     else
@@ -355,7 +365,9 @@ class Trainer {
     io::u32(os, static_cast<std::uint32_t>(bad_epochs_));
     io::f64(os, initial_ppl_);
     std::ostringstream rs;
-    rs << rng_;  // softmax mode never draws: the freshly seeded generator
+    // NCE draws advanced the library's generator; softmax mode never draws
+    // (the freshly seeded one)
+    rs << (static_cast<int>(cfg_.mode) == 0 ? library_rng() : rng_);
     io::str(os, rs.str());
     io::u64(os, static_cast<std::uint64_t>(N));
     for (std::int64_t c : cur) io::u64(os, static_cast<std::uint64_t>(c));
@@ -385,6 +397,24 @@ class Trainer {
   std::vector<std::uint32_t> valid_;
   mutable Model model_;
   std::mt19937_64 rng_;
+
+  // rng_ <-> the library's generator (312 words + position, stream order)
+  void put_rng() {
+    std::stringstream ss;
+    ss << rng_;
+    std::uint64_t st[313];
+    for (auto& v : st) ss >> v;
+    check(dl_set_rng_state(model_.get(), st), model_.get());
+  }
+  std::mt19937_64 library_rng() const {
+    std::uint64_t st[313];
+    check(dl_get_rng_state(model_.get(), st), model_.get());
+    std::stringstream ss;
+    for (auto v : st) ss << v << ' ';
+    std::mt19937_64 r;
+    ss >> r;
+    return r;
+  }
   std::vector<EpochLog> logs_;
   int epoch_ = 0;
   int bad_epochs_ = 0;

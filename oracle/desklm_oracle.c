@@ -793,8 +793,9 @@ int orc_train(const orc_train_config* c, int64_t V, float* w_in, float* w_rec,
               double* eta_out, double* best_out, int* bad_out, int* epoch_out) {
   const int64_t H = c->nstate, B = c->minibatch, T = c->unroll;
   const int64_t N = (int64_t)c->noffset * B;
-  if (c->mode != 1) return 1; /* NCE is out of scope for this oracle */
+  if (c->mode != 0 && c->mode != 1) return 1;
   if (L < N) return 1;
+  const int nce = c->mode == 0;
   for (int64_t i = 0; i < N; ++i) cursors[i] = i * L / N;
   const float a0 = act_f(c->act, 0.0f);
   for (int64_t i = 0; i < N * H; ++i) hidden[i] = a0;
@@ -816,6 +817,28 @@ int orc_train(const orc_train_config* c, int64_t V, float* w_in, float* w_rec,
   float* gd = (float*)malloc(sizeof(float) * T * B * H);
   float* grec = (float*)malloc(sizeof(float) * H * H);
   float* gout = (float*)malloc(sizeof(float) * V * H);
+  /* NCE: NoiseModel::from_stream (nce.hpp:69-76, trainer.hpp:207-209) and
+   * Trainer::rng_(seed) (trainer.hpp:184) */
+  const int K1 = nce ? c->nce_k + 1 : 1;
+  double *nq = NULL, *nlnkq = NULL, *nprob = NULL;
+  uint32_t *nalias = NULL, *gow = NULL;
+  float* god = NULL;
+  uint64_t rng[313];
+  if (nce) {
+    double* counts = (double*)calloc((size_t)V, sizeof(double));
+    for (int64_t i = 0; i < L; ++i)
+      if (ids[i] != 1u) counts[ids[i]] += 1.0;
+    nq = (double*)malloc(sizeof(double) * V);
+    nlnkq = (double*)malloc(sizeof(double) * V);
+    nprob = (double*)malloc(sizeof(double) * V);
+    nalias = (uint32_t*)malloc(sizeof(uint32_t) * V);
+    rc = orc_noise_build(V, counts, c->nce_k, c->noise_floor, nq, nlnkq, nprob, nalias);
+    free(counts);
+    orc_mt_state(c->seed, rng);
+    gow = (uint32_t*)malloc(sizeof(uint32_t) * T * B * K1);
+    god = (float*)malloc(sizeof(float) * T * B * K1 * H);
+    if (rc) goto done;
+  }
   if (run_epochs) {
     double tl;
     uint64_t pr;
@@ -837,14 +860,24 @@ int orc_train(const orc_train_config* c, int64_t V, float* w_in, float* w_rec,
           double loss;
           uint64_t pos;
           int64_t nrows;
-          orc_bptt(V, H, c->act, w_in, w_rec, w_out, T, B, xin, yt, wt, h0,
-                   1.0 / (double)(B * T), (float)c->clip, 1, 1, hf, &nrows, gw,
-                   gd, grec, gout, &loss, &pos);
+          int applied;
+          if (nce) {
+            int64_t nout;
+            orc_bptt_nce(V, H, c->act, w_in, w_rec, w_out, T, B, xin, yt, wt, h0,
+                         1.0 / (double)(B * T), (float)c->clip, 1, c->nce_k, nlnkq, nprob,
+                         nalias, rng, hf, &nrows, gw, gd, grec, &nout, gow, god, NULL, &loss,
+                         &pos);
+            orc_rmsprop(V, H, w_in, w_rec, w_out, m_rec, m_in, m_out, c->rho, c->eps, eta,
+                        nrows, gw, gd, grec, 0, nout, gow, god, &applied);
+          } else {
+            orc_bptt(V, H, c->act, w_in, w_rec, w_out, T, B, xin, yt, wt, h0,
+                     1.0 / (double)(B * T), (float)c->clip, 1, 1, hf, &nrows, gw,
+                     gd, grec, gout, &loss, &pos);
+            orc_rmsprop(V, H, w_in, w_rec, w_out, m_rec, m_in, m_out, c->rho,
+                        c->eps, eta, nrows, gw, gd, grec, 1, 0, NULL, gout, &applied);
+          }
           loss_sum += loss;
           ++windows;
-          int applied;
-          orc_rmsprop(V, H, w_in, w_rec, w_out, m_rec, m_in, m_out, c->rho,
-                      c->eps, eta, nrows, gw, gd, grec, 1, 0, NULL, gout, &applied);
           if (!applied) ++skipped;
           for (int64_t b = 0; b < B; ++b) {
             memcpy(hidden + (s0 + b) * H, hf + b * H, sizeof(float) * H);
@@ -896,5 +929,11 @@ done:
   free(gd);
   free(grec);
   free(gout);
+  free(nq);
+  free(nlnkq);
+  free(nprob);
+  free(nalias);
+  free(gow);
+  free(god);
   return rc;
 }

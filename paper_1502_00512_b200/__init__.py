@@ -471,7 +471,9 @@ def rescore_nbest(utts: List[NBestUtt], model: GpuRnn, vocab_words: Sequence[str
 # ---------------------------------------------------------------- trainer
 @dataclass
 class TrainConfig:
-    """trainer.hpp:43-93 (mode: 1 = softmax; NCE (0) is not on this path)."""
+    """trainer.hpp:43-93.  mode: 0 = NCE (LossMode::kNce: k = nce_k noise
+    samples per position from the unigram NoiseModel, the reference's default),
+    1 = exact softmax (this mirror's default)."""
     nstate: int = 256
     nproj: int = 0
     noffset: int = 128
@@ -524,8 +526,8 @@ class TrainConfig:
             raise ValueError("config: init_range must be > 0")
         if self.threads < 1:
             raise ValueError("config: threads must be >= 1")
-        if self.mode != 1:
-            raise ValueError("config: only the exact-softmax loss runs on the B200 path")
+        if self.mode not in (0, 1):
+            raise ValueError("config: mode must be 0 (NCE) or 1 (softmax)")
         if self.nproj != 0:
             raise ValueError("config: bottleneck models are not on the B200 path")
 
@@ -595,6 +597,15 @@ class Trainer:
             self.model.set_vocab_shard(vocab_shard)
         self.model.set_params(w_in, w_rec, w_out)
         self.model.set_opt(None, None, None, cfg.rho, cfg.eps)
+        if cfg.mode == 0:
+            # NoiseModel::from_stream (nce.hpp:69-76; trainer.hpp:207-209):
+            # every non-bos token of the training stream; Trainer::rng_ is
+            # seeded with cfg.seed (trainer.hpp:184)
+            ids = self.train_ids
+            counts = np.bincount(ids[ids != BOS_ID], minlength=V).astype(np.float64)
+            self.model.set_loss_mode(0)
+            self.model.set_noise(counts, cfg.nce_k, cfg.noise_floor)
+            self.model.set_rng_state(rng_seed_state(cfg.seed))
         self.model.trainer_init(self.train_ids, cfg.noffset, cfg.minibatch, cfg.unroll,
                                 cfg.clip)
         self.logs: List[EpochLog] = []
@@ -653,9 +664,11 @@ class Trainer:
     # ---- checkpointing (RTRN, trainer.hpp:274-341)
     def save_checkpoint(self) -> bytes:
         cur, hid = self.model.trainer_state()
+        # the rng as `os << rng_` (trainer.hpp:284): it only advances in NCE mode
+        rng_text = " ".join(str(int(v)) for v in self.model.rng_state()) \
+            if self.cfg.mode == 0 else formats.mt19937_64_text(self.cfg.seed)
         return formats.write_trainer(self.cfg, self.epoch, self.eta, self.best_ppl,
-                                     self.bad_epochs, self.initial_ppl,
-                                     formats.mt19937_64_text(self.cfg.seed), cur, hid,
+                                     self.bad_epochs, self.initial_ppl, rng_text, cur, hid,
                                      self.model.params(), self.vocab, self.model.opt())
 
     def load_checkpoint(self, data: bytes):
@@ -672,3 +685,8 @@ class Trainer:
         self.model.set_params(*st["params"])
         self.model.set_opt(*st["opt"], cfg.rho, cfg.eps)
         self.model.trainer_set_state(st["cursors"], st["hidden"])
+        if cfg.mode == 0:
+            words = st["rng_text"].split()
+            if len(words) != 313:
+                raise DataError("trainer checkpoint: bad rng state")
+            self.model.set_rng_state(np.array([int(v) for v in words], np.uint64))

@@ -195,6 +195,7 @@ struct dl_ctx {
   uint32_t* g_out_words = nullptr;  // [Vo] words of the compact sparse rows
   int* g_out_n = nullptr;
   std::vector<uint32_t> h_rec;  // host staging: rec_word | rec_row | proc_r
+  std::vector<uint32_t> h_ids;  // trainer: host copy of the stream (NCE draws)
   void* nce_pin = nullptr;      // pinned copy of h_rec for the H2D
   size_t nce_pin_bytes = 0;
 
@@ -1664,6 +1665,9 @@ int dl_trainer_init(dl_ctx* c, const uint32_t* ids, int64_t L, int noffset, int 
     c->bos = bos;
     c->ids = dalloc<uint32_t>(L);
     DL_CUDA(cudaMemcpyAsync(c->ids, ids, L * 4, cudaMemcpyHostToDevice, c->st));
+    // NCE windows draw their noise on the host from the window's targets:
+    // the host keeps the stream too (any mode may be selected later)
+    c->h_ids.assign(ids, ids + L);
     const int64_t Nl = (int64_t)noffset * minibatch;
     c->cursors = dalloc<int64_t>(Nl);
     c->hidden = dalloc<float>(Nl * c->H);
@@ -1749,9 +1753,10 @@ void trainer_window(dl_ctx* c, double eta) {
   // the dense W_out update overlaps the dh GEMM when it cannot be rejected
   // (finite clip, see run_window), a second bf16 shadow exists and no
   // allreduce is pending
-  const bool fuse = fuse_ok(c, c->clip);
-  const bool late = !fuse && late_ok(c);
-  const bool fork = !fuse && !late && fork_ok(c);
+  const bool sm = c->loss_mode != 0;  // (the W_out update placements are softmax-only)
+  const bool fuse = sm && fuse_ok(c, c->clip);
+  const bool late = sm && !fuse && late_ok(c);
+  const bool fork = sm && !fuse && !late && fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0, fuse ? eta : 0.0,
              late ? eta : 0.0);
   run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork || fuse || late);
@@ -1772,9 +1777,42 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     DL_CUDA(cudaMemsetAsync(c->d_loss, 0, 8, c->st));
     DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
     DL_CUDA(cudaMemsetAsync(c->d_skipped, 0, 8, c->st));
-    const bool graphs = c->use_graph && !c->profiling && c->comm == nullptr;
+    const bool nce = c->loss_mode == 0;
+    DL_REQUIRE(!nce || c->comm == nullptr, 1, "NCE mode: multi-rank training is not supported");
+    const bool graphs = c->use_graph && !c->profiling && c->comm == nullptr && !nce;
     presize(c, c->unroll, c->minibatch);
-    if (graphs) {
+    if (nce) {
+      // the noise draws depend on the window's targets / mask, which the
+      // device builds from the resident stream: the host mirrors the same
+      // schedule (cursors, window counter; trainer.hpp:374-406) to draw
+      // them, window by window, in the reference's order
+      const int64_t B = c->minibatch, T = c->unroll, Nl = (int64_t)c->noffset * B;
+      std::vector<int64_t> cur(Nl);
+      DL_CUDA(cudaMemcpyAsync(cur.data(), c->cursors, Nl * 8, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      std::vector<uint32_t> y(T * B);
+      std::vector<uint8_t> w(T * B);
+      const int64_t L = c->L;
+      for (int64_t i = 0; i < count; ++i) {
+        const int64_t s0 = ((first + i) % c->noffset) * B;
+        for (int64_t t = 0; t < T; ++t)
+          for (int64_t b = 0; b < B; ++b) {
+            const int64_t pos = cur[s0 + b] + t;
+            y[t * B + b] = c->h_ids[(pos + 1) % L];
+            w[t * B + b] = y[t * B + b] == c->bos ? 0 : 1;
+          }
+        ensure_window(c, T, B);
+        nce_prepare(c, T, B, y.data(), w.data());
+        trainer_window(c, eta);
+        for (int64_t b = 0; b < B; ++b) {
+          int64_t v = cur[s0 + b] + T;
+          if (v >= L) v -= L;
+          cur[s0 + b] = v;
+        }
+        // (nce_prepare's next upload reuses the pinned records buffer)
+        DL_CUDA(cudaStreamSynchronize(c->st));
+      }
+    } else if (graphs) {
       // one graph per W_out-shadow parity (the forked update writes the
       // other shadow, so consecutive windows alternate between two graphs)
       const int nvar = !fuse_ok(c, c->clip) && !late_ok(c) && fork_ok(c) ? 2 : 1;

@@ -53,9 +53,10 @@ def test_errors_without_gpu_are_reported_not_crashes():
 def test_config_validation_mirrors_reference():
     from paper_1502_00512_b200 import TrainConfig
     TrainConfig(mode=1).validate()
+    TrainConfig(mode=0).validate()  # NCE (LossMode::kNce, the reference default)
     for bad in (dict(nstate=0), dict(noffset=0), dict(eta=0.0), dict(rho=1.0), dict(eps=0.0),
                 dict(clip=0.0), dict(max_epochs=0), dict(divergence_factor=1.0),
                 dict(valid_limit=-1), dict(valid_shards=0), dict(init_range=0.0),
-                dict(threads=0), dict(mode=0)):
+                dict(threads=0), dict(mode=2), dict(mode=0, nce_k=0)):
         with pytest.raises(ValueError):
             TrainConfig(**dict(dict(mode=1), **bad)).validate()

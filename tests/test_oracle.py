@@ -231,3 +231,25 @@ def test_nce_random_configs_vs_reference(orc, ref, seed):
     assert a["loss"] == b["loss"] and a["positions"] == b["positions"]
     for key in ("h_final", "g_in_dense", "g_rec", "g_out_words", "g_out_rows"):
         assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("k,floor,act,eta", [(7, 1e-3, 0, 0.05), (3, 1e-3, 1, 0.005)])
+def test_trainer_nce_vs_reference(orc, ref, k, floor, act, eta):
+    """Trainer<StandardTraits> in its default NCE mode (trainer.hpp:53,
+    207-209, 363-365): the oracle's epochs, final parameters, accumulators,
+    cursors and the rng state in the RTRN bytes equal the reference's."""
+    from paper_1502_00512_b200 import TrainConfig, formats
+    V, H, L = 40, 8, 600
+    tr, va = ref.random_stream_pair(77, V, L + 16, 150)
+    tr = tr[:L]
+    params = ref.init_uniform(V, H, 3)
+    kw = dict(nstate=H, noffset=2, minibatch=2, unroll=5, eta=eta, max_epochs=3, mode=0,
+              nce_k=k, noise_floor=floor, act=act, divergence_factor=1e9)
+    blob, logs, ini = ref.train(oracle.TrainConfig(**kw), params, tr, va)
+    r = orc.train(oracle.TrainConfig(**kw), params, tr, va)
+    assert ini == r["initial_ppl"]
+    assert np.array_equal(r["logs"][:, [0, 1, 2, 3, 6]], logs[:, [0, 1, 2, 3, 6]])
+    st = formats.read_trainer(blob, TrainConfig(**kw), 2 * 2, H, L)
+    assert np.array_equal(st["cursors"], r["cursors"])
+    for u, v in zip(st["params"] + st["opt"], r["params"] + r["opt"]):
+        assert np.array_equal(u, v)
