@@ -125,10 +125,11 @@ def synthetic_stream(seed: int, V: int, L: int) -> np.ndarray:
     return out[:L]
 
 
-def flops_per_word(V, H):
+def flops_per_word(V, H, nce_k=0):
     """6*H*V + 6*H^2: forward logits + recurrence, dS.W_out + dW_out, the
-    recurrent backward and dW_rec."""
-    return 6 * H * V + 6 * H * H
+    recurrent backward and dW_rec.  NCE: the output layer
+    touches k + 1 rows per word instead of V."""
+    return 6 * H * (nce_k + 1 if nce_k else V) + 6 * H * H
 
 
 class ClockSampler:
@@ -260,6 +261,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--loss", default="softmax", choices=["softmax", "nce"],
+                    help="output layer: exact softmax (the north-star path) or NCE "
+                         "(LossMode::kNce, the reference's default training mode)")
+    ap.add_argument("--nce-k", type=int, default=64)
     ap.add_argument("--dp-mode", default="vocab", choices=["vocab", "dense"],
                     help="N>1 data parallel: vocabulary-parallel output layer (default) or "
                          "the dense dW_out allreduce")
@@ -308,6 +313,11 @@ def main():
             model.set_vocab_shard("dp")
     model.set_params(*params)
     model.set_opt(None, None, None, 0.9995, 1e-6)
+    if args.loss == "nce":
+        counts = np.bincount(ids[ids != 1], minlength=V).astype(np.float64)
+        model.set_loss_mode(0)
+        model.set_noise(counts, args.nce_k, 1e-8)
+        model.set_rng_state(dl.rng_seed_state(1))
     model.trainer_init(ids, noffset, B, T, 1.0)
     eta = 1e-3
     stream = torch.cuda.ExternalStream(dl._lib.load().dl_cuda_stream(model.handle))
@@ -343,15 +353,16 @@ def main():
     # all ranks cooperate on the same B streams
     words = (1 if vshard else world) * B * T * args.steps
     value = words / (ms / 1000.0)
-    fpw = flops_per_word(V, H)
+    fpw = flops_per_word(V, H, args.nce_k if args.loss == "nce" else 0)
 
     # per-kernel device times (eager launches + CUDA events on the library
     # stream) -> roofline of the dominant kernel
     model.set_profiling(True)
     model.trainer_run(args.warmup + args.steps, args.profile_steps, eta)
     phases = {}
-    for name in ("recurrence_fwd", "logits", "softmax", "dh", "dw_out", "recurrence_bwd",
-                 "dw_rec", "embed_grad", "rmsprop", "rmsprop_out"):
+    for name in ("recurrence_fwd", "logits", "softmax", "dh", "dw_out", "nce_loss", "nce_dh",
+                 "recurrence_bwd", "dw_rec", "embed_grad", "nce_out_rows", "rmsprop",
+                 "rmsprop_out"):
         v = model.kernel_ms(name)
         if v >= 0:
             phases[name] = v
@@ -449,7 +460,9 @@ def main():
                "config": {"workload": args.config, "desc": cfg["desc"], "V": V, "H": H,
                           "T": T, "B_per_gpu": B,
                           "global_minibatch": B if vshard else B * world,
-                          "noffset": noffset, "L": L, "loss": "exact softmax",
+                          "noffset": noffset, "L": L,
+                          "loss": ("exact softmax" if args.loss == "softmax"
+                                   else f"NCE k={args.nce_k}"),
                           "optimizer": "rmsprop (per-word W_in/W_out scalars)",
                           "parallelism": (f"vocab{world}" if vshard else
                                           f"dp{world}+vocab-parallel-output"

@@ -28,6 +28,10 @@ struct NceRecs {
   size_t temp_bytes;
 };
 
+void nce_records(const uint8_t* w, const uint32_t* y, int64_t T, int64_t B, int64_t P, int K1,
+                 const unsigned long long* raw, const double* prob, const uint32_t* alias,
+                 int64_t V, uint32_t* pos_of, int* first, uint32_t* rec_word, uint32_t* rec_row,
+                 uint32_t* proc_r, cudaStream_t st);
 void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
                 const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st);
 void nce_loss(const float* score, const uint32_t* rec_word, const double* ln_kq, int64_t P,

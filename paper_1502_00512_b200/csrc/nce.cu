@@ -145,7 +145,97 @@ __global__ void k_nce_long(const int* __restrict__ seg_start, const int* __restr
   if (seg_start[s + 1] - seg_start[s] > short_max) long_list[atomicAdd(n_long, 1)] = s;
 }
 
+// Unmasked positions of the window in t-major order (one block): pos_of[p] =
+// t*B + b of the p-th, first[t] = index of row t's first one (first[T] = P).
+__global__ void k_nce_positions(const uint8_t* __restrict__ w, int64_t T, int64_t B,
+                                uint32_t* __restrict__ pos_of, int* __restrict__ first) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x % 32, wid = threadIdx.x / 32, nw = blockDim.x / 32;
+  const int64_t n = T * B;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int f = (i < n && w[i]) ? 1 : 0;
+    // block-wide exclusive scan of f
+    int x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane < nw) warp_tot[lane] = v;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - f;
+    if (i < n) {
+      if (i % B == 0) first[i / B] = excl;  // row t starts here
+      if (f) pos_of[excl] = (uint32_t)i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[nw - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) first[T] = carry;
+}
+
+// Records of the window from the raw mt19937_64 outputs (2 per draw, in
+// the reference's draw order): AliasSampler::sample (rng.hpp:91-94) with
+// uniform_index / uniform01 (rng.hpp:37-50) -- the same IEEE double
+// operations as the host, so the words are identical.
+__global__ void k_nce_records(const uint32_t* __restrict__ y, const uint32_t* __restrict__ pos_of,
+                              const int* __restrict__ first, int64_t B, int64_t P, int K1,
+                              const unsigned long long* __restrict__ raw,
+                              const double* __restrict__ prob, const uint32_t* __restrict__ alias,
+                              int64_t V, uint32_t* __restrict__ rec_word,
+                              uint32_t* __restrict__ rec_row, uint32_t* __restrict__ proc_r,
+                              int64_t T) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= P * K1) return;
+  const int64_t p = r / K1;
+  const int j = (int)(r % K1);
+  const uint32_t idx = pos_of[p];
+  uint32_t word;
+  if (j == 0) {
+    word = y[idx];
+  } else {
+    const int64_t d = p * (K1 - 1) + (j - 1);
+    const double u1 = (double)(raw[2 * d] >> 11) * 0x1.0p-53;
+    const uint64_t i = (uint64_t)(u1 * (double)V);
+    const double u2 = (double)(raw[2 * d + 1] >> 11) * 0x1.0p-53;
+    word = u2 < prob[i] ? (uint32_t)i : alias[i];
+  }
+  rec_word[r] = word;
+  rec_row[r] = idx;
+  // processing order: rows t descending, positions ascending, records ascending
+  const int64_t t = idx / B;
+  const int64_t q_pos = (P - first[t + 1]) + (p - first[t]);
+  proc_r[q_pos * K1 + j] = (uint32_t)r;
+  (void)T;
+}
+
 }  // namespace
+
+void nce_records(const uint8_t* w, const uint32_t* y, int64_t T, int64_t B, int64_t P, int K1,
+                 const unsigned long long* raw, const double* prob, const uint32_t* alias,
+                 int64_t V, uint32_t* pos_of, int* first, uint32_t* rec_word, uint32_t* rec_row,
+                 uint32_t* proc_r, cudaStream_t st) {
+  k_nce_positions<<<1, 1024, 0, st>>>(w, T, B, pos_of, first);
+  const int64_t N = P * K1;
+  if (N > 0)
+    k_nce_records<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+        y, pos_of, first, B, P, K1, raw, prob, alias, V, rec_word, rec_row, proc_r, T);
+}
 
 void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
                 const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st) {

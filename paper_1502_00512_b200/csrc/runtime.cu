@@ -9,7 +9,9 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -194,10 +196,18 @@ struct dl_ctx {
   EmbedWs nce_ws{};
   uint32_t* g_out_words = nullptr;  // [Vo] words of the compact sparse rows
   int* g_out_n = nullptr;
-  std::vector<uint32_t> h_rec;  // host staging: rec_word | rec_row | proc_r
+  double* nz_prob_d = nullptr;    // alias tables on the device (draws from raw outputs)
+  uint32_t* nz_alias_d = nullptr;
+  unsigned long long* raw_d = nullptr;  // [2 k P] raw mt19937_64 outputs of the window
+  uint32_t* pos_of_d = nullptr;   // [TB] unmasked positions in t-major order
+  int* first_d = nullptr;         // [T + 1]
+  int64_t raw_cap = 0;
+  void* raw_pin[2] = {nullptr, nullptr};  // double-buffered host staging of raw outputs
+  cudaEvent_t raw_ev[2] = {nullptr, nullptr};
+  int raw_slot = 0;
+  bool nce_pending = false;       // records of the prepared window not built yet
+  double nce_wait_s = 0.0, nce_gen_s = 0.0, nce_res_s = 0.0, nce_copy_s = 0.0;  // (DL_DEBUG)
   std::vector<uint32_t> h_ids;  // trainer: host copy of the stream (NCE draws)
-  void* nce_pin = nullptr;      // pinned copy of h_rec for the H2D
-  size_t nce_pin_bytes = 0;
 
   // profiling
   bool profiling = false;
@@ -542,19 +552,15 @@ void nce_build(dl_ctx* c, const double* counts, int64_t V, int k, double floor) 
   }
   for (uint32_t i : large) prob[i] = 1.0;
   for (uint32_t i : small) prob[i] = 1.0;
-  c->nz_prob = std::move(prob);
-  c->nz_alias = std::move(alias);
   c->nce_k = k;
   if (!c->ln_kq_d) c->ln_kq_d = dalloc<double>(V);
+  if (!c->nz_prob_d) c->nz_prob_d = dalloc<double>(V);
+  if (!c->nz_alias_d) c->nz_alias_d = dalloc<uint32_t>(V);
   DL_CUDA(cudaMemcpy(c->ln_kq_d, lnkq.data(), V * 8, cudaMemcpyHostToDevice));
-}
-
-// AliasSampler::sample with uniform_index / uniform01 (rng.hpp:37-50, 91-94)
-inline uint32_t nce_draw(dl_ctx* c) {
-  const double u1 = static_cast<double>(c->rng() >> 11) * 0x1.0p-53;
-  const uint64_t i = static_cast<uint64_t>(u1 * static_cast<double>(c->nz_prob.size()));
-  const double u2 = static_cast<double>(c->rng() >> 11) * 0x1.0p-53;
-  return u2 < c->nz_prob[i] ? static_cast<uint32_t>(i) : c->nz_alias[i];
+  DL_CUDA(cudaMemcpy(c->nz_prob_d, prob.data(), V * 8, cudaMemcpyHostToDevice));
+  DL_CUDA(cudaMemcpy(c->nz_alias_d, alias.data(), V * 4, cudaMemcpyHostToDevice));
+  c->nz_prob = std::move(prob);
+  c->nz_alias = std::move(alias);
 }
 
 void nce_reserve(dl_ctx* c, int64_t N) {
@@ -589,57 +595,58 @@ void nce_reserve(dl_ctx* c, int64_t N) {
 }
 
 // The window's noise draws (backprop.hpp:126-156 order: t, b, then sample;
-// masked positions draw nothing) and its records in forward and processing
-// order, uploaded on the context stream.  targets / weights: host arrays.
-void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint32_t* targets,
-                 const uint8_t* weights) {
+// masked positions draw nothing): the host advances the trainer's
+// mt19937_64 by exactly the reference's 2 outputs per draw and ships the raw
+// outputs; the device turns them into words with the alias tables and
+// builds the records (nce.cu k_nce_records) once the window's targets and
+// mask are on the device (run_window).  The staging is double-buffered so
+// the host can draw the next window while the device runs this one.
+void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
   DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
              "bptt: NCE mode needs noise model and rng (dl_set_noise)");
   const int K1 = c->nce_k + 1;
   int64_t P = 0;
   for (int64_t i = 0; i < T * B; ++i) P += weights[i] ? 1 : 0;
-  const int64_t N = P * K1;
-  nce_reserve(c, std::max<int64_t>(N, 1));
-  c->h_rec.resize(3 * std::max<int64_t>(N, 1));
-  uint32_t* word = c->h_rec.data();
-  uint32_t* row = word + N;
-  uint32_t* proc = row + N;
-  std::vector<int64_t> first(T + 1, 0);  // forward index of row t's first position
-  int64_t p = 0;
-  for (int64_t t = 0; t < T; ++t) {
-    first[t] = p;
-    for (int64_t b = 0; b < B; ++b) {
-      const int64_t idx = t * B + b;
-      if (!weights[idx]) continue;
-      const int64_t r0 = p * K1;
-      word[r0] = targets[idx];
-      for (int j = 1; j < K1; ++j) word[r0 + j] = nce_draw(c);
-      for (int j = 0; j < K1; ++j) row[r0 + j] = static_cast<uint32_t>(idx);
-      ++p;
+  const int64_t N = P * K1, ND = 2 * P * c->nce_k;  // raw outputs
+  const auto r0 = std::chrono::steady_clock::now();
+  // (for the window's maximum, every position unmasked: no reallocation --
+  // a device-synchronising cudaFree -- as the masked count varies)
+  nce_reserve(c, std::max<int64_t>(T * B * K1, 1));
+  c->nce_res_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - r0).count();
+  if (ND > c->raw_cap || !c->pos_of_d || c->capT * c->capB > c->raw_cap / 2) {
+    const int64_t cap = std::max<int64_t>({ND, 2 * c->capT * c->capB * c->nce_k, 2});
+    for (int i = 0; i < 2; ++i) {
+      if (c->raw_ev[i]) DL_CUDA(cudaEventSynchronize(c->raw_ev[i]));
+      if (c->raw_pin[i]) cudaFreeHost(c->raw_pin[i]);
+      DL_CUDA(cudaMallocHost(&c->raw_pin[i], cap * 8));
+      if (!c->raw_ev[i])
+        DL_CUDA(cudaEventCreateWithFlags(&c->raw_ev[i], cudaEventDisableTiming));
     }
+    if (c->raw_d) cudaFree(c->raw_d);
+    if (c->pos_of_d) cudaFree(c->pos_of_d);
+    if (c->first_d) cudaFree(c->first_d);
+    c->raw_d = dalloc<unsigned long long>(cap);
+    c->pos_of_d = dalloc<uint32_t>(std::max<int64_t>(c->capT * c->capB, T * B));
+    c->first_d = dalloc<int>(std::max(c->capT, T) + 1);
+    c->raw_cap = cap;
   }
-  first[T] = p;
-  // processing order: t descending, b ascending, record ascending
-  int64_t q = 0;
-  for (int64_t t = T - 1; t >= 0; --t)
-    for (int64_t pp = first[t]; pp < first[t + 1]; ++pp)
-      for (int j = 0; j < K1; ++j) proc[q++] = static_cast<uint32_t>(pp * K1 + j);
+  const int slot = c->raw_slot;
+  c->raw_slot ^= 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  DL_CUDA(cudaEventSynchronize(c->raw_ev[slot]));  // its previous upload is done
+  const auto t1 = std::chrono::steady_clock::now();
+  unsigned long long* raw = static_cast<unsigned long long*>(c->raw_pin[slot]);
+  for (int64_t i = 0; i < ND; ++i) raw[i] = c->rng();
+  const auto t2 = std::chrono::steady_clock::now();
+  c->nce_wait_s += std::chrono::duration<double>(t1 - t0).count();
+  c->nce_gen_s += std::chrono::duration<double>(t2 - t1).count();
+  if (ND > 0)
+    DL_CUDA(cudaMemcpyAsync(c->raw_d, raw, ND * 8, cudaMemcpyHostToDevice, c->st));
+  DL_CUDA(cudaEventRecord(c->raw_ev[slot], c->st));
+  c->nce_copy_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
   c->nce_P = P;
   c->nce_N = N;
-  if (N > 0) {
-    if (c->nce_pin_bytes < (size_t)(3 * N * 4)) {
-      if (c->nce_pin) cudaFreeHost(c->nce_pin);
-      DL_CUDA(cudaMallocHost(&c->nce_pin, 3 * N * 4));
-      c->nce_pin_bytes = 3 * N * 4;
-    }
-    uint32_t* pin = static_cast<uint32_t*>(c->nce_pin);
-    std::memcpy(pin, word, 3 * N * 4);
-    DL_CUDA(cudaMemcpyAsync(c->rec_word_d, pin, N * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->rec_row_d, pin + N, N * 4, cudaMemcpyHostToDevice, c->st));
-    DL_CUDA(cudaMemcpyAsync(c->proc_r_d, pin + 2 * N, N * 4, cudaMemcpyHostToDevice, c->st));
-    // (the staging buffer is reused by the next H2D only after this stream
-    // has consumed it: window_call synchronises every call)
-  }
+  c->nce_pending = true;
 }
 
 // One window with device-resident inputs (x_d, y_d, w_d, htape[0]).
@@ -719,6 +726,11 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // NCE loss over the window's records (backprop.hpp:126-156)
     Phase p(c, "nce_loss");
     const int K1 = c->nce_k + 1;
+    DL_REQUIRE(c->nce_pending, 1, "NCE window without prepared draws");
+    nce_records(c->w_d, c->y_d, T, B, c->nce_P, K1, c->raw_d, c->nz_prob_d, c->nz_alias_d, V,
+                c->pos_of_d, c->first_d, c->rec_word_d, c->rec_row_d, c->proc_r_d, st);
+    c->nce_pending = false;
+    c->launches += 2;
     nce_scores(Hs, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st);
     nce_loss(c->score_d, c->rec_word_d, c->ln_kq_d, c->nce_P, K1, scale, c->loss_pos_d, c->ds_d,
              st);
@@ -1222,6 +1234,7 @@ int dl_destroy(dl_ctx* c) {
                   c->nce_scale, c->loss_pos_d, c->sort_keys_in, c->sort_vals_in,
                   c->sort_keys_out, c->sort_vals_out, c->sort_head, c->sort_slot, c->sort_temp,
                   c->nce_ws.seg_start, c->nce_ws.order_pos, c->g_out_words, c->g_out_n,
+                  c->nz_prob_d, c->nz_alias_d, c->raw_d, c->pos_of_d, c->first_d,
                   c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1230,7 +1243,10 @@ int dl_destroy(dl_ctx* c) {
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
-  if (c->nce_pin) cudaFreeHost(c->nce_pin);
+  for (int i = 0; i < 2; ++i) {
+    if (c->raw_pin[i]) cudaFreeHost(c->raw_pin[i]);
+    if (c->raw_ev[i]) cudaEventDestroy(c->raw_ev[i]);
+  }
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->st2) cudaStreamDestroy(c->st2);
@@ -1316,7 +1332,7 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
     return fail(c, DL_EINVAL, "NCE mode: multi-rank windows are not supported");
   return guarded(c, [&] {
     ensure_window(c, T, B);
-    if (c->loss_mode == 0) nce_prepare(c, T, B, targets, weights);
+    if (c->loss_mode == 0) nce_prepare(c, T, B, weights);
     const int64_t TB = T * B, BH = B * c->H;
     // H2D of the window: page-locked caller buffers are copied from directly,
     // pageable ones through one pinned staging buffer
@@ -1793,6 +1809,8 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
       std::vector<uint32_t> y(T * B);
       std::vector<uint8_t> w(T * B);
       const int64_t L = c->L;
+      double host_draw_s = 0.0, host_enqueue_s = 0.0;
+      const auto run0 = std::chrono::steady_clock::now();
       for (int64_t i = 0; i < count; ++i) {
         const int64_t s0 = ((first + i) % c->noffset) * B;
         for (int64_t t = 0; t < T; ++t)
@@ -1802,16 +1820,29 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
             w[t * B + b] = y[t * B + b] == c->bos ? 0 : 1;
           }
         ensure_window(c, T, B);
-        nce_prepare(c, T, B, y.data(), w.data());
+        const auto h0 = std::chrono::steady_clock::now();
+        nce_prepare(c, T, B, w.data());
+        const auto h1 = std::chrono::steady_clock::now();
         trainer_window(c, eta);
+        const auto h2 = std::chrono::steady_clock::now();
+        host_draw_s += std::chrono::duration<double>(h1 - h0).count();
+        host_enqueue_s += std::chrono::duration<double>(h2 - h1).count();
         for (int64_t b = 0; b < B; ++b) {
           int64_t v = cur[s0 + b] + T;
           if (v >= L) v -= L;
           cur[s0 + b] = v;
         }
-        // (nce_prepare's next upload reuses the pinned records buffer)
-        DL_CUDA(cudaStreamSynchronize(c->st));
       }
+      if (std::getenv("DL_DEBUG"))
+        fprintf(stderr, "[desklm] NCE trainer: %lld windows, host draws %.3f ms/window, "
+                "enqueue %.3f ms/window, wall %.3f ms/window (slot wait %.3f, rng %.3f, reserve "
+                "%.3f, copy %.3f ms total)\n",
+                (long long)count,
+                1e3 * host_draw_s / std::max<int64_t>(count, 1),
+                1e3 * host_enqueue_s / std::max<int64_t>(count, 1),
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - run0)
+                          .count() / std::max<int64_t>(count, 1),
+                1e3 * c->nce_wait_s, 1e3 * c->nce_gen_s, 1e3 * c->nce_res_s, 1e3 * c->nce_copy_s);
     } else if (graphs) {
       // one graph per W_out-shadow parity (the forked update writes the
       // other shadow, so consecutive windows alternate between two graphs)
