@@ -235,6 +235,77 @@ class _Backend:
         return dict(total_logprob=tl.value, predicted=pr.value, perplexity=ppl.value)
 
 
+    # ---- bottleneck model (compress.hpp:38-415)
+    def _bn_fn(self, name, argtypes):
+        f = getattr(self.lib, self.prefix + name)
+        f.argtypes = argtypes
+        return f
+
+    def bn_init_uniform(self, V, H, P, seed, rng=0.1):
+        e = np.empty((V, P), np.float32)
+        u = np.empty((P, H), np.float32)
+        w_rec = np.empty((H, H), np.float32)
+        d = np.empty((H, P), np.float32)
+        f = self._bn_fn("bn_init_uniform", [_i64, _i64, _i64, _u64, C.c_double, _f32p, _f32p,
+                                             _f32p, _f32p])
+        self._check(f(V, H, P, seed, rng, e, u, w_rec, d))
+        return e, u, w_rec, d
+
+    def bn_bptt(self, params, act, inputs, targets, weights, h0, loss_scale=1.0,
+                clip=3.4028234663852886e38, compute_grads=True):
+        """bptt_run over BottleneckAdapter, softmax mode.  Returns dict(loss,
+        positions, h_final, g_e (dense V x P), g_u, g_rec, g_d)."""
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        T, B = inputs.shape
+        hf = np.empty((B, H), np.float32)
+        g = [np.zeros(s, np.float32) for s in ((V, P), (P, H), (H, H), (H, P))]
+        loss, pos = C.c_double(), C.c_uint64()
+        f = self._bn_fn("bn_bptt", [_i64, _i64, _i64, C.c_int, _f32p, _f32p, _f32p, _f32p,
+                                    _i64, _i64, _u32p, _u32p, _u8p, _f32p, C.c_double,
+                                    C.c_float, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_uint64)])
+        self._check(f(V, H, P, act, e, u, w_rec, d, T, B,
+                      np.ascontiguousarray(inputs, np.uint32),
+                      np.ascontiguousarray(targets, np.uint32),
+                      np.ascontiguousarray(weights, np.uint8),
+                      np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                      int(compute_grads), hf.ctypes.data, *(x.ctypes.data for x in g),
+                      C.byref(loss), C.byref(pos)))
+        r = dict(loss=loss.value, positions=pos.value, h_final=hf)
+        if compute_grads:
+            r.update(g_e=g[0], g_u=g[1], g_rec=g[2], g_d=g[3])
+        return r
+
+    def bn_update(self, params, state, grads, rho, eps, eta):
+        """bottleneck_update on copies; state = (m_e, m_u, m_rec, m_d)."""
+        p = [np.array(x, np.float32, copy=True) for x in params]
+        m = [np.array(x, np.float32, copy=True) for x in state]
+        V, P = p[0].shape
+        H = p[2].shape[0]
+        applied = C.c_int()
+        f = self._bn_fn("bn_update", [_i64, _i64, _i64] + [_f32p] * 8 +
+                        [C.c_double] * 3 + [_f32p] * 4 + [C.POINTER(C.c_int)])
+        gs = [np.ascontiguousarray(grads[k], np.float32) for k in ("g_e", "g_u", "g_rec", "g_d")]
+        self._check(f(V, H, P, *p, *m, rho, eps, eta, *gs, C.byref(applied)))
+        return tuple(p), tuple(m), bool(applied.value)
+
+    def bn_sharded_ppl(self, params, act, ids, shards, bos=1):
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        tl, pr, ppl = C.c_double(), C.c_uint64(), C.c_double()
+        ids = np.ascontiguousarray(ids, np.uint32)
+        f = self._bn_fn("bn_sharded_ppl", [_i64, _i64, _i64, C.c_int, _f32p, _f32p, _f32p,
+                                           _f32p, _u32p, _i64, C.c_int, C.c_uint32,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_double)])
+        self._check(f(V, H, P, act, e, u, w_rec, d, ids, len(ids), shards, bos,
+                      C.byref(tl), C.byref(pr), C.byref(ppl)))
+        return dict(total_logprob=tl.value, predicted=pr.value, perplexity=ppl.value)
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, msg=""):
         super().__init__(f"oracle status {code}: {msg}")
@@ -404,6 +475,24 @@ class Ref(_Backend):
         self._rescore.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p,
                                   C.c_char_p, C.c_double, C.c_double, C.c_int, _vp,
                                   _u64, C.POINTER(C.c_uint64)]
+
+    def bn_write(self, params, state, rho, eps, act=0):
+        """write_bottleneck (RNBL, vocabulary make_vocab(V)) and
+        write_bottleneck_opt (RBOP) bytes."""
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        f = self.lib.ref_bn_write
+        f.argtypes = [_i64, _i64, _i64, C.c_int] + [_f32p] * 4 + [C.c_double] * 2 + \
+            [_f32p] * 4 + [_vp, _u64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        cap = 4 * (2 * V * P + 2 * P * H + 2 * H * H + 2 * H * P + V) + 32 * V + 4096
+        buf = np.zeros(cap, np.uint8)
+        lp, ln = C.c_uint64(), C.c_uint64()
+        m = [np.ascontiguousarray(x, np.float32) for x in state]
+        self._check(f(V, H, P, act, e, u, w_rec, d, rho, eps, *m, buf.ctypes.data, cap,
+                      C.byref(lp), C.byref(ln)))
+        b = bytes(buf[: ln.value])
+        return b[: lp.value], b[lp.value:]
 
     def sharded_logprobs(self, params, act, ids, shards, bos=1):
         w_in, w_rec, w_out = params

@@ -937,3 +937,241 @@ done:
   free(god);
   return rc;
 }
+
+/* ------------------------------------------------------- bottleneck model */
+/* Tied-embedding bottleneck model (compress.hpp:38-415):
+ *   pre = float(h . W_rec^T); pre = float(double(pre) + E[x] . U);
+ *   h' = act(pre); z = float(h' . D); s_w = float(E[w] . z).
+ * E is V x P, U is P x H, W_rec is H x H, D is H x P (row-major). */
+
+/* BottleneckParams::init_uniform (compress.hpp:78-82): e, u, w_rec, d. */
+int orc_bn_init_uniform(int64_t V, int64_t H, int64_t P, uint64_t seed, double range,
+                        float* e, float* u, float* w_rec, float* d) {
+  if (V < 1 || H < 1 || P < 1 || P > H) return 1;
+  orc_mt64 m;
+  orc_mt_seed(&m, seed);
+  for (int64_t i = 0; i < V * P; ++i) e[i] = (float)uniform(&m, -range, range);
+  for (int64_t i = 0; i < P * H; ++i) u[i] = (float)uniform(&m, -range, range);
+  for (int64_t i = 0; i < H * H; ++i) w_rec[i] = (float)uniform(&m, -range, range);
+  for (int64_t i = 0; i < H * P; ++i) d[i] = (float)uniform(&m, -range, range);
+  return 0;
+}
+
+/* BottleneckAdapter::input_forward (compress.hpp:170-174): gathered rows
+ * then matmul_nn accumulate into pre. */
+static void bn_input_forward(const float* e, const float* u, int64_t H, int64_t P,
+                             const uint32_t* words, int64_t B, float* eb, float* pre,
+                             double* acc) {
+  for (int64_t b = 0; b < B; ++b) memcpy(eb + b * P, e + (int64_t)words[b] * P, sizeof(float) * P);
+  matmul_nn(eb, u, pre, B, H, P, 1, acc);
+}
+
+/* Softmax-mode window, bptt_run (backprop.hpp:76-222) over the bottleneck
+ * adapter (compress.hpp:121-244): dense embedding gradient g_e [V x P]
+ * (output side matmul_tn_add, input side row adds), g_u [P x H],
+ * g_rec [H x H], g_d [H x P]; clipped at the end (compress.hpp:96-104). */
+int orc_bn_bptt(int64_t V, int64_t H, int64_t P, int act, const float* e, const float* u,
+                const float* w_rec, const float* d, int64_t T, int64_t B,
+                const uint32_t* inputs, const uint32_t* targets, const uint8_t* weights,
+                const float* h0, double loss_scale, float clip, int compute_grads,
+                float* h_final, float* g_e, float* g_u, float* g_rec, float* g_d,
+                double* loss, uint64_t* positions) {
+  if (T < 1 || B < 1 || P < 1 || P > H) return 1;
+  const int64_t BH = B * H, BP = B * P;
+  const int64_t W = V > H ? V : H;
+  float* h = (float*)malloc(sizeof(float) * (T + 1) * BH);
+  float* z = (float*)malloc(sizeof(float) * T * BP);
+  float* pre = (float*)malloc(sizeof(float) * BH);
+  float* eb = (float*)malloc(sizeof(float) * BP);
+  float* scores = (float*)malloc(sizeof(float) * B * V);
+  double* acc = (double*)malloc(sizeof(double) * W);
+  float* dsc = compute_grads ? (float*)calloc((size_t)(T * B * V), sizeof(float)) : NULL;
+  memcpy(h, h0, sizeof(float) * BH);
+  /* forward: bptt_run loop + out_begin (compress.hpp:195-202) */
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(h + t * BH, w_rec, pre, B, H, H);
+    bn_input_forward(e, u, H, P, inputs + t * B, B, eb, pre, acc);
+    for (int64_t i = 0; i < BH; ++i) h[(t + 1) * BH + i] = act_f(act, pre[i]);
+    matmul_nn(h + (t + 1) * BH, d, z + t * BP, B, P, H, 0, acc);
+  }
+  if (h_final) memcpy(h_final, h + T * BH, sizeof(float) * BH);
+  /* softmax loss: softmax_scores = z . E^T (compress.hpp:227-230) */
+  double L = 0.0;
+  uint64_t pos = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(z + t * BP, e, scores, B, V, P);
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t idx = t * B + b;
+      if (!weights[idx]) continue;
+      ++pos;
+      const float* s = scores + b * V;
+      double mx = (double)s[0];
+      for (int64_t w = 1; w < V; ++w) mx = (mx < (double)s[w]) ? (double)s[w] : mx;
+      double zz = 0.0;
+      for (int64_t w = 0; w < V; ++w) zz += exp((double)s[w] - mx);
+      const double lse = mx + log(zz);
+      const uint32_t y = targets[idx];
+      L += loss_scale * (lse - (double)s[y]);
+      if (compute_grads) {
+        float* dd = dsc + idx * V;
+        for (int64_t w = 0; w < V; ++w) dd[w] = (float)(loss_scale * exp((double)s[w] - lse));
+        dd[y] -= (float)loss_scale;
+      }
+    }
+  }
+  *loss = L;
+  *positions = pos;
+  if (compute_grads) {
+    float* dh = (float*)calloc((size_t)BH, sizeof(float));
+    float* dpre = (float*)malloc(sizeof(float) * BH);
+    float* dz = (float*)malloc(sizeof(float) * BP);
+    float* din = (float*)malloc(sizeof(float) * BP);
+    memset(g_e, 0, sizeof(float) * V * P);
+    memset(g_u, 0, sizeof(float) * P * H);
+    memset(g_rec, 0, sizeof(float) * H * H);
+    memset(g_d, 0, sizeof(float) * H * P);
+    for (int64_t t = T - 1; t >= 0; --t) {
+      const float* dst = dsc + t * B * V;
+      const float* ht1 = h + (t + 1) * BH;
+      const float* zt = z + t * BP;
+      /* softmax_backward (compress.hpp:237-243) */
+      matmul_nn(dst, e, dz, B, P, V, 0, acc);
+      matmul_tn_add(dst, zt, g_e, B, V, P);
+      /* out_end (compress.hpp:221-225): dh += dz . D^T (double, one rounding) */
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < H; ++i)
+          dh[b * H + i] = (float)((double)dh[b * H + i] + dot_acc(dz + b * P, d + i * P, P));
+      matmul_tn_add(ht1, dz, g_d, B, H, P);
+      for (int64_t i = 0; i < BH; ++i) dpre[i] = dh[i] * act_deriv_f(act, ht1[i]);
+      matmul_tn_add(dpre, h + t * BH, g_rec, B, H, H);
+      /* input_backward (compress.hpp:176-193) */
+      const uint32_t* words = inputs + t * B;
+      for (int64_t b = 0; b < B; ++b)
+        memcpy(eb + b * P, e + (int64_t)words[b] * P, sizeof(float) * P);
+      matmul_tn_add(eb, dpre, g_u, B, P, H);
+      matmul_nt(dpre, u, din, B, P, H);
+      for (int64_t b = 0; b < B; ++b) {
+        float* dstrow = g_e + (int64_t)words[b] * P;
+        for (int64_t k = 0; k < P; ++k) dstrow[k] += din[b * P + k];
+      }
+      if (t > 0) matmul_nn(dpre, w_rec, dh, B, H, H, 0, acc);
+    }
+    for (int64_t i = 0; i < V * P; ++i) g_e[i] = clip1(g_e[i], clip);
+    for (int64_t i = 0; i < P * H; ++i) g_u[i] = clip1(g_u[i], clip);
+    for (int64_t i = 0; i < H * H; ++i) g_rec[i] = clip1(g_rec[i], clip);
+    for (int64_t i = 0; i < H * P; ++i) g_d[i] = clip1(g_d[i], clip);
+    free(dh);
+    free(dpre);
+    free(dz);
+    free(din);
+  }
+  free(h);
+  free(z);
+  free(pre);
+  free(eb);
+  free(scores);
+  free(acc);
+  free(dsc);
+  return 0;
+}
+
+/* rms_dense_elem (compress.hpp:282-292) */
+static void rms_elem(float* w, const float* g, float* m, int64_t n, double rho, double eps,
+                     double eta) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double gi = (double)g[i];
+    m[i] = (float)(rho * (double)m[i] + (1.0 - rho) * gi * gi);
+    w[i] -= (float)(eta * gi / sqrt((double)m[i] + eps));
+  }
+}
+
+/* bottleneck_update, dense embedding gradient (compress.hpp:296-309). */
+int orc_bn_update(int64_t V, int64_t H, int64_t P, float* e, float* u, float* w_rec, float* d,
+                  float* m_e, float* m_u, float* m_rec, float* m_d, double rho, double eps,
+                  double eta, const float* g_e, const float* g_u, const float* g_rec,
+                  const float* g_d, int* applied) {
+  if (!(all_finite(g_e, V * P) && all_finite(g_u, P * H) && all_finite(g_rec, H * H) &&
+        all_finite(g_d, H * P))) {
+    *applied = 0;
+    return 0;
+  }
+  update_rows_dense(e, V, P, g_e, m_e, rho, eps, eta);
+  rms_elem(u, g_u, m_u, P * H, rho, eps, eta);
+  rms_elem(w_rec, g_rec, m_rec, H * H, rho, eps, eta);
+  rms_elem(d, g_d, m_d, H * P, rho, eps, eta);
+  *applied = 1;
+  return 0;
+}
+
+/* sharded_perplexity (eval.hpp:151-222) over the bottleneck adapter:
+ * scores_t = E . z (compress.hpp:232-235). */
+int orc_bn_sharded_ppl(int64_t V, int64_t H, int64_t P, int act, const float* e,
+                       const float* u, const float* w_rec, const float* d,
+                       const uint32_t* ids, int64_t n, int shards, uint32_t bos,
+                       double* total_logprob, uint64_t* predicted, double* ppl) {
+  if (n < 2 || shards < 1) return 1;
+  const int64_t S = shards < n / 2 ? shards : n / 2;
+  int64_t max_len = 0;
+  for (int64_t s = 0; s < S; ++s) {
+    const int64_t len = (s + 1) * n / S - s * n / S;
+    if (len > max_len) max_len = len;
+  }
+  const float a0 = act_f(act, 0.0f);
+  const int64_t W = V > H ? V : H;
+  float* h = (float*)malloc(sizeof(float) * S * H);
+  float* pre = (float*)malloc(sizeof(float) * S * H);
+  float* eb = (float*)malloc(sizeof(float) * S * P);
+  float* z = (float*)malloc(sizeof(float) * S * P);
+  float* sc = (float*)malloc(sizeof(float) * V);
+  double* acc = (double*)malloc(sizeof(double) * W);
+  uint32_t* in = (uint32_t*)malloc(sizeof(uint32_t) * S);
+  int64_t* tgt = (int64_t*)malloc(sizeof(int64_t) * S);
+  for (int64_t i = 0; i < S * H; ++i) h[i] = a0;
+  double total = 0.0;
+  uint64_t pred = 0;
+  int rc = 0;
+  for (int64_t j = 0; j + 1 < max_len; ++j) {
+    int any = 0;
+    for (int64_t s = 0; s < S; ++s) {
+      const int64_t b0 = s * n / S, len = (s + 1) * n / S - b0;
+      if (j + 1 < len) {
+        const uint32_t x = ids[b0 + j], y = ids[b0 + j + 1];
+        if (x >= (uint64_t)V || y >= (uint64_t)V) {
+          rc = 2;
+          goto done;
+        }
+        in[s] = x;
+        tgt[s] = (y == bos) ? -1 : (int64_t)y;
+      } else {
+        in[s] = 0;
+        tgt[s] = -1;
+      }
+      any = any || tgt[s] >= 0;
+    }
+    matmul_nt(h, w_rec, pre, S, H, H);
+    bn_input_forward(e, u, H, P, in, S, eb, pre, acc);
+    for (int64_t i = 0; i < S * H; ++i) h[i] = act_f(act, pre[i]);
+    if (!any) continue;
+    matmul_nn(h, d, z, S, P, H, 0, acc);
+    for (int64_t s = 0; s < S; ++s) {
+      if (tgt[s] < 0) continue;
+      for (int64_t w = 0; w < V; ++w) sc[w] = (float)dot_acc(e + w * P, z + s * P, P);
+      total += (double)sc[tgt[s]] - lse_vec(sc, V);
+      ++pred;
+    }
+  }
+  *total_logprob = total;
+  *predicted = pred;
+  if (pred == 0) rc = 1;
+  else *ppl = exp(-total / (double)pred);
+done:
+  free(h);
+  free(pre);
+  free(eb);
+  free(z);
+  free(sc);
+  free(acc);
+  free(in);
+  free(tgt);
+  return rc;
+}

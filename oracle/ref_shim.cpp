@@ -521,4 +521,144 @@ int ref_rescore(std::int64_t V, std::int64_t H, int act, const float* w_in,
   });
 }
 
+// ----- bottleneck model (compress.hpp) -----
+//   ref_bn_init_uniform   -> BottleneckParams<float>::init_uniform  compress.hpp:78-82
+//   ref_bn_bptt           -> bptt_run(BottleneckAdapter<float>)     backprop.hpp:76-222
+//   ref_bn_update         -> bottleneck_update                      compress.hpp:296-309
+//   ref_bn_sharded_ppl    -> sharded_perplexity(BottleneckAdapter)  eval.hpp:151-222
+//   ref_bn_write          -> write_bottleneck + write_bottleneck_opt compress.hpp:315-368
+
+static BottleneckParams<float> make_bn(std::int64_t V, std::int64_t H, std::int64_t P, int act,
+                                       const float* e, const float* u, const float* w_rec,
+                                       const float* d) {
+  BottleneckParams<float> p(V, H, P, static_cast<Activation>(act));
+  std::memcpy(p.e.a.data(), e, sizeof(float) * V * P);
+  std::memcpy(p.u.a.data(), u, sizeof(float) * P * H);
+  std::memcpy(p.w_rec.a.data(), w_rec, sizeof(float) * H * H);
+  std::memcpy(p.d.a.data(), d, sizeof(float) * H * P);
+  return p;
+}
+
+int ref_bn_init_uniform(std::int64_t V, std::int64_t H, std::int64_t P, std::uint64_t seed,
+                        double range, float* e, float* u, float* w_rec, float* d) {
+  return guarded([&] {
+    BottleneckParams<float> p(V, H, P);
+    p.init_uniform(seed, range);
+    std::memcpy(e, p.e.a.data(), sizeof(float) * V * P);
+    std::memcpy(u, p.u.a.data(), sizeof(float) * P * H);
+    std::memcpy(w_rec, p.w_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(d, p.d.a.data(), sizeof(float) * H * P);
+  });
+}
+
+int ref_bn_bptt(std::int64_t V, std::int64_t H, std::int64_t P, int act, const float* e,
+                const float* u, const float* w_rec, const float* d, std::int64_t T,
+                std::int64_t B, const std::uint32_t* inputs, const std::uint32_t* targets,
+                const std::uint8_t* weights, const float* h0, double loss_scale, float clip,
+                int compute_grads, float* h_final, float* g_e, float* g_u, float* g_rec,
+                float* g_d, double* loss, std::uint64_t* positions) {
+  return guarded([&] {
+    const BottleneckParams<float> p = make_bn(V, H, P, act, e, u, w_rec, d);
+    WindowBatch wb;
+    wb.resize(T, B);
+    std::memcpy(wb.inputs.data(), inputs, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.targets.data(), targets, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.weights.data(), weights, T * B);
+    Mat<float> h0m(B, H);
+    std::memcpy(h0m.a.data(), h0, sizeof(float) * B * H);
+    BottleneckAdapter<float> a(p);
+    BpttOptions<float> opt;
+    opt.mode = LossMode::kSoftmax;
+    opt.loss_scale = loss_scale;
+    opt.clip = clip;
+    opt.compute_grads = compute_grads != 0;
+    BottleneckGrads<float> g;
+    Mat<float> hf;
+    const BpttResult res = bptt_run(a, wb, h0m, compute_grads ? &g : nullptr,
+                                    h_final ? &hf : nullptr, opt);
+    *loss = res.loss;
+    *positions = res.positions;
+    if (h_final) std::memcpy(h_final, hf.a.data(), sizeof(float) * B * H);
+    if (compute_grads) {
+      std::memcpy(g_e, g.e_dense.a.data(), sizeof(float) * V * P);
+      std::memcpy(g_u, g.u.a.data(), sizeof(float) * P * H);
+      std::memcpy(g_rec, g.w_rec.a.data(), sizeof(float) * H * H);
+      std::memcpy(g_d, g.d.a.data(), sizeof(float) * H * P);
+    }
+  });
+}
+
+int ref_bn_update(std::int64_t V, std::int64_t H, std::int64_t P, float* e, float* u,
+                  float* w_rec, float* d, float* m_e, float* m_u, float* m_rec, float* m_d,
+                  double rho, double eps, double eta, const float* g_e, const float* g_u,
+                  const float* g_rec, const float* g_d, int* applied) {
+  return guarded([&] {
+    BottleneckParams<float> p = make_bn(V, H, P, 0, e, u, w_rec, d);
+    BottleneckOptState s(V, H, P, rho, eps);
+    std::memcpy(s.m_e.data(), m_e, sizeof(float) * V);
+    std::memcpy(s.m_u.a.data(), m_u, sizeof(float) * P * H);
+    std::memcpy(s.m_rec.a.data(), m_rec, sizeof(float) * H * H);
+    std::memcpy(s.m_d.a.data(), m_d, sizeof(float) * H * P);
+    BottleneckGrads<float> g;
+    g.e_is_dense = true;
+    g.e_dense = Mat<float>(V, P);
+    g.u = Mat<float>(P, H);
+    g.w_rec = Mat<float>(H, H);
+    g.d = Mat<float>(H, P);
+    std::memcpy(g.e_dense.a.data(), g_e, sizeof(float) * V * P);
+    std::memcpy(g.u.a.data(), g_u, sizeof(float) * P * H);
+    std::memcpy(g.w_rec.a.data(), g_rec, sizeof(float) * H * H);
+    std::memcpy(g.d.a.data(), g_d, sizeof(float) * H * P);
+    *applied = bottleneck_update(p, g, s, eta) ? 1 : 0;
+    std::memcpy(e, p.e.a.data(), sizeof(float) * V * P);
+    std::memcpy(u, p.u.a.data(), sizeof(float) * P * H);
+    std::memcpy(w_rec, p.w_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(d, p.d.a.data(), sizeof(float) * H * P);
+    std::memcpy(m_e, s.m_e.data(), sizeof(float) * V);
+    std::memcpy(m_u, s.m_u.a.data(), sizeof(float) * P * H);
+    std::memcpy(m_rec, s.m_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(m_d, s.m_d.a.data(), sizeof(float) * H * P);
+  });
+}
+
+int ref_bn_sharded_ppl(std::int64_t V, std::int64_t H, std::int64_t P, int act, const float* e,
+                       const float* u, const float* w_rec, const float* d,
+                       const std::uint32_t* ids, std::int64_t n, int shards, std::uint32_t bos,
+                       double* total_logprob, std::uint64_t* predicted, double* ppl) {
+  return guarded([&] {
+    const BottleneckParams<float> p = make_bn(V, H, P, act, e, u, w_rec, d);
+    IdStream st;
+    st.ids.assign(ids, ids + n);
+    BottleneckAdapter<float> a(p);
+    const PerplexityResult r = sharded_perplexity(a, st, shards, bos);
+    *total_logprob = r.total_logprob;
+    *predicted = r.predicted;
+    *ppl = r.perplexity;
+  });
+}
+
+// RNBL (params + vocabulary "w<i>") followed by RBOP, as two byte strings
+// concatenated: *len_params gives the split.
+int ref_bn_write(std::int64_t V, std::int64_t H, std::int64_t P, int act, const float* e,
+                 const float* u, const float* w_rec, const float* d, double rho, double eps,
+                 const float* m_e, const float* m_u, const float* m_rec, const float* m_d,
+                 std::uint8_t* buf, std::uint64_t cap, std::uint64_t* len_params,
+                 std::uint64_t* len) {
+  return guarded([&] {
+    const BottleneckParams<float> p = make_bn(V, H, P, act, e, u, w_rec, d);
+    std::ostringstream os(std::ios::binary);
+    write_bottleneck(os, p, testutil::make_vocab(V));
+    *len_params = os.str().size();
+    BottleneckOptState s(V, H, P, rho, eps);
+    std::memcpy(s.m_e.data(), m_e, sizeof(float) * V);
+    std::memcpy(s.m_u.a.data(), m_u, sizeof(float) * P * H);
+    std::memcpy(s.m_rec.a.data(), m_rec, sizeof(float) * H * H);
+    std::memcpy(s.m_d.a.data(), m_d, sizeof(float) * H * P);
+    write_bottleneck_opt(os, s);
+    const std::string b = os.str();
+    *len = b.size();
+    if (b.size() <= cap) std::memcpy(buf, b.data(), b.size());
+  });
+}
+
 }  // extern "C"

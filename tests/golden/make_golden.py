@@ -69,6 +69,40 @@ def write_nce(ref, out):
         np.savez_compressed(os.path.join(out, f"nce_{i}.npz"), **nce_case(ref, *args))
 
 
+def bn_case(ref, V, H, P, T, B, act, mask, clip, seed):
+    """Bottleneck model (compress.hpp): a softmax window, bottleneck_update,
+    sharded_perplexity and the RNBL / RBOP bytes."""
+    rng = np.random.default_rng(seed)
+    params = ref.bn_init_uniform(V, H, P, seed + 1)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) >= mask).astype(np.uint8)
+    h0 = rng.uniform(-0.5, 0.5, (B, H)).astype(np.float32)
+    r = ref.bn_bptt(params, act, x, y, w, h0, 1.0 / (T * B), clip)
+    state = (rng.uniform(0, 0.01, V).astype(np.float32),
+             rng.uniform(0, 0.01, (P, H)).astype(np.float32),
+             rng.uniform(0, 0.01, (H, H)).astype(np.float32),
+             rng.uniform(0, 0.01, (H, P)).astype(np.float32))
+    p2, s2, applied = ref.bn_update(params, state, r, 0.9995, 1e-6, 0.05)
+    ids = ref.random_stream(seed + 2, V, 40 * T * B)
+    sp = ref.bn_sharded_ppl(params, act, ids, 8)
+    rnbl, rbop = ref.bn_write(params, state, 0.9995, 1e-6, act)
+    return dict(V=V, H=H, P=P, T=T, B=B, act=act, clip=clip, e=params[0], u=params[1],
+                w_rec=params[2], d=params[3], x=x, y=y, w=w, h0=h0, loss=r["loss"],
+                positions=r["positions"], h_final=r["h_final"], g_e=r["g_e"], g_u=r["g_u"],
+                g_rec=r["g_rec"], g_d=r["g_d"], m_e=state[0], m_u=state[1], m_rec=state[2],
+                m_d=state[3], u_e=p2[0], u_u=p2[1], u_w_rec=p2[2], u_d=p2[3], u_m_e=s2[0],
+                u_m_u=s2[1], u_m_rec=s2[2], u_m_d=s2[3], applied=applied, ids=ids,
+                sharded=np.array([sp["total_logprob"], sp["predicted"], sp["perplexity"]]),
+                rnbl=np.frombuffer(rnbl, np.uint8), rbop=np.frombuffer(rbop, np.uint8))
+
+
+def write_bn(ref, out):
+    for i, args in enumerate([(60, 16, 8, 5, 4, 0, 0.15, 1.0, 401),
+                              (300, 32, 16, 6, 8, 1, 0.1, 0.05, 433)]):
+        np.savez_compressed(os.path.join(out, f"bn_{i}.npz"), **bn_case(ref, *args))
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -108,6 +142,7 @@ def main():
                         stream_1001=ref.random_stream(1001, 10000, 200)[:200],
                         init_11=np.concatenate([a.ravel()[:16] for a in ref.init_uniform(7, 5, 11)]))
     write_nce(ref, out)
+    write_bn(ref, out)
     print("golden fixtures written to", out)
 
 

@@ -253,3 +253,55 @@ def test_trainer_nce_vs_reference(orc, ref, k, floor, act, eta):
     assert np.array_equal(st["cursors"], r["cursors"])
     for u, v in zip(st["params"] + st["opt"], r["params"] + r["opt"]):
         assert np.array_equal(u, v)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_*.npz"))))
+def test_bottleneck_golden_bitexact(orc, path):
+    """Bottleneck model (compress.hpp:38-415): window, bottleneck_update and
+    sharded_perplexity of the C restatement equal the reference fixture."""
+    g = np.load(path)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    T, B = g["x"].shape
+    r = orc.bn_bptt(params, int(g["act"]), g["x"], g["y"], g["w"], g["h0"], 1.0 / (T * B),
+                    float(g["clip"]))
+    assert r["loss"] == float(g["loss"]) and r["positions"] == int(g["positions"])
+    for key in ("h_final", "g_e", "g_u", "g_rec", "g_d"):
+        assert np.array_equal(r[key], g[key]), key
+    state = (g["m_e"], g["m_u"], g["m_rec"], g["m_d"])
+    p2, s2, ok = orc.bn_update(params, state, r, 0.9995, 1e-6, 0.05)
+    assert ok == bool(g["applied"])
+    for a, key in zip(p2 + s2, ("u_e", "u_u", "u_w_rec", "u_d", "u_m_e", "u_m_u", "u_m_rec",
+                                "u_m_d")):
+        assert np.array_equal(a, g[key]), key
+    sp = orc.bn_sharded_ppl(params, int(g["act"]), g["ids"], 8)
+    assert [sp["total_logprob"], sp["predicted"], sp["perplexity"]] == list(g["sharded"])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_bottleneck_random_configs_vs_reference(orc, ref, seed):
+    rng = np.random.default_rng(100 + seed)
+    V, H = int(rng.integers(20, 300)), int(rng.integers(4, 40))
+    P = int(rng.integers(1, H + 1))
+    T, B, act = int(rng.integers(1, 7)), int(rng.integers(1, 6)), int(rng.integers(0, 2))
+    pa, pb = orc.bn_init_uniform(V, H, P, seed), ref.bn_init_uniform(V, H, P, seed)
+    assert all(np.array_equal(a, b) for a, b in zip(pa, pb))
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(0, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.2).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    a = orc.bn_bptt(pa, act, x, y, w, h0, 0.1, 0.5)
+    b = ref.bn_bptt(pa, act, x, y, w, h0, 0.1, 0.5)
+    assert a["loss"] == b["loss"] and a["positions"] == b["positions"]
+    for key in ("h_final", "g_e", "g_u", "g_rec", "g_d"):
+        assert np.array_equal(a[key], b[key]), key
+    state = tuple(rng.uniform(0, 0.01, s).astype(np.float32) for s in (V, (P, H), (H, H), (H, P)))
+    ua, ub = orc.bn_update(pa, state, a, 0.9995, 1e-6, 0.05), ref.bn_update(pa, state, a, 0.9995,
+                                                                            1e-6, 0.05)
+    assert all(np.array_equal(p, q) for p, q in zip(ua[0] + ua[1], ub[0] + ub[1]))
+    # a non-finite gradient rejects the whole update (compress.hpp:300)
+    bad = dict(a)
+    bad["g_d"] = a["g_d"].copy()
+    bad["g_d"].flat[0] = np.nan
+    assert not orc.bn_update(pa, state, bad, 0.9995, 1e-6, 0.05)[2]
+    ids = orc.random_stream(seed, V, 300)
+    assert orc.bn_sharded_ppl(pa, act, ids, 4) == ref.bn_sharded_ppl(pa, act, ids, 4)
