@@ -252,6 +252,58 @@ void* dl_cuda_stream(const dl_ctx* ctx);
 int dl_set_profiling(dl_ctx* ctx, int on);
 double dl_kernel_ms(const dl_ctx* ctx, const char* name);
 
+/* ------------------------------------------------------------------
+ * Bottleneck / tied-embedding model (compress.hpp:38-415), a second model
+ * family on the same engine: BottleneckParams {E [V x P], U [P x H],
+ * W_rec [H x H], D [H x P]} with h' = act(E[x] . U + W_rec . h),
+ * z = h' . D, s_w = E[w] . z.  One context per (host thread, GPU); the
+ * device boundary is again per window and per scoring call.  Replaces the
+ * reference's BottleneckAdapter / BottleneckTraits seams:
+ *   dl_bn_create / dl_bn_set_params   BottleneckParams (compress.hpp:54-83)
+ *   dl_bn_set_opt / dl_bn_get_opt     BottleneckOptState (compress.hpp:252-278)
+ *   dl_bn_window                      bptt_run(BottleneckAdapter), softmax mode
+ *                                     (backprop.hpp:76-222, compress.hpp:121-244)
+ *   dl_bn_get_grads                   BottleneckGrads, dense E (compress.hpp:87-115)
+ *   dl_bn_rmsprop                     bottleneck_update (compress.hpp:296-309)
+ *   dl_bn_sharded_perplexity          sharded_perplexity(BottleneckAdapter)
+ *                                     (eval.hpp:151-222)
+ * Same status codes and error behaviour as the standard model's calls;
+ * P > H is rejected like the reference constructor (compress.hpp:72-73).
+ * ------------------------------------------------------------------ */
+typedef struct dl_bn dl_bn;
+
+int dl_bn_create(dl_bn** out, int device, int64_t V, int64_t H, int64_t P, int act,
+                 int precision);
+int dl_bn_destroy(dl_bn* ctx);
+const char* dl_bn_last_error(const dl_bn* ctx);
+/* e [V x P], u [P x H], w_rec [H x H], d [H x P], row-major fp32 */
+int dl_bn_set_params(dl_bn* ctx, const float* e, const float* u, const float* w_rec,
+                     const float* d);
+int dl_bn_get_params(dl_bn* ctx, float* e, float* u, float* w_rec, float* d);
+/* m_e [V], m_u [P x H], m_rec [H x H], m_d [H x P]; NULL = zeros */
+int dl_bn_set_opt(dl_bn* ctx, const float* m_e, const float* m_u, const float* m_rec,
+                  const float* m_d, double rho, double eps);
+int dl_bn_get_opt(dl_bn* ctx, float* m_e, float* m_u, float* m_rec, float* m_d);
+/* One softmax-mode window; arrays as dl_window. */
+int dl_bn_window(dl_bn* ctx, int64_t T, int64_t B, const uint32_t* inputs,
+                 const uint32_t* targets, const uint8_t* weights, const float* h0,
+                 float* h_final, double loss_scale, float clip, int compute_grads,
+                 double* loss, uint64_t* positions);
+/* Clipped gradients of the last window: dense g_e [V x P], g_u, g_rec, g_d. */
+int dl_bn_get_grads(dl_bn* ctx, float* g_e, float* g_u, float* g_rec, float* g_d);
+/* *applied = 0 mirrors bottleneck_update returning false (non-finite). */
+int dl_bn_rmsprop(dl_bn* ctx, double eta, int* applied);
+/* dl_bn_window + dl_bn_rmsprop in one call. */
+int dl_bn_train_window(dl_bn* ctx, int64_t T, int64_t B, const uint32_t* inputs,
+                       const uint32_t* targets, const uint8_t* weights, const float* h0,
+                       float* h_final, double loss_scale, float clip, double eta,
+                       double* loss, uint64_t* positions, int* applied);
+int dl_bn_sharded_perplexity(dl_bn* ctx, const uint32_t* ids, int64_t n, int shards,
+                             uint32_t bos, double* total_logprob, uint64_t* predicted,
+                             double* perplexity);
+uint64_t dl_bn_launch_count(const dl_bn* ctx);
+void* dl_bn_cuda_stream(const dl_bn* ctx);
+
 #ifdef __cplusplus
 }
 #endif

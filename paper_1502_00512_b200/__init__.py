@@ -16,7 +16,9 @@ this package                reference
 ``rescore_nbest``           ``rescore_nbest`` RNN part (eval.hpp:693-790)
 ``TrainConfig``/``Trainer`` ``TrainConfig``/``Trainer<StandardTraits>``
                             (trainer.hpp:43-93, :171-476)
-``formats``                 RNLM / ROPT / RTRN byte layouts
+``formats``                 RNLM / ROPT / RTRN (+ RNBL / RBOP) byte layouts
+``bottleneck``              ``BottleneckParams`` / ``BottleneckAdapter`` /
+                            ``bottleneck_update`` (compress.hpp:38-415)
 ==========================  ===============================================
 
 Every number is computed by libdesklm_cuda.so (sm_100a kernels); this

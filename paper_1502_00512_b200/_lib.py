@@ -24,7 +24,10 @@ EXPORTS = (
     "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
     "dl_local_group_destroy", "dl_comm_init_local", "dl_set_vocab_shard",
     "dl_set_loss_mode", "dl_set_noise", "dl_set_rng_state", "dl_get_rng_state",
-    "dl_rng_seed_state",
+    "dl_rng_seed_state", "dl_bn_create", "dl_bn_destroy", "dl_bn_last_error",
+    "dl_bn_set_params", "dl_bn_get_params", "dl_bn_set_opt", "dl_bn_get_opt", "dl_bn_window",
+    "dl_bn_get_grads", "dl_bn_rmsprop", "dl_bn_train_window", "dl_bn_sharded_perplexity",
+    "dl_bn_launch_count", "dl_bn_cuda_stream",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -95,6 +98,24 @@ def load():
         "dl_set_rng_state": (C.c_int, [vp, vp]),
         "dl_get_rng_state": (C.c_int, [vp, vp]),
         "dl_rng_seed_state": (C.c_int, [u64, vp]),
+        "dl_bn_create": (C.c_int, [P(vp), C.c_int, i64, i64, i64, C.c_int, C.c_int]),
+        "dl_bn_destroy": (C.c_int, [vp]),
+        "dl_bn_last_error": (C.c_char_p, [vp]),
+        "dl_bn_set_params": (C.c_int, [vp, vp, vp, vp, vp]),
+        "dl_bn_get_params": (C.c_int, [vp, vp, vp, vp, vp]),
+        "dl_bn_set_opt": (C.c_int, [vp, vp, vp, vp, vp, C.c_double, C.c_double]),
+        "dl_bn_get_opt": (C.c_int, [vp, vp, vp, vp, vp]),
+        "dl_bn_window": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, C.c_double, C.c_float,
+                                   C.c_int, P(C.c_double), P(C.c_uint64)]),
+        "dl_bn_get_grads": (C.c_int, [vp, vp, vp, vp, vp]),
+        "dl_bn_rmsprop": (C.c_int, [vp, C.c_double, P(C.c_int)]),
+        "dl_bn_train_window": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, C.c_double,
+                                         C.c_float, C.c_double, P(C.c_double), P(C.c_uint64),
+                                         P(C.c_int)]),
+        "dl_bn_sharded_perplexity": (C.c_int, [vp, vp, i64, C.c_int, C.c_uint32,
+                                               P(C.c_double), P(C.c_uint64), P(C.c_double)]),
+        "dl_bn_launch_count": (u64, [vp]),
+        "dl_bn_cuda_stream": (vp, [vp]),
         "dl_launch_count": (u64, [vp]),
         "dl_cuda_stream": (vp, [vp]),
         "dl_set_profiling": (C.c_int, [vp, C.c_int]),

@@ -1,0 +1,202 @@
+"""Bottleneck / tied-embedding model (compress.hpp:38-415) on the device.
+
+==============================  =============================================
+this module                     reference (include/desklm/compress.hpp)
+==============================  =============================================
+``bottleneck_param_count``      ``bottleneck_param_count`` (:47-52)
+``bn_init_uniform``             ``BottleneckParams::init_uniform`` (:78-82)
+``GpuBottleneck``               ``BottleneckParams<float>`` +
+                                ``BottleneckAdapter`` + ``BottleneckOptState``
+``bn_bptt_run``                 ``bptt_run(BottleneckAdapter)``, softmax mode
+                                (backprop.hpp:76-222)
+``bottleneck_update``           ``bottleneck_update`` (:296-309)
+``bn_sharded_perplexity``       ``sharded_perplexity(BottleneckAdapter)``
+                                (eval.hpp:151-222)
+``formats.write_bottleneck``    RNBL / RBOP byte layouts (:313-386)
+==============================  =============================================
+
+Every number comes from libdesklm_cuda.so (csrc/bottleneck.cu); this module
+only moves host arrays across the C ABI (include/desklm_cuda.h, dl_bn_*).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import DL_BF16, DL_FP32, check, load
+
+_PREC = {"fp32": DL_FP32, "bf16": DL_BF16}
+
+
+def bottleneck_param_count(v: int, h: int, p: int) -> int:
+    """compress.hpp:47-52: V*P + P*H + H*H + H*P."""
+    if v < 1 or h < 1 or p < 1:
+        raise ValueError("bottleneck param count: V,H,P >= 1")
+    return v * p + p * h + h * h + h * p
+
+
+def bn_init_uniform(V: int, H: int, P: int, seed: int, init_range: float = 0.1):
+    """BottleneckParams::init_uniform (compress.hpp:78-82): one
+    std::mt19937_64(seed) over e, u, w_rec, d in order (host, bit-exact)."""
+    if V < 1 or H < 1 or P < 1:
+        raise ValueError("BottleneckParams: V,H,P >= 1")
+    if P > H:
+        raise ValueError("BottleneckParams: P must not exceed H")
+    from . import init_uniform  # the engine's host mt19937_64 stream
+    # one generator over V*P + P*H + H*H + H*P values: the first n values of
+    # the (n x 1) standard stream (its w_in) are exactly that sequence
+    n = V * P + P * H + H * H + H * P
+    flat = init_uniform(n, 1, seed, init_range)[0].ravel()
+    sizes = [V * P, P * H, H * H, H * P]
+    shapes = [(V, P), (P, H), (H, H), (H, P)]
+    out, o = [], 0
+    for sz, sh in zip(sizes, shapes):
+        out.append(flat[o:o + sz].reshape(sh).copy())
+        o += sz
+    return tuple(out)
+
+
+class _Res:
+    def __init__(self, loss, positions):
+        self.loss, self.positions = loss, positions
+
+
+class GpuBottleneck:
+    """Device-resident bottleneck model {E [V x P], U [P x H], W_rec [H x H],
+    D [H x P]} with its rmsprop state.  precision: "fp32" (parity mode) or
+    "bf16" (tcgen05 tensor cores; V, H, P multiples of 8)."""
+
+    def __init__(self, V: int, H: int, P: int, act: int = 0, precision: str = "fp32",
+                 device: int = 0):
+        lib = load()
+        self.V, self.H, self.P, self.act, self.precision = int(V), int(H), int(P), int(act), precision
+        h = C.c_void_p()
+        rc = lib.dl_bn_create(C.byref(h), device, self.V, self.H, self.P, self.act,
+                              _PREC[precision])
+        if rc:
+            check_bn(rc, None)
+        self._h = h
+        self.rho, self.eps = 0.9995, 1e-6
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().dl_bn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        check_bn(rc, self._h)
+
+    def _shapes(self):
+        return ((self.V, self.P), (self.P, self.H), (self.H, self.H), (self.H, self.P))
+
+    def set_params(self, e, u, w_rec, d):
+        a = [np.ascontiguousarray(x, np.float32) for x in (e, u, w_rec, d)]
+        if tuple(x.shape for x in a) != self._shapes():
+            raise ValueError("set_params: shape mismatch")
+        self._chk(load().dl_bn_set_params(self._h, *(x.ctypes.data for x in a)))
+
+    def params(self):
+        out = [np.empty(s, np.float32) for s in self._shapes()]
+        self._chk(load().dl_bn_get_params(self._h, *(x.ctypes.data for x in out)))
+        return tuple(out)
+
+    def set_opt(self, m_e=None, m_u=None, m_rec=None, m_d=None, rho=0.9995, eps=1e-6):
+        a = [None if x is None else np.ascontiguousarray(x, np.float32)
+             for x in (m_e, m_u, m_rec, m_d)]
+        self._chk(load().dl_bn_set_opt(self._h, *(None if x is None else x.ctypes.data
+                                                  for x in a), rho, eps))
+        self.rho, self.eps = rho, eps
+
+    def opt(self):
+        out = [np.empty(s, np.float32) for s in ((self.V,),) + self._shapes()[1:]]
+        self._chk(load().dl_bn_get_opt(self._h, *(x.ctypes.data for x in out)))
+        return tuple(out)
+
+    def grads(self):
+        """Clipped gradients of the last window: (g_e dense, g_u, g_rec, g_d)."""
+        out = [np.empty(s, np.float32) for s in self._shapes()]
+        self._chk(load().dl_bn_get_grads(self._h, *(x.ctypes.data for x in out)))
+        return tuple(out)
+
+    def launch_count(self) -> int:
+        return int(load().dl_bn_launch_count(self._h))
+
+
+def check_bn(rc, h):
+    if rc == 0:
+        return
+    from ._lib import DL_EDATA, DL_EINVAL, DataError, DeviceError
+    msg = (load().dl_bn_last_error(h) or b"").decode()
+    if rc == DL_EINVAL:
+        raise ValueError(msg)
+    if rc == DL_EDATA:
+        raise DataError(msg)
+    raise DeviceError(msg)
+
+
+def _window_arrays(model, wb, h0):
+    x = np.ascontiguousarray(wb.inputs, np.uint32)
+    y = np.ascontiguousarray(wb.targets, np.uint32)
+    w = np.ascontiguousarray(wb.weights, np.uint8)
+    if x.shape != y.shape or x.shape != w.shape or x.ndim != 2:
+        raise ValueError("bptt: window size mismatch")
+    T, B = x.shape
+    h0 = np.ascontiguousarray(h0, np.float32)
+    if h0.shape != (B, model.H):
+        raise ValueError("bptt: initial state shape mismatch")
+    return x, y, w, T, B, h0
+
+
+def bn_bptt_run(model: GpuBottleneck, wb, h0, loss_scale: float = 1.0, clip: float = 1.0,
+                compute_grads: bool = True):
+    """bptt_run over the bottleneck adapter (softmax mode); returns
+    (BpttResult, h_final); gradients stay on the device."""
+    from . import BpttResult
+    x, y, w, T, B, h0 = _window_arrays(model, wb, h0)
+    hf = np.empty((B, model.H), np.float32)
+    loss, pos = C.c_double(), C.c_uint64()
+    model._chk(load().dl_bn_window(model.handle, T, B, x.ctypes.data, y.ctypes.data,
+                                   w.ctypes.data, h0.ctypes.data, hf.ctypes.data,
+                                   float(loss_scale), float(clip), int(compute_grads),
+                                   C.byref(loss), C.byref(pos)))
+    return BpttResult(loss.value, pos.value), hf
+
+
+def bn_train_window(model: GpuBottleneck, wb, h0, loss_scale: float, clip: float, eta: float):
+    """bptt_run + bottleneck_update in one call; (BpttResult, h_final, applied)."""
+    from . import BpttResult
+    x, y, w, T, B, h0 = _window_arrays(model, wb, h0)
+    hf = np.empty((B, model.H), np.float32)
+    loss, pos, applied = C.c_double(), C.c_uint64(), C.c_int()
+    model._chk(load().dl_bn_train_window(model.handle, T, B, x.ctypes.data, y.ctypes.data,
+                                         w.ctypes.data, h0.ctypes.data, hf.ctypes.data,
+                                         float(loss_scale), float(clip), float(eta),
+                                         C.byref(loss), C.byref(pos), C.byref(applied)))
+    return BpttResult(loss.value, pos.value), hf, bool(applied.value)
+
+
+def bottleneck_update(model: GpuBottleneck, eta: float) -> bool:
+    applied = C.c_int()
+    model._chk(load().dl_bn_rmsprop(model.handle, float(eta), C.byref(applied)))
+    return bool(applied.value)
+
+
+def bn_sharded_perplexity(model: GpuBottleneck, ids, shards: int, bos_id: int = 1):
+    from . import PerplexityResult
+    ids = np.ascontiguousarray(ids, np.uint32)
+    tot, pred, ppl = C.c_double(), C.c_uint64(), C.c_double()
+    model._chk(load().dl_bn_sharded_perplexity(model.handle, ids.ctypes.data, len(ids), shards,
+                                               bos_id, C.byref(tot), C.byref(pred),
+                                               C.byref(ppl)))
+    return PerplexityResult(ppl.value, tot.value, pred.value)

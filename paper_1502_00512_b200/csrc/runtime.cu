@@ -1111,7 +1111,8 @@ void alloc_output(dl_ctx* c) {
     c->w_out_bf_next = dalloc<bf16>(Vo * H);
     c->g_out_bf = dalloc<bf16>(Vo * H);
     c->rowsq_n = tc_n_tiles((int)H);
-    c->rowsq = dalloc<double>((size_t)c->rowsq_n * Vo);
+    // (the fused dW_out epilogue writes 2 partials per 128-column tile)
+    c->rowsq = dalloc<double>((size_t)std::max<int64_t>(c->rowsq_n, 2 * ((H + 127) / 128)) * Vo);
     c->rms_cnt = dalloc<unsigned>((Vo + 255) / 256);
   }
   c->fuse_cap = -1;

@@ -173,6 +173,79 @@ def read_rmsprop(data_or_reader):
     return V, H, rho, eps, (m_rec, m_in, m_out)
 
 
+# ------------------------------------------------------------ RNBL / RBOP
+BOTTLENECK_FORMAT_VERSION = 1
+
+
+def write_bottleneck(params, vocab_words, act: int = 0) -> bytes:
+    """write_bottleneck (compress.hpp:315-328): e, u, w_rec, d row-major."""
+    e, u, w_rec, d = params
+    V, P = e.shape
+    H = w_rec.shape[0]
+    out = io.BytesIO()
+    out.write(b"RNBL" + _u32(BOTTLENECK_FORMAT_VERSION) + _u64(V) + _u64(H) + _u64(P) + _u8(act))
+    for m in (e, u, w_rec, d):
+        out.write(np.ascontiguousarray(m, "<f4").tobytes())
+    out.write(_u64(len(vocab_words)))
+    for w in vocab_words:
+        out.write(_str(w))
+    return out.getvalue()
+
+
+def read_bottleneck(data_or_reader):
+    """read_bottleneck (compress.hpp:330-354) -> ((e, u, w_rec, d), act, words)."""
+    r = data_or_reader if isinstance(data_or_reader, Reader) else Reader(data_or_reader)
+    r.magic("RNBL", "bottleneck checkpoint")
+    ver = r.u32()
+    if ver != BOTTLENECK_FORMAT_VERSION:
+        raise DataError(f"bottleneck checkpoint: unsupported version {ver}")
+    V, H, P = r.u64(), r.u64(), r.u64()
+    if V < 1 or H < 1 or P < 1 or V > (1 << 26) or H > (1 << 20) or P > (1 << 20):
+        raise DataError("bottleneck checkpoint: implausible dimensions")
+    act = r.u8()
+    if P > H:
+        raise ValueError("BottleneckParams: P must not exceed H")
+    e = r.f32s(V * P).reshape(V, P)
+    u = r.f32s(P * H).reshape(P, H)
+    w_rec = r.f32s(H * H).reshape(H, H)
+    d = r.f32s(H * P).reshape(H, P)
+    n = r.u64()
+    if n != V:
+        raise DataError("bottleneck checkpoint: vocabulary size mismatch")
+    words = [r.string() for _ in range(n)]
+    return (e, u, w_rec, d), act, words
+
+
+def write_bottleneck_opt(V, H, P, rho, eps, state) -> bytes:
+    """write_bottleneck_opt (compress.hpp:356-368): m_e, m_u, m_rec, m_d."""
+    m_e, m_u, m_rec, m_d = state
+    return (b"RBOP" + _u32(BOTTLENECK_FORMAT_VERSION) + _u64(V) + _u64(H) + _u64(P) + _f64(rho) +
+            _f64(eps) + b"".join(np.ascontiguousarray(m, "<f4").tobytes()
+                                 for m in (m_e, m_u, m_rec, m_d)))
+
+
+def read_bottleneck_opt(data_or_reader):
+    """read_bottleneck_opt (compress.hpp:370-386) -> (V, H, P, rho, eps, state)."""
+    r = data_or_reader if isinstance(data_or_reader, Reader) else Reader(data_or_reader)
+    r.magic("RBOP", "bottleneck optimizer state")
+    ver = r.u32()
+    if ver != BOTTLENECK_FORMAT_VERSION:
+        raise DataError(f"bottleneck optimizer state: unsupported version {ver}")
+    V, H, P = r.u64(), r.u64(), r.u64()
+    rho, eps = r.f64(), r.f64()
+    if V < 1 or H < 1 or P < 1:
+        raise ValueError("opt state: V,H,P >= 1")
+    if not (0.0 < rho < 1.0):
+        raise ValueError("opt state: rho must be in (0, 1)")
+    if not eps > 0.0:
+        raise ValueError("opt state: eps must be > 0")
+    m_e = r.f32s(V)
+    m_u = r.f32s(P * H).reshape(P, H)
+    m_rec = r.f32s(H * H).reshape(H, H)
+    m_d = r.f32s(H * P).reshape(H, P)
+    return V, H, P, rho, eps, (m_e, m_u, m_rec, m_d)
+
+
 # ---------------------------------------------------------- mt19937_64 text
 def mt19937_64_text(seed: int) -> str:
     """`os << std::mt19937_64(seed)` as libstdc++ prints it: the 312 state

@@ -60,3 +60,16 @@ def test_config_validation_mirrors_reference():
                 dict(threads=0), dict(mode=2), dict(mode=0, nce_k=0)):
         with pytest.raises(ValueError):
             TrainConfig(**dict(dict(mode=1), **bad)).validate()
+
+
+def test_bottleneck_argument_errors_without_gpu():
+    """dl_bn_create validates like the BottleneckParams constructor
+    (compress.hpp:66-74) before touching the device."""
+    from paper_1502_00512_b200 import _lib
+    lib = _lib.load()
+    h = C.c_void_p()
+    assert lib.dl_bn_create(C.byref(h), 0, 0, 4, 2, 0, 0) == _lib.DL_EINVAL
+    assert lib.dl_bn_create(C.byref(h), 0, 16, 4, 8, 0, 0) == _lib.DL_EINVAL  # P > H
+    assert b"P must not exceed H" in lib.dl_bn_last_error(None)
+    assert lib.dl_bn_create(C.byref(h), 0, 16, 8, 4, 0, 1) == _lib.DL_EINVAL  # bf16 needs %8
+    assert lib.dl_bn_create(C.byref(h), 0, 16, 8, 8, 3, 0) == _lib.DL_EINVAL  # act
