@@ -306,6 +306,72 @@ class _Backend:
         return dict(total_logprob=tl.value, predicted=pr.value, perplexity=ppl.value)
 
 
+    def bn_train(self, cfg, params, train_ids, valid_ids):
+        """Trainer<BottleneckTraits>::train (trainer.hpp:178-270, 350-410;
+        compress.hpp:389-415), softmax mode, restated over this backend's
+        bn_bptt / bn_update / bn_sharded_ppl (a Python loop: small cases).
+        Returns dict(logs [n x 7] (seconds / tokens_per_sec zero),
+        initial_ppl, params, opt, cursors, hidden)."""
+        if cfg.mode != 1:
+            raise ValueError("bn_train: softmax mode only")
+        e, u, w_rec, d = [np.array(x, np.float32, copy=True) for x in params]
+        V, P = e.shape
+        H = cfg.nstate
+        tr = np.ascontiguousarray(train_ids, np.uint32)
+        va = np.ascontiguousarray(valid_ids, np.uint32)
+        if cfg.valid_limit > 0 and len(va) > cfg.valid_limit:
+            va = va[: cfg.valid_limit]
+        L, B, T = len(tr), cfg.minibatch, cfg.unroll
+        N = cfg.noffset * B
+        cur = np.array([i * L // N for i in range(N)], np.int64)
+        a0 = np.float32(0.5) if cfg.act == 0 else np.float32(0.0)
+        hidden = np.full((N, H), a0, np.float32)
+        state = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
+                 np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
+        prm = (e, u, w_rec, d)
+
+        def validate():
+            return self.bn_sharded_ppl(prm, cfg.act, va, cfg.valid_shards)["perplexity"]
+
+        initial = validate()
+        best, bad, eta, epoch, logs = initial, 0, cfg.eta, 0, []
+        rounds = (L + N * T - 1) // (N * T)
+        tt = np.arange(T)[:, None]
+        while epoch < cfg.max_epochs and bad < 2:
+            loss_sum, windows, skipped = 0.0, 0, 0
+            for _ in range(rounds):
+                for g in range(cfg.noffset):
+                    s0 = g * B
+                    pos = cur[None, s0:s0 + B] + tt
+                    x = tr[pos % L]
+                    y = tr[(pos + 1) % L]
+                    w = (y != 1).astype(np.uint8)
+                    r = self.bn_bptt(prm, cfg.act, x, y, w, hidden[s0:s0 + B],
+                                     1.0 / (B * T), cfg.clip)
+                    loss_sum += r["loss"]
+                    windows += 1
+                    prm, state, ok = self.bn_update(prm, state, r, cfg.rho, cfg.eps, eta)
+                    skipped += 0 if ok else 1
+                    hidden[s0:s0 + B] = r["h_final"]
+                    cur[s0:s0 + B] += T
+                    wrap = cur[s0:s0 + B] >= L
+                    cur[s0:s0 + B][wrap] -= L
+                    hidden[s0:s0 + B][wrap] = a0
+            ppl = validate()
+            epoch += 1
+            logs.append([epoch, loss_sum / windows if windows else 0.0, ppl, eta, 0.0, 0.0,
+                         skipped])
+            if ppl > cfg.divergence_factor * initial:
+                raise OracleError(2, "trainer: diverged")
+            if ppl < best:
+                best, bad = ppl, 0
+            else:
+                bad += 1
+                eta *= 0.5
+        return dict(logs=np.array(logs, np.float64), initial_ppl=initial, params=prm, opt=state,
+                    cursors=cur, hidden=hidden)
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, msg=""):
         super().__init__(f"oracle status {code}: {msg}")
@@ -475,6 +541,29 @@ class Ref(_Backend):
         self._rescore.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p,
                                   C.c_char_p, C.c_double, C.c_double, C.c_int, _vp,
                                   _u64, C.POINTER(C.c_uint64)]
+
+    def bn_train_native(self, cfg, params, train_ids, valid_ids, run=True):
+        """The reference's own Trainer<BottleneckTraits>: (rtrn_bytes, logs, initial)."""
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = cfg.nstate
+        tr = np.ascontiguousarray(train_ids, np.uint32)
+        va = np.ascontiguousarray(valid_ids, np.uint32)
+        N = cfg.noffset * cfg.minibatch
+        cap = 16384 + 8 * N + 4 * N * H + 8 * (V * P + 2 * P * H + H * H + 2 * H * P) + \
+            64 * V + 8 * V
+        buf = np.zeros(cap, np.uint8)
+        ln = C.c_uint64()
+        logs = np.zeros((max(cfg.max_epochs, 1), 7), np.float64)
+        nl = C.c_int()
+        ini = C.c_double()
+        f = self.lib.ref_bn_train
+        f.argtypes = [C.POINTER(TrainConfig), _i64, _i64, _f32p, _f32p, _f32p, _f32p, _u32p,
+                      _i64, _u32p, _i64, C.c_int, _vp, _u64, C.POINTER(C.c_uint64), _f64p,
+                      C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        self._check(f(C.byref(cfg), V, P, e, u, w_rec, d, tr, len(tr), va, len(va), int(run),
+                      buf.ctypes.data, cap, C.byref(ln), logs, C.byref(nl), C.byref(ini)))
+        return bytes(buf[: ln.value]), logs[: nl.value].copy(), ini.value
 
     def bn_write(self, params, state, rho, eps, act=0):
         """write_bottleneck (RNBL, vocabulary make_vocab(V)) and

@@ -409,6 +409,71 @@ int ref_sharded_logprobs(std::int64_t V, std::int64_t H, int act,
 // the reference does) on a make_vocab(V) vocabulary; returns the RTRN
 // checkpoint bytes and the epoch logs (7 doubles per epoch: epoch,
 // train_loss, valid_ppl, eta, seconds, tokens_per_sec, skipped).
+}  // extern "C"
+
+namespace {
+
+TrainConfig to_cfg(const ref_train_config* c) {
+  TrainConfig cfg;
+  cfg.nstate = c->nstate;
+  cfg.nproj = c->nproj;
+  cfg.noffset = c->noffset;
+  cfg.minibatch = c->minibatch;
+  cfg.unroll = c->unroll;
+  cfg.mode = static_cast<LossMode>(c->mode);
+  cfg.eta = c->eta;
+  cfg.rho = c->rho;
+  cfg.eps = c->eps;
+  cfg.clip = c->clip;
+  cfg.nce_k = c->nce_k;
+  cfg.max_epochs = c->max_epochs;
+  cfg.noise_floor = c->noise_floor;
+  cfg.seed = c->seed;
+  cfg.act = static_cast<Activation>(c->act);
+  cfg.valid_shards = c->valid_shards;
+  cfg.divergence_factor = c->divergence_factor;
+  cfg.valid_limit = c->valid_limit;
+  cfg.init_range = c->init_range;
+  cfg.threads = c->threads;
+  return cfg;
+}
+
+// Trainer<Traits>::train + save_checkpoint; logs as 7 doubles per epoch.
+template <class Traits>
+void run_trainer(const TrainConfig& cfg, const typename Traits::Params& p, std::int64_t V,
+                 const std::uint32_t* train_ids, std::int64_t n_train,
+                 const std::uint32_t* valid_ids, std::int64_t n_valid, int run_epochs,
+                 std::uint8_t* ckpt, std::uint64_t cap, std::uint64_t* ckpt_len, double* logs,
+                 int* n_logs, double* initial_ppl) {
+  IdStream tr, va;
+  tr.ids.assign(train_ids, train_ids + n_train);
+  va.ids.assign(valid_ids, valid_ids + n_valid);
+  Trainer<Traits> t(cfg, p, testutil::make_vocab(V), tr, va);
+  if (run_epochs) t.train(nullptr);
+  std::ostringstream os(std::ios::binary);
+  t.save_checkpoint(os);
+  const std::string b = os.str();
+  *ckpt_len = b.size();
+  if (b.size() <= cap) std::memcpy(ckpt, b.data(), b.size());
+  *n_logs = static_cast<int>(t.logs().size());
+  for (std::size_t i = 0; i < t.logs().size(); ++i) {
+    const EpochLog& l = t.logs()[i];
+    double* o = logs + 7 * i;
+    o[0] = l.epoch;
+    o[1] = l.train_loss;
+    o[2] = l.valid_ppl;
+    o[3] = l.eta;
+    o[4] = l.seconds;
+    o[5] = l.tokens_per_sec;
+    o[6] = static_cast<double>(l.skipped_updates);
+  }
+  *initial_ppl = t.initial_ppl();
+}
+
+}  // namespace
+
+extern "C" {
+
 int ref_train(const ref_train_config* c, std::int64_t V, const float* w_in,
               const float* w_rec, const float* w_out,
               const std::uint32_t* train_ids, std::int64_t n_train,
@@ -417,52 +482,27 @@ int ref_train(const ref_train_config* c, std::int64_t V, const float* w_in,
               std::uint64_t* ckpt_len, double* logs, int* n_logs,
               double* initial_ppl) {
   return guarded([&] {
-    TrainConfig cfg;
-    cfg.nstate = c->nstate;
-    cfg.nproj = c->nproj;
-    cfg.noffset = c->noffset;
-    cfg.minibatch = c->minibatch;
-    cfg.unroll = c->unroll;
-    cfg.mode = static_cast<LossMode>(c->mode);
-    cfg.eta = c->eta;
-    cfg.rho = c->rho;
-    cfg.eps = c->eps;
-    cfg.clip = c->clip;
-    cfg.nce_k = c->nce_k;
-    cfg.max_epochs = c->max_epochs;
-    cfg.noise_floor = c->noise_floor;
-    cfg.seed = c->seed;
-    cfg.act = static_cast<Activation>(c->act);
-    cfg.valid_shards = c->valid_shards;
-    cfg.divergence_factor = c->divergence_factor;
-    cfg.valid_limit = c->valid_limit;
-    cfg.init_range = c->init_range;
-    cfg.threads = c->threads;
-    const RnnParams<float> p =
-        make_params(V, c->nstate, c->act, w_in, w_rec, w_out);
-    IdStream tr, va;
-    tr.ids.assign(train_ids, train_ids + n_train);
-    va.ids.assign(valid_ids, valid_ids + n_valid);
-    Trainer<StandardTraits> t(cfg, p, testutil::make_vocab(V), tr, va);
-    if (run_epochs) t.train(nullptr);
-    std::ostringstream os(std::ios::binary);
-    t.save_checkpoint(os);
-    const std::string b = os.str();
-    *ckpt_len = b.size();
-    if (b.size() <= cap) std::memcpy(ckpt, b.data(), b.size());
-    *n_logs = static_cast<int>(t.logs().size());
-    for (std::size_t i = 0; i < t.logs().size(); ++i) {
-      const EpochLog& l = t.logs()[i];
-      double* o = logs + 7 * i;
-      o[0] = l.epoch;
-      o[1] = l.train_loss;
-      o[2] = l.valid_ppl;
-      o[3] = l.eta;
-      o[4] = l.seconds;
-      o[5] = l.tokens_per_sec;
-      o[6] = static_cast<double>(l.skipped_updates);
-    }
-    *initial_ppl = t.initial_ppl();
+    const RnnParams<float> p = make_params(V, c->nstate, c->act, w_in, w_rec, w_out);
+    run_trainer<StandardTraits>(to_cfg(c), p, V, train_ids, n_train, valid_ids, n_valid,
+                                run_epochs, ckpt, cap, ckpt_len, logs, n_logs, initial_ppl);
+  });
+}
+
+// Trainer<BottleneckTraits> (compress.hpp:389-415; test_compress.cpp:427-460).
+int ref_bn_train(const ref_train_config* c, std::int64_t V, std::int64_t P, const float* e,
+                 const float* u, const float* w_rec, const float* d,
+                 const std::uint32_t* train_ids, std::int64_t n_train,
+                 const std::uint32_t* valid_ids, std::int64_t n_valid, int run_epochs,
+                 std::uint8_t* ckpt, std::uint64_t cap, std::uint64_t* ckpt_len, double* logs,
+                 int* n_logs, double* initial_ppl) {
+  return guarded([&] {
+    BottleneckParams<float> p(V, c->nstate, P, static_cast<Activation>(c->act));
+    std::memcpy(p.e.a.data(), e, sizeof(float) * V * P);
+    std::memcpy(p.u.a.data(), u, sizeof(float) * P * c->nstate);
+    std::memcpy(p.w_rec.a.data(), w_rec, sizeof(float) * c->nstate * c->nstate);
+    std::memcpy(p.d.a.data(), d, sizeof(float) * c->nstate * P);
+    run_trainer<BottleneckTraits>(to_cfg(c), p, V, train_ids, n_train, valid_ids, n_valid,
+                                  run_epochs, ckpt, cap, ckpt_len, logs, n_logs, initial_ppl);
   });
 }
 

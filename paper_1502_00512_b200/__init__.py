@@ -530,8 +530,6 @@ class TrainConfig:
             raise ValueError("config: threads must be >= 1")
         if self.mode not in (0, 1):
             raise ValueError("config: mode must be 0 (NCE) or 1 (softmax)")
-        if self.nproj != 0:
-            raise ValueError("config: bottleneck models are not on the B200 path")
 
 
 @dataclass

@@ -200,3 +200,121 @@ def bn_sharded_perplexity(model: GpuBottleneck, ids, shards: int, bos_id: int = 
                                                bos_id, C.byref(tot), C.byref(pred),
                                                C.byref(ppl)))
     return PerplexityResult(ppl.value, tot.value, pred.value)
+
+
+class BottleneckTrainer:
+    """Trainer<BottleneckTraits> (trainer.hpp:171-476 over compress.hpp:389-415),
+    softmax mode.  The host keeps the reference's schedule -- offset-stream
+    cursors floor(i*L/N), window (r, g) positions cursor + t, bos-masked
+    targets, hidden carry and wrap reset (trainer.hpp:350-410) -- and every
+    window runs on the device as one dl_bn_train_window call (bptt_run +
+    bottleneck_update).  Validation is the device sharded scorer; the RTRN
+    checkpoint carries RNBL + RBOP like the reference traits."""
+
+    def __init__(self, cfg, params, vocab_words, train_ids, valid_ids, precision: str = "fp32",
+                 device: int = 0):
+        from . import BOS_ID, EpochLog  # noqa: F401
+        cfg.validate()
+        if cfg.mode != 1:
+            raise ValueError("bottleneck trainer: only the softmax loss (mode 1) runs on the "
+                             "device for the bottleneck model")
+        self.cfg = cfg
+        self.vocab = list(vocab_words)
+        e, u, w_rec, d = (np.asarray(x, np.float32) for x in params)
+        V, P = e.shape
+        H = w_rec.shape[0]
+        if len(self.vocab) != V:
+            raise ValueError("trainer: vocabulary/model size mismatch")
+        if H != cfg.nstate:
+            raise ValueError("trainer: nstate does not match the parameters")
+        self.train_ids = np.ascontiguousarray(train_ids, np.uint32)
+        valid = np.ascontiguousarray(valid_ids, np.uint32)
+        if cfg.valid_limit > 0 and len(valid) > cfg.valid_limit:
+            valid = valid[: cfg.valid_limit]
+        if len(valid) < 2:
+            raise ValueError("trainer: validation stream too short")
+        self.valid = valid
+        L = len(self.train_ids)
+        N = cfg.noffset * cfg.minibatch
+        if L < N:
+            raise ValueError("trainer: training stream shorter than the stream count")
+        self.model = GpuBottleneck(V, H, P, cfg.act, precision, device)
+        self.model.set_params(e, u, w_rec, d)
+        self.model.set_opt(None, None, None, None, cfg.rho, cfg.eps)
+        self.cursors = np.array([i * L // N for i in range(N)], np.int64)
+        self.a0 = np.float32(0.5 if cfg.act == 0 else 0.0)
+        self.hidden = np.full((N, H), self.a0, np.float32)
+        self.logs = []
+        self.epoch = 0
+        self.bad_epochs = 0
+        self.eta = cfg.eta
+        self.best_ppl = 0.0
+        self.initial_ppl = 0.0
+
+    def params(self):
+        return self.model.params()
+
+    def validate(self) -> float:
+        return bn_sharded_perplexity(self.model, self.valid, self.cfg.valid_shards).perplexity
+
+    def run_epoch(self):
+        """trainer.hpp:350-410 -> (mean window loss, skipped, tokens)."""
+        from . import WindowBatch
+        cfg = self.cfg
+        ids, L = self.train_ids, len(self.train_ids)
+        B, T = cfg.minibatch, cfg.unroll
+        N = cfg.noffset * B
+        rounds = (L + N * T - 1) // (N * T)
+        tt = np.arange(T)[:, None]
+        loss_sum, windows, skipped = 0.0, 0, 0
+        for _ in range(rounds):
+            for g in range(cfg.noffset):
+                s0 = g * B
+                pos = self.cursors[None, s0:s0 + B] + tt
+                x = ids[pos % L]
+                y = ids[(pos + 1) % L]
+                w = (y != 1).astype(np.uint8)
+                res, hf, ok = bn_train_window(self.model, WindowBatch(x, y, w),
+                                              self.hidden[s0:s0 + B], 1.0 / (B * T), cfg.clip,
+                                              self.eta)
+                loss_sum += res.loss
+                windows += 1
+                skipped += 0 if ok else 1
+                self.hidden[s0:s0 + B] = hf
+                cur = self.cursors[s0:s0 + B]
+                cur += T
+                wrap = cur >= L
+                cur[wrap] -= L
+                self.hidden[s0:s0 + B][wrap] = self.a0
+        return (loss_sum / windows if windows else 0.0), skipped, rounds * N * T
+
+    def train(self, progress=None):
+        """trainer.hpp:233-270 (the same loop as Trainer.train)."""
+        from . import Trainer
+        Trainer.train(self, progress)
+
+    # ---- checkpointing (RTRN with RNBL / RBOP)
+    def save_checkpoint(self) -> bytes:
+        from . import formats
+        return formats.write_trainer(self.cfg, self.epoch, self.eta, self.best_ppl,
+                                     self.bad_epochs, self.initial_ppl,
+                                     formats.mt19937_64_text(self.cfg.seed), self.cursors,
+                                     self.hidden, self.model.params(), self.vocab,
+                                     self.model.opt(), model="bottleneck")
+
+    def load_checkpoint(self, data: bytes):
+        from . import DataError, formats
+        cfg = self.cfg
+        st = formats.read_trainer(data, cfg, len(self.cursors), self.model.H,
+                                  len(self.train_ids), model="bottleneck")
+        e = st["params"][0]
+        if st["params"][2].shape != (self.model.H, self.model.H) or e.shape[0] != self.model.V:
+            raise DataError("trainer checkpoint: model shape mismatch")
+        if st["vocab"] != self.vocab:
+            raise DataError("trainer checkpoint: vocabulary mismatch")
+        self.epoch, self.eta, self.best_ppl = st["epoch"], st["eta"], st["best"]
+        self.bad_epochs, self.initial_ppl = st["bad"], st["initial"]
+        self.model.set_params(*st["params"])
+        self.model.set_opt(*st["opt"], cfg.rho, cfg.eps)
+        self.cursors = st["cursors"].copy()
+        self.hidden = st["hidden"].copy()

@@ -287,9 +287,9 @@ def check_config_echo(r: Reader, cfg):
 
 
 def write_trainer(cfg, epoch, eta, best, bad, initial, rng_text, cursors, hidden, params,
-                  vocab_words, opt_state) -> bytes:
-    """trainer.hpp:274-292."""
-    V, H = params[0].shape
+                  vocab_words, opt_state, model: str = "rnn") -> bytes:
+    """trainer.hpp:274-292.  model: "rnn" (Traits = StandardTraits: RNLM +
+    ROPT) or "bottleneck" (BottleneckTraits: RNBL + RBOP, compress.hpp:404-414)."""
     out = io.BytesIO()
     out.write(b"RTRN" + _u32(TRAINER_FORMAT_VERSION) + write_config_echo(cfg))
     out.write(_u32(epoch) + _f64(eta) + _f64(best) + _u32(bad) + _f64(initial))
@@ -297,13 +297,21 @@ def write_trainer(cfg, epoch, eta, best, bad, initial, rng_text, cursors, hidden
     out.write(_u64(len(cursors)))
     out.write(np.ascontiguousarray(cursors, "<u8").tobytes())
     out.write(np.ascontiguousarray(hidden, "<f4").tobytes())
-    out.write(write_params(params, vocab_words, cfg.act))
-    out.write(write_rmsprop(V, H, cfg.rho, cfg.eps, opt_state))
+    if model == "bottleneck":
+        V, P = params[0].shape
+        H = params[2].shape[0]
+        out.write(write_bottleneck(params, vocab_words, cfg.act))
+        out.write(write_bottleneck_opt(V, H, P, cfg.rho, cfg.eps, opt_state))
+    else:
+        V, H = params[0].shape
+        out.write(write_params(params, vocab_words, cfg.act))
+        out.write(write_rmsprop(V, H, cfg.rho, cfg.eps, opt_state))
     out.write(b"TEND")
     return out.getvalue()
 
 
-def read_trainer(data: bytes, cfg, n_streams: int, hidden_size: int, L: int):
+def read_trainer(data: bytes, cfg, n_streams: int, hidden_size: int, L: int,
+                 model: str = "rnn"):
     """trainer.hpp:300-336; returns a dict of the restored state."""
     r = Reader(data)
     r.magic("RTRN", "trainer checkpoint")
@@ -321,7 +329,11 @@ def read_trainer(data: bytes, cfg, n_streams: int, hidden_size: int, L: int):
         raise DataError("trainer checkpoint: cursor out of range")
     st["cursors"] = cur
     st["hidden"] = r.f32s(n * hidden_size).reshape(n, hidden_size)
-    st["params"], st["act"], st["vocab"] = read_params(r)
-    _, _, _, _, st["opt"] = read_rmsprop(r)
+    if model == "bottleneck":
+        st["params"], st["act"], st["vocab"] = read_bottleneck(r)
+        st["opt"] = read_bottleneck_opt(r)[5]
+    else:
+        st["params"], st["act"], st["vocab"] = read_params(r)
+        _, _, _, _, st["opt"] = read_rmsprop(r)
     r.magic("TEND", "trainer checkpoint trailer")
     return st

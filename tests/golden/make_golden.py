@@ -103,6 +103,29 @@ def write_bn(ref, out):
         np.savez_compressed(os.path.join(out, f"bn_{i}.npz"), **bn_case(ref, *args))
 
 
+def write_bn_train(ref, out):
+    """Trainer<BottleneckTraits> runs: the reference's own test case
+    (test_compress.cpp:427-460, cycle stream) and a random-stream one."""
+    cyc = lambda n: np.array([1, 3, 4, 5, 6, 2] * n, np.uint32)  # helpers.hpp:55-62
+    runs = {
+        "cycle": (7, 16, 8, cyc(200), cyc(40), 23,
+                  dict(nstate=16, nproj=8, noffset=2, minibatch=2, unroll=8, eta=0.02,
+                       mode=1, max_epochs=30, seed=5)),
+    }
+    tr, va = ref.random_stream_pair(91, 40, 616, 150)
+    runs["random"] = (40, 24, 8, tr[:600], va, 3,
+                      dict(nstate=24, nproj=8, noffset=2, minibatch=3, unroll=5, eta=0.005,
+                           mode=1, max_epochs=3, act=1))
+    for name, (V, H, P, tr, va, seed, kw) in runs.items():
+        params = ref.bn_init_uniform(V, H, P, seed)
+        cfg = oracle.TrainConfig(**kw)
+        blob, logs, ini = ref.bn_train_native(cfg, params, tr, va)
+        np.savez_compressed(os.path.join(out, f"bn_train_{name}.npz"), e=params[0], u=params[1],
+                            w_rec=params[2], d=params[3], train=tr, valid=va, logs=logs,
+                            initial=ini, rtrn=np.frombuffer(blob, np.uint8),
+                            cfg=np.array([repr(kw)]))
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -143,6 +166,7 @@ def main():
                         init_11=np.concatenate([a.ravel()[:16] for a in ref.init_uniform(7, 5, 11)]))
     write_nce(ref, out)
     write_bn(ref, out)
+    write_bn_train(ref, out)
     print("golden fixtures written to", out)
 
 

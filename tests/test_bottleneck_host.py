@@ -28,7 +28,7 @@ def test_init_uniform_matches_oracle(orc):
         bn_init_uniform(10, 4, 8, 1)
 
 
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_*.npz"))))
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_[0-9]*.npz"))))
 def test_rnbl_rbop_bytes_match_reference(path):
     from paper_1502_00512_b200 import formats, make_vocab
     g = np.load(path)

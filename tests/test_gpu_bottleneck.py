@@ -66,7 +66,7 @@ def test_bn_window_fp32_matches_oracle(orc, V, H, P, T, B, act, mask, clip):
         assert ok_, err
 
 
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_*.npz"))))
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_[0-9]*.npz"))))
 def test_bn_window_matches_reference_fixture(path):
     """Against the reference's own BottleneckAdapter window and update."""
     import paper_1502_00512_b200 as dl
@@ -189,3 +189,41 @@ def test_bn_training_windows_follow_oracle(orc, precision):
     if precision == "fp32":
         for a, b in zip(m.params(), cur):
             assert np.mean(np.abs(a - b)) < 1e-4 * np.mean(np.abs(b))
+
+
+@pytest.mark.parametrize("name", ["random", "cycle"])
+def test_bn_trainer_matches_reference_fixture(name):
+    """BottleneckTrainer (device windows, host schedule) against the
+    reference's Trainer<BottleneckTraits> epochs (tests/golden/bn_train_*),
+    then a checkpoint round trip that resumes bit-for-bit."""
+    import ast
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    g = np.load(os.path.join(GOLD, f"bn_train_{name}.npz"))
+    kw = ast.literal_eval(str(g["cfg"][0]))
+    cfg = dl.TrainConfig(**kw)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    V = params[0].shape[0]
+    t = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"])
+    t.train()
+    assert t.initial_ppl == pytest.approx(float(g["initial"]), rel=1e-5)
+    want = g["logs"]
+    if name == "random":
+        assert len(t.logs) == len(want)
+        for a, b in zip(t.logs, want):
+            assert a.train_loss == pytest.approx(b[1], rel=1e-4)
+            assert a.valid_ppl == pytest.approx(b[2], rel=1e-4)
+            assert a.eta == b[3]
+    else:
+        # the reference's own test (test_compress.cpp:427-446): 30 epochs on
+        # a deterministic cycle must drive validation perplexity below 1.3.
+        # (At eta 0.02 the first rmsprop steps move weights by ~eta each, so
+        # the trajectory is chaotic: summation-order differences already show
+        # in the first epoch, and the -ffp-contract=off reference build of
+        # the fixture stalls at 1.48 -- only the test's criterion is shared.)
+        assert t.best_ppl < 1.3
+    blob = t.save_checkpoint()
+    t2 = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"])
+    t2.load_checkpoint(blob)
+    assert t2.save_checkpoint() == blob
+    assert len(blob) == len(g["rtrn"])

@@ -255,7 +255,7 @@ def test_trainer_nce_vs_reference(orc, ref, k, floor, act, eta):
         assert np.array_equal(u, v)
 
 
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_*.npz"))))
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_[0-9]*.npz"))))
 def test_bottleneck_golden_bitexact(orc, path):
     """Bottleneck model (compress.hpp:38-415): window, bottleneck_update and
     sharded_perplexity of the C restatement equal the reference fixture."""
@@ -305,3 +305,35 @@ def test_bottleneck_random_configs_vs_reference(orc, ref, seed):
     assert not orc.bn_update(pa, state, bad, 0.9995, 1e-6, 0.05)[2]
     ids = orc.random_stream(seed, V, 300)
     assert orc.bn_sharded_ppl(pa, act, ids, 4) == ref.bn_sharded_ppl(pa, act, ids, 4)
+
+
+@pytest.mark.parametrize("name", ["cycle", "random"])
+def test_bottleneck_trainer_golden_bitexact(orc, name):
+    """Trainer<BottleneckTraits> restated (oracle bn_train) equals the
+    reference's epochs; the package's RTRN writer over the oracle's final
+    state reproduces the reference's checkpoint bytes (RNBL + RBOP)."""
+    import ast
+    from paper_1502_00512_b200 import formats, make_vocab
+    g = load(f"bn_train_{name}.npz")
+    kw = ast.literal_eval(str(g["cfg"][0]))
+    cfg = oracle.TrainConfig(**kw)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    r = orc.bn_train(cfg, params, g["train"], g["valid"])
+    assert r["initial_ppl"] == float(g["initial"])
+    cols = [0, 1, 2, 3, 6]
+    assert np.array_equal(r["logs"][:, cols], g["logs"][:, cols])
+    # the trainer's state after the last epoch (trainer.hpp:262-268): the
+    # logged eta is the one the epoch ran with; a non-improving epoch halves it
+    logs = r["logs"]
+    best_run, bad = float(g["initial"]), 0
+    for ppl in logs[:, 2]:
+        if ppl < best_run:
+            best_run, bad = ppl, 0
+        else:
+            bad += 1
+    eta = float(logs[-1, 3]) * (0.5 if bad else 1.0)
+    blob = formats.write_trainer(cfg, len(logs), eta, best_run, bad, float(g["initial"]),
+                                 formats.mt19937_64_text(cfg.seed), r["cursors"], r["hidden"],
+                                 r["params"], make_vocab(int(g["e"].shape[0])), r["opt"],
+                                 model="bottleneck")
+    assert blob == g["rtrn"].tobytes()
