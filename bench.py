@@ -52,6 +52,12 @@ CONFIGS = {
     # lock-step scoring step over S streams
     "c5": dict(V=64000, H=2048, T=1, B=1024, noffset=1, L=1 << 22, seed=5001, score=True,
                desc="perplexity scoring forward pass, hidden=2048, vocab=64K, 1024 streams"),
+    # the bottleneck / tied-embedding model (compress.hpp) at the C3 shape
+    # with a 512-wide projection: a step = one window through the C ABI
+    # (dl_bn_train_window), host window arrays copied in every step
+    "bn3": dict(V=64000, H=2048, P=512, T=16, B=128, noffset=8, L=1 << 22, seed=3001,
+                bottleneck=True,
+                desc="bottleneck RNNLM hidden=2048, projection=512, tied vocab=64K, 128 streams"),
 }
 
 
@@ -101,6 +107,93 @@ def run_scoring(args, cfg):
         "roofline": {"bound": "tensor", "kernel": "whole scoring step", "unit": "TFLOP/s",
                      "achieved": value * fpw / 1e12, "peak": peak,
                      "frac": value * fpw / 1e12 / peak, "traffic": None}}), flush=True)
+
+
+def run_bottleneck(args, cfg):
+    """Bottleneck model training words/s: bptt_run + bottleneck_update per
+    window through dl_bn_train_window (device-timed with CUDA events on the
+    library stream; each step copies its window in and its loss / h_final
+    out, so value and e2e coincide)."""
+    import torch
+
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    from paper_1502_00512_b200._lib import load
+    V, H, P, T, B = cfg["V"], cfg["H"], cfg["P"], cfg["T"], cfg["B"]
+    ids = synthetic_stream(cfg["seed"], V, cfg["L"])
+    rng = np.random.default_rng(7)
+    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                   for s in ((V, P), (P, H), (H, H), (H, P)))
+    model = bn.GpuBottleneck(V, H, P, 0, args.precision, 0)
+    model.set_params(*params)
+    TB = T * B
+    n = args.warmup + args.steps
+    wins = []
+    for i in range(n):
+        s0 = (i * TB * 7) % (len(ids) - TB - 2)
+        x = ids[s0:s0 + TB].reshape(T, B)
+        y = ids[s0 + 1:s0 + 1 + TB].reshape(T, B)
+        wins.append(dl.WindowBatch(x, y, (y != 1).astype(np.uint8)))
+    h = np.full((B, H), 0.5, np.float32)
+    stream = torch.cuda.ExternalStream(load().dl_bn_cuda_stream(model.handle))
+    eta = 1e-3
+    for wb in wins[: args.warmup]:
+        _, h, _ = bn.bn_train_window(model, wb, h, 1.0 / TB, 1.0, eta)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = model.launch_count()
+    loss = 0.0
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for wb in wins[args.warmup:]:
+            r, h, _ = bn.bn_train_window(model, wb, h, 1.0 / TB, 1.0, eta)
+            loss += r.loss
+        e1.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.25)
+    ms = e0.elapsed_time(e1)
+    launches = model.launch_count() - launches0
+    value = TB * args.steps / (ms / 1000.0)
+    # forward XU, Z (4PH), logits (2PV), recurrence (2H^2); backward dZ, gE
+    # (4PV), dh_out, gD, gU, din (8PH), recurrence + gRec (4H^2)
+    fpw = 6 * P * V + 6 * H * H + 12 * P * H
+    peak = PEAKS["bf16_tflops_sustained"]
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            import oracle
+            orc = oracle.Orc()
+            Bs = 1
+            t0 = time.perf_counter()
+            wb = wins[0]
+            r = orc.bn_bptt(params, 0, wb.inputs[:, :Bs], wb.targets[:, :Bs], wb.weights[:, :Bs],
+                            np.full((Bs, H), 0.5, np.float32), 1.0 / (T * Bs), 1.0)
+            st = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
+                  np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
+            orc.bn_update(params, st, r, 0.9995, 1e-6, eta)
+            dt = time.perf_counter() - t0
+            cpu = {"value": T * Bs / dt, "unit": "words/s", "cores": 1, "kind": "port",
+                   "sample": f"one window T={T} x B={Bs} stream (bptt_run + bottleneck_update) "
+                             f"at the full V/H/P, oracle C restatement, {dt:.1f} s"}
+        except Exception as ex:
+            cpu = {"value": None, "error": str(ex)[:200]}
+    print(json.dumps({
+        "metric": "training words/sec", "value": value, "unit": "words/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": "bn3", "desc": cfg["desc"], "V": V, "H": H, "P": P, "T": T,
+                   "B_per_gpu": B, "loss": "exact softmax", "model": "bottleneck (tied E)"},
+        "flops_per_word": fpw, "mean_window_loss": loss / args.steps, "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "tensor", "kernel": "whole window (GEMMs + recurrence + update)",
+                     "unit": "TFLOP/s", "achieved": value * fpw / 1e12, "peak": peak,
+                     "frac": value * fpw / 1e12 / peak, "traffic": None,
+                     "peak_kind": "measured sustained (MEASURED_PEAKS.json)"},
+        "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": TB * 9 + B * H * 4,
+                "d2h_bytes_per_step": B * H * 4 + 16,
+                "api": "dl_bn_train_window per step, host window arrays"},
+        "cpu_baseline": cpu}), flush=True)
 
 
 def synthetic_stream(seed: int, V: int, L: int) -> np.ndarray:
@@ -281,6 +374,9 @@ def main():
         return
     if cfg.get("score"):
         run_scoring(args, cfg)
+        return
+    if cfg.get("bottleneck"):
+        run_bottleneck(args, cfg)
         return
 
     import torch
