@@ -291,6 +291,34 @@ class _Backend:
         self._check(f(V, H, P, *p, *m, rho, eps, eta, *gs, C.byref(applied)))
         return tuple(p), tuple(m), bool(applied.value)
 
+    def _bn_nce_result(self, V, H, P, compute_grads, hf, loss, pos, ne, gew, ged, g):
+        r = dict(loss=loss.value, positions=pos.value, h_final=hf)
+        if compute_grads:
+            n = ne.value
+            dense = np.zeros((V, P), np.float32)
+            for s_ in range(n):
+                dense[gew[s_]] += ged[s_]
+            r.update(g_e_words=gew[:n].copy(), g_e_rows=ged[:n].copy(), g_e=dense, g_u=g[0],
+                     g_rec=g[1], g_d=g[2])
+        return r
+
+    def bn_update_sparse(self, params, state, grads, rho, eps, eta):
+        """bottleneck_update with the sparse embedding gradient (NCE mode)."""
+        p = [np.array(x, np.float32, copy=True) for x in params]
+        m = [np.array(x, np.float32, copy=True) for x in state]
+        V, P = p[0].shape
+        H = p[2].shape[0]
+        applied = C.c_int()
+        f = self._bn_fn("bn_update_sparse", [_i64, _i64, _i64] + [_f32p] * 8 +
+                        [C.c_double] * 3 + [_i64, _vp, _vp] + [_f32p] * 3 +
+                        [C.POINTER(C.c_int)])
+        words = np.ascontiguousarray(grads["g_e_words"], np.uint32)
+        rows = np.ascontiguousarray(grads["g_e_rows"], np.float32)
+        gs = [np.ascontiguousarray(grads[k], np.float32) for k in ("g_u", "g_rec", "g_d")]
+        self._check(f(V, H, P, *p, *m, rho, eps, eta, len(words), words.ctypes.data,
+                      rows.ctypes.data, *gs, C.byref(applied)))
+        return tuple(p), tuple(m), bool(applied.value)
+
     def bn_sharded_ppl(self, params, act, ids, shards, bos=1):
         e, u, w_rec, d = params
         V, P = e.shape
@@ -312,8 +340,6 @@ class _Backend:
         bn_bptt / bn_update / bn_sharded_ppl (a Python loop: small cases).
         Returns dict(logs [n x 7] (seconds / tokens_per_sec zero),
         initial_ppl, params, opt, cursors, hidden)."""
-        if cfg.mode != 1:
-            raise ValueError("bn_train: softmax mode only")
         e, u, w_rec, d = [np.array(x, np.float32, copy=True) for x in params]
         V, P = e.shape
         H = cfg.nstate
@@ -329,6 +355,14 @@ class _Backend:
         state = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
                  np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
         prm = (e, u, w_rec, d)
+        nce = cfg.mode == 0
+        if nce:
+            # NoiseModel::from_stream over the non-bos training tokens; the
+            # trainer's rng seeded with cfg.seed (trainer.hpp:184, 207-209)
+            counts = np.bincount(tr[tr != 1], minlength=V).astype(np.float64)
+            noise = self.noise_build(counts, cfg.nce_k, cfg.noise_floor) \
+                if hasattr(self, "noise_build") else None
+            st_rng = self.mt_state(cfg.seed)
 
         def validate():
             return self.bn_sharded_ppl(prm, cfg.act, va, cfg.valid_shards)["perplexity"]
@@ -346,11 +380,16 @@ class _Backend:
                     x = tr[pos % L]
                     y = tr[(pos + 1) % L]
                     w = (y != 1).astype(np.uint8)
-                    r = self.bn_bptt(prm, cfg.act, x, y, w, hidden[s0:s0 + B],
-                                     1.0 / (B * T), cfg.clip)
+                    if nce:
+                        r = self.bn_bptt_nce(prm, cfg.act, x, y, w, hidden[s0:s0 + B],
+                                             1.0 / (B * T), cfg.clip, noise, st_rng)
+                    else:
+                        r = self.bn_bptt(prm, cfg.act, x, y, w, hidden[s0:s0 + B],
+                                         1.0 / (B * T), cfg.clip)
                     loss_sum += r["loss"]
                     windows += 1
-                    prm, state, ok = self.bn_update(prm, state, r, cfg.rho, cfg.eps, eta)
+                    upd = self.bn_update_sparse if nce else self.bn_update
+                    prm, state, ok = upd(prm, state, r, cfg.rho, cfg.eps, eta)
                     skipped += 0 if ok else 1
                     hidden[s0:s0 + B] = r["h_final"]
                     cur[s0:s0 + B] += T
@@ -369,7 +408,7 @@ class _Backend:
                 bad += 1
                 eta *= 0.5
         return dict(logs=np.array(logs, np.float64), initial_ppl=initial, params=prm, opt=state,
-                    cursors=cur, hidden=hidden)
+                    cursors=cur, hidden=hidden, rng=st_rng if nce else self.mt_state(cfg.seed))
 
 
 class OracleError(RuntimeError):
@@ -472,6 +511,36 @@ class Orc(_Backend):
         self._check(f(len(noise["prob"]), noise["prob"].ctypes.data, noise["alias"].ctypes.data,
                       rng.ctypes.data, n, out.ctypes.data))
         return out
+
+    def bn_bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, noise,
+                    rng, compute_grads=True):
+        """bptt_run over the bottleneck adapter in NCE mode; rng advanced in place."""
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        T, B = inputs.shape
+        k = noise["k"]
+        hf = np.empty((B, H), np.float32)
+        ne = C.c_int64(0)
+        gew = np.zeros(T * B * (k + 2), np.uint32)
+        ged = np.zeros((T * B * (k + 2), P), np.float32)
+        g = [np.zeros(sh, np.float32) for sh in ((P, H), (H, H), (H, P))]
+        loss, pos = C.c_double(), C.c_uint64()
+        f = self.lib.orc_bn_bptt_nce
+        f.argtypes = [_i64, _i64, _i64, C.c_int] + [_f32p] * 4 + [_i64, _i64, _u32p, _u32p,
+                                                                   _u8p, _f32p, C.c_double,
+                                                                   C.c_float, C.c_int, C.c_int] + \
+            [_vp] * 11 + [C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._check(f(V, H, P, act, e, u, w_rec, d, T, B,
+                      np.ascontiguousarray(inputs, np.uint32),
+                      np.ascontiguousarray(targets, np.uint32),
+                      np.ascontiguousarray(weights, np.uint8),
+                      np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                      int(compute_grads), k, noise["ln_kq"].ctypes.data,
+                      noise["prob"].ctypes.data, noise["alias"].ctypes.data, rng.ctypes.data,
+                      hf.ctypes.data, C.addressof(ne), gew.ctypes.data, ged.ctypes.data,
+                      *(x.ctypes.data for x in g), C.byref(loss), C.byref(pos)))
+        return self._bn_nce_result(V, H, P, compute_grads, hf, loss, pos, ne, gew, ged, g)
 
     def bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, noise, rng,
                  compute_grads=True):
@@ -657,6 +726,36 @@ class Ref(_Backend):
         self._check(f(V, counts.ctypes.data, int(k), float(floor), rng.ctypes.data, n,
                       out.ctypes.data, lnkq.ctypes.data))
         return out, lnkq
+
+    def bn_bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, counts,
+                    k, floor, rng, compute_grads=True):
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        T, B = inputs.shape
+        counts = np.ascontiguousarray(counts, np.float64)
+        hf = np.empty((B, H), np.float32)
+        ne = C.c_int64(0)
+        gew = np.zeros(T * B * (k + 2), np.uint32)
+        ged = np.zeros((T * B * (k + 2), P), np.float32)
+        g = [np.zeros(sh, np.float32) for sh in ((P, H), (H, H), (H, P))]
+        loss, pos = C.c_double(), C.c_uint64()
+        f = self.lib.ref_bn_bptt_nce
+        f.argtypes = [_i64, _i64, _i64, C.c_int] + [_f32p] * 4 + [_i64, _i64, _u32p, _u32p,
+                                                                   _u8p, _f32p, C.c_double,
+                                                                   C.c_float, C.c_int, _vp,
+                                                                   C.c_int, C.c_double] + \
+            [_vp] * 8 + [C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._check(f(V, H, P, act, e, u, w_rec, d, T, B,
+                      np.ascontiguousarray(inputs, np.uint32),
+                      np.ascontiguousarray(targets, np.uint32),
+                      np.ascontiguousarray(weights, np.uint8),
+                      np.ascontiguousarray(h0, np.float32), loss_scale, clip,
+                      int(compute_grads), counts.ctypes.data, int(k), float(floor),
+                      rng.ctypes.data, hf.ctypes.data, C.addressof(ne), gew.ctypes.data,
+                      ged.ctypes.data, *(x.ctypes.data for x in g), C.byref(loss),
+                      C.byref(pos)))
+        return self._bn_nce_result(V, H, P, compute_grads, hf, loss, pos, ne, gew, ged, g)
 
     def bptt_nce(self, params, act, inputs, targets, weights, h0, loss_scale, clip, counts, k,
                  floor, rng, compute_grads=True):

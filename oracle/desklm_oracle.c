@@ -1175,3 +1175,165 @@ done:
   free(tgt);
   return rc;
 }
+
+/* NCE-mode window over the bottleneck adapter (backprop.hpp:126-156,
+ * 193-222; compress.hpp:204-225): scores float(dot_acc(z_b, E[w])), the
+ * embedding gradient as one SparseRowGrads in first-touch slot order over
+ * both sides (per step t: the output records, then the input rows) --
+ * g_e_words / g_e_data must hold T*B*(k+2) rows. */
+int orc_bn_bptt_nce(int64_t V, int64_t H, int64_t P, int act, const float* e, const float* u,
+                    const float* w_rec, const float* d, int64_t T, int64_t B,
+                    const uint32_t* inputs, const uint32_t* targets, const uint8_t* weights,
+                    const float* h0, double loss_scale, float clip, int compute_grads, int k,
+                    const double* ln_kq, const double* prob, const uint32_t* alias,
+                    uint64_t* rng, float* h_final, int64_t* g_e_rows, uint32_t* g_e_words,
+                    float* g_e_data, float* g_u, float* g_rec, float* g_d, double* loss,
+                    uint64_t* positions) {
+  if (T < 1 || B < 1 || k < 1 || P < 1 || P > H) return 1;
+  const int64_t BH = B * H, BP = B * P, K1 = k + 1;
+  orc_mt64 m;
+  mt_load(&m, rng);
+  float* h = (float*)malloc(sizeof(float) * (T + 1) * BH);
+  float* z = (float*)malloc(sizeof(float) * T * BP);
+  float* pre = (float*)malloc(sizeof(float) * BH);
+  float* eb = (float*)malloc(sizeof(float) * BP);
+  double* acc = (double*)malloc(sizeof(double) * (V > H ? V : H));
+  uint32_t* rw = (uint32_t*)malloc(sizeof(uint32_t) * T * B * K1);
+  float* rds = (float*)malloc(sizeof(float) * T * B * K1);
+  int* has = (int*)calloc((size_t)(T * B), sizeof(int));
+  memcpy(h, h0, sizeof(float) * BH);
+  for (int64_t t = 0; t < T; ++t) {
+    matmul_nt(h + t * BH, w_rec, pre, B, H, H);
+    bn_input_forward(e, u, H, P, inputs + t * B, B, eb, pre, acc);
+    for (int64_t i = 0; i < BH; ++i) h[(t + 1) * BH + i] = act_f(act, pre[i]);
+    matmul_nn(h + (t + 1) * BH, d, z + t * BP, B, P, H, 0, acc);
+  }
+  if (h_final) memcpy(h_final, h + T * BH, sizeof(float) * BH);
+  double L = 0.0;
+  uint64_t pos = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    const float* zt = z + t * BP;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t idx = t * B + b;
+      if (!weights[idx]) continue;
+      ++pos;
+      has[idx] = 1;
+      const uint32_t y = targets[idx];
+      const double st = (double)(float)dot_acc(zt + b * P, e + (int64_t)y * P, P);
+      const double at = st - ln_kq[y];
+      L += loss_scale * softplus(-at);
+      rw[idx * K1] = y;
+      rds[idx * K1] = (float)(-loss_scale * sigmoid(-at));
+      for (int j = 0; j < k; ++j) {
+        const uint32_t w = alias_sample(&m, V, prob, alias);
+        const double s = (double)(float)dot_acc(zt + b * P, e + (int64_t)w * P, P);
+        const double a = s - ln_kq[w];
+        L += loss_scale * softplus(a);
+        rw[idx * K1 + 1 + j] = w;
+        rds[idx * K1 + 1 + j] = (float)(loss_scale * sigmoid(a));
+      }
+    }
+  }
+  mt_store(&m, rng);
+  *loss = L;
+  *positions = pos;
+  if (compute_grads) {
+    float* dh = (float*)calloc((size_t)BH, sizeof(float));
+    float* dpre = (float*)malloc(sizeof(float) * BH);
+    float* dz = (float*)malloc(sizeof(float) * BP);
+    float* din = (float*)malloc(sizeof(float) * BP);
+    int32_t* slot = (int32_t*)malloc(sizeof(int32_t) * V);
+    for (int64_t w = 0; w < V; ++w) slot[w] = -1;
+    int64_t ne = 0;
+#define BN_ROW(w_)                                                     \
+  do {                                                                 \
+    if (slot[(w_)] < 0) {                                              \
+      slot[(w_)] = (int32_t)ne;                                        \
+      g_e_words[ne] = (w_);                                            \
+      memset(g_e_data + ne * P, 0, sizeof(float) * P);                 \
+      ++ne;                                                            \
+    }                                                                  \
+  } while (0)
+    memset(g_u, 0, sizeof(float) * P * H);
+    memset(g_rec, 0, sizeof(float) * H * H);
+    memset(g_d, 0, sizeof(float) * H * P);
+    for (int64_t t = T - 1; t >= 0; --t) {
+      const float* ht1 = h + (t + 1) * BH;
+      const float* zt = z + t * BP;
+      memset(dz, 0, sizeof(float) * BP);
+      /* score_backward per record (compress.hpp:209-219) */
+      for (int64_t b = 0; b < B; ++b) {
+        const int64_t idx = t * B + b;
+        if (!has[idx]) continue;
+        for (int64_t r = 0; r < K1; ++r) {
+          const uint32_t w = rw[idx * K1 + r];
+          const float ds = rds[idx * K1 + r];
+          const float* er = e + (int64_t)w * P;
+          float* db = dz + b * P;
+          for (int64_t i = 0; i < P; ++i) db[i] += ds * er[i];
+          BN_ROW(w);
+          float* gr = g_e_data + (int64_t)slot[w] * P;
+          const float* zb = zt + b * P;
+          for (int64_t i = 0; i < P; ++i) gr[i] += ds * zb[i];
+        }
+      }
+      /* out_end (compress.hpp:221-225) */
+      for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < H; ++i)
+          dh[b * H + i] = (float)((double)dh[b * H + i] + dot_acc(dz + b * P, d + i * P, P));
+      matmul_tn_add(ht1, dz, g_d, B, H, P);
+      for (int64_t i = 0; i < BH; ++i) dpre[i] = dh[i] * act_deriv_f(act, ht1[i]);
+      matmul_tn_add(dpre, h + t * BH, g_rec, B, H, H);
+      const uint32_t* words = inputs + t * B;
+      for (int64_t b = 0; b < B; ++b)
+        memcpy(eb + b * P, e + (int64_t)words[b] * P, sizeof(float) * P);
+      matmul_tn_add(eb, dpre, g_u, B, P, H);
+      matmul_nt(dpre, u, din, B, P, H);
+      for (int64_t b = 0; b < B; ++b) {
+        BN_ROW(words[b]);
+        float* gr = g_e_data + (int64_t)slot[words[b]] * P;
+        for (int64_t i = 0; i < P; ++i) gr[i] += 1.0f * din[b * P + i];
+      }
+      if (t > 0) matmul_nn(dpre, w_rec, dh, B, H, H, 0, acc);
+    }
+#undef BN_ROW
+    *g_e_rows = ne;
+    for (int64_t i = 0; i < ne * P; ++i) g_e_data[i] = clip1(g_e_data[i], clip);
+    for (int64_t i = 0; i < P * H; ++i) g_u[i] = clip1(g_u[i], clip);
+    for (int64_t i = 0; i < H * H; ++i) g_rec[i] = clip1(g_rec[i], clip);
+    for (int64_t i = 0; i < H * P; ++i) g_d[i] = clip1(g_d[i], clip);
+    free(dh);
+    free(dpre);
+    free(dz);
+    free(din);
+    free(slot);
+  }
+  free(h);
+  free(z);
+  free(pre);
+  free(eb);
+  free(acc);
+  free(rw);
+  free(rds);
+  free(has);
+  return 0;
+}
+
+/* bottleneck_update with a sparse embedding gradient (compress.hpp:303-304). */
+int orc_bn_update_sparse(int64_t V, int64_t H, int64_t P, float* e, float* u, float* w_rec,
+                         float* d, float* m_e, float* m_u, float* m_rec, float* m_d, double rho,
+                         double eps, double eta, int64_t n_rows, const uint32_t* words,
+                         const float* rows, const float* g_u, const float* g_rec,
+                         const float* g_d, int* applied) {
+  if (!(all_finite(rows, n_rows * P) && all_finite(g_u, P * H) && all_finite(g_rec, H * H) &&
+        all_finite(g_d, H * P))) {
+    *applied = 0;
+    return 0;
+  }
+  update_rows_sparse(e, P, n_rows, words, rows, m_e, V, rho, eps, eta);
+  rms_elem(u, g_u, m_u, P * H, rho, eps, eta);
+  rms_elem(w_rec, g_rec, m_rec, H * H, rho, eps, eta);
+  rms_elem(d, g_d, m_d, H * P, rho, eps, eta);
+  *applied = 1;
+  return 0;
+}

@@ -701,4 +701,87 @@ int ref_bn_write(std::int64_t V, std::int64_t H, std::int64_t P, int act, const 
   });
 }
 
+// bptt_run(BottleneckAdapter) in NCE mode; the sparse embedding gradient in
+// SparseRowGrads slot order (g_e_words / g_e_data hold T*B*(k+2) rows).
+int ref_bn_bptt_nce(std::int64_t V, std::int64_t H, std::int64_t P, int act, const float* e,
+                    const float* u, const float* w_rec, const float* d, std::int64_t T,
+                    std::int64_t B, const std::uint32_t* inputs, const std::uint32_t* targets,
+                    const std::uint8_t* weights, const float* h0, double loss_scale, float clip,
+                    int compute_grads, const double* counts, int k, double floor,
+                    std::uint64_t* rng, float* h_final, std::int64_t* g_e_rows,
+                    std::uint32_t* g_e_words, float* g_e_data, float* g_u, float* g_rec,
+                    float* g_d, double* loss, std::uint64_t* positions) {
+  return guarded([&] {
+    const BottleneckParams<float> p = make_bn(V, H, P, act, e, u, w_rec, d);
+    WindowBatch wb;
+    wb.resize(T, B);
+    std::memcpy(wb.inputs.data(), inputs, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.targets.data(), targets, sizeof(std::uint32_t) * T * B);
+    std::memcpy(wb.weights.data(), weights, T * B);
+    Mat<float> h0m(B, H);
+    std::memcpy(h0m.a.data(), h0, sizeof(float) * B * H);
+    BottleneckAdapter<float> a(p);
+    NoiseModel nm(std::vector<double>(counts, counts + V), k, floor);
+    std::mt19937_64 r = rng_from(rng);
+    BpttOptions<float> opt;
+    opt.mode = LossMode::kNce;
+    opt.noise = &nm;
+    opt.rng = &r;
+    opt.loss_scale = loss_scale;
+    opt.clip = clip;
+    opt.compute_grads = compute_grads != 0;
+    BottleneckGrads<float> g;
+    Mat<float> hf;
+    const BpttResult res = bptt_run(a, wb, h0m, compute_grads ? &g : nullptr,
+                                    h_final ? &hf : nullptr, opt);
+    rng_to(r, rng);
+    *loss = res.loss;
+    *positions = res.positions;
+    if (h_final) std::memcpy(h_final, hf.a.data(), sizeof(float) * B * H);
+    if (compute_grads) {
+      *g_e_rows = static_cast<std::int64_t>(g.e_sp.rows());
+      for (std::size_t s2 = 0; s2 < g.e_sp.rows(); ++s2) g_e_words[s2] = g.e_sp.words[s2];
+      std::memcpy(g_e_data, g.e_sp.data.data(), sizeof(float) * g.e_sp.data.size());
+      std::memcpy(g_u, g.u.a.data(), sizeof(float) * P * H);
+      std::memcpy(g_rec, g.w_rec.a.data(), sizeof(float) * H * H);
+      std::memcpy(g_d, g.d.a.data(), sizeof(float) * H * P);
+    }
+  });
+}
+
+// bottleneck_update with a sparse embedding gradient.
+int ref_bn_update_sparse(std::int64_t V, std::int64_t H, std::int64_t P, float* e, float* u,
+                         float* w_rec, float* d, float* m_e, float* m_u, float* m_rec,
+                         float* m_d, double rho, double eps, double eta, std::int64_t n_rows,
+                         const std::uint32_t* words, const float* rows, const float* g_u,
+                         const float* g_rec, const float* g_d, int* applied) {
+  return guarded([&] {
+    BottleneckParams<float> p = make_bn(V, H, P, 0, e, u, w_rec, d);
+    BottleneckOptState s(V, H, P, rho, eps);
+    std::memcpy(s.m_e.data(), m_e, sizeof(float) * V);
+    std::memcpy(s.m_u.a.data(), m_u, sizeof(float) * P * H);
+    std::memcpy(s.m_rec.a.data(), m_rec, sizeof(float) * H * H);
+    std::memcpy(s.m_d.a.data(), m_d, sizeof(float) * H * P);
+    BottleneckGrads<float> g;
+    g.e_is_dense = false;
+    g.e_sp.reset(P);
+    for (std::int64_t i = 0; i < n_rows; ++i) g.e_sp.axpy_row(words[i], 1.0f, rows + i * P);
+    g.u = Mat<float>(P, H);
+    g.w_rec = Mat<float>(H, H);
+    g.d = Mat<float>(H, P);
+    std::memcpy(g.u.a.data(), g_u, sizeof(float) * P * H);
+    std::memcpy(g.w_rec.a.data(), g_rec, sizeof(float) * H * H);
+    std::memcpy(g.d.a.data(), g_d, sizeof(float) * H * P);
+    *applied = bottleneck_update(p, g, s, eta) ? 1 : 0;
+    std::memcpy(e, p.e.a.data(), sizeof(float) * V * P);
+    std::memcpy(u, p.u.a.data(), sizeof(float) * P * H);
+    std::memcpy(w_rec, p.w_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(d, p.d.a.data(), sizeof(float) * H * P);
+    std::memcpy(m_e, s.m_e.data(), sizeof(float) * V);
+    std::memcpy(m_u, s.m_u.a.data(), sizeof(float) * P * H);
+    std::memcpy(m_rec, s.m_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(m_d, s.m_d.a.data(), sizeof(float) * H * P);
+  });
+}
+
 }  // extern "C"

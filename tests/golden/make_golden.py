@@ -126,6 +126,48 @@ def write_bn_train(ref, out):
                             cfg=np.array([repr(kw)]))
 
 
+def bn_nce_case(ref, V, H, P, T, B, k, floor, act, seed):
+    """Bottleneck model in NCE mode: one window (draws from a seeded
+    mt19937_64) and the sparse-embedding bottleneck_update."""
+    rng = np.random.default_rng(seed)
+    params = ref.bn_init_uniform(V, H, P, seed + 1)
+    counts = rng.integers(0, 40, V).astype(np.float64)
+    counts[1] = 0
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(2, V, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) >= 0.15).astype(np.uint8)
+    h0 = rng.uniform(-0.5, 0.5, (B, H)).astype(np.float32)
+    st0 = ref.mt_state(seed + 7)
+    st = st0.copy()
+    r = ref.bn_bptt_nce(params, act, x, y, w, h0, 1.0 / (T * B), 1.0, counts, k, floor, st)
+    state = (rng.uniform(0, 0.01, V).astype(np.float32),
+             rng.uniform(0, 0.01, (P, H)).astype(np.float32),
+             rng.uniform(0, 0.01, (H, H)).astype(np.float32),
+             rng.uniform(0, 0.01, (H, P)).astype(np.float32))
+    p2, s2, applied = ref.bn_update_sparse(params, state, r, 0.9995, 1e-6, 0.05)
+    return dict(V=V, H=H, P=P, T=T, B=B, k=k, floor=floor, act=act, e=params[0], u=params[1],
+                w_rec=params[2], d=params[3], counts=counts, x=x, y=y, w=w, h0=h0, rng0=st0,
+                rng1=st, loss=r["loss"], positions=r["positions"], h_final=r["h_final"],
+                g_e_words=r["g_e_words"], g_e_rows=r["g_e_rows"], g_u=r["g_u"], g_rec=r["g_rec"],
+                g_d=r["g_d"], m_e=state[0], m_u=state[1], m_rec=state[2], m_d=state[3],
+                u_e=p2[0], u_u=p2[1], u_w_rec=p2[2], u_d=p2[3], u_m_e=s2[0], u_m_u=s2[1],
+                u_m_rec=s2[2], u_m_d=s2[3], applied=applied)
+
+
+def write_bn_nce(ref, out):
+    for i, args in enumerate([(60, 16, 8, 5, 4, 5, 1e-3, 0, 501),
+                              (300, 32, 16, 6, 8, 16, 1e-8, 1, 533)]):
+        np.savez_compressed(os.path.join(out, f"bn_nce_{i}.npz"), **bn_nce_case(ref, *args))
+    tr, va = ref.random_stream_pair(77, 40, 616, 150)
+    kw = dict(nstate=16, nproj=8, noffset=2, minibatch=2, unroll=5, eta=0.05, mode=0, nce_k=7,
+              noise_floor=1e-3, max_epochs=3, divergence_factor=1e9)
+    params = ref.bn_init_uniform(40, 16, 8, 3)
+    blob, logs, ini = ref.bn_train_native(oracle.TrainConfig(**kw), params, tr[:600], va)
+    np.savez_compressed(os.path.join(out, "bn_train_nce.npz"), e=params[0], u=params[1],
+                        w_rec=params[2], d=params[3], train=tr[:600], valid=va, logs=logs,
+                        initial=ini, rtrn=np.frombuffer(blob, np.uint8), cfg=np.array([repr(kw)]))
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -167,6 +209,7 @@ def main():
     write_nce(ref, out)
     write_bn(ref, out)
     write_bn_train(ref, out)
+    write_bn_nce(ref, out)
     print("golden fixtures written to", out)
 
 

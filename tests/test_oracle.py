@@ -337,3 +337,55 @@ def test_bottleneck_trainer_golden_bitexact(orc, name):
                                  r["params"], make_vocab(int(g["e"].shape[0])), r["opt"],
                                  model="bottleneck")
     assert blob == g["rtrn"].tobytes()
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_nce_*.npz"))))
+def test_bottleneck_nce_golden_bitexact(orc, path):
+    """Bottleneck model, NCE mode: draws, loss, the sparse embedding rows in
+    slot order and the sparse-embedding bottleneck_update equal the
+    reference fixture."""
+    g = np.load(path)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    T, B = g["x"].shape
+    noise = orc.noise_build(g["counts"], int(g["k"]), float(g["floor"]))
+    st = g["rng0"].copy()
+    r = orc.bn_bptt_nce(params, int(g["act"]), g["x"], g["y"], g["w"], g["h0"], 1.0 / (T * B),
+                        1.0, noise, st)
+    assert np.array_equal(st, g["rng1"])
+    assert r["loss"] == float(g["loss"]) and r["positions"] == int(g["positions"])
+    for key in ("h_final", "g_e_words", "g_e_rows", "g_u", "g_rec", "g_d"):
+        assert np.array_equal(r[key], g[key]), key
+    state = (g["m_e"], g["m_u"], g["m_rec"], g["m_d"])
+    p2, s2, ok = orc.bn_update_sparse(params, state, r, 0.9995, 1e-6, 0.05)
+    assert ok == bool(g["applied"])
+    for a, key in zip(p2 + s2, ("u_e", "u_u", "u_w_rec", "u_d", "u_m_e", "u_m_u", "u_m_rec",
+                                "u_m_d")):
+        assert np.array_equal(a, g[key]), key
+
+
+def test_bottleneck_trainer_nce_golden(orc):
+    """Trainer<BottleneckTraits> in its default NCE mode: epochs and the
+    RTRN checkpoint (generator state included) equal the reference's."""
+    import ast
+    from paper_1502_00512_b200 import formats, make_vocab
+    g = load("bn_train_nce.npz")
+    kw = ast.literal_eval(str(g["cfg"][0]))
+    cfg = oracle.TrainConfig(**kw)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    r = orc.bn_train(cfg, params, g["train"], g["valid"])
+    cols = [0, 1, 2, 3, 6]
+    assert r["initial_ppl"] == float(g["initial"])
+    assert np.array_equal(r["logs"][:, cols], g["logs"][:, cols])
+    logs = r["logs"]
+    best, bad = float(g["initial"]), 0
+    for ppl in logs[:, 2]:
+        if ppl < best:
+            best, bad = ppl, 0
+        else:
+            bad += 1
+    eta = float(logs[-1, 3]) * (0.5 if bad else 1.0)
+    rng_text = " ".join(str(int(v)) for v in r["rng"])
+    blob = formats.write_trainer(cfg, len(logs), eta, best, bad, float(g["initial"]), rng_text,
+                                 r["cursors"], r["hidden"], r["params"],
+                                 make_vocab(int(g["e"].shape[0])), r["opt"], model="bottleneck")
+    assert blob == g["rtrn"].tobytes()
