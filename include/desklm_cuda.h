@@ -301,6 +301,14 @@ int dl_bn_train_window(dl_bn* ctx, int64_t T, int64_t B, const uint32_t* inputs,
 int dl_bn_sharded_perplexity(dl_bn* ctx, const uint32_t* ids, int64_t n, int shards,
                              uint32_t bos, double* total_logprob, uint64_t* predicted,
                              double* perplexity);
+/* NCE mode (LossMode::kNce) for the bottleneck model: as dl_set_loss_mode /
+ * dl_set_noise / dl_{set,get}_rng_state of the standard model (the noise
+ * model over E, sparse embedding gradient; backprop.hpp:126-156,
+ * compress.hpp:204-225). */
+int dl_bn_set_loss_mode(dl_bn* ctx, int mode);
+int dl_bn_set_noise(dl_bn* ctx, const double* counts, int64_t V, int k, double floor);
+int dl_bn_set_rng_state(dl_bn* ctx, const uint64_t state[313]);
+int dl_bn_get_rng_state(const dl_bn* ctx, uint64_t state[313]);
 uint64_t dl_bn_launch_count(const dl_bn* ctx);
 void* dl_bn_cuda_stream(const dl_bn* ctx);
 

@@ -132,6 +132,25 @@ class GpuBottleneck:
     def launch_count(self) -> int:
         return int(load().dl_bn_launch_count(self._h))
 
+    # ---- NCE mode (the reference Trainer's default loss)
+    def set_loss_mode(self, mode: int):
+        """0 = NCE (LossMode::kNce), 1 = exact softmax."""
+        self._chk(load().dl_bn_set_loss_mode(self._h, int(mode)))
+
+    def set_noise(self, counts, k: int, floor: float = 1e-8):
+        """NoiseModel over the vocabulary (nce.hpp:41-66) + AliasSampler."""
+        c = np.ascontiguousarray(counts, np.float64)
+        self._chk(load().dl_bn_set_noise(self._h, c.ctypes.data, len(c), int(k), float(floor)))
+
+    def set_rng_state(self, state):
+        st = np.ascontiguousarray(state, np.uint64)
+        self._chk(load().dl_bn_set_rng_state(self._h, st.ctypes.data))
+
+    def rng_state(self):
+        st = np.zeros(313, np.uint64)
+        self._chk(load().dl_bn_get_rng_state(self._h, st.ctypes.data))
+        return st
+
 
 def check_bn(rc, h):
     if rc == 0:
@@ -204,7 +223,7 @@ def bn_sharded_perplexity(model: GpuBottleneck, ids, shards: int, bos_id: int = 
 
 class BottleneckTrainer:
     """Trainer<BottleneckTraits> (trainer.hpp:171-476 over compress.hpp:389-415),
-    softmax mode.  The host keeps the reference's schedule -- offset-stream
+    softmax (mode 1) or NCE (mode 0, the reference default).  The host keeps the reference's schedule -- offset-stream
     cursors floor(i*L/N), window (r, g) positions cursor + t, bos-masked
     targets, hidden carry and wrap reset (trainer.hpp:350-410) -- and every
     window runs on the device as one dl_bn_train_window call (bptt_run +
@@ -215,9 +234,6 @@ class BottleneckTrainer:
                  device: int = 0):
         from . import BOS_ID, EpochLog  # noqa: F401
         cfg.validate()
-        if cfg.mode != 1:
-            raise ValueError("bottleneck trainer: only the softmax loss (mode 1) runs on the "
-                             "device for the bottleneck model")
         self.cfg = cfg
         self.vocab = list(vocab_words)
         e, u, w_rec, d = (np.asarray(x, np.float32) for x in params)
@@ -241,6 +257,15 @@ class BottleneckTrainer:
         self.model = GpuBottleneck(V, H, P, cfg.act, precision, device)
         self.model.set_params(e, u, w_rec, d)
         self.model.set_opt(None, None, None, None, cfg.rho, cfg.eps)
+        if cfg.mode == 0:
+            # NoiseModel::from_stream over the non-bos training tokens and the
+            # trainer's rng seeded with cfg.seed (trainer.hpp:184, 207-209)
+            from . import rng_seed_state
+            ids = self.train_ids
+            counts = np.bincount(ids[ids != 1], minlength=V).astype(np.float64)
+            self.model.set_loss_mode(0)
+            self.model.set_noise(counts, cfg.nce_k, cfg.noise_floor)
+            self.model.set_rng_state(rng_seed_state(cfg.seed))
         self.cursors = np.array([i * L // N for i in range(N)], np.int64)
         self.a0 = np.float32(0.5 if cfg.act == 0 else 0.0)
         self.hidden = np.full((N, H), self.a0, np.float32)
@@ -296,9 +321,10 @@ class BottleneckTrainer:
     # ---- checkpointing (RTRN with RNBL / RBOP)
     def save_checkpoint(self) -> bytes:
         from . import formats
+        rng_text = " ".join(str(int(v)) for v in self.model.rng_state()) \
+            if self.cfg.mode == 0 else formats.mt19937_64_text(self.cfg.seed)
         return formats.write_trainer(self.cfg, self.epoch, self.eta, self.best_ppl,
-                                     self.bad_epochs, self.initial_ppl,
-                                     formats.mt19937_64_text(self.cfg.seed), self.cursors,
+                                     self.bad_epochs, self.initial_ppl, rng_text, self.cursors,
                                      self.hidden, self.model.params(), self.vocab,
                                      self.model.opt(), model="bottleneck")
 
@@ -318,3 +344,8 @@ class BottleneckTrainer:
         self.model.set_opt(*st["opt"], cfg.rho, cfg.eps)
         self.cursors = st["cursors"].copy()
         self.hidden = st["hidden"].copy()
+        if cfg.mode == 0:
+            words = st["rng_text"].split()
+            if len(words) != 313:
+                raise DataError("trainer checkpoint: bad rng state")
+            self.model.set_rng_state(np.array([int(v) for v in words], np.uint64))

@@ -20,6 +20,15 @@
 //   update    bottleneck_update (compress.hpp:296-309): E dense rows (one
 //             accumulator per word), U / W_rec / D per element
 //
+// NCE mode (LossMode::kNce, the reference Trainer's default): the same
+// window with the output side replaced by the engine's NCE kernels (nce.cu)
+// over z and E: host-drawn reference noise (mt19937_64 + AliasSampler),
+// 8-lane double scores float(z_b . E[w]), dz from the records, and a sparse
+// embedding gradient -- the output records' rows plus the input rows, each
+// summed per word in the reference's processing order -- applied with the
+// sparse row update (rmsprop.hpp:77-92: every accumulator decays, touched
+// rows step).
+//
 // The GEMMs are the engine's: tcgen05 (bf16 operands, fp32 accumulate) in
 // the BF16 mode, the fp32 SIMT kernel in the parity mode.  All buffers are
 // device resident; host arrays are only read/written by the C ABI calls.
@@ -27,6 +36,8 @@
 #include <cfloat>
 #include <cmath>
 #include <cstring>
+#include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -85,6 +96,28 @@ struct dl_bn {
   float* splitws = nullptr;
   size_t split_cap = 0;
   unsigned* bar_counter = nullptr;
+  // NCE mode
+  int loss_mode = 1;  // 1 softmax, 0 NCE
+  int nce_k = 0;
+  std::vector<double> nz_prob;
+  double *ln_kq_d = nullptr, *nz_prob_d = nullptr;
+  uint32_t* nz_alias_d = nullptr;
+  std::mt19937_64 rng{1};
+  int64_t nce_cap = 0, nce_P = 0, nce_N = 0;
+  unsigned long long* raw_d = nullptr;
+  std::vector<unsigned long long> raw_h;
+  uint32_t *pos_of_d = nullptr, *rec_word = nullptr, *rec_row = nullptr, *proc_r = nullptr;
+  int* first_d = nullptr;
+  float *score = nullptr, *ds = nullptr, *nce_scale = nullptr, *out_rows = nullptr;
+  double* loss_pos = nullptr;
+  uint32_t *keys_in = nullptr, *vals_in = nullptr, *keys_out = nullptr, *vals_out = nullptr;
+  uint32_t* out_words = nullptr;
+  int *head = nullptr, *slot = nullptr, *out_n = nullptr;
+  void* sort_temp = nullptr;
+  size_t sort_temp_bytes = 0;
+  EmbedWs nce_ws{};
+  uint8_t* touched = nullptr;  // [V] rows of the sparse embedding gradient
+  bool e_sparse = false;       // the last window's embedding gradient is sparse
 };
 
 namespace {
@@ -150,12 +183,47 @@ __global__ void k_iota(uint32_t* x, int64_t n) {
 // gE[words[s]] += rows[s] for the window's distinct input words (each word
 // once, so no two slots touch the same row)
 __global__ void k_add_rows(const float* __restrict__ rows, const uint32_t* __restrict__ words,
-                           const int* __restrict__ n_seg, int64_t P, float* __restrict__ dense) {
+                           const int* __restrict__ n_seg, int64_t P, float* __restrict__ dense,
+                           uint8_t* __restrict__ touched) {
   const int slot = blockIdx.x;
   if (slot >= *n_seg) return;
+  if (touched && threadIdx.x == 0) touched[words[slot]] = 1;
   float* dst = dense + (int64_t)words[slot] * P;
   const float* src = rows + (int64_t)slot * P;
   for (int64_t j = threadIdx.x; j < P; j += blockDim.x) dst[j] += src[j];
+}
+
+// update_rows_sparse (rmsprop.hpp:77-92) over a dense gradient with a
+// touched-row mask: every accumulator decays, m = float(rho m); a touched
+// row then takes m += float((1-rho) mean_sq) and w -= float(eta g / sqrt(m +
+// eps)).  One warp per row; skipped entirely on a non-finite gradient.
+__global__ void k_rms_rows_masked(float* __restrict__ w, bf16* __restrict__ wb,
+                                  float* __restrict__ m, const float* __restrict__ g,
+                                  const uint8_t* __restrict__ touched, int64_t V, int64_t P,
+                                  double rho, double eps, double eta,
+                                  const int* __restrict__ nonfinite) {
+  if (*nonfinite) return;
+  const int lane = threadIdx.x % 32;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < V; r += nw) {
+    float mr = (float)(rho * (double)m[r]);
+    if (touched[r]) {
+      const float* gr = g + r * P;
+      double sq = 0.0;
+      for (int64_t i = lane; i < P; i += 32) sq += (double)gr[i] * (double)gr[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      mr = mr + (float)((1.0 - rho) * (sq / (double)P));
+      const double denom = sqrt((double)mr + eps), inv = 1.0 / denom;
+      float* wr = w + r * P;
+      for (int64_t i = lane; i < P; i += 32) {
+        const float v = wr[i] - rms_step(eta, gr[i], denom, inv);
+        wr[i] = v;
+        if (wb) wb[r * P + i] = __float2bfloat16_rn(v);
+      }
+    }
+    if (lane == 0) m[r] = mr;
+  }
 }
 
 unsigned grid_n(int64_t n) {
@@ -254,6 +322,10 @@ void ensure_window(dl_bn* c, int64_t T, int64_t N) {
   c->in_rows = bn_alloc<float>(n * P);
   c->in_words = bn_alloc<uint32_t>(n);
   c->in_n = bn_alloc<int>(1);
+  bn_free(c->pos_of_d);
+  bn_free(c->first_d);
+  c->pos_of_d = bn_alloc<uint32_t>(n);
+  c->first_d = bn_alloc<int>(t + 1);
   if (tcm(c)) {
     c->htape_bf = bn_alloc<bf16>((n + n) * H);
     c->eg_bf = bn_alloc<bf16>(n * P);
@@ -269,6 +341,46 @@ void ensure_window(dl_bn* c, int64_t T, int64_t N) {
   k_iota<<<grid_n(n), 256, 0, c->st>>>(c->iota, n);
   c->capN = n;
   c->capT = t;
+}
+
+// NCE record buffers for up to N = T*B*(k+1) records
+void nce_reserve(dl_bn* c, int64_t N) {
+  if (N <= c->nce_cap) return;
+  DL_CUDA(cudaStreamSynchronize(c->st));
+  for (void** p : {(void**)&c->rec_word, (void**)&c->rec_row, (void**)&c->proc_r,
+                   (void**)&c->score, (void**)&c->ds, (void**)&c->nce_scale, (void**)&c->loss_pos,
+                   (void**)&c->keys_in, (void**)&c->vals_in, (void**)&c->keys_out,
+                   (void**)&c->vals_out, (void**)&c->head, (void**)&c->slot, &c->sort_temp,
+                   (void**)&c->nce_ws.seg_start, (void**)&c->nce_ws.order_pos,
+                   (void**)&c->out_rows, (void**)&c->out_words, (void**)&c->out_n,
+                   (void**)&c->raw_d})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+  c->rec_word = bn_alloc<uint32_t>(N);
+  c->rec_row = bn_alloc<uint32_t>(N);
+  c->proc_r = bn_alloc<uint32_t>(N);
+  c->score = bn_alloc<float>(N);
+  c->ds = bn_alloc<float>(N);
+  c->nce_scale = bn_alloc<float>(N);
+  c->loss_pos = bn_alloc<double>(N);
+  c->keys_in = bn_alloc<uint32_t>(N);
+  c->vals_in = bn_alloc<uint32_t>(N);
+  c->keys_out = bn_alloc<uint32_t>(N);
+  c->vals_out = bn_alloc<uint32_t>(N);
+  c->head = bn_alloc<int>(N);
+  c->slot = bn_alloc<int>(N);
+  c->sort_temp_bytes = nce_sort_temp_bytes(N);
+  c->sort_temp = bn_alloc<uint8_t>(c->sort_temp_bytes);
+  c->nce_ws.seg_start = bn_alloc<int>(2 * N + 2);
+  c->nce_ws.order_pos = bn_alloc<int>(N);
+  c->nce_ws.cap = N;
+  c->out_rows = bn_alloc<float>(N * c->P);
+  c->out_words = bn_alloc<uint32_t>(N);
+  c->out_n = bn_alloc<int>(1);
+  c->raw_d = bn_alloc<unsigned long long>(2 * N);
+  c->nce_cap = N;
 }
 
 void refresh_shadows(dl_bn* c) {
@@ -370,26 +482,63 @@ void check_ids(const dl_bn* c, const uint32_t* ids, int64_t n, const char* what)
 void run_window(dl_bn* c, int64_t T, int64_t B, double scale, float clip, bool grads) {
   const int64_t H = c->H, P = c->P, V = c->V, N = T * B, BH = B * H;
   cudaStream_t st = c->st;
+  const bool nce = c->loss_mode == 0;
+  const bool t16 = tcm(c);
   input_side(c, N);
   recurrence_fwd(c, T, B);
   const float* Hs = c->htape + BH;
-  const bf16* Hs_bf = tcm(c) ? c->htape_bf + BH : nullptr;
-  output_side(c, N, Hs, Hs_bf, scale, grads);
+  const bf16* Hs_bf = t16 ? c->htape_bf + BH : nullptr;
   DL_CUDA(cudaMemsetAsync(c->d_loss, 0, sizeof(double), st));
   DL_CUDA(cudaMemsetAsync(c->d_pos, 0, sizeof(unsigned long long), st));
-  sum_rows(c->loss_row, c->w, N, c->d_loss, c->d_pos, st);
-  c->launches++;
+  const int K1 = c->nce_k + 1;
+  if (nce) {
+    // Z = Hs . D, then the NCE records over z and E (backprop.hpp:126-156;
+    // compress.hpp:204-207)
+    if (t16)
+      mm(c, (int)N, (int)P, (int)H, K_MAJOR, Hs_bf, H, MN_MAJOR, c->d_bf, P, c->z);
+    else
+      mm(c, (int)N, (int)P, (int)H, K_MAJOR, Hs, H, MN_MAJOR, c->d, P, c->z);
+    nce_records(c->w, c->y, T, B, c->nce_P, K1, c->raw_d, c->nz_prob_d, c->nz_alias_d, V,
+                c->pos_of_d, c->first_d, c->rec_word, c->rec_row, c->proc_r, st);
+    nce_scores(c->z, c->e, P, c->rec_word, c->rec_row, c->nce_N, c->score, st);
+    nce_loss(c->score, c->rec_word, c->ln_kq_d, c->nce_P, K1, scale, c->loss_pos, c->ds, st);
+    sum_rows(c->loss_pos, nullptr, c->nce_P, c->d_loss, c->d_pos, st);
+    c->launches += 5;
+  } else {
+    output_side(c, N, Hs, Hs_bf, scale, grads);
+    sum_rows(c->loss_row, c->w, N, c->d_loss, c->d_pos, st);
+    c->launches++;
+  }
   if (!grads) return;
   DL_CUDA(cudaMemsetAsync(c->nonfinite, 0, sizeof(int), st));
-  const bool t16 = tcm(c);
-  // softmax_backward (compress.hpp:237-243):
-  //   dZ = dS . E  [N x P];  gE = dS^T . Z  [V x P]
-  if (t16) {
+  c->e_sparse = nce;
+  if (nce) {
+    // score_backward of every record (compress.hpp:209-219): dz[b] += ds E[w];
+    // the embedding rows sum ds * z[b] per word in processing order
+    DL_CUDA(cudaMemsetAsync(c->dz, 0, N * P * sizeof(float), st));
+    nce_dh(c->e, P, c->rec_word, c->rec_row, c->ds, c->nce_P, K1, c->dz, st);
+    DL_CUDA(cudaMemsetAsync(c->g_e, 0, V * P * sizeof(float), st));
+    DL_CUDA(cudaMemsetAsync(c->touched, 0, V, st));
+    NceRecs R{c->rec_word, c->rec_row, c->proc_r, c->ds, c->keys_in, c->vals_in, c->keys_out,
+              c->vals_out, c->head, c->slot, c->sort_temp, c->sort_temp_bytes};
+    nce_out_rows(R, c->nce_N, V, c->z, P, FLT_MAX, c->nce_ws, c->nce_scale, c->out_rows,
+                 c->out_words, c->out_n, nullptr, st);
+    k_add_rows<<<(unsigned)std::max<int64_t>(c->nce_N, 1), 128, 0, st>>>(
+        c->out_rows, c->out_words, c->out_n, P, c->g_e, c->touched);
+    c->launches += 10;
+    if (t16) {
+      f32_to_bf16(c->dz, c->dz_bf, N * P, st);
+      c->launches++;
+    }
+  } else if (t16) {
+    // softmax_backward (compress.hpp:237-243):
+    //   dZ = dS . E  [N x P];  gE = dS^T . Z  [V x P]
     mm(c, (int)N, (int)P, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->e_bf, P, c->dz);
     mm(c, (int)V, (int)P, (int)N, MN_MAJOR, c->S, V, MN_MAJOR, c->z_bf, P, c->g_e);
     f32_to_bf16(c->dz, c->dz_bf, N * P, st);
     c->launches++;
   } else {
+    // softmax_backward, fp32
     mm(c, (int)N, (int)P, (int)V, K_MAJOR, c->S, V, MN_MAJOR, c->e, P, c->dz);
     mm(c, (int)V, (int)P, (int)N, MN_MAJOR, c->S, V, MN_MAJOR, c->z, P, c->g_e);
   }
@@ -443,7 +592,8 @@ void run_window(dl_bn* c, int64_t T, int64_t B, double scale, float clip, bool g
   // reference's processing order, added to the dense gradient
   embed_grads(c->x, T, B, 1, V, c->din, P, FLT_MAX, c->ews, c->in_rows, c->in_words, c->in_n,
               nullptr, st);
-  k_add_rows<<<(unsigned)N, 128, 0, st>>>(c->in_rows, c->in_words, c->in_n, P, c->g_e);
+  k_add_rows<<<(unsigned)N, 128, 0, st>>>(c->in_rows, c->in_words, c->in_n, P, c->g_e,
+                                          nce ? c->touched : nullptr);
   c->launches += 4;
   // BottleneckGrads::clip + finite (compress.hpp:96-114)
   reduce_splits(c->g_e, 1, 0, V * P, c->g_e, clip, 1, c->nonfinite, st);
@@ -459,8 +609,13 @@ void run_window(dl_bn* c, int64_t T, int64_t B, double scale, float clip, bool g
 void run_update(dl_bn* c, double eta) {
   cudaStream_t st = c->st;
   const bool t16 = tcm(c);
-  rms_rows(c->e, t16 ? c->e_bf : nullptr, c->m_e, c->g_e, nullptr, nullptr, c->V, c->P, c->rho,
-           c->eps, eta, 1, c->nonfinite, st);
+  if (c->e_sparse)
+    k_rms_rows_masked<<<148 * 8, 256, 0, st>>>(c->e, t16 ? c->e_bf : nullptr, c->m_e, c->g_e,
+                                               c->touched, c->V, c->P, c->rho, c->eps, eta,
+                                               c->nonfinite);
+  else
+    rms_rows(c->e, t16 ? c->e_bf : nullptr, c->m_e, c->g_e, nullptr, nullptr, c->V, c->P, c->rho,
+             c->eps, eta, 1, c->nonfinite, st);
   rms_rec(c->u, t16 ? c->u_bf : nullptr, c->m_u, c->g_u, c->P * c->H, c->rho, c->eps, eta,
           c->nonfinite, st);
   rms_rec(c->w_rec, t16 ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho, c->eps,
@@ -558,7 +713,14 @@ int dl_bn_destroy(dl_bn* c) {
                   (void*)c->dh, (void*)c->dpre, (void*)c->dpre_bf, (void*)c->din,
                   (void*)c->loss_row, (void*)c->logp_row, (void*)c->d_loss, (void*)c->d_pos,
                   (void*)c->ews.seg_start, (void*)c->ews.order_pos, (void*)c->in_rows,
-                  (void*)c->in_words, (void*)c->in_n, (void*)c->splitws, (void*)c->bar_counter})
+                  (void*)c->in_words, (void*)c->in_n, (void*)c->splitws, (void*)c->bar_counter,
+                  (void*)c->ln_kq_d, (void*)c->nz_prob_d, (void*)c->nz_alias_d, (void*)c->raw_d,
+                  (void*)c->pos_of_d, (void*)c->first_d, (void*)c->rec_word, (void*)c->rec_row,
+                  (void*)c->proc_r, (void*)c->score, (void*)c->ds, (void*)c->nce_scale,
+                  (void*)c->loss_pos, (void*)c->keys_in, (void*)c->vals_in, (void*)c->keys_out,
+                  (void*)c->vals_out, (void*)c->head, (void*)c->slot, c->sort_temp,
+                  (void*)c->nce_ws.seg_start, (void*)c->nce_ws.order_pos, (void*)c->out_rows,
+                  (void*)c->out_words, (void*)c->out_n, (void*)c->touched})
     if (p) cudaFree(p);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -636,6 +798,23 @@ int dl_bn_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
       if (weights[i]) DL_REQUIRE(targets[i] < (uint64_t)c->V, DL_EDATA, "bptt: id out of vocabulary range");
     ensure_window(c, T, N);
     cudaStream_t st = c->st;
+    if (c->loss_mode == 0) {
+      // the window's noise draws (t, b, then sample; masked positions draw
+      // nothing): 2 raw mt19937_64 outputs per draw, turned into words on
+      // the device with the alias tables (nce.cu k_nce_records)
+      DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
+                 "bptt: NCE mode needs noise model and rng (dl_bn_set_noise)");
+      int64_t Pn = 0;
+      for (int64_t i = 0; i < N; ++i) Pn += weights[i] ? 1 : 0;
+      nce_reserve(c, std::max<int64_t>(N * (c->nce_k + 1), 1));
+      const int64_t ND = 2 * Pn * c->nce_k;
+      c->raw_h.resize(std::max<int64_t>(ND, 1));
+      for (int64_t i = 0; i < ND; ++i) c->raw_h[i] = c->rng();
+      if (ND > 0)
+        DL_CUDA(cudaMemcpyAsync(c->raw_d, c->raw_h.data(), ND * 8, cudaMemcpyHostToDevice, st));
+      c->nce_P = Pn;
+      c->nce_N = Pn * (c->nce_k + 1);
+    }
     DL_CUDA(cudaMemcpyAsync(c->x, inputs, N * 4, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->y, targets, N * 4, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->w, weights, N, cudaMemcpyHostToDevice, st));
@@ -754,6 +933,51 @@ int dl_bn_sharded_perplexity(dl_bn* c, const uint32_t* ids, int64_t n, int shard
   if (total_logprob) *total_logprob = tot;
   if (predicted) *predicted = pred;
   if (perplexity) *perplexity = std::exp(-tot / (double)pred);
+  return DL_OK;
+}
+
+int dl_bn_set_loss_mode(dl_bn* c, int mode) {
+  if (!c) return bn_fail(c, DL_EINVAL, "dl_bn_set_loss_mode: null ctx");
+  if (mode != 0 && mode != 1) return bn_fail(c, DL_EINVAL, "loss mode must be 0 (NCE) or 1 (softmax)");
+  c->loss_mode = mode;
+  return DL_OK;
+}
+
+int dl_bn_set_noise(dl_bn* c, const double* counts, int64_t V, int k, double floor) {
+  if (!c || !counts) return bn_fail(c, DL_EINVAL, "dl_bn_set_noise: null argument");
+  if (V != c->V) return bn_fail(c, DL_EINVAL, "NoiseModel: vocabulary size mismatch");
+  if (k < 1) return bn_fail(c, DL_EINVAL, "NoiseModel: k >= 1");
+  if (!(floor > 0.0)) return bn_fail(c, DL_EINVAL, "NoiseModel: floor must be > 0");
+  return bn_guarded(c, [&] {
+    std::vector<double> lnkq, prob;
+    std::vector<uint32_t> alias;
+    noise_tables(counts, V, k, floor, lnkq, prob, alias);
+    if (!c->ln_kq_d) c->ln_kq_d = bn_alloc<double>(V);
+    if (!c->nz_prob_d) c->nz_prob_d = bn_alloc<double>(V);
+    if (!c->nz_alias_d) c->nz_alias_d = bn_alloc<uint32_t>(V);
+    if (!c->touched) c->touched = bn_alloc<uint8_t>(V);
+    DL_CUDA(cudaMemcpy(c->ln_kq_d, lnkq.data(), V * 8, cudaMemcpyHostToDevice));
+    DL_CUDA(cudaMemcpy(c->nz_prob_d, prob.data(), V * 8, cudaMemcpyHostToDevice));
+    DL_CUDA(cudaMemcpy(c->nz_alias_d, alias.data(), V * 4, cudaMemcpyHostToDevice));
+    c->nz_prob = std::move(prob);
+    c->nce_k = k;
+  });
+}
+
+int dl_bn_set_rng_state(dl_bn* c, const uint64_t state[313]) {
+  if (!c || !state) return bn_fail(c, DL_EINVAL, "dl_bn_set_rng_state: null argument");
+  std::stringstream ss;
+  for (int i = 0; i < 313; ++i) ss << state[i] << ' ';
+  ss >> c->rng;
+  if (!ss) return bn_fail(c, DL_EINVAL, "dl_bn_set_rng_state: bad state");
+  return DL_OK;
+}
+
+int dl_bn_get_rng_state(const dl_bn* c, uint64_t state[313]) {
+  if (!c || !state) return bn_fail(nullptr, DL_EINVAL, "dl_bn_get_rng_state: null argument");
+  std::stringstream ss;
+  ss << c->rng;
+  for (int i = 0; i < 313; ++i) ss >> state[i];
   return DL_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -45,6 +46,9 @@ void nce_out_rows(const NceRecs& R, int64_t N, int64_t V, const float* h, int64_
                   struct EmbedWs& ws, float* order_scale, float* rows, uint32_t* words,
                   int* n_rows, int* nonfinite, cudaStream_t st);
 int embed_short_max();
+// NoiseModel + AliasSampler tables (host; nce.cu)
+void noise_tables(const double* counts, int64_t V, int k, double floor, std::vector<double>& lnkq,
+                  std::vector<double>& prob, std::vector<uint32_t>& alias);
 
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
 void fill_f32(float* x, float v, int64_t n, cudaStream_t st);

@@ -22,6 +22,10 @@
 //                 then the segmented ds * h sums of kernels.cu (embed_rows).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace dl {
@@ -289,6 +293,55 @@ void nce_out_rows(const NceRecs& R, int64_t N, int64_t V, const float* h, int64_
   k_nce_long<<<g, 256, 0, st>>>(ws.seg_start, n_rows, embed_short_max(), ws.long_list(),
                                 ws.n_long());
   embed_rows(N, h, H, clip, ws, rows, n_rows, nonfinite, st, order_scale);
+}
+
+// NoiseModel (nce.hpp:41-66) + AliasSampler (rng.hpp:54-89) tables, host side:
+// q = max(count/total, floor) renormalised, ln(k q), and the alias tables
+// built with the reference's small/large stack discipline (bit-identical
+// sampling).
+void noise_tables(const double* counts, int64_t V, int k, double floor, std::vector<double>& lnkq,
+                  std::vector<double>& prob, std::vector<uint32_t>& alias) {
+  double total = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    DL_REQUIRE(counts[w] >= 0.0, 1, "NoiseModel: negative count");
+    total += counts[w];
+  }
+  DL_REQUIRE(total > 0.0, 1, "NoiseModel: zero total");
+  std::vector<double> q(V);
+  lnkq.assign(V, 0.0);
+  double qsum = 0.0;
+  for (int64_t w = 0; w < V; ++w) {
+    q[w] = std::max(counts[w] / total, floor);
+    qsum += q[w];
+  }
+  for (int64_t w = 0; w < V; ++w) {
+    q[w] /= qsum;
+    lnkq[w] = std::log(static_cast<double>(k) * q[w]);
+  }
+  double tw = 0.0;
+  for (double v : q) tw += v;
+  std::vector<double> scaled(V);
+  prob.assign(V, 0.0);
+  alias.assign(V, 0);
+  std::vector<uint32_t> small, large;
+  small.reserve(V);
+  large.reserve(V);
+  for (int64_t i = 0; i < V; ++i) {
+    scaled[i] = q[i] * static_cast<double>(V) / tw;
+    (scaled[i] < 1.0 ? small : large).push_back(static_cast<uint32_t>(i));
+  }
+  while (!small.empty() && !large.empty()) {
+    const uint32_t sm = small.back();
+    small.pop_back();
+    const uint32_t lg = large.back();
+    large.pop_back();
+    prob[sm] = scaled[sm];
+    alias[sm] = lg;
+    scaled[lg] = (scaled[lg] + scaled[sm]) - 1.0;
+    (scaled[lg] < 1.0 ? small : large).push_back(lg);
+  }
+  for (uint32_t i : large) prob[i] = 1.0;
+  for (uint32_t i : small) prob[i] = 1.0;
 }
 
 }  // namespace dl

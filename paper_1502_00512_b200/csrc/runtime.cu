@@ -514,44 +514,9 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
 // ------------------------------------------------------------------ NCE
 // NoiseModel (nce.hpp:41-66) + AliasSampler (rng.hpp:54-89), host side.
 void nce_build(dl_ctx* c, const double* counts, int64_t V, int k, double floor) {
-  double total = 0.0;
-  for (int64_t w = 0; w < V; ++w) {
-    DL_REQUIRE(counts[w] >= 0.0, 1, "NoiseModel: negative count");
-    total += counts[w];
-  }
-  DL_REQUIRE(total > 0.0, 1, "NoiseModel: zero total");
-  std::vector<double> q(V), lnkq(V);
-  double qsum = 0.0;
-  for (int64_t w = 0; w < V; ++w) {
-    q[w] = std::max(counts[w] / total, floor);
-    qsum += q[w];
-  }
-  for (int64_t w = 0; w < V; ++w) {
-    q[w] /= qsum;
-    lnkq[w] = std::log(static_cast<double>(k) * q[w]);
-  }
-  double tw = 0.0;
-  for (double v : q) tw += v;
-  std::vector<double> prob(V, 0.0), scaled(V);
-  std::vector<uint32_t> alias(V, 0), small, large;
-  small.reserve(V);
-  large.reserve(V);
-  for (int64_t i = 0; i < V; ++i) {
-    scaled[i] = q[i] * static_cast<double>(V) / tw;
-    (scaled[i] < 1.0 ? small : large).push_back(static_cast<uint32_t>(i));
-  }
-  while (!small.empty() && !large.empty()) {
-    const uint32_t sm = small.back();
-    small.pop_back();
-    const uint32_t lg = large.back();
-    large.pop_back();
-    prob[sm] = scaled[sm];
-    alias[sm] = lg;
-    scaled[lg] = (scaled[lg] + scaled[sm]) - 1.0;
-    (scaled[lg] < 1.0 ? small : large).push_back(lg);
-  }
-  for (uint32_t i : large) prob[i] = 1.0;
-  for (uint32_t i : small) prob[i] = 1.0;
+  std::vector<double> lnkq, prob;
+  std::vector<uint32_t> alias;
+  noise_tables(counts, V, k, floor, lnkq, prob, alias);
   c->nce_k = k;
   if (!c->ln_kq_d) c->ln_kq_d = dalloc<double>(V);
   if (!c->nz_prob_d) c->nz_prob_d = dalloc<double>(V);

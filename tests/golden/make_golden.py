@@ -159,7 +159,7 @@ def write_bn_nce(ref, out):
                               (300, 32, 16, 6, 8, 16, 1e-8, 1, 533)]):
         np.savez_compressed(os.path.join(out, f"bn_nce_{i}.npz"), **bn_nce_case(ref, *args))
     tr, va = ref.random_stream_pair(77, 40, 616, 150)
-    kw = dict(nstate=16, nproj=8, noffset=2, minibatch=2, unroll=5, eta=0.05, mode=0, nce_k=7,
+    kw = dict(nstate=16, nproj=8, noffset=2, minibatch=2, unroll=5, eta=0.005, mode=0, nce_k=7,
               noise_floor=1e-3, max_epochs=3, divergence_factor=1e9)
     params = ref.bn_init_uniform(40, 16, 8, 3)
     blob, logs, ini = ref.bn_train_native(oracle.TrainConfig(**kw), params, tr[:600], va)

@@ -227,3 +227,109 @@ def test_bn_trainer_matches_reference_fixture(name):
     t2.load_checkpoint(blob)
     assert t2.save_checkpoint() == blob
     assert len(blob) == len(g["rtrn"])
+
+
+# ----------------------------------------------------------------- NCE mode
+def bn_nce_model(bn, params, counts, k, floor, precision, act=0, state=None):
+    m = bn_model(bn, params, act, precision)
+    m.set_loss_mode(0)
+    m.set_noise(counts, k, floor)
+    m.set_rng_state(state)
+    return m
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "bn_nce_*.npz"))))
+def test_bn_nce_window_matches_reference_fixture(path):
+    """NCE window over the bottleneck adapter against the reference's own:
+    the generator state after the draws, loss, the sparse embedding
+    gradient (dense view) and the sparse-embedding update."""
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    g = np.load(path)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    V, P = params[0].shape
+    T, B = g["x"].shape
+    m = bn_nce_model(bn, params, g["counts"], int(g["k"]), float(g["floor"]), "fp32",
+                     int(g["act"]), g["rng0"])
+    m.set_opt(g["m_e"], g["m_u"], g["m_rec"], g["m_d"])
+    res, hf = bn.bn_bptt_run(m, dl.WindowBatch(g["x"], g["y"], g["w"]), g["h0"], 1.0 / (T * B),
+                             1.0)
+    assert np.array_equal(m.rng_state(), g["rng1"])
+    assert res.positions == int(g["positions"])
+    assert res.loss == pytest.approx(float(g["loss"]), rel=1e-6)
+    assert close(hf, g["h_final"])[0]
+    g_e = np.zeros((V, P), np.float32)
+    g_e[g["g_e_words"]] = g["g_e_rows"]
+    for got, want in zip(m.grads(), (g_e, g["g_u"], g["g_rec"], g["g_d"])):
+        ok, err = close(got, want)
+        assert ok, err
+    assert bn.bottleneck_update(m, 0.05) == bool(g["applied"])
+    for got, key in zip(m.params() + m.opt(), ("u_e", "u_u", "u_w_rec", "u_d", "u_m_e", "u_m_u",
+                                                "u_m_rec", "u_m_d")):
+        ok, err = close(got, g[key], rel=1e-4, floor_frac=1e-5)
+        assert ok, (key, err)
+
+
+@pytest.mark.parametrize("V,H,P,T,B,k,act", [(504, 64, 32, 6, 8, 16, 1), (4096, 256, 64, 8, 32, 32, 0)])
+def test_bn_nce_window_matches_oracle(orc, V, H, P, T, B, k, act):
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    rng = np.random.default_rng(V + k)
+    params = orc.bn_init_uniform(V, H, P, 2)
+    counts = rng.integers(0, 50, V).astype(np.float64)
+    x, y, w = rand_window(rng, T, B, V, 0.1)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    noise = orc.noise_build(counts, k, 1e-8)
+    st = orc.mt_state(11)
+    want = orc.bn_bptt_nce(params, act, x, y, w, h0, 1.0 / (T * B), 1.0, noise, st)
+    for precision in ("fp32", "bf16"):
+        m = bn_nce_model(bn, params, counts, k, 1e-8, precision, act, orc.mt_state(11))
+        res, hf = bn.bn_bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
+        assert np.array_equal(m.rng_state(), st)
+        if precision == "fp32":
+            assert res.loss == pytest.approx(want["loss"], rel=1e-6)
+            for got, key in zip(m.grads(), ("g_e", "g_u", "g_rec", "g_d")):
+                ok, err = close(got, want[key])
+                assert ok, (key, err)
+        else:
+            assert res.loss == pytest.approx(want["loss"], rel=1e-2)
+            ge = m.grads()[0]
+            cos = float(np.dot(ge.ravel(), want["g_e"].ravel()) /
+                        (np.linalg.norm(ge) * np.linalg.norm(want["g_e"]) + 1e-30))
+            assert cos > 0.99
+
+
+def test_bn_trainer_nce_matches_reference_fixture():
+    """BottleneckTrainer in NCE mode (the reference Trainer default) against
+    the reference's epochs; the generator advances exactly as the
+    reference's and the checkpoint resumes bit-for-bit."""
+    import ast
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    g = np.load(os.path.join(GOLD, "bn_train_nce.npz"))
+    kw = ast.literal_eval(str(g["cfg"][0]))
+    cfg = dl.TrainConfig(**kw)
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    V = params[0].shape[0]
+    t = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"])
+    t.train()
+    want = g["logs"]
+    assert t.initial_ppl == pytest.approx(float(g["initial"]), rel=1e-5)
+    assert len(t.logs) == len(want)
+    for a, b in zip(t.logs, want):
+        assert a.train_loss == pytest.approx(b[1], rel=1e-4)
+        assert a.valid_ppl == pytest.approx(b[2], rel=1e-4)
+    blob = t.save_checkpoint()
+    assert len(blob) == len(g["rtrn"])
+    # same draws made (generator state), same schedule (cursors)
+    from paper_1502_00512_b200 import formats
+    L = len(g["train"])
+    mine = formats.read_trainer(blob, cfg, len(t.cursors), t.model.H, L, model="bottleneck")
+    ref = formats.read_trainer(g["rtrn"].tobytes(), cfg, len(t.cursors), t.model.H, L,
+                               model="bottleneck")
+    assert mine["rng_text"] == ref["rng_text"]
+    assert np.array_equal(mine["cursors"], ref["cursors"])
+    assert (mine["epoch"], mine["eta"], mine["bad"]) == (ref["epoch"], ref["eta"], ref["bad"])
+    t2 = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"])
+    t2.load_checkpoint(blob)
+    assert t2.save_checkpoint() == blob
