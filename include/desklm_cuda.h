@@ -131,6 +131,13 @@ int dl_rnn_perplexity(dl_ctx* ctx, const uint32_t* ids, int64_t n,
                       uint32_t bos_id, double* total_logprob,
                       uint64_t* predicted, double* perplexity);
 
+/* ln_z_samples (eval.hpp:805-857): ln Z at up to `count` hidden states taken
+ * at stride max(1, n / count) from one pass over the stream (state carried
+ * across sentences).  out: count doubles; *n_out: states taken.  The host
+ * drift_stats (eval.hpp:859-880) runs on these. */
+int dl_ln_z_samples(dl_ctx* ctx, const uint32_t* ids, int64_t n, int64_t count, double* out,
+                    int64_t* n_out);
+
 /* ---- device-resident trainer (Trainer<Traits>::run_epoch) -------------- */
 
 /* Uploads the training IdStream once and sets up the offset-stream schedule

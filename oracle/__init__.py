@@ -319,6 +319,29 @@ class _Backend:
                       rows.ctypes.data, *gs, C.byref(applied)))
         return tuple(p), tuple(m), bool(applied.value)
 
+    def ln_z_samples(self, params, act, ids, count):
+        """ln_z_samples (eval.hpp:805-857) -> float64 array."""
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        ids = np.ascontiguousarray(ids, np.uint32)
+        out = np.empty(count, np.float64)
+        ns = C.c_int64()
+        if self.prefix == "ref_":
+            stats = np.zeros(6, np.float64)
+            f = self.lib.ref_ln_z_samples
+            f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64, _i64, _vp,
+                          C.POINTER(C.c_int64), _vp]
+            self._check(f(V, H, act, w_in, w_rec, w_out, ids, len(ids), count, out.ctypes.data,
+                          C.byref(ns), stats.ctypes.data))
+            self.last_drift_stats = stats
+        else:
+            f = self.lib.orc_ln_z_samples
+            f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64, _i64, _vp,
+                          C.POINTER(C.c_int64)]
+            self._check(f(V, H, act, w_in, w_rec, w_out, ids, len(ids), count, out.ctypes.data,
+                          C.byref(ns)))
+        return out[: ns.value].copy()
+
     def bn_sharded_ppl(self, params, act, ids, shards, bos=1):
         e, u, w_rec, d = params
         V, P = e.shape

@@ -1337,3 +1337,36 @@ int orc_bn_update_sparse(int64_t V, int64_t H, int64_t P, float* e, float* u, fl
   *applied = 1;
   return 0;
 }
+
+/* ln_z_samples (eval.hpp:805-857) for the standard model: one pass, state
+ * carried across sentences, ln Z = lse over W_out . h (float scores, double
+ * lse) of the states after ids[i], i % stride == 0, stride = max(1, n/count). */
+int orc_ln_z_samples(int64_t V, int64_t H, int act, const float* w_in, const float* w_rec,
+                     const float* w_out, const uint32_t* ids, int64_t n, int64_t count,
+                     double* out, int64_t* n_out) {
+  if (n < 1 || count < 1) return 1;
+  const int64_t stride = (n / count) > 1 ? n / count : 1;
+  float* h = (float*)malloc(sizeof(float) * H);
+  float* pre = (float*)malloc(sizeof(float) * H);
+  float* sc = (float*)malloc(sizeof(float) * V);
+  const float a0 = act_f(act, 0.0f);
+  for (int64_t j = 0; j < H; ++j) h[j] = a0;
+  int64_t ns = 0;
+  int rc = 0;
+  for (int64_t i = 0; i < n && ns < count; ++i) {
+    if (ids[i] >= (uint64_t)V) {
+      rc = 2;
+      break;
+    }
+    matmul_nt(h, w_rec, pre, 1, H, H);
+    for (int64_t j = 0; j < H; ++j) h[j] = act_f(act, pre[j] + w_in[(int64_t)ids[i] * H + j]);
+    if (i % stride != 0) continue;
+    for (int64_t w = 0; w < V; ++w) sc[w] = (float)dot_acc(w_out + w * H, h, H);
+    out[ns++] = lse_vec(sc, V);
+  }
+  *n_out = ns;
+  free(h);
+  free(pre);
+  free(sc);
+  return rc;
+}

@@ -784,4 +784,30 @@ int ref_bn_update_sparse(std::int64_t V, std::int64_t H, std::int64_t P, float* 
   });
 }
 
+// ln_z_samples(StandardAdapter) + drift_stats (eval.hpp:805-880); stats =
+// {mean, median, q25, q75, iqr, contexts} (only when >= 100 samples).
+int ref_ln_z_samples(std::int64_t V, std::int64_t H, int act, const float* w_in,
+                     const float* w_rec, const float* w_out, const std::uint32_t* ids,
+                     std::int64_t n, std::int64_t count, double* out, std::int64_t* n_out,
+                     double* stats) {
+  return guarded([&] {
+    const RnnParams<float> p = make_params(V, H, act, w_in, w_rec, w_out);
+    IdStream st;
+    st.ids.assign(ids, ids + n);
+    StandardAdapter<float> a(p);
+    const std::vector<double> z = ln_z_samples(a, st, static_cast<std::size_t>(count));
+    *n_out = static_cast<std::int64_t>(z.size());
+    std::memcpy(out, z.data(), sizeof(double) * z.size());
+    if (z.size() >= 100) {
+      const DriftStats d = drift_stats(z);
+      stats[0] = d.mean;
+      stats[1] = d.median;
+      stats[2] = d.q25;
+      stats[3] = d.q75;
+      stats[4] = d.iqr;
+      stats[5] = static_cast<double>(d.contexts);
+    }
+  });
+}
+
 }  // extern "C"

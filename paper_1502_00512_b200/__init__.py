@@ -14,6 +14,7 @@ this package                reference
 ``sharded_perplexity``      ``sharded_perplexity`` (eval.hpp:151-222)
 ``rnn_perplexity``          ``rnn_perplexity`` (eval.hpp:84-145)
 ``rescore_nbest``           ``rescore_nbest`` RNN part (eval.hpp:693-790)
+``ln_z_samples``            ``ln_z_samples`` / ``drift_stats`` (eval.hpp:805-880)
 ``TrainConfig``/``Trainer`` ``TrainConfig``/``Trainer<StandardTraits>``
                             (trainer.hpp:43-93, :171-476)
 ``formats``                 RNLM / ROPT / RTRN (+ RNBL / RBOP) byte layouts
@@ -44,7 +45,8 @@ __all__ = [
     "rmsprop_update", "train_window", "sharded_perplexity", "rng_seed_state", "rnn_perplexity", "score",
     "TrainConfig", "EpochLog", "Trainer", "DataError", "DeviceError", "formats",
     "param_count", "make_vocab", "KSIGMOID", "KTANH", "rescore_nbest",
-    "read_nbest", "write_nbest", "NBestHyp", "NBestUtt",
+    "read_nbest", "write_nbest", "NBestHyp", "NBestUtt", "ln_z_samples", "drift_stats",
+    "DriftStats",
 ]
 
 KSIGMOID, KTANH = 0, 1
@@ -375,6 +377,49 @@ def sharded_perplexity(model: GpuRnn, ids, shards: int, bos_id: int = BOS_ID):
     model._chk(load().dl_sharded_perplexity(model.handle, ids.ctypes.data, len(ids), shards,
                                             bos_id, C.byref(tot), C.byref(pred), C.byref(ppl)))
     return PerplexityResult(ppl.value, tot.value, pred.value)
+
+
+def ln_z_samples(model: GpuRnn, ids, count: int) -> np.ndarray:
+    """ln_z_samples (eval.hpp:805-857): ln Z of up to `count` hidden states
+    sampled at stride max(1, n / count) from one pass over the stream."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    out = np.empty(max(int(count), 1), np.float64)
+    n = C.c_int64()
+    model._chk(load().dl_ln_z_samples(model.handle, ids.ctypes.data, len(ids), int(count),
+                                      out.ctypes.data, C.byref(n)))
+    return out[: n.value].copy()
+
+
+@dataclass
+class DriftStats:
+    mean: float = 0.0
+    median: float = 0.0
+    q25: float = 0.0
+    q75: float = 0.0
+    iqr: float = 0.0
+    contexts: int = 0
+
+
+def drift_stats(ln_z) -> DriftStats:
+    """drift_stats (eval.hpp:859-880): mean and linearly interpolated
+    quartiles of the sorted samples (host arithmetic, same order)."""
+    v = sorted(float(x) for x in ln_z)
+    if len(v) < 100:
+        raise ValueError("drift stats: need at least 100 contexts")
+    total = 0.0
+    for x in v:
+        total += x
+
+    def quantile(q):
+        pos = q * float(len(v) - 1)
+        lo = int(pos)
+        frac = pos - float(lo)
+        if lo + 1 >= len(v):
+            return v[-1]
+        return v[lo] * (1.0 - frac) + v[lo + 1] * frac
+
+    q25, q75 = quantile(0.25), quantile(0.75)
+    return DriftStats(total / float(len(v)), quantile(0.5), q25, q75, q75 - q25, len(v))
 
 
 def rnn_perplexity(model: GpuRnn, ids, bos_id: int = BOS_ID):

@@ -1588,6 +1588,83 @@ int dl_rnn_perplexity(dl_ctx* c, const uint32_t* ids, int64_t n, uint32_t bos,
   return DL_OK;
 }
 
+// ln_z_samples (eval.hpp:805-857): one pass over the stream with the state
+// carried across sentences; after reading ids[i] with i % stride == 0 the
+// state's log partition function ln Z = lse_w(s_w) is recorded, stride =
+// max(1, n / count), until count states are taken.  The recurrence runs in
+// banks on the device; the sampled states come back to the host and go
+// through the logits GEMM + block log-sum-exp in chunks.
+int dl_ln_z_samples(dl_ctx* c, const uint32_t* ids, int64_t n, int64_t count, double* out,
+                    int64_t* n_out) {
+  if (!c) return fail(c, DL_EINVAL, "dl_ln_z_samples: null ctx");
+  if (!ids || n < 1 || count < 1) return fail(c, DL_EINVAL, "ln Z samples: empty stream or zero count");
+  if (c->vshard) return fail(c, DL_EINVAL, "ln Z samples: not on a vocabulary-sharded context");
+  const int64_t stride = std::max<int64_t>(1, n / count);
+  std::vector<int64_t> pos;
+  int64_t steps = 0;
+  for (int64_t i = 0; i < n && (int64_t)pos.size() < count; ++i) {
+    if (ids[i] >= (uint64_t)c->V) return fail(c, DL_EDATA, "ln Z samples: id out of vocabulary range");
+    steps = i + 1;
+    if (i % stride == 0) pos.push_back(i);
+  }
+  return guarded(c, [&] {
+    const int64_t H = c->H, V = c->Vo;
+    const int64_t bank = std::min<int64_t>(steps, 4096);
+    ensure_window(c, bank, 1);
+    cudaStream_t st = c->st;
+    fill_f32(c->htape, act0(c->act), H, st);
+    std::vector<float> states(pos.size() * H);
+    size_t k = 0;
+    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
+      const int64_t nb = std::min(bank, steps - j0);
+      DL_CUDA(cudaMemcpyAsync(c->x_d, ids + j0, nb * 4, cudaMemcpyHostToDevice, st));
+      if (tc(c)) f32_to_bf16(c->htape, c->htape_bf, H, st);
+      for (int64_t t = 0; t < nb; ++t)
+        rec_step_fwd(c, 1, c->htape + t * H, tc(c) ? c->htape_bf + t * H : nullptr, c->x_d + t,
+                     c->htape + (t + 1) * H, tc(c) ? c->htape_bf + (t + 1) * H : nullptr);
+      while (k < pos.size() && pos[k] < j0 + nb) {
+        DL_CUDA(cudaMemcpyAsync(states.data() + k * H, c->htape + (pos[k] - j0 + 1) * H, H * 4,
+                                cudaMemcpyDeviceToHost, st));
+        ++k;
+      }
+      DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * H, H * 4, cudaMemcpyDeviceToDevice, st));
+      DL_CUDA(cudaStreamSynchronize(st));
+    }
+    // ln Z of the sampled states, `bank` rows at a time (softmax_scores_t +
+    // lse_column, eval.hpp:829-837)
+    const int64_t ns = (int64_t)pos.size();
+    DL_CUDA(cudaMemsetAsync(c->y_d, 0xff, bank * 4, st));  // no target column
+    for (int64_t r0 = 0; r0 < ns; r0 += bank) {
+      const int64_t M = std::min(bank, ns - r0);
+      DL_CUDA(cudaMemcpyAsync(c->htape, states.data() + r0 * H, M * H * 4, cudaMemcpyHostToDevice,
+                              st));
+      if (tc(c)) {
+        f32_to_bf16(c->htape, c->htape_bf, M * H, st);
+        GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, c->htape_bf, H, K_MAJOR, c->w_out_bf, H,
+                          nullptr, 0);
+        g.logits = 1;
+        g.S = nullptr;
+        g.lds = V;
+        g.part = c->part;
+        g.tgt = c->y_d;
+        g.tgt_logit = c->tgt_logit;
+        g.no_pair = c->logits_pair ? 0 : 1;
+        gemm(c, g);
+        block_lse_bf16(c->part, c->part_tiles, M, c->loss_row, st);
+      } else {
+        GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, c->htape, H, K_MAJOR, c->w_out, H,
+                          static_cast<float*>(c->S), V);
+        gemm(c, g);
+        block_lse_f32(static_cast<float*>(c->S), M, V, c->y_d, c->loss_row, c->dh_out, st);
+      }
+      c->launches += 2;
+      DL_CUDA(cudaMemcpyAsync(out + r0, c->loss_row, M * 8, cudaMemcpyDeviceToHost, st));
+      DL_CUDA(cudaStreamSynchronize(st));
+    }
+    if (n_out) *n_out = ns;
+  });
+}
+
 // RnnParams::init_uniform (rnn.hpp:79-83): one std::mt19937_64(seed), w_in
 // then w_rec then w_out, each element float(lo + (hi - lo) * u) with
 // u = (rng() >> 11) * 2^-53 (rng.hpp:37-44).  Pure host code; bit-exact.

@@ -168,6 +168,16 @@ def write_bn_nce(ref, out):
                         initial=ini, rtrn=np.frombuffer(blob, np.uint8), cfg=np.array([repr(kw)]))
 
 
+def write_ln_z(ref, out):
+    """ln_z_samples + drift_stats (eval.hpp:805-880) of the reference."""
+    params = ref.init_uniform(300, 24, 13)
+    ids = ref.random_stream(55, 300, 6000)
+    z = ref.ln_z_samples(params, 0, ids, 200)
+    np.savez_compressed(os.path.join(out, "ln_z.npz"), w_in=params[0], w_rec=params[1],
+                        w_out=params[2], ids=ids, act=0, count=200, ln_z=z,
+                        stats=ref.last_drift_stats)
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -210,6 +220,7 @@ def main():
     write_bn(ref, out)
     write_bn_train(ref, out)
     write_bn_nce(ref, out)
+    write_ln_z(ref, out)
     print("golden fixtures written to", out)
 
 

@@ -96,3 +96,34 @@ def test_rescore_matches_reference(ref):
         fa, fb = a.split("\t"), b.split("\t")
         assert fa[:4] == fb[:4] and fa[6] == fb[6]
         assert float(fa[4]) == pytest.approx(float(fb[4]), abs=2e-3)
+
+
+def test_ln_z_samples_match_reference_fixture():
+    """ln_z_samples (eval.hpp:805-857) on the device (fp32 parity mode)
+    against the reference's fixture; drift_stats over them."""
+    import os
+    import paper_1502_00512_b200 as dl
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ln_z.npz"))
+    V, H = g["w_in"].shape
+    m = dl.GpuRnn(V, H, int(g["act"]), "fp32")
+    m.set_params(g["w_in"], g["w_rec"], g["w_out"])
+    z = dl.ln_z_samples(m, g["ids"], int(g["count"]))
+    assert len(z) == len(g["ln_z"])
+    np.testing.assert_allclose(z, g["ln_z"], rtol=1e-6)
+    s = dl.drift_stats(z)
+    assert s.contexts == int(g["stats"][5])
+    assert s.median == pytest.approx(g["stats"][1], rel=1e-6)
+
+
+def test_ln_z_samples_bf16_close_to_oracle(orc):
+    import paper_1502_00512_b200 as dl
+    V, H = 4096, 256
+    params = orc.init_uniform(V, H, 21)
+    ids = orc.random_stream(3, V, 20000)
+    want = orc.ln_z_samples(params, 0, ids, 300)
+    for precision, tol in (("fp32", 1e-6), ("bf16", 5e-3)):
+        m = dl.GpuRnn(V, H, 0, precision)
+        m.set_params(*params)
+        z = dl.ln_z_samples(m, ids, 300)
+        assert len(z) == len(want)
+        np.testing.assert_allclose(z, want, rtol=tol)

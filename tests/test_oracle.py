@@ -389,3 +389,17 @@ def test_bottleneck_trainer_nce_golden(orc):
                                  r["cursors"], r["hidden"], r["params"],
                                  make_vocab(int(g["e"].shape[0])), r["opt"], model="bottleneck")
     assert blob == g["rtrn"].tobytes()
+
+
+def test_ln_z_samples_golden_and_drift_stats(orc):
+    """ln_z_samples (eval.hpp:805-857) restated bit-exact; the package's
+    host drift_stats (eval.hpp:859-880) equals the reference's."""
+    import paper_1502_00512_b200 as dl
+    g = load("ln_z.npz")
+    params = (g["w_in"], g["w_rec"], g["w_out"])
+    z = orc.ln_z_samples(params, int(g["act"]), g["ids"], int(g["count"]))
+    assert np.array_equal(z, g["ln_z"])
+    s = dl.drift_stats(z)
+    assert [s.mean, s.median, s.q25, s.q75, s.iqr, s.contexts] == list(g["stats"])
+    with pytest.raises(ValueError):
+        dl.drift_stats(z[:99])
