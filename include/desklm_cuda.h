@@ -287,6 +287,16 @@ const char* dl_bn_last_error(const dl_bn* ctx);
 int dl_bn_set_params(dl_bn* ctx, const float* e, const float* u, const float* w_rec,
                      const float* d);
 int dl_bn_get_params(dl_bn* ctx, float* e, float* u, float* w_rec, float* d);
+/* RNQZ load path (read_quantized + dequantize_model, compress.hpp:481-523):
+ * the four linearly quantised matrices e, u, w_rec, d (packed codes,
+ * least-significant bit first, as in the file) are dequantised on the
+ * device into the fp32 parameters. */
+typedef struct dl_qmatrix {
+  int bits;              /* 1..16 */
+  float min, max;        /* QuantizedMatrix::min / max */
+  const uint8_t* codes;  /* ceil(rows * cols * bits / 8) bytes */
+} dl_qmatrix;
+int dl_bn_set_params_quantized(dl_bn* ctx, const dl_qmatrix m[4]);
 /* m_e [V], m_u [P x H], m_rec [H x H], m_d [H x P]; NULL = zeros */
 int dl_bn_set_opt(dl_bn* ctx, const float* m_e, const float* m_u, const float* m_rec,
                   const float* m_d, double rho, double eps);

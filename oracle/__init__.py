@@ -657,6 +657,24 @@ class Ref(_Backend):
                       buf.ctypes.data, cap, C.byref(ln), logs, C.byref(nl), C.byref(ini)))
         return bytes(buf[: ln.value]), logs[: nl.value].copy(), ini.value
 
+    def bn_quantize(self, params, bits, act=0):
+        """quantize_model + write_quantized (RNQZ bytes) and the dequantized
+        parameters of read_quantized + dequantize_model."""
+        e, u, w_rec, d = params
+        V, P = e.shape
+        H = w_rec.shape[0]
+        f = self.lib.ref_bn_quantize
+        f.argtypes = [_i64, _i64, _i64, C.c_int] + [_f32p] * 4 + [C.c_int, _vp, _u64,
+                                                                  C.POINTER(C.c_uint64)] + \
+            [_f32p] * 4
+        cap = (V * P + 2 * P * H + H * H) * 2 + 64 * V + 4096
+        buf = np.zeros(cap, np.uint8)
+        ln = C.c_uint64()
+        out = [np.empty(s_, np.float32) for s_ in ((V, P), (P, H), (H, H), (H, P))]
+        self._check(f(V, H, P, act, e, u, w_rec, d, int(bits), buf.ctypes.data, cap,
+                      C.byref(ln), *out))
+        return bytes(buf[: ln.value]), tuple(out)
+
     def bn_write(self, params, state, rho, eps, act=0):
         """write_bottleneck (RNBL, vocabulary make_vocab(V)) and
         write_bottleneck_opt (RBOP) bytes."""

@@ -810,4 +810,28 @@ int ref_ln_z_samples(std::int64_t V, std::int64_t H, int act, const float* w_in,
   });
 }
 
+// quantize_model + write_quantized (RNQZ) of a bottleneck model, and the
+// dequantize_model round trip (compress.hpp:417-621).
+int ref_bn_quantize(std::int64_t V, std::int64_t H, std::int64_t P, int act, const float* e,
+                    const float* u, const float* w_rec, const float* d, int bits,
+                    std::uint8_t* buf, std::uint64_t cap, std::uint64_t* len, float* de,
+                    float* du, float* dw_rec, float* dd) {
+  return guarded([&] {
+    const BottleneckParams<float> p = make_bn(V, H, P, act, e, u, w_rec, d);
+    const QuantizedModel q = quantize_model(p, testutil::make_vocab(V), bits);
+    std::ostringstream os(std::ios::binary);
+    write_quantized(os, q);
+    const std::string b = os.str();
+    *len = b.size();
+    if (b.size() != quantized_size_bytes(q)) throw std::runtime_error("size mismatch");
+    if (b.size() <= cap) std::memcpy(buf, b.data(), b.size());
+    std::istringstream is(b);
+    auto [p2, v2] = dequantize_model(read_quantized(is));
+    std::memcpy(de, p2.e.a.data(), sizeof(float) * V * P);
+    std::memcpy(du, p2.u.a.data(), sizeof(float) * P * H);
+    std::memcpy(dw_rec, p2.w_rec.a.data(), sizeof(float) * H * H);
+    std::memcpy(dd, p2.d.a.data(), sizeof(float) * H * P);
+  });
+}
+
 }  // extern "C"

@@ -28,7 +28,7 @@ EXPORTS = (
     "dl_bn_set_params", "dl_bn_get_params", "dl_bn_set_opt", "dl_bn_get_opt", "dl_bn_window",
     "dl_bn_get_grads", "dl_bn_rmsprop", "dl_bn_train_window", "dl_bn_sharded_perplexity",
     "dl_bn_launch_count", "dl_bn_cuda_stream", "dl_bn_set_loss_mode", "dl_bn_set_noise",
-    "dl_bn_set_rng_state", "dl_bn_get_rng_state",
+    "dl_bn_set_rng_state", "dl_bn_get_rng_state", "dl_bn_set_params_quantized",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -117,6 +117,7 @@ def load():
         "dl_bn_sharded_perplexity": (C.c_int, [vp, vp, i64, C.c_int, C.c_uint32,
                                                P(C.c_double), P(C.c_uint64), P(C.c_double)]),
         "dl_bn_set_loss_mode": (C.c_int, [vp, C.c_int]),
+        "dl_bn_set_params_quantized": (C.c_int, [vp, vp]),
         "dl_bn_set_noise": (C.c_int, [vp, vp, i64, C.c_int, C.c_double]),
         "dl_bn_set_rng_state": (C.c_int, [vp, vp]),
         "dl_bn_get_rng_state": (C.c_int, [vp, vp]),

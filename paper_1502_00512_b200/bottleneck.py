@@ -106,6 +106,20 @@ class GpuBottleneck:
             raise ValueError("set_params: shape mismatch")
         self._chk(load().dl_bn_set_params(self._h, *(x.ctypes.data for x in a)))
 
+    def set_params_quantized(self, q):
+        """RNQZ load (read_quantized + dequantize_model, compress.hpp:481-617):
+        q is a formats.QuantizedModel; the codes are dequantised on the device."""
+        if (q.v, q.h, q.p) != (self.V, self.H, self.P):
+            raise ValueError("set_params_quantized: shape mismatch")
+
+        class QM(C.Structure):
+            _fields_ = [("bits", C.c_int), ("min", C.c_float), ("max", C.c_float),
+                        ("codes", C.c_void_p)]
+
+        bufs = [np.frombuffer(m.codes, np.uint8) for m in q.mats]
+        arr = (QM * 4)(*[QM(m.bits, m.min, m.max, b.ctypes.data) for m, b in zip(q.mats, bufs)])
+        self._chk(load().dl_bn_set_params_quantized(self._h, C.cast(arr, C.c_void_p)))
+
     def params(self):
         out = [np.empty(s, np.float32) for s in self._shapes()]
         self._chk(load().dl_bn_get_params(self._h, *(x.ctypes.data for x in out)))

@@ -226,6 +226,24 @@ __global__ void k_rms_rows_masked(float* __restrict__ w, bf16* __restrict__ wb,
   }
 }
 
+// dequantize_matrix (compress.hpp:481-488) on the device: code i is bits
+// [i*bits, (i+1)*bits) of the packed payload, least-significant bit first;
+// value = float(double(min) + step * code).
+__global__ void k_dequant(const uint8_t* __restrict__ codes, int64_t nbytes, int64_t n, int bits,
+                          float mn, double step, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bit = i * bits;
+    const int64_t b0 = bit >> 3;
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (b0 + j < nbytes) word |= (uint32_t)codes[b0 + j] << (8 * j);
+    const uint32_t code = (word >> (bit & 7)) & ((1u << bits) - 1u);
+    out[i] = (float)((double)mn + step * (double)code);
+  }
+}
+
 unsigned grid_n(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
 }
@@ -735,6 +753,34 @@ int dl_bn_set_params(dl_bn* c, const float* e, const float* u, const float* w_re
     upload(c, c->u, u, c->P * c->H);
     upload(c, c->w_rec, w_rec, c->H * c->H);
     upload(c, c->d, d, c->H * c->P);
+    refresh_shadows(c);
+    c->have_grads = false;
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_bn_set_params_quantized(dl_bn* c, const dl_qmatrix m[4]) {
+  if (!c || !m) return bn_fail(c, DL_EINVAL, "dl_bn_set_params_quantized: null argument");
+  const int64_t rows[4] = {c->V, c->P, c->H, c->H}, cols[4] = {c->P, c->H, c->H, c->P};
+  for (int k = 0; k < 4; ++k) {
+    if (m[k].bits < 1 || m[k].bits > 16) return bn_fail(c, DL_EDATA, "quantized model: bits out of range");
+    if (!m[k].codes) return bn_fail(c, DL_EINVAL, "dl_bn_set_params_quantized: null codes");
+  }
+  return bn_guarded(c, [&] {
+    float* dst[4] = {c->e, c->u, c->w_rec, c->d};
+    for (int k = 0; k < 4; ++k) {
+      const int64_t n = rows[k] * cols[k];
+      const int64_t nbytes = (n * m[k].bits + 7) / 8;
+      uint8_t* dcodes = bn_alloc<uint8_t>(nbytes);
+      DL_CUDA(cudaMemcpyAsync(dcodes, m[k].codes, nbytes, cudaMemcpyHostToDevice, c->st));
+      // QuantizedMatrix::step (compress.hpp:431-436)
+      const double range = (double)m[k].max - (double)m[k].min;
+      const double step = range > 0.0 ? range / (double)((1u << m[k].bits) - 1u) : 0.0;
+      k_dequant<<<grid_n(n), 256, 0, c->st>>>(dcodes, nbytes, n, m[k].bits, m[k].min, step, dst[k]);
+      c->launches++;
+      DL_CUDA(cudaStreamSynchronize(c->st));
+      cudaFree(dcodes);
+    }
     refresh_shadows(c);
     c->have_grads = false;
     DL_CUDA(cudaStreamSynchronize(c->st));

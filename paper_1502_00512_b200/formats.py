@@ -9,6 +9,7 @@ reference's documented layouts:
 from __future__ import annotations
 
 import io
+from dataclasses import dataclass
 import struct
 
 import numpy as np
@@ -244,6 +245,136 @@ def read_bottleneck_opt(data_or_reader):
     m_rec = r.f32s(H * H).reshape(H, H)
     m_d = r.f32s(H * P).reshape(H, P)
     return V, H, P, rho, eps, (m_e, m_u, m_rec, m_d)
+
+
+# ------------------------------------------------------------------ RNQZ
+QUANTIZED_FORMAT_VERSION = 1
+
+
+@dataclass
+class QuantizedMatrix:
+    """QuantizedMatrix (compress.hpp:423-448): per-matrix linear codes,
+    packed without padding, least-significant bit first."""
+    rows: int
+    cols: int
+    bits: int
+    min: float
+    max: float
+    codes: bytes
+
+    def step(self) -> float:
+        rng = float(np.float32(self.max)) - float(np.float32(self.min))
+        return rng / float((1 << self.bits) - 1) if rng > 0.0 else 0.0
+
+    def code_array(self) -> np.ndarray:
+        n = self.rows * self.cols
+        b = np.unpackbits(np.frombuffer(self.codes, np.uint8), bitorder="little")
+        b = b[: n * self.bits].reshape(n, self.bits).astype(np.uint32)
+        return (b << np.arange(self.bits, dtype=np.uint32)).sum(axis=1, dtype=np.uint32)
+
+
+def quantize_matrix(m, bits: int) -> QuantizedMatrix:
+    """quantize_matrix (compress.hpp:450-479): step = (max - min) / (2^bits - 1),
+    code = clamp(llround((x - min) / step)) in double."""
+    if bits < 1 or bits > 16:
+        raise ValueError("quantize: bits must be in [1, 16]")
+    a = np.ascontiguousarray(m, np.float32)
+    if a.size == 0:
+        raise ValueError("quantize: empty matrix")
+    mn, mx = np.float32(a.min()), np.float32(a.max())
+    q = QuantizedMatrix(a.shape[0], a.shape[1] if a.ndim > 1 else 1, bits, float(mn), float(mx),
+                        b"")
+    n = a.size
+    step = q.step()
+    codes = np.zeros(n, np.int64)
+    if step > 0.0:
+        x = (a.ravel().astype(np.float64) - float(mn)) / step
+        codes = np.clip(np.floor(x + 0.5), 0, (1 << bits) - 1).astype(np.int64)  # x >= 0: llround
+    bitsarr = ((codes[:, None] >> np.arange(bits)) & 1).astype(np.uint8).ravel()
+    q.codes = np.packbits(bitsarr, bitorder="little").tobytes()
+    return q
+
+
+def dequantize_matrix(q: QuantizedMatrix) -> np.ndarray:
+    """dequantize_matrix (compress.hpp:481-488): float(min + step * code)."""
+    v = float(np.float32(q.min)) + q.step() * q.code_array().astype(np.float64)
+    return v.astype(np.float32).reshape(q.rows, q.cols)
+
+
+@dataclass
+class QuantizedModel:
+    v: int
+    h: int
+    p: int
+    act: int
+    bits: int
+    mats: tuple  # (e, u, w_rec, d) QuantizedMatrix
+    words: list
+
+
+def quantize_model(params, vocab_words, bits: int, act: int = 0) -> QuantizedModel:
+    """quantize_model (compress.hpp:498-512)."""
+    e, u, w_rec, d = params
+    V, P = np.asarray(e).shape
+    H = np.asarray(w_rec).shape[0]
+    return QuantizedModel(V, H, P, act, bits, tuple(quantize_matrix(m, bits)
+                                                    for m in (e, u, w_rec, d)),
+                          list(vocab_words))
+
+
+def dequantize_model(q: QuantizedModel):
+    """dequantize_model (compress.hpp:514-523) -> ((e, u, w_rec, d), act, words)."""
+    return tuple(dequantize_matrix(m) for m in q.mats), q.act, q.words
+
+
+def write_quantized(q: QuantizedModel) -> bytes:
+    """write_quantized (compress.hpp:575-586): RNQZ header, vocabulary, then
+    each matrix's bits, min, max and code payload."""
+    out = io.BytesIO()
+    out.write(b"RNQZ" + _u32(QUANTIZED_FORMAT_VERSION) + _u64(q.v) + _u64(q.h) + _u64(q.p) +
+              _u8(q.act) + _u64(len(q.words)))
+    for w in q.words:
+        out.write(_str(w))
+    for m in q.mats:
+        out.write(_u32(m.bits) + struct.pack("<f", m.min) + struct.pack("<f", m.max) + m.codes)
+    return out.getvalue()
+
+
+def quantized_size_bytes(q: QuantizedModel) -> int:
+    """quantized_size_bytes (compress.hpp:563-573)."""
+    n = 4 + 4 + 8 + 8 + 8 + 1 + 8 + sum(8 + len(w.encode()) for w in q.words)
+    return n + sum(12 + len(m.codes) for m in q.mats)
+
+
+def read_quantized(data_or_reader) -> QuantizedModel:
+    """read_quantized (compress.hpp:588-617)."""
+    r = data_or_reader if isinstance(data_or_reader, Reader) else Reader(data_or_reader)
+    r.magic("RNQZ", "quantized model")
+    ver = r.u32()
+    if ver != QUANTIZED_FORMAT_VERSION:
+        raise DataError(f"quantized model: unsupported version {ver}")
+    V, H, P = r.u64(), r.u64(), r.u64()
+    if V < 1 or H < 1 or P < 1 or P > H or V > (1 << 26) or H > (1 << 20):
+        raise DataError("quantized model: implausible dimensions")
+    act = r.u8()
+    n = r.u64()
+    if n != V:
+        raise DataError("quantized model: vocabulary size mismatch")
+    words = [r.string() for _ in range(n)]
+    mats = []
+    for rows, cols in ((V, P), (P, H), (H, H), (H, P)):
+        bits = r.u32()
+        if bits < 1 or bits > 16:
+            raise DataError("quantized model: bits out of range")
+        mn = struct.unpack("<f", r.take(4))[0]
+        mx = struct.unpack("<f", r.take(4))[0]
+        nbytes = (rows * cols * bits + 7) // 8
+        try:
+            codes = r.take(nbytes)
+        except DataError:
+            raise DataError("quantized model: truncated payload")
+        mats.append(QuantizedMatrix(rows, cols, bits, mn, mx, codes))
+    return QuantizedModel(V, H, P, act, mats[0].bits, tuple(mats), words)
 
 
 # ---------------------------------------------------------- mt19937_64 text

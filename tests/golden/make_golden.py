@@ -178,6 +178,19 @@ def write_ln_z(ref, out):
                         stats=ref.last_drift_stats)
 
 
+def write_rnqz(ref, out):
+    """RNQZ bytes (quantize_model + write_quantized) and the dequantized
+    parameters of a bottleneck model at several bit widths."""
+    params = ref.bn_init_uniform(120, 24, 16, 61)
+    d = dict(e=params[0], u=params[1], w_rec=params[2], d=params[3])
+    for bits in (3, 8, 13):
+        blob, dq = ref.bn_quantize(params, bits, act=1)
+        d[f"rnqz_{bits}"] = np.frombuffer(blob, np.uint8)
+        for k, m in zip(("e", "u", "w_rec", "d"), dq):
+            d[f"dq_{bits}_{k}"] = m
+    np.savez_compressed(os.path.join(out, "rnqz.npz"), **d)
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -221,6 +234,7 @@ def main():
     write_bn_train(ref, out)
     write_bn_nce(ref, out)
     write_ln_z(ref, out)
+    write_rnqz(ref, out)
     print("golden fixtures written to", out)
 
 

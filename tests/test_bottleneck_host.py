@@ -49,3 +49,23 @@ def test_rnbl_rbop_bytes_match_reference(path):
         assert np.array_equal(a, b)
     with pytest.raises(formats.DataError):
         formats.read_bottleneck(b"RNLM" + rnbl[4:])
+
+
+@pytest.mark.parametrize("bits", [3, 8, 13])
+def test_rnqz_bytes_and_dequantization_match_reference(bits):
+    """quantize_model / write_quantized / read_quantized / dequantize_model
+    (compress.hpp:417-617) against the reference's bytes and values."""
+    from paper_1502_00512_b200 import formats, make_vocab
+    g = np.load(os.path.join(GOLD, "rnqz.npz"))
+    params = (g["e"], g["u"], g["w_rec"], g["d"])
+    q = formats.quantize_model(params, make_vocab(params[0].shape[0]), bits, act=1)
+    blob = formats.write_quantized(q)
+    assert blob == g[f"rnqz_{bits}"].tobytes()
+    assert formats.quantized_size_bytes(q) == len(blob)
+    q2 = formats.read_quantized(blob)
+    dq, act, words = formats.dequantize_model(q2)
+    assert act == 1 and words == make_vocab(params[0].shape[0])
+    for a, k in zip(dq, ("e", "u", "w_rec", "d")):
+        assert np.array_equal(a, g[f"dq_{bits}_{k}"]), k
+    with pytest.raises(formats.DataError):
+        formats.read_quantized(blob[:-3])

@@ -333,3 +333,22 @@ def test_bn_trainer_nce_matches_reference_fixture():
     t2 = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"])
     t2.load_checkpoint(blob)
     assert t2.save_checkpoint() == blob
+
+
+@pytest.mark.parametrize("bits", [3, 8, 13])
+def test_rnqz_device_dequantization_bitexact(bits, orc):
+    """RNQZ -> device dequantisation (dl_bn_set_params_quantized) gives the
+    reference's dequantized parameters bit for bit; the scorer then runs on
+    them (sharded perplexity vs the oracle)."""
+    from paper_1502_00512_b200 import bottleneck as bn, formats
+    g = np.load(os.path.join(GOLD, "rnqz.npz"))
+    q = formats.read_quantized(g[f"rnqz_{bits}"].tobytes())
+    m = bn.GpuBottleneck(q.v, q.h, q.p, q.act, "fp32")
+    m.set_params_quantized(q)
+    got = m.params()
+    for a, k in zip(got, ("e", "u", "w_rec", "d")):
+        assert np.array_equal(a, g[f"dq_{bits}_{k}"]), k
+    ids = orc.random_stream(5, q.v, 2000)
+    want = orc.bn_sharded_ppl(got, q.act, ids, 8)
+    r = bn.bn_sharded_perplexity(m, ids, 8)
+    assert r.perplexity == pytest.approx(want["perplexity"], rel=1e-4)
