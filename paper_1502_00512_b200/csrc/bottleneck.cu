@@ -36,7 +36,9 @@
 #include <cfloat>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <random>
+#include <tuple>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -118,6 +120,11 @@ struct dl_bn {
   EmbedWs nce_ws{};
   uint8_t* touched = nullptr;  // [V] rows of the sparse embedding gradient
   bool e_sparse = false;       // the last window's embedding gradient is sparse
+  // softmax-mode training windows replay one CUDA graph per (T, B, scale,
+  // clip, eta); buffers are sized by an eager run first
+  std::map<std::tuple<int64_t, int64_t, double, float, double>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int64_t, int64_t, double, float, double>, uint64_t> graph_launches;
+  bool use_graphs = true;
 };
 
 namespace {
@@ -300,9 +307,16 @@ void mm(dl_bn* c, int M, int N, int K, int am, const void* A, int64_t lda, int b
 }
 
 // ------------------------------------------------------------- buffers
+void drop_graphs(dl_bn* c) {
+  for (auto& kv : c->graphs)
+    if (kv.second) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();
+}
+
 void ensure_window(dl_bn* c, int64_t T, int64_t N) {
   if (N <= c->capN && T <= c->capT) return;
   DL_CUDA(cudaStreamSynchronize(c->st));
+  drop_graphs(c);
   const int64_t n = std::max(N, c->capN), t = std::max(T, c->capT);
   const int64_t H = c->H, P = c->P, V = c->V;
   for (void** p : {(void**)&c->x, (void**)&c->y, (void**)&c->iota, (void**)&c->w,
@@ -721,6 +735,7 @@ int dl_bn_destroy(dl_bn* c) {
   if (!c) return DL_OK;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
+  drop_graphs(c);
   for (void* p : {(void*)c->e, (void*)c->u, (void*)c->w_rec, (void*)c->d, (void*)c->e_bf,
                   (void*)c->u_bf, (void*)c->w_rec_bf, (void*)c->d_bf, (void*)c->m_e,
                   (void*)c->m_u, (void*)c->m_rec, (void*)c->m_d, (void*)c->g_e, (void*)c->g_u,
@@ -829,10 +844,16 @@ int dl_bn_get_opt(dl_bn* c, float* m_e, float* m_u, float* m_rec, float* m_d) {
   });
 }
 
-int dl_bn_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
-                 const uint32_t* targets, const uint8_t* weights, const float* h0,
-                 float* h_final, double loss_scale, float clip, int compute_grads, double* loss,
-                 uint64_t* positions) {
+}  // extern "C"
+
+namespace {
+// dl_bn_window / dl_bn_train_window: validate, copy the window in, run it
+// (+ bottleneck_update when eta > 0) and read loss, positions, the update's
+// verdict and h_final back with one synchronisation.
+int bn_window_call(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
+                   const uint32_t* targets, const uint8_t* weights, const float* h0,
+                   float* h_final, double loss_scale, float clip, bool grads, double eta,
+                   double* loss, uint64_t* positions, int* applied) {
   if (!c) return bn_fail(c, DL_EINVAL, "dl_bn_window: null ctx");
   if (T < 1 || B < 1) return bn_fail(c, DL_EINVAL, "bptt: empty window");
   if (!inputs || !targets || !weights || !h0)
@@ -865,18 +886,62 @@ int dl_bn_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
     DL_CUDA(cudaMemcpyAsync(c->y, targets, N * 4, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->w, weights, N, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->htape, h0, B * c->H * 4, cudaMemcpyHostToDevice, st));
-    run_window(c, T, B, loss_scale, clip, compute_grads != 0);
-    double l = 0.0;
-    unsigned long long p = 0;
-    DL_CUDA(cudaMemcpyAsync(&l, c->d_loss, sizeof l, cudaMemcpyDeviceToHost, st));
-    DL_CUDA(cudaMemcpyAsync(&p, c->d_pos, sizeof p, cudaMemcpyDeviceToHost, st));
+    auto body = [&] {
+      run_window(c, T, B, loss_scale, clip, grads);
+      if (grads && eta > 0.0) run_update(c, eta);
+    };
+    // softmax training windows: one graph per shape/hyper-parameters, after
+    // an eager run has sized every buffer
+    const auto key = std::make_tuple(T, B, loss_scale, clip, eta);
+    const bool graphable = c->use_graphs && c->loss_mode == 1 && grads && eta > 0.0;
+    auto it = graphable ? c->graphs.find(key) : c->graphs.end();
+    if (it != c->graphs.end()) {
+      DL_CUDA(cudaGraphLaunch(it->second, st));
+      c->launches += c->graph_launches[key];
+      c->e_sparse = false;
+      c->have_grads = true;
+    } else if (graphable && c->graphs.count(std::make_tuple(T, B, -1.0, 0.f, 0.0))) {
+      cudaGraph_t gr = nullptr;
+      const uint64_t l0 = c->launches;
+      DL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      body();
+      DL_CUDA(cudaStreamEndCapture(st, &gr));
+      c->graph_launches[key] = c->launches - l0;
+      cudaGraphExec_t ex = nullptr;
+      DL_CUDA(cudaGraphInstantiate(&ex, gr, 0));
+      cudaGraphDestroy(gr);
+      c->graphs[key] = ex;
+      DL_CUDA(cudaGraphLaunch(ex, st));
+    } else {
+      body();
+      // (a marker: this shape has run eagerly, so its buffers are sized)
+      if (graphable) c->graphs[std::make_tuple(T, B, -1.0, 0.f, 0.0)] = nullptr;
+    }
+    struct { double l; unsigned long long p; int bad; } res{};
+    DL_CUDA(cudaMemcpyAsync(&res.l, c->d_loss, sizeof res.l, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaMemcpyAsync(&res.p, c->d_pos, sizeof res.p, cudaMemcpyDeviceToHost, st));
+    if (grads && eta > 0.0)
+      DL_CUDA(cudaMemcpyAsync(&res.bad, c->nonfinite, sizeof res.bad, cudaMemcpyDeviceToHost, st));
     if (h_final)
       DL_CUDA(cudaMemcpyAsync(h_final, c->htape + T * B * c->H, B * c->H * 4,
                               cudaMemcpyDeviceToHost, st));
     DL_CUDA(cudaStreamSynchronize(st));
-    if (loss) *loss = l;
-    if (positions) *positions = p;
+    if (eta > 0.0) c->have_grads = false;
+    if (loss) *loss = res.l;
+    if (positions) *positions = res.p;
+    if (applied) *applied = res.bad ? 0 : 1;
   });
+}
+}  // namespace
+
+extern "C" {
+
+int dl_bn_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
+                 const uint32_t* targets, const uint8_t* weights, const float* h0,
+                 float* h_final, double loss_scale, float clip, int compute_grads, double* loss,
+                 uint64_t* positions) {
+  return bn_window_call(c, T, B, inputs, targets, weights, h0, h_final, loss_scale, clip,
+                        compute_grads != 0, 0.0, loss, positions, nullptr);
 }
 
 int dl_bn_get_grads(dl_bn* c, float* g_e, float* g_u, float* g_rec, float* g_d) {
@@ -908,10 +973,9 @@ int dl_bn_train_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
                        const uint32_t* targets, const uint8_t* weights, const float* h0,
                        float* h_final, double loss_scale, float clip, double eta, double* loss,
                        uint64_t* positions, int* applied) {
-  const int rc = dl_bn_window(c, T, B, inputs, targets, weights, h0, h_final, loss_scale, clip, 1,
-                              loss, positions);
-  if (rc != DL_OK) return rc;
-  return dl_bn_rmsprop(c, eta, applied);
+  if (!(eta > 0.0)) return bn_fail(c, DL_EINVAL, "config: eta must be > 0");
+  return bn_window_call(c, T, B, inputs, targets, weights, h0, h_final, loss_scale, clip, true,
+                        eta, loss, positions, applied);
 }
 
 // sharded_perplexity over the bottleneck adapter (eval.hpp:151-222): S
