@@ -138,6 +138,13 @@ int dl_rnn_perplexity(dl_ctx* ctx, const uint32_t* ids, int64_t n,
 int dl_ln_z_samples(dl_ctx* ctx, const uint32_t* ids, int64_t n, int64_t count, double* out,
                     int64_t* n_out);
 
+/* RnnHitScorer (eval.hpp:476-510) over one stream: after each input id
+ * in[j], the raw scores float(h . W_out[w]) (8-lane double dot, as
+ * Adapter::score) of the candidates cand[j*K .. j*K+K) (-1 = none) into
+ * out[j*K + k]; the host ranks them (hit_rate, eval.hpp:544-592). */
+int dl_score_candidates(dl_ctx* ctx, const uint32_t* in, int64_t steps, int64_t K,
+                        const int64_t* cand, float* out);
+
 /* ---- device-resident trainer (Trainer<Traits>::run_epoch) -------------- */
 
 /* Uploads the training IdStream once and sets up the offset-stream schedule

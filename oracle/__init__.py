@@ -657,6 +657,62 @@ class Ref(_Backend):
                       buf.ctypes.data, cap, C.byref(ln), logs, C.byref(nl), C.byref(ini)))
         return bytes(buf[: ln.value]), logs[: nl.value].copy(), ini.value
 
+    def ngram_query(self, train, V, order, contexts, words, k, eval_ids):
+        """count_ngrams + estimate_kn, then logprob / shortlist per query and
+        ngram_perplexity_full of eval_ids."""
+        ctx_len = max(1, max((len(c) for c in contexts), default=1))
+        nq = len(words)
+        ctx = np.full((nq, ctx_len), -1, np.int64)
+        for i, c in enumerate(contexts):
+            if len(c):
+                ctx[i, ctx_len - len(c):] = c
+        words = np.ascontiguousarray(words, np.uint32)
+        logp = np.empty(nq, np.float64)
+        sl = np.empty((nq, k), np.uint32)
+        ppl = np.empty(3, np.float64)
+        tr = np.ascontiguousarray(train, np.uint32)
+        ev = np.ascontiguousarray(eval_ids, np.uint32)
+        f = self.lib.ref_ngram_query
+        f.argtypes = [_u32p, _i64, _i64, C.c_int, _i64, C.c_int, _vp, _u32p, _vp, C.c_int, _vp,
+                      _u32p, _i64, _vp]
+        self._check(f(tr, len(tr), V, order, nq, ctx_len, ctx.ctypes.data, words,
+                      logp.ctypes.data, k, sl.ctypes.data, ev, len(ev), ppl.ctypes.data))
+        return logp, [list(r[r != 0xffffffff]) for r in sl], ppl
+
+    def interp_terms(self, params, act, Vf, train, order, eval_ids):
+        """interpolation_terms + tune_lambda (RNN vocabulary make_vocab(Vr),
+        n-gram vocabulary make_vocab(Vf))."""
+        w_in, w_rec, w_out = params
+        Vr, H = w_in.shape
+        tr = np.ascontiguousarray(train, np.uint32)
+        ev = np.ascontiguousarray(eval_ids, np.uint32)
+        a = np.empty(len(ev), np.float64)
+        b = np.empty(len(ev), np.float64)
+        nt = C.c_int64()
+        lp = np.empty(2, np.float64)
+        f = self.lib.ref_interp_terms
+        f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _i64, _u32p, _i64, C.c_int,
+                      _u32p, _i64, _vp, _vp, C.POINTER(C.c_int64), _vp]
+        self._check(f(Vr, H, act, w_in, w_rec, w_out, Vf, tr, len(tr), order, ev, len(ev),
+                      a.ctypes.data, b.ctypes.data, C.byref(nt), lp.ctypes.data))
+        n = nt.value
+        return a[:n].copy(), b[:n].copy(), float(lp[0]), float(lp[1])
+
+    def hit_rate(self, params, act, train, order, eval_ids, shortlist_k, top_k, kind):
+        """hit_rate with RnnHitScorer (kind 0) or NgramHitScorer (kind 1)."""
+        w_in, w_rec, w_out = params
+        V, H = w_in.shape
+        tr = np.ascontiguousarray(train, np.uint32)
+        ev = np.ascontiguousarray(eval_ids, np.uint32)
+        pos, hits = C.c_uint64(), C.c_uint64()
+        f = self.lib.ref_hit_rate
+        f.argtypes = [_i64, _i64, C.c_int, _f32p, _f32p, _f32p, _u32p, _i64, C.c_int, _u32p,
+                      _i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                      C.POINTER(C.c_uint64)]
+        self._check(f(V, H, act, w_in, w_rec, w_out, tr, len(tr), order, ev, len(ev),
+                      shortlist_k, top_k, kind, C.byref(pos), C.byref(hits)))
+        return pos.value, hits.value
+
     def bn_quantize(self, params, bits, act=0):
         """quantize_model + write_quantized (RNQZ bytes) and the dequantized
         parameters of read_quantized + dequantize_model."""

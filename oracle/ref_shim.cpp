@@ -834,4 +834,94 @@ int ref_bn_quantize(std::int64_t V, std::int64_t H, std::int64_t P, int act, con
   });
 }
 
+// ----- n-gram side of the interpolation / hit-rate scorers (ngram.hpp,
+// eval.hpp:231-592) -----
+//   ref_ngram_query   count_ngrams + estimate_kn over a training stream
+//                     (make_vocab(V)), then logprob(ctx, w) for each query
+//                     (contexts: ctx_len ids each, -1 padded on the left) and
+//                     shortlist(ctx, k) per context
+//   ref_interp_terms  interpolation_terms + tune_lambda (RNN vocabulary
+//                     make_vocab(Vr), n-gram vocabulary make_vocab(Vf))
+//   ref_hit_rate      hit_rate with RnnHitScorer (kind 0) or NgramHitScorer (1)
+
+static NGramModel build_ngram(const std::uint32_t* train, std::int64_t n_train, std::int64_t V,
+                              int order) {
+  IdStream tr;
+  tr.ids.assign(train, train + n_train);
+  return estimate_kn(count_ngrams(tr, order), testutil::make_vocab(V));
+}
+
+int ref_ngram_query(const std::uint32_t* train, std::int64_t n_train, std::int64_t V, int order,
+                    std::int64_t nq, int ctx_len, const std::int64_t* ctx,
+                    const std::uint32_t* words, double* logp, int k, std::uint32_t* shortlists,
+                    const std::uint32_t* eval, std::int64_t n_eval, double* ppl) {
+  return guarded([&] {
+    const NGramModel m = build_ngram(train, n_train, V, order);
+    for (std::int64_t q = 0; q < nq; ++q) {
+      std::vector<WordId> c;
+      for (int i = 0; i < ctx_len; ++i)
+        if (ctx[q * ctx_len + i] >= 0) c.push_back(static_cast<WordId>(ctx[q * ctx_len + i]));
+      logp[q] = m.logprob(c, words[q]);
+      const std::vector<WordId> sl = m.shortlist(c, static_cast<std::size_t>(k));
+      for (int i = 0; i < k; ++i)
+        shortlists[q * k + i] = i < (int)sl.size() ? sl[i] : 0xffffffffu;
+    }
+    IdStream ev;
+    ev.ids.assign(eval, eval + n_eval);
+    const PerplexityResult r = ngram_perplexity_full(m, ev);
+    ppl[0] = r.total_logprob;
+    ppl[1] = static_cast<double>(r.predicted);
+    ppl[2] = r.perplexity;
+  });
+}
+
+int ref_interp_terms(std::int64_t Vr, std::int64_t H, int act, const float* w_in,
+                     const float* w_rec, const float* w_out, std::int64_t Vf,
+                     const std::uint32_t* train, std::int64_t n_train, int order,
+                     const std::uint32_t* eval, std::int64_t n_eval, double* a, double* b,
+                     std::int64_t* n_terms, double* lambda_ppl) {
+  return guarded([&] {
+    const RnnParams<float> p = make_params(Vr, H, act, w_in, w_rec, w_out);
+    StandardAdapter<float> ad(p);
+    const NGramModel m = build_ngram(train, n_train, Vf, order);
+    const VocabMap map = make_vocab_map(testutil::make_vocab(Vr), testutil::make_vocab(Vf));
+    IdStream ev;
+    ev.ids.assign(eval, eval + n_eval);
+    const std::vector<InterpTerm> t = interpolation_terms(ad, map, m, ev);
+    *n_terms = static_cast<std::int64_t>(t.size());
+    for (std::size_t i = 0; i < t.size(); ++i) {
+      a[i] = t[i].a;
+      b[i] = t[i].b;
+    }
+    double best = 0.0;
+    lambda_ppl[0] = tune_lambda(t, &best);
+    lambda_ppl[1] = best;
+  });
+}
+
+int ref_hit_rate(std::int64_t V, std::int64_t H, int act, const float* w_in, const float* w_rec,
+                 const float* w_out, const std::uint32_t* train, std::int64_t n_train, int order,
+                 const std::uint32_t* eval, std::int64_t n_eval, int shortlist_k, int top_k,
+                 int kind, std::uint64_t* positions, std::uint64_t* hits) {
+  return guarded([&] {
+    const NGramModel m = build_ngram(train, n_train, V, order);
+    IdStream ev;
+    ev.ids.assign(eval, eval + n_eval);
+    HitRateResult r;
+    if (kind == 0) {
+      const RnnParams<float> p = make_params(V, H, act, w_in, w_rec, w_out);
+      StandardAdapter<float> ad(p);
+      RnnHitScorer<StandardAdapter<float>> sc(ad);
+      r = hit_rate(ev, m, static_cast<std::size_t>(shortlist_k),
+                   static_cast<std::size_t>(top_k), sc);
+    } else {
+      NgramHitScorer sc(m);
+      r = hit_rate(ev, m, static_cast<std::size_t>(shortlist_k),
+                   static_cast<std::size_t>(top_k), sc);
+    }
+    *positions = r.positions;
+    *hits = r.hits;
+  });
+}
+
 }  // extern "C"

@@ -23,7 +23,7 @@ EXPORTS = (
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
     "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
     "dl_local_group_destroy", "dl_comm_init_local", "dl_set_vocab_shard",
-    "dl_ln_z_samples", "dl_set_loss_mode", "dl_set_noise", "dl_set_rng_state", "dl_get_rng_state",
+    "dl_ln_z_samples", "dl_score_candidates", "dl_set_loss_mode", "dl_set_noise", "dl_set_rng_state", "dl_get_rng_state",
     "dl_rng_seed_state", "dl_bn_create", "dl_bn_destroy", "dl_bn_last_error",
     "dl_bn_set_params", "dl_bn_get_params", "dl_bn_set_opt", "dl_bn_get_opt", "dl_bn_window",
     "dl_bn_get_grads", "dl_bn_rmsprop", "dl_bn_train_window", "dl_bn_sharded_perplexity",
@@ -78,6 +78,7 @@ def load():
         "dl_rnn_perplexity": (C.c_int, [vp, vp, i64, C.c_uint32, P(C.c_double),
                                         P(C.c_uint64), P(C.c_double)]),
         "dl_ln_z_samples": (C.c_int, [vp, vp, i64, i64, vp, P(C.c_int64)]),
+        "dl_score_candidates": (C.c_int, [vp, vp, i64, i64, vp, vp]),
         "dl_trainer_init": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_uint32]),
         "dl_trainer_run": (C.c_int, [vp, i64, i64, C.c_double, P(C.c_double),

@@ -1665,6 +1665,69 @@ int dl_ln_z_samples(dl_ctx* c, const uint32_t* ids, int64_t n, int64_t count, do
   });
 }
 
+// RnnHitScorer::score over a single stream (eval.hpp:476-510): after each
+// input id, the raw scores float(dot_acc(h, W_out[w])) of up to K candidate
+// words (cand[j*K + k], -1 = none) -- the NCE score kernel's 8-lane double
+// dot product, bit-identical to the reference's Adapter::score.
+int dl_score_candidates(dl_ctx* c, const uint32_t* in, int64_t steps, int64_t K,
+                        const int64_t* cand, float* out) {
+  if (!c) return fail(c, DL_EINVAL, "dl_score_candidates: null ctx");
+  if (!in || steps < 1 || K < 1 || !cand || !out)
+    return fail(c, DL_EINVAL, "dl_score_candidates: bad arguments");
+  if (c->vshard) return fail(c, DL_EINVAL, "dl_score_candidates: not on a vocabulary-sharded context");
+  for (int64_t i = 0; i < steps; ++i)
+    if (in[i] >= (uint64_t)c->V) return fail(c, DL_EDATA, "hit rate: id out of vocabulary range");
+  for (int64_t i = 0; i < steps * K; ++i)
+    if (cand[i] >= c->V) return fail(c, DL_EDATA, "hit rate: candidate out of vocabulary range");
+  return guarded(c, [&] {
+    const int64_t H = c->H;
+    const int64_t bank = std::min<int64_t>(steps, 4096);
+    ensure_window(c, bank, 1);
+    cudaStream_t st = c->st;
+    uint32_t* rw = dalloc<uint32_t>(bank * K);
+    uint32_t* rr = dalloc<uint32_t>(bank * K);
+    float* sc = dalloc<float>(bank * K);
+    std::vector<uint32_t> hw, hr;
+    std::vector<int64_t> slot;
+    std::vector<float> hs;
+    fill_f32(c->htape, act0(c->act), H, st);
+    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
+      const int64_t nb = std::min(bank, steps - j0);
+      DL_CUDA(cudaMemcpyAsync(c->x_d, in + j0, nb * 4, cudaMemcpyHostToDevice, st));
+      if (tc(c)) f32_to_bf16(c->htape, c->htape_bf, H, st);
+      for (int64_t t = 0; t < nb; ++t)
+        rec_step_fwd(c, 1, c->htape + t * H, tc(c) ? c->htape_bf + t * H : nullptr, c->x_d + t,
+                     c->htape + (t + 1) * H, tc(c) ? c->htape_bf + (t + 1) * H : nullptr);
+      hw.clear();
+      hr.clear();
+      slot.clear();
+      for (int64_t t = 0; t < nb; ++t)
+        for (int64_t k = 0; k < K; ++k) {
+          const int64_t w = cand[(j0 + t) * K + k];
+          if (w < 0) continue;
+          hw.push_back((uint32_t)w);
+          hr.push_back((uint32_t)(t + 1));  // htape row of the state after in[j0+t]
+          slot.push_back((j0 + t) * K + k);
+        }
+      const int64_t N = (int64_t)hw.size();
+      if (N > 0) {
+        DL_CUDA(cudaMemcpyAsync(rw, hw.data(), N * 4, cudaMemcpyHostToDevice, st));
+        DL_CUDA(cudaMemcpyAsync(rr, hr.data(), N * 4, cudaMemcpyHostToDevice, st));
+        nce_scores(c->htape, c->w_out, H, rw, rr, N, sc, st);
+        c->launches++;
+        hs.resize(N);
+        DL_CUDA(cudaMemcpyAsync(hs.data(), sc, N * 4, cudaMemcpyDeviceToHost, st));
+      }
+      DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * H, H * 4, cudaMemcpyDeviceToDevice, st));
+      DL_CUDA(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < N; ++i) out[slot[i]] = hs[i];
+    }
+    cudaFree(rw);
+    cudaFree(rr);
+    cudaFree(sc);
+  });
+}
+
 // RnnParams::init_uniform (rnn.hpp:79-83): one std::mt19937_64(seed), w_in
 // then w_rec then w_out, each element float(lo + (hi - lo) * u) with
 // u = (rng() >> 11) * 2^-53 (rng.hpp:37-44).  Pure host code; bit-exact.

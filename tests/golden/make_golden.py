@@ -191,6 +191,42 @@ def write_rnqz(ref, out):
     np.savez_compressed(os.path.join(out, "rnqz.npz"), **d)
 
 
+def write_ngram_scorers(ref, out):
+    """n-gram model queries (count_ngrams + estimate_kn + logprob /
+    shortlist / perplexity), interpolation terms + tune_lambda, and shortlist
+    hit rates with both scorers, from the reference."""
+    Vf, Vr, H, order = 90, 70, 16, 3
+    train = ref.random_stream(21, Vf, 30000)
+    evals = ref.random_stream(22, Vf, 1500)
+    rng = np.random.default_rng(23)
+    ctxs = [list(rng.integers(0, Vf, rng.integers(0, 4))) for _ in range(300)]
+    words = rng.integers(0, Vf, 300).astype(np.uint32)
+    ctx_arr = np.full((300, 3), -1, np.int64)
+    for i, c in enumerate(ctxs):
+        if len(c):
+            ctx_arr[i, 3 - len(c):] = c
+    d = dict(Vf=Vf, Vr=Vr, H=H, order=order, train=train, eval=evals, ctx=ctx_arr, words=words)
+    for o in (1, 2, 3, 4):
+        lp, sls, ppl = ref.ngram_query(train, Vf, o, ctxs, words, 12, evals)
+        d[f"logp_{o}"] = lp
+        d[f"shortlist_{o}"] = np.array([sl + [-1] * (12 - len(sl)) for sl in sls], np.int64)
+        d[f"ppl_{o}"] = ppl
+    params = ref.init_uniform(Vr, H, 24)
+    d.update(w_in=params[0], w_rec=params[1], w_out=params[2])
+    a, b, lam, best = ref.interp_terms(params, 0, Vf, train, order, evals)
+    d.update(interp_a=a, interp_b=b, interp_lambda=lam, interp_ppl=best)
+    # hit rate over the full vocabulary model (V = Vf)
+    params_f = ref.init_uniform(Vf, H, 25)
+    d.update(hw_in=params_f[0], hw_rec=params_f[1], hw_out=params_f[2])
+    hits = []
+    for sk, tk in ((10, 1), (20, 5)):
+        for kind in (0, 1):
+            pos, h = ref.hit_rate(params_f, 0, train, order, evals, sk, tk, kind)
+            hits.append([sk, tk, kind, pos, h])
+    d["hits"] = np.array(hits, np.int64)
+    np.savez_compressed(os.path.join(out, "ngram_scorers.npz"), **d)
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -235,6 +271,7 @@ def main():
     write_bn_nce(ref, out)
     write_ln_z(ref, out)
     write_rnqz(ref, out)
+    write_ngram_scorers(ref, out)
     print("golden fixtures written to", out)
 
 
