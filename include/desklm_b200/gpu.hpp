@@ -156,6 +156,109 @@ PerplexityResult rnn_perplexity(Model& m, const IdStream& s, std::uint32_t bos =
   return r;
 }
 
+// ----------------------------------------------- bottleneck model
+// BottleneckParams<float> + BottleneckAdapter on the device (compress.hpp:
+// 38-415).  Params: any type with v, h, p, act and Mat-like e, u, w_rec, d
+// (desklm::BottleneckParams<float> fits).
+inline void check_bn(int rc, const dl_bn* ctx) {
+  if (rc == DL_OK) return;
+  const std::string msg = dl_bn_last_error(ctx);
+  if (rc == DL_EINVAL) throw std::invalid_argument(msg);
+  if (rc == DL_EDATA) throw DataError(msg);
+  throw std::runtime_error(msg);
+}
+
+class BottleneckModel {
+ public:
+  BottleneckModel(std::int64_t V, std::int64_t H, std::int64_t P, int act = DL_SIGMOID,
+                  Precision prec = Precision::kBf16, int device = 0)
+      : v_(V), h_(H), p_(P) {
+    check_bn(dl_bn_create(&ctx_, device, V, H, P, act, static_cast<int>(prec)), nullptr);
+  }
+  template <class Params>
+  explicit BottleneckModel(const Params& params, Precision prec = Precision::kBf16,
+                           int device = 0)
+      : BottleneckModel(params.v, params.h, params.p, static_cast<int>(params.act), prec,
+                        device) {
+    upload(params);
+  }
+  BottleneckModel(const BottleneckModel&) = delete;
+  BottleneckModel& operator=(const BottleneckModel&) = delete;
+  ~BottleneckModel() { dl_bn_destroy(ctx_); }
+
+  dl_bn* get() const { return ctx_; }
+  std::int64_t vocab() const { return v_; }
+  std::int64_t hidden() const { return h_; }
+  std::int64_t proj() const { return p_; }
+
+  template <class Params>
+  void upload(const Params& p) {
+    check_bn(dl_bn_set_params(ctx_, p.e.a.data(), p.u.a.data(), p.w_rec.a.data(), p.d.a.data()),
+             ctx_);
+  }
+  template <class Params>
+  void download(Params& p) const {
+    check_bn(dl_bn_get_params(ctx_, p.e.a.data(), p.u.a.data(), p.w_rec.a.data(), p.d.a.data()),
+             ctx_);
+  }
+  void set_opt(const float* m_e, const float* m_u, const float* m_rec, const float* m_d,
+               double rho, double eps) {
+    check_bn(dl_bn_set_opt(ctx_, m_e, m_u, m_rec, m_d, rho, eps), ctx_);
+  }
+
+ private:
+  dl_bn* ctx_ = nullptr;
+  std::int64_t v_, h_, p_;
+};
+
+// bptt_run over the bottleneck adapter (softmax mode unless
+// dl_bn_set_loss_mode switched the context to NCE).
+template <class WindowBatch, class MatF>
+BpttResult bptt_run(BottleneckModel& m, const WindowBatch& wb, const MatF& h0, MatF* h_final,
+                    double loss_scale, float clip, bool compute_grads = true) {
+  BpttResult r;
+  std::uint64_t pos = 0;
+  if (h_final) h_final->a.resize(static_cast<std::size_t>(wb.B * m.hidden()));
+  check_bn(dl_bn_window(m.get(), wb.T, wb.B, wb.inputs.data(), wb.targets.data(),
+                        wb.weights.data(), h0.a.data(), h_final ? h_final->a.data() : nullptr,
+                        loss_scale, clip, compute_grads ? 1 : 0, &r.loss, &pos),
+           m.get());
+  r.positions = pos;
+  return r;
+}
+
+// bottleneck_update (compress.hpp:296-309): false = rejected non-finite gradient.
+inline bool bottleneck_update(BottleneckModel& m, double eta) {
+  int applied = 0;
+  check_bn(dl_bn_rmsprop(m.get(), eta, &applied), m.get());
+  return applied != 0;
+}
+
+template <class IdStream>
+PerplexityResult sharded_perplexity(BottleneckModel& m, const IdStream& s, int shards,
+                                    std::uint32_t bos = 1) {
+  PerplexityResult r;
+  std::uint64_t pred = 0;
+  check_bn(dl_bn_sharded_perplexity(m.get(), s.ids.data(),
+                                    static_cast<std::int64_t>(s.ids.size()), shards, bos,
+                                    &r.total_logprob, &pred, &r.perplexity),
+           m.get());
+  r.predicted = pred;
+  return r;
+}
+
+// ln_z_samples (eval.hpp:805-857) for the standard model.
+template <class IdStream>
+std::vector<double> ln_z_samples(Model& m, const IdStream& s, std::size_t count) {
+  std::vector<double> out(count);
+  std::int64_t n = 0;
+  check(dl_ln_z_samples(m.get(), s.ids.data(), static_cast<std::int64_t>(s.ids.size()),
+                        static_cast<std::int64_t>(count), out.data(), &n),
+        m.get());
+  out.resize(static_cast<std::size_t>(n));
+  return out;
+}
+
 // ----------------------------------------------------- binary primitives
 namespace io {
 inline void u8(std::ostream& o, std::uint8_t v) { o.put(static_cast<char>(v)); }

@@ -58,3 +58,36 @@ def test_cpp_trainer_matches_python_and_oracle(tmp_path, orc):
     g = orc.bptt(params, 0, x, y, w, np.full((B, H), 0.5, np.float32), 1.0 / (T * B), 1.0)
     assert float(loss) == pytest.approx(g["loss"], rel=1e-4)
     assert int(pos) == g["positions"] and int(ok) == 1
+
+
+@pytest.mark.gpu
+def test_cpp_bottleneck_matches_python(tmp_path, orc):
+    """The C++ BottleneckModel API (bptt_run / bottleneck_update /
+    sharded_perplexity overloads) gives the Python API's numbers."""
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], check=True,
+                   capture_output=True)
+    V, H, P, T, B, windows, eta = 80, 16, 8, 5, 4, 3, 0.01
+    params = orc.bn_init_uniform(V, H, P, 7)
+    ids = orc.random_stream(3, V, (windows + 1) * T * B + 1)[: (windows + 1) * T * B + 1]
+    np.concatenate([p.ravel() for p in params]).astype(np.float32).tofile(tmp_path / "params.f32")
+    ids.astype(np.uint32).tofile(tmp_path / "ids.u32")
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "bn_example")
+    r = subprocess.run([exe, str(tmp_path), str(V), str(H), str(P), str(T), str(B), str(windows),
+                        str(eta)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.split()
+    m = bn.GpuBottleneck(V, H, P, 0, "fp32")
+    m.set_params(*params)
+    h = np.full((B, H), 0.5, np.float32)
+    for w in range(windows):
+        x = ids[w * T * B:(w + 1) * T * B].reshape(T, B)
+        y = ids[w * T * B + 1:(w + 1) * T * B + 1].reshape(T, B)
+        res, h, ok = bn.bn_train_window(m, dl.WindowBatch(x, y, (y != 1).astype(np.uint8)), h,
+                                        1.0 / (T * B), 1.0, eta)
+        loss, pos, ok_c = lines[w].split(",")
+        assert float(loss) == res.loss and int(pos) == res.positions and bool(int(ok_c)) == ok
+    ppl, pred = lines[windows].split(",")
+    want = bn.bn_sharded_perplexity(m, ids, 8)
+    assert float(ppl) == want.perplexity and int(pred) == want.predicted
