@@ -221,6 +221,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 // 32 x 32 fp32 chunks (4 KB each, 16-byte units XOR swizzled by row) filled
 // by cp.async, all in flight at once (measured: 3 stages + 4 chunks beat
 // 5 + 2 and 4 + 2/3 by 1-2% on the C3 dW_out).
+#ifndef DL_PAIR_STAGES
+#define DL_PAIR_STAGES 6
+#endif
 #ifndef DL_RMS_STAGES
 #define DL_RMS_STAGES 3
 #endif
@@ -232,7 +235,7 @@ struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2;   // 128 rows of A
   static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = RMS ? DL_RMS_STAGES : 6;
+  static constexpr int STAGES = RMS ? DL_RMS_STAGES : DL_PAIR_STAGES;
   static constexpr int TMEM_COLS = 512;         // 2 accumulator stages x 256 columns
   static constexpr int EPI_OFF = STAGES * STAGE + 256;
   static constexpr int EPI_CHUNK_BYTES = 32 * 32 * 4;
