@@ -135,6 +135,9 @@ __global__ void k_reduce(const float* __restrict__ part, int splits, int64_t spl
 //   loss_row = w ? scale*(lse - s_y) : 0 ;  logp_row = s_y - lse
 //   grads: dS = w ? float(scale*exp(s - lse)) - [w==y] float(scale) : 0
 constexpr int kRowThreads = 512;
+#ifndef DL_SOFTMAX_UNROLL
+#define DL_SOFTMAX_UNROLL 4  // 16-byte loads in flight per thread in the dS pass
+#endif
 
 // Vocabulary-sharded rows: every rank holds a V/G column
 // block of the logits.  lse over the full vocabulary is the log-sum-exp of
@@ -243,19 +246,33 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
     const float lsef = (float)lse, scf = (float)scale;
     const float kLog2e = 1.4426950408889634f;
     if ((V % 8) == 0) {
+      // four 16-byte loads in flight per thread before any store (the row
+      // streams at HBM speed only with enough bytes outstanding)
       uint4* s8 = reinterpret_cast<uint4*>(s);
-      for (int64_t q = threadIdx.x; q < V / 8; q += blockDim.x) {
-        uint4 u = s8[q];
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+      const int64_t n8 = V / 8;
+      constexpr int U = DL_SOFTMAX_UNROLL;
+      for (int64_t q0 = threadIdx.x; q0 < n8; q0 += (int64_t)U * blockDim.x) {
+        uint4 u[U];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float2 f = __bfloat1622float2(h2[k]);
-          const int64_t w0 = q * 8 + 2 * k;
-          f.x = scf * exp2f((f.x - lsef) * kLog2e) - (w0 == y ? scf : 0.f);
-          f.y = scf * exp2f((f.y - lsef) * kLog2e) - (w0 + 1 == y ? scf : 0.f);
-          h2[k] = __float22bfloat162_rn(f);
+        for (int j = 0; j < U; ++j) {
+          const int64_t q = q0 + (int64_t)j * blockDim.x;
+          if (q < n8) u[j] = __ldcs(s8 + q);
         }
-        s8[q] = u;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int64_t q = q0 + (int64_t)j * blockDim.x;
+          if (q >= n8) continue;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u[j]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float2 f = __bfloat1622float2(h2[k]);
+            const int64_t w0 = q * 8 + 2 * k;
+            f.x = scf * exp2f((f.x - lsef) * kLog2e) - (w0 == y ? scf : 0.f);
+            f.y = scf * exp2f((f.y - lsef) * kLog2e) - (w0 + 1 == y ? scf : 0.f);
+            h2[k] = __float22bfloat162_rn(f);
+          }
+          s8[q] = u[j];
+        }
       }
     } else {
       for (int64_t w = threadIdx.x; w < V; w += blockDim.x) {
