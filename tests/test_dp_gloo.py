@@ -96,3 +96,65 @@ def test_dp_decomposition_gloo_world2():
     for k in ("g_rec", "g_out", "g_in_dense"):
         assert out[k] < 1e-5, (k, out[k])
     assert out["hfinal_ok"]
+
+
+def _vshard_worker(rank, world, port, out):
+    """The two vocabulary-parallel exchanges:
+    per-row block log-sum-exps gathered from every rank and combined, the
+    target logit summed from its owner, dS local to the shard, dh summed
+    (vshard) or reduce-scattered over the gathered rows (dp + vocab-parallel
+    output)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(0)
+        M, V, H = 12, 50, 6
+        h = rng.uniform(0, 1, (world * M, H))        # rank-blocked rows (dpv gathers them)
+        w_out = rng.uniform(-1, 1, (V, H))
+        y = rng.integers(0, V, world * M)
+        scale = 1.0 / (world * M)
+        # rank r owns rows [r V / G, (r+1) V / G) of W_out (dl_set_vocab_shard)
+        v0, v1 = rank * V // world, (rank + 1) * V // world
+        s = h @ w_out[v0:v1].T                        # local logits over all gathered rows
+        mx = s.max(axis=1)
+        blk = mx + np.log(np.exp(s - mx[:, None]).sum(axis=1))
+        allb = [torch.zeros(world * M, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allb, torch.from_numpy(blk))
+        B = np.stack([t.numpy() for t in allb])
+        gm = B.max(axis=0)
+        lse = gm + np.log(np.exp(B - gm).sum(axis=0))
+        own = (y >= v0) & (y < v1)
+        tl = torch.from_numpy(np.where(own, s[np.arange(world * M), np.clip(y - v0, 0, v1 - v0 - 1)], 0.0))
+        dist.all_reduce(tl)
+        loss = float((scale * (lse - tl.numpy())).sum())
+        ds = scale * np.exp(s - lse[:, None])
+        ds[np.arange(world * M)[own], (y - v0)[own]] -= scale
+        dh_part = torch.from_numpy(ds @ w_out[v0:v1])
+        # dp + vocab-parallel output: each rank keeps its own M rows of dh
+        mine = torch.zeros(M, H, dtype=torch.float64)
+        dist.reduce_scatter(mine, list(dh_part.reshape(world, M, H).unbind(0)))
+        if rank == 0:
+            full = h @ w_out.T
+            fm = full.max(axis=1)
+            flse = fm + np.log(np.exp(full - fm[:, None]).sum(axis=1))
+            floss = float((scale * (flse - full[np.arange(world * M), y])).sum())
+            fds = scale * np.exp(full - flse[:, None])
+            fds[np.arange(world * M), y] -= scale
+            fdh = fds @ w_out
+            out["loss"] = (loss, floss)
+            out["lse"] = float(np.abs(lse - flse).max())
+            out["dh0"] = float(np.abs(mine.numpy() - fdh[:M]).max())
+            out["dw_block"] = float(np.abs(ds.T @ h - (fds.T @ h)[v0:v1]).max())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_vocab_parallel_exchanges_gloo_world2():
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_vshard_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    assert res["loss"][0] == pytest.approx(res["loss"][1], rel=1e-12)
+    assert res["lse"] < 1e-12 and res["dh0"] < 1e-12 and res["dw_block"] < 1e-12
