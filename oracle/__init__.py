@@ -713,6 +713,20 @@ class Ref(_Backend):
                       shortlist_k, top_k, kind, C.byref(pos), C.byref(hits)))
         return pos.value, hits.value
 
+    def gen_corpus(self, gen_seed, train_tokens, train_seed, valid_tokens, valid_seed, V):
+        """TextGenerator(GenConfig{}, gen_seed) -> normalize -> build_vocab
+        -> encode: (train ids, valid ids)."""
+        ct, cv = int(train_tokens * 1.5) + 1000, int(valid_tokens * 1.5) + 1000
+        a = np.empty(ct, np.uint32)
+        b = np.empty(cv, np.uint32)
+        na, nb = C.c_int64(), C.c_int64()
+        f = self.lib.ref_gen_corpus
+        f.argtypes = [_u64, _i64, _u64, _i64, _u64, _i64, _vp, _i64, C.POINTER(C.c_int64), _vp,
+                      _i64, C.POINTER(C.c_int64)]
+        self._check(f(gen_seed, train_tokens, train_seed, valid_tokens, valid_seed, V,
+                      a.ctypes.data, ct, C.byref(na), b.ctypes.data, cv, C.byref(nb)))
+        return a[: min(na.value, ct)].copy(), b[: min(nb.value, cv)].copy()
+
     def bn_quantize(self, params, bits, act=0):
         """quantize_model + write_quantized (RNQZ bytes) and the dequantized
         parameters of read_quantized + dequantize_model."""

@@ -924,4 +924,24 @@ int ref_hit_rate(std::int64_t V, std::int64_t H, int act, const float* w_in, con
   });
 }
 
+// The SURVEY §8d C1 PPL-match corpus: TextGenerator(GenConfig{}, gen_seed)
+// text -> normalize_text -> build_vocab(train, V) -> encode (train and
+// valid under the train vocabulary).
+int ref_gen_corpus(std::uint64_t gen_seed, std::int64_t train_tokens, std::uint64_t train_seed,
+                   std::int64_t valid_tokens, std::uint64_t valid_seed, std::int64_t V,
+                   std::uint32_t* out_train, std::int64_t cap_train, std::int64_t* n_train,
+                   std::uint32_t* out_valid, std::int64_t cap_valid, std::int64_t* n_valid) {
+  return guarded([&] {
+    TextGenerator gen(GenConfig{}, gen_seed);
+    const SentenceCorpus tr = normalize_text(gen.generate(train_tokens, train_seed));
+    const SentenceCorpus va = normalize_text(gen.generate(valid_tokens, valid_seed));
+    const Vocabulary vocab = build_vocab(tr, static_cast<std::size_t>(V));
+    const IdStream a = encode(tr, vocab), b = encode(va, vocab);
+    *n_train = static_cast<std::int64_t>(a.ids.size());
+    *n_valid = static_cast<std::int64_t>(b.ids.size());
+    std::memcpy(out_train, a.ids.data(), sizeof(std::uint32_t) * std::min<std::int64_t>(*n_train, cap_train));
+    std::memcpy(out_valid, b.ids.data(), sizeof(std::uint32_t) * std::min<std::int64_t>(*n_valid, cap_valid));
+  });
+}
+
 }  // extern "C"

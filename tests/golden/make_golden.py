@@ -227,6 +227,22 @@ def write_ngram_scorers(ref, out):
     np.savez_compressed(os.path.join(out, "ngram_scorers.npz"), **d)
 
 
+def write_ppl_match(ref, out):
+    """SURVEY §8d C1 PPL match: the reference's generated corpus, one epoch
+    of Trainer<StandardTraits> (H=128, T=8, B=8, noffset=128, softmax,
+    eta 0.05) on the first 262,144 ids, validation on 50,000 (slow: ~5 min
+    on 8 host threads)."""
+    tr, va = ref.gen_corpus(555, 1_000_000, 1, 60_000, 2, 10000)
+    tr, va = tr[:262144], va[:50000]
+    V, H = 10000, 128
+    params = ref.init_uniform(V, H, 1)
+    cfg = oracle.TrainConfig(nstate=H, noffset=128, minibatch=8, unroll=8, eta=0.05,
+                             max_epochs=1, mode=1, threads=os.cpu_count())
+    _, logs, ini = ref.train(cfg, params, tr, va)
+    np.savez_compressed(os.path.join(out, "ppl_match_c1.npz"), train=tr, valid=va, init_seed=1,
+                        V=V, H=H, logs=logs, initial=ini, eta=0.05)
+
+
 def main():
     ref = oracle.Ref()
     out = os.path.join(HERE)
@@ -272,6 +288,7 @@ def main():
     write_ln_z(ref, out)
     write_rnqz(ref, out)
     write_ngram_scorers(ref, out)
+    write_ppl_match(ref, out)
     print("golden fixtures written to", out)
 
 

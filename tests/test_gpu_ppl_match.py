@@ -1,0 +1,31 @@
+"""PPL match at the C1 configuration: the reference's
+own PPL-match corpus (TextGenerator(GenConfig{}, 555), normalized, 10,000-word
+vocabulary, first 262,144 training ids, 50,000 validation ids), init_uniform
+seed 1, H=128, T=8, B=8, noffset=128 (N=1,024 streams), softmax, eta 0.05:
+validation perplexity after one epoch (4,096 windows) of the device trainer
+within 1% of the reference CPU trainer's (tests/golden/ppl_match_c1.npz, made
+by the compiled reference, 283 s on 8 host threads)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.mark.parametrize("precision,rel", [("bf16", 1e-2), ("fp32", 1e-2)])
+def test_c1_ppl_match_one_epoch(precision, rel):
+    import paper_1502_00512_b200 as dl
+    g = np.load(os.path.join(GOLD, "ppl_match_c1.npz"))
+    V, H = int(g["V"]), int(g["H"])
+    params = dl.init_uniform(V, H, int(g["init_seed"]))
+    cfg = dl.TrainConfig(nstate=H, noffset=128, minibatch=8, unroll=8, eta=float(g["eta"]),
+                         max_epochs=1, mode=1)
+    t = dl.Trainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"], precision)
+    t.train()
+    assert t.initial_ppl == pytest.approx(float(g["initial"]), rel=1e-3)
+    assert len(t.logs) == 1
+    assert t.logs[0].valid_ppl == pytest.approx(float(g["logs"][0][2]), rel=rel)
+    assert t.logs[0].train_loss == pytest.approx(float(g["logs"][0][1]), rel=rel)
