@@ -1468,7 +1468,9 @@ int dl_score(dl_ctx* c, int64_t S, int64_t steps, const uint32_t* in, const int6
   return guarded(c, [&] {
     const int64_t H = c->H, SH = S * H;
     // bank several steps per logits GEMM (eval.hpp:45 kScoreBank idea)
-    int64_t bank = std::max<int64_t>(1, std::min<int64_t>(steps, 4096 / S));
+    // (16,384 rows per logits GEMM: 2 GB of bf16 logits at V = 64,000 --
+    // fewer host synchronisations per scored word)
+    int64_t bank = std::max<int64_t>(1, std::min<int64_t>(steps, 16384 / S));
     if (bank < 1) bank = 1;
     ensure_window(c, bank, S);
     std::vector<double> lp(S * steps, NAN);
