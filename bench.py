@@ -312,8 +312,19 @@ def run_reference(args, cfg):
     Ts = min(T, args.ref_unroll)
     ids = synthetic_stream(cfg["seed"], V, 1 << 16)
     rng = np.random.default_rng(1)
-    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32) for s in ((V, H), (H, H), (V, H)))
-    state = (np.zeros((H, H), np.float32), np.zeros(V, np.float32), np.zeros(V, np.float32))
+    bnm = bool(cfg.get("bottleneck"))
+    if bnm:
+        # the bottleneck model: bptt_run(BottleneckAdapter) + bottleneck_update
+        P = cfg["P"]
+        Bs = 1
+        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                       for s in ((V, P), (P, H), (H, H), (H, P)))
+        state = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
+                 np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
+    else:
+        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                       for s in ((V, H), (H, H), (V, H)))
+        state = (np.zeros((H, H), np.float32), np.zeros(V, np.float32), np.zeros(V, np.float32))
     h0 = np.full((Bs, H), 0.5, np.float32)
     times = []
     for i in range(args.warmup + args.steps):
@@ -322,8 +333,12 @@ def run_reference(args, cfg):
         y = ids[s0 + 1:s0 + 1 + Ts * Bs].reshape(Ts, Bs)
         w = (y != 1).astype(np.uint8)
         t0 = time.perf_counter()
-        g = ref.bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0, True, cores)
-        params, state, _ = ref.rmsprop(params, state, g, 0.9995, 1e-6, 0.05)
+        if bnm:
+            g = ref.bn_bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0)
+            params, state, _ = ref.bn_update(params, state, g, 0.9995, 1e-6, 0.05)
+        else:
+            g = ref.bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0, True, cores)
+            params, state, _ = ref.rmsprop(params, state, g, 0.9995, 1e-6, 0.05)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -333,6 +348,11 @@ def run_reference(args, cfg):
     value = words * len(times) / sum(times)
     sample = (f"window-sampled: {len(times)} window(s) of B={Bs} streams x T={Ts} at "
               f"V={V}, H={H} (bptt_run + rmsprop_update, softmax), threads={cores}")
+    if bnm:
+        cores = 1
+        sample = (f"window-sampled: {len(times)} window(s) of B={Bs} stream x T={Ts} at "
+                  f"V={V}, H={H}, P={cfg['P']} (bptt_run(BottleneckAdapter) + "
+                  f"bottleneck_update, softmax), threads=1")
     out = {"metric": "training words/sec", "value": value, "unit": "words/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
