@@ -388,17 +388,23 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
     cp_async_commit();
   };
   double sq = 0.0;
+  // two 32-column TMEM loads in flight per wait
 #pragma unroll 1
-  for (int c = c0; c < ((DL_RMS_DIAG & 4) ? c0 : c0 + kRmsChunks); ++c) {
-    float v[32];
-    tmem_ld32(taddr + c * 32, v);
-    float s = 0.f;
+  for (int c = c0; c < ((DL_RMS_DIAG & 4) ? c0 : c0 + kRmsChunks); c += 2) {
+    uint32_t r0[32], r1[32];
+    tmem_ld32_async(taddr + c * 32, r0);
+    tmem_ld32_async(taddr + (c + 1) * 32, r1);
+    tmem_wait_ld();
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const float x = clip1(v[j], g.clip);
-      s = fmaf(x, x, s);
+      const float x0 = clip1(__uint_as_float(r0[j]), g.clip);
+      const float x1 = clip1(__uint_as_float(r1[j]), g.clip);
+      s0 = fmaf(x0, x0, s0);
+      s1 = fmaf(x1, x1, s1);
     }
-    sq += (double)s;
+    sq += (double)s0;
+    sq += (double)s1;
   }
   if (mvalid) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
   __syncwarp();
