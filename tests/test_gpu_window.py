@@ -242,3 +242,34 @@ def test_train_window_equals_window_then_rmsprop(orc, precision, V, H):
             np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-7)
         for a, b in zip(o1, o2):
             np.testing.assert_allclose(a, b, rtol=1e-3, atol=1e-12)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("V,H,T,B,mask", [(8, 8, 1, 1, 0.0), (16, 8, 3, 2, 1.0), (64, 16, 1, 5, 0.5)])
+def test_degenerate_windows_match_oracle(orc, precision, V, H, T, B, mask):
+    """Edge shapes the reference tests exercise: a single position, a fully
+    masked window (no scored positions: zero loss, zero output gradient),
+    one step of several streams."""
+    import paper_1502_00512_b200 as dl
+    rng = np.random.default_rng(V * 7 + T)
+    params = orc.init_uniform(V, H, 2)
+    x, y, w = rand_window(rng, T, B, V, 0.0)
+    if mask == 1.0:
+        w[:] = 0
+    elif mask > 0.0:
+        w[:, ::2] = 0
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    want = orc.bptt(params, 0, x, y, w, h0, 1.0 / (T * B), 1.0)
+    m = dl.GpuRnn(V, H, 0, precision)
+    m.set_params(*params)
+    res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
+    assert res.positions == want["positions"]
+    tol = 1e-4 if precision == "fp32" else 2e-2
+    assert res.loss == pytest.approx(want["loss"], rel=tol, abs=1e-12)
+    g_in, g_rec, g_out = m.grads()
+    if mask == 1.0:
+        assert res.loss == 0.0 and not np.any(g_out) and not np.any(g_rec) and not np.any(g_in)
+    else:
+        ok, err = close(g_out, want["g_out"], rel=tol, floor_frac=1e-3 if precision == "bf16" else 1e-4)
+        assert ok, err
+    assert dl.rmsprop_update(m, 0.05)
