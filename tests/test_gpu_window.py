@@ -273,3 +273,26 @@ def test_degenerate_windows_match_oracle(orc, precision, V, H, T, B, mask):
         ok, err = close(g_out, want["g_out"], rel=tol, floor_frac=1e-3 if precision == "bf16" else 1e-4)
         assert ok, err
     assert dl.rmsprop_update(m, 0.05)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_v65536_shape_check(orc, precision):
+    """V = 65,536 (2^16, tile-aligned everywhere) once as a
+    shape check next to the 64,000 / 10,000 configurations."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 65536, 256, 2, 16
+    rng = np.random.default_rng(65536)
+    params = orc.init_uniform(V, H, 6)
+    x, y, w = rand_window(rng, T, B, V, 0.1)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    want = orc.bptt(params, 0, x, y, w, h0, 1.0 / (T * B), 1.0)
+    m = dl.GpuRnn(V, H, 0, precision)
+    m.set_params(*params)
+    res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
+    tol = 1e-4 if precision == "fp32" else 1e-2
+    assert res.positions == want["positions"]
+    assert res.loss == pytest.approx(want["loss"], rel=tol)
+    g_out = m.grads()[2]
+    cos = float(np.dot(g_out.ravel(), want["g_out"].ravel()) /
+                (np.linalg.norm(g_out) * np.linalg.norm(want["g_out"]) + 1e-30))
+    assert cos > (0.99999 if precision == "fp32" else 0.99)
