@@ -370,7 +370,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
@@ -515,6 +515,7 @@ def main():
                 "algorithmic_flops_per_launch": gemm_flops[dom],
                 "step_frac_of_sustained_peak": value / world * fpw / 1e12
                 / PEAKS["bf16_tflops_sustained"],
+                "step_frac_of_burst_peak": value / world * fpw / 1e12 / PEAKS["bf16_tflops"],
                 "phase_ms": phases}
     if dom == "dw_out":
         roofline["note"] = ("dW_out GEMM with the dense W_out rmsprop fused into its epilogue "
