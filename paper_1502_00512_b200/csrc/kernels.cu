@@ -877,7 +877,7 @@ __global__ void k_window_build(const uint32_t* __restrict__ ids, int64_t L,
                                const int64_t* __restrict__ win_counter, int noffset, int64_t B,
                                int64_t T, int64_t H, uint32_t bos, uint32_t* __restrict__ x,
                                uint32_t* __restrict__ y, uint8_t* __restrict__ w,
-                               float* __restrict__ h0) {
+                               float* __restrict__ h0, bf16* __restrict__ h0b) {
   const int64_t g = *win_counter % noffset;
   const int64_t s0 = g * B;  // cursors / hidden hold this rank's streams only
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -891,45 +891,44 @@ __global__ void k_window_build(const uint32_t* __restrict__ ids, int64_t L,
     y[i] = yi;
     w[i] = yi == bos ? 0 : 1;
   }
-  for (int64_t i = tid; i < B * H; i += nthreads) h0[i] = hidden[s0 * H + i];
-}
-
-// After the window (trainer.hpp:396-405): hidden <- h_final, cursor += T,
-// wrap -> cursor -= L and hidden = act(0).  Advances the window counter.
-__global__ void k_hidden_carry(const int64_t* __restrict__ cursors, float* __restrict__ hidden,
-                               const float* __restrict__ h_final,
-                               const int64_t* __restrict__ win_counter, int noffset, int64_t B,
-                               int64_t T, int64_t H, int64_t L, float a0) {
-  const int64_t s0 = (*win_counter % noffset) * B;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  if ((H % 4) == 0) {
-    const float4* src = reinterpret_cast<const float4*>(h_final);
-    float4* dst = reinterpret_cast<float4*>(hidden + s0 * H);
-    for (int64_t i = tid; i < B * H / 4; i += nthreads) {
-      const bool wrap = cursors[s0 + (4 * i) / H] + T >= L;
-      dst[i] = wrap ? make_float4(a0, a0, a0, a0) : src[i];
-    }
-  } else {
-    for (int64_t i = tid; i < B * H; i += nthreads) {
-      const bool wrap = cursors[s0 + i / H] + T >= L;
-      hidden[s0 * H + i] = wrap ? a0 : h_final[i];
-    }
+  for (int64_t i = tid; i < B * H; i += nthreads) {
+    const float v = hidden[s0 * H + i];
+    h0[i] = v;
+    if (h0b) h0b[i] = __float2bfloat16_rn(v);  // the recurrence's first A operand
   }
 }
 
-// Runs after k_hidden_carry (which reads the old cursors); advances the
-// window counter at the end.
-__global__ void k_cursor_advance(int64_t* __restrict__ cursors, int64_t* win_counter,
-                                 int noffset, int64_t B, int64_t T, int64_t L) {
+// After the window (trainer.hpp:396-405), one block per stream: hidden <-
+// h_final (or act(0) on a wrap), then the stream's cursor += T (-= L on a
+// wrap).  The window counter advances in k_window_tail.
+__global__ void k_window_finish(int64_t* __restrict__ cursors, float* __restrict__ hidden,
+                                const float* __restrict__ h_final,
+                                const int64_t* __restrict__ win_counter, int noffset, int64_t B,
+                                int64_t T, int64_t H, int64_t L, float a0) {
   const int64_t s0 = (*win_counter % noffset) * B;
-  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
-    int64_t c = cursors[s0 + b] + T;
-    if (c >= L) c -= L;
-    cursors[s0 + b] = c;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const int64_t cur = cursors[s0 + b];
+    const bool wrap = cur + T >= L;
+    float* dst = hidden + (s0 + b) * H;
+    const float* src = h_final + b * H;
+    if ((H % 4) == 0) {
+      for (int64_t i = threadIdx.x; i < H / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(dst)[i] =
+            wrap ? make_float4(a0, a0, a0, a0) : reinterpret_cast<const float4*>(src)[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < H; i += blockDim.x) dst[i] = wrap ? a0 : src[i];
+    }
+    __syncthreads();  // every thread has read the old cursor
+    if (threadIdx.x == 0) cursors[s0 + b] = wrap ? cur + T - L : cur + T;
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x == 0) win_counter[0] += 1;
+}
+
+// window counter += 1; skipped += the update's non-finite verdict
+__global__ void k_window_tail(int64_t* win_counter, const int* __restrict__ nonfinite,
+                              unsigned long long* skipped) {
+  if (nonfinite && skipped && *nonfinite) skipped[0] += 1ull;
+  win_counter[0] += 1;
 }
 
 }  // namespace
@@ -1095,16 +1094,17 @@ void set_flag(int* dst, const int* src, int value, cudaStream_t st) {
 }
 void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
                   const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
-                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st) {
+                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st,
+                  bf16* h0b) {
   k_window_build<<<grid_for(std::max(T * B, B * H)), 256, 0, st>>>(
-      ids, L, cursors, hidden, win_counter, noffset, B, T, H, bos, x, y, w, h0);
+      ids, L, cursors, hidden, win_counter, noffset, B, T, H, bos, x, y, w, h0, h0b);
 }
 void window_finish(int64_t* cursors, float* hidden, const float* h_final, int64_t* win_counter,
                    int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0,
-                   cudaStream_t st) {
-  k_hidden_carry<<<grid_for(B * H / 4), 256, 0, st>>>(cursors, hidden, h_final, win_counter,
-                                                       noffset, B, T, H, L, a0);
-  k_cursor_advance<<<1, 256, 0, st>>>(cursors, win_counter, noffset, B, T, L);
+                   cudaStream_t st, const int* nonfinite, unsigned long long* skipped) {
+  k_window_finish<<<(unsigned)std::min<int64_t>(B, 148 * 4), 256, 0, st>>>(
+      cursors, hidden, h_final, win_counter, noffset, B, T, H, L, a0);
+  k_window_tail<<<1, 1, 0, st>>>(win_counter, nonfinite, skipped);
 }
 
 }  // namespace dl

@@ -126,9 +126,13 @@ void accum_loss(double* acc, const double* v, unsigned long long* cnt,
                 const unsigned long long* vc, cudaStream_t st);
 void window_build(const uint32_t* ids, int64_t L, const int64_t* cursors, const float* hidden,
                   const int64_t* win_counter, int noffset, int64_t B, int64_t T, int64_t H,
-                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st);
+                  uint32_t bos, uint32_t* x, uint32_t* y, uint8_t* w, float* h0, cudaStream_t st,
+                  bf16* h0b = nullptr);
+// hidden carry + cursor advance; then the window counter (and, with
+// nonfinite / skipped, the skipped-update count) in one tail kernel
 void window_finish(int64_t* cursors, float* hidden, const float* h_final, int64_t* win_counter,
                    int noffset, int64_t B, int64_t T, int64_t H, int64_t L, float a0,
-                   cudaStream_t st);
+                   cudaStream_t st, const int* nonfinite = nullptr,
+                   unsigned long long* skipped = nullptr);
 
 }  // namespace dl

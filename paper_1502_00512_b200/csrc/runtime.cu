@@ -133,6 +133,7 @@ struct dl_ctx {
   // recurrence steps as one cluster kernel each (rec_tc.cu); DL_REC_CLUSTER=0
   // falls back to split-K GEMM + reduction kernels (both are sm_100a CUDA)
   bool rec_cluster = true;
+  bool h0_bf_ready = false;  // window_build already wrote htape_bf[0] (trainer path)
   // DL_FORK_OUT=1: run the dense W_out update concurrently with the dh GEMM
   // (measured neutral on B200: both contend for L2/HBM bandwidth)
   bool fork_out = false;
@@ -645,7 +646,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     c->launches++;
     DL_CUDA(cudaEventRecord(c->ev_sort_join, c->st2));
   }
-  if (tc(c)) {
+  if (tc(c) && !c->h0_bf_ready) {
     f32_to_bf16(c->htape, c->htape_bf, BH, st);
     c->launches++;
   }
@@ -1024,7 +1025,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
 
 // rmsprop_update (rmsprop.hpp:113-133).  skip_out: the dense W_out part was
 // already issued on the side stream by run_window (fork_out_eta).
-void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
+void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false, bool count = true) {
   Phase p(c, "rmsprop");
   cudaStream_t st = c->st;
   rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
@@ -1047,8 +1048,8 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false) {
   else if (!skip_out)
     rms_rows(c->w_out, tc(c) ? c->w_out_bf : nullptr, c->m_out, c->g_out, nullptr, nullptr, c->Vo,
              c->H, c->rho, c->eps, eta, 1, c->nonfinite, st);
-  count_skip(c->nonfinite, c->d_skipped, st);
-  c->launches += 4;
+  if (count) count_skip(c->nonfinite, c->d_skipped, st);
+  c->launches += count ? 4 : 3;
 }
 
 float act0(int act) { return act == 0 ? 0.5f : 0.0f; }
@@ -1872,8 +1873,9 @@ void trainer_window(dl_ctx* c, double eta) {
   const int64_t B = c->minibatch, T = c->unroll, H = c->H;
   const double scale = 1.0 / (double)(B * dp_ranks(c) * T);
   window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
-               c->x_d, c->y_d, c->w_d, c->htape, c->st);
+               c->x_d, c->y_d, c->w_d, c->htape, c->st, tc(c) ? c->htape_bf : nullptr);
   c->launches++;
+  c->h0_bf_ready = tc(c);
   // the dense W_out update overlaps the dh GEMM when it cannot be rejected
   // (finite clip, see run_window), a second bf16 shadow exists and no
   // allreduce is pending
@@ -1883,9 +1885,10 @@ void trainer_window(dl_ctx* c, double eta) {
   const bool fork = sm && !fuse && !late && fork_ok(c);
   run_window(c, T, B, scale, (float)c->clip, true, fork ? eta : 0.0, fuse ? eta : 0.0,
              late ? eta : 0.0);
-  run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork || fuse || late);
+  c->h0_bf_ready = false;
+  run_rmsprop(c, eta, T * B * dp_ranks(c), /*skip_out=*/fork || fuse || late, /*count=*/false);
   window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
-                c->L, act0(c->act), c->st);
+                c->L, act0(c->act), c->st, c->nonfinite, c->d_skipped);
   c->launches += 2;
   if (fork || late) DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   if (fork) swap_shadow(c);
