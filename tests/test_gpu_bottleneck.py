@@ -133,16 +133,17 @@ def test_bn_nonfinite_gradient_skips_update(orc):
         assert np.array_equal(a, b, equal_nan=True)
 
 
-@pytest.mark.parametrize("V,H,P,T,B", [(4096, 256, 64, 8, 32), (8192, 512, 128, 16, 64)])
-def test_bn_window_bf16_close_to_oracle(orc, V, H, P, T, B):
+@pytest.mark.parametrize("V,H,P,T,B,act", [(4096, 256, 64, 8, 32, 0), (8192, 512, 128, 16, 64, 0),
+                                            (4096, 256, 128, 8, 16, 1)])
+def test_bn_window_bf16_close_to_oracle(orc, V, H, P, T, B, act):
     import paper_1502_00512_b200 as dl
     from paper_1502_00512_b200 import bottleneck as bn
     rng = np.random.default_rng(V)
     params = orc.bn_init_uniform(V, H, P, 4)
     x, y, w = rand_window(rng, T, B, V, 0.1)
     h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
-    want = orc.bn_bptt(params, 0, x, y, w, h0, 1.0 / (T * B), 1.0)
-    m = bn_model(bn, params, 0, "bf16")
+    want = orc.bn_bptt(params, act, x, y, w, h0, 1.0 / (T * B), 1.0)
+    m = bn_model(bn, params, act, "bf16")
     res, hf = bn.bn_bptt_run(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0)
     assert res.loss == pytest.approx(want["loss"], rel=1e-2)
     assert np.max(np.abs(hf - want["h_final"])) < 2e-2
@@ -155,7 +156,7 @@ def test_bn_window_bf16_close_to_oracle(orc, V, H, P, T, B):
     ids = orc.random_stream(9, V, 20000)
     r = bn.bn_sharded_perplexity(m, ids, 64)
     p2 = m.params()
-    want_p = orc.bn_sharded_ppl(p2, 0, ids, 64)
+    want_p = orc.bn_sharded_ppl(p2, act, ids, 64)
     assert r.perplexity == pytest.approx(want_p["perplexity"], rel=1e-2)
 
 
