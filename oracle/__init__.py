@@ -37,7 +37,7 @@ _u64 = C.c_uint64
 
 class TrainConfig(C.Structure):
     """Field order of the RTRN config echo (trainer.hpp:412-432); defaults
-    follow TrainConfig (trainer.hpp:43-63) except mode=softmax."""
+    follow TrainConfig (trainer.hpp:43-63), NCE mode included."""
 
     _fields_ = [
         ("nstate", C.c_int64), ("nproj", C.c_int64),
@@ -53,7 +53,7 @@ class TrainConfig(C.Structure):
 
     def __init__(self, **kw):
         d = dict(nstate=256, nproj=0, noffset=128, minibatch=8, unroll=16,
-                 mode=1, eta=1e-3, rho=0.9995, eps=1e-6, clip=1.0, nce_k=64,
+                 mode=0, eta=1e-3, rho=0.9995, eps=1e-6, clip=1.0, nce_k=64,
                  max_epochs=20, noise_floor=1e-8, seed=1, act=0,
                  valid_shards=8, divergence_factor=10.0, valid_limit=0,
                  init_range=0.1, threads=1, pad_=0)
@@ -509,10 +509,12 @@ class Orc(_Backend):
                          C.byref(ep))
         if rc not in (0,):
             raise OracleError(rc, "orc_train")
+        rng = np.zeros(313, np.uint64)
+        self.lib.orc_last_train_rng(rng.ctypes.data_as(C.c_void_p))
         return dict(params=(w_in, w_rec, w_out), opt=(m_rec, m_in, m_out),
                     cursors=cur, hidden=hid, logs=logs[: nl.value].copy(),
                     initial_ppl=ini.value, eta=eta.value, best_ppl=best.value,
-                    bad_epochs=bad.value, epoch=ep.value)
+                    bad_epochs=bad.value, epoch=ep.value, rng_state=rng)
 
 
     def noise_build(self, counts, k, floor=1e-8):

@@ -781,6 +781,12 @@ typedef struct {
   int32_t threads, pad_;
 } orc_train_config;
 
+/* State of Trainer::rng_ after the last orc_train (313 words: the 312 state
+ * words and the position, as `os << rng_` writes them, trainer.hpp:283-285):
+ * it only advances in NCE mode (2 outputs per noise draw). */
+static uint64_t g_train_rng[313];
+void orc_last_train_rng(uint64_t* out) { memcpy(out, g_train_rng, sizeof g_train_rng); }
+
 /* Trainer<StandardTraits> in softmax mode: constructor (trainer.hpp:178-212),
  * train() (:233-270), run_epoch() (:350-410), validate() (:223-228).
  * Params (inout), opt state (out), cursors (out, N), hidden (out, N*H),
@@ -915,6 +921,8 @@ int orc_train(const orc_train_config* c, int64_t V, float* w_in, float* w_rec,
     }
   }
 done:
+  if (nce) memcpy(g_train_rng, rng, sizeof g_train_rng);
+  else orc_mt_state(c->seed, g_train_rng);
   *initial_ppl = initial;
   *eta_out = eta;
   *best_out = best;

@@ -518,9 +518,9 @@ def rescore_nbest(utts: List[NBestUtt], model: GpuRnn, vocab_words: Sequence[str
 # ---------------------------------------------------------------- trainer
 @dataclass
 class TrainConfig:
-    """trainer.hpp:43-93.  mode: 0 = NCE (LossMode::kNce: k = nce_k noise
-    samples per position from the unigram NoiseModel, the reference's default),
-    1 = exact softmax (this mirror's default)."""
+    """trainer.hpp:43-93, same defaults.  mode: 0 = NCE (LossMode::kNce, the
+    reference's default, trainer.hpp:53: k = nce_k noise samples per position
+    from the unigram NoiseModel), 1 = exact softmax."""
     nstate: int = 256
     nproj: int = 0
     noffset: int = 128
@@ -530,7 +530,7 @@ class TrainConfig:
     rho: float = 0.9995
     eps: float = 1e-6
     clip: float = 1.0
-    mode: int = 1
+    mode: int = 0
     nce_k: int = 64
     noise_floor: float = 1e-8
     max_epochs: int = 20
@@ -638,6 +638,7 @@ class Trainer:
             self.model.comm_init_local(comm[0], comm[2])
         elif comm is not None:
             self.model.comm_init(comm[0], comm[1], comm[2])
+        self.model_sharded = bool(vocab_shard)
         if vocab_shard:
             self.model.set_vocab_shard(vocab_shard)
         self.model.set_params(w_in, w_rec, w_out)
@@ -707,7 +708,18 @@ class Trainer:
                 self.eta *= 0.5
 
     # ---- checkpointing (RTRN, trainer.hpp:274-341)
+    def _single_rank_only(self, what):
+        # a rank holds only its own streams' cursors / hidden state (and, with
+        # a vocabulary-sharded output layer, its own W_out / m_out rows): an
+        # RTRN blob written by one rank is not the run's checkpoint
+        if self.nranks > 1:
+            raise NotImplementedError(
+                f"{what}: RTRN checkpoints of multi-rank trainers are not supported "
+                f"(each rank holds 1/{self.nranks} of the streams"
+                + (" and of W_out" if self.model_sharded else "") + ")")
+
     def save_checkpoint(self) -> bytes:
+        self._single_rank_only("save_checkpoint")
         cur, hid = self.model.trainer_state()
         # the rng as `os << rng_` (trainer.hpp:284): it only advances in NCE mode
         rng_text = " ".join(str(int(v)) for v in self.model.rng_state()) \
@@ -717,6 +729,7 @@ class Trainer:
                                      self.model.params(), self.vocab, self.model.opt())
 
     def load_checkpoint(self, data: bytes):
+        self._single_rank_only("load_checkpoint")
         cfg = self.cfg
         n = cfg.noffset * cfg.minibatch
         st = formats.read_trainer(data, cfg, n, self.model.H, len(self.train_ids))

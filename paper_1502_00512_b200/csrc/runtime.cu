@@ -299,8 +299,23 @@ void prof_collect(dl_ctx* c) {
 }
 
 // ----------------------------------------------------------- allocation
+// A workspace is about to be freed and reallocated: the per-window CUDA
+// graphs of dl_trainer_run hold its old pointers, so finish the work in
+// flight and drop them (they are re-captured on the next dl_trainer_run).
+// Never inside a capture (presize() sizes everything before capturing).
+void invalidate_workspace(dl_ctx* c) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DL_CUDA(cudaStreamIsCapturing(c->st, &cs));
+  DL_REQUIRE(cs == cudaStreamCaptureStatusNone, DL_EDEVICE,
+             "internal: workspace reallocation during graph capture");
+  DL_CUDA(cudaStreamSynchronize(c->st));
+  if (c->st2) DL_CUDA(cudaStreamSynchronize(c->st2));
+  drop_graphs(c);
+}
+
 void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   if (T <= c->capT && B <= c->capB && c->htape) return;
+  invalidate_workspace(c);
   const int64_t nT = std::max(T, c->capT), nB = std::max(B, c->capB);
   const int64_t TB = nT * nB, H = c->H, V = c->V;
   auto fr = [](auto*& p) {
@@ -364,6 +379,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
 
 void ensure_splitws(dl_ctx* c, size_t elems) {
   if (elems <= c->splitws_elems) return;
+  invalidate_workspace(c);
   if (c->splitws) cudaFree(c->splitws);
   c->splitws = dalloc<float>(elems);
   c->splitws_elems = elems;

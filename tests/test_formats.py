@@ -31,7 +31,7 @@ def test_rnlm_matches_golden_and_roundtrips():
 def test_rtrn_untrained_matches_golden():
     g = np.load(os.path.join(GOLD, "train.npz"))
     params = (g["w_in"], g["w_rec"], g["w_out"])
-    cfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3)
+    cfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3, mode=1)
     L = len(g["train"])
     N = 4
     cur = np.array([i * L // N for i in range(N)], np.int64)
@@ -44,17 +44,17 @@ def test_rtrn_untrained_matches_golden():
     st = formats.read_trainer(blob, cfg, N, 8, L)
     assert np.array_equal(st["cursors"], cur)
     with pytest.raises(DataError):  # config mismatch
-        formats.read_trainer(blob, TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=6), N, 8, L)
+        formats.read_trainer(blob, TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=6, mode=1), N, 8, L)
     # max_epochs may change on resume (trainer.hpp:446-447)
     formats.read_trainer(blob, TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05,
-                                           max_epochs=9), N, 8, L)
+                                           max_epochs=9, mode=1), N, 8, L)
     with pytest.raises(DataError):
         formats.read_trainer(blob, cfg, N + 1, 8, L)
 
 
 def test_rtrn_trained_roundtrip_via_writer():
     g = np.load(os.path.join(GOLD, "train.npz"))
-    cfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3)
+    cfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3, mode=1)
     blob = g["rtrn"].tobytes()
     st = formats.read_trainer(blob, cfg, 4, 8, len(g["train"]))
     again = formats.write_trainer(cfg, st["epoch"], st["eta"], st["best"], st["bad"],
@@ -86,7 +86,7 @@ def test_rng_text_matches_reference(ref):
         cfg = oracle.TrainConfig(nstate=H, noffset=1, minibatch=1, unroll=2, mode=1, seed=seed)
         tr = ref.random_stream(3, V, 50)
         blob, _, _ = ref.train(cfg, ref.init_uniform(V, H, 1), tr, tr, run=False)
-        pcfg = TrainConfig(nstate=H, noffset=1, minibatch=1, unroll=2, seed=seed)
+        pcfg = TrainConfig(nstate=H, noffset=1, minibatch=1, unroll=2, seed=seed, mode=1)
         st = formats.read_trainer(blob, pcfg, 1, H, len(tr))
         assert st["rng_text"] == formats.mt19937_64_text(seed)
 

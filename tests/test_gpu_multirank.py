@@ -224,6 +224,9 @@ def test_dp_trainer_matches_global_minibatch(orc):
             assert np.array_equal(c[g * 4:(g + 1) * 4], cs[g * Bg + r * 4:g * Bg + (r + 1) * 4])
     for a, b in zip(trainers[0].params(), trainers[1].params()):
         assert np.array_equal(a, b)
+    # a rank holds only its streams' state: no single-rank RTRN blob
+    with pytest.raises(NotImplementedError):
+        trainers[0].save_checkpoint()
 
 
 @pytest.mark.parametrize("G,precision", [(2, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])

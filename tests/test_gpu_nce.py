@@ -171,16 +171,14 @@ def test_nce_trainer_matches_oracle(orc, precision):
         assert a.valid_ppl == pytest.approx(b[2], rel=5 * rel)
     cur, _ = t.model.trainer_state()
     assert np.array_equal(cur, want["cursors"])
-    # the generator advanced by exactly the reference's draws: replay them
-    noise = orc.noise_build(np.bincount(tr[tr != 1], minlength=V).astype(np.float64), 7, 1e-3)
-    st = orc.mt_state(kw.get("seed", 1))
-    positions = sum(int(lg.positions) for lg in t.logs) if hasattr(t.logs[0], "positions") else None
-    blob = t.save_checkpoint()
+    # the generator advanced by exactly the reference's draws (2 outputs per
+    # noise sample, backprop.hpp:126-156): the oracle trainer's final state
+    assert np.array_equal(t.model.rng_state(), want["rng_state"])
+    assert not np.array_equal(t.model.rng_state(), orc.mt_state(kw.get("seed", 1)))
+    # and it survives the RTRN round trip (trainer.hpp:283-285, :312-317)
     t2 = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, precision)
-    t2.load_checkpoint(blob)
+    t2.load_checkpoint(t.save_checkpoint())
     assert np.array_equal(t2.model.rng_state(), t.model.rng_state())
-    assert not np.array_equal(t.model.rng_state(), st)  # it did advance
-    del noise, positions
 
 
 def oracle_cfg(kw):

@@ -91,6 +91,57 @@ def test_checkpoint_resume_is_bit_exact(orc):
     assert b.save_checkpoint() == straight.save_checkpoint()
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_resume_then_several_epochs_is_bit_exact(orc, precision):
+    """Resume followed by two more epochs: after load_checkpoint
+    train() skips the initial validation, so the first epoch's window graphs
+    are captured before validate() grows the workspace; the next epoch must
+    re-capture rather than replay graphs holding freed buffers."""
+    import paper_1502_00512_b200 as dl
+    V, H = 64, 16
+    tr, va = make_data(orc, V, 1500, 400, 45)
+    params = orc.init_uniform(V, H, 19)
+    kw = dict(nstate=H, noffset=2, minibatch=8, unroll=6, eta=0.05, max_epochs=4, mode=1)
+    straight = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, precision)
+    straight.train()
+    a = dl.Trainer(dl.TrainConfig(**dict(kw, max_epochs=2)), params, dl.make_vocab(V), tr, va,
+                   precision)
+    a.train()
+    b = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, precision)
+    b.load_checkpoint(a.save_checkpoint())
+    b.train()
+    assert b.epoch == straight.epoch >= 3
+    assert [l.train_loss for l in b.logs] == [l.train_loss for l in straight.logs[2:]]
+    assert b.save_checkpoint() == straight.save_checkpoint()
+
+
+def test_scoring_between_trainer_runs(orc):
+    """dl_score / sharded_perplexity with a larger bank between two
+    dl_trainer_run calls reallocates the window workspace: the trainer's
+    cached graphs must be dropped (identical to running without scoring)."""
+    import paper_1502_00512_b200 as dl
+    V, H = 80, 32
+    tr, va = make_data(orc, V, 2000, 3000, 46)
+    params = orc.init_uniform(V, H, 23)
+    runs = []
+    for interleave in (False, True):
+        m = dl.GpuRnn(V, H, 0, "bf16")
+        m.set_params(*params)
+        m.set_opt(None, None, None, 0.9995, 1e-6)
+        m.trainer_init(tr, 2, 8, 5, 1.0)
+        l1, _ = m.trainer_run(0, 6, 0.05)
+        if interleave:
+            dl.sharded_perplexity(m, va, 16)   # grows the window buffers
+            dl.sharded_perplexity(m, va, 64)
+        l2, _ = m.trainer_run(6, 6, 0.05)
+        runs.append((l1, l2, m.params(), m.trainer_state()))
+        m.close()
+    (a1, a2, pa, sa), (b1, b2, pb, sb) = runs
+    assert a1 == b1 and a2 == b2
+    for x, y in zip(pa + sa, pb + sb):
+        assert np.array_equal(x, y)
+
+
 def test_checkpoint_layout_matches_reference(orc, ref):
     """Untrained trainer: the RTRN bytes equal the reference's exactly."""
     import paper_1502_00512_b200 as dl

@@ -60,7 +60,8 @@ def test_train_golden_bitexact(orc):
     r = orc.train(cfg, params, g["train"], g["valid"])
     assert r["initial_ppl"] == float(g["initial"])
     assert np.array_equal(r["logs"][:, [0, 1, 2, 3, 6]], g["logs"][:, [0, 1, 2, 3, 6]])
-    pcfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3)
+    pcfg = TrainConfig(nstate=8, noffset=2, minibatch=2, unroll=5, eta=0.05, max_epochs=3,
+                       mode=1)
     st = formats.read_trainer(g["rtrn"].tobytes(), pcfg, 4, 8, len(g["train"]))
     assert np.array_equal(st["cursors"], r["cursors"])
     assert np.array_equal(st["hidden"], r["hidden"])
