@@ -61,9 +61,29 @@ CONFIGS = {
 }
 
 
-def run_scoring(args, cfg):
-    """C5: sharded-perplexity scoring words/s (eval.hpp:151-222 lock-step walk
-    over S streams, exact softmax), device-timed on the library stream."""
+def cpu_baseline_for(name: str, steps: int = 1):
+    """The reference arm's measurement on a short bounded sample (a
+    subprocess: `bench.py --impl reference --config name`), reported as
+    this line's cpu_baseline."""
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                            "--config", name, "--steps", str(steps), "--warmup", "0"],
+                           capture_output=True, text=True, timeout=900)
+        line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+        d = json.loads(line)
+        if "unavailable" in d:
+            return {"value": None, "error": d["unavailable"]}
+        return dict(d["cpu_baseline"], same_config=d.get("same_config"))
+    except Exception as ex:  # report, never fake
+        return {"value": None, "error": str(ex)[:200]}
+
+
+def measure_scoring(args, cfg, steps, warmup, cpu=True):
+    """C5: sharded_perplexity scoring (eval.hpp:151-222 lock-step walk over S
+    streams, exact softmax).  value: the scorer's kernels per step (CUDA
+    events around each kernel class on the library stream, inputs resident);
+    e2e: the public dl_score call with host arrays (H2D of the ids and
+    targets, D2H of the per-token log-probs), CUDA events on the same stream."""
     import torch
 
     import paper_1502_00512_b200 as dl
@@ -74,39 +94,64 @@ def run_scoring(args, cfg):
     params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32) for s in ((V, H), (H, H), (V, H)))
     model = dl.GpuRnn(V, H, 0, args.precision, 0)
     model.set_params(*params)
-    steps = args.steps + args.warmup
     n = len(ids) // S
     begin = np.arange(S) * n
-    j = np.arange(steps)[:, None]
+    j = np.arange(steps + warmup)[:, None]
     x = ids[begin[None, :] + j].astype(np.uint32)
     y = ids[begin[None, :] + j + 1].astype(np.int64)
     t = np.where(y == 1, -1, y)
     stream = torch.cuda.ExternalStream(load().dl_cuda_stream(model.handle))
-    dl.score(model, x[: args.warmup], t[: args.warmup])  # warm-up (tile setup)
+    for _ in range(max(1, min(warmup, 3))):  # warm-up: same shape (buffers, tensor maps)
+        dl.score(model, x[warmup:], t[warmup:])
+    launches0 = model.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        lp, tot, pred, _ = dl.score(model, x[args.warmup:], t[args.warmup:])
+        lp, tot, pred, _ = dl.score(model, x[warmup:], t[warmup:])
         e1.record(stream)
         torch.cuda.synchronize()
         time.sleep(0.25)
-    ms = e0.elapsed_time(e1)
-    words = S * args.steps
-    value = words / (ms / 1000.0)
+    launches = model.launch_count() - launches0
+    e2e_ms = e0.elapsed_time(e1)
+    # kernel-only time per step (profiling: events around each kernel class
+    # over exactly one scoring bank of `bank` lock-step steps)
+    bank = max(1, min(steps, 16384 // S))
+    model.set_profiling(True)
+    dl.score(model, x[warmup:warmup + bank], t[warmup:warmup + bank])
+    phases = {k: model.kernel_ms(k) for k in ("recurrence_fwd", "logits", "softmax")}
+    model.set_profiling(False)
+    kern_ms = sum(v for v in phases.values() if v > 0) * steps / bank
+    words = S * steps
+    value = words / (kern_ms / 1000.0)
     fpw = 2 * H * V + 2 * H * H
-    peak = PEAKS["bf16_tflops_sustained"]
-    print(json.dumps({
+    logit_ms = phases["logits"]
+    logit_flops = 2.0 * bank * S * V * H
+    achieved = logit_flops / (logit_ms / 1000.0) / 1e12
+    out = {
         "metric": "scoring words/sec", "value": value, "unit": "words/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "steps": steps, "warmup": warmup, "ms_per_step": kern_ms / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": "c5", "desc": cfg["desc"], "V": V, "H": H, "streams": S},
-        "flops_per_word": fpw, "mean_logprob": tot / max(pred, 1),
+        "config": {"workload": cfg["name"], "desc": cfg["desc"], "V": V, "H": H, "streams": S,
+                   "l2": "inputs larger than L2 (W_out bf16 262 MB read per scoring bank)"},
+        "flops_per_word": fpw, "mean_logprob": tot / max(pred, 1), "gpu_launches": launches,
         "clocks": clk.summary(),
-        "roofline": {"bound": "tensor", "kernel": "whole scoring step", "unit": "TFLOP/s",
-                     "achieved": value * fpw / 1e12, "peak": peak,
-                     "frac": value * fpw / 1e12 / peak, "traffic": None}}), flush=True)
+        "roofline": {"bound": "tensor", "kernel": "tc_gemm[logits]", "unit": "TFLOP/s",
+                     "achieved": achieved, "peak": PEAKS["bf16_tflops"],
+                     "frac": achieved / PEAKS["bf16_tflops"], "traffic": None,
+                     "peak_kind": "measured burst (MEASURED_PEAKS.json bf16_tflops)",
+                     "algorithmic_flops_per_launch": logit_flops,
+                     "step_frac_of_sustained_peak": value * fpw / 1e12
+                     / PEAKS["bf16_tflops_sustained"], "phase_ms_per_bank": phases},
+        "e2e": {"value": words / (e2e_ms / 1000.0), "unit": "words/s",
+                "h2d_bytes_per_step": S * 12, "d2h_bytes_per_step": S * 8,
+                "api": "dl_score (host ids / targets in, host per-token log-probs out), "
+                       "CUDA events on the library stream"}}
+    if cpu:
+        out["cpu_baseline"] = cpu_baseline_for(cfg["name"])
+    model.close()
+    return out
 
 
 def run_bottleneck(args, cfg):
@@ -269,62 +314,113 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# Bounded sample of each workload for the reference CPU timer: B streams x
+# Ts unrolled steps per window (softmax training), or S slices (scoring).
+# The reference's dW_out product (matmul_tn_add, mat.hpp:168-184) is single-
+# threaded and streams the whole V x H gradient once per position, so at
+# the C2-C4 shapes one window position costs seconds: T is cut to 1 (B
+# stays the config's, except C4's 256K x 4K gradient).
+REF_SAMPLE = {"c1": dict(T=8, B=8), "c2": dict(T=1, B=128), "c3": dict(T=1, B=128),
+              "c4": dict(T=1, B=16), "c5": dict(S=1024), "bn3": dict(T=1, B=1)}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    name = line.split(":", 1)[1].strip()
+                    break
+            else:
+                name = "unknown"
+        with open("/proc/cpuinfo") as f:
+            txt = f.read()
+        fam = [l.split(":")[1].strip() for l in txt.splitlines() if l.startswith("model\t")]
+        return f"{name} (model {fam[0] if fam else '?'}), {os.cpu_count()} logical CPUs"
+    except Exception:
+        return "unknown"
+
+
 def run_reference(args, cfg):
-    """The reference's own CPU trainer (oracle/_ref = the unmodified
-    /root/reference headers compiled here) on a bounded sample of the same
-    workload: one window of B_s streams x T steps at full V and H
-    (bptt_run + rmsprop_update), all host threads."""
+    """The reference's own CPU implementation of the path, timed in-process:
+    oracle/_ref/ref_bench (the unmodified /root/reference headers built with
+    the reference's flags -O3 -march=<host ISA>, threads = all host CPUs)
+    runs Trainer::run_epoch's window body -- bptt_run + rmsprop_update on
+    resident parameters -- or sharded_perplexity, for exactly --warmup +
+    --steps steps of a bounded sample of the workload (REF_SAMPLE)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
     cores = os.cpu_count() or 1
-    try:
-        ref = oracle.Ref()
-        kind = "reference"
-    except FileNotFoundError:
-        ref = oracle.Orc()
-        kind = "port"
     V, H, T = cfg["V"], cfg["H"], cfg["T"]
-    if cfg.get("score"):
-        # sharded_perplexity over S = 64 slices of a short stream (a bounded
-        # sample of the 1024-stream scoring workload)
-        ids = synthetic_stream(cfg["seed"], V, 64 * 4 + 1)
-        rng = np.random.default_rng(1)
-        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
-                       for s in ((V, H), (H, H), (V, H)))
-        t0 = time.perf_counter()
-        r = ref.sharded_ppl(params, 0, ids, 64)
-        dt = time.perf_counter() - t0
-        value = 64 * 3 / dt
-        print(json.dumps({
-            "metric": "scoring words/sec", "value": value, "unit": "words/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": 3, "warmup": 0,
-            "ms_per_step": 1000 * dt / 3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 (f64 accumulate)", "data": "synthetic",
-            "config": {"workload": "c5", "V": V, "H": H},
-            "cpu_baseline": {"value": value, "unit": "words/s", "cores": cores, "kind": kind,
-                             "sample": "sharded_perplexity, 64 slices x 3 steps, threads=1"},
-            "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}), flush=True)
+    smp = REF_SAMPLE[cfg["name"]]
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    score = bool(cfg.get("score"))
+    if cfg.get("bottleneck"):
+        return run_reference_bn(args, cfg, cores)
+    if not os.path.exists(exe):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/ref_bench not built (needs /root/reference at build time)"}))
         return
-    Bs = min(cfg["B"], args.ref_streams)
-    Ts = min(T, args.ref_unroll)
+    if score:
+        S = smp["S"]
+        argv = [exe, "score", str(V), str(H), str(S), "-", str(args.steps), str(args.warmup),
+                str(cores)]
+        words_per_step = S
+        sample = (f"sharded_perplexity over S={S} slices (the C5 config), {args.steps} timed "
+                  f"lock-step scoring steps after {args.warmup} warm-up steps, threads={cores}")
+        metric = "scoring words/sec"
+    else:
+        Ts, Bs = smp["T"], smp["B"]
+        argv = [exe, "train", str(V), str(H), str(Ts), str(Bs), str(args.steps), str(args.warmup),
+                str(cores)]
+        words_per_step = Ts * Bs
+        sample = (f"window-sampled: {args.steps} timed windows (+{args.warmup} warm-up) of "
+                  f"B={Bs} streams x T={Ts} at V={V}, H={H} (config: B={cfg['B']}, T={T}); "
+                  f"bptt_run(StandardAdapter, softmax) + rmsprop_update in-process on resident "
+                  f"params, threads={cores}")
+        metric = "training words/sec"
+    r = subprocess.run(argv, capture_output=True, text=True)
+    if r.returncode != 0:
+        print(json.dumps({"impl": "reference", "unavailable": f"ref_bench failed: "
+                          f"{r.stderr.strip()[:200]}"}))
+        return
+    res = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    times = res["step_s"]
+    value = words_per_step * len(times) / sum(times)
+    same = score or (smp.get("T") == T and smp.get("B") == cfg["B"])
+    print(json.dumps({
+        "metric": metric, "value": value, "unit": "words/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
+        "data": "synthetic",
+        "config": {"workload": cfg["name"], "desc": cfg["desc"], "V": V, "H": H, "T": T,
+                   "B_per_gpu": cfg["B"]},
+        "same_config": same,
+        "cpu_baseline": {"value": value, "unit": "words/s", "cores": cores, "kind": "reference",
+                         "sample": sample, "cpu": cpu_model(),
+                         "build": "g++ -O3 -march=sapphirerapids (the GPU host's native ISA)"},
+        "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_reference_bn(args, cfg, cores):
+    """Bottleneck model reference arm: bptt_run(BottleneckAdapter) +
+    bottleneck_update through the compiled reference shim (or the oracle)."""
+    import oracle
+    try:
+        ref, kind = oracle.Ref(), "reference"
+    except FileNotFoundError:
+        ref, kind = oracle.Orc(), "port"
+    V, H, P, T = cfg["V"], cfg["H"], cfg["P"], cfg["T"]
+    Bs, Ts = 1, 1
     ids = synthetic_stream(cfg["seed"], V, 1 << 16)
     rng = np.random.default_rng(1)
-    bnm = bool(cfg.get("bottleneck"))
-    if bnm:
-        # the bottleneck model: bptt_run(BottleneckAdapter) + bottleneck_update
-        P = cfg["P"]
-        Bs = 1
-        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
-                       for s in ((V, P), (P, H), (H, H), (H, P)))
-        state = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
-                 np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
-    else:
-        params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
-                       for s in ((V, H), (H, H), (V, H)))
-        state = (np.zeros((H, H), np.float32), np.zeros(V, np.float32), np.zeros(V, np.float32))
+    params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                   for s in ((V, P), (P, H), (H, H), (H, P)))
+    state = (np.zeros(V, np.float32), np.zeros((P, H), np.float32),
+             np.zeros((H, H), np.float32), np.zeros((H, P), np.float32))
     h0 = np.full((Bs, H), 0.5, np.float32)
     times = []
     for i in range(args.warmup + args.steps):
@@ -333,83 +429,34 @@ def run_reference(args, cfg):
         y = ids[s0 + 1:s0 + 1 + Ts * Bs].reshape(Ts, Bs)
         w = (y != 1).astype(np.uint8)
         t0 = time.perf_counter()
-        if bnm:
-            g = ref.bn_bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0)
-            params, state, _ = ref.bn_update(params, state, g, 0.9995, 1e-6, 0.05)
-        else:
-            g = ref.bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0, True, cores)
-            params, state, _ = ref.rmsprop(params, state, g, 0.9995, 1e-6, 0.05)
-        dt = time.perf_counter() - t0
+        g = ref.bn_bptt(params, 0, x, y, w, h0, 1.0 / (Bs * Ts), 1.0)
+        params, state, _ = ref.bn_update(params, state, g, 0.9995, 1e-6, 0.05)
         if i >= args.warmup:
-            times.append(dt)
-        if sum(times) > args.ref_budget_s and len(times) >= 1:
-            break
-    words = Bs * Ts
-    value = words * len(times) / sum(times)
-    sample = (f"window-sampled: {len(times)} window(s) of B={Bs} streams x T={Ts} at "
-              f"V={V}, H={H} (bptt_run + rmsprop_update, softmax), threads={cores}")
-    if bnm:
-        cores = 1
-        sample = (f"window-sampled: {len(times)} window(s) of B={Bs} stream x T={Ts} at "
-                  f"V={V}, H={H}, P={cfg['P']} (bptt_run(BottleneckAdapter) + "
-                  f"bottleneck_update, softmax), threads=1")
-    out = {"metric": "training words/sec", "value": value, "unit": "words/s",
-           "impl": "reference", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
-           "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
-           "data": "synthetic", "config": {"workload": cfg["name"], "desc": cfg["desc"],
-                                            "V": V, "H": H, "T": T, "B_per_gpu": cfg["B"]},
-           "cpu_baseline": {"value": value, "unit": "words/s", "cores": cores, "kind": kind,
-                            "sample": sample},
-           "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+            times.append(time.perf_counter() - t0)
+    value = Bs * Ts * len(times) / sum(times)
+    print(json.dumps({
+        "metric": "training words/sec", "value": value, "unit": "words/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
+        "data": "synthetic", "config": {"workload": cfg["name"], "V": V, "H": H, "P": P},
+        "cpu_baseline": {"value": value, "unit": "words/s", "cores": 1, "kind": kind,
+                         "sample": f"{len(times)} windows of B={Bs} x T={Ts} (bptt_run("
+                                   f"BottleneckAdapter) + bottleneck_update), threads=1",
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--loss", default="softmax", choices=["softmax", "nce"],
-                    help="output layer: exact softmax (the north-star path) or NCE "
-                         "(LossMode::kNce, the reference's default training mode)")
-    ap.add_argument("--nce-k", type=int, default=64)
-    ap.add_argument("--dp-mode", default="vocab", choices=["vocab", "dense"],
-                    help="N>1 data parallel: vocabulary-parallel output layer (default) or "
-                         "the dense dW_out allreduce")
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--profile-steps", type=int, default=3)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-streams", type=int, default=8)
-    ap.add_argument("--ref-unroll", type=int, default=4)
-    ap.add_argument("--ref-budget-s", type=float, default=25.0)
-    args = ap.parse_args()
-    cfg = dict(CONFIGS[args.config], name=args.config)
-    if args.impl == "reference":
-        run_reference(args, cfg)
-        return
-    if cfg.get("score"):
-        run_scoring(args, cfg)
-        return
-    if cfg.get("bottleneck"):
-        run_bottleneck(args, cfg)
-        return
-
+def measure_training(args, cfg, world, rank, local, steps, warmup, dist=None, cpu=True):
+    """Training words/s of one configuration: a step is one window of the
+    offset-stream schedule run by the device trainer (dl_trainer_run),
+    CUDA events on the library stream, max over ranks; then per-kernel times,
+    the roofline of the dominant kernel, and the e2e figure through
+    dl_train_window with page-locked host arrays."""
     import torch
-    import torch.distributed as dist
 
     import paper_1502_00512_b200 as dl
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     V, H, T, B, noffset = cfg["V"], cfg["H"], cfg["T"], cfg["B"], cfg["noffset"]
     L = cfg["L"]
     ids = synthetic_stream(cfg["seed"], V, L)
@@ -428,6 +475,7 @@ def main():
             # V x H gradient on the links, the W_out update split N ways
             model.set_vocab_shard("dp")
     model.set_params(*params)
+    del params
     model.set_opt(None, None, None, 0.9995, 1e-6)
     if args.loss == "nce":
         counts = np.bincount(ids[ids != 1], minlength=V).astype(np.float64)
@@ -447,13 +495,13 @@ def main():
     # (nvidia-smi's 100 ms period would otherwise miss a short timed region)
     with ClockSampler(local) as clk:
         # warm-up (also captures the per-window CUDA graphs)
-        model.trainer_run(0, args.warmup, eta)
+        model.trainer_run(0, warmup, eta)
         torch.cuda.synchronize()
         launches0 = model.launch_count()
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        loss_sum, skipped = model.trainer_run(args.warmup, args.steps, eta)
+        loss_sum, skipped = model.trainer_run(warmup, steps, eta)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -461,24 +509,24 @@ def main():
     ms = e0.elapsed_time(e1)
     launches = model.launch_count() - launches0
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
     vshard = bool(cfg.get("vshard"))
     # data parallel: every rank trains its own B streams; vocabulary-sharded:
     # all ranks cooperate on the same B streams
-    words = (1 if vshard else world) * B * T * args.steps
+    words = (1 if vshard else world) * B * T * steps
     value = words / (ms / 1000.0)
     fpw = flops_per_word(V, H, args.nce_k if args.loss == "nce" else 0)
 
     # per-kernel device times (eager launches + CUDA events on the library
     # stream) -> roofline of the dominant kernel
     model.set_profiling(True)
-    model.trainer_run(args.warmup + args.steps, args.profile_steps, eta)
+    model.trainer_run(warmup + steps, args.profile_steps, eta)
     phases = {}
     for name in ("recurrence_fwd", "logits", "softmax", "dh", "dw_out", "nce_loss", "nce_dh",
                  "recurrence_bwd", "dw_rec", "embed_grad", "nce_out_rows", "rmsprop",
-                 "rmsprop_out"):
+                 "rmsprop_out", "vocab_exchange"):
         v = model.kernel_ms(name)
         if v >= 0:
             phases[name] = v
@@ -486,8 +534,9 @@ def main():
     TB = T * B
     # W_out rows on this GPU; with the vocabulary-parallel DP output layer
     # each GPU scores world x TB rows against V / world
-    Vloc = V // world if (vshard or (world > 1 and args.dp_mode == "vocab")) else V
-    TBo = TB * world if (world > 1 and args.dp_mode == "vocab" and not vshard) else TB
+    dpv = world > 1 and args.dp_mode == "vocab" and not vshard
+    Vloc = V // world if (vshard or dpv) else V
+    TBo = TB * world if dpv else TB
     gemm_flops = {"logits": 2.0 * TBo * Vloc * H, "dh": 2.0 * TBo * Vloc * H,
                   "dw_out": 2.0 * TBo * Vloc * H}
     dom = max(gemm_flops, key=lambda k: phases.get(k, 0.0))
@@ -497,15 +546,15 @@ def main():
     # the step: the burst peak applies; the whole step is held against the
     # sustained peak
     peak = PEAKS["bf16_tflops"]
-    step_ms = ms / args.steps
+    step_ms = ms / steps
     traffic, traffic_src = None, None  # DRAM bytes per launch from the committed ncu capture
     try:
         import glob
         for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json"))):
             with open(path) as f:
-                s = json.load(f).get("dominant_kernel_for_bench_roofline", {})
-            if s.get("kernel") == f"tc_gemm[{dom}]" and s.get("config") == args.config:
-                traffic, traffic_src = s["traffic_bytes_per_launch"], os.path.basename(path)
+                sm = json.load(f).get("dominant_kernel_for_bench_roofline", {})
+            if sm.get("kernel") == f"tc_gemm[{dom}]" and sm.get("config") == cfg["name"]:
+                traffic, traffic_src = sm["traffic_bytes_per_launch"], os.path.basename(path)
     except Exception:
         pass
     roofline = {"bound": "tensor", "kernel": f"tc_gemm[{dom}]", "achieved": achieved,
@@ -522,17 +571,17 @@ def main():
                             "(+10 B/elem of W_out: fp32 master read+write, bf16 shadow write)")
 
     # end-to-end through the public API with host buffers: dl_train_window
-    # per step (H2D of the window ids/targets/mask/h0 from host, bptt_run +
-    # rmsprop_update, D2H of loss, positions, applied and h_final)
+    # per step (H2D of the window ids/targets/mask/h0 from page-locked host
+    # memory, bptt_run + rmsprop_update, D2H of loss, positions, applied and
+    # h_final), CUDA events on the library stream around all the calls
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e and args.loss == "softmax":
         def pinned(shape, dtype):
             return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 
-        # each step's window and the carried hidden state live in page-locked
-        # host memory (the copies themselves are inside the timed region)
+        n_e2e = steps + 3
         wins = []
-        for i in range(args.e2e_steps + 1):
+        for i in range(n_e2e):
             s0 = (i * TB * 7) % (L - TB - 2)
             x, y, w = pinned((T, B), torch.int32), pinned((T, B), torch.int32), \
                 pinned((T, B), torch.uint8)
@@ -542,55 +591,120 @@ def main():
             wins.append(dl.WindowBatch(x.view(np.uint32), y.view(np.uint32), w))
         hbuf = [pinned((B, H), torch.float32) for _ in range(2)]
         hbuf[0][:] = 0.5
-        dl.train_window(model, wins[0], hbuf[0], 1.0 / TB, 1.0, eta, h_final=hbuf[1])
+        for i in range(3):  # warm-up
+            dl.train_window(model, wins[i], hbuf[i % 2], 1.0 / TB, 1.0, eta,
+                            h_final=hbuf[(i + 1) % 2])
         barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for i, wb in enumerate(wins[1:]):
+        e0.record(stream)
+        for i, wb in enumerate(wins[3:]):
             dl.train_window(model, wb, hbuf[(i + 1) % 2], 1.0 / TB, 1.0, eta,
                             h_final=hbuf[i % 2])
-        dt = time.perf_counter() - t0
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        dt = e0.elapsed_time(e1) / 1000.0
         if world > 1:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e = {"value": world * TB * args.e2e_steps / dt, "unit": "words/s",
-               "h2d_bytes_per_step": TB * 9 + B * H * 4, "d2h_bytes_per_step": B * H * 4 + 8 + 8 + 4,
-               "api": "dl_train_window (bptt_run + rmsprop_update), page-locked host arrays"}
+            tt = torch.tensor([dt, wall], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt, wall = float(tt[0].item()), float(tt[1].item())
+        e2e = {"value": world * TB * steps / dt, "unit": "words/s", "steps": steps,
+               "h2d_bytes_per_step": TB * 9 + B * H * 4,
+               "d2h_bytes_per_step": B * H * 4 + 8 + 8 + 4,
+               "wall_clock_value": world * TB * steps / wall,
+               "api": "dl_train_window (bptt_run + rmsprop_update), page-locked host arrays, "
+                      "CUDA events on the library stream"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
-                                "--config", args.config, "--steps", "1", "--warmup", "0"],
-                               capture_output=True, text=True, timeout=600)
-            line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
-            cpu = json.loads(line)["cpu_baseline"]
-        except Exception as ex:  # report, never fake
-            cpu = {"value": None, "error": str(ex)[:200]}
+    cpu_b = None
+    if cpu and rank == 0 and world == 1:
+        cpu_b = cpu_baseline_for(cfg["name"])
+    out = {"metric": "training words/sec", "value": value, "unit": "words/s",
+           "n_gpus": world, "steps": steps, "warmup": warmup,
+           "ms_per_step": step_ms, "higher_is_better": True,
+           "scaling": "strong" if vshard else "weak",
+           "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+           "config": {"workload": cfg["name"], "desc": cfg["desc"], "V": V, "H": H,
+                      "T": T, "B_per_gpu": B,
+                      "global_minibatch": B if vshard else B * world,
+                      "noffset": noffset, "L": L,
+                      "loss": ("exact softmax" if args.loss == "softmax"
+                               else f"NCE k={args.nce_k}"),
+                      "optimizer": "rmsprop (per-word W_in/W_out scalars)",
+                      "parallelism": (f"vocab{world}" if vshard else
+                                      f"dp{world}+vocab-parallel-output"
+                                      if world > 1 and args.dp_mode == "vocab"
+                                      else f"dp{world}"),
+                      "l2": "inputs larger than L2 (W_out bf16 + fp32 master, "
+                            f"{6 * Vloc * H / 1e6:.0f} MB, streamed every window)"},
+           "flops_per_word": fpw, "mean_window_loss": loss_sum / steps,
+           "skipped_updates": skipped, "gpu_launches": launches,
+           "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
+           "cpu_baseline": cpu_b}
+    model.close()
+    return out
 
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--loss", default="softmax", choices=["softmax", "nce"],
+                    help="output layer: exact softmax (the north-star path) or NCE "
+                         "(LossMode::kNce, the reference's default training mode)")
+    ap.add_argument("--nce-k", type=int, default=64)
+    ap.add_argument("--dp-mode", default="vocab", choices=["vocab", "dense"],
+                    help="N>1 data parallel: vocabulary-parallel output layer (default) or "
+                         "the dense dW_out allreduce")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default="c2,c5,c4",
+                    help="configs measured after the headline one (N=1 only) and reported "
+                         "in the line's `secondary` list; '' for none")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    if cfg.get("bottleneck"):
+        run_bottleneck(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cpu = not args.no_cpu_baseline
+    if cfg.get("score"):
+        out = measure_scoring(args, cfg, args.steps, args.warmup, cpu=cpu)
+    else:
+        out = measure_training(args, cfg, world, rank, local, args.steps, args.warmup, dist,
+                               cpu=cpu)
+    if world == 1 and args.secondary:
+        sec = []
+        for name in [n for n in args.secondary.split(",") if n and n != args.config]:
+            c2 = dict(CONFIGS[name], name=name)
+            try:
+                if c2.get("score"):
+                    sec.append(measure_scoring(args, c2, args.steps, args.warmup, cpu=cpu))
+                else:
+                    sec.append(measure_training(args, c2, 1, 0, local, args.steps, args.warmup,
+                                                cpu=cpu))
+            except Exception as ex:  # report, never fake
+                sec.append({"config": {"workload": name}, "error": str(ex)[:300]})
+            torch.cuda.empty_cache()
+        out["secondary"] = sec
     if rank == 0:
-        out = {"metric": "training words/sec", "value": value, "unit": "words/s",
-               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": step_ms, "higher_is_better": True,
-               "scaling": "strong" if vshard else "weak",
-               "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-               "config": {"workload": args.config, "desc": cfg["desc"], "V": V, "H": H,
-                          "T": T, "B_per_gpu": B,
-                          "global_minibatch": B if vshard else B * world,
-                          "noffset": noffset, "L": L,
-                          "loss": ("exact softmax" if args.loss == "softmax"
-                                   else f"NCE k={args.nce_k}"),
-                          "optimizer": "rmsprop (per-word W_in/W_out scalars)",
-                          "parallelism": (f"vocab{world}" if vshard else
-                                          f"dp{world}+vocab-parallel-output"
-                                          if world > 1 and args.dp_mode == "vocab"
-                                          else f"dp{world}"),
-                          "l2": "inputs larger than L2 (W_out bf16 262 MB + fp32 master 524 MB "
-                                "streamed every window)"},
-               "flops_per_word": fpw, "mean_window_loss": loss_sum / args.steps,
-               "skipped_updates": skipped, "gpu_launches": launches,
-               "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
-               "cpu_baseline": cpu}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

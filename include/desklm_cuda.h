@@ -203,6 +203,12 @@ int dl_set_loss_mode(dl_ctx* ctx, int mode);
  * rng.hpp:54-94 on the host, the ln(k q) table lives on the device. */
 int dl_set_noise(dl_ctx* ctx, const double* counts, int64_t V, int k, double floor);
 
+/* The same noise model from its normalised distribution q (NoiseModel::q,
+ * nce.hpp:54-64, already floored and renormalised by the caller, e.g. a
+ * reference NoiseModel): ln(k q) and the AliasSampler(q) tables are built
+ * from q exactly as the reference builds them. */
+int dl_set_noise_dist(dl_ctx* ctx, const double* q, int64_t V, int k);
+
 /* The std::mt19937_64 the noise draws come from (BpttOptions::rng,
  * backprop.hpp:52-61; Trainer::rng_, trainer.hpp:184, :284, :314): 312 state
  * words then the position, as the libstdc++ stream operators write them.
@@ -325,12 +331,19 @@ int dl_bn_train_window(dl_bn* ctx, int64_t T, int64_t B, const uint32_t* inputs,
 int dl_bn_sharded_perplexity(dl_bn* ctx, const uint32_t* ids, int64_t n, int shards,
                              uint32_t bos, double* total_logprob, uint64_t* predicted,
                              double* perplexity);
+/* Lock-step scorer over S streams, as dl_score (sharded_perplexity /
+ * rnn_perplexity / rescore_nbest over the BottleneckAdapter, eval.hpp:84-222,
+ * :693-790): per-token log-probs (NaN where tgt = -1), sums in (j, s) order. */
+int dl_bn_score(dl_bn* ctx, int64_t S, int64_t steps, const uint32_t* in, const int64_t* tgt,
+                const float* h0, float* h_final, double* logp, double* total_logprob,
+                uint64_t* predicted);
 /* NCE mode (LossMode::kNce) for the bottleneck model: as dl_set_loss_mode /
  * dl_set_noise / dl_{set,get}_rng_state of the standard model (the noise
  * model over E, sparse embedding gradient; backprop.hpp:126-156,
  * compress.hpp:204-225). */
 int dl_bn_set_loss_mode(dl_bn* ctx, int mode);
 int dl_bn_set_noise(dl_bn* ctx, const double* counts, int64_t V, int k, double floor);
+int dl_bn_set_noise_dist(dl_bn* ctx, const double* q, int64_t V, int k);
 int dl_bn_set_rng_state(dl_bn* ctx, const uint64_t state[313]);
 int dl_bn_get_rng_state(const dl_bn* ctx, uint64_t state[313]);
 uint64_t dl_bn_launch_count(const dl_bn* ctx);

@@ -156,9 +156,17 @@ static double dot_acc(const float* x, const float* y, int64_t n) {
   return ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) + tail;
 }
 
+/* The three GEMMs split their work over OpenMP threads by output element
+ * (matmul_nt), output column block (matmul_nn) or output row
+ * (matmul_tn_add): every output element still sees exactly the reference's
+ * sequence of operations, so the results do not depend on the thread count
+ * (as parallel_rows, mat.hpp:95-114).  Small products stay serial. */
+#define ORC_PAR_MIN 262144
+
 /* C[MxN] = A[MxK] . B[NxK]^T, rounded to float (mat.hpp:116-134). */
 static void matmul_nt(const float* A, const float* B, float* C, int64_t M,
                       int64_t N, int64_t K) {
+#pragma omp parallel for collapse(2) schedule(static) if (M * N * K >= ORC_PAR_MIN)
   for (int64_t i = 0; i < M; ++i)
     for (int64_t j = 0; j < N; ++j) C[i * N + j] = (float)dot_acc(A + i * K, B + j * K, K);
 }
@@ -167,28 +175,34 @@ static void matmul_nt(const float* A, const float* B, float* C, int64_t M,
  * entries are skipped (mat.hpp:136-166). */
 static void matmul_nn(const float* A, const float* B, float* C, int64_t M,
                       int64_t N, int64_t K, int accumulate, double* acc) {
+  const int64_t JB = 256;
   for (int64_t i = 0; i < M; ++i) {
-    for (int64_t j = 0; j < N; ++j) acc[j] = accumulate ? (double)C[i * N + j] : 0.0;
-    for (int64_t k = 0; k < K; ++k) {
-      const double a = (double)A[i * K + k];
-      if (a == 0.0) continue;
-      const float* bk = B + k * N;
-      for (int64_t j = 0; j < N; ++j) acc[j] += a * (double)bk[j];
+#pragma omp parallel for schedule(static) if (N * K >= ORC_PAR_MIN)
+    for (int64_t j0 = 0; j0 < N; j0 += JB) {
+      const int64_t j1 = j0 + JB < N ? j0 + JB : N;
+      for (int64_t j = j0; j < j1; ++j) acc[j] = accumulate ? (double)C[i * N + j] : 0.0;
+      for (int64_t k = 0; k < K; ++k) {
+        const double a = (double)A[i * K + k];
+        if (a == 0.0) continue;
+        const float* bk = B + k * N;
+        for (int64_t j = j0; j < j1; ++j) acc[j] += a * (double)bk[j];
+      }
+      for (int64_t j = j0; j < j1; ++j) C[i * N + j] = (float)acc[j];
     }
-    for (int64_t j = 0; j < N; ++j) C[i * N + j] = (float)acc[j];
   }
 }
 
-/* C[MxN] += A[KxM]^T . B[KxN], float accumulate, k outer (mat.hpp:168-184). */
+/* C[MxN] += A[KxM]^T . B[KxN], float accumulate, k outer (mat.hpp:168-184);
+ * each row of C accumulates its k terms in the same ascending order. */
 static void matmul_tn_add(const float* A, const float* B, float* C, int64_t K,
                           int64_t M, int64_t N) {
-  for (int64_t k = 0; k < K; ++k) {
-    const float* ak = A + k * M;
-    const float* bk = B + k * N;
-    for (int64_t i = 0; i < M; ++i) {
-      const float a = ak[i];
+#pragma omp parallel for schedule(static) if (M * N * K >= ORC_PAR_MIN)
+  for (int64_t i = 0; i < M; ++i) {
+    float* ci = C + i * N;
+    for (int64_t k = 0; k < K; ++k) {
+      const float a = A[k * M + i];
       if (a == 0.0f) continue;
-      float* ci = C + i * N;
+      const float* bk = B + k * N;
       for (int64_t j = 0; j < N; ++j) ci[j] += a * bk[j];
     }
   }
@@ -675,6 +689,7 @@ int orc_sharded_logprobs(int64_t V, int64_t H, int act, const float* w_in,
       double v = NAN;
       if (any && tgt[s] >= 0) {
         /* scores_t column s: W_out . h_s (eval.hpp:207, rnn.hpp:248-251) */
+#pragma omp parallel for schedule(static) if (V * H >= ORC_PAR_MIN)
         for (int64_t w = 0; w < V; ++w) sc[w] = (float)dot_acc(w_out + w * H, h + s * H, H);
         v = (double)sc[tgt[s]] - lse_vec(sc, V);
         total += v;

@@ -23,12 +23,13 @@ EXPORTS = (
     "dl_launch_count", "dl_set_profiling", "dl_kernel_ms", "dl_test_gemm", "dl_cuda_stream",
     "dl_test_embed", "dl_rank_cursors", "dl_init_uniform", "dl_local_group_create",
     "dl_local_group_destroy", "dl_comm_init_local", "dl_set_vocab_shard",
-    "dl_ln_z_samples", "dl_score_candidates", "dl_set_loss_mode", "dl_set_noise", "dl_set_rng_state", "dl_get_rng_state",
+    "dl_ln_z_samples", "dl_score_candidates", "dl_set_loss_mode", "dl_set_noise", "dl_set_noise_dist", "dl_set_rng_state", "dl_get_rng_state",
     "dl_rng_seed_state", "dl_bn_create", "dl_bn_destroy", "dl_bn_last_error",
     "dl_bn_set_params", "dl_bn_get_params", "dl_bn_set_opt", "dl_bn_get_opt", "dl_bn_window",
     "dl_bn_get_grads", "dl_bn_rmsprop", "dl_bn_train_window", "dl_bn_sharded_perplexity",
     "dl_bn_launch_count", "dl_bn_cuda_stream", "dl_bn_set_loss_mode", "dl_bn_set_noise",
-    "dl_bn_set_rng_state", "dl_bn_get_rng_state", "dl_bn_set_params_quantized",
+    "dl_bn_set_rng_state", "dl_bn_get_rng_state", "dl_bn_set_params_quantized", "dl_bn_score",
+    "dl_bn_set_noise_dist",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -98,6 +99,7 @@ def load():
         "dl_set_vocab_shard": (C.c_int, [vp, C.c_int]),
         "dl_set_loss_mode": (C.c_int, [vp, C.c_int]),
         "dl_set_noise": (C.c_int, [vp, vp, i64, C.c_int, C.c_double]),
+        "dl_set_noise_dist": (C.c_int, [vp, vp, i64, C.c_int]),
         "dl_set_rng_state": (C.c_int, [vp, vp]),
         "dl_get_rng_state": (C.c_int, [vp, vp]),
         "dl_rng_seed_state": (C.c_int, [u64, vp]),
@@ -120,6 +122,8 @@ def load():
         "dl_bn_set_loss_mode": (C.c_int, [vp, C.c_int]),
         "dl_bn_set_params_quantized": (C.c_int, [vp, vp]),
         "dl_bn_set_noise": (C.c_int, [vp, vp, i64, C.c_int, C.c_double]),
+        "dl_bn_set_noise_dist": (C.c_int, [vp, vp, i64, C.c_int]),
+        "dl_bn_score": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, P(C.c_double), P(u64)]),
         "dl_bn_set_rng_state": (C.c_int, [vp, vp]),
         "dl_bn_get_rng_state": (C.c_int, [vp, vp]),
         "dl_bn_launch_count": (u64, [vp]),

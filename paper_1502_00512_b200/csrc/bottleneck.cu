@@ -981,6 +981,60 @@ int dl_bn_train_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
 // sharded_perplexity over the bottleneck adapter (eval.hpp:151-222): S
 // slices walked cold in lockstep, banked so that each output GEMM scores
 // several steps at once
+// Lock-step forward scorer over S streams (the bottleneck adapter's
+// softmax_scores_t + lse_column, eval.hpp:176-220 / :725-751): in[j*S+s]
+// input ids, tgt[j*S+s] target or -1; h0 (S x H) may be NULL for act(0).
+int dl_bn_score(dl_bn* c, int64_t S, int64_t steps, const uint32_t* in, const int64_t* tgt,
+                const float* h0, float* h_final, double* logp, double* total_logprob,
+                uint64_t* predicted) {
+  if (!c) return bn_fail(c, DL_EINVAL, "dl_bn_score: null ctx");
+  if (S < 1 || steps < 0 || (steps > 0 && (!in || !tgt)))
+    return bn_fail(c, DL_EINVAL, "dl_bn_score: bad shape");
+  std::vector<uint32_t> yv(S * steps);
+  std::vector<uint8_t> wv(S * steps);
+  for (int64_t i = 0; i < S * steps; ++i) {
+    if (in[i] >= (uint64_t)c->V || tgt[i] >= c->V)
+      return bn_fail(c, DL_EDATA, "score: id out of vocabulary range");
+    yv[i] = tgt[i] >= 0 ? (uint32_t)tgt[i] : 0u;
+    wv[i] = tgt[i] >= 0 ? 1 : 0;
+  }
+  double tot = 0.0;
+  uint64_t pred = 0;
+  return bn_guarded(c, [&] {
+    const int64_t H = c->H, SH = S * H;
+    const int64_t bank = std::max<int64_t>(1, std::min<int64_t>(steps, 4096 / S));
+    ensure_window(c, bank, bank * S);
+    cudaStream_t st = c->st;
+    if (h0) DL_CUDA(cudaMemcpyAsync(c->htape, h0, SH * 4, cudaMemcpyHostToDevice, st));
+    else fill_f32(c->htape, act0(c->act), SH, st);
+    std::vector<double> lp(bank * S);
+    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
+      const int64_t nb = std::min(bank, steps - j0), N = nb * S;
+      DL_CUDA(cudaMemcpyAsync(c->x, in + j0 * S, N * 4, cudaMemcpyHostToDevice, st));
+      DL_CUDA(cudaMemcpyAsync(c->y, yv.data() + j0 * S, N * 4, cudaMemcpyHostToDevice, st));
+      DL_CUDA(cudaMemcpyAsync(c->w, wv.data() + j0 * S, N, cudaMemcpyHostToDevice, st));
+      input_side(c, N);
+      recurrence_fwd(c, nb, S);
+      output_side(c, N, c->htape + SH, tcm(c) ? c->htape_bf + SH : nullptr, 1.0, false);
+      DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * SH, SH * 4, cudaMemcpyDeviceToDevice, st));
+      DL_CUDA(cudaMemcpyAsync(lp.data(), c->logp_row, N * 8, cudaMemcpyDeviceToHost, st));
+      DL_CUDA(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < N; ++i) {
+        const bool scored = wv[j0 * S + i] != 0;
+        if (logp) logp[j0 * S + i] = scored ? lp[i] : NAN;
+        if (scored) {
+          tot += lp[i];
+          ++pred;
+        }
+      }
+    }
+    if (h_final) DL_CUDA(cudaMemcpyAsync(h_final, c->htape, SH * 4, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaStreamSynchronize(st));
+    if (total_logprob) *total_logprob = tot;
+    if (predicted) *predicted = pred;
+  });
+}
+
 int dl_bn_sharded_perplexity(dl_bn* c, const uint32_t* ids, int64_t n, int shards, uint32_t bos,
                              double* total_logprob, uint64_t* predicted, double* perplexity) {
   if (!c) return bn_fail(c, DL_EINVAL, "dl_bn_sharded_perplexity: null ctx");
@@ -992,52 +1046,25 @@ int dl_bn_sharded_perplexity(dl_bn* c, const uint32_t* ids, int64_t n, int shard
   int64_t max_len = 0;
   for (int64_t s = 0; s < S; ++s) max_len = std::max(max_len, begin[s + 1] - begin[s]);
   const int64_t steps = std::max<int64_t>(0, max_len - 1);
-  std::vector<uint32_t> in(S * steps), yv(S * steps);
-  std::vector<uint8_t> wv(S * steps);
+  std::vector<uint32_t> in(S * steps);
+  std::vector<int64_t> tg(S * steps);
   for (int64_t j = 0; j < steps; ++j)
     for (int64_t s = 0; s < S; ++s) {
       const int64_t len = begin[s + 1] - begin[s], i = j * S + s;
       in[i] = 0;
-      yv[i] = 0;
-      wv[i] = 0;
+      tg[i] = -1;
       if (j + 1 < len) {
         const uint32_t x = ids[begin[s] + j], y = ids[begin[s] + j + 1];
         if (x >= (uint64_t)c->V || y >= (uint64_t)c->V)
           return bn_fail(c, DL_EDATA, "sharded perplexity: id out of vocabulary range");
         in[i] = x;
-        if (y != bos) {
-          yv[i] = y;
-          wv[i] = 1;
-        }
+        if (y != bos) tg[i] = y;
       }
     }
   double tot = 0.0;
   uint64_t pred = 0;
-  const int rc = bn_guarded(c, [&] {
-    const int64_t H = c->H, SH = S * H;
-    const int64_t bank = std::max<int64_t>(1, std::min<int64_t>(steps, 4096 / S));
-    ensure_window(c, bank, bank * S);
-    cudaStream_t st = c->st;
-    fill_f32(c->htape, act0(c->act), SH, st);
-    std::vector<double> lp(bank * S);
-    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
-      const int64_t nb = std::min(bank, steps - j0), N = nb * S;
-      DL_CUDA(cudaMemcpyAsync(c->x, in.data() + j0 * S, N * 4, cudaMemcpyHostToDevice, st));
-      DL_CUDA(cudaMemcpyAsync(c->y, yv.data() + j0 * S, N * 4, cudaMemcpyHostToDevice, st));
-      DL_CUDA(cudaMemcpyAsync(c->w, wv.data() + j0 * S, N, cudaMemcpyHostToDevice, st));
-      input_side(c, N);
-      recurrence_fwd(c, nb, S);
-      output_side(c, N, c->htape + SH, tcm(c) ? c->htape_bf + SH : nullptr, 1.0, false);
-      DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * SH, SH * 4, cudaMemcpyDeviceToDevice, st));
-      DL_CUDA(cudaMemcpyAsync(lp.data(), c->logp_row, N * 8, cudaMemcpyDeviceToHost, st));
-      DL_CUDA(cudaStreamSynchronize(st));
-      for (int64_t i = 0; i < N; ++i)
-        if (wv[j0 * S + i]) {
-          tot += lp[i];
-          ++pred;
-        }
-    }
-  });
+  const int rc = dl_bn_score(c, S, steps, in.data(), tg.data(), nullptr, nullptr, nullptr, &tot,
+                             &pred);
   if (rc != DL_OK) return rc;
   if (pred == 0) return bn_fail(c, DL_EINVAL, "sharded perplexity: no predicted tokens");
   if (total_logprob) *total_logprob = tot;
@@ -1053,15 +1080,17 @@ int dl_bn_set_loss_mode(dl_bn* c, int mode) {
   return DL_OK;
 }
 
-int dl_bn_set_noise(dl_bn* c, const double* counts, int64_t V, int k, double floor) {
+namespace {
+int bn_noise(dl_bn* c, const double* counts, int64_t V, int k, double floor, bool dist) {
   if (!c || !counts) return bn_fail(c, DL_EINVAL, "dl_bn_set_noise: null argument");
   if (V != c->V) return bn_fail(c, DL_EINVAL, "NoiseModel: vocabulary size mismatch");
   if (k < 1) return bn_fail(c, DL_EINVAL, "NoiseModel: k >= 1");
-  if (!(floor > 0.0)) return bn_fail(c, DL_EINVAL, "NoiseModel: floor must be > 0");
+  if (!dist && !(floor > 0.0)) return bn_fail(c, DL_EINVAL, "NoiseModel: floor must be > 0");
   return bn_guarded(c, [&] {
     std::vector<double> lnkq, prob;
     std::vector<uint32_t> alias;
-    noise_tables(counts, V, k, floor, lnkq, prob, alias);
+    if (dist) noise_tables_q(counts, V, k, lnkq, prob, alias);
+    else noise_tables(counts, V, k, floor, lnkq, prob, alias);
     if (!c->ln_kq_d) c->ln_kq_d = bn_alloc<double>(V);
     if (!c->nz_prob_d) c->nz_prob_d = bn_alloc<double>(V);
     if (!c->nz_alias_d) c->nz_alias_d = bn_alloc<uint32_t>(V);
@@ -1072,6 +1101,15 @@ int dl_bn_set_noise(dl_bn* c, const double* counts, int64_t V, int k, double flo
     c->nz_prob = std::move(prob);
     c->nce_k = k;
   });
+}
+}  // namespace
+
+int dl_bn_set_noise(dl_bn* c, const double* counts, int64_t V, int k, double floor) {
+  return bn_noise(c, counts, V, k, floor, false);
+}
+
+int dl_bn_set_noise_dist(dl_bn* c, const double* q, int64_t V, int k) {
+  return bn_noise(c, q, V, k, 0.0, true);
 }
 
 int dl_bn_set_rng_state(dl_bn* c, const uint64_t state[313]) {

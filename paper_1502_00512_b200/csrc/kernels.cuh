@@ -49,6 +49,8 @@ int embed_short_max();
 // NoiseModel + AliasSampler tables (host; nce.cu)
 void noise_tables(const double* counts, int64_t V, int k, double floor, std::vector<double>& lnkq,
                   std::vector<double>& prob, std::vector<uint32_t>& alias);
+void noise_tables_q(const double* q, int64_t V, int k, std::vector<double>& lnkq,
+                    std::vector<double>& prob, std::vector<uint32_t>& alias);
 
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
 void fill_f32(float* x, float v, int64_t n, cudaStream_t st);

@@ -308,18 +308,26 @@ void noise_tables(const double* counts, int64_t V, int k, double floor, std::vec
   }
   DL_REQUIRE(total > 0.0, 1, "NoiseModel: zero total");
   std::vector<double> q(V);
-  lnkq.assign(V, 0.0);
   double qsum = 0.0;
   for (int64_t w = 0; w < V; ++w) {
     q[w] = std::max(counts[w] / total, floor);
     qsum += q[w];
   }
+  for (int64_t w = 0; w < V; ++w) q[w] /= qsum;
+  noise_tables_q(q.data(), V, k, lnkq, prob, alias);
+}
+
+// ln(k q) and AliasSampler(q) from NoiseModel's normalised distribution
+// (nce.hpp:60-64; rng.hpp:54-89): the caller already built q.
+void noise_tables_q(const double* q, int64_t V, int k, std::vector<double>& lnkq,
+                    std::vector<double>& prob, std::vector<uint32_t>& alias) {
+  lnkq.assign(V, 0.0);
   for (int64_t w = 0; w < V; ++w) {
-    q[w] /= qsum;
+    DL_REQUIRE(q[w] > 0.0, 1, "NoiseModel: distribution must be positive");
     lnkq[w] = std::log(static_cast<double>(k) * q[w]);
   }
   double tw = 0.0;
-  for (double v : q) tw += v;
+  for (int64_t i = 0; i < V; ++i) tw += q[i];
   std::vector<double> scaled(V);
   prob.assign(V, 0.0);
   alias.assign(V, 0);

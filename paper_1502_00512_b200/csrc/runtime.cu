@@ -530,10 +530,12 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
 
 // ------------------------------------------------------------------ NCE
 // NoiseModel (nce.hpp:41-66) + AliasSampler (rng.hpp:54-89), host side.
-void nce_build(dl_ctx* c, const double* counts, int64_t V, int k, double floor) {
+void nce_build(dl_ctx* c, const double* counts, int64_t V, int k, double floor,
+               bool dist = false) {
   std::vector<double> lnkq, prob;
   std::vector<uint32_t> alias;
-  noise_tables(counts, V, k, floor, lnkq, prob, alias);
+  if (dist) noise_tables_q(counts, V, k, lnkq, prob, alias);
+  else noise_tables(counts, V, k, floor, lnkq, prob, alias);
   c->nce_k = k;
   if (!c->ln_kq_d) c->ln_kq_d = dalloc<double>(V);
   if (!c->nz_prob_d) c->nz_prob_d = dalloc<double>(V);
@@ -2084,6 +2086,13 @@ int dl_set_noise(dl_ctx* c, const double* counts, int64_t V, int k, double floor
   if (k < 1) return fail(c, DL_EINVAL, "NoiseModel: k must be >= 1");
   if (!(floor > 0.0)) return fail(c, DL_EINVAL, "config: noise_floor must be > 0");
   return guarded(c, [&] { nce_build(c, counts, V, k, floor); });
+}
+
+int dl_set_noise_dist(dl_ctx* c, const double* q, int64_t V, int k) {
+  if (!c || !q) return fail(c, DL_EINVAL, "dl_set_noise_dist: null argument");
+  if (V != c->V) return fail(c, DL_EINVAL, "NoiseModel: vocabulary size mismatch");
+  if (k < 1) return fail(c, DL_EINVAL, "NoiseModel: k must be >= 1");
+  return guarded(c, [&] { nce_build(c, q, V, k, 0.0, true); });
 }
 
 int dl_set_rng_state(dl_ctx* c, const uint64_t state[313]) {

@@ -243,7 +243,29 @@ def write_ppl_match(ref, out):
                         V=V, H=H, logs=logs, initial=ini, eta=0.05)
 
 
+def write_ppl_match_h1024(ref, out):
+    """The PPL match at H = 1,024 (bf16 contractions of K = 1,024 in the
+    recurrence / logits / dh, K = 10,000 in dh): the same corpus, V = 10,000,
+    one epoch of Trainer<StandardTraits> over the first 65,536 training ids
+    (N = 1,024 streams, T = 8: 1,024 windows), validation on the first
+    20,000 ids, eta 0.01 (0.05 diverges at this width on the reference too),
+    init_uniform seed 1 (slow: ~15 min on 8 host threads)."""
+    tr, va = ref.gen_corpus(555, 1_000_000, 1, 60_000, 2, 10000)
+    tr, va = tr[:65536], va[:20000]
+    V, H, eta = 10000, 1024, 0.01
+    params = ref.init_uniform(V, H, 1)
+    cfg = oracle.TrainConfig(nstate=H, noffset=128, minibatch=8, unroll=8, eta=eta,
+                             max_epochs=1, mode=1, threads=os.cpu_count())
+    _, logs, ini = ref.train(cfg, params, tr, va)
+    np.savez_compressed(os.path.join(out, "ppl_match_h1024.npz"), train=tr, valid=va,
+                        init_seed=1, V=V, H=H, logs=logs, initial=ini, eta=eta)
+
+
 def main():
+    import sys
+    if len(sys.argv) > 1:  # regenerate one fixture: make_golden.py write_ppl_match_h1024
+        getattr(sys.modules[__name__], sys.argv[1])(oracle.Ref(), HERE)
+        return
     ref = oracle.Ref()
     out = os.path.join(HERE)
     # bptt windows: the pinned FD instance shape (test_backprop.cpp:185-231),
@@ -289,6 +311,7 @@ def main():
     write_rnqz(ref, out)
     write_ngram_scorers(ref, out)
     write_ppl_match(ref, out)
+    write_ppl_match_h1024(ref, out)
     print("golden fixtures written to", out)
 
 

@@ -1,4 +1,4 @@
-"""PPL match at the C1 configuration: the reference's
+"""PPL match at the C1 configuration (and at H = 1,024): the reference's
 own PPL-match corpus (TextGenerator(GenConfig{}, 555), normalized, 10,000-word
 vocabulary, first 262,144 training ids, 50,000 validation ids), init_uniform
 seed 1, H=128, T=8, B=8, noffset=128 (N=1,024 streams), softmax, eta 0.05:
@@ -15,10 +15,14 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-@pytest.mark.parametrize("precision,rel", [("bf16", 1e-2), ("fp32", 1e-2)])
-def test_c1_ppl_match_one_epoch(precision, rel):
+@pytest.mark.parametrize("fixture,precision,rel", [
+    ("ppl_match_c1.npz", "bf16", 1e-2), ("ppl_match_c1.npz", "fp32", 1e-2),
+    # H = 1,024 (K = 1,024 bf16 contractions in the recurrence and logits,
+    # K = 10,000 in dh): tests/golden/make_golden.py write_ppl_match_h1024
+    ("ppl_match_h1024.npz", "bf16", 1e-2), ("ppl_match_h1024.npz", "fp32", 1e-2)])
+def test_ppl_match_one_epoch(fixture, precision, rel):
     import paper_1502_00512_b200 as dl
-    g = np.load(os.path.join(GOLD, "ppl_match_c1.npz"))
+    g = np.load(os.path.join(GOLD, fixture))
     V, H = int(g["V"]), int(g["H"])
     params = dl.init_uniform(V, H, int(g["init_seed"]))
     cfg = dl.TrainConfig(nstate=H, noffset=128, minibatch=8, unroll=8, eta=float(g["eta"]),
