@@ -286,6 +286,57 @@ inline void str(std::ostream& o, const std::string& s) {
   u64(o, s.size());
   o.write(s.data(), static_cast<std::streamsize>(s.size()));
 }
+// little-endian readers (util.hpp:115-162); short reads are DataError
+inline void need(std::istream& is, const char* what) {
+  if (!is) throw DataError(std::string("truncated input: ") + what);
+}
+inline std::uint8_t get_u8(std::istream& is) {
+  char c = 0;
+  is.get(c);
+  need(is, "u8");
+  return static_cast<std::uint8_t>(c);
+}
+inline std::uint32_t get_u32(std::istream& is) {
+  unsigned char b[4];
+  is.read(reinterpret_cast<char*>(b), 4);
+  need(is, "u32");
+  std::uint32_t v = 0;
+  for (int i = 3; i >= 0; --i) v = (v << 8) | b[i];
+  return v;
+}
+inline std::uint64_t get_u64(std::istream& is) {
+  unsigned char b[8];
+  is.read(reinterpret_cast<char*>(b), 8);
+  need(is, "u64");
+  std::uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+  return v;
+}
+inline float get_f32(std::istream& is) {
+  const std::uint32_t u = get_u32(is);
+  float v;
+  std::memcpy(&v, &u, 4);
+  return v;
+}
+inline double get_f64(std::istream& is) {
+  const std::uint64_t u = get_u64(is);
+  double v;
+  std::memcpy(&v, &u, 8);
+  return v;
+}
+inline std::string get_str(std::istream& is) {
+  const std::uint64_t n = get_u64(is);
+  if (n > (1ull << 30)) throw DataError("implausible string length");
+  std::string s(static_cast<std::size_t>(n), '\0');
+  is.read(&s[0], static_cast<std::streamsize>(n));
+  need(is, "string");
+  return s;
+}
+inline void magic(std::istream& is, const char* m, const char* what) {
+  char b[4];
+  is.read(b, 4);
+  if (!is || std::memcmp(b, m, 4) != 0) throw DataError(std::string(what) + ": bad magic");
+}
 }  // namespace io
 
 // RNLM (rnn.hpp:263-285): W_out stored H x V.
@@ -330,18 +381,31 @@ struct EpochLog {
   std::size_t skipped_updates = 0;
 };
 
-// Trainer<StandardTraits> (trainer.hpp:171-476), softmax mode, with the
-// epoch loop on the device.  Cfg is the reference's TrainConfig (or any
-// struct with its field names).
+namespace detail {
+inline std::vector<std::string> words_of(std::vector<std::string> w) { return w; }
+template <class Vocab>
+auto words_of(const Vocab& v) -> decltype(v.words(), std::vector<std::string>()) {
+  return std::vector<std::string>(v.words().begin(), v.words().end());
+}
+}  // namespace detail
+
+// Trainer<StandardTraits> (trainer.hpp:171-476) with the epoch loop on the
+// device (window build, bptt, rmsprop, hidden carry, wrap reset in one CUDA
+// graph per window), softmax or NCE (TrainConfig::mode).  Cfg is the
+// reference's TrainConfig (or any struct with its field names); the
+// vocabulary is a desklm::Vocabulary (or its word list).  Same public
+// interface as the reference's Trainer: train / validate / logs / epoch /
+// eta / best_ppl / initial_ppl / config / vocab / params (download) and
+// RTRN save_checkpoint / load_checkpoint, byte-compatible.  (For the
+// reference's own Trainer class over the device see traits.hpp.)
 template <class Cfg>
 class Trainer {
  public:
-  template <class Params, class IdStream>
-  Trainer(const Cfg& cfg, const Params& params, std::vector<std::string> vocab,
-          const IdStream& train, const IdStream& valid, Precision prec = Precision::kBf16,
-          int device = 0)
+  template <class Params, class IdStream, class Vocab>
+  Trainer(const Cfg& cfg, const Params& params, const Vocab& vocab, const IdStream& train,
+          const IdStream& valid, Precision prec = Precision::kBf16, int device = 0)
       : cfg_(cfg),
-        vocab_(std::move(vocab)),
+        vocab_(detail::words_of(vocab)),
         train_(train.ids),
         model_(params.v, params.h, static_cast<int>(params.act), prec, device),
         rng_(cfg.seed) {
@@ -373,6 +437,13 @@ class Trainer {
     eta_ = cfg_.eta;
   }
 
+  const Cfg& config() const { return cfg_; }
+  const std::vector<std::string>& vocab() const { return vocab_; }
+  // the parameters as the reference's RnnParams<float> (downloaded)
+  template <class Params>
+  void params(Params& out) const {
+    model_.download(out);
+  }
   const std::vector<EpochLog>& logs() const { return logs_; }
   int epoch() const { return epoch_; }
   double eta() const { return eta_; }
@@ -481,6 +552,101 @@ class Trainer {
     os.write("TEND", 4);
   }
 
+  // trainer.hpp:300-336: a checkpoint written with an identical
+  // configuration (max_epochs may differ) and streams; training then
+  // continues as if uninterrupted.  DataError on any mismatch.
+  void load_checkpoint(std::istream& is) {
+    io::magic(is, "RTRN", "trainer checkpoint");
+    const std::uint32_t version = io::get_u32(is);
+    if (version != 1) throw DataError("trainer checkpoint: unsupported version " +
+                                      std::to_string(version));
+    const bool ok =
+        io::get_u64(is) == static_cast<std::uint64_t>(cfg_.nstate) &&
+        io::get_u64(is) == static_cast<std::uint64_t>(cfg_.nproj) &&
+        io::get_u32(is) == static_cast<std::uint32_t>(cfg_.noffset) &&
+        io::get_u32(is) == static_cast<std::uint32_t>(cfg_.minibatch) &&
+        io::get_u32(is) == static_cast<std::uint32_t>(cfg_.unroll) &&
+        io::get_f64(is) == cfg_.eta && io::get_f64(is) == cfg_.rho &&
+        io::get_f64(is) == cfg_.eps && io::get_f64(is) == cfg_.clip &&
+        io::get_u8(is) == static_cast<std::uint8_t>(cfg_.mode) &&
+        io::get_u32(is) == static_cast<std::uint32_t>(cfg_.nce_k) &&
+        io::get_f64(is) == cfg_.noise_floor && (static_cast<void>(io::get_u32(is)), true) &&
+        io::get_u64(is) == static_cast<std::uint64_t>(cfg_.seed) &&
+        io::get_u8(is) == static_cast<std::uint8_t>(cfg_.act) &&
+        io::get_f64(is) == cfg_.divergence_factor &&
+        io::get_u64(is) == static_cast<std::uint64_t>(cfg_.valid_limit) &&
+        io::get_u32(is) == static_cast<std::uint32_t>(cfg_.valid_shards) &&
+        io::get_f64(is) == cfg_.init_range;
+    if (!ok) throw DataError("trainer checkpoint: configuration does not match this run");
+    const int epoch = static_cast<int>(io::get_u32(is));
+    const double eta = io::get_f64(is), best = io::get_f64(is);
+    const int bad = static_cast<int>(io::get_u32(is));
+    const double initial = io::get_f64(is);
+    std::mt19937_64 rng;
+    {
+      std::istringstream rs(io::get_str(is));
+      rs >> rng;
+      if (rs.fail()) throw DataError("trainer checkpoint: bad generator state");
+    }
+    const std::int64_t V = model_.vocab(), H = model_.hidden();
+    const std::int64_t N = static_cast<std::int64_t>(cfg_.noffset) * cfg_.minibatch;
+    if (io::get_u64(is) != static_cast<std::uint64_t>(N))
+      throw DataError("trainer checkpoint: cursor count mismatch");
+    std::vector<std::int64_t> cur(N);
+    const std::int64_t L = static_cast<std::int64_t>(train_.size());
+    for (auto& c : cur) {
+      c = static_cast<std::int64_t>(io::get_u64(is));
+      if (c < 0 || c >= L) throw DataError("trainer checkpoint: cursor out of range");
+    }
+    std::vector<float> hid(N * H);
+    for (auto& x : hid) x = io::get_f32(is);
+    // RNLM (rnn.hpp:283-308), W_out stored H x V
+    io::magic(is, "RNLM", "rnn checkpoint");
+    if (io::get_u32(is) != 1) throw DataError("rnn checkpoint: unsupported version");
+    const std::int64_t v = static_cast<std::int64_t>(io::get_u64(is));
+    const std::int64_t h = static_cast<std::int64_t>(io::get_u64(is));
+    if (v != V || h != H) throw DataError("trainer checkpoint: model shape mismatch");
+    io::get_u8(is);  // activation (part of the configuration echo)
+    std::vector<float> w_in(V * H), w_rec(H * H), w_out(V * H);
+    for (auto& x : w_in) x = io::get_f32(is);
+    for (auto& x : w_rec) x = io::get_f32(is);
+    for (std::int64_t i = 0; i < H; ++i)
+      for (std::int64_t w = 0; w < V; ++w) w_out[w * H + i] = io::get_f32(is);
+    if (io::get_u64(is) != static_cast<std::uint64_t>(V))
+      throw DataError("rnn checkpoint: vocabulary size mismatch");
+    for (std::int64_t i = 0; i < V; ++i)
+      if (io::get_str(is) != vocab_[static_cast<std::size_t>(i)])
+        throw DataError("trainer checkpoint: vocabulary mismatch");
+    // ROPT (rmsprop.hpp:151-166)
+    io::magic(is, "ROPT", "rmsprop state");
+    if (io::get_u32(is) != 1) throw DataError("rmsprop state: unsupported version");
+    if (io::get_u64(is) != static_cast<std::uint64_t>(V) ||
+        io::get_u64(is) != static_cast<std::uint64_t>(H))
+      throw DataError("trainer checkpoint: model shape mismatch");
+    const double rho = io::get_f64(is), eps = io::get_f64(is);
+    std::vector<float> m_rec(H * H), m_in(V), m_out(V);
+    for (auto& x : m_rec) x = io::get_f32(is);
+    for (auto& x : m_in) x = io::get_f32(is);
+    for (auto& x : m_out) x = io::get_f32(is);
+    io::magic(is, "TEND", "trainer checkpoint trailer");
+    check(dl_trainer_set_state(model_.get(), cur.data(), hid.data()), model_.get());
+    check(dl_set_params(model_.get(), w_in.data(), w_rec.data(), w_out.data()), model_.get());
+    model_.set_opt(m_rec.data(), m_in.data(), m_out.data(), rho, eps);
+    rng_ = rng;
+    if (static_cast<int>(cfg_.mode) == 0) put_rng();
+    epoch_ = epoch;
+    eta_ = eta;
+    best_ppl_ = best;
+    bad_epochs_ = bad;
+    initial_ppl_ = initial;
+  }
+
+  void load_checkpoint(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw DataError("cannot open input file: " + path);
+    load_checkpoint(in);
+  }
+
   void save_checkpoint(const std::string& path) const {
     const std::string tmp = path + ".tmp";
     {
@@ -558,11 +724,11 @@ struct WindowBatch {
   std::vector<std::uint32_t> inputs, targets;
   std::vector<std::uint8_t> weights;
 };
-struct TrainConfig {  // trainer.hpp:43-93 defaults (mode 1 = softmax)
+struct TrainConfig {  // trainer.hpp:43-93 defaults (mode 0 = LossMode::kNce)
   std::int64_t nstate = 256, nproj = 0;
   int noffset = 128, minibatch = 8, unroll = 16;
   double eta = 1e-3, rho = 0.9995, eps = 1e-6, clip = 1.0;
-  int mode = 1, nce_k = 64;
+  int mode = 0, nce_k = 64;
   double noise_floor = 1e-8;
   int max_epochs = 20;
   std::uint64_t seed = 1;

@@ -40,6 +40,7 @@ int main(int argc, char** argv) {
     cfg.unroll = std::stoi(argv[6]);
     cfg.max_epochs = std::stoi(argv[7]);
     cfg.eta = std::stod(argv[8]);
+    cfg.mode = 1;  // exact softmax (the reference default is NCE, trainer.hpp:53)
     const auto prec = std::string(argv[9]) == "bf16" ? b2::Precision::kBf16 : b2::Precision::kFp32;
     b2::lite::RnnParams p(V, H);
     const auto w = slurp<float>(dir + "/params.f32");
@@ -53,6 +54,13 @@ int main(int argc, char** argv) {
     b2::Trainer<b2::lite::TrainConfig> tr(cfg, p, vocab, train, valid, prec);
     tr.train(&std::cerr);
     tr.save_checkpoint(dir + "/ckpt.rtrn");
+    {
+      // load_checkpoint (trainer.hpp:300-336) round trip: a fresh trainer
+      // restored from the file writes the same bytes
+      b2::Trainer<b2::lite::TrainConfig> again(cfg, p, vocab, train, valid, prec);
+      again.load_checkpoint(dir + "/ckpt.rtrn");
+      again.save_checkpoint(dir + "/ckpt2.rtrn");
+    }
     std::ofstream log(dir + "/logs.csv");
     log.precision(17);
     log << tr.initial_ppl() << "\n";

@@ -38,6 +38,7 @@ def test_cpp_trainer_matches_python_and_oracle(tmp_path, orc):
                         str(epochs), str(eta), "fp32"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     blob = (tmp_path / "ckpt.rtrn").read_bytes()
+    assert (tmp_path / "ckpt2.rtrn").read_bytes() == blob  # load_checkpoint round trip
     kw = dict(nstate=H, noffset=noffset, minibatch=B, unroll=T, eta=eta, max_epochs=epochs,
               mode=1)
     t = dl.Trainer(dl.TrainConfig(**kw), params, dl.make_vocab(V), tr, va, "fp32")
