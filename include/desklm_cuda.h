@@ -178,7 +178,10 @@ int dl_trainer_set_state(dl_ctx* ctx, const int64_t* cursors,
 /* ---- multi-GPU ----------------------------------------------------------- */
 
 /* NCCL communicator for data-parallel streams (gradient allreduce before
- * clip).  Rank 0 calls dl_comm_unique_id and broadcasts the 128 bytes. */
+ * clip).  Rank 0 calls dl_comm_unique_id and broadcasts the 128 bytes.  A
+ * one-rank communicator is a real NCCL communicator: the multi-rank code
+ * paths (collectives, gathered windows, the sharded output layer) run on a
+ * single GPU with identity exchanges. */
 int dl_comm_unique_id(uint8_t id[128]);
 int dl_comm_init(dl_ctx* ctx, const uint8_t id[128], int nranks, int rank);
 

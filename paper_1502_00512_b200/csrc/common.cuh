@@ -79,6 +79,15 @@ __device__ __forceinline__ float rms_step(double eta, float g, double denom, dou
 // GEMM problem description shared by the SIMT (fp32) and tcgen05 (bf16)
 // kernels.  C (+ split * split_stride) receives fp32 results; for k_splits>1
 // the caller reduces the slices.
+// dS of one logit (backprop.hpp:179-186) from the row's lse (fp32) and
+// scale: scale * 2^((s - lse) log2 e); the target column subtracts the scale
+// afterwards.  Shared by the in-place softmax rows kernel and the dh GEMM's
+// operand transform so both produce the same bits.
+constexpr float kDsLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float ds_of_logit(float s, float lse, float sc) {
+  return sc * exp2f((s - lse) * kDsLog2e);
+}
+
 struct GemmDesc {
   int M, N, K;
   int a_major, b_major;
@@ -119,9 +128,23 @@ struct GemmDesc {
   float* rms_m;
   unsigned* rms_cnt;  // [ceil(M / 256)], zero at launch
   double rho, eps, eta;
+  // dS on the fly (the dh GEMM over bf16 logits, A K-major; pair tiles):
+  // each A tile is rewritten in shared memory before the MMAs as
+  //   bf16(xf_sc[r] * exp2((s - xf_lse[r]) * log2 e) - (k == xf_tgt[r] ? xf_sc[r] : 0))
+  // (backprop.hpp:179-186) and the CTAs of N tile 0 store it to xf_out
+  // (ld = lda) for the dW_out GEMM.
+  int xf;
+  const float* xf_lse;
+  const float* xf_sc;
+  const uint32_t* xf_tgt;
+  bf16* xf_out;
   unsigned long long* trace;  // DL_GEMM_TRACE diagnostics (fused kernel), or null
   int trace_warps;            // DL_GEMM_TRACE_WARPS: trace three warps of one CTA
 };
+
+// whether gemm_tc runs an M x N GEMM on CTA-pair tiles (the xf transform
+// and the fused rmsprop epilogue exist only there)
+bool tc_pair_tiles(int M, int N);
 
 // gemm_simt.cu
 void gemm_f32(const GemmDesc& g, cudaStream_t st);

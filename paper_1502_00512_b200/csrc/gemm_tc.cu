@@ -230,6 +230,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #ifndef DL_RMS_RING
 #define DL_RMS_RING 4  // cp.async chunks of the fp32 master in flight per warp (all of pass 2)
 #endif
+#ifndef DL_XF_DIAG
+#define DL_XF_DIAG 0  // timing diagnostics of the dS transform (wrong results): 1 no math,
+                      // 2 no proxy fence, 4 no cross-CTA handshake, 8 no smem pass,
+                      // 16 no dS stores, 32 producer ignores `stored`
+#endif
+#ifndef DL_RMS_PREFETCH
+#define DL_RMS_PREFETCH 0  // L2 prefetch of the next tile's A (dS^T) in the fused kernel
+#endif                     // (measured: 0.564 vs 0.527 ms at C3 -- off)
 template <bool RMS>
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2;   // 128 rows of A
@@ -237,7 +245,10 @@ struct Cfg2 {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = RMS ? DL_RMS_STAGES : DL_PAIR_STAGES;
   static constexpr int TMEM_COLS = 512;         // 2 accumulator stages x 256 columns
-  static constexpr int EPI_OFF = STAGES * STAGE + 256;
+  // barriers: full, empty [STAGES]; tfull, tempty [2]; (xf) afull, xready,
+  // stored [STAGES]; then the TMEM address slot
+  static constexpr int BAR_BYTES = (5 * STAGES + 4) * 8 + 16;
+  static constexpr int EPI_OFF = STAGES * STAGE + (BAR_BYTES + 255) / 256 * 256;
   static constexpr int EPI_CHUNK_BYTES = 32 * 32 * 4;
   static constexpr int EPI_WARP_BYTES = RMS ? DL_RMS_RING * EPI_CHUNK_BYTES : 0;
   static constexpr int SMEM = EPI_OFF + kEpiWarps * EPI_WARP_BYTES + 1024;
@@ -274,6 +285,45 @@ __device__ __forceinline__ void mbar_arrive_rank0(uint32_t bar) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(0));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// wait with cluster-scope acquire: the arrivals are the peer CTA's
+// release.cluster arrives after its shared-memory writes
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -482,16 +532,26 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
   if (tr && lane == 0) tr[3] = gtimer_ns();
 }
 
-template <bool A_MN, bool B_MN, bool RMS>
+// XF: the A tile (bf16 logits, K-major) is turned into dS in shared memory
+// by the epilogue warps before the MMAs read it (GemmDesc::xf): the A load
+// completes on a CTA-local barrier (afull), the eight epilogue warps of both
+// CTAs rewrite their tile and arrive on the leader's xready, the leader's MMA
+// waits for B (full) and both transformed A halves (xready).  On N tile 0 the
+// rewritten tile is also stored to xf_out by TMA; `stored` holds the stage
+// until that store has read it.  The epilogue warps transform tile u's k-
+// blocks, then drain its accumulator, then move on (the dh GEMM has one or
+// two long-K tiles per pair).
+template <bool A_MN, bool B_MN, bool RMS, bool XF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                GemmDesc g, Sched sc) {
+                const __grid_constant__ CUtensorMap tmD, GemmDesc g, Sched sc) {
   using C = Cfg2<RMS>;
+  static_assert(!XF || (!A_MN && !RMS), "xf: K-major A, plain epilogue");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * C::STAGES + 4);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -500,10 +560,19 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
   auto tfull = [&](int a) { return smem_u32(&bars[2 * C::STAGES + a]); };
   auto tempty = [&](int a) { return smem_u32(&bars[2 * C::STAGES + 2 + a]); };
+  auto afull = [&](int s) { return smem_u32(&bars[2 * C::STAGES + 4 + s]); };
+  auto xready = [&](int s) { return smem_u32(&bars[3 * C::STAGES + 4 + s]); };
+  auto stored = [&](int s) { return smem_u32(&bars[4 * C::STAGES + 4 + s]); };
 
   if (threadIdx.x == 32) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 2 * kEpiWarps); }
+    if (XF)
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init(afull(s), 1);
+        mbar_init(xready(s), 2 * kEpiWarps);
+        mbar_init(stored(s), kEpiWarps);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -531,12 +600,38 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         sc.decode(u, mt, nt, kb0, kb1);
         const int m0 = mt * 256 + (int)rank * 128;
         const int n0 = nt * 256 + (int)rank * 128;
+#if DL_RMS_PREFETCH
+        if (RMS && u + npairs < total) {
+          // the fused dW_out kernel's A (dS^T, read once from HBM per M
+          // block): pull the next tile's half into L2 while this tile runs,
+          // so the short-K mainloop (32 k-blocks) never waits on HBM
+          int mt2, nt2, kc0, kc1;
+          sc.decode(u + npairs, mt2, nt2, kc0, kc1);
+          if (nt2 == 0) {  // one pair per M block (the others read it from L2)
+            const int pm0 = mt2 * 256 + (int)rank * 128;
+            for (int kb = kc0; kb < kc1; ++kb) {
+              tma_prefetch_2d(&tmA, pm0, kb * BK);
+              tma_prefetch_2d(&tmA, pm0 + 64, kb * BK);
+            }
+          }
+        }
+#endif
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty(stage), phase ^ 1);
           const uint32_t a_s = sbase + stage * C::STAGE;
           const uint32_t b_s = a_s + C::A_BYTES;
-          if (leader) mbar_expect_tx(full(stage), 2 * C::STAGE);
-          if (!A_MN) {
+          if (XF) {
+            // A on this CTA's own barrier (the epilogue warps transform it);
+            // the stage's previous dS store must have read the tile
+            if (!(DL_XF_DIAG & 32)) mbar_wait(stored(stage), phase ^ 1);
+            if (leader) mbar_expect_tx(full(stage), 2 * C::B_BYTES);
+            mbar_expect_tx(afull(stage), C::A_BYTES);
+            tma_load_2d(a_s, &tmA, afull(stage), kb * BK, m0);
+          } else if (leader) {
+            mbar_expect_tx(full(stage), 2 * C::STAGE);
+          }
+          if (XF) {
+          } else if (!A_MN) {
             tma_load_2d_pair(a_s, &tmA, full(stage), kb * BK, m0);
           } else {
             tma_load_2d_pair(a_s, &tmA, full(stage), m0, kb * BK);
@@ -571,6 +666,7 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t d = tmem_base + acc * 256;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full(stage), phase);
+          if (XF && !(DL_XF_DIAG & 4)) mbar_wait_cluster(xready(stage), phase);
           fence_after();
           const uint32_t a_s = sbase + stage * C::STAGE;
           const uint32_t b_s = a_s + C::A_BYTES;
@@ -603,10 +699,95 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                   ? g.trace + 3 * 64 * 4 + (blockIdx.x * 8 + (warp - 2)) * 32
                                   : nullptr;
     int it = 0;
+    // xf: ring position of the transform (advances like the MMA's) and the
+    // stage whose dS store has not been retired yet (thread 64 owns stores)
+    int xs = 0;
+    uint32_t xph = 0;
+    int pend = -1;
     for (int u = pair; u < total; u += npairs, ++it) {
       int mt, nt, kb0, kb1;
       sc.decode(u, mt, nt, kb0, kb1);
       const int split = u % sc.k_splits;
+      if constexpr (XF) {
+        // epilogue warp w' (0..7) rewrites rows [16 w', 16 w' + 16) of the
+        // CTA's 128-row A tile: lane owns physical 16-byte chunk lane % 8 of
+        // rows 16 w' + lane / 8 + 4 j (j = 0..3); the logical 8-column group
+        // of a chunk is its physical index XOR row % 8 (SWIZZLE_128B)
+        const int wq = warp - 2;
+        const int pc = lane & 7;
+        const int m0 = mt * 256 + (int)rank * 128;
+        float xnl[4], xsc[4];
+        int xy[4], xc[4], xr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 16 * wq + (lane >> 3) + 4 * j;
+          const int m = m0 + r;
+          const bool ok = m < g.M;
+          xr[j] = r;
+          xnl[j] = ok ? g.xf_lse[m] : 0.f;
+          xsc[j] = ok ? g.xf_sc[m] : 0.f;
+          xy[j] = ok ? (int)g.xf_tgt[m] : -1;
+          xc[j] = pc ^ (r & 7);
+        }
+        const bool writer = nt == 0 && g.xf_out != nullptr && !(DL_XF_DIAG & 16);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(afull(xs), xph);
+          const uint32_t a_s = sbase + xs * C::STAGE;
+#pragma unroll
+          for (int j = 0; j < ((DL_XF_DIAG & 8) ? 0 : 4); ++j) {
+            const uint32_t addr = a_s + xr[j] * 128 + pc * 16;
+            uint32_t q[4];
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+                         : "r"(addr));
+            const int dt = xy[j] - (kb * BK + xc[j] * 8);
+            if (DL_XF_DIAG & 1) {
+            } else if (static_cast<unsigned>(dt) >= 8u) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float lo = __uint_as_float(q[e] << 16);
+                const float hi = __uint_as_float(q[e] & 0xFFFF0000u);
+                const __nv_bfloat162 p = __floats2bfloat162_rn(ds_of_logit(lo, xnl[j], xsc[j]),
+                                                               ds_of_logit(hi, xnl[j], xsc[j]));
+                q[e] = *reinterpret_cast<const uint32_t*>(&p);
+              }
+            } else {
+              // the chunk holds the target column: dS[y] -= scale
+              // (backprop.hpp:184-185), subtracted before the bf16 rounding
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float lo = __uint_as_float(q[e] << 16);
+                const float hi = __uint_as_float(q[e] & 0xFFFF0000u);
+                const float a0 = ds_of_logit(lo, xnl[j], xsc[j]) - (2 * e == dt ? xsc[j] : 0.f);
+                const float a1 =
+                    ds_of_logit(hi, xnl[j], xsc[j]) - (2 * e + 1 == dt ? xsc[j] : 0.f);
+                const __nv_bfloat162 p = __floats2bfloat162_rn(a0, a1);
+                q[e] = *reinterpret_cast<const uint32_t*>(&p);
+              }
+            }
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(q[0]),
+                         "r"(q[1]), "r"(q[2]), "r"(q[3])
+                         : "memory");
+          }
+          if (!(DL_XF_DIAG & 2)) fence_async_smem();  // generic writes -> async proxy
+          __syncwarp();
+          if (lane == 0) {
+            if (DL_XF_DIAG & 4) mbar_arrive(xready(xs));
+            else mbar_arrive_rank0(xready(xs));
+            // N tile 0: store this warp's 16 rewritten rows (dS for dW_out),
+            // then retire the previous stage's store -- its tile is read --
+            // so the producer may refill that stage
+            if (writer) tma_store_2d(&tmD, a_s + 16 * wq * 128, kb * BK, m0 + 16 * wq);
+            if (pend >= 0) {
+              if (writer) bulk_wait_read<1>();
+              else bulk_wait_read<0>();
+              mbar_arrive(stored(pend));
+            }
+            pend = xs;
+          }
+          if (++xs == C::STAGES) { xs = 0; xph ^= 1; }
+        }
+      }
       mbar_wait(tfull(acc), acc_phase);
       fence_after();
       // (slots 0..2: warp 2 of pairs 0, 1, 35; with DL_GEMM_TRACE_WARPS the
@@ -631,6 +812,11 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
+    if (XF && lane == 0) {
+      bulk_wait_read<0>();
+      if (pend >= 0) mbar_arrive(stored(pend));
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dS stores complete
+    }
   }
   fence_before();
   __syncthreads();
@@ -849,7 +1035,7 @@ void launch(const GemmDesc& g, cudaStream_t st) {
 template <bool A_MN, bool B_MN, bool RMS>
 int max_pairs() {
   static const int n = [] {
-    auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS>;
+    auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS, false>;
     DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg2<RMS>::SMEM));
     cudaLaunchConfig_t cfg = {};
@@ -863,10 +1049,10 @@ int max_pairs() {
   return n;
 }
 
-template <bool A_MN, bool B_MN, bool RMS>
+template <bool A_MN, bool B_MN, bool RMS, bool XF = false>
 void launch2(const GemmDesc& g, cudaStream_t st) {
   using C = Cfg2<RMS>;
-  auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS>;
+  auto kern = tc_gemm2_kernel<A_MN, B_MN, RMS, XF>;
   static std::once_flag once;
   std::call_once(once, [&] {
     DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -895,7 +1081,9 @@ void launch2(const GemmDesc& g, cudaStream_t st) {
     DL_REQUIRE(pairs > 0 && (kNumSMs / 2 / sc.n_tiles) * sc.n_tiles <= (max_pairs<A_MN, B_MN, true>()),
                1, "fused rmsprop epilogue: not enough co-resident CTA pairs");
   }
-  kern<<<2 * pairs, kThreads, C::SMEM, st>>>(ta, tb, g, sc);
+  // xf: the dS store map has the A map's geometry over xf_out
+  const CUtensorMap td = XF && g.xf_out ? make_map(g.xf_out, g.M, g.K, g.lda, 16) : ta;
+  kern<<<2 * pairs, kThreads, C::SMEM, st>>>(ta, tb, td, g, sc);
   DL_CUDA(cudaGetLastError());
 }
 
@@ -928,6 +1116,11 @@ bool tc_rms_fusable(int M, int N) {
   return pairs > 0 && pairs <= tc::max_pairs<true, true, true>();
 }
 
+bool tc_pair_tiles(int M, int N) {
+  const char* e = std::getenv("DL_GEMM_2CTA");
+  return !(e && std::atoi(e) == 0) && N >= 256 && M >= 256;
+}
+
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
   const int bn = g.N >= 256 ? 256 : (g.N >= 128 ? 128 : 64);
   const bool am = g.a_major == MN_MAJOR, bm = g.b_major == MN_MAJOR;
@@ -936,7 +1129,10 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     return !(e && std::atoi(e) == 0);
   }();
   if (pair_ok && !g.no_pair && bn == 256 && g.M >= 256) {
-    if (g.rms) {
+    if (g.xf) {
+      DL_REQUIRE(!am && bm && !g.rms, 1, "xf: dS.W_out operands (A K-major, B MN-major)");
+      tc::launch2<false, true, false, true>(g, st);
+    } else if (g.rms) {
       DL_REQUIRE(am && bm, 1, "fused rmsprop epilogue: dW_out operands are MN-major");
       tc::launch2<true, true, true>(g, st);
     } else if (!am && !bm) tc::launch2<false, false, false>(g, st);
@@ -945,6 +1141,7 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     else tc::launch2<true, true, false>(g, st);
     return (g.N + 255) / 256;
   }
+  DL_REQUIRE(!g.xf, 1, "xf: needs CTA-pair tiles (tc_pair_tiles)");
 #define DL_TC_CASE(BN_)                                            \
   if (bn == BN_) {                                                 \
     if (!am && !bm) tc::launch<BN_, false, false>(g, st);          \

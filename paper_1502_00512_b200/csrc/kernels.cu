@@ -244,7 +244,7 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
   if (grads) {
     const uint32_t y = tgt[r];
     const float lsef = (float)lse, scf = (float)scale;
-    const float kLog2e = 1.4426950408889634f;
+
     if ((V % 8) == 0) {
       // four 16-byte loads in flight per thread before any store (the row
       // streams at HBM speed only with enough bytes outstanding)
@@ -267,8 +267,8 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
           for (int k = 0; k < 4; ++k) {
             float2 f = __bfloat1622float2(h2[k]);
             const int64_t w0 = q * 8 + 2 * k;
-            f.x = scf * exp2f((f.x - lsef) * kLog2e) - (w0 == y ? scf : 0.f);
-            f.y = scf * exp2f((f.y - lsef) * kLog2e) - (w0 + 1 == y ? scf : 0.f);
+            f.x = ds_of_logit(f.x, lsef, scf) - (w0 == y ? scf : 0.f);
+            f.y = ds_of_logit(f.y, lsef, scf) - (w0 + 1 == y ? scf : 0.f);
             h2[k] = __float22bfloat162_rn(f);
           }
           s8[q] = u[j];
@@ -277,9 +277,57 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
     } else {
       for (int64_t w = threadIdx.x; w < V; w += blockDim.x) {
         const float f = __bfloat162float(s[w]);
-        s[w] = __float2bfloat16_rn(scf * exp2f((f - lsef) * kLog2e) - (w == y ? scf : 0.f));
+        s[w] = __float2bfloat16_rn(ds_of_logit(f, lsef, scf) - (w == y ? scf : 0.f));
       }
     }
+  }
+}
+
+// The row half of k_softmax_rows_bf16 when dS is formed on the fly in the
+// dh GEMM's operand path (gemm_tc.cu, GemmDesc::xf): per row the
+// log-sum-exp from the logits epilogue's partials (backprop.hpp:168-178),
+// loss / log-prob, and the transform's constants lse (fp32, as the in-place
+// kernel uses it) and the row scale (0 for masked rows).
+__global__ void __launch_bounds__(kRowThreads)
+k_lse_rows_bf16(int64_t M, const float2* __restrict__ part, int n_tiles,
+                const float* __restrict__ tgt_logit, const uint8_t* __restrict__ wts,
+                double scale, double* __restrict__ loss_row, double* __restrict__ logp_row,
+                float* __restrict__ lse_f, float* __restrict__ sc_f,
+                const double* __restrict__ lse_all, int G) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  const bool active = wts == nullptr || wts[r] != 0;
+  if (!active) {
+    if (threadIdx.x == 0) {
+      if (loss_row) loss_row[r] = 0.0;
+      if (logp_row) logp_row[r] = NAN;
+      lse_f[r] = 0.f;
+      sc_f[r] = 0.f;
+    }
+    return;
+  }
+  double lse;
+  if (lse_all) {
+    lse = lse_of_blocks(lse_all, G, M, r);
+  } else {
+    double mx = -INFINITY;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+      mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+    mx = block_max_d<kRowThreads>(mx, red);
+    double z = 0.0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+      const float2 p = part[(int64_t)t * M + r];
+      if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
+    }
+    z = block_sum_d<kRowThreads>(z, red);
+    lse = mx + log(z);
+  }
+  if (threadIdx.x == 0) {
+    const double sy = (double)tgt_logit[r];
+    if (loss_row) loss_row[r] = scale * (lse - sy);
+    if (logp_row) logp_row[r] = sy - lse;
+    lse_f[r] = (float)lse;
+    sc_f[r] = (float)scale;
   }
 }
 
@@ -739,6 +787,78 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
   }
 }
 
+// The same from the bf16 gradient for H = 256*NV, one warp per row: the
+// row's step first (from the GEMM's partial sums of squares), then the row
+// streams with 4 gradient and 8 master vectors per lane in flight (6 KB per
+// warp), so one small block per SM (128 threads, <= 96
+// registers: what the persistent recurrence's 208-register CTA leaves free)
+// streams at HBM speed while sharing the SM with the latency-bound kernels
+// it overlaps.
+template <int NV>
+__global__ void __launch_bounds__(128, 5)
+k_rms_dense_g16r(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
+                 const bf16* __restrict__ g, const double* __restrict__ rowsq, int nsub,
+                 int64_t V, double rho, double eps, double eta) {
+  constexpr int64_t H = 256 * NV;
+  const int lane = threadIdx.x % 32;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp0; r < V; r += nwarps) {
+    const uint4* g8 = reinterpret_cast<const uint4*>(g + r * H);
+    float4* w4 = reinterpret_cast<float4*>(w + r * H);
+    uint4* b8 = reinterpret_cast<uint4*>(wb + r * H);
+    // the row's step needs only the partial sums of squares: known before
+    // the row streams (fixed order: lanes' partials, then the warp tree)
+    double s = 0.0;
+    for (int k = lane; k < nsub; k += 32) s += rowsq[(int64_t)k * V + r];
+    s = warp_sum_d(s);
+    const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
+    const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
+    constexpr int U = NV < 4 ? NV : 4;  // 16-byte gradient vectors per lane in flight
+#pragma unroll
+    for (int k0 = 0; k0 < NV; k0 += U) {
+      uint4 q[U];
+      float4 o[2 * U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int j = lane + 32 * (k0 + k);
+        q[k] = __ldcs(g8 + j);
+        o[2 * k] = w4[2 * j];
+        o[2 * k + 1] = w4[2 * j + 1];
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int j = lane + 32 * (k0 + k);
+        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q[k]);
+        const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
+        const float2 c = __bfloat1622float2(q2[2]), d = __bfloat1622float2(q2[3]);
+        float4& o0 = o[2 * k];
+        float4& o1 = o[2 * k + 1];
+        o0.x -= rms_step(eta, a.x, denom, inv);
+        o0.y -= rms_step(eta, a.y, denom, inv);
+        o0.z -= rms_step(eta, b.x, denom, inv);
+        o0.w -= rms_step(eta, b.y, denom, inv);
+        o1.x -= rms_step(eta, c.x, denom, inv);
+        o1.y -= rms_step(eta, c.y, denom, inv);
+        o1.z -= rms_step(eta, d.x, denom, inv);
+        o1.w -= rms_step(eta, d.y, denom, inv);
+        w4[2 * j] = o0;
+        w4[2 * j + 1] = o1;
+        uint4 ob;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(o0.x, o0.y), p1 = __floats2bfloat162_rn(o0.z, o0.w);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(o1.x, o1.y), p3 = __floats2bfloat162_rn(o1.z, o1.w);
+        ob.x = *reinterpret_cast<uint32_t*>(&p0);
+        ob.y = *reinterpret_cast<uint32_t*>(&p1);
+        ob.z = *reinterpret_cast<uint32_t*>(&p2);
+        ob.w = *reinterpret_cast<uint32_t*>(&p3);
+        b8[j] = ob;
+      }
+    }
+    if (lane == 0) m[r] = mw;
+  }
+}
+
 // Dense W_out rmsprop (rmsprop.hpp:94-107) from the bf16 gradient the dW_out
 // GEMM epilogue wrote, with mean_sq assembled from its per-(half tile, row)
 // partial sums of squares (fixed order): one pass over the row, 12 B/elem
@@ -976,6 +1096,14 @@ void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_
                                                            wts, scale, grads, loss_row, logp_row,
                                                            lse_all, G);
 }
+void lse_rows_bf16(int64_t M, const float2* part, int n_tiles, const float* tgt_logit,
+                   const uint8_t* wts, double scale, double* loss_row, double* logp_row,
+                   float* lse_f, float* sc_f, cudaStream_t st, const double* lse_all, int G) {
+  if (M <= 0) return;
+  k_lse_rows_bf16<<<(unsigned)M, kRowThreads, 0, st>>>(M, part, n_tiles, tgt_logit, wts, scale,
+                                                       loss_row, logp_row, lse_f, sc_f, lse_all,
+                                                       G);
+}
 void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
                    cudaStream_t st) {
   if (M <= 0) return;
@@ -1082,6 +1210,20 @@ void rms_dense_g16c(float* w, bf16* wb, float* m, const bf16* g, int64_t V, int6
 }
 void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
                    int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st) {
+  static const int per_sm = [] {
+    const char* e = std::getenv("DL_RMS_G16_BLOCKS");  // blocks per SM (tuning)
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  const int rblocks = (int)std::min<int64_t>((V + 3) / 4, 148 * per_sm);
+#define DL_G16R(NV_)                                                                        \
+  if (H == 256 * (NV_)) {                                                                   \
+    k_rms_dense_g16r<NV_><<<rblocks, 128, 0, st>>>(w, wb, m, g, rowsq, nsub, V, rho, eps, eta); \
+    return;                                                                                 \
+  }
+  DL_G16R(4)
+  DL_G16R(8)
+  DL_G16R(16)
+#undef DL_G16R
   const int blocks = (int)std::min<int64_t>((V * 32 + 255) / 256, 148 * 8);
   k_rms_dense_g16<<<blocks, 256, 0, st>>>(w, wb, m, g, rowsq, nsub, V, H, rho, eps, eta);
 }

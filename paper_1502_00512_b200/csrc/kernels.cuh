@@ -66,6 +66,12 @@ void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const
                       double scale, int grads, double* loss_row, double* logp_row,
                       cudaStream_t st, const double* lse_all = nullptr, int G = 0,
                       const float* tgt_logit = nullptr);
+// per-row lse / loss / log-prob and the dS transform's (lse, scale) for the
+// dh GEMM's on-the-fly softmax (GemmDesc::xf)
+void lse_rows_bf16(int64_t M, const float2* part, int n_tiles, const float* tgt_logit,
+                   const uint8_t* wts, double scale, double* loss_row, double* logp_row,
+                   float* lse_f, float* sc_f, cudaStream_t st, const double* lse_all = nullptr,
+                   int G = 1);
 void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_tiles,
                        const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts,
                        double scale, int grads, double* loss_row, double* logp_row,

@@ -95,6 +95,17 @@ struct dl_ctx {
   uint32_t *x_d = nullptr, *y_d = nullptr;
   uint8_t* w_d = nullptr;
   void* S = nullptr;  // logits / dS: fp32 or bf16 [TB x V]
+  // bf16 mode: dS formed on the fly in the dh GEMM's operand path
+  // (GemmDesc::xf) -- the dh GEMM stores it here for dW_out; the softmax
+  // rows kernel then only computes lse / loss and the transform constants
+  bf16* dS = nullptr;
+  float *xf_lse = nullptr, *xf_sc = nullptr;
+  const uint32_t* xf_tgt = nullptr;  // the target columns of this window's output rows
+  // DL_XF=1 turns it on: bit-identical to the in-place softmax kernel but
+  // slower at C3 (dh 1.27 vs 0.34 ms: the SFU-bound transform sits on the
+  // MMA's critical path, plus a cross-CTA handshake per k-block)
+  bool xf = false;
+  bool xf_on = false;                // this window's dS is formed in the dh GEMM
   float2* part = nullptr;
   int part_tiles = 0;
   float* tgt_logit = nullptr;
@@ -327,6 +338,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->g_in_rows); fr(c->g_in_words); fr(c->ews.seg_start); fr(c->ews.order_pos); fr(c->h0_d);
   fr(c->x_all); fr(c->dpre_all);
   fr(c->hs_all_bf); fr(c->hs_all); fr(c->y_all); fr(c->w_all); fr(c->dh_all);
+  fr(c->dS); fr(c->xf_lse); fr(c->xf_sc);
   c->capT = nT;
   c->capB = nB;
   const int64_t G = dp_ranks(c);  // W_in gradient rows cover the gathered window
@@ -362,6 +374,11 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
     c->htape_bf = dalloc<bf16>((nT + 1) * nB * H);
     c->dpre_bf = dalloc<bf16>(TB * H);
     c->S = dalloc<bf16>(MO * Vo);
+    if (c->xf && tc_pair_tiles((int)MO, (int)c->H)) {
+      c->dS = dalloc<bf16>(MO * Vo);
+      c->xf_lse = dalloc<float>(MO);
+      c->xf_sc = dalloc<float>(MO);
+    }
     c->part_tiles = tc_n_tiles((int)Vo);
     c->part = dalloc<float2>((size_t)c->part_tiles * MO);
     c->tgt_logit = dalloc<float>(MO);
@@ -503,11 +520,21 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
       c->comm->allreduce_sum(c->tgt_logit, (size_t)M, DType::F32, c->st);
     }
     Phase p(c, "softmax");
-    softmax_rows_bf16(grads ? static_cast<bf16*>(c->S) : nullptr, M, V, c->part, c->part_tiles,
-                      c->tgt_logit, tgt, wts, scale, grads ? 1 : 0, loss_row, logp_row, c->st,
-                      vs ? c->lse_all : nullptr, c->nranks);
+    // dS on the fly in the dh GEMM (pair tiles over the whole output-row
+    // block): only the rows' lse / loss here
+    c->xf_on = grads && c->dS != nullptr && tc_pair_tiles((int)M, (int)H);
+    if (c->xf_on) {
+      c->xf_tgt = tgt;
+      lse_rows_bf16(M, c->part, c->part_tiles, c->tgt_logit, wts, scale, loss_row, logp_row,
+                    c->xf_lse, c->xf_sc, c->st, vs ? c->lse_all : nullptr, c->nranks);
+    } else {
+      softmax_rows_bf16(grads ? static_cast<bf16*>(c->S) : nullptr, M, V, c->part,
+                        c->part_tiles, c->tgt_logit, tgt, wts, scale, grads ? 1 : 0, loss_row,
+                        logp_row, c->st, vs ? c->lse_all : nullptr, c->nranks);
+    }
     c->launches++;
   } else {
+    c->xf_on = false;
     GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs, H, K_MAJOR, c->w_out, H,
                       static_cast<float*>(c->S), V);
     {
@@ -751,8 +778,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     Phase p(c, "dw_out");
     if (fused) {
       // + the dense rmsprop of every row (rmsprop.hpp:94-107) in the epilogue
-      GemmDesc g = desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
-                        nullptr, H);
+      GemmDesc g = desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->xf_on ? c->dS : c->S, Vo,
+                        MN_MAJOR, Hs_bf, H, nullptr, H);
       g.raster = 1;
       g.clip = clip;
       g.rowsq = c->rowsq;
@@ -829,8 +856,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       }
       return;
     }
-    GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs_bf, H,
-                              c->g_out, H)
+    GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->xf_on ? c->dS : c->S, Vo,
+                              MN_MAJOR, Hs_bf, H, c->g_out, H)
                        : desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
                               c->g_out, H);
     g.raster = 1;
@@ -862,23 +889,24 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
            c->dh_out, st);
     c->launches++;
   }
-  if (!fused && !late && !nce) dw_out();
-  if (dp) {
-    // data parallel: sum dW_out over ranks, then clip --
-    // on the communication stream, overlapping dh and the backward
-    // recurrence; joined before the update
-    DL_CUDA(cudaEventRecord(c->ev_fork, st));
-    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-    if (c->dp16) {
-      // bf16 on the wire: half the NVLink bytes of the fp32 gradient; clip
-      // and the update follow in rms_dense_g16c
-      c->comm->allreduce_sum(c->g_out_bf, (size_t)(V * H), DType::BF16, c->st2);
-    } else {
-      c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
-      reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
-      c->launches++;
+  auto reduce_dw = [&] {
+    if (dp) {
+      // data parallel: sum dW_out over ranks, then clip --
+      // on the communication stream, overlapping dh and the backward
+      // recurrence; joined before the update
+      DL_CUDA(cudaEventRecord(c->ev_fork, st));
+      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+      if (c->dp16) {
+        // bf16 on the wire: half the NVLink bytes of the fp32 gradient; clip
+        // and the update follow in rms_dense_g16c
+        c->comm->allreduce_sum(c->g_out_bf, (size_t)(V * H), DType::BF16, c->st2);
+      } else {
+        c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
+        reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
+        c->launches++;
+      }
     }
-  }
+  };
   // With a finite clip bound every clipped component is finite (clip1 maps
   // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
   // cannot fail and the dense W_out update -- HBM-bound -- may start as soon
@@ -908,7 +936,16 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     }
     DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
   };
-  if (fork_out_eta > 0.0) fork_update(fork_out_eta, c->w_out_bf_next);
+  // (dW_out reads the dS the dh GEMM stores when it is formed there)
+  const bool dw_after_dh = fused || late || c->xf_on;
+  auto after_dw = [&] {
+    reduce_dw();
+    if (fork_out_eta > 0.0) fork_update(fork_out_eta, c->w_out_bf_next);
+  };
+  if (!dw_after_dh && !nce) {
+    dw_out();
+    after_dw();
+  }
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
   auto dh = [&] {
     Phase p(c, "dh");
@@ -919,6 +956,15 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                        : desc((int)MO, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out, H,
                               dst, H);
     g.raster = 0;
+    if (c->xf_on) {
+      // the A tiles are logits: dS = scale (p - 1[y]) is formed in shared
+      // memory (backprop.hpp:179-186) and stored to c->dS for dW_out
+      g.xf = 1;
+      g.xf_lse = c->xf_lse;
+      g.xf_sc = c->xf_sc;
+      g.xf_tgt = c->xf_tgt;
+      g.xf_out = c->dS;
+    }
     if (s > 1) {
       ensure_splitws(c, (size_t)s * MO * H);
       g.C = c->splitws;
@@ -932,7 +978,10 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     }
   };
   if (!nce) dh();
-  if (fused || late) dw_out();
+  if (dw_after_dh && !nce) {
+    dw_out();
+    after_dw();
+  }
   if (late) fork_update(late_eta, c->w_out_bf);
   if (vs) {
     // each rank contracted its vocabulary block: dh_out = sum over ranks.
@@ -1145,6 +1194,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_G16")) c->g16 = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_FUSE_OUT")) c->fuse_out = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_FORK_LATE")) c->fork_late = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_XF")) c->xf = std::atoi(e) != 0;
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
@@ -1220,7 +1270,8 @@ int dl_destroy(dl_ctx* c) {
                   c->sort_keys_out, c->sort_vals_out, c->sort_head, c->sort_slot, c->sort_temp,
                   c->nce_ws.seg_start, c->nce_ws.order_pos, c->g_out_words, c->g_out_n,
                   c->nz_prob_d, c->nz_alias_d, c->raw_d, c->pos_of_d, c->first_d,
-                  c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt};
+                  c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt, c->dS, c->xf_lse,
+                  c->xf_sc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -2037,7 +2088,8 @@ int dl_comm_init(dl_ctx* c, const uint8_t id[128], int nranks, int rank) {
     drop_graphs(c);
     delete c->comm;
     c->comm = nullptr;
-    if (nranks == 1) return;
+    // (a one-rank communicator is real too: it runs the multi-rank code
+    // paths -- collectives, gathered windows, sharded output -- on one GPU)
     c->comm = new NcclComm(id, nranks, rank);
   });
 }
@@ -2124,8 +2176,8 @@ int dl_rng_seed_state(uint64_t seed, uint64_t state[313]) {
 int dl_set_vocab_shard(dl_ctx* c, int on) {
   if (!c) return fail(c, DL_EINVAL, "dl_set_vocab_shard: null ctx");
   if (on) {
-    if (!c->comm || c->nranks < 2)
-      return fail(c, DL_EINVAL, "dl_set_vocab_shard: needs a communicator of >= 2 ranks");
+    if (!c->comm)
+      return fail(c, DL_EINVAL, "dl_set_vocab_shard: needs a communicator (dl_comm_init)");
     if (c->V % c->nranks != 0)
       return fail(c, DL_EINVAL, "dl_set_vocab_shard: V must be a multiple of the rank count");
     if (c->precision == DL_BF16 && ((c->V / c->nranks) % 8) != 0)

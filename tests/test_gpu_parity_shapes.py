@@ -112,7 +112,7 @@ def test_bf16_fused_window_update_at_c3(orc):
     with the dense W_out rmsprop fused into its epilogue (72 CTA pairs, eight
     N-tiles per 256-row block exchanging per-row sums of squares)."""
     import paper_1502_00512_b200 as dl
-    V, H, T, B = 64000, 2048, 4, 16
+    V, H, T, B = 64000, 2048, 4, 64  # TB = 256: the dh / logits GEMMs on pair tiles
     rng = np.random.default_rng(3)
     params = make_params(V, H, 33)
     x, y, w = make_window(rng, T, B, V)
@@ -172,6 +172,36 @@ def test_bf16_fused_window_update_at_c3(orc):
     for name, got, ref_ in (("dW_out", g_out, want["g_out"]), ("dW_rec", g_rec, want["g_rec"]),
                             ("dW_in", g_in, want["g_in_dense"])):
         assert rel_l2(got, ref_) < 2e-2, (name, rel_l2(got, ref_))
+
+
+def test_bf16_ds_in_dh_gemm_equals_softmax_kernel():
+    """dS formed on the fly in the dh GEMM's operand path (GemmDesc::xf, the
+    logits never rewritten in HBM) is bit-identical to the in-place softmax
+    rows kernel (DL_XF=0): same loss, h_final, updated parameters and
+    accumulators after a training window at the C3 shape (TB = 512)."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 64000, 2048, 4, 128
+    rng = np.random.default_rng(8)
+    params = make_params(V, H, 81)
+    x, y, w = make_window(rng, T, B, V, mask_p=0.15)
+    h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
+    out = []
+    for xf in ("0", "1"):
+        os.environ["DL_XF"] = xf
+        try:
+            m = dl.GpuRnn(V, H, 0, "bf16")
+        finally:
+            del os.environ["DL_XF"]
+        m.set_params(*params)
+        m.set_opt(None, None, None, RHO, EPS)
+        r, hf, ok = dl.train_window(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0, 0.01)
+        assert ok
+        out.append((r.loss, r.positions, hf, m.params(), m.opt()))
+        m.close()
+    (l0, p0, h0_, pa, oa), (l1, p1, h1_, pb, ob) = out
+    assert l0 == l1 and p0 == p1 and np.array_equal(h0_, h1_)
+    for a, b in zip(pa + oa, pb + ob):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("act", [0, 1])
