@@ -652,7 +652,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "tf32x3"])
     ap.add_argument("--loss", default="softmax", choices=["softmax", "nce"],
                     help="output layer: exact softmax (the north-star path) or NCE "
                          "(LossMode::kNce, the reference's default training mode)")

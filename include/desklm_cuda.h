@@ -33,8 +33,12 @@ enum { DL_OK = 0, DL_EINVAL = 1, DL_EDATA = 2, DL_EDEVICE = 3 };
 
 /* Arithmetic of the GEMMs.  DL_FP32: fp32 SIMT kernels (parity mode,
  * reference tolerance 1e-4).  DL_BF16: tcgen05/TMEM tensor-core kernels with
- * bf16 operands, fp32 accumulation, fp32 master weights (throughput mode). */
-enum { DL_FP32 = 0, DL_BF16 = 1 };
+ * bf16 operands, fp32 accumulation, fp32 master weights (throughput mode).
+ * DL_TF32X3: the fp32 mode with its GEMMs on the tensor cores as 3xTF32
+ * (tcgen05 kind::tf32: hi.hi + hi.lo + lo.hi of the split fp32 operands,
+ * fp32 accumulation in K chunks summed round-to-nearest) -- fp32-class
+ * numbers at 5-10x the SIMT speed; everything else as DL_FP32. */
+enum { DL_FP32 = 0, DL_BF16 = 1, DL_TF32X3 = 2 };
 
 /* Activation (rnn.hpp:35: enum class Activation { kSigmoid, kTanh }). */
 enum { DL_SIGMOID = 0, DL_TANH = 1 };

@@ -38,7 +38,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import formats
-from ._lib import DL_BF16, DL_FP32, DataError, DeviceError, check, load
+from ._lib import DL_BF16, DL_FP32, DL_TF32X3, DataError, DeviceError, check, load
 
 __all__ = [
     "GpuRnn", "WindowBatch", "BpttResult", "PerplexityResult", "bptt_run",
@@ -51,7 +51,7 @@ __all__ = [
 
 KSIGMOID, KTANH = 0, 1
 UNK_ID, BOS_ID, EOS_ID = 0, 1, 2
-_PREC = {"fp32": DL_FP32, "bf16": DL_BF16}
+_PREC = {"fp32": DL_FP32, "bf16": DL_BF16, "tf32x3": DL_TF32X3}
 
 
 def _p(a):
@@ -73,7 +73,8 @@ def make_vocab(v: int) -> List[str]:
 class GpuRnn:
     """Device-resident bias-free Elman RNNLM (V x H W_in, H x H W_rec, V x H
     word-major W_out) with its rmsprop state.  precision: "fp32" (parity
-    mode, SIMT fp32 GEMMs) or "bf16" (tcgen05 tensor cores)."""
+    mode, SIMT fp32 GEMMs), "tf32x3" (the fp32 mode with 3xTF32 tensor-core
+    GEMMs) or "bf16" (tcgen05 tensor cores, bf16 operands)."""
 
     def __init__(self, V: int, H: int, act: int = KSIGMOID, precision: str = "fp32",
                  device: int = 0):

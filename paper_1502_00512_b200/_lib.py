@@ -33,7 +33,7 @@ EXPORTS = (
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
-DL_FP32, DL_BF16 = 0, 1
+DL_FP32, DL_BF16, DL_TF32X3 = 0, 1, 2
 
 _lib = None
 

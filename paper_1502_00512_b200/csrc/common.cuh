@@ -146,6 +146,12 @@ struct GemmDesc {
 // and the fused rmsprop epilogue exist only there)
 bool tc_pair_tiles(int M, int N);
 
+// 3xTF32 tensor-core GEMM for the fp32 parity mode (gemm_tc.cu): same
+// GemmDesc contract as gemm_f32 (fp32 operands and output, clip / split-K)
+bool tf32x3_ok(const GemmDesc& g);
+int tf32_splits(int K, int desired);
+int gemm_tf32x3(const GemmDesc& g, cudaStream_t st);
+
 // gemm_simt.cu
 void gemm_f32(const GemmDesc& g, cudaStream_t st);
 // gemm_tc.cu  (returns the number of N-tiles used for logits partials)

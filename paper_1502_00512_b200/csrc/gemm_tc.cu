@@ -974,6 +974,270 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
       }
 }
 
+// --------------------------------------------------------------------------
+// 3xTF32: the fp32 parity mode's GEMMs on the tensor cores (tcgen05
+// kind::tf32, fp32 accumulation in TMEM).  fp32 operands arrive by TMA
+// (SWIZZLE_128B, 32 elements per 128-byte row, BK = 32); four converter warps
+// split every stage in shared memory into hi = tf32(x) (in place, exact
+// round-to-nearest) and lo = x - hi, and the MMA warp issues
+// hi.hi + hi.lo + lo.hi -- about 21 significant bits per product, fp32
+// accumulation like the SIMT kernel it replaces (the reference accumulates
+// in double, mat.hpp:59-78; the parity bar is 1e-4).  128 x 128 tiles.
+// Roles: warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (two per TMEM lane
+// quarter), warps 10..13 converters.
+constexpr int kXBK = 32;  // fp32 elements per k-block (one 128-byte swizzle row)
+constexpr int kXBN = 128;
+constexpr int kXConvWarps = 4;
+constexpr int kXChunk = 8;  // k-blocks (K = 256) per fresh TMEM accumulation
+constexpr int kXThreads = 64 + 32 * kEpiWarps + 32 * kXConvWarps;
+struct CfgX {
+  static constexpr int A_BYTES = BM * kXBK * 4;   // 16 KB
+  static constexpr int B_BYTES = kXBN * kXBK * 4;  // 16 KB
+  static constexpr int STAGE = 2 * (A_BYTES + B_BYTES);  // hi (in place) + lo copies
+  static constexpr int STAGES = 3;
+  static constexpr int TMEM_COLS = 2 * kXBN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+static_assert(CfgX::SMEM <= 227 * 1024, "tf32 kernel shared memory");
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kXThreads, 1)
+tc_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 GemmDesc g, Sched sc) {
+  using C = CfgX;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  // full[S], split[S], empty[S], tfull[2], tempty[2]; then the TMEM slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 4);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return smem_u32(&bars[s]); };
+  auto split = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[2 * C::STAGES + s]); };
+  auto tfull = [&](int a) { return smem_u32(&bars[3 * C::STAGES + a]); };
+  auto tempty = [&](int a) { return smem_u32(&bars[3 * C::STAGES + 2 + a]); };
+  // stage layout: A hi | B hi | A lo | B lo
+  auto a_hi = [&](int s) { return sbase + s * C::STAGE; };
+  auto b_hi = [&](int s) { return sbase + s * C::STAGE + C::A_BYTES; };
+  auto a_lo = [&](int s) { return sbase + s * C::STAGE + C::A_BYTES + C::B_BYTES; };
+  auto b_lo = [&](int s) { return sbase + s * C::STAGE + 2 * C::A_BYTES + C::B_BYTES; };
+
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(split(s), kXConvWarps);
+      mbar_init(empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), kEpiWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1);
+          mbar_expect_tx(full(stage), C::A_BYTES + C::B_BYTES);
+          if (!A_MN) {
+            tma_load_2d(a_hi(stage), &tmA, full(stage), kb * kXBK, mt * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              tma_load_2d(a_hi(stage) + j * 4096, &tmA, full(stage), mt * BM + 32 * j, kb * kXBK);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_hi(stage), &tmB, full(stage), kb * kXBK, nt * kXBN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kXBN / 32; ++j)
+              tma_load_2d(b_hi(stage) + j * 4096, &tmB, full(stage), nt * kXBN + 32 * j,
+                          kb * kXBK);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::tf32: D f32 (bits 4-5 = 1), A / B tf32 (bits 7-9 / 10-12 = 2)
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                                 (static_cast<uint32_t>(A_MN) << 15) |
+                                 (static_cast<uint32_t>(B_MN) << 16) |
+                                 (static_cast<uint32_t>(kXBN >> 3) << 17) |
+                                 (static_cast<uint32_t>(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        sc.decode(u, mt, nt, kb0, kb1);
+        // the tile's K range in chunks of kXChunk k-blocks, each accumulated
+        // afresh in alternating TMEM buffers and summed by the epilogue in
+        // registers (round-to-nearest): the tensor core's fp32 accumulation
+        // truncates, and over a long K that bias would reach 1e-4
+        for (int c0 = kb0; c0 < kb1; c0 += kXChunk) {
+          const int c1 = min(kb1, c0 + kXChunk);
+          mbar_wait(tempty(acc), acc_phase ^ 1);
+          fence_after();
+          const uint32_t d = tmem_base + acc * kXBN;
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(split(stage), phase);
+            fence_after();
+            const uint32_t ah = a_hi(stage), bh = b_hi(stage), al = a_lo(stage),
+                           bl = b_lo(stage);
+#pragma unroll
+            for (int ks = 0; ks < kXBK / 8; ++ks) {
+              auto da = [&](uint32_t base) {
+                return A_MN ? make_desc(base + ks * 1024, 4096, 1024)
+                            : make_desc(base + ks * 32, 16, 1024);
+              };
+              auto db = [&](uint32_t base) {
+                return B_MN ? make_desc(base + ks * 1024, 4096, 1024)
+                            : make_desc(base + ks * 32, 16, 1024);
+              };
+              // small terms first, then hi.hi
+              mma_tf32(d, da(al), db(bh), idesc, (kb > c0 || ks > 0) ? 1u : 0u);
+              mma_tf32(d, da(ah), db(bl), idesc, 1u);
+              mma_tf32(d, da(ah), db(bh), idesc, 1u);
+            }
+            mma_commit(empty(stage));
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(tfull(acc));
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ---------------- converters: x -> hi = tf32_rna(x) in place, lo = x - hi
+    const int t = threadIdx.x - (64 + 32 * kEpiWarps);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      int mt, nt, kb0, kb1;
+      sc.decode(u, mt, nt, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(full(stage), phase);
+        constexpr int kVec = (C::A_BYTES + C::B_BYTES) / 16;  // 16-byte vectors of A hi | B hi
+#pragma unroll 4
+        for (int i = t; i < kVec; i += 32 * kXConvWarps) {
+          const uint32_t src = a_hi(stage) + i * 16;
+          const uint32_t dst = a_lo(stage) + i * 16;
+          float4 x = ld_shared_v4(src), h, l;
+          uint32_t hb;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x.x)); h.x = __uint_as_float(hb);
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x.y)); h.y = __uint_as_float(hb);
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x.z)); h.z = __uint_as_float(hb);
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x.w)); h.w = __uint_as_float(hb);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          st_shared_v4(src, h);
+          st_shared_v4(dst, l);
+        }
+        fence_async_smem();  // generic writes -> the MMA's async proxy
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split(stage));
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9)
+    const int quarter = warp % 4, half = (warp - 2) / 4;
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    bool bad = false;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      int mt, nt, kb0, kb1;
+      sc.decode(u, mt, nt, kb0, kb1);
+      const int split_i = u % sc.k_splits;
+      // this thread's row, columns [64 half, 64 half + 64): the chunks'
+      // partial sums added in registers
+      float sum[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) sum[j] = 0.f;
+      for (int c0 = kb0; c0 < kb1; c0 += kXChunk) {
+        mbar_wait(tfull(acc), acc_phase);
+        fence_after();
+        const uint32_t taddr =
+            tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kXBN + half * 64;
+        uint32_t r0[32], r1[32];
+        tmem_ld32_async(taddr, r0);
+        tmem_ld32_async(taddr + 32, r1);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty(acc));
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sum[j] += __uint_as_float(r0[j]);
+          sum[32 + j] += __uint_as_float(r1[j]);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      // fp32 store (+ clip / finite flag, split-K slice) as epilogue_row
+      const int m = mt * BM + row;
+      const bool mvalid = m < g.M;
+      const int n0 = nt * kXBN + half * 64;
+      if (g.do_clip) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          sum[j] = clip1(sum[j], g.clip);
+          bad |= mvalid && (n0 + j < g.N) && !isfinite(sum[j]);
+        }
+      }
+      if (mvalid) {
+        float* Crow = g.C + split_i * g.split_stride + static_cast<int64_t>(m) * g.ldc;
+        if (n0 + 64 <= g.N && (g.ldc % 4) == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            reinterpret_cast<float4*>(Crow + n0)[j] =
+                make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (n0 + j < g.N) Crow[n0 + j] = sum[j];
+        }
+      }
+    }
+    if (g.do_clip && g.nonfinite && bad) atomicExch(g.nonfinite, 1);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------- host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1004,6 +1268,51 @@ CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int64_t ld, i
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DL_REQUIRE(r == CUDA_SUCCESS, 3, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
+}
+
+// fp32 variant for the 3xTF32 kernel: box {32 cols (128 bytes), box_rows}
+CUtensorMap make_map_f32(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  DL_REQUIRE((reinterpret_cast<uintptr_t>(base) % 16) == 0, 1, "tma: base not 16B aligned");
+  DL_REQUIRE((ld * 4) % 16 == 0, 1, "tma: leading dimension must be a multiple of 4 elements");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DL_REQUIRE(r == CUDA_SUCCESS, 3, "cuTensorMapEncodeTiled (fp32) failed: " + std::to_string(r));
+  return m;
+}
+
+template <bool A_MN, bool B_MN>
+void launch_tf32x3(const GemmDesc& g, cudaStream_t st) {
+  using C = CfgX;
+  auto kern = tc_tf32x3_kernel<A_MN, B_MN>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    DL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  });
+  const CUtensorMap ta = A_MN ? make_map_f32(g.A, g.K, g.M, g.lda, kXBK)
+                              : make_map_f32(g.A, g.M, g.K, g.lda, BM);
+  const CUtensorMap tb = B_MN ? make_map_f32(g.B, g.K, g.N, g.ldb, kXBK)
+                              : make_map_f32(g.B, g.N, g.K, g.ldb, kXBN);
+  Sched sc;
+  sc.m_tiles = (g.M + BM - 1) / BM;
+  sc.n_tiles = (g.N + kXBN - 1) / kXBN;
+  sc.kb_total = (g.K + kXBK - 1) / kXBK;
+  sc.k_splits = std::max(1, std::min(g.k_splits, sc.kb_total));
+  sc.kbps = (sc.kb_total + sc.k_splits - 1) / sc.k_splits;
+  sc.k_splits = (sc.kb_total + sc.kbps - 1) / sc.kbps;
+  DL_REQUIRE(sc.k_splits == std::max(1, g.k_splits), 1,
+             "tf32x3 gemm: k_splits not normalised with tf32_splits()");
+  sc.raster = g.raster;
+  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
+  const int grid = std::min(total, kNumSMs);
+  kern<<<grid, kXThreads, C::SMEM, st>>>(ta, tb, g, sc);
+  DL_CUDA(cudaGetLastError());
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -1114,6 +1423,32 @@ bool tc_rms_fusable(int M, int N) {
   const int nt = N / 256;
   const int pairs = (kNumSMs / 2 / nt) * nt;
   return pairs > 0 && pairs <= tc::max_pairs<true, true, true>();
+}
+
+// k-slices the 3xTF32 kernel produces for a requested split count (BK = 32)
+int tf32_splits(int K, int desired) {
+  const int kb_total = (K + tc::kXBK - 1) / tc::kXBK;
+  const int s = std::max(1, std::min(desired, kb_total));
+  const int kbps = (kb_total + s - 1) / s;
+  return (kb_total + kbps - 1) / kbps;
+}
+
+// Whether the 3xTF32 kernel can take this fp32 GEMM (TMA: 16-byte aligned
+// bases and leading dimensions) -- else the SIMT kernel runs.
+bool tf32x3_ok(const GemmDesc& g) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+  return !g.logits && !g.Cb && !g.rms && !g.xf && al(g.A) && al(g.B) && g.lda % 4 == 0 &&
+         g.ldb % 4 == 0;
+}
+
+int gemm_tf32x3(const GemmDesc& g, cudaStream_t st) {
+  DL_REQUIRE(tf32x3_ok(g), 1, "tf32x3: unsupported GEMM (alignment / epilogue)");
+  const bool am = g.a_major == MN_MAJOR, bm = g.b_major == MN_MAJOR;
+  if (!am && !bm) tc::launch_tf32x3<false, false>(g, st);
+  else if (!am && bm) tc::launch_tf32x3<false, true>(g, st);
+  else if (am && !bm) tc::launch_tf32x3<true, false>(g, st);
+  else tc::launch_tf32x3<true, true>(g, st);
+  return (g.N + tc::kXBN - 1) / tc::kXBN;
 }
 
 bool tc_pair_tiles(int M, int N) {

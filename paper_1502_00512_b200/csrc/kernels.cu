@@ -787,78 +787,6 @@ k_rms_dense_rows(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict
   }
 }
 
-// The same from the bf16 gradient for H = 256*NV, one warp per row: the
-// row's step first (from the GEMM's partial sums of squares), then the row
-// streams with 4 gradient and 8 master vectors per lane in flight (6 KB per
-// warp), so one small block per SM (128 threads, <= 96
-// registers: what the persistent recurrence's 208-register CTA leaves free)
-// streams at HBM speed while sharing the SM with the latency-bound kernels
-// it overlaps.
-template <int NV>
-__global__ void __launch_bounds__(128, 5)
-k_rms_dense_g16r(float* __restrict__ w, bf16* __restrict__ wb, float* __restrict__ m,
-                 const bf16* __restrict__ g, const double* __restrict__ rowsq, int nsub,
-                 int64_t V, double rho, double eps, double eta) {
-  constexpr int64_t H = 256 * NV;
-  const int lane = threadIdx.x % 32;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
-  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-  for (int64_t r = warp0; r < V; r += nwarps) {
-    const uint4* g8 = reinterpret_cast<const uint4*>(g + r * H);
-    float4* w4 = reinterpret_cast<float4*>(w + r * H);
-    uint4* b8 = reinterpret_cast<uint4*>(wb + r * H);
-    // the row's step needs only the partial sums of squares: known before
-    // the row streams (fixed order: lanes' partials, then the warp tree)
-    double s = 0.0;
-    for (int k = lane; k < nsub; k += 32) s += rowsq[(int64_t)k * V + r];
-    s = warp_sum_d(s);
-    const float mw = (float)(rho * (double)m[r] + (1.0 - rho) * (s / (double)H));
-    const double denom = sqrt((double)mw + eps);
-    const double inv = 1.0 / denom;
-    constexpr int U = NV < 4 ? NV : 4;  // 16-byte gradient vectors per lane in flight
-#pragma unroll
-    for (int k0 = 0; k0 < NV; k0 += U) {
-      uint4 q[U];
-      float4 o[2 * U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int j = lane + 32 * (k0 + k);
-        q[k] = __ldcs(g8 + j);
-        o[2 * k] = w4[2 * j];
-        o[2 * k + 1] = w4[2 * j + 1];
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int j = lane + 32 * (k0 + k);
-        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q[k]);
-        const float2 a = __bfloat1622float2(q2[0]), b = __bfloat1622float2(q2[1]);
-        const float2 c = __bfloat1622float2(q2[2]), d = __bfloat1622float2(q2[3]);
-        float4& o0 = o[2 * k];
-        float4& o1 = o[2 * k + 1];
-        o0.x -= rms_step(eta, a.x, denom, inv);
-        o0.y -= rms_step(eta, a.y, denom, inv);
-        o0.z -= rms_step(eta, b.x, denom, inv);
-        o0.w -= rms_step(eta, b.y, denom, inv);
-        o1.x -= rms_step(eta, c.x, denom, inv);
-        o1.y -= rms_step(eta, c.y, denom, inv);
-        o1.z -= rms_step(eta, d.x, denom, inv);
-        o1.w -= rms_step(eta, d.y, denom, inv);
-        w4[2 * j] = o0;
-        w4[2 * j + 1] = o1;
-        uint4 ob;
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(o0.x, o0.y), p1 = __floats2bfloat162_rn(o0.z, o0.w);
-        __nv_bfloat162 p2 = __floats2bfloat162_rn(o1.x, o1.y), p3 = __floats2bfloat162_rn(o1.z, o1.w);
-        ob.x = *reinterpret_cast<uint32_t*>(&p0);
-        ob.y = *reinterpret_cast<uint32_t*>(&p1);
-        ob.z = *reinterpret_cast<uint32_t*>(&p2);
-        ob.w = *reinterpret_cast<uint32_t*>(&p3);
-        b8[j] = ob;
-      }
-    }
-    if (lane == 0) m[r] = mw;
-  }
-}
-
 // Dense W_out rmsprop (rmsprop.hpp:94-107) from the bf16 gradient the dW_out
 // GEMM epilogue wrote, with mean_sq assembled from its per-(half tile, row)
 // partial sums of squares (fixed order): one pass over the row, 12 B/elem
@@ -1061,6 +989,31 @@ static inline int grid_for(int64_t n, int tpb = 256, int cap = 148 * 16) {
   return (int)g;
 }
 
+// out[c][r] = in[r][c] for an fp32 rows x cols matrix (32 x 32 tiles through
+// shared memory): the 3xTF32 GEMM's MN-major operands made K-major
+// (kind::tf32 reads K-major tiles only).
+__global__ void k_transpose_f32(const float* __restrict__ in, int64_t rows, int64_t cols,
+                                int64_t ld_in, float* __restrict__ out, int64_t ld_out) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    t[i][threadIdx.x] = (r < rows && c < cols) ? in[r * ld_in + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) out[c * ld_out + r] = t[threadIdx.x][i];
+  }
+}
+
+void transpose_f32(const float* in, int64_t rows, int64_t cols, int64_t ld_in, float* out,
+                   int64_t ld_out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  k_transpose_f32<<<grid, dim3(32, 8), 0, st>>>(in, rows, cols, ld_in, out, ld_out);
+}
+
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st) {
   k_f32_to_bf16<<<grid_for(n), 256, 0, st>>>(x, y, n);
 }
@@ -1210,20 +1163,6 @@ void rms_dense_g16c(float* w, bf16* wb, float* m, const bf16* g, int64_t V, int6
 }
 void rms_dense_g16(float* w, bf16* wb, float* m, const bf16* g, const double* rowsq, int nsub,
                    int64_t V, int64_t H, double rho, double eps, double eta, cudaStream_t st) {
-  static const int per_sm = [] {
-    const char* e = std::getenv("DL_RMS_G16_BLOCKS");  // blocks per SM (tuning)
-    return e ? std::max(1, std::atoi(e)) : 1;
-  }();
-  const int rblocks = (int)std::min<int64_t>((V + 3) / 4, 148 * per_sm);
-#define DL_G16R(NV_)                                                                        \
-  if (H == 256 * (NV_)) {                                                                   \
-    k_rms_dense_g16r<NV_><<<rblocks, 128, 0, st>>>(w, wb, m, g, rowsq, nsub, V, rho, eps, eta); \
-    return;                                                                                 \
-  }
-  DL_G16R(4)
-  DL_G16R(8)
-  DL_G16R(16)
-#undef DL_G16R
   const int blocks = (int)std::min<int64_t>((V * 32 + 255) / 256, 148 * 8);
   k_rms_dense_g16<<<blocks, 256, 0, st>>>(w, wb, m, g, rowsq, nsub, V, H, rho, eps, eta);
 }

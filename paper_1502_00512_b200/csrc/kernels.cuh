@@ -53,6 +53,9 @@ void noise_tables_q(const double* q, int64_t V, int k, std::vector<double>& lnkq
                     std::vector<double>& prob, std::vector<uint32_t>& alias);
 
 void f32_to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st);
+// out [cols x rows] (ld_out) = transpose of in [rows x cols] (ld_in), fp32
+void transpose_f32(const float* in, int64_t rows, int64_t cols, int64_t ld_in, float* out,
+                   int64_t ld_out, cudaStream_t st);
 void fill_f32(float* x, float v, int64_t n, cudaStream_t st);
 void rec_fwd(const float* part, int splits, int64_t split_stride, int64_t Bn, int64_t H,
              const float* w_in, const uint32_t* x, int act, float* h, bf16* hb, cudaStream_t st);

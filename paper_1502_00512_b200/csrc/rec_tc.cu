@@ -470,12 +470,22 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       const int m = row, n = nt * BN + col;
       if (m >= p.M || n >= p.N) continue;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gemm)
-        for (int q = 0; q < p.S; ++q) {
-          const float* peer = cluster.map_shared_rank(part, q);
-          const float4 v = *reinterpret_cast<const float4*>(peer + row * C::PSTRIDE + col);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
+      if (gemm) {
+        // every peer's partial in flight at once (distributed shared memory
+        // round trips dominate), then summed in rank order as before
+        float4 pv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p.S) {
+            const float* peer = cluster.map_shared_rank(part, q);
+            pv[q] = *reinterpret_cast<const float4*>(peer + row * C::PSTRIDE + col);
+          }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p.S) {
+            acc.x += pv[q].x; acc.y += pv[q].y; acc.z += pv[q].z; acc.w += pv[q].w;
+          }
+      }
       const int64_t o = static_cast<int64_t>(m) * p.N + n;
       float4 ea, eb;
       if (k < C::NPRE) {

@@ -105,6 +105,11 @@ struct dl_ctx {
   // slower at C3 (dh 1.27 vs 0.34 ms: the SFU-bound transform sits on the
   // MMA's critical path, plus a cross-CTA handshake per k-block)
   bool xf = false;
+  // DL_TF32X3: the fp32 mode's GEMMs as 3xTF32 on the tensor cores
+  // (gemm_tc.cu) instead of the fp32 FMA kernel (gemm_simt.cu)
+  bool tf32x3 = false;
+  float *xpose_a = nullptr, *xpose_b = nullptr;  // K-major copies of MN-major operands
+  size_t xpose_a_cap = 0, xpose_b_cap = 0;
   bool xf_on = false;                // this window's dS is formed in the dh GEMM
   float2* part = nullptr;
   int part_tiles = 0;
@@ -338,7 +343,8 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->g_in_rows); fr(c->g_in_words); fr(c->ews.seg_start); fr(c->ews.order_pos); fr(c->h0_d);
   fr(c->x_all); fr(c->dpre_all);
   fr(c->hs_all_bf); fr(c->hs_all); fr(c->y_all); fr(c->w_all); fr(c->dh_all);
-  fr(c->dS); fr(c->xf_lse); fr(c->xf_sc);
+  fr(c->dS); fr(c->xf_lse); fr(c->xf_sc); fr(c->xpose_a); fr(c->xpose_b);
+  c->xpose_a_cap = c->xpose_b_cap = 0;
   c->capT = nT;
   c->capB = nB;
   const int64_t G = dp_ranks(c);  // W_in gradient rows cover the gathered window
@@ -384,6 +390,16 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
     c->tgt_logit = dalloc<float>(MO);
   } else {
     c->S = dalloc<float>(MO * Vo);
+    if (c->tf32x3) {
+      // the window's MN-major fp32 operands, made K-major for 3xTF32:
+      // A -- dS^T [Vo x MO] (dW_out), dpre^T [H x TB] (dW_rec);
+      // B -- W_out^T [H x Vo] (dh), Hs^T [H x MO] (dW_out), W_rec^T (recurrence)
+      auto r4 = [](int64_t x) { return (x + 3) / 4 * 4; };
+      c->xpose_a_cap = (size_t)std::max(Vo * r4(MO), H * r4(TB));
+      c->xpose_b_cap = (size_t)std::max({H * r4(Vo), H * r4(MO), H * r4(H)});
+      c->xpose_a = dalloc<float>(c->xpose_a_cap);
+      c->xpose_b = dalloc<float>(c->xpose_b_cap);
+    }
   }
   fr(c->tgt_loc); fr(c->lse_loc); fr(c->lse_all);
   if (c->vshard) {
@@ -427,14 +443,48 @@ int pick_splits(dl_ctx* c, int M, int N, int K, int max_splits = 32) {
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   int s = std::max(1, std::min(max_splits, kNumSMs / std::max(1, tiles)));
   if (tc(c)) s = tc_splits(K, s);
+  else if (c->tf32x3) s = tf32_splits(K, s);  // (valid for the SIMT kernel too)
   else s = std::max(1, std::min(s, (K + 63) / 64));
   return s;
 }
 
+// fp32 mode on the tensor cores: 3xTF32 (gemm_tc.cu), whose tcgen05
+// kind::tf32 MMAs read K-major operands only -- an MN-major operand is
+// transposed into the context's scratch first (xpose_a / xpose_b, sized by
+// ensure_window for the window's GEMMs)
 void gemm(dl_ctx* c, GemmDesc g) {
   c->launches++;
-  if (tc(c)) gemm_tc(g, c->st);
-  else gemm_f32(g, c->st);
+  if (tc(c)) {
+    gemm_tc(g, c->st);
+    return;
+  }
+  auto fits = [](int64_t rows, int64_t cols, size_t cap) {
+    return (size_t)rows * (size_t)((cols + 3) / 4 * 4) <= cap;
+  };
+  if (c->tf32x3 && (g.a_major == K_MAJOR || fits(g.M, g.K, c->xpose_a_cap)) &&
+      (g.b_major == K_MAJOR || fits(g.N, g.K, c->xpose_b_cap))) {
+    if (g.a_major == MN_MAJOR) {
+      const int64_t ld = (g.K + 3) / 4 * 4;
+      transpose_f32(static_cast<const float*>(g.A), g.K, g.M, g.lda, c->xpose_a, ld, c->st);
+      g.A = c->xpose_a;
+      g.lda = ld;
+      g.a_major = K_MAJOR;
+      c->launches++;
+    }
+    if (g.b_major == MN_MAJOR) {
+      const int64_t ld = (g.K + 3) / 4 * 4;
+      transpose_f32(static_cast<const float*>(g.B), g.K, g.N, g.ldb, c->xpose_b, ld, c->st);
+      g.B = c->xpose_b;
+      g.ldb = ld;
+      g.b_major = K_MAJOR;
+      c->launches++;
+    }
+    if (tf32x3_ok(g)) {
+      gemm_tf32x3(g, c->st);
+      return;
+    }
+  }
+  gemm_f32(g, c->st);
 }
 
 GemmDesc desc(int M, int N, int K, int am, const void* A, int64_t lda, int bm, const void* B,
@@ -1179,7 +1229,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   *out = nullptr;
   if (V < 1 || H < 1) return fail(nullptr, DL_EINVAL, "RnnParams: V,H >= 1");
   if (act != DL_SIGMOID && act != DL_TANH) return fail(nullptr, DL_EINVAL, "bad activation");
-  if (precision != DL_FP32 && precision != DL_BF16) return fail(nullptr, DL_EINVAL, "bad precision");
+  if (precision != DL_FP32 && precision != DL_BF16 && precision != DL_TF32X3)
+    return fail(nullptr, DL_EINVAL, "bad precision");
   if (precision == DL_BF16 && ((H % 8) != 0 || (V % 8) != 0))
     return fail(nullptr, DL_EINVAL, "bf16 tensor-core mode needs V and H multiples of 8 (TMA)");
   dl_ctx* c = new dl_ctx();
@@ -1195,6 +1246,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_FUSE_OUT")) c->fuse_out = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_FORK_LATE")) c->fork_late = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_XF")) c->xf = std::atoi(e) != 0;
+  c->tf32x3 = precision == DL_TF32X3;
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
@@ -1271,7 +1323,7 @@ int dl_destroy(dl_ctx* c) {
                   c->nce_ws.seg_start, c->nce_ws.order_pos, c->g_out_words, c->g_out_n,
                   c->nz_prob_d, c->nz_alias_d, c->raw_d, c->pos_of_d, c->first_d,
                   c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt, c->dS, c->xf_lse,
-                  c->xf_sc};
+                  c->xf_sc, c->xpose_a, c->xpose_b};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -2288,13 +2340,34 @@ int dl_test_gemm(dl_ctx* c, int M, int N, int K, int a_major, int b_major, const
       }
       cudaFree(part); cudaFree(tl); cudaFree(tg); cudaFree(S); cudaFree(lse);
     } else {
-      const int s = tc(c) ? tc_splits(K, std::max(1, splits)) : std::max(1, splits);
+      const int s = tc(c)        ? tc_splits(K, std::max(1, splits))
+                    : c->tf32x3 ? tf32_splits(K, std::max(1, splits))
+                                : std::max(1, splits);
       float* out = dalloc<float>((int64_t)s * M * N);
       float* red = dalloc<float>((int64_t)M * N);
       GemmDesc g = desc(M, N, K, a_major, Ap, lda, b_major, Bp, ldb, out, N);
       g.k_splits = s;
       g.split_stride = (int64_t)M * N;
+      // (fp32 / 3xTF32: transpose scratch for this shape)
+      float *sa = c->xpose_a, *sb = c->xpose_b;
+      const size_t ca = c->xpose_a_cap, cb = c->xpose_b_cap;
+      const int64_t k4 = (K + 3) / 4 * 4;
+      if (!tc(c) && c->tf32x3) {
+        c->xpose_a = dalloc<float>((int64_t)M * k4);
+        c->xpose_b = dalloc<float>((int64_t)N * k4);
+        c->xpose_a_cap = (size_t)M * k4;
+        c->xpose_b_cap = (size_t)N * k4;
+      }
       gemm(c, g);
+      if (!tc(c) && c->tf32x3) {
+        DL_CUDA(cudaStreamSynchronize(c->st));
+        cudaFree(c->xpose_a);
+        cudaFree(c->xpose_b);
+        c->xpose_a = sa;
+        c->xpose_b = sb;
+        c->xpose_a_cap = ca;
+        c->xpose_b_cap = cb;
+      }
       reduce_splits(out, s, (int64_t)M * N, (int64_t)M * N, red, 0.f, 0, nullptr, c->st);
       DL_CUDA(cudaMemcpyAsync(Cout, red, (size_t)M * N * 4, cudaMemcpyDeviceToHost, c->st));
       DL_CUDA(cudaStreamSynchronize(c->st));

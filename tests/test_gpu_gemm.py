@@ -39,7 +39,7 @@ SHAPES = [  # M, N, K
 ]
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("precision", ["bf16", "fp32", "tf32x3"])
 @pytest.mark.parametrize("am,bm", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", SHAPES)
 def test_gemm_layouts(precision, am, bm, M, N, K):

@@ -5,10 +5,17 @@ allreduce -- and the data-parallel + vocabulary-parallel output layer
 (hidden-state allgather, block log-sum-exp exchange, dh reduce-scatter, the
 fused dW_out + rmsprop epilogue under a communicator); each must train like
 a context without a communicator (identity exchanges)."""
+import os
+
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+# NCCL's cuMem allocations need POSIX-fd-shareable VMM handles, which the
+# container does not grant ("Cuda failure 'invalid argument'", alloc.h) --
+# plain cudaMalloc buffers do for a one-rank communicator
+os.environ.setdefault("NCCL_CUMEM_ENABLE", "0")
 
 
 def _train(dl, params, ids, V, H, precision, mode, windows=12):

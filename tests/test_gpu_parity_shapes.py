@@ -73,8 +73,9 @@ def sparse_rows(g_in_dense):
     return words, np.ascontiguousarray(g_in_dense[words])
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("H", [1024, 2048])
-def test_fp32_window_and_update_at_c2_c3(orc, H):
+def test_fp32_window_and_update_at_c2_c3(orc, H, precision):
     import paper_1502_00512_b200 as dl
     V, T, B = 64000, 4, 8
     rng = np.random.default_rng(H)
@@ -83,7 +84,7 @@ def test_fp32_window_and_update_at_c2_c3(orc, H):
     h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
     scale, clip, eta = 1.0 / (T * B), 1.0, 0.05
     want = orc.bptt(params, 0, x, y, w, h0, scale, clip)
-    m = dl.GpuRnn(V, H, 0, "fp32")
+    m = dl.GpuRnn(V, H, 0, precision)
     m.set_params(*params)
     m.set_opt(None, None, None, RHO, EPS)
     res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, scale, clip)
@@ -235,7 +236,7 @@ def test_bf16_persistent_recurrence_steps_at_h2048(act):
         h_dev = hf
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3", "bf16"])
 def test_c5_scorer_1024_streams(orc, precision):
     """sharded_perplexity's lock-step walk at the C5 shape: 1,024 slices of a
     stream, 3 scoring steps each; 24 slices re-scored by the oracle."""
@@ -261,7 +262,7 @@ def test_c5_scorer_1024_streams(orc, precision):
     assert want.shape == got.shape
     mask = ~np.isnan(want)
     assert np.array_equal(mask, ~np.isnan(got))
-    if precision == "fp32":
+    if precision != "bf16":
         assert np.allclose(got[mask], want[mask], rtol=1e-4, atol=1e-5)
     else:
         d = np.abs(got[mask] - want[mask])

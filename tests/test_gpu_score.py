@@ -8,16 +8,17 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("V,H,shards,n,act", [
     (30, 8, 8, 200, 0), (200, 32, 3, 1000, 1), (1000, 64, 64, 4000, 0),
     (10000, 128, 8, 3000, 0),
 ])
-def test_sharded_logprobs_match_oracle(orc, V, H, shards, n, act):
+def test_sharded_logprobs_match_oracle(orc, V, H, shards, n, act, precision):
     import paper_1502_00512_b200 as dl
     params = orc.init_uniform(V, H, 5 + V)
     ids = orc.random_stream(77 + V, V, n)[:n]
     want = orc.sharded_logprobs(params, act, ids, shards)
-    m = dl.GpuRnn(V, H, act, "fp32")
+    m = dl.GpuRnn(V, H, act, precision)
     m.set_params(*params)
     r = dl.sharded_perplexity(m, ids, shards)
     ro = orc.sharded_ppl(params, act, ids, shards)

@@ -45,8 +45,9 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("V,H,T,B,act,mask,clip", CASES)
-def test_window_fp32_matches_oracle(orc, V, H, T, B, act, mask, clip):
+def test_window_fp32_matches_oracle(orc, V, H, T, B, act, mask, clip, precision):
     import paper_1502_00512_b200 as dl
     rng = np.random.default_rng(V * 31 + H)
     params = orc.init_uniform(V, H, 11 + V)
@@ -54,7 +55,7 @@ def test_window_fp32_matches_oracle(orc, V, H, T, B, act, mask, clip):
     h0 = rng.uniform(-0.5, 0.5, (B, H)).astype(np.float32)
     scale = 1.0 / (T * B)
     want = orc.bptt(params, act, x, y, w, h0, scale, clip)
-    m = dl.GpuRnn(V, H, act, "fp32")
+    m = dl.GpuRnn(V, H, act, precision)
     m.set_params(*params)
     res, hf = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, scale, clip)
     assert res.positions == want["positions"]
