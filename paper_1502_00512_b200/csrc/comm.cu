@@ -29,8 +29,10 @@ static ncclDataType_t nccl_type(DType t) {
   return ncclFloat;
 }
 
-static void nccl_ok(ncclResult_t r) {
-  if (r != ncclSuccess) throw Error(3, std::string("NCCL: ") + ncclGetErrorString(r));
+static void nccl_ok(ncclResult_t r, const char* op = "", size_t n = 0, DType t = DType::F32) {
+  if (r != ncclSuccess)
+    throw Error(3, std::string("NCCL: ") + ncclGetErrorString(r) + " (" + op + ", " +
+                       std::to_string(n) + " x " + std::to_string(dtype_size(t)) + " B)");
 }
 
 NcclComm::NcclComm(const uint8_t id[128], int n, int r) {
@@ -46,16 +48,17 @@ NcclComm::~NcclComm() {
 }
 
 void NcclComm::allreduce_sum(void* buf, size_t n, DType t, cudaStream_t st) {
-  nccl_ok(ncclAllReduce(buf, buf, n, nccl_type(t), ncclSum, comm, st));
+  nccl_ok(ncclAllReduce(buf, buf, n, nccl_type(t), ncclSum, comm, st), "allreduce", n, t);
 }
 
 void NcclComm::allgather(const void* send, void* recv, size_t n, DType t, cudaStream_t st) {
-  nccl_ok(ncclAllGather(send, recv, n, nccl_type(t), comm, st));
+  nccl_ok(ncclAllGather(send, recv, n, nccl_type(t), comm, st), "allgather", n, t);
 }
 
 void NcclComm::reduce_scatter_sum(const void* send, void* recv, size_t n, DType t,
                                   cudaStream_t st) {
-  nccl_ok(ncclReduceScatter(send, recv, n, nccl_type(t), ncclSum, comm, st));
+  nccl_ok(ncclReduceScatter(send, recv, n, nccl_type(t), ncclSum, comm, st), "reduce_scatter",
+          n, t);
 }
 
 // ------------------------------------------------------------- LocalComm

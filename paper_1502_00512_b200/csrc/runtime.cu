@@ -370,7 +370,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   c->ews.order_pos = dalloc<int>(G * TB);
   c->ews.cap = G * TB;
   c->h0_d = dalloc<float>(nB * H);
-  if (G > 1) {
+  if (G > 1 || c->comm) {  // (a one-rank communicator gathers too)
     c->x_all = dalloc<uint32_t>(G * TB);
     c->dpre_all = dalloc<float>(G * TB * H);
   }
