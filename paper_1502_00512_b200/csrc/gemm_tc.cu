@@ -472,7 +472,15 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
   for (int k = 0; k < DL_RMS_RING; ++k) issue(k, ring + k * 4096);
   if (lane == 0) {
 #if !(DL_RMS_DIAG & 1)
-    while (ld_relaxed(g.rms_cnt + mt) < target) __nanosleep(32);
+    // bounded: the block's other pairs are co-resident by construction
+    // (launch2 checks cudaOccupancyMaxActiveClusters and the runtime never
+    // fuses beside another spinning kernel); if that is ever violated the
+    // kernel traps -- a loud launch failure, not a silent hang (~4 s)
+    long spins = 0;
+    while (ld_relaxed(g.rms_cnt + mt) < target) {
+      __nanosleep(32);
+      if (++spins > (1l << 27)) __trap();
+    }
 #endif
     ld_acquire_u32(g.rms_cnt + mt);  // acquire without waiting for the loads
     if (tr) tr[2] = gtimer_ns();

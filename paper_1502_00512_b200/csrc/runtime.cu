@@ -108,6 +108,7 @@ struct dl_ctx {
   // DL_TF32X3: the fp32 mode's GEMMs as 3xTF32 on the tensor cores
   // (gemm_tc.cu) instead of the fp32 FMA kernel (gemm_simt.cu)
   bool tf32x3 = false;
+  int dp_chunks = 4;  // dense DP: dW_out GEMM + allreduce in V chunks (DL_DP_CHUNKS)
   float *xpose_a = nullptr, *xpose_b = nullptr;  // K-major copies of MN-major operands
   size_t xpose_a_cap = 0, xpose_b_cap = 0;
   bool xf_on = false;                // this window's dS is formed in the dh GEMM
@@ -928,7 +929,38 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       g.Cb = c->g_out_bf;
       g.clip = INFINITY;
     }
-    gemm(c, g);
+    if (!dp) {
+      gemm(c, g);
+      return;
+    }
+    // data parallel: dW_out in V chunks, each summed over
+    // the ranks on the communication stream as soon as its GEMM is done --
+    // the allreduce of chunk i overlaps the GEMM of chunk i+1, the last one
+    // overlaps dh and the backward recurrence (joined before the update);
+    // the fp32 sum is clipped after the reduction
+    const int64_t nch = std::min<int64_t>(c->dp_chunks, std::max<int64_t>(1, Vo / 256));
+    for (int64_t k = 0; k < nch; ++k) {
+      const int64_t v0 = (Vo * k / nch) / 256 * 256;
+      const int64_t v1 = k + 1 == nch ? Vo : (Vo * (k + 1) / nch) / 256 * 256;
+      GemmDesc gk = g;
+      gk.M = (int)(v1 - v0);
+      gk.A = tc(c) ? (const void*)(static_cast<const bf16*>(gk.A) + v0)
+                   : (const void*)(static_cast<const float*>(gk.A) + v0);
+      gk.C = c->g_out + v0 * H;
+      if (gk.Cb) gk.Cb = c->g_out_bf + v0 * H;
+      gemm(c, gk);
+      DL_CUDA(cudaEventRecord(c->ev_fork, st));
+      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+      if (c->dp16) {
+        c->comm->allreduce_sum(c->g_out_bf + v0 * H, (size_t)((v1 - v0) * H), DType::BF16,
+                               c->st2);
+      } else {
+        c->comm->allreduce_sum(c->g_out + v0 * H, (size_t)((v1 - v0) * H), DType::F32, c->st2);
+        reduce_splits(c->g_out + v0 * H, 1, 0, (v1 - v0) * H, c->g_out + v0 * H, clip, 1,
+                      c->nonfinite, c->st2);
+        c->launches++;
+      }
+    }
   };
   if (nce) {
     // score_backward of every record: dh[t][b] = sum ds * W_out[w]
@@ -939,24 +971,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
            c->dh_out, st);
     c->launches++;
   }
-  auto reduce_dw = [&] {
-    if (dp) {
-      // data parallel: sum dW_out over ranks, then clip --
-      // on the communication stream, overlapping dh and the backward
-      // recurrence; joined before the update
-      DL_CUDA(cudaEventRecord(c->ev_fork, st));
-      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
-      if (c->dp16) {
-        // bf16 on the wire: half the NVLink bytes of the fp32 gradient; clip
-        // and the update follow in rms_dense_g16c
-        c->comm->allreduce_sum(c->g_out_bf, (size_t)(V * H), DType::BF16, c->st2);
-      } else {
-        c->comm->allreduce_sum(c->g_out, (size_t)(V * H), DType::F32, c->st2);
-        reduce_splits(c->g_out, 1, 0, V * H, c->g_out, clip, 1, c->nonfinite, c->st2);
-        c->launches++;
-      }
-    }
-  };
   // With a finite clip bound every clipped component is finite (clip1 maps
   // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
   // cannot fail and the dense W_out update -- HBM-bound -- may start as soon
@@ -989,7 +1003,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   // (dW_out reads the dS the dh GEMM stores when it is formed there)
   const bool dw_after_dh = fused || late || c->xf_on;
   auto after_dw = [&] {
-    reduce_dw();
     if (fork_out_eta > 0.0) fork_update(fork_out_eta, c->w_out_bf_next);
   };
   if (!dw_after_dh && !nce) {
@@ -1247,6 +1260,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_FORK_LATE")) c->fork_late = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_XF")) c->xf = std::atoi(e) != 0;
   c->tf32x3 = precision == DL_TF32X3;
+  if (const char* e = std::getenv("DL_DP_CHUNKS")) c->dp_chunks = std::max(1, std::atoi(e));
   const int rc = guarded(c, [&] {
     int n = 0;
     DL_CUDA(cudaGetDeviceCount(&n));
