@@ -102,11 +102,13 @@ def main():
     total = sum(d.get("gpu__time_duration.sum") or 0 for d in win)
     kernels = full_captures(tag)
     # the GEMM each pair-kernel instantiation serves in the C3 window
-    roles = {"tc_gemm2_kernel<0, 0, 0>": "tc_gemm[logits]", "tc_gemm2_kernel<0, 1, 0>": "tc_gemm[dh]",
-             "tc_gemm2_kernel<1, 1, 1>": "tc_gemm[dw_out]", "tc_gemm2_kernel<1, 1, 0>": "tc_gemm[dw_rec]"}
+    # (<A-major, B-major, fused rmsprop[, XF]>)
+    roles = {"tc_gemm2_kernel<0, 0, 0": "tc_gemm[logits]", "tc_gemm2_kernel<0, 1, 0": "tc_gemm[dh]",
+             "tc_gemm2_kernel<1, 1, 1": "tc_gemm[dw_out]", "tc_gemm2_kernel<1, 1, 0": "tc_gemm[dw_rec]"}
     for k in kernels:
         for pat, role in roles.items():
-            if pat in k["kernel"]:
+            i = k["kernel"].find(pat)
+            if i >= 0 and k["kernel"][i + len(pat)] in ",>":
                 k["role"] = role
     gemms = [k for k in kernels if k.get("role") in ("tc_gemm[logits]", "tc_gemm[dh]",
                                                      "tc_gemm[dw_out]")]

@@ -10,9 +10,10 @@ GOLD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 fx = sys.argv[1] if len(sys.argv) > 1 else "ppl_match_c1.npz"
 g = np.load(os.path.join(GOLD, fx))
 V, H = int(g["V"]), int(g["H"])
-ref = float(g["logs"][0][2])
-for prec in ("fp32", "tf32x3", "bf16"):
-    vals = []
+ref, ref_loss = float(g["logs"][0][2]), float(g["logs"][0][1])
+precs = sys.argv[2].split(",") if len(sys.argv) > 2 else ("fp32", "tf32x3", "bf16")
+for prec in precs:
+    vals, losses = [], []
     for k in range(-1, 4):
         params = [p.copy() for p in dl.init_uniform(V, H, int(g["init_seed"]))]
         if k >= 0:
@@ -23,5 +24,7 @@ for prec in ("fp32", "tf32x3", "bf16"):
         t = dl.Trainer(cfg, params, dl.make_vocab(V), g["train"], g["valid"], prec)
         t.train()
         vals.append(t.logs[0].valid_ppl / ref - 1)
+        losses.append(t.logs[0].train_loss / ref_loss - 1)
         t.model.close()
-    print(prec, " ".join(f"{100 * v:+.2f}%" for v in vals), flush=True)
+    print(prec, "valid ppl", " ".join(f"{100 * v:+.2f}%" for v in vals), "| train loss",
+          " ".join(f"{100 * v:+.2f}%" for v in losses), flush=True)

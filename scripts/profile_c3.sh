@@ -17,7 +17,7 @@ for k in "tc_gemm2_kernel:4" "rec_persist_kernel:2" "k_rms:4" "k_softmax:1" "k_e
       -o $OUT/${TAG}_prof_${name} $CMD > $OUT/${TAG}_prof_${name}.log 2>&1
 done
 # the fp32-class tensor-core mode's GEMM (3xTF32) at C2
-ncu --set full --clock-control none --import-source on -k regex:tc_tf32x3 -s 6 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:tc_tf32x3 -s 0 -c 40 \
     -o $OUT/${TAG}_prof_tc_tf32x3 python bench.py --steps 2 --warmup 2 --no-e2e --profile-steps 0 \
     --no-cpu-baseline --secondary= --config c2 --precision tf32x3 > $OUT/${TAG}_prof_tc_tf32x3.log 2>&1
 ls -la $OUT
