@@ -335,6 +335,22 @@ int dl_bn_train_window(dl_bn* ctx, int64_t T, int64_t B, const uint32_t* inputs,
                        const uint32_t* targets, const uint8_t* weights, const float* h0,
                        float* h_final, double loss_scale, float clip, double eta,
                        double* loss, uint64_t* positions, int* applied);
+/* Trainer<BottleneckTraits>::run_epoch on the device (trainer.hpp:350-410
+ * over compress.hpp:389-415), as dl_trainer_init / _run / _get_state /
+ * _set_state: the stream and the offset-stream schedule (cursors
+ * floor(i*L/N), hidden act(0)) live on the device; window w of a run is
+ * group w % noffset, built, trained (loss_scale 1/(minibatch*unroll), clip)
+ * and carried on the device (softmax windows replay one CUDA graph; NCE
+ * windows draw their noise on the host in the reference's order).
+ * dl_bn_trainer_run adds the windows' loss sum, target positions and
+ * skipped (non-finite) updates to the outputs (any may be NULL). */
+int dl_bn_trainer_init(dl_bn* ctx, const uint32_t* ids, int64_t L, int noffset, int minibatch,
+                       int unroll, double clip, uint32_t bos);
+int dl_bn_trainer_run(dl_bn* ctx, int64_t first, int64_t count, double eta, double* loss_sum,
+                      uint64_t* positions, uint64_t* skipped);
+/* cursors [noffset*minibatch], hidden [noffset*minibatch x H]; NULL skips */
+int dl_bn_trainer_get_state(dl_bn* ctx, int64_t* cursors, float* hidden);
+int dl_bn_trainer_set_state(dl_bn* ctx, const int64_t* cursors, const float* hidden);
 int dl_bn_sharded_perplexity(dl_bn* ctx, const uint32_t* ids, int64_t n, int shards,
                              uint32_t bos, double* total_logprob, uint64_t* predicted,
                              double* perplexity);

@@ -29,7 +29,8 @@ EXPORTS = (
     "dl_bn_get_grads", "dl_bn_rmsprop", "dl_bn_train_window", "dl_bn_sharded_perplexity",
     "dl_bn_launch_count", "dl_bn_cuda_stream", "dl_bn_set_loss_mode", "dl_bn_set_noise",
     "dl_bn_set_rng_state", "dl_bn_get_rng_state", "dl_bn_set_params_quantized", "dl_bn_score",
-    "dl_bn_set_noise_dist",
+    "dl_bn_set_noise_dist", "dl_bn_trainer_init", "dl_bn_trainer_run",
+    "dl_bn_trainer_get_state", "dl_bn_trainer_set_state",
 )
 
 DL_OK, DL_EINVAL, DL_EDATA, DL_EDEVICE = 0, 1, 2, 3
@@ -124,6 +125,12 @@ def load():
         "dl_bn_set_noise": (C.c_int, [vp, vp, i64, C.c_int, C.c_double]),
         "dl_bn_set_noise_dist": (C.c_int, [vp, vp, i64, C.c_int]),
         "dl_bn_score": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, P(C.c_double), P(u64)]),
+        "dl_bn_trainer_init": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_double,
+                                         C.c_uint32]),
+        "dl_bn_trainer_run": (C.c_int, [vp, i64, i64, C.c_double, P(C.c_double), P(u64),
+                                        P(u64)]),
+        "dl_bn_trainer_get_state": (C.c_int, [vp, vp, vp]),
+        "dl_bn_trainer_set_state": (C.c_int, [vp, vp, vp]),
         "dl_bn_set_rng_state": (C.c_int, [vp, vp]),
         "dl_bn_get_rng_state": (C.c_int, [vp, vp]),
         "dl_bn_launch_count": (u64, [vp]),

@@ -146,6 +146,31 @@ class GpuBottleneck:
     def launch_count(self) -> int:
         return int(load().dl_bn_launch_count(self._h))
 
+    # ---- device-resident epoch schedule (dl_bn_trainer_*)
+    def trainer_init(self, ids, noffset, minibatch, unroll, clip, bos=1):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        self._chk(load().dl_bn_trainer_init(self._h, ids.ctypes.data, len(ids), noffset,
+                                            minibatch, unroll, float(clip), bos))
+        self._n_streams = noffset * minibatch
+
+    def trainer_run(self, first, count, eta):
+        """Windows [first, first+count) -> (loss sum, target positions, skipped)."""
+        ls, pos, sk = C.c_double(0.0), C.c_uint64(0), C.c_uint64(0)
+        self._chk(load().dl_bn_trainer_run(self._h, first, count, eta, C.byref(ls),
+                                           C.byref(pos), C.byref(sk)))
+        return ls.value, pos.value, sk.value
+
+    def trainer_state(self):
+        cur = np.empty(self._n_streams, np.int64)
+        hid = np.empty((self._n_streams, self.H), np.float32)
+        self._chk(load().dl_bn_trainer_get_state(self._h, cur.ctypes.data, hid.ctypes.data))
+        return cur, hid
+
+    def trainer_set_state(self, cursors, hidden):
+        cur = np.ascontiguousarray(cursors, np.int64)
+        hid = np.ascontiguousarray(hidden, np.float32)
+        self._chk(load().dl_bn_trainer_set_state(self._h, cur.ctypes.data, hid.ctypes.data))
+
     # ---- NCE mode (the reference Trainer's default loss)
     def set_loss_mode(self, mode: int):
         """0 = NCE (LossMode::kNce), 1 = exact softmax."""
@@ -239,13 +264,16 @@ class BottleneckTrainer:
     """Trainer<BottleneckTraits> (trainer.hpp:171-476 over compress.hpp:389-415),
     softmax (mode 1) or NCE (mode 0, the reference default).  The host keeps the reference's schedule -- offset-stream
     cursors floor(i*L/N), window (r, g) positions cursor + t, bos-masked
-    targets, hidden carry and wrap reset (trainer.hpp:350-410) -- and every
-    window runs on the device as one dl_bn_train_window call (bptt_run +
+    targets, hidden carry and wrap reset (trainer.hpp:350-410).  By default
+    the schedule itself is device resident (dl_bn_trainer_run: the epoch's
+    windows are built, trained and carried on the device, softmax windows
+    replayed from one CUDA graph); device_loop=False keeps it on the host
+    and runs every window as one dl_bn_train_window call (bptt_run +
     bottleneck_update).  Validation is the device sharded scorer; the RTRN
     checkpoint carries RNBL + RBOP like the reference traits."""
 
     def __init__(self, cfg, params, vocab_words, train_ids, valid_ids, precision: str = "fp32",
-                 device: int = 0):
+                 device: int = 0, device_loop: bool = True):
         from . import BOS_ID, EpochLog  # noqa: F401
         cfg.validate()
         self.cfg = cfg
@@ -280,9 +308,14 @@ class BottleneckTrainer:
             self.model.set_loss_mode(0)
             self.model.set_noise(counts, cfg.nce_k, cfg.noise_floor)
             self.model.set_rng_state(rng_seed_state(cfg.seed))
-        self.cursors = np.array([i * L // N for i in range(N)], np.int64)
         self.a0 = np.float32(0.5 if cfg.act == 0 else 0.0)
-        self.hidden = np.full((N, H), self.a0, np.float32)
+        self.device_loop = device_loop
+        if device_loop:
+            self.model.trainer_init(self.train_ids, cfg.noffset, cfg.minibatch, cfg.unroll,
+                                    cfg.clip)
+        else:
+            self._cursors = np.array([i * L // N for i in range(N)], np.int64)
+            self._hidden = np.full((N, H), self.a0, np.float32)
         self.logs = []
         self.epoch = 0
         self.bad_epochs = 0
@@ -296,35 +329,63 @@ class BottleneckTrainer:
     def validate(self) -> float:
         return bn_sharded_perplexity(self.model, self.valid, self.cfg.valid_shards).perplexity
 
+    # the schedule's state (cursors, hidden carry): device resident unless
+    # device_loop=False
+    @property
+    def cursors(self):
+        return self.model.trainer_state()[0] if self.device_loop else self._cursors
+
+    @property
+    def hidden(self):
+        return self.model.trainer_state()[1] if self.device_loop else self._hidden
+
+    def _set_schedule(self, cursors, hidden):
+        if self.device_loop:
+            self.model.trainer_set_state(cursors, hidden)
+        else:
+            self._cursors = np.array(cursors, np.int64)
+            self._hidden = np.array(hidden, np.float32)
+
     def run_epoch(self):
         """trainer.hpp:350-410 -> (mean window loss, skipped, tokens)."""
+        cfg = self.cfg
+        L = len(self.train_ids)
+        B, T = cfg.minibatch, cfg.unroll
+        N = cfg.noffset * B
+        rounds = (L + N * T - 1) // (N * T)
+        if self.device_loop:
+            windows = rounds * cfg.noffset
+            loss_sum, _, skipped = self.model.trainer_run(0, windows, self.eta)
+            return (loss_sum / windows if windows else 0.0), skipped, rounds * N * T
+        return self._run_epoch_host(rounds)
+
+    def _run_epoch_host(self, rounds):
         from . import WindowBatch
         cfg = self.cfg
         ids, L = self.train_ids, len(self.train_ids)
         B, T = cfg.minibatch, cfg.unroll
         N = cfg.noffset * B
-        rounds = (L + N * T - 1) // (N * T)
         tt = np.arange(T)[:, None]
         loss_sum, windows, skipped = 0.0, 0, 0
         for _ in range(rounds):
             for g in range(cfg.noffset):
                 s0 = g * B
-                pos = self.cursors[None, s0:s0 + B] + tt
+                pos = self._cursors[None, s0:s0 + B] + tt
                 x = ids[pos % L]
                 y = ids[(pos + 1) % L]
                 w = (y != 1).astype(np.uint8)
                 res, hf, ok = bn_train_window(self.model, WindowBatch(x, y, w),
-                                              self.hidden[s0:s0 + B], 1.0 / (B * T), cfg.clip,
+                                              self._hidden[s0:s0 + B], 1.0 / (B * T), cfg.clip,
                                               self.eta)
                 loss_sum += res.loss
                 windows += 1
                 skipped += 0 if ok else 1
-                self.hidden[s0:s0 + B] = hf
-                cur = self.cursors[s0:s0 + B]
+                self._hidden[s0:s0 + B] = hf
+                cur = self._cursors[s0:s0 + B]
                 cur += T
                 wrap = cur >= L
                 cur[wrap] -= L
-                self.hidden[s0:s0 + B][wrap] = self.a0
+                self._hidden[s0:s0 + B][wrap] = self.a0
         return (loss_sum / windows if windows else 0.0), skipped, rounds * N * T
 
     def train(self, progress=None):
@@ -356,8 +417,7 @@ class BottleneckTrainer:
         self.bad_epochs, self.initial_ppl = st["bad"], st["initial"]
         self.model.set_params(*st["params"])
         self.model.set_opt(*st["opt"], cfg.rho, cfg.eps)
-        self.cursors = st["cursors"].copy()
-        self.hidden = st["hidden"].copy()
+        self._set_schedule(st["cursors"], st["hidden"])
         if cfg.mode == 0:
             words = st["rng_text"].split()
             if len(words) != 313:

@@ -125,6 +125,24 @@ struct dl_bn {
   std::map<std::tuple<int64_t, int64_t, double, float, double>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int64_t, int64_t, double, float, double>, uint64_t> graph_launches;
   bool use_graphs = true;
+  // device-resident epoch schedule (dl_bn_trainer_*): the stream, the
+  // offset-stream cursors and hidden carry, the window counter and the run's
+  // loss / position / skipped-update sums; softmax windows replay one graph
+  int64_t L = 0;
+  int noffset = 0, minibatch = 0, unroll = 0;
+  double clip = 1.0;
+  uint32_t bos = 1;
+  uint32_t* ids = nullptr;
+  std::vector<uint32_t> h_ids;  // (NCE: the host mirrors the schedule to draw)
+  int64_t* cursors = nullptr;
+  float* hidden = nullptr;
+  int64_t* win_counter = nullptr;
+  double* t_loss = nullptr;
+  unsigned long long *t_pos = nullptr, *t_skipped = nullptr;
+  cudaGraphExec_t tgraph = nullptr;
+  double tgraph_eta = 0.0;
+  uint64_t tgraph_launches = 0;
+  bool tgraph_sized = false;
 };
 
 namespace {
@@ -276,6 +294,23 @@ int splits_for(const dl_bn* c, int M, int N, int K, int max_splits) {
   return s;
 }
 
+void drop_graphs(dl_bn* c);
+
+// Grow the split-K workspace: recorded graphs hold the old pointer, so they
+// are dropped (growth happens in eager windows only -- every graphed shape
+// has run eagerly first)
+void grow_splitws(dl_bn* c, size_t need) {
+  if (need <= c->split_cap) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DL_CUDA(cudaStreamIsCapturing(c->st, &cs));
+  DL_REQUIRE(cs == cudaStreamCaptureStatusNone, DL_EDEVICE, "split workspace grown inside a capture");
+  DL_CUDA(cudaStreamSynchronize(c->st));
+  drop_graphs(c);
+  bn_free(c->splitws);
+  c->splitws = bn_alloc<float>(need);
+  c->split_cap = need;
+}
+
 void run_gemm(dl_bn* c, const GemmDesc& g) {
   c->launches++;
   if (tcm(c)) gemm_tc(g, c->st);
@@ -290,11 +325,7 @@ void mm(dl_bn* c, int M, int N, int K, int am, const void* A, int64_t lda, int b
   const int s = splits_for(c, M, N, K, max_splits);
   if (s > 1) {
     const size_t need = (size_t)s * M * N;
-    if (need > c->split_cap) {
-      bn_free(c->splitws);
-      c->splitws = bn_alloc<float>(need);
-      c->split_cap = need;
-    }
+    grow_splitws(c, need);
     g.C = c->splitws;
     g.k_splits = s;
     g.split_stride = (int64_t)M * N;
@@ -311,6 +342,9 @@ void drop_graphs(dl_bn* c) {
   for (auto& kv : c->graphs)
     if (kv.second) cudaGraphExecDestroy(kv.second);
   c->graphs.clear();
+  if (c->tgraph) cudaGraphExecDestroy(c->tgraph);
+  c->tgraph = nullptr;
+  c->tgraph_sized = false;
 }
 
 void ensure_window(dl_bn* c, int64_t T, int64_t N) {
@@ -444,11 +478,7 @@ void recurrence_fwd(dl_bn* c, int64_t T, int64_t Bn) {
   for (int64_t t = 0; t < T; ++t) {
     const int s = splits_for(c, (int)Bn, (int)H, (int)H, 32);
     const size_t need = (size_t)s * BH;
-    if (need > c->split_cap) {
-      bn_free(c->splitws);
-      c->splitws = bn_alloc<float>(need);
-      c->split_cap = need;
-    }
+    grow_splitws(c, need);
     GemmDesc g = tcm(c) ? mk((int)Bn, (int)H, (int)H, K_MAJOR, c->htape_bf + t * BH, H, K_MAJOR,
                              c->w_rec_bf, H, c->splitws, H)
                         : mk((int)Bn, (int)H, (int)H, K_MAJOR, c->htape + t * BH, H, K_MAJOR,
@@ -592,11 +622,7 @@ void run_window(dl_bn* c, int64_t T, int64_t B, double scale, float clip, bool g
     if (t < T - 1) {
       s = splits_for(c, (int)B, (int)H, (int)H, 32);
       const size_t need = (size_t)s * BH;
-      if (need > c->split_cap) {
-        bn_free(c->splitws);
-        c->splitws = bn_alloc<float>(need);
-        c->split_cap = need;
-      }
+      grow_splitws(c, need);
       GemmDesc g = t16 ? mk((int)B, (int)H, (int)H, K_MAJOR, c->dpre_bf + (t + 1) * BH, H, MN_MAJOR,
                             c->w_rec_bf, H, c->splitws, H)
                        : mk((int)B, (int)H, (int)H, K_MAJOR, c->dpre + (t + 1) * BH, H, MN_MAJOR,
@@ -655,6 +681,25 @@ void run_update(dl_bn* c, double eta) {
   rms_rec(c->d, t16 ? c->d_bf : nullptr, c->m_d, c->g_d, c->H * c->P, c->rho, c->eps, eta,
           c->nonfinite, st);
   c->launches += 4;
+}
+
+// The window's noise draws (t, b, then sample; masked positions draw
+// nothing): 2 raw mt19937_64 outputs per draw, turned into words on the
+// device with the alias tables (nce.cu k_nce_records).  (Pageable source:
+// the copy has consumed raw_h when cudaMemcpyAsync returns.)
+void nce_draws(dl_bn* c, const uint8_t* weights, int64_t N) {
+  DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
+             "bptt: NCE mode needs noise model and rng (dl_bn_set_noise)");
+  int64_t Pn = 0;
+  for (int64_t i = 0; i < N; ++i) Pn += weights[i] ? 1 : 0;
+  nce_reserve(c, std::max<int64_t>(N * (c->nce_k + 1), 1));
+  const int64_t ND = 2 * Pn * c->nce_k;
+  c->raw_h.resize(std::max<int64_t>(ND, 1));
+  for (int64_t i = 0; i < ND; ++i) c->raw_h[i] = c->rng();
+  if (ND > 0)
+    DL_CUDA(cudaMemcpyAsync(c->raw_d, c->raw_h.data(), ND * 8, cudaMemcpyHostToDevice, c->st));
+  c->nce_P = Pn;
+  c->nce_N = Pn * (c->nce_k + 1);
 }
 
 void upload(dl_bn* c, float* dst, const float* src, int64_t n) {
@@ -753,7 +798,9 @@ int dl_bn_destroy(dl_bn* c) {
                   (void*)c->loss_pos, (void*)c->keys_in, (void*)c->vals_in, (void*)c->keys_out,
                   (void*)c->vals_out, (void*)c->head, (void*)c->slot, c->sort_temp,
                   (void*)c->nce_ws.seg_start, (void*)c->nce_ws.order_pos, (void*)c->out_rows,
-                  (void*)c->out_words, (void*)c->out_n, (void*)c->touched})
+                  (void*)c->out_words, (void*)c->out_n, (void*)c->touched, (void*)c->ids,
+                  (void*)c->cursors, (void*)c->hidden, (void*)c->win_counter, (void*)c->t_loss,
+                  (void*)c->t_pos, (void*)c->t_skipped})
     if (p) cudaFree(p);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -865,23 +912,7 @@ int bn_window_call(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
       if (weights[i]) DL_REQUIRE(targets[i] < (uint64_t)c->V, DL_EDATA, "bptt: id out of vocabulary range");
     ensure_window(c, T, N);
     cudaStream_t st = c->st;
-    if (c->loss_mode == 0) {
-      // the window's noise draws (t, b, then sample; masked positions draw
-      // nothing): 2 raw mt19937_64 outputs per draw, turned into words on
-      // the device with the alias tables (nce.cu k_nce_records)
-      DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
-                 "bptt: NCE mode needs noise model and rng (dl_bn_set_noise)");
-      int64_t Pn = 0;
-      for (int64_t i = 0; i < N; ++i) Pn += weights[i] ? 1 : 0;
-      nce_reserve(c, std::max<int64_t>(N * (c->nce_k + 1), 1));
-      const int64_t ND = 2 * Pn * c->nce_k;
-      c->raw_h.resize(std::max<int64_t>(ND, 1));
-      for (int64_t i = 0; i < ND; ++i) c->raw_h[i] = c->rng();
-      if (ND > 0)
-        DL_CUDA(cudaMemcpyAsync(c->raw_d, c->raw_h.data(), ND * 8, cudaMemcpyHostToDevice, st));
-      c->nce_P = Pn;
-      c->nce_N = Pn * (c->nce_k + 1);
-    }
+    if (c->loss_mode == 0) nce_draws(c, weights, N);
     DL_CUDA(cudaMemcpyAsync(c->x, inputs, N * 4, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->y, targets, N * 4, cudaMemcpyHostToDevice, st));
     DL_CUDA(cudaMemcpyAsync(c->w, weights, N, cudaMemcpyHostToDevice, st));
@@ -976,6 +1007,179 @@ int dl_bn_train_window(dl_bn* c, int64_t T, int64_t B, const uint32_t* inputs,
   if (!(eta > 0.0)) return bn_fail(c, DL_EINVAL, "config: eta must be > 0");
   return bn_window_call(c, T, B, inputs, targets, weights, h0, h_final, loss_scale, clip, true,
                         eta, loss, positions, applied);
+}
+
+// ------------------------------------------------------------- trainer
+// Trainer<BottleneckTraits>::run_epoch on the device (trainer.hpp:350-410
+// over compress.hpp:389-415): the stream, the offset-stream cursors
+// floor(i*L/N), the hidden carry and the window counter live in HBM; each
+// window is window_build -> bptt_run -> bottleneck_update -> window_finish,
+// with the loss / skipped-update sums kept on the device.  Softmax windows
+// replay one CUDA graph; NCE windows draw their noise on the host (the
+// reference's generator order), which mirrors the schedule for the targets.
+int dl_bn_trainer_init(dl_bn* c, const uint32_t* ids, int64_t L, int noffset, int minibatch,
+                       int unroll, double clip, uint32_t bos) {
+  if (!c) return bn_fail(c, DL_EINVAL, "dl_bn_trainer_init: null ctx");
+  if (noffset < 1 || minibatch < 1 || unroll < 1)
+    return bn_fail(c, DL_EINVAL, "config: noffset, minibatch, unroll must be >= 1");
+  if (!(clip > 0.0)) return bn_fail(c, DL_EINVAL, "config: clip must be > 0");
+  const int64_t N = (int64_t)noffset * minibatch;
+  if (!ids || L < N)
+    return bn_fail(c, DL_EINVAL, "trainer: training stream shorter than the stream count");
+  for (int64_t i = 0; i < L; ++i)
+    if (ids[i] >= (uint64_t)c->V) return bn_fail(c, DL_EDATA, "trainer: id out of vocabulary range");
+  return bn_guarded(c, [&] {
+    DL_CUDA(cudaStreamSynchronize(c->st));
+    drop_graphs(c);
+    for (void** p : {(void**)&c->ids, (void**)&c->cursors, (void**)&c->hidden})
+      if (*p) {
+        cudaFree(*p);
+        *p = nullptr;
+      }
+    c->L = L;
+    c->noffset = noffset;
+    c->minibatch = minibatch;
+    c->unroll = unroll;
+    c->clip = clip;
+    c->bos = bos;
+    c->ids = bn_alloc<uint32_t>(L);
+    c->h_ids.assign(ids, ids + L);
+    DL_CUDA(cudaMemcpyAsync(c->ids, c->h_ids.data(), L * 4, cudaMemcpyHostToDevice, c->st));
+    c->cursors = bn_alloc<int64_t>(N);
+    c->hidden = bn_alloc<float>(N * c->H);
+    if (!c->win_counter) c->win_counter = bn_alloc<int64_t>(1);
+    if (!c->t_loss) c->t_loss = bn_alloc<double>(1);
+    if (!c->t_pos) c->t_pos = bn_alloc<unsigned long long>(1);
+    if (!c->t_skipped) c->t_skipped = bn_alloc<unsigned long long>(1);
+    std::vector<int64_t> cur(N);
+    for (int64_t i = 0; i < N; ++i) cur[i] = i * L / N;  // trainer.hpp:194-195
+    DL_CUDA(cudaMemcpyAsync(c->cursors, cur.data(), N * 8, cudaMemcpyHostToDevice, c->st));
+    fill_f32(c->hidden, act0(c->act), N * c->H, c->st);
+    c->launches++;
+    ensure_window(c, unroll, (int64_t)unroll * minibatch);
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_bn_trainer_get_state(dl_bn* c, int64_t* cursors, float* hidden) {
+  if (!c || !c->cursors) return bn_fail(c, DL_EINVAL, "trainer not initialised");
+  return bn_guarded(c, [&] {
+    const int64_t N = (int64_t)c->noffset * c->minibatch;
+    if (cursors) DL_CUDA(cudaMemcpyAsync(cursors, c->cursors, N * 8, cudaMemcpyDeviceToHost, c->st));
+    if (hidden) DL_CUDA(cudaMemcpyAsync(hidden, c->hidden, N * c->H * 4, cudaMemcpyDeviceToHost, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int dl_bn_trainer_set_state(dl_bn* c, const int64_t* cursors, const float* hidden) {
+  if (!c || !c->cursors) return bn_fail(c, DL_EINVAL, "trainer not initialised");
+  const int64_t N = (int64_t)c->noffset * c->minibatch;
+  if (cursors)
+    for (int64_t i = 0; i < N; ++i)
+      if (cursors[i] < 0 || cursors[i] >= c->L)
+        return bn_fail(c, DL_EDATA, "trainer checkpoint: cursor out of range");
+  return bn_guarded(c, [&] {
+    if (cursors) DL_CUDA(cudaMemcpyAsync(c->cursors, cursors, N * 8, cudaMemcpyHostToDevice, c->st));
+    if (hidden) DL_CUDA(cudaMemcpyAsync(c->hidden, hidden, N * c->H * 4, cudaMemcpyHostToDevice, c->st));
+    DL_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+namespace {
+void bn_trainer_window(dl_bn* c, double eta) {
+  const int64_t B = c->minibatch, T = c->unroll, H = c->H;
+  cudaStream_t st = c->st;
+  window_build(c->ids, c->L, c->cursors, c->hidden, c->win_counter, c->noffset, B, T, H, c->bos,
+               c->x, c->y, c->w, c->htape, st);
+  c->launches++;
+  run_window(c, T, B, 1.0 / (double)(B * T), (float)c->clip, true);
+  run_update(c, eta);
+  accum_loss(c->t_loss, c->d_loss, c->t_pos, c->d_pos, st);
+  window_finish(c->cursors, c->hidden, c->htape + T * B * H, c->win_counter, c->noffset, B, T, H,
+                c->L, act0(c->act), st, c->nonfinite, c->t_skipped);
+  c->launches += 3;
+}
+}  // namespace
+
+int dl_bn_trainer_run(dl_bn* c, int64_t first, int64_t count, double eta, double* loss_sum,
+                      uint64_t* positions, uint64_t* skipped) {
+  if (!c || !c->ids) return bn_fail(c, DL_EINVAL, "trainer not initialised");
+  if (!(eta > 0.0)) return bn_fail(c, DL_EINVAL, "config: eta must be > 0");
+  if (first < 0 || count < 0) return bn_fail(c, DL_EINVAL, "dl_bn_trainer_run: negative window");
+  return bn_guarded(c, [&] {
+    cudaStream_t st = c->st;
+    const int64_t B = c->minibatch, T = c->unroll, N = (int64_t)c->noffset * B;
+    DL_CUDA(cudaMemcpyAsync(c->win_counter, &first, 8, cudaMemcpyHostToDevice, st));
+    DL_CUDA(cudaMemsetAsync(c->t_loss, 0, 8, st));
+    DL_CUDA(cudaMemsetAsync(c->t_pos, 0, 8, st));
+    DL_CUDA(cudaMemsetAsync(c->t_skipped, 0, 8, st));
+    ensure_window(c, T, T * B);
+    if (c->loss_mode == 0) {
+      // the host mirrors the schedule (cursors; trainer.hpp:374-406) for the
+      // window's targets / mask, then draws in the reference's order
+      std::vector<int64_t> cur(N);
+      DL_CUDA(cudaMemcpyAsync(cur.data(), c->cursors, N * 8, cudaMemcpyDeviceToHost, st));
+      DL_CUDA(cudaStreamSynchronize(st));
+      std::vector<uint8_t> w(T * B);
+      const int64_t L = c->L;
+      for (int64_t i = 0; i < count; ++i) {
+        const int64_t s0 = ((first + i) % c->noffset) * B;
+        for (int64_t t = 0; t < T; ++t)
+          for (int64_t b = 0; b < B; ++b)
+            w[t * B + b] = c->h_ids[(cur[s0 + b] + t + 1) % L] == c->bos ? 0 : 1;
+        nce_draws(c, w.data(), T * B);
+        bn_trainer_window(c, eta);
+        for (int64_t b = 0; b < B; ++b) {
+          int64_t v = cur[s0 + b] + T;
+          cur[s0 + b] = v >= L ? v - L : v;
+        }
+      }
+    } else if (c->use_graphs && count > 0) {
+      // one eager window sizes every lazily grown buffer, then one graph
+      // (build -> window -> update -> sums -> finish) replays the rest
+      int64_t i = 0;
+      if (!c->tgraph_sized) {
+        bn_trainer_window(c, eta);
+        c->tgraph_sized = true;
+        ++i;
+      }
+      if (i < count && (!c->tgraph || c->tgraph_eta != eta)) {
+        if (c->tgraph) cudaGraphExecDestroy(c->tgraph);
+        c->tgraph = nullptr;
+        cudaGraph_t gr = nullptr;
+        const uint64_t l0 = c->launches;
+        DL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          bn_trainer_window(c, eta);
+        } catch (...) {
+          cudaStreamEndCapture(st, &gr);
+          if (gr) cudaGraphDestroy(gr);
+          throw;
+        }
+        DL_CUDA(cudaStreamEndCapture(st, &gr));
+        c->tgraph_launches = c->launches - l0;
+        c->launches = l0;  // counted when replayed
+        DL_CUDA(cudaGraphInstantiate(&c->tgraph, gr, 0));
+        cudaGraphDestroy(gr);
+        c->tgraph_eta = eta;
+      }
+      for (; i < count; ++i) {
+        DL_CUDA(cudaGraphLaunch(c->tgraph, st));
+        c->launches += c->tgraph_launches;
+      }
+    } else {
+      for (int64_t i = 0; i < count; ++i) bn_trainer_window(c, eta);
+    }
+    c->have_grads = false;
+    struct { double l; unsigned long long p, s; } res{};
+    DL_CUDA(cudaMemcpyAsync(&res.l, c->t_loss, 8, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaMemcpyAsync(&res.p, c->t_pos, 8, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaMemcpyAsync(&res.s, c->t_skipped, 8, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaStreamSynchronize(st));
+    if (loss_sum) *loss_sum += res.l;
+    if (positions) *positions += res.p;
+    if (skipped) *skipped += res.s;
+  });
 }
 
 // sharded_perplexity over the bottleneck adapter (eval.hpp:151-222): S

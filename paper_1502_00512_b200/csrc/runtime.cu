@@ -87,6 +87,8 @@ struct dl_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sort_fork = nullptr, ev_sort_join = nullptr;  // W_in id sort on st2
   cudaEvent_t ev_hfinal = nullptr;  // forward recurrence done (h_final readable)
+  // data-parallel + vocabulary-parallel: dh partials ready / dh reduce-scattered
+  cudaEvent_t ev_dh = nullptr, ev_rs = nullptr;
 
   // window workspace
   int64_t capT = 0, capB = 0;
@@ -219,13 +221,21 @@ struct dl_ctx {
   unsigned long long* raw_d = nullptr;  // [2 k P] raw mt19937_64 outputs of the window
   uint32_t* pos_of_d = nullptr;   // [TB] unmasked positions in t-major order
   int* first_d = nullptr;         // [T + 1]
-  int64_t raw_cap = 0;
+  int64_t raw_cap = 0, pos_cap = 0;
   void* raw_pin[2] = {nullptr, nullptr};  // double-buffered host staging of raw outputs
   cudaEvent_t raw_ev[2] = {nullptr, nullptr};
   int raw_slot = 0;
   bool nce_pending = false;       // records of the prepared window not built yet
   double nce_wait_s = 0.0, nce_gen_s = 0.0, nce_res_s = 0.0, nce_copy_s = 0.0;  // (DL_DEBUG)
   std::vector<uint32_t> h_ids;  // trainer: host copy of the stream (NCE draws)
+  // NCE under data parallel ranks: every rank runs the (cheap, sparse) NCE
+  // output layer over the whole global window -- the gathered targets, mask
+  // and hidden states laid out t-major over the global streams r*B + b --
+  // with the shared generator's draws, so the loss, the sparse W_out rows
+  // and their update are identical on every rank; each keeps its own dh rows
+  uint32_t *ng_y = nullptr, *ng_y_rb = nullptr;
+  uint8_t *ng_w = nullptr, *ng_w_rb = nullptr;
+  float *ng_hs = nullptr, *ng_hs_rb = nullptr, *ng_dh = nullptr;
 
   // profiling
   bool profiling = false;
@@ -345,6 +355,8 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->x_all); fr(c->dpre_all);
   fr(c->hs_all_bf); fr(c->hs_all); fr(c->y_all); fr(c->w_all); fr(c->dh_all);
   fr(c->dS); fr(c->xf_lse); fr(c->xf_sc); fr(c->xpose_a); fr(c->xpose_b);
+  fr(c->ng_y); fr(c->ng_y_rb); fr(c->ng_w); fr(c->ng_w_rb); fr(c->ng_hs); fr(c->ng_hs_rb);
+  fr(c->ng_dh);
   c->xpose_a_cap = c->xpose_b_cap = 0;
   c->capT = nT;
   c->capB = nB;
@@ -374,6 +386,15 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   if (G > 1 || c->comm) {  // (a one-rank communicator gathers too)
     c->x_all = dalloc<uint32_t>(G * TB);
     c->dpre_all = dalloc<float>(G * TB * H);
+  }
+  if (c->comm && !c->vshard && c->loss_mode == 0) {
+    c->ng_y = dalloc<uint32_t>(G * TB);
+    c->ng_y_rb = dalloc<uint32_t>(G * TB);
+    c->ng_w = dalloc<uint8_t>(G * TB);
+    c->ng_w_rb = dalloc<uint8_t>(G * TB);
+    c->ng_hs = dalloc<float>(G * TB * H);
+    c->ng_hs_rb = dalloc<float>(G * TB * H);
+    c->ng_dh = dalloc<float>(G * TB * H);
   }
   const int64_t Vo = c->Vo;  // output rows held by this context
   (void)V;
@@ -675,7 +696,8 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
   // a device-synchronising cudaFree -- as the masked count varies)
   nce_reserve(c, std::max<int64_t>(T * B * K1, 1));
   c->nce_res_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - r0).count();
-  if (ND > c->raw_cap || !c->pos_of_d || c->capT * c->capB > c->raw_cap / 2) {
+  if (ND > c->raw_cap || !c->pos_of_d || c->capT * c->capB > c->raw_cap / 2 ||
+      c->pos_cap < T * B) {
     const int64_t cap = std::max<int64_t>({ND, 2 * c->capT * c->capB * c->nce_k, 2});
     for (int i = 0; i < 2; ++i) {
       if (c->raw_ev[i]) DL_CUDA(cudaEventSynchronize(c->raw_ev[i]));
@@ -688,7 +710,8 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
     if (c->pos_of_d) cudaFree(c->pos_of_d);
     if (c->first_d) cudaFree(c->first_d);
     c->raw_d = dalloc<unsigned long long>(cap);
-    c->pos_of_d = dalloc<uint32_t>(std::max<int64_t>(c->capT * c->capB, T * B));
+    c->pos_cap = std::max<int64_t>(c->capT * c->capB, T * B);
+    c->pos_of_d = dalloc<uint32_t>(c->pos_cap);
     c->first_d = dalloc<int>(std::max(c->capT, T) + 1);
     c->raw_cap = cap;
   }
@@ -784,16 +807,40 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     wo = c->w_all;
   }
   const bool nce = c->loss_mode == 0;
+  // NCE with data-parallel ranks: the output layer runs over the global
+  // window (t-major over the global streams r*B + b) on every rank
+  const bool nce_dp = nce && dp;
+  const int64_t Bn = nce_dp ? c->nranks * B : B;  // streams of the NCE window
+  const float* Hn = Hs;
+  if (nce_dp) {
+    Phase p(c, "nce_gather");
+    DL_REQUIRE(c->ng_hs != nullptr, DL_EDEVICE, "internal: NCE gather buffers");
+    const int G = c->nranks;
+    c->comm->allgather(c->y_d, c->ng_y_rb, (size_t)TB, DType::U32, st);
+    c->comm->allgather(c->w_d, c->ng_w_rb, (size_t)TB, DType::U8, st);
+    c->comm->allgather(Hs, c->ng_hs_rb, (size_t)(TB * H), DType::F32, st);
+    // rank-blocked [r][t][b] -> t-major [t][r][b]
+    for (int r = 0; r < G; ++r) {
+      DL_CUDA(cudaMemcpy2DAsync(c->ng_y + r * B, Bn * 4, c->ng_y_rb + r * TB, B * 4, B * 4, T,
+                                cudaMemcpyDeviceToDevice, st));
+      DL_CUDA(cudaMemcpy2DAsync(c->ng_w + r * B, Bn, c->ng_w_rb + r * TB, B, B, T,
+                                cudaMemcpyDeviceToDevice, st));
+      DL_CUDA(cudaMemcpy2DAsync(c->ng_hs + r * B * H, Bn * H * 4, c->ng_hs_rb + r * TB * H,
+                                B * H * 4, B * H * 4, T, cudaMemcpyDeviceToDevice, st));
+    }
+    Hn = c->ng_hs;
+  }
   if (nce) {
     // NCE loss over the window's records (backprop.hpp:126-156)
     Phase p(c, "nce_loss");
     const int K1 = c->nce_k + 1;
     DL_REQUIRE(c->nce_pending, 1, "NCE window without prepared draws");
-    nce_records(c->w_d, c->y_d, T, B, c->nce_P, K1, c->raw_d, c->nz_prob_d, c->nz_alias_d, V,
-                c->pos_of_d, c->first_d, c->rec_word_d, c->rec_row_d, c->proc_r_d, st);
+    nce_records(nce_dp ? c->ng_w : c->w_d, nce_dp ? c->ng_y : c->y_d, T, Bn, c->nce_P, K1,
+                c->raw_d, c->nz_prob_d, c->nz_alias_d, V, c->pos_of_d, c->first_d,
+                c->rec_word_d, c->rec_row_d, c->proc_r_d, st);
     c->nce_pending = false;
     c->launches += 2;
-    nce_scores(Hs, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st);
+    nce_scores(Hn, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st);
     nce_loss(c->score_d, c->rec_word_d, c->ln_kq_d, c->nce_P, K1, scale, c->loss_pos_d, c->ds_d,
              st);
     sum_rows(c->loss_pos_d, nullptr, c->nce_P, c->d_loss, c->d_pos, st);
@@ -966,10 +1013,13 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // score_backward of every record: dh[t][b] = sum ds * W_out[w]
     // (rnn.hpp:251-255); masked positions contribute nothing
     Phase p(c, "nce_dh");
-    DL_CUDA(cudaMemsetAsync(c->dh_out, 0, TB * H * sizeof(float), st));
-    nce_dh(c->w_out, H, c->rec_word_d, c->rec_row_d, c->ds_d, c->nce_P, c->nce_k + 1,
-           c->dh_out, st);
+    float* dhn = nce_dp ? c->ng_dh : c->dh_out;
+    DL_CUDA(cudaMemsetAsync(dhn, 0, T * Bn * H * sizeof(float), st));
+    nce_dh(c->w_out, H, c->rec_word_d, c->rec_row_d, c->ds_d, c->nce_P, c->nce_k + 1, dhn, st);
     c->launches++;
+    if (nce_dp)  // this rank's rows of the global window
+      DL_CUDA(cudaMemcpy2DAsync(c->dh_out, B * H * 4, c->ng_dh + c->rank * B * H, Bn * H * 4,
+                                B * H * 4, T, cudaMemcpyDeviceToDevice, st));
   }
   // With a finite clip bound every clipped component is finite (clip1 maps
   // NaN to -c), so rmsprop_update's all-finite check (rmsprop.hpp:116)
@@ -1000,8 +1050,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     }
     DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
   };
-  // (dW_out reads the dS the dh GEMM stores when it is formed there)
-  const bool dw_after_dh = fused || late || c->xf_on;
+  // (dW_out reads the dS the dh GEMM stores when it is formed there; with
+  // the vocabulary-parallel layer the dh reduce-scatter runs under dW_out)
+  const bool dw_after_dh = fused || late || c->xf_on || dpv;
   auto after_dw = [&] {
     if (fork_out_eta > 0.0) fork_update(fork_out_eta, c->w_out_bf_next);
   };
@@ -1041,6 +1092,27 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     }
   };
   if (!nce) dh();
+  if (dpv && !nce) {
+    // every rank's partial dh over the global window, summed over ranks and
+    // scattered (this rank keeps its own TB rows) on the side stream while
+    // dW_out runs; the backward recurrence joins it.  (Against the fused
+    // dW_out's co-resident CTAs the collective only delays some of them: it
+    // never waits on them, so the spin-waits resolve once it finishes.)
+    DL_CUDA(cudaEventRecord(c->ev_dh, st));
+    DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_dh, 0));
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) {
+      a = ev_get(c);
+      b = ev_get(c);
+      DL_CUDA(cudaEventRecord(a, c->st2));
+    }
+    c->comm->reduce_scatter_sum(c->dh_all, c->dh_out, (size_t)(TB * H), DType::F32, c->st2);
+    if (c->profiling) {
+      DL_CUDA(cudaEventRecord(b, c->st2));
+      c->pending.push_back({"vocab_exchange", {a, b}});
+    }
+    DL_CUDA(cudaEventRecord(c->ev_rs, c->st2));
+  }
   if (dw_after_dh && !nce) {
     dw_out();
     after_dw();
@@ -1052,9 +1124,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     // replicated computations on identical inputs.
     Phase p(c, "vocab_exchange");
     c->comm->allreduce_sum(c->dh_out, (size_t)(TB * H), DType::F32, st);
+  } else if (dpv && !nce) {
+    DL_CUDA(cudaStreamWaitEvent(st, c->ev_rs, 0));
   } else if (dpv) {
-    // every rank's partial dh over the global window, summed over ranks and
-    // scattered: this rank keeps its own TB rows
     Phase p(c, "vocab_exchange");
     c->comm->reduce_scatter_sum(c->dh_all, c->dh_out, (size_t)(TB * H), DType::F32, st);
   }
@@ -1140,7 +1212,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     NceRecs R{c->rec_word_d, c->rec_row_d, c->proc_r_d, c->ds_d, c->sort_keys_in,
               c->sort_vals_in, c->sort_keys_out, c->sort_vals_out, c->sort_head,
               c->sort_slot, c->sort_temp, c->sort_temp_bytes};
-    nce_out_rows(R, c->nce_N, Vo, Hs, H, clip, c->nce_ws, c->nce_scale, c->g_out,
+    nce_out_rows(R, c->nce_N, Vo, Hn, H, clip, c->nce_ws, c->nce_scale, c->g_out,
                  c->g_out_words, c->g_out_n, c->nonfinite, st);
     c->launches += 8;
   }
@@ -1281,6 +1353,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_join, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_hfinal, cudaEventDisableTiming));
+    DL_CUDA(cudaEventCreateWithFlags(&c->ev_dh, cudaEventDisableTiming));
+    DL_CUDA(cudaEventCreateWithFlags(&c->ev_rs, cudaEventDisableTiming));
     c->w_in = dalloc<float>(V * H);
     c->w_rec = dalloc<float>(H * H);
     c->m_rec = dalloc<float>(H * H);
@@ -1337,7 +1411,8 @@ int dl_destroy(dl_ctx* c) {
                   c->nce_ws.seg_start, c->nce_ws.order_pos, c->g_out_words, c->g_out_n,
                   c->nz_prob_d, c->nz_alias_d, c->raw_d, c->pos_of_d, c->first_d,
                   c->rowsq, c->tgt_loc, c->lse_loc, c->lse_all, c->rms_cnt, c->dS, c->xf_lse,
-                  c->xf_sc, c->xpose_a, c->xpose_b};
+                  c->xf_sc, c->xpose_a, c->xpose_b, c->ng_y, c->ng_y_rb, c->ng_w, c->ng_w_rb,
+                  c->ng_hs, c->ng_hs_rb, c->ng_dh};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1345,6 +1420,8 @@ int dl_destroy(dl_ctx* c) {
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
+  if (c->ev_dh) cudaEventDestroy(c->ev_dh);
+  if (c->ev_rs) cudaEventDestroy(c->ev_rs);
   for (int i = 0; i < 2; ++i) {
     if (c->raw_pin[i]) cudaFreeHost(c->raw_pin[i]);
     if (c->raw_ev[i]) cudaEventDestroy(c->raw_ev[i]);
@@ -2040,7 +2117,8 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
     DL_CUDA(cudaMemsetAsync(c->d_pos, 0, 8, c->st));
     DL_CUDA(cudaMemsetAsync(c->d_skipped, 0, 8, c->st));
     const bool nce = c->loss_mode == 0;
-    DL_REQUIRE(!nce || c->comm == nullptr, 1, "NCE mode: multi-rank training is not supported");
+    DL_REQUIRE(!nce || c->comm == nullptr || !c->vshard, 1,
+               "NCE mode: not with a vocabulary-sharded output layer");
     const bool graphs = c->use_graph && !c->profiling && c->comm == nullptr && !nce;
     presize(c, c->unroll, c->minibatch);
     if (nce) {
@@ -2048,36 +2126,52 @@ int dl_trainer_run(dl_ctx* c, int64_t first, int64_t count, double eta, double* 
       // device builds from the resident stream: the host mirrors the same
       // schedule (cursors, window counter; trainer.hpp:374-406) to draw
       // them, window by window, in the reference's order
+      // With data-parallel ranks the draws cover the global window (every
+      // rank's streams, in the reference's (t, global stream, sample) order)
+      // and every rank makes all of them: the generator stays identical
+      // across ranks, as the reference's single Trainer::rng_.
       const int64_t B = c->minibatch, T = c->unroll, Nl = (int64_t)c->noffset * B;
-      std::vector<int64_t> cur(Nl);
-      DL_CUDA(cudaMemcpyAsync(cur.data(), c->cursors, Nl * 8, cudaMemcpyDeviceToHost, c->st));
-      DL_CUDA(cudaStreamSynchronize(c->st));
-      std::vector<uint32_t> y(T * B);
-      std::vector<uint8_t> w(T * B);
+      const int64_t G = c->comm ? c->nranks : 1, BG = G * B;
+      ensure_window(c, T, B);
+      std::vector<int64_t> cur(G * Nl);  // [rank][group * B + b]
+      if (G > 1 || c->comm) {
+        int64_t* cur_all = dalloc<int64_t>(G * Nl);
+        c->comm->allgather(c->cursors, cur_all, (size_t)Nl, DType::U64, c->st);
+        DL_CUDA(cudaMemcpyAsync(cur.data(), cur_all, G * Nl * 8, cudaMemcpyDeviceToHost, c->st));
+        DL_CUDA(cudaStreamSynchronize(c->st));
+        cudaFree(cur_all);
+      } else {
+        DL_CUDA(cudaMemcpyAsync(cur.data(), c->cursors, Nl * 8, cudaMemcpyDeviceToHost, c->st));
+        DL_CUDA(cudaStreamSynchronize(c->st));
+      }
+      std::vector<uint32_t> y(T * BG);
+      std::vector<uint8_t> w(T * BG);
       const int64_t L = c->L;
       double host_draw_s = 0.0, host_enqueue_s = 0.0;
       const auto run0 = std::chrono::steady_clock::now();
       for (int64_t i = 0; i < count; ++i) {
         const int64_t s0 = ((first + i) % c->noffset) * B;
         for (int64_t t = 0; t < T; ++t)
-          for (int64_t b = 0; b < B; ++b) {
-            const int64_t pos = cur[s0 + b] + t;
-            y[t * B + b] = c->h_ids[(pos + 1) % L];
-            w[t * B + b] = y[t * B + b] == c->bos ? 0 : 1;
-          }
-        ensure_window(c, T, B);
+          for (int64_t r = 0; r < G; ++r)
+            for (int64_t b = 0; b < B; ++b) {
+              const int64_t pos = cur[r * Nl + s0 + b] + t;
+              const int64_t k = t * BG + r * B + b;
+              y[k] = c->h_ids[(pos + 1) % L];
+              w[k] = y[k] == c->bos ? 0 : 1;
+            }
         const auto h0 = std::chrono::steady_clock::now();
-        nce_prepare(c, T, B, w.data());
+        nce_prepare(c, T, BG, w.data());
         const auto h1 = std::chrono::steady_clock::now();
         trainer_window(c, eta);
         const auto h2 = std::chrono::steady_clock::now();
         host_draw_s += std::chrono::duration<double>(h1 - h0).count();
         host_enqueue_s += std::chrono::duration<double>(h2 - h1).count();
-        for (int64_t b = 0; b < B; ++b) {
-          int64_t v = cur[s0 + b] + T;
-          if (v >= L) v -= L;
-          cur[s0 + b] = v;
-        }
+        for (int64_t r = 0; r < G; ++r)
+          for (int64_t b = 0; b < B; ++b) {
+            int64_t v = cur[r * Nl + s0 + b] + T;
+            if (v >= L) v -= L;
+            cur[r * Nl + s0 + b] = v;
+          }
       }
       if (std::getenv("DL_DEBUG"))
         fprintf(stderr, "[desklm] NCE trainer: %lld windows, host draws %.3f ms/window, "
@@ -2195,6 +2289,7 @@ int dl_set_loss_mode(dl_ctx* c, int mode) {
   c->loss_mode = mode;
   c->have_grads = false;
   drop_graphs(c);
+  if (c->comm) c->capT = c->capB = 0;  // (re)size the NCE gather buffers
   return DL_OK;
 }
 

@@ -353,3 +353,64 @@ def test_rnqz_device_dequantization_bitexact(bits, orc):
     want = orc.bn_sharded_ppl(got, q.act, ids, 8)
     r = bn.bn_sharded_perplexity(m, ids, 8)
     assert r.perplexity == pytest.approx(want["perplexity"], rel=1e-4)
+
+
+@pytest.mark.parametrize("precision,mode", [("fp32", 1), ("bf16", 1), ("fp32", 0), ("bf16", 0)])
+def test_bn_device_epoch_loop_matches_host_schedule(orc, precision, mode):
+    """dl_bn_trainer_run (the epoch's windows built, trained and carried on
+    the device; softmax windows from one CUDA graph) against the host-side
+    schedule driving dl_bn_train_window per window: the same windows in the
+    same order, so logs, parameters, optimiser state, cursors, hidden carry
+    and the generator are bit-identical; then a checkpoint written by one
+    resumes in the other."""
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200 import bottleneck as bn
+    V, H, P = 512, 64, 32
+    tr, va = orc.random_stream_pair(17, V, 6000, 800)
+    params = orc.bn_init_uniform(V, H, P, 4)
+    # (the comparison is between the two schedules, not about convergence:
+    # no divergence stop)
+    cfg = dl.TrainConfig(nstate=H, nproj=P, noffset=3, minibatch=8, unroll=6,
+                         eta=0.02 if mode == 1 else 0.004, mode=mode, nce_k=8, max_epochs=2,
+                         seed=3, divergence_factor=1e30)
+    runs = []
+    for device_loop in (True, False):
+        t = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), tr, va, precision,
+                                 device_loop=device_loop)
+        t.train()
+        runs.append(t)
+    a, b = runs
+    assert [(l.train_loss, l.valid_ppl, l.eta) for l in a.logs] == \
+        [(l.train_loss, l.valid_ppl, l.eta) for l in b.logs]
+    for x, y in zip(a.model.params() + a.model.opt(), b.model.params() + b.model.opt()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.cursors, b.cursors)
+    assert np.array_equal(a.hidden, b.hidden)
+    assert np.array_equal(a.model.rng_state(), b.model.rng_state())
+    blob = a.save_checkpoint()
+    assert blob == b.save_checkpoint()
+    c = bn.BottleneckTrainer(cfg, params, dl.make_vocab(V), tr, va, precision,
+                             device_loop=False)
+    c.load_checkpoint(blob)
+    assert c.save_checkpoint() == blob
+    # one more epoch each from the same state: still identical
+    a.eta = c.eta = 0.01
+    la, lc = a.run_epoch(), c.run_epoch()
+    assert la == lc
+    for x, y in zip(a.model.params(), c.model.params()):
+        assert np.array_equal(x, y)
+
+
+def test_bn_device_epoch_loop_errors():
+    from paper_1502_00512_b200 import DataError, bottleneck as bn
+    m = bn.GpuBottleneck(64, 16, 8, 0, "fp32")
+    with pytest.raises(ValueError):
+        m.trainer_run(0, 1, 0.1)  # not initialised
+    with pytest.raises(ValueError):
+        m.trainer_init(np.arange(10, dtype=np.uint32), 4, 4, 2, 1.0)  # L < N
+    with pytest.raises(DataError):
+        m.trainer_init(np.full(100, 64, np.uint32), 2, 2, 2, 1.0)  # id >= V
+    m.trainer_init(np.arange(100, dtype=np.uint32) % 64, 2, 2, 2, 1.0)
+    with pytest.raises(DataError):
+        m.trainer_set_state(np.full(4, 100, np.int64), np.zeros((4, 16), np.float32))
+    m.close()

@@ -229,6 +229,40 @@ def test_dp_trainer_matches_global_minibatch(orc):
         trainers[0].save_checkpoint()
 
 
+@pytest.mark.parametrize("G", [2, 3])
+def test_dp_nce_trainer_matches_global_minibatch(orc, G):
+    """NCE (LossMode::kNce, the reference's default) under data-parallel
+    ranks: the noise of the global window is drawn in the reference's
+    (t, global stream, sample) order from one generator -- identical on every
+    rank -- so G ranks x minibatch 4 train exactly like one trainer with
+    minibatch 4G (trainer.hpp:53, backprop.hpp:126-156)."""
+    import paper_1502_00512_b200 as dl
+    V, H = 60, 16
+    tr, va = orc.random_stream_pair(23, V, 3016, 400)
+    tr = tr[:3000]
+    params = orc.init_uniform(V, H, 11)
+    kw = dict(nstate=H, noffset=3, unroll=5, eta=0.05, max_epochs=2, mode=0, nce_k=5,
+              noise_floor=1e-3, divergence_factor=1e9)
+    single = dl.Trainer(dl.TrainConfig(minibatch=G * 4, **kw), params, dl.make_vocab(V), tr, va,
+                        "fp32")
+    single.train()
+    group = dl.LocalGroup(G)
+    trainers = [dl.Trainer(dl.TrainConfig(minibatch=4, **kw), params, dl.make_vocab(V), tr, va,
+                           "fp32", comm=(group, G, r)) for r in range(G)]
+    with ThreadPoolExecutor(G) as ex:
+        list(ex.map(lambda t: t.train(), trainers))
+    for t in trainers:
+        assert len(t.logs) == len(single.logs)
+        for a, b in zip(t.logs, single.logs):
+            tol = 1e-4 if a.epoch == 1 else 1e-2
+            assert a.train_loss == pytest.approx(b.train_loss, rel=tol)
+            assert a.valid_ppl == pytest.approx(b.valid_ppl, rel=tol)
+        # the generator advanced by the global window's draws on every rank
+        assert np.array_equal(t.model.rng_state(), single.model.rng_state())
+    for a, b in zip(trainers[0].params(), trainers[-1].params()):
+        assert np.array_equal(a, b)  # replicas stay bit-identical
+
+
 @pytest.mark.parametrize("G,precision", [(2, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])
 def test_dp_vocab_parallel_window_matches_global_window(orc, G, precision):
     """Data-parallel streams + vocabulary-parallel output layer

@@ -33,15 +33,28 @@ def _train(dl, params, ids, V, H, precision, mode, windows=12):
     return out
 
 
-@pytest.mark.parametrize("precision,mode", [("fp32", "dense"), ("fp32", "dp"),
-                                            ("bf16", "dense"), ("bf16", "dp")])
-def test_one_rank_nccl_matches_single_context(orc, precision, mode):
-    import paper_1502_00512_b200 as dl
+def _setup(orc):
     V, H = 4096, 256
     ids = orc.random_stream(71, V, 40000)[:40000]
     rng = np.random.default_rng(5)
     params = tuple(rng.uniform(-0.1, 0.1, s).astype(np.float32) for s in ((V, H), (H, H), (V, H)))
+    return V, H, ids, params
+
+
+@pytest.mark.parametrize("precision,mode", [("fp32", "dense"), ("fp32", "dp"),
+                                            ("bf16", "dense"), ("bf16", "dp")])
+def test_one_rank_nccl_matches_single_context(orc, monkeypatch, precision, mode):
+    import paper_1502_00512_b200 as dl
+    V, H, ids, params = _setup(orc)
+    if precision == "bf16" and mode == "dense":
+        # dense DP sums a bf16 dW_out: the single context's matching path is
+        # the unfused bf16 gradient + row sums (env read at context creation)
+        for k in ("DL_FUSE_OUT", "DL_FORK_OUT", "DL_FORK_LATE"):
+            monkeypatch.setenv(k, "0")
     ref = _train(dl, params, ids, V, H, precision, None)
+    monkeypatch.delenv("DL_FUSE_OUT", raising=False)
+    monkeypatch.delenv("DL_FORK_OUT", raising=False)
+    monkeypatch.delenv("DL_FORK_LATE", raising=False)
     got = _train(dl, params, ids, V, H, precision, mode)
     assert got[1] == ref[1] == 0
     # fp32: identity exchanges, the same sums (the gathered W_in rows and the
@@ -59,6 +72,22 @@ def test_one_rank_nccl_matches_single_context(orc, precision, mode):
             rel = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
             assert rel <= 1e-2, rel
     assert np.array_equal(got[4][0], ref[4][0])  # cursors: the same schedule
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_dense_dp_chunked_allreduce_is_exact(orc, monkeypatch, precision):
+    """The dense-DP dW_out GEMM + allreduce in V chunks (the allreduce of
+    chunk i under the GEMM of chunk i+1) gives the unchunked result bit for
+    bit: every element is the same dot product and the same rank sum."""
+    import paper_1502_00512_b200 as dl
+    V, H, ids, params = _setup(orc)
+    monkeypatch.setenv("DL_DP_CHUNKS", "1")
+    one = _train(dl, params, ids, V, H, precision, "dense", windows=6)
+    monkeypatch.setenv("DL_DP_CHUNKS", "5")
+    five = _train(dl, params, ids, V, H, precision, "dense", windows=6)
+    assert one[0] == five[0]
+    for a, b in zip(one[2] + one[3], five[2] + five[3]):
+        assert np.array_equal(a, b)
 
 
 def test_one_rank_nccl_scoring_and_window(orc):
