@@ -235,9 +235,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                       // 2 no proxy fence, 4 no cross-CTA handshake, 8 no smem pass,
                       // 16 no dS stores, 32 producer ignores `stored`
 #endif
-#ifndef DL_RMS_PUB
-#define DL_RMS_PUB 1  // fused dW_out: an 11th warp publishes the row sums (fence + spin off
-#endif                // the epilogue warps, whose fences would drain their pass-2 stores)
 #ifndef DL_RMS_PREFETCH
 #define DL_RMS_PREFETCH 0  // L2 prefetch of the next tile's A (dS^T) in the fused kernel
 #endif                     // (measured: 0.564 vs 0.527 ms at C3 -- off)
@@ -254,13 +251,7 @@ struct Cfg2 {
   static constexpr int EPI_OFF = STAGES * STAGE + (BAR_BYTES + 255) / 256 * 256;
   static constexpr int EPI_CHUNK_BYTES = 32 * 32 * 4;
   static constexpr int EPI_WARP_BYTES = RMS ? DL_RMS_RING * EPI_CHUNK_BYTES : 0;
-  // (fused rmsprop, publisher warp) the CTA's 128 row sums (f64), the rows'
-  // steps (f32), two barriers: row sums ready, steps ready
-  static constexpr bool PUB = RMS && DL_RMS_PUB;
-  static constexpr int PUB_OFF = EPI_OFF + kEpiWarps * EPI_WARP_BYTES;
-  static constexpr int PUB_BYTES = PUB ? 128 * 8 + 128 * 4 + 16 : 0;
-  static constexpr int THREADS = kThreads + (PUB ? 32 : 0);
-  static constexpr int SMEM = PUB_OFF + PUB_BYTES + 1024;
+  static constexpr int SMEM = EPI_OFF + kEpiWarps * EPI_WARP_BYTES + 1024;
 };
 static_assert(Cfg2<true>::SMEM <= 227 * 1024 && Cfg2<false>::SMEM <= 227 * 1024,
               "pair kernel shared memory");
@@ -560,165 +551,6 @@ __device__ __forceinline__ void epilogue_rms(const GemmDesc& g, uint32_t taddr, 
   if (tr && lane == 0) tr[3] = gtimer_ns();
 }
 
-// Publisher variant of epilogue_rms (DL_RMS_PUB): pass 1 adds the warp's
-// per-row partial (its 128 columns) into the CTA's shared row sums (two
-// exact f64 additions onto zero: order-free) and arrives on `rs_full`; the
-// publisher warp (rms_publisher) exchanges the block's row sums through
-// global memory and hands back each row's step on `step_ready` (phase =
-// tile parity).  The epilogue warps never fence: a fence here would wait
-// for the previous tile's pass-2 stores.
-__device__ __forceinline__ void epilogue_rms_pub(const GemmDesc& g, uint32_t taddr, int m,
-                                                 int nt, int row, int c0, uint32_t ring,
-                                                 double* sqs,
-                                                 const float* steps, uint32_t rs_full,
-                                                 uint32_t step_ready, uint32_t par) {
-  const int lane = threadIdx.x % 32;
-  const int rbase = m - lane;
-  const int cr = lane >> 3, cu = lane & 7;
-  const int64_t col0 = static_cast<int64_t>(nt) * 256 + c0 * 32 + 4 * cu;
-  auto issue = [&](int k, uint32_t buf) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rr = 4 * i + cr;
-      if (rbase + rr < g.M)
-        cp_async16(buf + chunk_off(rr, cu),
-                   g.rms_w + static_cast<int64_t>(rbase + rr) * g.ldc + col0 + k * 32);
-    }
-    cp_async_commit();
-  };
-  double sq = 0.0;
-#pragma unroll 1
-  for (int c = c0; c < c0 + kRmsChunks; c += 2) {
-    uint32_t r0[32], r1[32];
-    tmem_ld32_async(taddr + c * 32, r0);
-    tmem_ld32_async(taddr + (c + 1) * 32, r1);
-    tmem_wait_ld();
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x0 = clip1(__uint_as_float(r0[j]), g.clip);
-      const float x1 = clip1(__uint_as_float(r1[j]), g.clip);
-      s0 = fmaf(x0, x0, s0);
-      s1 = fmaf(x1, x1, s1);
-    }
-    sq += (double)s0;
-    sq += (double)s1;
-  }
-  atomicAdd(sqs + row, sq);
-  __syncwarp();
-  if (lane == 0) mbar_arrive(rs_full);
-  // the master's chunks load while the publisher exchanges the row sums
-#pragma unroll
-  for (int k = 0; k < DL_RMS_RING; ++k) issue(k, ring + k * 4096);
-  mbar_wait(step_ready, par);
-  const float step = steps[row];
-#pragma unroll 1
-  for (int k = 0; k < kRmsChunks; ++k) {
-    const uint32_t buf = ring + (k % DL_RMS_RING) * 4096;
-    if (kRmsChunks - 1 - k >= DL_RMS_RING - 1) cp_async_wait<DL_RMS_RING - 1>();
-    else if (kRmsChunks - 1 - k == 2) cp_async_wait<2>();
-    else if (kRmsChunks - 1 - k == 1) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncwarp();
-    float v[32];
-    tmem_ld32(taddr + (c0 + k) * 32, v);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t a = buf + chunk_off(lane, u);
-      float4 w = ld_shared_v4(a);
-      w.x -= step * clip1(v[4 * u + 0], g.clip);
-      w.y -= step * clip1(v[4 * u + 1], g.clip);
-      w.z -= step * clip1(v[4 * u + 2], g.clip);
-      w.w -= step * clip1(v[4 * u + 3], g.clip);
-      st_shared_v4(a, w);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rr = 4 * i + cr;
-      const float4 w = ld_shared_v4(buf + chunk_off(rr, cu));
-      if (rbase + rr < g.M) {
-        const int64_t off = static_cast<int64_t>(rbase + rr) * g.ldc + col0 + k * 32;
-        *reinterpret_cast<float4*>(g.rms_w + off) = w;
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(w.x, w.y);
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(w.z, w.w);
-        uint2 q;
-        q.x = *reinterpret_cast<uint32_t*>(&p0);
-        q.y = *reinterpret_cast<uint32_t*>(&p1);
-        *reinterpret_cast<uint2*>(g.rms_wb + off) = q;
-      }
-    }
-    __syncwarp();
-    if (k + DL_RMS_RING < kRmsChunks) issue(k + DL_RMS_RING, buf);
-  }
-}
-
-// The publisher warp of the fused dW_out + rmsprop kernel: per tile, the
-// CTA's 128 row sums (one partial per row and N tile, rowsq[nt][m]) go to
-// global memory, one release-increment of the M block's counter, a spin
-// until the block's 2 x n_tiles CTAs have published, then each row's
-// rmsprop accumulator m' = rho m + (1 - rho) mean(g^2) and step
-// eta / sqrt(m' + eps) (rmsprop.hpp:94-107) into shared memory.  m is read
-// before this CTA's arrival; the N-tile-0 pair writes m' only after every
-// pair of the block has arrived.
-__device__ __forceinline__ void rms_publisher(const GemmDesc& g, const Sched& sc, int pair,
-                                              int npairs, uint32_t rank, double* sqs,
-                                              float* steps, uint32_t rs_full,
-                                              uint32_t step_ready) {
-  const int lane = threadIdx.x % 32;
-  const int total = sc.m_tiles * sc.n_tiles * sc.k_splits;
-  const unsigned target = 2u * sc.n_tiles;
-  int it = 0;
-  for (int u = pair; u < total; u += npairs, ++it) {
-    int mt, nt, kb0, kb1;
-    sc.decode(u, mt, nt, kb0, kb1);
-    int ms[4];
-    float mold[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      ms[j] = mt * 256 + (int)rank * 128 + 32 * j + lane;
-      mold[j] = ms[j] < g.M ? g.rms_m[ms[j]] : 0.f;
-    }
-    mbar_wait(rs_full, it & 1);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double v = sqs[32 * j + lane];
-      sqs[32 * j + lane] = 0.0;
-      if (ms[j] < g.M) g.rowsq[static_cast<int64_t>(nt) * g.M + ms[j]] = v;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      atomicAdd(g.rms_cnt + mt, 1u);
-      // bounded: the block's other pairs are co-resident by construction
-      // (launch2 checks cudaOccupancyMaxActiveClusters); if that is ever
-      // violated the kernel traps -- a loud launch failure, not a hang
-      long spins = 0;
-      while (ld_relaxed(g.rms_cnt + mt) < target) {
-        __nanosleep(32);
-        if (++spins > (1l << 27)) __trap();
-      }
-      ld_acquire_u32(g.rms_cnt + mt);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float step = 0.f;
-      if (ms[j] < g.M) {
-        double tot = 0.0;
-        for (int k = 0; k < sc.n_tiles; ++k)
-          tot += __ldcg(g.rowsq + static_cast<int64_t>(k) * g.M + ms[j]);
-        const float mw = (float)(g.rho * (double)mold[j] + (1.0 - g.rho) * (tot / (double)g.N));
-        step = (float)(g.eta / sqrt((double)mw + g.eps));
-        if (nt == 0) g.rms_m[ms[j]] = mw;
-      }
-      steps[32 * j + lane] = step;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(step_ready);
-  }
-}
-
 // XF: the A tile (bf16 logits, K-major) is turned into dS in shared memory
 // by the epilogue warps before the MMAs read it (GemmDesc::xf): the A load
 // completes on a CTA-local barrier (afull), the eight epilogue warps of both
@@ -729,7 +561,7 @@ __device__ __forceinline__ void rms_publisher(const GemmDesc& g, const Sched& sc
 // blocks, then drain its accumulator, then move on (the dh GEMM has one or
 // two long-K tiles per pair).
 template <bool A_MN, bool B_MN, bool RMS, bool XF = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<RMS>::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, GemmDesc g, Sched sc) {
   using C = Cfg2<RMS>;
@@ -754,12 +586,6 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (threadIdx.x == 32) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(tfull(a), 1); mbar_init(tempty(a), 2 * kEpiWarps); }
-    if constexpr (C::PUB) {
-      mbar_init(sbase + C::PUB_OFF + 1536, kEpiWarps);  // row sums in shared memory
-      mbar_init(sbase + C::PUB_OFF + 1544, 1);          // steps in shared memory
-      double* sqs = reinterpret_cast<double*>(smem + C::PUB_OFF);
-      for (int r = 0; r < 128; ++r) sqs[r] = 0.0;
-    }
     if (XF)
       for (int s = 0; s < C::STAGES; ++s) {
         mbar_init(afull(s), 1);
@@ -878,11 +704,6 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (C::PUB && warp == 2 + kEpiWarps) {
-    if constexpr (C::PUB)
-      rms_publisher(g, sc, pair, npairs, rank, reinterpret_cast<double*>(smem + C::PUB_OFF),
-                    reinterpret_cast<float*>(smem + C::PUB_OFF + 1024), sbase + C::PUB_OFF + 1536,
-                    sbase + C::PUB_OFF + 1544);
   } else {
     const int quarter = warp % 4, half = (warp - 2) / 4;
     const int row = quarter * 32 + lane;
@@ -998,13 +819,7 @@ tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (tr && lane == 0) tr[0] = gtimer_ns();
       const int m = mt * 256 + (int)rank * 128 + row;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256;
-      if constexpr (C::PUB)
-        epilogue_rms_pub(g, taddr, m, nt, row, half * 4,
-                         sbase + C::EPI_OFF + (warp - 2) * C::EPI_WARP_BYTES,
-                         reinterpret_cast<double*>(smem + C::PUB_OFF),
-                         reinterpret_cast<const float*>(smem + C::PUB_OFF + 1024),
-                         sbase + C::PUB_OFF + 1536, sbase + C::PUB_OFF + 1544, it & 1);
-      else if constexpr (RMS)
+      if constexpr (RMS)
         epilogue_rms(g, taddr, m, mt, nt, half, half * 4, 2 * sc.n_tiles, 16u * sc.n_tiles,
                      sbase + C::EPI_OFF + (warp - 2) * C::EPI_WARP_BYTES, tr,
                      (arr && it < 32) ? arr + it : nullptr);
@@ -1553,7 +1368,7 @@ int max_pairs() {
                                  Cfg2<RMS>::SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kNumSMs, 1, 1);
-    cfg.blockDim = dim3(Cfg2<RMS>::THREADS, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = Cfg2<RMS>::SMEM;
     int k = 0;
     DL_CUDA(cudaOccupancyMaxActiveClusters(&k, kern, &cfg));
@@ -1596,7 +1411,7 @@ void launch2(const GemmDesc& g, cudaStream_t st) {
   }
   // xf: the dS store map has the A map's geometry over xf_out
   const CUtensorMap td = XF && g.xf_out ? make_map(g.xf_out, g.M, g.K, g.lda, 16) : ta;
-  kern<<<2 * pairs, C::THREADS, C::SMEM, st>>>(ta, tb, td, g, sc);
+  kern<<<2 * pairs, kThreads, C::SMEM, st>>>(ta, tb, td, g, sc);
   DL_CUDA(cudaGetLastError());
 }
 
