@@ -1364,9 +1364,11 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->v0 = 0;
     alloc_output(c);
     c->g_in_n = dalloc<int>(1);
-    c->nonfinite = dalloc<int>(1);
-    c->d_loss = dalloc<double>(1);
-    c->d_pos = dalloc<unsigned long long>(1);
+    // loss, positions and the non-finite flag side by side: a window's
+    // results come back in one 24-byte copy
+    c->d_loss = dalloc<double>(4);
+    c->d_pos = reinterpret_cast<unsigned long long*>(c->d_loss + 1);
+    c->nonfinite = reinterpret_cast<int*>(c->d_loss + 2);
     c->d_skipped = dalloc<unsigned long long>(1);
     c->bar_counter = dalloc<unsigned>(256);  // rec_tc.cu kRecCounters
     c->win_loss = dalloc<double>(2);
@@ -1399,9 +1401,9 @@ int dl_destroy(dl_ctx* c) {
   delete c->comm;
   void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->w_out_bf_next, c->m_rec, c->m_in,
                   c->m_out, c->g_rec, c->g_out, c->g_in_rows, c->g_in_words, c->g_in_n,
-                  c->nonfinite, c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
+                  c->htape, c->htape_bf, c->x_d, c->y_d, c->w_d, c->S, c->part,
                   c->tgt_logit, c->loss_row, c->logp_row, c->dh_out, c->dpre, c->dpre_bf,
-                  c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss, c->d_pos,
+                  c->splitws, c->ews.seg_start, c->ews.order_pos, c->d_loss,
                   c->d_skipped, c->h0_d, c->ids, c->cursors, c->hidden, c->win_counter,
                   c->win_loss, c->x_all, c->dpre_all, c->bar_counter, c->g_out_bf,
                   c->hs_all_bf, c->hs_all, c->y_all, c->w_all, c->dh_all,
@@ -1538,11 +1540,10 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
     } else {
       run_window(c, T, B, loss_scale, clip, grads);
     }
-    struct { double l; unsigned long long p; int bad; } res;
-    DL_CUDA(cudaMemcpyAsync(&res.l, c->d_loss, 8, cudaMemcpyDeviceToHost, c->st));
-    DL_CUDA(cudaMemcpyAsync(&res.p, c->d_pos, 8, cudaMemcpyDeviceToHost, c->st));
-    if (eta > 0.0)
-      DL_CUDA(cudaMemcpyAsync(&res.bad, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->st));
+    // loss, positions, non-finite flag: adjacent on the device (dl_create)
+    struct { double l; unsigned long long p; int bad; int pad; } res{};
+    static_assert(sizeof(res) == 24, "result block layout");
+    DL_CUDA(cudaMemcpyAsync(&res, c->d_loss, eta > 0.0 ? 20 : 16, cudaMemcpyDeviceToHost, c->st));
     // h_final is final after the forward recurrence: its D2H runs on the
     // side stream, under the rest of the window
     if (h_final) {

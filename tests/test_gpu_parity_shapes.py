@@ -9,9 +9,10 @@ the compiled reference), never with another GPU path:
 * fp32 mode, one window: loss, h_final, dW_in, dW_rec, dW_out and the
   rmsprop step within 1e-4 relative (+ 1e-4 x max-abs floor for
   near-cancelling sums), backprop.hpp:76-222, rmsprop.hpp:113-133;
-* bf16 mode, one training window through dl_train_window at the C3 shape:
-  the fused dW_out + dense rmsprop epilogue (per-row sums of squares over all
-  eight N-tiles of an M block) against the oracle's rmsprop_update applied to
+* bf16 mode, one training window through dl_train_window at the C3 shape
+  (and at the C4 width, H = 4,096): the fused dW_out + dense rmsprop
+  epilogue (per-row sums of squares over all eight / sixteen N-tiles of an
+  M block) against the oracle's rmsprop_update applied to
   the same device gradient (m_out 1e-6 relative, W_out within a few ulps of
   the step), the other updates <= 1 ulp, and the bf16 gradients against the
   fp32 oracle's;
@@ -108,12 +109,15 @@ def test_fp32_window_and_update_at_c2_c3(orc, H, precision):
         assert ok, (name, e)
 
 
-def test_bf16_fused_window_update_at_c3(orc):
+@pytest.mark.parametrize("V,H", [(64000, 2048), (16384, 4096)])
+def test_bf16_fused_window_update_at_c3(orc, V, H):
     """dl_train_window in bf16 mode at V=64,000, H=2,048: the dW_out GEMM
     with the dense W_out rmsprop fused into its epilogue (72 CTA pairs, eight
-    N-tiles per 256-row block exchanging per-row sums of squares)."""
+    N-tiles per 256-row block exchanging per-row sums of squares); and at the
+    C4 width H = 4,096 (64 pairs, sixteen N-tiles per block, the persistent
+    recurrence at H = 4,096) on a 16,384-word vocabulary."""
     import paper_1502_00512_b200 as dl
-    V, H, T, B = 64000, 2048, 4, 64  # TB = 256: the dh / logits GEMMs on pair tiles
+    T, B = 4, 64  # TB = 256: the dh / logits GEMMs on pair tiles
     rng = np.random.default_rng(3)
     params = make_params(V, H, 33)
     x, y, w = make_window(rng, T, B, V)
