@@ -110,6 +110,19 @@ struct GemmDesc {
   float2* part;          // [n_tiles][M]
   const uint32_t* tgt;   // [M] target column per row
   float* tgt_logit;      // [M]
+  // shifted-exponential logits (bf16 trainer path, "pfac"): with shift set
+  // the epilogue stores E = 2^(min((s - shift[r]) log2 e, 100)) in bf16
+  // instead of s, and the partials become (tile max of s, sum of E)
+  const float* shift;
+  // fp32 epilogue: row r of the product is multiplied by row_scale[r]
+  // (the dh GEMM over E: dS = diag(row_scale) E)
+  const float* row_scale;
+  // + row_resid[r] * resid_w[resid_idx[r]][n] (bf16 rows, ld = N): the part
+  // of the target column's dS that E' rounded away (k_pfac_rows), so dh's
+  // dominant term is formed in fp32
+  const float* row_resid;
+  const uint32_t* resid_idx;
+  const bf16* resid_w;
   int raster;            // 0: M-tiles fastest, 1: N-tiles fastest
   int no_pair;           // 1: keep the single-CTA kernel (no cta_group::2 tiles)
   // bf16 gradient epilogue (dW_out in throughput mode): clipped values to Cb

@@ -372,16 +372,6 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ float4 ld_shared_v4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -897,11 +887,34 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
         if (mvalid && g.rowsq) g.rowsq[static_cast<int64_t>(sub) * g.M + m] = sq;
       } else if (!g.logits) {
         float* Crow = g.C + split * g.split_stride + static_cast<int64_t>(m) * g.ldc;
+        const float rs = (g.row_scale && mvalid) ? g.row_scale[m] : 1.f;
+        const float rr = (g.row_resid && mvalid && split == 0) ? g.row_resid[m] : 0.f;  // once over splits
+        const bf16* rw = rr != 0.f ? g.resid_w + static_cast<int64_t>(g.resid_idx[m]) * g.N : nullptr;
 #pragma unroll 1
         for (int c = c0; c < c1; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           const int n0 = nt * BN + c * 32;
+          if (g.row_scale) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= rs;
+          }
+          if (rw && n0 + 32 <= g.N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = *reinterpret_cast<const uint4*>(rw + n0 + 8 * q);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                v[8 * q + 2 * e] = fmaf(rr, f.x, v[8 * q + 2 * e]);
+                v[8 * q + 2 * e + 1] = fmaf(rr, f.y, v[8 * q + 2 * e + 1]);
+              }
+            }
+          } else if (rw) {
+            for (int j = 0; j < 32 && n0 + j < g.N; ++j)
+              v[j] = fmaf(rr, __bfloat162float(rw[n0 + j]), v[j]);
+          }
           if (g.do_clip) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -927,6 +940,63 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
         bool thit = false;
         const int tg = mvalid ? static_cast<int>(g.tgt[m]) : -1;
         bf16* Srow = g.S ? g.S + static_cast<int64_t>(m) * g.lds : nullptr;
+        if (g.shift) {
+          // shifted exponentials E = e^(s - shift) (bf16) replace the logits:
+          // dS = row_scale * E with row_scale = scale e^(shift - lse) comes
+          // out of the row's lse alone (k_pfac_rows), so no pass over the
+          // logits after this GEMM.  The exponent is capped at 2^100 (the
+          // row is then recomputed with shift = its max, k_pfac_rows).
+          const float sb = (mvalid ? g.shift[m] : 0.f) * kLog2e;
+#pragma unroll 1
+          for (int c = c0; c < c1; ++c) {
+            float v[32];
+            tmem_ld32(taddr + c * 32, v);
+            const int n0 = nt * BN + c * 32;
+            const bool whole = n0 + 32 <= g.N;
+            if (static_cast<unsigned>(tg - n0) < 32u) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j == tg) tval = v[j];
+              thit = true;
+            }
+            float cmax = -INFINITY, part_sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const bool in = whole || n0 + j < g.N;
+              cmax = in ? fmaxf(cmax, v[j]) : cmax;
+              v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
+              part_sum += in ? v[j] : 0.f;
+            }
+            mrun = fmaxf(mrun, cmax);
+            srun += part_sum;
+            if (!mvalid) continue;
+            if (whole && (g.lds % 8) == 0) {
+              uint4* dst = reinterpret_cast<uint4*>(Srow + n0);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 q;
+                __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * j + 0], v[8 * j + 1]);
+                __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+                __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+                __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+                q.x = *reinterpret_cast<uint32_t*>(&p0);
+                q.y = *reinterpret_cast<uint32_t*>(&p1);
+                q.z = *reinterpret_cast<uint32_t*>(&p2);
+                q.w = *reinterpret_cast<uint32_t*>(&p3);
+                dst[j] = q;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < g.N) Srow[n0 + j] = __float2bfloat16_rn(v[j]);
+            }
+          }
+          if (mvalid) {
+            g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(mrun, srun);
+            if (thit) g.tgt_logit[m] = tval;
+          }
+          return;
+        }
 #pragma unroll 1
         for (int c = c0; c < c1; ++c) {
           float v[32];

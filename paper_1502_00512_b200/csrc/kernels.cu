@@ -331,6 +331,183 @@ k_lse_rows_bf16(int64_t M, const float2* __restrict__ part, int n_tiles,
   }
 }
 
+// ------------------------------------------- shifted-exponential softmax
+// The bf16 trainer's output layer without a pass over the logits
+// (backprop.hpp:157-189 restated): the logits GEMM epilogue stores
+// E = e^(s - c_r) in bf16 for a per-row shift c_r fixed before the GEMM, so
+//   p = e^(s - lse) = E * e^(c_r - lse)   and   dS = scale (p - 1[y])
+//                                              = diag(sigma) E'
+// with sigma_r = scale e^(c_r - lse_r) and E' = E except at the target
+// column, which k_pfac_rows overwrites with (p_y - 1) / e^(c_r - lse_r)
+// (computed from the fp32 target logit, not from the rounded E).  The row
+// factor then moves out of both gradient GEMMs: dh = diag(sigma) (E' W_out)
+// (the dh epilogue's row_scale) and dW_out = E'^T (diag(sigma) Hs) (its B
+// operand scaled once, B x H instead of TB x V).
+//
+// c_r = the row's target logit (dot of the bf16 operands the GEMM uses):
+// E then stays within bf16 range for every logit less than ~69 nats above
+// the target's, i.e. unless the position's loss exceeds that; a row whose
+// largest logit is more than kPfacRepairNats above c_r is recomputed here
+// with c_r = that maximum (a block-wide GEMV over W_out -- slow, and only in
+// that pathological case).
+__global__ void __launch_bounds__(256)
+k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t H, int64_t M,
+               const uint32_t* __restrict__ tgt, int64_t V, float* __restrict__ shift) {
+  const int64_t r = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= M) return;
+  const uint32_t y = tgt[r];
+  float acc = 0.f;
+  if (y < V) {
+    const bf16* a = hs + r * H;
+    const bf16* b = w + (int64_t)y * H;
+    if ((H % 8) == 0) {
+      for (int64_t k = 8 * lane; k < H; k += 256) {
+        const uint4 qa = *reinterpret_cast<const uint4*>(a + k);
+        const uint4 qb = *reinterpret_cast<const uint4*>(b + k);
+        const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&qa);
+        const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&qb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
+          acc = fmaf(fa.x, fb.x, acc);
+          acc = fmaf(fa.y, fb.y, acc);
+        }
+      }
+    } else {
+      for (int64_t k = lane; k < H; k += 32)
+        acc = fmaf(__bfloat162float(a[k]), __bfloat162float(b[k]), acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) shift[r] = acc;
+}
+
+constexpr int kPfacThreads = 256;
+
+// The row's log-sum-exp relative to its shift from the logits epilogue's
+// partials; a row with a logit more than repair_nats above the shift is
+// recomputed with the shift = its maximum (E rewritten).  Block-uniform.
+__device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t M, int64_t H, int64_t r,
+                             const float2* __restrict__ part, int n_tiles, double& c, double& z,
+                             const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
+                             float repair_nats, int* repaired, double* red) {
+  double mx = -INFINITY;
+  z = 0.0;
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) {
+    const float2 p = part[(int64_t)t * M + r];
+    mx = fmax(mx, (double)p.x);
+    z += (double)p.y;
+  }
+  mx = block_max_d<kPfacThreads>(mx, red);
+  z = block_sum_d<kPfacThreads>(z, red);
+  if (mx - c > (double)repair_nats) {
+    // rare: some logit is far above the target's -- recompute the row's E
+    // with c = the row maximum (logits as the GEMM forms them: bf16
+    // operands, fp32 accumulation)
+    c = mx;
+    const float cb = (float)c;
+    const bf16* a = hs_bf + r * H;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    double zz = 0.0;
+    for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
+      const bf16* b = w + v * H;
+      float acc = 0.f;
+      for (int64_t k = lane; k < H; k += 32)
+        acc = fmaf(__bfloat162float(a[k]), __bfloat162float(b[k]), acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const float e = expf(acc - cb);
+      if (lane == 0) {
+        erow[v] = __float2bfloat16_rn(e);
+        zz += (double)e;
+      }
+    }
+    z = block_sum_d<kPfacThreads>(zz, red);
+    if (threadIdx.x == 0 && repaired) atomicAdd(repaired, 1);
+  }
+}
+
+// Vocabulary-sharded output layer: this rank's block log-sum-exp (after the
+// repair), exchanged before k_pfac_rows; shift[r] updated when repaired.
+__global__ void __launch_bounds__(kPfacThreads)
+k_pfac_lse(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* __restrict__ part,
+           int n_tiles, const uint8_t* __restrict__ wts, float* __restrict__ shift,
+           double* __restrict__ lse_loc, const bf16* __restrict__ hs_bf,
+           const bf16* __restrict__ w, float repair_nats, int* __restrict__ repaired) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  const bool active = wts == nullptr || wts[r] != 0;
+  double c = (double)shift[r], z;
+  pfac_row_lse(E + r * V, V, M, H, r, part, n_tiles, c, z, hs_bf, w,
+               active ? repair_nats : INFINITY, repaired, red);
+  if (threadIdx.x == 0) {
+    lse_loc[r] = c + log(z);
+    shift[r] = (float)c;
+  }
+}
+
+__global__ void __launch_bounds__(kPfacThreads)
+k_pfac_rows(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* __restrict__ part,
+            int n_tiles, const float* __restrict__ tgt_logit, const uint32_t* __restrict__ tgt,
+            const uint8_t* __restrict__ wts, double scale, double* __restrict__ loss_row,
+            double* __restrict__ logp_row, const float* __restrict__ shift,
+            float* __restrict__ sigma, float* __restrict__ resid, const float* __restrict__ hs,
+            bf16* __restrict__ hs_sc, const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
+            float repair_nats, int* __restrict__ repaired, const double* __restrict__ lse_all,
+            int G) {
+  __shared__ double red[32];
+  const int64_t r = blockIdx.x;
+  const bool active = wts == nullptr || wts[r] != 0;
+  bf16* hrow = hs_sc + r * H;
+  if (!active) {
+    // dS row = 0: sigma = 0 and a zero row of the scaled B operand (E stays
+    // finite: its exponent is capped in the epilogue)
+    if (threadIdx.x == 0) {
+      if (loss_row) loss_row[r] = 0.0;
+      if (logp_row) logp_row[r] = NAN;
+      sigma[r] = 0.f;
+      resid[r] = 0.f;
+    }
+    const bf16 z = __float2bfloat16_rn(0.f);
+    for (int64_t k = threadIdx.x; k < H; k += kPfacThreads) hrow[k] = z;
+    return;
+  }
+  double c = (double)shift[r], lse;
+  bf16* erow = E + r * V;
+  if (lse_all) {
+    lse = lse_of_blocks(lse_all, G, M, r);  // (shift repaired by k_pfac_lse)
+  } else {
+    double z;
+    pfac_row_lse(erow, V, M, H, r, part, n_tiles, c, z, hs_bf, w, repair_nats, repaired, red);
+    lse = c + log(z);
+  }
+  const double sy = (double)tgt_logit[r];
+  const float sg = (float)(scale * exp(c - lse));
+  if (threadIdx.x == 0) {
+    if (loss_row) loss_row[r] = scale * (lse - sy);
+    if (logp_row) logp_row[r] = sy - lse;
+    sigma[r] = sg;
+    // the target column (its owner's block): sigma * E'[y] = scale (p_y - 1);
+    // what the bf16 rounding of E'[y] loses goes to the dh epilogue as resid
+    // (dW_out keeps the rounded value: an error of the order of its bf16 Hs)
+    const uint32_t y = tgt[r];
+    float rsd = 0.f;
+    if (y < V) {
+      const double ds = scale * expm1(sy - lse);
+      const bf16 e = __float2bfloat16_rn(sg > 0.f ? (float)(ds / (double)sg) : 0.f);
+      erow[y] = e;
+      rsd = (float)(ds - (double)sg * (double)__bfloat162float(e));
+    }
+    resid[r] = rsd;
+  }
+  // the dW_out GEMM's B operand: diag(sigma) Hs, rounded once to bf16 (from
+  // the bf16 copy when the fp32 rows are not at hand: gathered windows)
+  for (int64_t k = threadIdx.x; k < H; k += kPfacThreads)
+    hrow[k] = __float2bfloat16_rn(sg * (hs ? hs[r * H + k] : __bfloat162float(hs_bf[r * H + k])));
+}
+
 // Sharded output layer helpers.  Targets inside [v0, v0 + Vo) become local
 // columns, all others ~0u (matches no column).
 __global__ void k_shard_targets(const uint32_t* __restrict__ y, int64_t M, int64_t v0, int64_t Vo,
@@ -1056,6 +1233,29 @@ void lse_rows_bf16(int64_t M, const float2* part, int n_tiles, const float* tgt_
   k_lse_rows_bf16<<<(unsigned)M, kRowThreads, 0, st>>>(M, part, n_tiles, tgt_logit, wts, scale,
                                                        loss_row, logp_row, lse_f, sc_f, lse_all,
                                                        G);
+}
+void target_shift(const bf16* hs, const bf16* w, int64_t H, int64_t M, const uint32_t* tgt,
+                  int64_t V, float* shift, cudaStream_t st) {
+  if (M <= 0) return;
+  k_target_shift<<<(unsigned)((M + 7) / 8), 256, 0, st>>>(hs, w, H, M, tgt, V, shift);
+}
+void pfac_rows(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
+               const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts, double scale,
+               double* loss_row, double* logp_row, const float* shift, float* sigma,
+               float* resid, const float* hs, bf16* hs_sc, const bf16* hs_bf, const bf16* w,
+               float repair_nats, int* repaired, cudaStream_t st, const double* lse_all, int G) {
+  if (M <= 0) return;
+  k_pfac_rows<<<(unsigned)M, kPfacThreads, 0, st>>>(E, V, M, H, part, n_tiles, tgt_logit, tgt,
+                                                    wts, scale, loss_row, logp_row, shift, sigma,
+                                                    resid, hs, hs_sc, hs_bf, w, repair_nats,
+                                                    repaired, lse_all, G);
+}
+void pfac_lse(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
+              const uint8_t* wts, float* shift, double* lse_loc, const bf16* hs_bf, const bf16* w,
+              float repair_nats, int* repaired, cudaStream_t st) {
+  if (M <= 0) return;
+  k_pfac_lse<<<(unsigned)M, kPfacThreads, 0, st>>>(E, V, M, H, part, n_tiles, wts, shift, lse_loc,
+                                                   hs_bf, w, repair_nats, repaired);
 }
 void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
                    cudaStream_t st) {

@@ -32,6 +32,10 @@ namespace tc {
 
 constexpr int kRecThreads = 256;
 constexpr int kRecCounters = 256;  // per-column-tile step counters (PersistParams::counter)
+constexpr int kTrSlots = 8;        // DL_REC_TRACE stamps per step
+#ifndef DL_REC_DIAG
+#define DL_REC_DIAG 0  // timing diagnostics only (wrong results): 1 no MMAs in the persistent kernel
+#endif
 
 struct RecParams {
   int M, N, K;          // rows (streams), H, H
@@ -251,7 +255,7 @@ struct PersistParams {
   float* out;             // fwd: htape (writes step s+1); bwd: dpre (writes step s)
   bf16* outb;
   unsigned* counter;      // [kRecCounters] per column-tile cluster, zeroed before the launch
-  unsigned long long* trace;  // DL_REC_TRACE: [4 CTAs][T][5] %globaltimer stamps, or null
+  unsigned long long* trace;  // DL_REC_TRACE: [4 CTAs][T][kTrSlots] %globaltimer stamps, or null
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -351,12 +355,12 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 
   // trace: CTAs (rank 0, column tiles 0, 8, 16, 24)
   unsigned long long* tr =
-      (p.trace && rank == 0 && nt % 8 == 0 && nt < 32) ? p.trace + (nt / 8) * p.T * 5 : nullptr;
+      (p.trace && rank == 0 && nt % 8 == 0 && nt < 32) ? p.trace + (nt / 8) * p.T * kTrSlots : nullptr;
   for (int j = 0; j < p.T; ++j) {
     const int s = p.mode == 0 ? j : p.T - 1 - j;   // time step written this iteration
     const bool gemm = p.mode == 0 || j > 0;        // bwd t = T-1 has no recurrent term
     const uint32_t ph = (p.mode == 0 ? j : j - 1) & 1;
-    if (tr && threadIdx.x == 0) tr[j * 5 + 0] = gtimer();
+    if (tr && threadIdx.x == 0) tr[j * kTrSlots + 0] = gtimer();
     // epilogue operands do not depend on the recurrence: issue their loads
     // now so they land while this step waits for its inputs
     float4 pre_a[C::NPRE], pre_b[C::NPRE];
@@ -397,7 +401,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           __syncwarp();  // order lane 0's loads after every lane's acquire
         }
         if (lane == 0) {
-          if (tr) tr[j * 5 + 1] = gtimer();
+          if (tr) tr[j * kTrSlots + 1] = gtimer();
           if (j > 0) asm volatile("fence.proxy.async.global;" ::: "memory");
           for (int i = 0; i < p.kbs; ++i) {
             mbar_wait(emptyA(a_stage), a_phase ^ 1);
@@ -406,6 +410,16 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                         arow);
             if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
           }
+          if (tr) tr[j * kTrSlots + 7] = gtimer();
+        }
+      } else if (warp == 2 && lane == 0 && tr) {
+        // (trace) when the first / last k-block of the step has landed
+        int st2 = a_stage;
+        uint32_t ph2 = a_phase;
+        for (int i = 0; i < p.kbs; ++i) {
+          mbar_wait(fullA(st2), ph2);
+          if (i == 0 || i == p.kbs - 1) tr[j * kTrSlots + (i == 0 ? 5 : 6)] = gtimer();
+          if (++st2 == C::NA) { st2 = 0; ph2 ^= 1; }
         }
       } else if (warp == 1 && lane == 0) {
         constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
@@ -423,7 +437,9 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             const uint64_t ad = make_desc(a_s + ks * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b_s + ks * 2048, 8192, 1024)
                                      : make_desc(b_s + ks * 32, 16, 1024);
+#if !(DL_REC_DIAG & 1)
             mma_bf16(tmem, ad, bd, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+#endif
           }
           mma_commit(emptyA(a_stage));
           if (++a_stage == C::NA) { a_stage = 0; a_phase ^= 1; }
@@ -433,7 +449,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       __syncwarp();
       mbar_wait(tfull, ph);
       fence_after();
-      if (tr && threadIdx.x == 64) tr[j * 5 + 2] = gtimer();
+      if (tr && threadIdx.x == 64) tr[j * kTrSlots + 2] = gtimer();
       {
         // the A ring is idle now (all MMAs of the step completed): drain the
         // accumulator into it as this CTA's fp32 partial (peers pull their
@@ -453,7 +469,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       fence_before();
       cluster.sync();
-      if (tr && threadIdx.x == 64) tr[j * 5 + 3] = gtimer();
+      if (tr && threadIdx.x == 64) tr[j * kTrSlots + 3] = gtimer();
     }
     // reduce my row slice over the cluster (rank order) + fused epilogue.
     // Only the bf16 copy feeds the next step (its TMA loads): it is stored
@@ -526,7 +542,7 @@ rec_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     // stores -> visible to their TMA loads)
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
-    if (tr && threadIdx.x == 0) tr[j * 5 + 4] = gtimer();
+    if (tr && threadIdx.x == 0) tr[j * kTrSlots + 4] = gtimer();
     if (threadIdx.x == 0)
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counter + nt) : "memory");
 #pragma unroll
@@ -615,8 +631,8 @@ bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, i
   static unsigned long long* trace = nullptr;
   static const bool tracing = std::getenv("DL_REC_TRACE") != nullptr;
   if (tracing) {
-    if (!trace) DL_CUDA(cudaMalloc(&trace, 4 * 64 * 5 * sizeof(unsigned long long)));
-    DL_CUDA(cudaMemsetAsync(trace, 0, 4 * 64 * 5 * sizeof(unsigned long long), st));
+    if (!trace) DL_CUDA(cudaMalloc(&trace, 4 * 64 * tc::kTrSlots * sizeof(unsigned long long)));
+    DL_CUDA(cudaMemsetAsync(trace, 0, 4 * 64 * tc::kTrSlots * sizeof(unsigned long long), st));
     p.trace = T <= 64 ? trace : nullptr;
   }
   const bool bmn = mode == 1;
@@ -642,27 +658,35 @@ bool rec_window_tc(int mode, int T, int M, int H, int act, const bf16* a_tape, i
   if (ok && p.trace) {
     // per-step phase durations (ns, CTA-averaged): wait, load+mma, reduce
     // (drain + cluster sync), epilogue+publish; and step-to-step period
-    std::vector<unsigned long long> h(4 * T * 5);
+    std::vector<unsigned long long> h(4 * T * tc::kTrSlots);
     DL_CUDA(cudaStreamSynchronize(st));
     DL_CUDA(cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost));
-    double ph[5] = {0, 0, 0, 0, 0};
+    double ph[5] = {0, 0, 0, 0, 0}, ex[3] = {0, 0, 0};
     int n = 0;
     for (int c = 0; c < 4; ++c)
       for (int j = 1; j + 1 < T; ++j) {
-        const unsigned long long* r = &h[(c * T + j) * 5];
-        const unsigned long long* q = &h[(c * T + j + 1) * 5];
+        const unsigned long long* r = &h[(c * T + j) * tc::kTrSlots];
+        const unsigned long long* q = &h[(c * T + j + 1) * tc::kTrSlots];
         if (!r[0] || !r[4] || !q[0]) continue;
         ph[0] += (double)(r[1] - r[0]);
         ph[1] += (double)(r[2] - r[1]);
         ph[2] += (double)(r[3] - r[2]);
         ph[3] += (double)(r[4] - r[3]);
         ph[4] += (double)(q[0] - r[0]);
+        if (r[5] && r[6] && r[7]) {
+          ex[0] += (double)(r[7] - r[1]);  // TMA issue loop
+          ex[1] += (double)(r[5] - r[1]);  // first k-block landed
+          ex[2] += (double)(r[6] - r[1]);  // last k-block landed
+        }
         ++n;
       }
     if (n)
       fprintf(stderr, "[desklm] rec trace mode=%d: wait %.0f  load+mma %.0f  drain+sync %.0f  "
               "epilogue %.0f  period %.0f ns\n", mode, ph[0] / n, ph[1] / n, ph[2] / n,
               ph[3] / n, ph[4] / n);
+    if (n)
+      fprintf(stderr, "[desklm] rec trace mode=%d: after deps: issue loop %.0f  first k-block %.0f  "
+              "last k-block %.0f ns\n", mode, ex[0] / n, ex[1] / n, ex[2] / n);
   }
   return ok;
 }

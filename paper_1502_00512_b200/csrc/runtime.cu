@@ -114,6 +114,16 @@ struct dl_ctx {
   float *xpose_a = nullptr, *xpose_b = nullptr;  // K-major copies of MN-major operands
   size_t xpose_a_cap = 0, xpose_b_cap = 0;
   bool xf_on = false;                // this window's dS is formed in the dh GEMM
+  // bf16 trainer: shifted-exponential softmax (kernels.cu k_pfac_rows) --
+  // the logits GEMM stores E = e^(s - shift), dS = diag(pf_sigma) E'; no
+  // pass over the logits after the GEMM.  DL_PFAC=0 keeps the in-place
+  // softmax rows kernel.  pf_on: this window used it (dh / dW_out follow).
+  bool pfac = true;
+  bool pf_on = false;
+  float *pf_shift = nullptr, *pf_sigma = nullptr, *pf_resid = nullptr;
+  const uint32_t* pf_tgt = nullptr;  // this window's output-row targets
+  bf16* pf_hs = nullptr;     // diag(sigma) Hs in bf16 [MO x H] (dW_out's B operand)
+  int* pf_repaired = nullptr;  // rows recomputed with the row maximum as shift (device counter)
   float2* part = nullptr;
   int part_tiles = 0;
   float* tgt_logit = nullptr;
@@ -355,6 +365,7 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
   fr(c->x_all); fr(c->dpre_all);
   fr(c->hs_all_bf); fr(c->hs_all); fr(c->y_all); fr(c->w_all); fr(c->dh_all);
   fr(c->dS); fr(c->xf_lse); fr(c->xf_sc); fr(c->xpose_a); fr(c->xpose_b);
+  fr(c->pf_shift); fr(c->pf_sigma); fr(c->pf_resid); fr(c->pf_hs);
   fr(c->ng_y); fr(c->ng_y_rb); fr(c->ng_w); fr(c->ng_w_rb); fr(c->ng_hs); fr(c->ng_hs_rb);
   fr(c->ng_dh);
   c->xpose_a_cap = c->xpose_b_cap = 0;
@@ -410,6 +421,12 @@ void ensure_window(dl_ctx* c, int64_t T, int64_t B) {
     c->part_tiles = tc_n_tiles((int)Vo);
     c->part = dalloc<float2>((size_t)c->part_tiles * MO);
     c->tgt_logit = dalloc<float>(MO);
+    if (c->pfac) {
+      c->pf_shift = dalloc<float>(MO);
+      c->pf_sigma = dalloc<float>(MO);
+      c->pf_resid = dalloc<float>(MO);
+      c->pf_hs = dalloc<bf16>(MO * H);
+    }
   } else {
     c->S = dalloc<float>(MO * Vo);
     if (c->tf32x3) {
@@ -568,9 +585,25 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     tgt = c->tgt_loc;
   }
   if (tc(c)) {
+    // shifted-exponential softmax (kernels.cu k_pfac_rows): the shift is
+    // the row's target logit, summed from its owner when the vocabulary is
+    // sharded (each rank's E is then relative to the same shift, until a
+    // rank repairs a row with its own block maximum -- the block lse
+    // exchange carries that)
+    c->pf_on = grads && c->pfac && c->pf_shift != nullptr && !c->xf;
+    float nats = 40.f;
+    if (const char* e = std::getenv("DL_PFAC_REPAIR_NATS")) nats = (float)std::atof(e);
+    if (c->pf_on) {
+      Phase p(c, "softmax");
+      target_shift(hs_bf, c->w_out_bf, H, M, tgt, V, c->pf_shift, c->st);
+      c->pf_tgt = tgt;
+      c->launches++;
+      if (vs) c->comm->allreduce_sum(c->pf_shift, (size_t)M, DType::F32, c->st);
+    }
     GemmDesc g = desc((int)M, (int)V, (int)H, K_MAJOR, hs_bf, H, K_MAJOR, c->w_out_bf, H, nullptr, 0);
     g.logits = 1;
     g.S = grads ? static_cast<bf16*>(c->S) : nullptr;
+    g.shift = c->pf_on ? c->pf_shift : nullptr;
     g.lds = V;
     g.part = c->part;
     g.tgt = tgt;
@@ -586,7 +619,11 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     }
     if (vs) {
       Phase p(c, "vocab_exchange");
-      block_lse_bf16(c->part, c->part_tiles, M, c->lse_loc, c->st);
+      if (c->pf_on)
+        pfac_lse(static_cast<bf16*>(c->S), M, V, H, c->part, c->part_tiles, wts, c->pf_shift,
+                 c->lse_loc, hs_bf, c->w_out_bf, nats, c->pf_repaired, c->st);
+      else
+        block_lse_bf16(c->part, c->part_tiles, M, c->lse_loc, c->st);
       c->launches++;
       c->comm->allgather(c->lse_loc, c->lse_all, (size_t)M, DType::F64, c->st);
       c->comm->allreduce_sum(c->tgt_logit, (size_t)M, DType::F32, c->st);
@@ -594,8 +631,15 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     Phase p(c, "softmax");
     // dS on the fly in the dh GEMM (pair tiles over the whole output-row
     // block): only the rows' lse / loss here
-    c->xf_on = grads && c->dS != nullptr && tc_pair_tiles((int)M, (int)H);
-    if (c->xf_on) {
+    c->xf_on = !c->pf_on && grads && c->dS != nullptr && tc_pair_tiles((int)M, (int)H);
+    if (c->pf_on) {
+      // (the gathered window of the vocabulary-parallel layout has its
+      // hidden states in bf16 only)
+      pfac_rows(static_cast<bf16*>(c->S), M, V, H, c->part, c->part_tiles, c->tgt_logit, tgt, wts,
+                scale, loss_row, logp_row, c->pf_shift, c->pf_sigma, c->pf_resid,
+                c->dpv ? nullptr : hs, c->pf_hs, hs_bf, c->w_out_bf, nats, c->pf_repaired, c->st,
+                vs ? c->lse_all : nullptr, c->nranks);
+    } else if (c->xf_on) {
       c->xf_tgt = tgt;
       lse_rows_bf16(M, c->part, c->part_tiles, c->tgt_logit, wts, scale, loss_row, logp_row,
                     c->xf_lse, c->xf_sc, c->st, vs ? c->lse_all : nullptr, c->nranks);
@@ -756,6 +800,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   const bool dprec = dp || dpv;
   const bool vs = c->comm != nullptr && c->vshard && !dpv;
   const int64_t MO = dpv ? c->nranks * TB : TB;  // output-layer rows
+  c->pf_on = false;  // (set by output_layer for this window)
   if (grads && !dprec) {
     // the W_in gradient's id sort depends on x only: run it on the side
     // stream under the forward recurrence (which leaves SMs free) (joined before embed_rows)
@@ -877,7 +922,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     if (fused) {
       // + the dense rmsprop of every row (rmsprop.hpp:94-107) in the epilogue
       GemmDesc g = desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->xf_on ? c->dS : c->S, Vo,
-                        MN_MAJOR, Hs_bf, H, nullptr, H);
+                        MN_MAJOR, c->pf_on ? c->pf_hs : Hs_bf, H, nullptr, H);
       g.raster = 1;
       g.clip = clip;
       g.rowsq = c->rowsq;
@@ -955,7 +1000,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
       return;
     }
     GemmDesc g = tc(c) ? desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->xf_on ? c->dS : c->S, Vo,
-                              MN_MAJOR, Hs_bf, H, c->g_out, H)
+                              MN_MAJOR, c->pf_on ? c->pf_hs : Hs_bf, H, c->g_out, H)
                        : desc((int)Vo, (int)H, (int)MO, MN_MAJOR, c->S, Vo, MN_MAJOR, Hs, H,
                               c->g_out, H);
     g.raster = 1;
@@ -1070,6 +1115,12 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                        : desc((int)MO, (int)H, (int)Vo, K_MAJOR, c->S, Vo, MN_MAJOR, c->w_out, H,
                               dst, H);
     g.raster = 0;
+    if (c->pf_on) {
+      g.row_scale = c->pf_sigma;  // dS = diag(sigma) E' (+ the target column's residual)
+      g.row_resid = c->pf_resid;
+      g.resid_idx = c->pf_tgt;
+      g.resid_w = c->w_out_bf;
+    }
     if (c->xf_on) {
       // the A tiles are logits: dS = scale (p - 1[y]) is formed in shared
       // memory (backprop.hpp:179-186) and stored to c->dS for dW_out
@@ -1331,6 +1382,7 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
   if (const char* e = std::getenv("DL_FUSE_OUT")) c->fuse_out = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_FORK_LATE")) c->fork_late = std::atoi(e) != 0;
   if (const char* e = std::getenv("DL_XF")) c->xf = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DL_PFAC")) c->pfac = std::atoi(e) != 0;
   c->tf32x3 = precision == DL_TF32X3;
   if (const char* e = std::getenv("DL_DP_CHUNKS")) c->dp_chunks = std::max(1, std::atoi(e));
   const int rc = guarded(c, [&] {
@@ -1369,6 +1421,8 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     c->d_loss = dalloc<double>(4);
     c->d_pos = reinterpret_cast<unsigned long long*>(c->d_loss + 1);
     c->nonfinite = reinterpret_cast<int*>(c->d_loss + 2);
+    c->pf_repaired = reinterpret_cast<int*>(c->d_loss + 3);
+    DL_CUDA(cudaMemsetAsync(c->d_loss + 3, 0, 8, c->st));
     c->d_skipped = dalloc<unsigned long long>(1);
     c->bar_counter = dalloc<unsigned>(256);  // rec_tc.cu kRecCounters
     c->win_loss = dalloc<double>(2);

@@ -193,10 +193,12 @@ def test_bf16_ds_in_dh_gemm_equals_softmax_kernel():
     out = []
     for xf in ("0", "1"):
         os.environ["DL_XF"] = xf
+        os.environ["DL_PFAC"] = "0"  # (the in-place kernel, not the shifted exponentials)
         try:
             m = dl.GpuRnn(V, H, 0, "bf16")
         finally:
             del os.environ["DL_XF"]
+            del os.environ["DL_PFAC"]
         m.set_params(*params)
         m.set_opt(None, None, None, RHO, EPS)
         r, hf, ok = dl.train_window(m, dl.WindowBatch(x, y, w), h0, 1.0 / (T * B), 1.0, 0.01)

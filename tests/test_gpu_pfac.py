@@ -1,0 +1,143 @@
+"""The bf16 trainer's shifted-exponential softmax (kernels.cu k_pfac_rows,
+gemm_tc.cu epilogue_row with GemmDesc::shift) against the C oracle and
+against the in-place softmax rows kernel it replaces (DL_PFAC=0).
+
+The logits GEMM stores E = e^(s - c_r) with c_r the row's target logit;
+dS = diag(sigma) E' with sigma_r = scale e^(c_r - lse_r) and the target
+column of E' patched to (p_y - 1) / e^(c_r - lse_r) (backprop.hpp:157-189
+restated).  dh = diag(sigma) (E' W_out), dW_out = E'^T bf16(diag(sigma) Hs).
+Checked here:
+* one window at the C3 width (V = 64,000, H = 2,048, TB = 256, 15% masked
+  positions): loss / positions / h_final and the three gradients against
+  the fp32 oracle -- no worse than the in-place path (the logits are no
+  longer rounded to bf16 before the exponential);
+* the repair path (a row whose largest logit is far above its target's is
+  recomputed with the row maximum as shift): forced on every row, and
+  triggered for real by a W_out row that puts one logit ~60 nats above the
+  rest, against the oracle;
+* a training window (the fused dW_out + rmsprop epilogue over E'^T and the
+  scaled hidden states) against the oracle's rmsprop_update.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_parity_shapes import RHO, EPS, make_params, make_window, rel_l2, sparse_rows
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(dl, V, H, **env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return dl.GpuRnn(V, H, 0, "bf16")
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _grads(dl, V, H, params, wb, h0, scale, clip, **env):
+    m = _ctx(dl, V, H, DL_G16="0", **env)
+    m.set_params(*params)
+    r, hf = dl.bptt_run(m, wb, h0, scale, clip)
+    g = m.grads()
+    m.close()
+    return r, hf, g
+
+
+def test_pfac_window_vs_oracle_and_inplace_at_c3(orc):
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 64000, 2048, 4, 64
+    rng = np.random.default_rng(11)
+    params = make_params(V, H, 5)
+    x, y, w = make_window(rng, T, B, V, mask_p=0.15)
+    wb = dl.WindowBatch(x, y, w)
+    h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
+    scale, clip = 1.0 / (T * B), 1.0
+    want = orc.bptt(params, 0, x, y, w, h0, scale, clip)
+    rp, hp, gp = _grads(dl, V, H, params, wb, h0, scale, clip, DL_PFAC="1")
+    ri, hi, gi = _grads(dl, V, H, params, wb, h0, scale, clip, DL_PFAC="0")
+    assert rp.positions == ri.positions == want["positions"]
+    assert np.array_equal(hp, hi)  # the forward recurrence is shared
+    assert rp.loss == pytest.approx(want["loss"], rel=2e-3)
+    assert rp.loss == pytest.approx(ri.loss, rel=1e-5)
+    for k, name in enumerate(("dW_in", "dW_rec", "dW_out")):
+        ref_ = want[("g_in_dense", "g_rec", "g_out")[k]]
+        ep, ei = rel_l2(gp[k], ref_), rel_l2(gi[k], ref_)
+        print(name, "pfac", ep, "in-place", ei)
+        assert ep < 2e-2, (name, ep)
+        # dh (hence dW_rec, dW_in) forms the target column's dS in fp32; dW_out
+        # keeps E'[y] rounded to bf16 -- an error of the order of its bf16 Hs
+        # operand's, where the in-place kernel's bf16(scale (p_y - 1)) is
+        # near exact while p_y << 1
+        assert ep <= (1.1 if name != "dW_out" else 1.5) * ei + 1e-4, (name, ep, ei)
+
+
+@pytest.mark.parametrize("mode", ["forced", "big_logit"])
+def test_pfac_repair_rows(orc, mode):
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 4096, 256, 4, 64
+    rng = np.random.default_rng(21)
+    w_in, w_rec, w_out = make_params(V, H, 9)
+    x, y, w = make_window(rng, T, B, V, mask_p=0.1)
+    h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
+    env = {"DL_PFAC": "1"}
+    if mode == "forced":
+        env["DL_PFAC_REPAIR_NATS"] = "-1e30"  # every row recomputed
+    else:
+        # word 7's logit is ~ 0.5 * sum(h) ~ 60 nats above every other one:
+        # E = e^(s - s_y) would leave bf16's range without the repair
+        w_out = w_out.copy()
+        w_out[7] = 0.5
+        y[y == 7] = 8
+    params = (w_in, w_rec, w_out)
+    wb = dl.WindowBatch(x, y, w)
+    scale, clip = 1.0 / (T * B), 5.0
+    want = orc.bptt(params, 0, x, y, w, h0, scale, clip)
+    r, hf, g = _grads(dl, V, H, params, wb, h0, scale, clip, **env)
+    assert r.positions == want["positions"]
+    assert r.loss == pytest.approx(want["loss"], rel=2e-3)
+    assert np.isfinite(r.loss)
+    for k, name in enumerate(("dW_in", "dW_rec", "dW_out")):
+        ref_ = want[("g_in_dense", "g_rec", "g_out")[k]]
+        assert np.all(np.isfinite(g[k])), name
+        assert rel_l2(g[k], ref_) < 2e-2, (name, rel_l2(g[k], ref_))
+
+
+def test_pfac_train_window_fused_update(orc):
+    """dl_train_window (fused dW_out + dense rmsprop over E'^T and the scaled
+    hidden states) against the oracle's rmsprop_update applied to the same
+    window's fp32 oracle gradient: W_out's step by the bf16 gradient's
+    accuracy, m_out to the gradient's relative error squared."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 64000, 2048, 4, 64
+    rng = np.random.default_rng(4)
+    params = make_params(V, H, 17)
+    x, y, w = make_window(rng, T, B, V)
+    wb = dl.WindowBatch(x, y, w)
+    h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
+    scale, clip, eta = 1.0 / (T * B), 1.0, 0.01
+    m = _ctx(dl, V, H, DL_PFAC="1")
+    m.set_params(*params)
+    m.set_opt(None, None, None, RHO, EPS)
+    r, hf, applied = dl.train_window(m, wb, h0, scale, clip, eta)
+    assert applied
+    want = orc.bptt(params, 0, x, y, w, h0, scale, clip)
+    assert r.loss == pytest.approx(want["loss"], rel=2e-3)
+    words, rows = sparse_rows(want["g_in_dense"])
+    grads = dict(g_in_words=words, g_in_rows=rows, g_rec=want["g_rec"], g_out=want["g_out"])
+    zero = (np.zeros((H, H), np.float32), np.zeros(V, np.float32), np.zeros(V, np.float32))
+    (_, _, w_out2), (_, _, m_out2), ok = orc.rmsprop(params, zero, grads, RHO, EPS, eta)
+    assert ok
+    gw_out = m.params()[2]
+    gm_out = m.opt()[2]
+    m.close()
+    step_ref = w_out2.astype(np.float64) - params[2]
+    step = gw_out.astype(np.float64) - params[2]
+    assert rel_l2(step, step_ref) < 3e-2, rel_l2(step, step_ref)
+    assert rel_l2(gm_out, m_out2) < 3e-2, rel_l2(gm_out, m_out2)
