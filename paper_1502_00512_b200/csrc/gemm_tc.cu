@@ -959,15 +959,20 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
                 if (n0 + j == tg) tval = v[j];
               thit = true;
             }
-            float cmax = -INFINITY, part_sum = 0.f;
+            float part_sum = 0.f;
+            if (whole) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const bool in = whole || n0 + j < g.N;
-              cmax = in ? fmaxf(cmax, v[j]) : cmax;
-              v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
-              part_sum += in ? v[j] : 0.f;
+              for (int j = 0; j < 32; ++j) {
+                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
+                part_sum += v[j];
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
+                part_sum += n0 + j < g.N ? v[j] : 0.f;
+              }
             }
-            mrun = fmaxf(mrun, cmax);
             srun += part_sum;
             if (!mvalid) continue;
             if (whole && (g.lds % 8) == 0) {
@@ -992,7 +997,9 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
             }
           }
           if (mvalid) {
-            g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(mrun, srun);
+            // (.x unused: a row too far above its shift is detected from the
+            // sums, k_pfac_rows)
+            g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(0.f, srun);
             if (thit) g.tgt_logit[m] = tval;
           }
           return;

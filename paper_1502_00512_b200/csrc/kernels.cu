@@ -387,38 +387,39 @@ k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t 
 constexpr int kPfacThreads = 256;
 
 // The row's log-sum-exp relative to its shift from the logits epilogue's
-// partials; a row with a logit more than repair_nats above the shift is
-// recomputed with the shift = its maximum (E rewritten).  Block-uniform.
+// partial sums of E; a row whose sum exceeds e^repair_nats -- every row with
+// a logit more than repair_nats above its shift, and every row whose E was
+// capped -- is recomputed with the shift = its largest logit (E rewritten;
+// two GEMV passes over W_out).  Block-uniform.
 __device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t M, int64_t H, int64_t r,
                              const float2* __restrict__ part, int n_tiles, double& c, double& z,
                              const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
                              float repair_nats, int* repaired, double* red) {
-  double mx = -INFINITY;
   z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) {
-    const float2 p = part[(int64_t)t * M + r];
-    mx = fmax(mx, (double)p.x);
-    z += (double)p.y;
-  }
-  mx = block_max_d<kPfacThreads>(mx, red);
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) z += (double)part[(int64_t)t * M + r].y;
   z = block_sum_d<kPfacThreads>(z, red);
-  if (mx - c > (double)repair_nats) {
-    // rare: some logit is far above the target's -- recompute the row's E
-    // with c = the row maximum (logits as the GEMM forms them: bf16
-    // operands, fp32 accumulation)
-    c = mx;
-    const float cb = (float)c;
+  if (!(log(z) <= (double)repair_nats)) {
+    // rare: some logit far above the target's.  Logits as the GEMM forms
+    // them (bf16 operands, fp32 accumulation), twice: the maximum, then E.
     const bf16* a = hs_bf + r * H;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    double zz = 0.0;
-    for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
+    auto logit = [&](int64_t v) {
       const bf16* b = w + v * H;
       float acc = 0.f;
       for (int64_t k = lane; k < H; k += 32)
         acc = fmaf(__bfloat162float(a[k]), __bfloat162float(b[k]), acc);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      const float e = expf(acc - cb);
+      return acc;
+    };
+    double mx = -INFINITY;
+    for (int64_t v = warp; v < V; v += kPfacThreads / 32) mx = fmax(mx, (double)logit(v));
+    mx = block_max_d<kPfacThreads>(mx, red);
+    c = mx;
+    const float cb = (float)c;
+    double zz = 0.0;
+    for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
+      const float e = expf(logit(v) - cb);
       if (lane == 0) {
         erow[v] = __float2bfloat16_rn(e);
         zz += (double)e;

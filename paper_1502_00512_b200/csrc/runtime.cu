@@ -1451,6 +1451,11 @@ int dl_destroy(dl_ctx* c) {
   if (!c) return DL_OK;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
+  if (c->pf_repaired && std::getenv("DL_DEBUG")) {
+    int n = 0;
+    if (cudaMemcpy(&n, c->pf_repaired, 4, cudaMemcpyDeviceToHost) == cudaSuccess)
+      fprintf(stderr, "[desklm] shifted-exponential softmax: %d row(s) recomputed\n", n);
+  }
   drop_graphs(c);
   delete c->comm;
   void* ptrs[] = {c->w_in, c->w_rec, c->w_out, c->w_rec_bf, c->w_out_bf, c->w_out_bf_next, c->m_rec, c->m_in,

@@ -11,7 +11,7 @@ mkdir -p $OUT
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --profile-steps 0 --no-cpu-baseline --secondary="
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file $OUT/${TAG}_launches.csv $CMD > $OUT/${TAG}_launches.log 2>&1
-for k in "tc_gemm2_kernel:4" "rec_persist_kernel:2" "k_rms:4" "k_softmax:1" "k_embed:2"; do
+for k in "tc_gemm2_kernel:4" "rec_persist_kernel:2" "k_rms:4" "k_pfac_rows:1" "k_embed:2"; do
   name=${k%%:*}; cnt=${k##*:}
   ncu --set full --clock-control none --import-source on -k regex:$name -s $((cnt * 3)) -c $cnt \
       -o $OUT/${TAG}_prof_${name} $CMD > $OUT/${TAG}_prof_${name}.log 2>&1

@@ -265,6 +265,27 @@ def write_ppl_match_seeds(ref, out, seeds=(2, 3, 4, 5)):
                         logs=np.array(logs_all), initial=np.array(inis), eta=0.05)
 
 
+def write_ppl_match_seeds_more(ref, out, seeds=(6, 7, 8, 9, 10)):
+    """More C1 seeds appended to ppl_match_c1_seeds.npz (the seed mean of
+    one chaotic epoch needs ~10 seeds for a standard error under 1.5%)."""
+    g = np.load(os.path.join(out, "ppl_match_c1.npz"))
+    sd = dict(np.load(os.path.join(out, "ppl_match_c1_seeds.npz")))
+    tr, va = g["train"], g["valid"]
+    V, H = int(g["V"]), int(g["H"])
+    for seed in seeds:
+        if seed in set(int(x) for x in sd["seeds"]):
+            continue
+        params = ref.init_uniform(V, H, seed)
+        cfg = oracle.TrainConfig(nstate=H, noffset=128, minibatch=8, unroll=8, eta=0.05,
+                                 max_epochs=1, mode=1, threads=os.cpu_count())
+        _, logs, ini = ref.train(cfg, params, tr, va)
+        sd["seeds"] = np.append(sd["seeds"], seed)
+        sd["logs"] = np.concatenate([sd["logs"], np.asarray(logs[:1])])
+        sd["initial"] = np.append(sd["initial"], ini)
+        print("seed", seed, "valid ppl", logs[0][2], flush=True)
+        np.savez_compressed(os.path.join(out, "ppl_match_c1_seeds.npz"), **sd)
+
+
 def write_ppl_match_h1024_seeds(ref, out, seeds=(2, 3, 4)):
     """The H = 1,024 PPL match over more init_uniform seeds (same corpus,
     schedule and eta as write_ppl_match_h1024; ~15 min each)."""
