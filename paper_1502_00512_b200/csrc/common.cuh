@@ -114,6 +114,7 @@ struct GemmDesc {
   // the epilogue stores E = 2^(min((s - shift[r]) log2 e, 100)) in bf16
   // instead of s, and the partials become (tile max of s, sum of E)
   const float* shift;
+  int part_n;            // (shift) partials per row: part is [M][part_n]
   // fp32 epilogue: row r of the product is multiplied by row_scale[r]
   // (the dh GEMM over E: dS = diag(row_scale) E)
   const float* row_scale;

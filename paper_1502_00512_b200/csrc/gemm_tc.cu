@@ -997,9 +997,10 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
             }
           }
           if (mvalid) {
-            // (.x unused: a row too far above its shift is detected from the
-            // sums, k_pfac_rows)
-            g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(0.f, srun);
+            // row-major [M][part_n] (k_pfac_rows reads a row's sums
+            // contiguously); .x unused: a row too far above its shift is
+            // detected from the sums
+            g.part[static_cast<int64_t>(m) * g.part_n + sub] = make_float2(0.f, srun);
             if (thit) g.tgt_logit[m] = tval;
           }
           return;

@@ -395,8 +395,8 @@ __device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t M, int64_t H, int64_
                              const float2* __restrict__ part, int n_tiles, double& c, double& z,
                              const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
                              float repair_nats, int* repaired, double* red) {
-  z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) z += (double)part[(int64_t)t * M + r].y;
+  z = 0.0;  // (the shifted epilogue's partials are row-major: [M][n_tiles])
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) z += (double)part[r * n_tiles + t].y;
   z = block_sum_d<kPfacThreads>(z, red);
   if (!(log(z) <= (double)repair_nats)) {
     // rare: some logit far above the target's.  Logits as the GEMM forms

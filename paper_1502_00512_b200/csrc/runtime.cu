@@ -604,6 +604,7 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     g.logits = 1;
     g.S = grads ? static_cast<bf16*>(c->S) : nullptr;
     g.shift = c->pf_on ? c->pf_shift : nullptr;
+    g.part_n = c->part_tiles;
     g.lds = V;
     g.part = c->part;
     g.tgt = tgt;
