@@ -111,7 +111,7 @@ struct GemmDesc {
   const uint32_t* tgt;   // [M] target column per row
   float* tgt_logit;      // [M]
   // shifted-exponential logits (bf16 trainer path, "pfac"): with shift set
-  // the epilogue stores E = 2^(min((s - shift[r]) log2 e, 100)) in bf16
+  // the epilogue stores E = 2^(min((s - shift[r]) log2 e, 120)) in bf16
   // instead of s, and the partials become (tile max of s, sum of E)
   const float* shift;
   int part_n;            // (shift) partials per row: part is [M][part_n]

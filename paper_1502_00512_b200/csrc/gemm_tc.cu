@@ -944,8 +944,9 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
           // shifted exponentials E = e^(s - shift) (bf16) replace the logits:
           // dS = row_scale * E with row_scale = scale e^(shift - lse) comes
           // out of the row's lse alone (k_pfac_rows), so no pass over the
-          // logits after this GEMM.  The exponent is capped at 2^100 (the
-          // row is then recomputed with shift = its max, k_pfac_rows).
+          // logits after this GEMM.  The exponent is capped at 2^120 (a
+          // 128-column partial sum stays below 2^127; rows far above their
+          // shift are rescaled by k_pfac_rows).
           const float sb = (mvalid ? g.shift[m] : 0.f) * kLog2e;
 #pragma unroll 1
           for (int c = c0; c < c1; ++c) {
@@ -963,13 +964,13 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
             if (whole) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
-                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
+                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 120.f));
                 part_sum += v[j];
               }
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
-                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 100.f));
+                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb), 120.f));
                 part_sum += n0 + j < g.N ? v[j] : 0.f;
               }
             }

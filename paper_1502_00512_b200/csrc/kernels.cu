@@ -345,11 +345,10 @@ k_lse_rows_bf16(int64_t M, const float2* __restrict__ part, int n_tiles,
 // operand scaled once, B x H instead of TB x V).
 //
 // c_r = the row's target logit (dot of the bf16 operands the GEMM uses):
-// E then stays within bf16 range for every logit less than ~69 nats above
-// the target's, i.e. unless the position's loss exceeds that; a row whose
-// largest logit is more than kPfacRepairNats above c_r is recomputed here
-// with c_r = that maximum (a block-wide GEMV over W_out -- slow, and only in
-// that pathological case).
+// E stays within range for every logit less than 83 nats above the
+// target's (the epilogue caps the exponent at 2^120); a row whose sum of E
+// exceeds e^40 (sigma = scale e^(c - lse) would underflow) gets a new shift
+// (pfac_row_lse).
 __global__ void __launch_bounds__(256)
 k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t H, int64_t M,
                const uint32_t* __restrict__ tgt, int64_t V, float* __restrict__ shift) {
@@ -387,47 +386,90 @@ k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t 
 constexpr int kPfacThreads = 256;
 
 // The row's log-sum-exp relative to its shift from the logits epilogue's
-// partial sums of E; a row whose sum exceeds e^repair_nats -- every row with
-// a logit more than repair_nats above its shift, and every row whose E was
-// capped -- is recomputed with the shift = its largest logit (E rewritten;
-// two GEMV passes over W_out).  Block-uniform.
-__device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t M, int64_t H, int64_t r,
+// partial sums of E (row-major [M][n_tiles]).  A row whose sum exceeds
+// e^repair_nats -- a target far less likely than the rest of the row, whose
+// sigma = scale e^(c - lse) would leave fp32's range -- gets a new shift:
+//   * sum below 2^110: no element reached the epilogue's cap (2^120), so E
+//     holds the row exactly and is rescaled in place to E / z = p (the
+//     shift becomes the lse itself) -- one streaming pass over the row;
+//   * otherwise (a logit ~76+ nats above the target's: some element may be
+//     capped) the row is recomputed from the operands, logits as the GEMM
+//     forms them (bf16 operands, fp32 accumulation), twice: the maximum,
+//     then E = e^(s - max).
+// repaired[0] counts the rescaled rows, repaired[1] the recomputed ones.
+// Block-uniform.
+__device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t H, int64_t r,
                              const float2* __restrict__ part, int n_tiles, double& c, double& z,
                              const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
                              float repair_nats, int* repaired, double* red) {
-  z = 0.0;  // (the shifted epilogue's partials are row-major: [M][n_tiles])
+  z = 0.0;
   for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) z += (double)part[r * n_tiles + t].y;
   z = block_sum_d<kPfacThreads>(z, red);
-  if (!(log(z) <= (double)repair_nats)) {
-    // rare: some logit far above the target's.  Logits as the GEMM forms
-    // them (bf16 operands, fp32 accumulation), twice: the maximum, then E.
-    const bf16* a = hs_bf + r * H;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    auto logit = [&](int64_t v) {
-      const bf16* b = w + v * H;
-      float acc = 0.f;
+  if (log(z) <= (double)repair_nats) return;
+  if (z < 0x1p110) {
+    const double inv = 1.0 / z;
+    if ((V % 8) == 0) {
+      uint4* e8 = reinterpret_cast<uint4*>(erow);
+      for (int64_t q = threadIdx.x; q < V / 8; q += kPfacThreads) {
+        uint4 u = e8[q];
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h2[k]);
+          h2[k] = __floats2bfloat162_rn((float)(f.x * inv), (float)(f.y * inv));
+        }
+        e8[q] = u;
+      }
+    } else {
+      for (int64_t v = threadIdx.x; v < V; v += kPfacThreads)
+        erow[v] = __float2bfloat16_rn((float)(__bfloat162float(erow[v]) * inv));
+    }
+    c += log(z);
+    z = 1.0;
+    if (threadIdx.x == 0 && repaired) atomicAdd(repaired, 1);
+    return;
+  }
+  const bf16* a = hs_bf + r * H;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto logit = [&](int64_t v) {
+    const bf16* b = w + v * H;
+    float acc = 0.f;
+    if ((H % 256) == 0) {
+      for (int64_t k = 8 * lane; k < H; k += 256) {
+        const uint4 qa = *reinterpret_cast<const uint4*>(a + k);
+        const uint4 qb = *reinterpret_cast<const uint4*>(b + k);
+        const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&qa);
+        const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&qb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
+          acc = fmaf(fa.x, fb.x, acc);
+          acc = fmaf(fa.y, fb.y, acc);
+        }
+      }
+    } else {
       for (int64_t k = lane; k < H; k += 32)
         acc = fmaf(__bfloat162float(a[k]), __bfloat162float(b[k]), acc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      return acc;
-    };
-    double mx = -INFINITY;
-    for (int64_t v = warp; v < V; v += kPfacThreads / 32) mx = fmax(mx, (double)logit(v));
-    mx = block_max_d<kPfacThreads>(mx, red);
-    c = mx;
-    const float cb = (float)c;
-    double zz = 0.0;
-    for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
-      const float e = expf(logit(v) - cb);
-      if (lane == 0) {
-        erow[v] = __float2bfloat16_rn(e);
-        zz += (double)e;
-      }
     }
-    z = block_sum_d<kPfacThreads>(zz, red);
-    if (threadIdx.x == 0 && repaired) atomicAdd(repaired, 1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+  };
+  double mx = -INFINITY;
+  for (int64_t v = warp; v < V; v += kPfacThreads / 32) mx = fmax(mx, (double)logit(v));
+  mx = block_max_d<kPfacThreads>(mx, red);
+  c = mx;
+  const float cb = (float)c;
+  double zz = 0.0;
+  for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
+    const float e = expf(logit(v) - cb);
+    if (lane == 0) {
+      erow[v] = __float2bfloat16_rn(e);
+      zz += (double)e;
+    }
   }
+  z = block_sum_d<kPfacThreads>(zz, red);
+  if (threadIdx.x == 0 && repaired) atomicAdd(repaired + 1, 1);
 }
 
 // Vocabulary-sharded output layer: this rank's block log-sum-exp (after the
@@ -441,7 +483,7 @@ k_pfac_lse(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* 
   const int64_t r = blockIdx.x;
   const bool active = wts == nullptr || wts[r] != 0;
   double c = (double)shift[r], z;
-  pfac_row_lse(E + r * V, V, M, H, r, part, n_tiles, c, z, hs_bf, w,
+  pfac_row_lse(E + r * V, V, H, r, part, n_tiles, c, z, hs_bf, w,
                active ? repair_nats : INFINITY, repaired, red);
   if (threadIdx.x == 0) {
     lse_loc[r] = c + log(z);
@@ -481,7 +523,7 @@ k_pfac_rows(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2*
     lse = lse_of_blocks(lse_all, G, M, r);  // (shift repaired by k_pfac_lse)
   } else {
     double z;
-    pfac_row_lse(erow, V, M, H, r, part, n_tiles, c, z, hs_bf, w, repair_nats, repaired, red);
+    pfac_row_lse(erow, V, H, r, part, n_tiles, c, z, hs_bf, w, repair_nats, repaired, red);
     lse = c + log(z);
   }
   const double sy = (double)tgt_logit[r];

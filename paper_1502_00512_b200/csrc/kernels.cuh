@@ -83,9 +83,10 @@ void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_
 // shift[r] = the row's target logit (bf16 operands, fp32 dot) before the
 // logits GEMM; after it, per row: lse, loss / log-prob, sigma[r] =
 // scale e^(shift - lse) (0 masked), E's target column patched so that
-// sigma E' = dS (resid[r]: the patch's bf16 rounding error), and hs_sc = bf16(sigma h) (dW_out's B operand).  Rows with a
-// logit more than repair_nats above the shift are recomputed (counted in
-// *repaired).
+// sigma E' = dS (resid[r]: the patch's bf16 rounding error), and hs_sc =
+// bf16(sigma h) (dW_out's B operand).  Rows whose sum of E exceeds
+// e^repair_nats get a new shift: rescaled in place (repaired[0]) or, when an
+// element may have hit the epilogue's cap, recomputed (repaired[1]).
 void target_shift(const bf16* hs, const bf16* w, int64_t H, int64_t M, const uint32_t* tgt,
                   int64_t V, float* shift, cudaStream_t st);
 void pfac_rows(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,

@@ -1453,9 +1453,10 @@ int dl_destroy(dl_ctx* c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->pf_repaired && std::getenv("DL_DEBUG")) {
-    int n = 0;
-    if (cudaMemcpy(&n, c->pf_repaired, 4, cudaMemcpyDeviceToHost) == cudaSuccess)
-      fprintf(stderr, "[desklm] shifted-exponential softmax: %d row(s) recomputed\n", n);
+    int n[2] = {0, 0};
+    if (cudaMemcpy(n, c->pf_repaired, 8, cudaMemcpyDeviceToHost) == cudaSuccess)
+      fprintf(stderr, "[desklm] shifted-exponential softmax: %d row(s) rescaled, %d recomputed\n",
+              n[0], n[1]);
   }
   drop_graphs(c);
   delete c->comm;

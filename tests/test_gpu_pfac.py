@@ -11,10 +11,10 @@ Checked here:
   positions): loss / positions / h_final and the three gradients against
   the fp32 oracle -- no worse than the in-place path (the logits are no
   longer rounded to bf16 before the exponential);
-* the repair path (a row whose largest logit is far above its target's is
-  recomputed with the row maximum as shift): forced on every row, and
-  triggered for real by a W_out row that puts one logit ~60 nats above the
-  rest, against the oracle;
+* the repair path (a row whose sum of E exceeds e^40 -- its target far less
+  likely than the rest -- is rescaled in place to E / z): forced on every
+  row, and triggered for real by a W_out row that puts one logit ~60 nats
+  above the rest, against the oracle;
 * a training window (the fused dW_out + rmsprop epilogue over E'^T and the
   scaled hidden states) against the oracle's rmsprop_update.
 """
@@ -91,7 +91,7 @@ def test_pfac_repair_rows(orc, mode):
         env["DL_PFAC_REPAIR_NATS"] = "-1e30"  # every row recomputed
     else:
         # word 7's logit is ~ 0.5 * sum(h) ~ 60 nats above every other one:
-        # E = e^(s - s_y) would leave bf16's range without the repair
+        # sigma = scale e^(s_y - lse) would underflow without the rescale
         w_out = w_out.copy()
         w_out[7] = 0.5
         y[y == 7] = 8
