@@ -129,6 +129,47 @@ __global__ void k_reduce(const float* __restrict__ part, int splits, int64_t spl
   if (do_clip && nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
 }
 
+// The dW_rec split-K reduction + clip (rnn.hpp:158-159) with the W_rec
+// rmsprop step (rmsprop.hpp:113-133, k_rms_rec's arithmetic) in the same
+// pass, for the trainer path with a finite clip (every clipped component
+// finite: the all-finite check cannot fail); g_rec is still written.
+__global__ void k_reduce_rms_rec(const float* __restrict__ part, int splits, int64_t split_stride,
+                                 int64_t n, float* __restrict__ g_out, float clip,
+                                 float* __restrict__ w, bf16* __restrict__ wb,
+                                 float* __restrict__ m, double rho, double eps, double eta) {
+  auto one = [&](float& wi, float& mi, float gf) {
+    const double gi = (double)gf;
+    mi = (float)(rho * (double)mi + (1.0 - rho) * gi * gi);
+    wi = wi - (float)(eta * gi / sqrt((double)mi + eps));
+  };
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    float4 v = p4[i];
+#pragma unroll 4
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 q = p4[sp * (split_stride / 4) + i];
+      v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
+    }
+    v = make_float4(clip1(v.x, clip), clip1(v.y, clip), clip1(v.z, clip), clip1(v.w, clip));
+    reinterpret_cast<float4*>(g_out)[i] = v;
+    float4 mq = reinterpret_cast<float4*>(m)[i];
+    float4 wq = reinterpret_cast<float4*>(w)[i];
+    one(wq.x, mq.x, v.x);
+    one(wq.y, mq.y, v.y);
+    one(wq.z, mq.z, v.z);
+    one(wq.w, mq.w, v.w);
+    reinterpret_cast<float4*>(m)[i] = mq;
+    reinterpret_cast<float4*>(w)[i] = wq;
+    if (wb) {
+      __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + 4 * i);
+      b2[0] = __floats2bfloat162_rn(wq.x, wq.y);
+      b2[1] = __floats2bfloat162_rn(wq.z, wq.w);
+    }
+  }
+}
+
 // ---------------------------------------------------------- softmax rows
 // fp32 path: S holds fp32 logits [M x V].  Per row (backprop.hpp:162-186):
 //   mx = max_w s (double), z = sum exp(s - mx) (double), lse = mx + log z
@@ -1247,6 +1288,12 @@ void rec_fwd(const float* part, int splits, int64_t ss, int64_t Bn, int64_t H, c
 void rec_bwd(const float* part, int splits, int64_t ss, int64_t n, const float* dh_out,
              const float* hnext, int act, float* dpre, bf16* dpreb, cudaStream_t st) {
   k_rec_bwd<<<grid_for(n), 256, 0, st>>>(part, splits, ss, n, dh_out, hnext, act, dpre, dpreb);
+}
+void reduce_rms_rec(const float* part, int splits, int64_t ss, int64_t n, float* g_out, float clip,
+                    float* w, bf16* wb, float* m, double rho, double eps, double eta,
+                    cudaStream_t st) {
+  k_reduce_rms_rec<<<grid_for(n / 4), 256, 0, st>>>(part, splits, ss, n, g_out, clip, w, wb, m,
+                                                    rho, eps, eta);
 }
 void reduce_splits(const float* part, int splits, int64_t ss, int64_t n, float* out, float clip,
                    int do_clip, int* nonfinite, cudaStream_t st) {

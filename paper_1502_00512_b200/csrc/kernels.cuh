@@ -63,6 +63,11 @@ void rec_bwd(const float* part, int splits, int64_t split_stride, int64_t n, con
              const float* hnext, int act, float* dpre, bf16* dpreb, cudaStream_t st);
 void reduce_splits(const float* part, int splits, int64_t split_stride, int64_t n, float* out,
                    float clip, int do_clip, int* nonfinite, cudaStream_t st);
+// the dW_rec reduction + clip and the W_rec rmsprop step in one pass (finite
+// clip, n and split_stride multiples of 4)
+void reduce_rms_rec(const float* part, int splits, int64_t split_stride, int64_t n, float* g_out,
+                    float clip, float* w, bf16* wb, float* m, double rho, double eps, double eta,
+                    cudaStream_t st);
 // lse_all != nullptr: vocabulary-sharded rows -- lse from the G gathered
 // block values [G][M], target logit from tgt_logit, tgt = local columns.
 void softmax_rows_f32(float* S, int64_t M, int64_t V, const uint32_t* tgt, const uint8_t* wts,

@@ -120,6 +120,7 @@ struct dl_ctx {
   // softmax rows kernel.  pf_on: this window used it (dh / dW_out follow).
   bool pfac = true;
   bool pf_on = false;
+  bool rec_fused = false;  // this window's W_rec step ran in the dW_rec reduction
   float *pf_shift = nullptr, *pf_sigma = nullptr, *pf_resid = nullptr;
   const uint32_t* pf_tgt = nullptr;  // this window's output-row targets
   bf16* pf_hs = nullptr;     // diag(sigma) Hs in bf16 [MO x H] (dW_out's B operand)
@@ -802,6 +803,7 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   const bool vs = c->comm != nullptr && c->vshard && !dpv;
   const int64_t MO = dpv ? c->nranks * TB : TB;  // output-layer rows
   c->pf_on = false;  // (set by output_layer for this window)
+  c->rec_fused = false;
   if (grads && !dprec) {
     // the W_in gradient's id sort depends on x only: run it on the side
     // stream under the forward recurrence (which leaves SMs free) (joined before embed_rows)
@@ -1228,7 +1230,14 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     g.k_splits = s;
     g.split_stride = H * H;
     gemm(c, g);
-    reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dprec ? 0 : 1, c->nonfinite, st);
+    // with the W_out update fused (a finite clip: nothing can be rejected)
+    // the W_rec rmsprop step rides on the reduction pass (run_rmsprop skips it)
+    c->rec_fused = fuse_eta > 0.0 && !dprec && tc(c) && std::isfinite(clip) && (H * H) % 4 == 0;
+    if (c->rec_fused)
+      reduce_rms_rec(c->splitws, s, H * H, H * H, c->g_rec, clip, c->w_rec, c->w_rec_bf, c->m_rec,
+                     c->rho, c->eps, fuse_eta, st);
+    else
+      reduce_splits(c->splitws, s, H * H, H * H, c->g_rec, clip, dprec ? 0 : 1, c->nonfinite, st);
     c->launches++;
   }
   if (dprec) {
@@ -1282,8 +1291,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
 void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false, bool count = true) {
   Phase p(c, "rmsprop");
   cudaStream_t st = c->st;
-  rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
-          c->eps, eta, c->nonfinite, st);
+  if (!(skip_out && c->rec_fused))  // (else applied by the dW_rec reduction, run_window)
+    rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
+            c->eps, eta, c->nonfinite, st);
   rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
