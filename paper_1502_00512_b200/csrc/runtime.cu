@@ -160,6 +160,20 @@ struct dl_ctx {
   double graph_eta = NAN;
   uint64_t graph_launches = 0;
   bool use_graph = true;
+  // dl_train_window as one CUDA graph per (T, B, scale, clip, eta): the
+  // window's H2D / D2H copies are graph nodes whose host side is re-pointed
+  // at each call's buffers (cudaGraphExecMemcpyNodeSetParams1D)
+  struct TwGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t e = nullptr;
+    cudaGraphNode_t nx = nullptr, ny = nullptr, nw = nullptr, nh0 = nullptr, nhf = nullptr;
+    int64_t T = 0, B = 0;
+    double scale = 0, eta = 0;
+    float clip = 0;
+    bool fuse = false;
+    uint8_t* pin = nullptr;  // staging: x, y, w, h0, h_final, results
+    uint64_t launches = 0;
+  } tw;
   // recurrence steps as one cluster kernel each (rec_tc.cu); DL_REC_CLUSTER=0
   // falls back to split-K GEMM + reduction kernels (both are sm_100a CUDA)
   bool rec_cluster = true;
@@ -291,6 +305,10 @@ void drop_graphs(dl_ctx* c) {
       c->graphs[v] = nullptr;
     }
   c->graph = nullptr;
+  if (c->tw.e) cudaGraphExecDestroy(c->tw.e);
+  if (c->tw.g) cudaGraphDestroy(c->tw.g);
+  if (c->tw.pin) cudaFreeHost(c->tw.pin);
+  c->tw = dl_ctx::TwGraph{};
 }
 
 // ---------------------------------------------------------------- timing
@@ -1567,6 +1585,117 @@ namespace {
 // dl_window / dl_train_window: validate, stage the window's host arrays
 // through pinned memory, run the window (+ the update when eta > 0), read
 // back loss, positions, h_final and the update's verdict.
+// dl_train_window's window (bptt_run + rmsprop_update) replayed from one
+// CUDA graph: the ~20 kernel launches, events and copies of a window cost
+// ~370 us of host time per call (measured at V = 1,000, H = 128, where the
+// device work is tiny), which a synchronous per-window API exposes.  The
+// graph holds the H2D copies of the window (from its own page-locked
+// staging), the device work, the results' D2H and h_final's D2H on the side
+// stream; per call the copies' host ends are re-pointed at the caller's
+// page-locked buffers (pageable ones go through the staging), then one
+// launch and one synchronize.
+void presize(dl_ctx* c, int64_t T, int64_t B);
+
+bool tw_graph_ok(dl_ctx* c) {
+  static const bool on = [] {
+    const char* e = std::getenv("DL_TW_GRAPH");
+    if (e && std::atoi(e) == 0) return false;
+    return std::getenv("DL_GEMM_TRACE") == nullptr && std::getenv("DL_REC_TRACE") == nullptr;
+  }();
+  return on && c->use_graph && !c->profiling && c->comm == nullptr && c->loss_mode != 0;
+}
+
+void train_window_graph(dl_ctx* c, int64_t T, int64_t B, const uint32_t* inputs,
+                        const uint32_t* targets, const uint8_t* weights, const float* h0,
+                        float* h_final, double loss_scale, float clip, double eta, double* loss,
+                        uint64_t* positions, int* applied) {
+  const int64_t TB = T * B, BH = B * c->H;
+  const bool fuse = fuse_ok(c, clip);
+  // staging layout: x | y | w | h0 | h_final | results
+  const size_t o_y = TB * 4, o_w = 2 * TB * 4, o_h0 = ((TB * 9 + 15) / 16) * 16,
+               o_hf = o_h0 + BH * 4, o_res = o_hf + BH * 4, bytes = o_res + 64;
+  auto& g = c->tw;
+  if (!g.e || g.T != T || g.B != B || g.scale != loss_scale || g.clip != clip || g.eta != eta ||
+      g.fuse != fuse) {
+    drop_graphs(c);  // (also any trainer graph: they share the window buffers)
+    presize(c, T, B);  // (no allocation inside the capture)
+    DL_CUDA(cudaMallocHost(&g.pin, bytes));
+    uint8_t* pin = g.pin;
+    const uint64_t before = c->launches.load();
+    DL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      DL_CUDA(cudaMemcpyAsync(c->x_d, pin, TB * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->y_d, pin + o_y, TB * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->w_d, pin + o_w, TB, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->htape, pin + o_h0, BH * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemsetAsync(c->d_loss, 0, 16, c->st));
+      run_window(c, T, B, loss_scale, clip, true, 0.0, fuse ? eta : 0.0);
+      run_rmsprop(c, eta, TB * dp_ranks(c), /*skip_out=*/fuse);
+      DL_CUDA(cudaMemcpyAsync(pin + o_res, c->d_loss, 20, cudaMemcpyDeviceToHost, c->st));
+      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_hfinal, 0));
+      DL_CUDA(cudaMemcpyAsync(pin + o_hf, c->htape + T * BH, BH * 4, cudaMemcpyDeviceToHost,
+                              c->st2));
+      DL_CUDA(cudaEventRecord(c->ev_join, c->st2));
+      DL_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    } catch (...) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(c->st, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    DL_CUDA(cudaStreamEndCapture(c->st, &g.g));
+    g.launches = c->launches.load() - before;
+    c->launches -= g.launches;  // counted when replayed
+    // the copy nodes whose host ends move per call
+    size_t nn = 0;
+    DL_CUDA(cudaGraphGetNodes(g.g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    DL_CUDA(cudaGraphGetNodes(g.g, nodes.data(), &nn));
+    for (cudaGraphNode_t n : nodes) {
+      cudaGraphNodeType ty;
+      DL_CUDA(cudaGraphNodeGetType(n, &ty));
+      if (ty != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms mp{};
+      DL_CUDA(cudaGraphMemcpyNodeGetParams(n, &mp));
+      const void* hp = mp.kind == cudaMemcpyHostToDevice ? mp.srcPtr.ptr : mp.dstPtr.ptr;
+      if (hp == pin) g.nx = n;
+      else if (hp == pin + o_y) g.ny = n;
+      else if (hp == pin + o_w) g.nw = n;
+      else if (hp == pin + o_h0) g.nh0 = n;
+      else if (hp == pin + o_hf) g.nhf = n;
+    }
+    DL_REQUIRE(g.nx && g.ny && g.nw && g.nh0 && g.nhf, DL_EDEVICE,
+               "internal: train-window graph copy nodes not found");
+    DL_CUDA(cudaGraphInstantiate(&g.e, g.g, 0));
+    g.T = T; g.B = B; g.scale = loss_scale; g.clip = clip; g.eta = eta; g.fuse = fuse;
+  }
+  uint8_t* pin = g.pin;
+  auto h2d = [&](cudaGraphNode_t n, void* dst, const void* src, size_t nb, size_t off) {
+    if (!is_pinned(src)) {
+      std::memcpy(pin + off, src, nb);
+      src = pin + off;
+    }
+    DL_CUDA(cudaGraphExecMemcpyNodeSetParams1D(g.e, n, dst, src, nb, cudaMemcpyHostToDevice));
+  };
+  h2d(g.nx, c->x_d, inputs, TB * 4, 0);
+  h2d(g.ny, c->y_d, targets, TB * 4, o_y);
+  h2d(g.nw, c->w_d, weights, TB, o_w);
+  h2d(g.nh0, c->htape, h0, BH * 4, o_h0);
+  const bool hf_direct = h_final && is_pinned(h_final);
+  DL_CUDA(cudaGraphExecMemcpyNodeSetParams1D(g.e, g.nhf, hf_direct ? (void*)h_final : pin + o_hf,
+                                             c->htape + T * BH, BH * 4, cudaMemcpyDeviceToHost));
+  DL_CUDA(cudaGraphLaunch(g.e, c->st));
+  c->launches += g.launches;
+  DL_CUDA(cudaStreamSynchronize(c->st));
+  if (h_final && !hf_direct) std::memcpy(h_final, pin + o_hf, BH * 4);
+  struct { double l; unsigned long long p; int bad; int pad; } res;
+  std::memcpy(&res, pin + o_res, 20);
+  if (loss) *loss = res.l;
+  if (positions) *positions = res.p;
+  if (applied) *applied = res.bad ? 0 : 1;
+  c->capT = std::max(c->capT, T);
+}
+
 int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t* inputs,
                 const uint32_t* targets, const uint8_t* weights, const float* h0,
                 float* h_final, double loss_scale, float clip, bool grads, double eta,
@@ -1584,6 +1713,11 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
     return fail(c, DL_EINVAL, "NCE mode: multi-rank windows are not supported");
   return guarded(c, [&] {
     ensure_window(c, T, B);
+    if (eta > 0.0 && tw_graph_ok(c)) {
+      train_window_graph(c, T, B, inputs, targets, weights, h0, h_final, loss_scale, clip, eta,
+                         loss, positions, applied);
+      return;
+    }
     if (c->loss_mode == 0) nce_prepare(c, T, B, weights);
     const int64_t TB = T * B, BH = B * c->H;
     // H2D of the window: page-locked caller buffers are copied from directly,
