@@ -132,6 +132,7 @@ struct dl_ctx {
   double* logp_row = nullptr;
   float* dh_out = nullptr;
   float* dpre = nullptr;
+  cudaEvent_t score_ev[2] = {nullptr, nullptr};  // dl_score's two host slots
   bf16* dpre_bf = nullptr;
   float* splitws = nullptr;
   size_t splitws_elems = 0;
@@ -1508,6 +1509,8 @@ int dl_destroy(dl_ctx* c) {
     if (p) cudaFree(p);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  for (auto e : c->score_ev)
+    if (e) cudaEventDestroy(e);
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
@@ -1893,24 +1896,54 @@ int dl_score(dl_ctx* c, int64_t S, int64_t steps, const uint32_t* in, const int6
     if (bank < 1) bank = 1;
     ensure_window(c, bank, S);
     std::vector<double> lp(S * steps, NAN);
-    double* pin = static_cast<double*>(ensure_pinned(c, sizeof(double) * bank * S * 2 + 64));
+    // two page-locked slots (ids, targets, mask, log-probs per bank): the
+    // host prepares bank j + 1 and scatters bank j - 1's log-probs while the
+    // device runs bank j -- no synchronisation inside the walk
+    const int64_t BS = bank * S;
+    const size_t slot_bytes = ((BS * 4 + 15) / 16) * 16 * 2 + ((BS + 15) / 16) * 16 + BS * 8;
+    uint8_t* pin = static_cast<uint8_t*>(ensure_pinned(c, 2 * slot_bytes + 64));
+    auto slot_x = [&](int k) { return reinterpret_cast<uint32_t*>(pin + k * slot_bytes); };
+    auto slot_y = [&](int k) {
+      return reinterpret_cast<uint32_t*>(pin + k * slot_bytes + ((BS * 4 + 15) / 16) * 16);
+    };
+    auto slot_w = [&](int k) { return pin + k * slot_bytes + ((BS * 4 + 15) / 16) * 16 * 2; };
+    auto slot_lp = [&](int k) {
+      return reinterpret_cast<double*>(pin + k * slot_bytes + ((BS * 4 + 15) / 16) * 16 * 2 +
+                                       ((BS + 15) / 16) * 16);
+    };
+    for (int k = 0; k < 2; ++k)
+      if (!c->score_ev[k]) DL_CUDA(cudaEventCreateWithFlags(&c->score_ev[k], cudaEventDisableTiming));
+    int64_t pend_j0[2] = {-1, -1}, pend_nb[2] = {0, 0};
+    auto drain = [&](int k) {  // bank in slot k done: scatter its log-probs
+      if (pend_j0[k] < 0) return;
+      DL_CUDA(cudaEventSynchronize(c->score_ev[k]));
+      const uint8_t* wk = slot_w(k);
+      const double* lk = slot_lp(k);
+      for (int64_t i = 0; i < pend_nb[k] * S; ++i)
+        if (wk[i]) lp[pend_j0[k] * S + i] = lk[i];
+      pend_j0[k] = -1;
+    };
     // initial state
     if (h0) DL_CUDA(cudaMemcpyAsync(c->htape, h0, SH * 4, cudaMemcpyHostToDevice, c->st));
     else fill_f32(c->htape, act0(c->act), SH, c->st);
-    std::vector<uint32_t> ytmp(bank * S);
-    std::vector<uint8_t> wtmp(bank * S);
-    for (int64_t j0 = 0; j0 < steps; j0 += bank) {
+    int k = 0;
+    for (int64_t j0 = 0; j0 < steps; j0 += bank, k ^= 1) {
       const int64_t nb = std::min(bank, steps - j0);
-      DL_CUDA(cudaMemcpyAsync(c->x_d, in + j0 * S, nb * S * 4, cudaMemcpyHostToDevice, c->st));
+      drain(k);  // (its bank two back: long finished while this one was prepared)
+      uint32_t* xk = slot_x(k);
+      uint32_t* yk = slot_y(k);
+      uint8_t* wk = slot_w(k);
+      std::memcpy(xk, in + j0 * S, nb * S * 4);
       bool any = false;
       for (int64_t i = 0; i < nb * S; ++i) {
         const int64_t t = tgt[j0 * S + i];
-        ytmp[i] = t >= 0 ? (uint32_t)t : 0u;
-        wtmp[i] = t >= 0 ? 1 : 0;
+        yk[i] = t >= 0 ? (uint32_t)t : 0u;
+        wk[i] = t >= 0 ? 1 : 0;
         any |= t >= 0;
       }
-      DL_CUDA(cudaMemcpyAsync(c->y_d, ytmp.data(), nb * S * 4, cudaMemcpyHostToDevice, c->st));
-      DL_CUDA(cudaMemcpyAsync(c->w_d, wtmp.data(), nb * S, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->x_d, xk, nb * S * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->y_d, yk, nb * S * 4, cudaMemcpyHostToDevice, c->st));
+      DL_CUDA(cudaMemcpyAsync(c->w_d, wk, nb * S, cudaMemcpyHostToDevice, c->st));
       if (tc(c)) f32_to_bf16(c->htape, c->htape_bf, SH, c->st);
       {
         Phase p(c, "recurrence_fwd");
@@ -1925,13 +1958,14 @@ int dl_score(dl_ctx* c, int64_t S, int64_t steps, const uint32_t* in, const int6
       // carry the last state to slot 0 for the next bank
       DL_CUDA(cudaMemcpyAsync(c->htape, c->htape + nb * SH, SH * 4, cudaMemcpyDeviceToDevice, c->st));
       if (any) {
-        DL_CUDA(cudaMemcpyAsync(pin, c->logp_row, nb * S * 8, cudaMemcpyDeviceToHost, c->st));
-        DL_CUDA(cudaStreamSynchronize(c->st));
-        for (int64_t i = 0; i < nb * S; ++i)
-          if (wtmp[i]) lp[j0 * S + i] = pin[i];
+        DL_CUDA(cudaMemcpyAsync(slot_lp(k), c->logp_row, nb * S * 8, cudaMemcpyDeviceToHost, c->st));
+        DL_CUDA(cudaEventRecord(c->score_ev[k], c->st));
+        pend_j0[k] = j0;
+        pend_nb[k] = nb;
       }
-      DL_CUDA(cudaStreamSynchronize(c->st));
     }
+    drain(0);
+    drain(1);
     if (h_final) DL_CUDA(cudaMemcpyAsync(h_final, c->htape, SH * 4, cudaMemcpyDeviceToHost, c->st));
     DL_CUDA(cudaStreamSynchronize(c->st));
     prof_collect(c);
