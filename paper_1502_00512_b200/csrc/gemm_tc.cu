@@ -948,6 +948,7 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
           // 128-column partial sum stays below 2^127; rows far above their
           // shift are rescaled by k_pfac_rows).
           const float sb = (mvalid ? g.shift[m] : 0.f) * kLog2e;
+          bool capped = false;  // an element of this half tile reached the cap
 #pragma unroll 1
           for (int c = c0; c < c1; ++c) {
             float v[32];
@@ -975,6 +976,7 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
               }
             }
             srun += part_sum;
+            capped |= mvalid && part_sum >= 0x1p120f;
             if (!mvalid) continue;
             if (whole && (g.lds % 8) == 0) {
               uint4* dst = reinterpret_cast<uint4*>(Srow + n0);
@@ -997,11 +999,47 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
                 if (n0 + j < g.N) Srow[n0 + j] = __float2bfloat16_rn(v[j]);
             }
           }
+          // (rare) a logit of this half tile more than 83 nats above the
+          // row's shift: the half tile is redone from TMEM relative to its
+          // own maximum, the offset (nats) recorded in the partial's .x --
+          // k_pfac_rows rescales the row to one shift, so nothing is lost
+          float off = 0.f;
+          if (__any_sync(0xffffffffu, capped)) {
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int c = c0; c < c1; ++c) {
+              float v[32];
+              tmem_ld32(taddr + c * 32, v);
+              const int n0 = nt * BN + c * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < g.N) mx = fmaxf(mx, v[j]);
+            }
+            off = capped ? mx - sb / kLog2e : 0.f;
+            const float sb2 = sb + off * kLog2e;
+            srun = 0.f;
+#pragma unroll 1
+            for (int c = c0; c < c1; ++c) {
+              float v[32];
+              tmem_ld32(taddr + c * 32, v);
+              const int n0 = nt * BN + c * 32;
+              float part_sum = 0.f;  // (as the first pass: per chunk, then into srun)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] = fast_exp2(fminf(fmaf(v[j], kLog2e, -sb2), 120.f));
+                part_sum += n0 + j < g.N ? v[j] : 0.f;
+              }
+              srun += part_sum;
+              if (!mvalid) continue;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < g.N) Srow[n0 + j] = __float2bfloat16_rn(v[j]);
+            }
+          }
           if (mvalid) {
             // row-major [M][part_n] (k_pfac_rows reads a row's sums
-            // contiguously); .x unused: a row too far above its shift is
-            // detected from the sums
-            g.part[static_cast<int64_t>(m) * g.part_n + sub] = make_float2(0.f, srun);
+            // contiguously); .x: the half tile's shift offset (normally 0)
+            g.part[static_cast<int64_t>(m) * g.part_n + sub] = make_float2(off, srun);
             if (thit) g.tgt_logit[m] = tval;
           }
           return;

@@ -427,105 +427,57 @@ k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t 
 constexpr int kPfacThreads = 256;
 
 // The row's log-sum-exp relative to its shift from the logits epilogue's
-// partial sums of E (row-major [M][n_tiles]).  A row whose sum exceeds
-// e^repair_nats -- a target far less likely than the rest of the row, whose
-// sigma = scale e^(c - lse) would leave fp32's range -- gets a new shift:
-//   * sum below 2^110: no element reached the epilogue's cap (2^120), so E
-//     holds the row exactly and is rescaled in place to E / z = p (the
-//     shift becomes the lse itself) -- one streaming pass over the row;
-//   * otherwise (a logit ~76+ nats above the target's: some element may be
-//     capped) the row is recomputed from the operands, logits as the GEMM
-//     forms them (bf16 operands, fp32 accumulation), twice: the maximum,
-//     then E = e^(s - max).
-// repaired[0] counts the rescaled rows, repaired[1] the recomputed ones.
+// partials (row-major [M][n_tiles]: .x the half tile's shift offset in
+// nats -- 0 unless one of its logits was more than 83 nats above the shift
+// and the epilogue redid it against its own maximum -- .y its sum of E).
+// A row with an offset tile, or whose sum exceeds e^repair_nats (a target
+// far less likely than the rest of the row: sigma = scale e^(c - lse) would
+// leave fp32's range), is rescaled in place to E / z = p with one factor
+// per half tile, the shift becoming the lse itself -- one streaming pass
+// over the row, nothing recomputed.  repaired[0] counts those rows,
+// repaired[1] the ones with offset tiles.  pw: columns per partial.
 // Block-uniform.
-__device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t H, int64_t r,
-                             const float2* __restrict__ part, int n_tiles, double& c, double& z,
-                             const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
-                             float repair_nats, int* repaired, double* red) {
+__device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t r, const float2* __restrict__ part,
+                             int n_tiles, int pw, double& c, double& z, float repair_nats,
+                             int* repaired, double* red, float* fac) {
+  const float2* pr = part + r * n_tiles;
+  double om = 0.0;
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) om = fmax(om, (double)pr[t].x);
+  om = block_max_d<kPfacThreads>(om, red);
   z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) z += (double)part[r * n_tiles + t].y;
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) {
+    const float2 q = pr[t];
+    z += q.x == 0.f && om == 0.0 ? (double)q.y : (double)q.y * exp((double)q.x - om);
+  }
   z = block_sum_d<kPfacThreads>(z, red);
-  if (log(z) <= (double)repair_nats) return;
-  if (z < 0x1p110) {
-    const double inv = 1.0 / z;
-    if ((V % 8) == 0) {
-      uint4* e8 = reinterpret_cast<uint4*>(erow);
-      for (int64_t q = threadIdx.x; q < V / 8; q += kPfacThreads) {
-        uint4 u = e8[q];
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __bfloat1622float2(h2[k]);
-          h2[k] = __floats2bfloat162_rn((float)(f.x * inv), (float)(f.y * inv));
-        }
-        e8[q] = u;
-      }
-    } else {
-      for (int64_t v = threadIdx.x; v < V; v += kPfacThreads)
-        erow[v] = __float2bfloat16_rn((float)(__bfloat162float(erow[v]) * inv));
-    }
-    c += log(z);
-    z = 1.0;
-    if (threadIdx.x == 0 && repaired) atomicAdd(repaired, 1);
-    return;
-  }
-  const bf16* a = hs_bf + r * H;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  auto logit = [&](int64_t v) {
-    const bf16* b = w + v * H;
-    float acc = 0.f;
-    if ((H % 256) == 0) {
-      for (int64_t k = 8 * lane; k < H; k += 256) {
-        const uint4 qa = *reinterpret_cast<const uint4*>(a + k);
-        const uint4 qb = *reinterpret_cast<const uint4*>(b + k);
-        const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&qa);
-        const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&qb);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
-          acc = fmaf(fa.x, fb.x, acc);
-          acc = fmaf(fa.y, fb.y, acc);
-        }
-      }
-    } else {
-      for (int64_t k = lane; k < H; k += 32)
-        acc = fmaf(__bfloat162float(a[k]), __bfloat162float(b[k]), acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc;
-  };
-  double mx = -INFINITY;
-  for (int64_t v = warp; v < V; v += kPfacThreads / 32) mx = fmax(mx, (double)logit(v));
-  mx = block_max_d<kPfacThreads>(mx, red);
-  c = mx;
-  const float cb = (float)c;
-  double zz = 0.0;
-  for (int64_t v = warp; v < V; v += kPfacThreads / 32) {
-    const float e = expf(logit(v) - cb);
-    if (lane == 0) {
-      erow[v] = __float2bfloat16_rn(e);
-      zz += (double)e;
-    }
-  }
-  z = block_sum_d<kPfacThreads>(zz, red);
-  if (threadIdx.x == 0 && repaired) atomicAdd(repaired + 1, 1);
+  if (om == 0.0 && log(z) <= (double)repair_nats) return;
+  // tile t's elements are e^(s - c - x_t): times e^(x_t - om - ln z) they
+  // become e^(s - lse)
+  const double lz = log(z);
+  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads)
+    fac[t] = (float)exp((double)pr[t].x - om - lz);
+  __syncthreads();
+  for (int64_t v = threadIdx.x; v < V; v += kPfacThreads)
+    erow[v] = __float2bfloat16_rn(__bfloat162float(erow[v]) * fac[v / pw]);
+  c += om + lz;
+  z = 1.0;
+  if (threadIdx.x == 0 && repaired) atomicAdd(repaired + (om > 0.0 ? 1 : 0), 1);
+  __syncthreads();  // (fac is reused by the caller's next row)
 }
 
 // Vocabulary-sharded output layer: this rank's block log-sum-exp (after the
 // repair), exchanged before k_pfac_rows; shift[r] updated when repaired.
 __global__ void __launch_bounds__(kPfacThreads)
-k_pfac_lse(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* __restrict__ part,
-           int n_tiles, const uint8_t* __restrict__ wts, float* __restrict__ shift,
-           double* __restrict__ lse_loc, const bf16* __restrict__ hs_bf,
-           const bf16* __restrict__ w, float repair_nats, int* __restrict__ repaired) {
+k_pfac_lse(bf16* __restrict__ E, int64_t V, int64_t M, const float2* __restrict__ part,
+           int n_tiles, int pw, const uint8_t* __restrict__ wts, float* __restrict__ shift,
+           double* __restrict__ lse_loc, float repair_nats, int* __restrict__ repaired) {
+  extern __shared__ float fac[];
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
   const bool active = wts == nullptr || wts[r] != 0;
   double c = (double)shift[r], z;
-  pfac_row_lse(E + r * V, V, H, r, part, n_tiles, c, z, hs_bf, w,
-               active ? repair_nats : INFINITY, repaired, red);
+  pfac_row_lse(E + r * V, V, r, part, n_tiles, pw, c, z, active ? repair_nats : INFINITY,
+               repaired, red, fac);
   if (threadIdx.x == 0) {
     lse_loc[r] = c + log(z);
     shift[r] = (float)c;
@@ -534,13 +486,13 @@ k_pfac_lse(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* 
 
 __global__ void __launch_bounds__(kPfacThreads)
 k_pfac_rows(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2* __restrict__ part,
-            int n_tiles, const float* __restrict__ tgt_logit, const uint32_t* __restrict__ tgt,
+            int n_tiles, int pw, const float* __restrict__ tgt_logit, const uint32_t* __restrict__ tgt,
             const uint8_t* __restrict__ wts, double scale, double* __restrict__ loss_row,
             double* __restrict__ logp_row, const float* __restrict__ shift,
             float* __restrict__ sigma, float* __restrict__ resid, const float* __restrict__ hs,
-            bf16* __restrict__ hs_sc, const bf16* __restrict__ hs_bf, const bf16* __restrict__ w,
-            float repair_nats, int* __restrict__ repaired, const double* __restrict__ lse_all,
-            int G) {
+            bf16* __restrict__ hs_sc, const bf16* __restrict__ hs_bf, float repair_nats,
+            int* __restrict__ repaired, const double* __restrict__ lse_all, int G) {
+  extern __shared__ float fac[];
   __shared__ double red[32];
   const int64_t r = blockIdx.x;
   const bool active = wts == nullptr || wts[r] != 0;
@@ -564,7 +516,7 @@ k_pfac_rows(bf16* __restrict__ E, int64_t V, int64_t M, int64_t H, const float2*
     lse = lse_of_blocks(lse_all, G, M, r);  // (shift repaired by k_pfac_lse)
   } else {
     double z;
-    pfac_row_lse(erow, V, H, r, part, n_tiles, c, z, hs_bf, w, repair_nats, repaired, red);
+    pfac_row_lse(erow, V, r, part, n_tiles, pw, c, z, repair_nats, repaired, red, fac);
     lse = c + log(z);
   }
   const double sy = (double)tgt_logit[r];
@@ -1332,20 +1284,20 @@ void target_shift(const bf16* hs, const bf16* w, int64_t H, int64_t M, const uin
 void pfac_rows(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
                const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts, double scale,
                double* loss_row, double* logp_row, const float* shift, float* sigma,
-               float* resid, const float* hs, bf16* hs_sc, const bf16* hs_bf, const bf16* w,
-               float repair_nats, int* repaired, cudaStream_t st, const double* lse_all, int G) {
+               float* resid, const float* hs, bf16* hs_sc, const bf16* hs_bf, float repair_nats,
+               int* repaired, cudaStream_t st, const double* lse_all, int G) {
   if (M <= 0) return;
-  k_pfac_rows<<<(unsigned)M, kPfacThreads, 0, st>>>(E, V, M, H, part, n_tiles, tgt_logit, tgt,
-                                                    wts, scale, loss_row, logp_row, shift, sigma,
-                                                    resid, hs, hs_sc, hs_bf, w, repair_nats,
-                                                    repaired, lse_all, G);
+  const int pw = (V >= 256 ? 256 : V >= 128 ? 128 : 64) / 2;  // (tc_n_tiles' half tiles)
+  k_pfac_rows<<<(unsigned)M, kPfacThreads, n_tiles * sizeof(float), st>>>(
+      E, V, M, H, part, n_tiles, pw, tgt_logit, tgt, wts, scale, loss_row, logp_row, shift, sigma,
+      resid, hs, hs_sc, hs_bf, repair_nats, repaired, lse_all, G);
 }
-void pfac_lse(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
-              const uint8_t* wts, float* shift, double* lse_loc, const bf16* hs_bf, const bf16* w,
-              float repair_nats, int* repaired, cudaStream_t st) {
+void pfac_lse(bf16* E, int64_t M, int64_t V, const float2* part, int n_tiles, const uint8_t* wts,
+              float* shift, double* lse_loc, float repair_nats, int* repaired, cudaStream_t st) {
   if (M <= 0) return;
-  k_pfac_lse<<<(unsigned)M, kPfacThreads, 0, st>>>(E, V, M, H, part, n_tiles, wts, shift, lse_loc,
-                                                   hs_bf, w, repair_nats, repaired);
+  const int pw = (V >= 256 ? 256 : V >= 128 ? 128 : 64) / 2;  // (tc_n_tiles' half tiles)
+  k_pfac_lse<<<(unsigned)M, kPfacThreads, n_tiles * sizeof(float), st>>>(
+      E, V, M, part, n_tiles, pw, wts, shift, lse_loc, repair_nats, repaired);
 }
 void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
                    cudaStream_t st) {

@@ -90,21 +90,20 @@ void softmax_rows_bf16(bf16* S, int64_t M, int64_t V, const float2* part, int n_
 // scale e^(shift - lse) (0 masked), E's target column patched so that
 // sigma E' = dS (resid[r]: the patch's bf16 rounding error), and hs_sc =
 // bf16(sigma h) (dW_out's B operand).  Rows whose sum of E exceeds
-// e^repair_nats get a new shift: rescaled in place (repaired[0]) or, when an
-// element may have hit the epilogue's cap, recomputed (repaired[1]).
+// e^repair_nats, or with a half tile the epilogue redid against its own
+// maximum, are rescaled in place to one shift (counted in repaired[0] /
+// repaired[1]).
 void target_shift(const bf16* hs, const bf16* w, int64_t H, int64_t M, const uint32_t* tgt,
                   int64_t V, float* shift, cudaStream_t st);
 void pfac_rows(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
                const float* tgt_logit, const uint32_t* tgt, const uint8_t* wts, double scale,
                double* loss_row, double* logp_row, const float* shift, float* sigma,
-               float* resid, const float* hs, bf16* hs_sc, const bf16* hs_bf, const bf16* w,
-               float repair_nats, int* repaired, cudaStream_t st, const double* lse_all = nullptr,
-               int G = 1);
-// vocabulary-sharded: this rank's block lse (lse_loc) after the repair, for
+               float* resid, const float* hs, bf16* hs_sc, const bf16* hs_bf, float repair_nats,
+               int* repaired, cudaStream_t st, const double* lse_all = nullptr, int G = 1);
+// vocabulary-sharded: this rank's block lse (lse_loc) after the rescales, for
 // the exchange before pfac_rows(..., lse_all, G)
-void pfac_lse(bf16* E, int64_t M, int64_t V, int64_t H, const float2* part, int n_tiles,
-              const uint8_t* wts, float* shift, double* lse_loc, const bf16* hs_bf, const bf16* w,
-              float repair_nats, int* repaired, cudaStream_t st);
+void pfac_lse(bf16* E, int64_t M, int64_t V, const float2* part, int n_tiles, const uint8_t* wts,
+              float* shift, double* lse_loc, float repair_nats, int* repaired, cudaStream_t st);
 void shard_targets(const uint32_t* y, int64_t M, int64_t v0, int64_t Vo, uint32_t* loc,
                    cudaStream_t st);
 void block_lse_bf16(const float2* part, int n_tiles, int64_t M, double* lse, cudaStream_t st);

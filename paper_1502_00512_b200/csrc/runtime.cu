@@ -641,8 +641,8 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
     if (vs) {
       Phase p(c, "vocab_exchange");
       if (c->pf_on)
-        pfac_lse(static_cast<bf16*>(c->S), M, V, H, c->part, c->part_tiles, wts, c->pf_shift,
-                 c->lse_loc, hs_bf, c->w_out_bf, nats, c->pf_repaired, c->st);
+        pfac_lse(static_cast<bf16*>(c->S), M, V, c->part, c->part_tiles, wts, c->pf_shift,
+                 c->lse_loc, nats, c->pf_repaired, c->st);
       else
         block_lse_bf16(c->part, c->part_tiles, M, c->lse_loc, c->st);
       c->launches++;
@@ -658,7 +658,7 @@ void output_layer(dl_ctx* c, int64_t M, const float* hs, const bf16* hs_bf, cons
       // hidden states in bf16 only)
       pfac_rows(static_cast<bf16*>(c->S), M, V, H, c->part, c->part_tiles, c->tgt_logit, tgt, wts,
                 scale, loss_row, logp_row, c->pf_shift, c->pf_sigma, c->pf_resid,
-                c->dpv ? nullptr : hs, c->pf_hs, hs_bf, c->w_out_bf, nats, c->pf_repaired, c->st,
+                c->dpv ? nullptr : hs, c->pf_hs, hs_bf, nats, c->pf_repaired, c->st,
                 vs ? c->lse_all : nullptr, c->nranks);
     } else if (c->xf_on) {
       c->xf_tgt = tgt;
@@ -1484,7 +1484,7 @@ int dl_destroy(dl_ctx* c) {
   if (c->pf_repaired && std::getenv("DL_DEBUG")) {
     int n[2] = {0, 0};
     if (cudaMemcpy(n, c->pf_repaired, 8, cudaMemcpyDeviceToHost) == cudaSuccess)
-      fprintf(stderr, "[desklm] shifted-exponential softmax: %d row(s) rescaled, %d recomputed\n",
+      fprintf(stderr, "[desklm] shifted-exponential softmax: %d row(s) rescaled, %d with redone tiles\n",
               n[0], n[1]);
   }
   drop_graphs(c);

@@ -12,9 +12,11 @@ Checked here:
   the fp32 oracle -- no worse than the in-place path (the logits are no
   longer rounded to bf16 before the exponential);
 * the repair path (a row whose sum of E exceeds e^40 -- its target far less
-  likely than the rest -- is rescaled in place to E / z): forced on every
-  row, and triggered for real by a W_out row that puts one logit ~60 nats
-  above the rest, against the oracle;
+  likely than the rest -- is rescaled in place to E / z; a half tile with a
+  logit beyond the epilogue's cap is redone against its own maximum and
+  rescaled with it): forced on every row, and triggered for real by a W_out
+  row that puts one logit ~60 / ~115 nats above the rest, against the
+  oracle;
 * a training window (the fused dW_out + rmsprop epilogue over E'^T and the
   scaled hidden states) against the oracle's rmsprop_update.
 """
@@ -78,7 +80,7 @@ def test_pfac_window_vs_oracle_and_inplace_at_c3(orc):
         assert ep <= (1.1 if name != "dW_out" else 1.5) * ei + 1e-4, (name, ep, ei)
 
 
-@pytest.mark.parametrize("mode", ["forced", "big_logit"])
+@pytest.mark.parametrize("mode", ["forced", "big_logit", "huge_logit"])
 def test_pfac_repair_rows(orc, mode):
     import paper_1502_00512_b200 as dl
     V, H, T, B = 4096, 256, 4, 64
@@ -92,8 +94,10 @@ def test_pfac_repair_rows(orc, mode):
     else:
         # word 7's logit is ~ 0.5 * sum(h) ~ 60 nats above every other one:
         # sigma = scale e^(s_y - lse) would underflow without the rescale
+        # ("huge": ~115 nats -- beyond the epilogue's 2^120 cap, so the half
+        # tile holding word 7 is redone against its own maximum)
         w_out = w_out.copy()
-        w_out[7] = 0.5
+        w_out[7] = 0.5 if mode == "big_logit" else 0.9
         y[y == 7] = 8
     params = (w_in, w_rec, w_out)
     wb = dl.WindowBatch(x, y, w)
