@@ -383,13 +383,14 @@ k_lse_rows_bf16(int64_t M, const float2* __restrict__ part, int n_tiles,
 // (computed from the fp32 target logit, not from the rounded E).  The row
 // factor then moves out of both gradient GEMMs: dh = diag(sigma) (E' W_out)
 // (the dh epilogue's row_scale) and dW_out = E'^T (diag(sigma) Hs) (its B
-// operand scaled once, B x H instead of TB x V).
+// operand scaled once: TB x H values instead of TB x V).
 //
 // c_r = the row's target logit (dot of the bf16 operands the GEMM uses):
 // E stays within range for every logit less than 83 nats above the
-// target's (the epilogue caps the exponent at 2^120); a row whose sum of E
-// exceeds e^40 (sigma = scale e^(c - lse) would underflow) gets a new shift
-// (pfac_row_lse).
+// target's (the epilogue caps the exponent at 2^120 and redoes a half tile
+// past the cap against its own maximum); a row with such a tile or whose
+// sum of E exceeds e^40 (sigma = scale e^(c - lse) would underflow) is
+// rescaled to one new shift (pfac_row_lse).
 __global__ void __launch_bounds__(256)
 k_target_shift(const bf16* __restrict__ hs, const bf16* __restrict__ w, int64_t H, int64_t M,
                const uint32_t* __restrict__ tgt, int64_t V, float* __restrict__ shift) {
