@@ -518,6 +518,7 @@ void output_side(dl_bn* c, int64_t N, const float* hs, const bf16* hs_bf, double
     g.S = grads ? static_cast<bf16*>(c->S) : nullptr;
     g.lds = V;
     g.part = c->part;
+    g.part_n = c->part_tiles;
     g.tgt = c->y;
     g.tgt_logit = c->tgt_logit;
     run_gemm(c, g);

@@ -1104,7 +1104,9 @@ __device__ __forceinline__ void epilogue_row(const GemmDesc& g, uint32_t taddr, 
           }
         }
         if (mvalid) {
-          g.part[static_cast<int64_t>(sub) * g.M + m] = make_float2(mrun, srun);
+          // row-major [M][part_n]: a row's partials contiguous for the
+          // combining kernels
+          g.part[static_cast<int64_t>(m) * g.part_n + sub] = make_float2(mrun, srun);
           if (thit) g.tgt_logit[m] = tval;
         }
       }

@@ -267,11 +267,11 @@ k_softmax_rows_bf16(bf16* __restrict__ S, int64_t V, int64_t M, const float2* __
   } else {
     double mx = -INFINITY;
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
-      mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+      mx = fmax(mx, (double)part[r * n_tiles + t].x);
     mx = block_max_d<kRowThreads>(mx, red);
     double z = 0.0;
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-      const float2 p = part[(int64_t)t * M + r];
+      const float2 p = part[r * n_tiles + t];
       if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
     }
     z = block_sum_d<kRowThreads>(z, red);
@@ -353,11 +353,11 @@ k_lse_rows_bf16(int64_t M, const float2* __restrict__ part, int n_tiles,
   } else {
     double mx = -INFINITY;
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
-      mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+      mx = fmax(mx, (double)part[r * n_tiles + t].x);
     mx = block_max_d<kRowThreads>(mx, red);
     double z = 0.0;
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-      const float2 p = part[(int64_t)t * M + r];
+      const float2 p = part[r * n_tiles + t];
       if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
     }
     z = block_sum_d<kRowThreads>(z, red);
@@ -564,11 +564,11 @@ k_block_lse_bf16(const float2* __restrict__ part, int n_tiles, int64_t M,
   const int64_t r = blockIdx.x;
   double mx = -INFINITY;
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
-    mx = fmax(mx, (double)part[(int64_t)t * M + r].x);
+    mx = fmax(mx, (double)part[r * n_tiles + t].x);
   mx = block_max_d<256>(mx, red);
   double z = 0.0;
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const float2 p = part[(int64_t)t * M + r];
+    const float2 p = part[r * n_tiles + t];
     if (p.y > 0.f) z += (double)p.y * exp((double)p.x - mx);
   }
   z = block_sum_d<256>(z, red);

@@ -2101,6 +2101,7 @@ int dl_ln_z_samples(dl_ctx* c, const uint32_t* ids, int64_t n, int64_t count, do
         g.S = nullptr;
         g.lds = V;
         g.part = c->part;
+        g.part_n = c->part_tiles;
         g.tgt = c->y_d;
         g.tgt_logit = c->tgt_logit;
         g.no_pair = c->logits_pair ? 0 : 1;
@@ -2666,6 +2667,7 @@ int dl_test_gemm(dl_ctx* c, int M, int N, int K, int a_major, int b_major, const
       g.S = S;
       g.lds = N;
       g.part = part;
+      g.part_n = nt;
       g.tgt = tg;
       g.tgt_logit = tl;
       gemm(c, g);
