@@ -145,3 +145,50 @@ def test_pfac_train_window_fused_update(orc):
     step = gw_out.astype(np.float64) - params[2]
     assert rel_l2(step, step_ref) < 3e-2, rel_l2(step, step_ref)
     assert rel_l2(gm_out, m_out2) < 3e-2, rel_l2(gm_out, m_out2)
+
+
+def test_train_window_graph_replay_matches_direct_launches():
+    """dl_train_window replays one CUDA graph per (T, B, scale, clip, eta)
+    whose copies are re-pointed at each call's buffers: three consecutive
+    windows from page-locked and pageable host arrays (alternating, so the
+    node updates and the staging path both run) give bit-identical losses,
+    h_final and parameters to direct launches (DL_TW_GRAPH=0)."""
+    import torch
+
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 4096, 256, 8, 64
+    rng = np.random.default_rng(31)
+    params = make_params(V, H, 12)
+    wins = [make_window(rng, T, B, V, mask_p=0.1) for _ in range(3)]
+    h0 = rng.uniform(0.0, 1.0, (B, H)).astype(np.float32)
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype={np.float32: torch.float32, np.uint8: torch.uint8,
+                                        np.uint32: torch.int32}[a.dtype.type], pin_memory=True)
+        out = t.numpy()
+        out[:] = a.view(out.dtype) if a.dtype == np.uint32 else a
+        return out.view(a.dtype) if a.dtype == np.uint32 else out
+
+    out = []
+    for graph in ("0", "1"):
+        m = _ctx(dl, V, H, DL_TW_GRAPH=graph)
+        m.set_params(*params)
+        m.set_opt(None, None, None, RHO, EPS)
+        h = h0
+        res = []
+        for i, (x, y, w) in enumerate(wins):
+            if i % 2 == 0:
+                x, y, w, h = pinned(x), pinned(y), pinned(w), pinned(h)
+            hf = pinned(np.zeros((B, H), np.float32)) if i % 2 == 0 else None
+            r, h, ok = dl.train_window(m, dl.WindowBatch(x, y, w), h, 1.0 / (T * B), 1.0, 0.01,
+                                       h_final=hf)
+            assert ok
+            res.append((r.loss, r.positions, np.array(h)))
+        res.append(m.params())
+        out.append(res)
+        m.close()
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert a[0] == b[0] and a[1] == b[1]
+        assert np.array_equal(a[2], b[2])
+    for a, b in zip(out[0][3], out[1][3]):
+        assert np.array_equal(a, b)
