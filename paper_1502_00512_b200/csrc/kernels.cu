@@ -56,6 +56,27 @@ __device__ double block_max_d(double v, double* red) {
   return red[0];
 }
 
+// max of a and sum of b over the block in one pass (fixed tree)
+template <int NT>
+__device__ void block_max_sum_d(double& a, double& b, double* red) {
+  a = warp_max_d(a);
+  b = warp_sum_d(b);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) { red[w] = a; red[16 + w] = b; }
+  __syncthreads();
+  if (w == 0) {
+    double x = l < NT / 32 ? red[l] : -INFINITY;
+    double y = l < NT / 32 ? red[16 + l] : 0.0;
+    x = warp_max_d(x);
+    y = warp_sum_d(y);
+    if (l == 0) { red[0] = x; red[16] = y; }
+  }
+  __syncthreads();
+  a = red[0];
+  b = red[16];
+}
+
 // ---------------------------------------------------------------- casts
 __global__ void k_f32_to_bf16(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -442,15 +463,22 @@ __device__ void pfac_row_lse(bf16* erow, int64_t V, int64_t r, const float2* __r
                              int n_tiles, int pw, double& c, double& z, float repair_nats,
                              int* repaired, double* red, float* fac) {
   const float2* pr = part + r * n_tiles;
+  // the offsets' maximum and the plain sum in one reduction (offsets are 0
+  // but in the rare redone tiles)
   double om = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) om = fmax(om, (double)pr[t].x);
-  om = block_max_d<kPfacThreads>(om, red);
   z = 0.0;
   for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads) {
     const float2 q = pr[t];
-    z += q.x == 0.f && om == 0.0 ? (double)q.y : (double)q.y * exp((double)q.x - om);
+    om = fmax(om, (double)q.x);
+    z += (double)q.y;
   }
-  z = block_sum_d<kPfacThreads>(z, red);
+  block_max_sum_d<kPfacThreads>(om, z, red);
+  if (om > 0.0) {
+    z = 0.0;
+    for (int t = threadIdx.x; t < n_tiles; t += kPfacThreads)
+      z += (double)pr[t].y * exp((double)pr[t].x - om);
+    z = block_sum_d<kPfacThreads>(z, red);
+  }
   if (om == 0.0 && log(z) <= (double)repair_nats) return;
   // tile t's elements are e^(s - c - x_t): times e^(x_t - om - ln z) they
   // become e^(s - lse)
