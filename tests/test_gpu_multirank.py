@@ -358,3 +358,47 @@ def test_dp_vocab_parallel_trainer_matches_global_minibatch(orc, precision):
         for a, b in zip(t.logs, single.logs):
             assert a.train_loss == pytest.approx(b.train_loss, rel=rel)
             assert a.valid_ppl == pytest.approx(b.valid_ppl, rel=10 * rel)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_vocab_shard_bf16_repaired_rows_match_oracle(orc, G):
+    """The shifted-exponential softmax across vocabulary shards when rows need
+    a new shift: W_out rows that put one logit ~48 nats (rescale) and one
+    ~110 nats (a half tile past the epilogue's cap, redone against its own
+    maximum) above the others, on different shards.  Each rank's block lse
+    after its own rescales goes through the exchange; loss and gradients
+    against the fp32 oracle."""
+    import paper_1502_00512_b200 as dl
+    V, H, T, B = 1024, 128, 4, 16
+    rng = np.random.default_rng(70 + G)
+    w_in, w_rec, w_out = (rng.uniform(-0.1, 0.1, s).astype(np.float32)
+                          for s in ((V, H), (H, H), (V, H)))
+    w_out[5] = 0.75           # ~48 nats above the rest (first shard): rescaled
+    w_out[V - 3] = 1.7        # ~110 nats (last shard): past the 2^120 cap
+    params = (w_in, w_rec, w_out)
+    x = rng.integers(0, V, (T, B)).astype(np.uint32)
+    y = rng.integers(8, V - 8, (T, B)).astype(np.uint32)
+    w = (rng.random((T, B)) > 0.1).astype(np.uint8)
+    h0 = rng.uniform(0, 1, (B, H)).astype(np.float32)
+    scale = 1.0 / (B * T)
+    want = orc.bptt(params, 0, x, y, w, h0, scale, 5.0)
+    ranks = _vshard_ranks(dl, G, V, H, "bf16", params)
+    wb = dl.WindowBatch(x, y, w)
+
+    def run(r):
+        res, hf = dl.bptt_run(ranks[r], wb, h0, scale, 5.0)
+        return res, ranks[r].grads()
+
+    with ThreadPoolExecutor(G) as ex:
+        outs = list(ex.map(run, range(G)))
+    for res, g in outs:
+        assert res.positions == want["positions"]
+        assert np.isfinite(res.loss)
+        assert res.loss == pytest.approx(want["loss"], rel=2e-3)
+    g_in, g_rec = outs[0][1][0], outs[0][1][1]
+    for name, got, ref_ in (("dW_in", g_in, want["g_in_dense"]), ("dW_rec", g_rec, want["g_rec"])):
+        assert np.all(np.isfinite(got)), name
+        err = np.linalg.norm(got - ref_) / np.linalg.norm(ref_)
+        assert err < 2e-2, (name, err)
+    for m in ranks:
+        m.close()
