@@ -916,6 +916,66 @@ __global__ void k_rms_decay(float* __restrict__ m, int64_t n, double rho,
     m[i] = (float)(rho * (double)m[i]);
 }
 
+// The same update with a block per row (H / 8 threads, two float4 per
+// thread): the row's gradient and master are loaded once, together, before
+// the block's sum of squares -- the one-warp-per-row kernel below keeps only
+// a warp's loads in flight per row and re-reads g for the update.
+template <int VPT>
+__global__ void k_rms_rows_blk(float* __restrict__ w, bf16* __restrict__ wb,
+                               float* __restrict__ m, const float* __restrict__ g,
+                               const uint32_t* __restrict__ words,
+                               const int* __restrict__ n_rows_dev, int64_t n_rows, int64_t H,
+                               double rho, double eps, double eta, int dense,
+                               const int* __restrict__ nonfinite) {
+  if (nonfinite && *nonfinite) return;
+  __shared__ double red[32];
+  const int64_t rows = n_rows_dev ? (int64_t)*n_rows_dev : n_rows;
+  const int lane = threadIdx.x % 32, wid = threadIdx.x / 32, nw = blockDim.x / 32;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t word = words ? (int64_t)words[r] : r;
+    const float4* g4 = reinterpret_cast<const float4*>(g + r * H);
+    float4* w4 = reinterpret_cast<float4*>(w + word * H);
+    float4 q[VPT], o[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      q[v] = g4[threadIdx.x + v * blockDim.x];
+      o[v] = w4[threadIdx.x + v * blockDim.x];
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v)
+      s += (double)q[v].x * (double)q[v].x + (double)q[v].y * (double)q[v].y +
+           (double)q[v].z * (double)q[v].z + (double)q[v].w * (double)q[v].w;
+    s = warp_sum_d(s);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int i = 0; i < nw; ++i) tot += red[i];  // fixed order, every thread
+    const double ms = tot / (double)H;
+    float mw;
+    if (dense) mw = (float)(rho * (double)m[word] + (1.0 - rho) * ms);
+    else mw = m[word] + (float)((1.0 - rho) * ms);
+    const double denom = sqrt((double)mw + eps);
+    const double inv = 1.0 / denom;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+      o[v].x -= rms_step(eta, q[v].x, denom, inv);
+      o[v].y -= rms_step(eta, q[v].y, denom, inv);
+      o[v].z -= rms_step(eta, q[v].z, denom, inv);
+      o[v].w -= rms_step(eta, q[v].w, denom, inv);
+      const int64_t j = threadIdx.x + v * blockDim.x;
+      w4[j] = o[v];
+      if (wb) {
+        __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(wb + word * H + 4 * j);
+        b2[0] = __floats2bfloat162_rn(o[v].x, o[v].y);
+        b2[1] = __floats2bfloat162_rn(o[v].z, o[v].w);
+      }
+    }
+    __syncthreads();  // every thread has read m[word] and red[]
+    if (threadIdx.x == 0) m[word] = mw;
+  }
+}
+
 // rmsprop.hpp:85-91: touched rows add (1-rho)*mean(g^2) to the decayed
 // scalar, then divide the whole row's step by sqrt(m + eps).
 // rmsprop.hpp:94-107 (dense=1): m = float(rho*m + (1-rho)*mean(g^2)).
@@ -1406,6 +1466,12 @@ static const bool use_dense_rows_kernel = [] {
   return e && std::atoi(e) != 0;
 }();
 
+// DL_WARP_ROWS=1: the one-warp-per-row kernel for every H
+static const bool use_warp_rows_kernel = [] {
+  const char* e = std::getenv("DL_WARP_ROWS");
+  return e && std::atoi(e) != 0;
+}();
+
 void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* words,
               const int* n_rows_dev, int64_t n_rows, int64_t H, double rho, double eps, double eta,
               int dense, const int* nonfinite, cudaStream_t st) {
@@ -1415,6 +1481,13 @@ void rms_rows(float* w, bf16* wb, float* m, const float* g, const uint32_t* word
       k_rms_dense_rows<8><<<blocks, 128, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
     else
       k_rms_dense_rows<16><<<blocks, 128, 0, st>>>(w, wb, m, g, n_rows, rho, eps, eta, nonfinite);
+    return;
+  }
+  if (H % 256 == 0 && H / 8 >= 64 && H / 8 <= 1024 && !use_warp_rows_kernel) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n_rows, 148 * 16));
+    k_rms_rows_blk<2><<<blocks, (unsigned)(H / 8), 0, st>>>(w, wb, m, g, words, n_rows_dev,
+                                                            n_rows, H, rho, eps, eta, dense,
+                                                            nonfinite);
     return;
   }
   const int64_t warps = n_rows;

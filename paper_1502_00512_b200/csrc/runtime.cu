@@ -121,6 +121,7 @@ struct dl_ctx {
   bool pfac = true;
   bool pf_on = false;
   bool rec_fused = false;  // this window's W_rec step ran in the dW_rec reduction
+  bool in_decayed = false;  // this window's m_in decay ran on the side stream (run_window)
   float *pf_shift = nullptr, *pf_sigma = nullptr, *pf_resid = nullptr;
   const uint32_t* pf_tgt = nullptr;  // this window's output-row targets
   bf16* pf_hs = nullptr;     // diag(sigma) Hs in bf16 [MO x H] (dW_out's B operand)
@@ -830,6 +831,14 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_sort_fork, 0));
     embed_sort(c->x_d, T, B, 1, V, c->ews, c->g_in_words, c->g_in_n, c->st2);
     c->launches++;
+    if (fuse_eta > 0.0 && std::isfinite(clip)) {
+      // this window's update cannot be rejected (a finite clip maps every
+      // gradient element to a finite value): every W_in accumulator's decay
+      // (rmsprop.hpp:84) runs here too, instead of after the backward pass
+      rms_decay(c->m_in, c->V, c->rho, nullptr, c->st2);
+      c->launches++;
+      c->in_decayed = true;
+    }
     DL_CUDA(cudaEventRecord(c->ev_sort_join, c->st2));
   }
   if (tc(c) && !c->h0_bf_ready) {
@@ -1313,7 +1322,12 @@ void run_rmsprop(dl_ctx* c, double eta, int64_t TB, bool skip_out = false, bool 
   if (!(skip_out && c->rec_fused))  // (else applied by the dW_rec reduction, run_window)
     rms_rec(c->w_rec, tc(c) ? c->w_rec_bf : nullptr, c->m_rec, c->g_rec, c->H * c->H, c->rho,
             c->eps, eta, c->nonfinite, st);
-  rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
+  if (c->in_decayed) {
+    c->in_decayed = false;
+    c->launches--;
+  } else {
+    rms_decay(c->m_in, c->V, c->rho, c->nonfinite, st);
+  }
   rms_rows(c->w_in, nullptr, c->m_in, c->g_in_rows, c->g_in_words, c->g_in_n, TB, c->H, c->rho,
            c->eps, eta, 0, c->nonfinite, st);
   if (!skip_out && c->out_sparse) {

@@ -73,3 +73,17 @@ def test_bottleneck_argument_errors_without_gpu():
     assert b"P must not exceed H" in lib.dl_bn_last_error(None)
     assert lib.dl_bn_create(C.byref(h), 0, 16, 8, 4, 0, 1) == _lib.DL_EINVAL  # bf16 needs %8
     assert lib.dl_bn_create(C.byref(h), 0, 16, 8, 8, 3, 0) == _lib.DL_EINVAL  # act
+
+
+def test_library_loaded_before_torch_leaves_torch_importable():
+    """The library and libtorch_cuda must share one libnccl.so.2: loaded
+    first, the library must not pin an older NCCL that leaves torch's
+    symbols unresolved (Makefile NCCL_LIB)."""
+    import subprocess
+    import sys
+    code = ("from paper_1502_00512_b200 import _lib; _lib.load()\n"
+            "import torch, torch.distributed\n"
+            "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
