@@ -575,7 +575,9 @@ def measure_training(args, cfg, world, rank, local, steps, warmup, dist=None, cp
     # memory, bptt_run + rmsprop_update, D2H of loss, positions, applied and
     # h_final), CUDA events on the library stream around all the calls
     e2e = None
-    if args.e2e and args.loss == "softmax":
+    # (NCE: single-rank windows only through this call; the noise of each
+    # window is drawn by the library from the context's generator)
+    if args.e2e and (args.loss == "softmax" or world == 1):
         def pinned(shape, dtype):
             return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 

@@ -252,6 +252,15 @@ struct dl_ctx {
   void* raw_pin[2] = {nullptr, nullptr};  // double-buffered host staging of raw outputs
   cudaEvent_t raw_ev[2] = {nullptr, nullptr};
   int raw_slot = 0;
+  int raw_last = 0;  // slot of the last prepared window's draws
+  // dl_window / dl_train_window in NCE mode draw the NEXT window's noise
+  // while the device runs this one (nce_predraw): pre_n outputs of the
+  // generator following rng's state, in raw_pin[pre_slot]; rng_ahead
+  // continues after them.  rng itself stays at the consumed point.
+  std::mt19937_64 rng_ahead{0};
+  int64_t pre_n = 0;
+  int pre_slot = 0;
+  int64_t pre_used = 0;  // outputs of the queue the last prepared window took
   bool nce_pending = false;       // records of the prepared window not built yet
   double nce_wait_s = 0.0, nce_gen_s = 0.0, nce_res_s = 0.0, nce_copy_s = 0.0;  // (DL_DEBUG)
   std::vector<uint32_t> h_ids;  // trainer: host copy of the stream (NCE draws)
@@ -750,7 +759,9 @@ void nce_reserve(dl_ctx* c, int64_t N) {
 // builds the records (nce.cu k_nce_records) once the window's targets and
 // mask are on the device (run_window).  The staging is double-buffered so
 // the host can draw the next window while the device runs this one.
-void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
+// predraw: the caller runs nce_predraw after launching the window (else
+// any pre-drawn outputs are dropped: rng is at the consumed point anyway).
+void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights, bool predraw = false) {
   DL_REQUIRE(c->nce_k > 0 && !c->nz_prob.empty(), 1,
              "bptt: NCE mode needs noise model and rng (dl_set_noise)");
   const int K1 = c->nce_k + 1;
@@ -765,6 +776,7 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
   if (ND > c->raw_cap || !c->pos_of_d || c->capT * c->capB > c->raw_cap / 2 ||
       c->pos_cap < T * B) {
     const int64_t cap = std::max<int64_t>({ND, 2 * c->capT * c->capB * c->nce_k, 2});
+    c->pre_n = 0;  // (any pre-drawn outputs live in the buffers freed here)
     for (int i = 0; i < 2; ++i) {
       if (c->raw_ev[i]) DL_CUDA(cudaEventSynchronize(c->raw_ev[i]));
       if (c->raw_pin[i]) cudaFreeHost(c->raw_pin[i]);
@@ -781,13 +793,32 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
     c->first_d = dalloc<int>(std::max(c->capT, T) + 1);
     c->raw_cap = cap;
   }
-  const int slot = c->raw_slot;
-  c->raw_slot ^= 1;
+  if (c->pre_used > 0) {  // (a window that failed after taking its draws)
+    c->rng.discard(c->pre_used);
+    c->pre_n = 0;
+  }
+  c->pre_used = 0;
+  int slot;
+  unsigned long long* raw;
   const auto t0 = std::chrono::steady_clock::now();
-  DL_CUDA(cudaEventSynchronize(c->raw_ev[slot]));  // its previous upload is done
-  const auto t1 = std::chrono::steady_clock::now();
-  unsigned long long* raw = static_cast<unsigned long long*>(c->raw_pin[slot]);
-  for (int64_t i = 0; i < ND; ++i) raw[i] = c->rng();
+  auto t1 = t0;
+  if (predraw && c->pre_n > 0 && c->pre_n >= ND) {
+    // drawn during the previous call (nce_predraw): the same outputs rng
+    // would give now; rng advances past them in nce_predraw
+    slot = c->pre_slot;
+    raw = static_cast<unsigned long long*>(c->raw_pin[slot]);
+    c->pre_used = ND;
+    t1 = std::chrono::steady_clock::now();
+  } else {
+    c->pre_n = 0;
+    slot = c->raw_slot;
+    DL_CUDA(cudaEventSynchronize(c->raw_ev[slot]));  // its previous upload is done
+    t1 = std::chrono::steady_clock::now();
+    raw = static_cast<unsigned long long*>(c->raw_pin[slot]);
+    for (int64_t i = 0; i < ND; ++i) raw[i] = c->rng();
+  }
+  c->raw_slot = slot ^ 1;
+  c->raw_last = slot;
   const auto t2 = std::chrono::steady_clock::now();
   c->nce_wait_s += std::chrono::duration<double>(t1 - t0).count();
   c->nce_gen_s += std::chrono::duration<double>(t2 - t1).count();
@@ -798,6 +829,37 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights) {
   c->nce_P = P;
   c->nce_N = N;
   c->nce_pending = true;
+}
+
+// After the window prepared by nce_prepare has been launched: rng moves to
+// the consumed point, then the outputs a next window of the same shape can
+// take at most (every position unmasked) are drawn into the other staging
+// slot while the device works -- what is left of the queue first, then
+// rng_ahead.  The sequence of outputs is the generator's either way.
+void nce_predraw(dl_ctx* c, int64_t T, int64_t B) {
+  const int64_t cap_n = 2 * T * B * c->nce_k;
+  const int cur = c->raw_last, nxt = cur ^ 1;
+  int64_t have = 0;
+  unsigned long long* dst = static_cast<unsigned long long*>(c->raw_pin[nxt]);
+  if (cap_n > c->raw_cap) {
+    if (c->pre_used > 0) c->rng.discard(c->pre_used);
+    c->pre_n = 0;
+    c->pre_used = 0;
+    return;
+  }
+  DL_CUDA(cudaEventSynchronize(c->raw_ev[nxt]));  // its last upload (two windows back)
+  if (c->pre_used > 0) {
+    c->rng.discard(c->pre_used);
+    have = c->pre_n - c->pre_used;
+    if (have > 0)
+      std::memcpy(dst, static_cast<unsigned long long*>(c->raw_pin[cur]) + c->pre_used, have * 8);
+  } else {
+    c->rng_ahead = c->rng;
+  }
+  for (; have < cap_n; ++have) dst[have] = c->rng_ahead();
+  c->pre_n = have;
+  c->pre_slot = nxt;
+  c->pre_used = 0;
 }
 
 // One window with device-resident inputs (x_d, y_d, w_d, htape[0]).
@@ -1735,7 +1797,7 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
                          loss, positions, applied);
       return;
     }
-    if (c->loss_mode == 0) nce_prepare(c, T, B, weights);
+    if (c->loss_mode == 0) nce_prepare(c, T, B, weights, /*predraw=*/true);
     const int64_t TB = T * B, BH = B * c->H;
     // H2D of the window: page-locked caller buffers are copied from directly,
     // pageable ones through one pinned staging buffer
@@ -1762,6 +1824,9 @@ int window_call(dl_ctx* c, const char* who, int64_t T, int64_t B, const uint32_t
     } else {
       run_window(c, T, B, loss_scale, clip, grads);
     }
+    // (NCE: the next window's draws on the host while the device runs this
+    // one; before the D2H below, which blocks until the window is done)
+    if (c->loss_mode == 0) nce_predraw(c, T, B);
     // loss, positions, non-finite flag: adjacent on the device (dl_create)
     struct { double l; unsigned long long p; int bad; int pad; } res{};
     static_assert(sizeof(res) == 24, "result block layout");
@@ -2569,6 +2634,7 @@ int dl_set_rng_state(dl_ctx* c, const uint64_t state[313]) {
   for (int i = 0; i < 313; ++i) ss << state[i] << ' ';
   ss >> c->rng;
   if (!ss) return fail(c, DL_EINVAL, "dl_set_rng_state: bad state");
+  c->pre_n = 0;
   drop_graphs(c);
   return DL_OK;
 }

@@ -96,6 +96,36 @@ def test_nce_window_sequence_rng_continues(orc):
         assert np.array_equal(m.rng_state(), st)
 
 
+def test_nce_window_predrawn_noise_across_shapes_and_reseed(orc):
+    """dl_window draws the next window's noise while the device runs the
+    current one (runtime.cu nce_predraw): windows that grow past the queue,
+    shrink below it, train (bptt + rmsprop) or reseed the generator in
+    between all consume exactly the reference's stream."""
+    import paper_1502_00512_b200 as dl
+    V, H, B, k = 300, 24, 6, 8
+    rng = np.random.default_rng(3)
+    params = orc.init_uniform(V, H, 9)
+    counts = rng.integers(1, 20, V).astype(np.float64)
+    noise = orc.noise_build(counts, k, 1e-8)
+    st = orc.mt_state(42)
+    m = nce_model(dl, params, counts, k, 1e-8, "fp32", seed=42)
+    for i, T in enumerate((4, 4, 6, 3, 3, -7, 4, 4)):
+        if T < 0:  # reseed: the queue drawn from the old state is dropped
+            st = orc.mt_state(-T)
+            m.set_rng_state(dl.rng_seed_state(-T))
+            continue
+        x, y, w = rand_window(rng, T, B, V, 0.2 if i % 2 else 0.0)
+        h0 = np.zeros((B, H), np.float32)
+        want = orc.bptt_nce(m.params(), 0, x, y, w, h0, 0.1, 1.0, noise, st,
+                            compute_grads=False)
+        if i == 6:
+            res, _, _ = dl.train_window(m, dl.WindowBatch(x, y, w), h0, 0.1, 1.0, 0.01)
+        else:
+            res, _ = dl.bptt_run(m, dl.WindowBatch(x, y, w), h0, 0.1, 1.0, compute_grads=False)
+        assert res.loss == pytest.approx(want["loss"], rel=1e-6), i
+        assert np.array_equal(m.rng_state(), st), i
+
+
 @pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "nce_*.npz"))))
 def test_nce_window_matches_reference_fixture(path):
     """Against the reference's own NCE window (tests/golden, made by
