@@ -652,7 +652,7 @@ __global__ void k_sum_rows(const double* __restrict__ v, const uint8_t* __restri
 // and the global stream index is r*B + b, so processing order i maps to
 // t = T-1 - i/(G*B), r = (i % (G*B)) / B, b = i % B.
 constexpr int kSortThreads = 1024;
-constexpr int kEmbedShort = 8;  // segments up to this many rows: k_embed_short
+constexpr int kEmbedShort = 64;  // segments up to this many rows: k_embed_short
 
 __device__ __forceinline__ int64_t gathered_pos(int64_t i, int64_t T, int64_t B, int64_t G) {
   const int64_t GB = G * B;
@@ -739,12 +739,13 @@ k_embed_radix(const uint32_t* __restrict__ x, int64_t T, int64_t B, int64_t G, i
 //   k_embed_short: a warp per (segment of <= kEmbedShort rows, 1024-column
 //     chunk), grid-stride; each row's columns are 8 float4 loads per lane,
 //     all in flight, rows added in order;
-//   k_embed_long: a block per (long segment, 32-column chunk); the block's 8
-//     warps stage up to 256 rows x 32 columns in shared memory with every
-//     load in flight (lane = column), then warp 0 adds them in order.
+//   k_embed_long: a block per (long segment, 32-column chunk); seven warps
+//     stage the next pass of rows x 32 columns in shared memory with every
+//     load in flight (lane = column) while warp 0 adds the current pass in
+//     order (double-buffered).
 // Both sum every word's rows in exactly the reference's float order.
 constexpr int kShortWarps = 8;     // warps per k_embed_short block
-constexpr int kLongRows = 256;     // rows staged per pass in k_embed_long
+constexpr int kLongPass = 7 * 24;  // rows staged per pass in k_embed_long (7 warps x 24)
 
 __global__ void __launch_bounds__(32 * kShortWarps)
 k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__ seg_start,
@@ -776,17 +777,25 @@ k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__
       }
       continue;
     }
-    float4 acc[8];
+    float4 acc[8], v[8], nv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = a; i < e; ++i) {
+    auto load_row = [&](int i, float4 (&dst)[8]) {
       const float* src = dpre + (int64_t)__ldg(order_pos + i) * H;
-      const float sc = order_scale ? __ldg(order_scale + i) : 1.0f;
-      float4 v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int64_t j = c0 + 4 * (lane + 32 * q);
-        if (j < H) v[q] = __ldg(reinterpret_cast<const float4*>(src + j));
+        if (j < H) dst[q] = __ldg(reinterpret_cast<const float4*>(src + j));
+      }
+    };
+    load_row(a, v);
+    float sc = order_scale ? __ldg(order_scale + a) : 1.0f;
+    for (int i = a; i < e; ++i) {
+      // the next row's loads go out before this row's adds
+      float nsc = 1.0f;
+      if (i + 1 < e) {
+        load_row(i + 1, nv);
+        nsc = order_scale ? __ldg(order_scale + i + 1) : 1.0f;
       }
       // (a scaled row is the reference's axpy_row: acc += s * x, two roundings)
 #pragma unroll
@@ -796,6 +805,9 @@ k_embed_short(const float* __restrict__ dpre, int64_t H, const int* __restrict__
         acc[q].z = __fadd_rn(acc[q].z, __fmul_rn(sc, v[q].z));
         acc[q].w = __fadd_rn(acc[q].w, __fmul_rn(sc, v[q].w));
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = nv[q];
+      sc = nsc;
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -815,38 +827,76 @@ k_embed_long(const float* __restrict__ dpre, int64_t H, const int* __restrict__ 
              const int* __restrict__ long_list, const int* __restrict__ n_long,
              const int* __restrict__ order_pos, const float* __restrict__ order_scale,
              float* __restrict__ rows, float clip, int* nonfinite) {
-  __shared__ float tile[kLongRows][32];
-  __shared__ int spos[kLongRows];
-  __shared__ float sscale[kLongRows];
+  // warps 1..7 stage pass p+1 (kLongPass rows x 32 columns, every load in
+  // flight, the row positions of pass p+2 already in registers) while warp 0
+  // adds pass p in order from the other buffer: a word with ~18,000 records
+  // (NCE's eos noise) is bound by its add chain, not by one L2 round trip
+  // per pass
+  constexpr int kPer = kLongPass / 7;  // rows per staging warp per pass
+  __shared__ float tile[2][kLongPass][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t nchunk = (H + 31) / 32;
   const int64_t items = (int64_t)__ldg(n_long) * nchunk;
   bool bad = false;
-  // grid-stride over (long segment, 32-column chunk)
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int slot = __ldg(long_list + it / nchunk);
     const int64_t j = (it % nchunk) * 32 + lane;
     const int a = __ldg(seg_start + slot), e = __ldg(seg_start + slot + 1);
+    const int npass = (e - a + kLongPass - 1) / kLongPass;
+    int pos[kPer];
+    float sc[kPer];
+    auto fetch = [&](int p) {  // row positions / scales of pass p (staging warps)
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = a + p * kLongPass + (warp - 1) + 7 * u;
+        pos[u] = (p < npass && i < e) ? __ldg(order_pos + i) : -1;
+        sc[u] = (p < npass && i < e && order_scale) ? __ldg(order_scale + i) : 1.0f;
+      }
+    };
+    float v[kPer], vs[kPer];
+    auto load = [&] {  // pass rows (positions in pos) -> v, loads left in flight
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        v[u] = (pos[u] >= 0 && j < H) ? __ldg(dpre + (int64_t)pos[u] * H + j) : 0.f;
+        vs[u] = sc[u];
+      }
+    };
+    auto store = [&](int b) {  // (the first use of the loaded values)
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) tile[b][(warp - 1) + 7 * u][lane] = __fmul_rn(vs[u], v[u]);
+    };
+    if (warp > 0) {
+      fetch(0);
+      load();
+      store(0);
+      fetch(1);
+      load();  // pass 1, stored during pass 0's adds
+      fetch(2);
+    }
+    __syncthreads();
     float acc = 0.f;
-    for (int base = a; base < e; base += kLongRows) {
-      const int cnt = min(kLongRows, e - base);
-      if (threadIdx.x < cnt) {
-        spos[threadIdx.x] = __ldg(order_pos + base + threadIdx.x);
-        sscale[threadIdx.x] = order_scale ? __ldg(order_scale + base + threadIdx.x) : 1.0f;
-      }
-      __syncthreads();
-      float v[kLongRows / 8];
+    for (int p = 0; p < npass; ++p) {
+      if (warp > 0) {
+        // pass p+1's values were loaded an iteration ago; pass p+2's loads
+        // go out now and land while the next passes are added
+        if (p + 1 < npass) store((p + 1) & 1);
+        if (p + 2 < npass) {
+          load();
+          fetch(p + 3);
+        }
+      } else {
+        const int cnt = min(kLongPass, e - a - p * kLongPass);
+        const float(*t)[32] = tile[p & 1];
+        int r = 0;
+        for (; r + 16 <= cnt; r += 16) {
+          float x[16];
 #pragma unroll
-      for (int u = 0; u < kLongRows / 8; ++u) {
-        const int r = warp + 8 * u;
-        v[u] = (r < cnt && j < H) ? __fmul_rn(sscale[r], __ldg(dpre + (int64_t)spos[r] * H + j))
-                                  : 0.f;
-      }
+          for (int u = 0; u < 16; ++u) x[u] = t[r + u][lane];
 #pragma unroll
-      for (int u = 0; u < kLongRows / 8; ++u) tile[warp + 8 * u][lane] = v[u];
-      __syncthreads();
-      if (warp == 0)
-        for (int r = 0; r < cnt; ++r) acc = __fadd_rn(acc, tile[r][lane]);
+          for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, x[u]);
+        }
+        for (; r < cnt; ++r) acc = __fadd_rn(acc, t[r][lane]);
+      }
       __syncthreads();
     }
     if (warp == 0 && j < H) {

@@ -5,7 +5,7 @@ TAG=${1:-tmp}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
-    python bench.py --steps 2 --warmup 3 --e2e-steps 0 --profile-steps 0 --no-cpu-baseline \
+    python bench.py --steps 2 --warmup 3 --no-e2e --secondary= --profile-steps 0 --no-cpu-baseline \
     > gpurun_out/${TAG}_launches.log 2>&1
 python - "$TAG" <<'PY'
 import sys

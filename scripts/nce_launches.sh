@@ -1,4 +1,4 @@
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/nce_launches.csv python bench.py --loss nce --steps 2 --warmup 2 --e2e-steps 0 --profile-steps 0 --no-cpu-baseline > /dev/null 2>&1
+mkdir -p gpurun_out; ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/nce_launches.csv python bench.py --loss nce --steps 2 --warmup 2 --no-e2e --secondary= --profile-steps 0 --no-cpu-baseline > /dev/null 2>&1
 python - <<'PY'
 import sys
 sys.path.insert(0, "scripts")
