@@ -1,7 +1,7 @@
 #!/bin/bash
 # Tuning: run the C3 bench for the default build and each variants/<name>.
 #   scripts/bench_variants.sh [bench args...]
-ARGS=${*:-"--steps 50 --e2e-steps 0 --no-cpu-baseline"}
+ARGS=${*:-"--steps 50 --no-e2e --no-cpu-baseline --secondary="}
 run() {
   local name=$1
   out=$(timeout 300 python bench.py $ARGS 2>&1 | grep '^{' | tail -1)
