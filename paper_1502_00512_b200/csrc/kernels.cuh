@@ -33,12 +33,15 @@ void nce_records(const uint8_t* w, const uint32_t* y, int64_t T, int64_t B, int6
                  const unsigned long long* raw, const double* prob, const uint32_t* alias,
                  int64_t V, uint32_t* pos_of, int* first, uint32_t* rec_word, uint32_t* rec_row,
                  uint32_t* proc_r, cudaStream_t st);
+// w_bf: score / backpropagate against the bf16 shadow of W_out (bf16 mode)
 void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
-                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st);
+                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st,
+                const bf16* w_bf = nullptr);
 void nce_loss(const float* score, const uint32_t* rec_word, const double* ln_kq, int64_t P,
               int K1, double scale, double* loss_pos, float* ds, cudaStream_t st);
 void nce_dh(const float* w_out, int64_t H, const uint32_t* rec_word, const uint32_t* rec_row,
-            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st);
+            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st,
+            const bf16* w_bf = nullptr);
 size_t nce_sort_temp_bytes(int64_t N);
 // sparse W_out gradient rows (slot order = by word), clipped: rows / words /
 // *n_rows on the device

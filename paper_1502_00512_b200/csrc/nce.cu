@@ -31,8 +31,23 @@
 namespace dl {
 namespace {
 
-// one record per 8 threads: thread q owns the reference's lane q
-__global__ void k_nce_scores(const float* __restrict__ h, const float* __restrict__ w_out,
+__device__ __forceinline__ float ld_f(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ld_f(const bf16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float4 ld_f4(const float* row, int64_t i4) {
+  return __ldg(reinterpret_cast<const float4*>(row) + i4);
+}
+__device__ __forceinline__ float4 ld_f4(const bf16* row, int64_t i4) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(row) + i4);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// one record per 8 threads: thread q owns the reference's lane q.  W (the
+// output rows) is the fp32 master, or (bf16 mode) its bf16 shadow: half the
+// bytes of the row gathers that bound this kernel and k_nce_dh
+template <typename X, typename W>
+__global__ void k_nce_scores(const X* __restrict__ h, const W* __restrict__ w_out,
                              int64_t H, const uint32_t* __restrict__ rec_word,
                              const uint32_t* __restrict__ rec_row, int64_t N,
                              float* __restrict__ score) {
@@ -41,14 +56,14 @@ __global__ void k_nce_scores(const float* __restrict__ h, const float* __restric
   const int q = (int)(gt % 8);
   const bool valid = r < N;
   double s = 0.0;
-  const float* x = nullptr;
-  const float* y = nullptr;
+  const X* x = nullptr;
+  const W* y = nullptr;
   const int64_t H8 = (H / 8) * 8;
   if (valid) {
     x = h + (int64_t)rec_row[r] * H;
     y = w_out + (int64_t)rec_word[r] * H;
     for (int64_t i = 0; i < H8; i += 8)
-      s = __dadd_rn(s, __dmul_rn((double)x[i + q], (double)y[i + q]));
+      s = __dadd_rn(s, __dmul_rn((double)x[i + q], (double)ld_f(y + i + q)));
   }
   // ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) + tail
   const int base = (threadIdx.x % 32) & ~7;
@@ -57,7 +72,8 @@ __global__ void k_nce_scores(const float* __restrict__ h, const float* __restric
   for (int k = 0; k < 8; ++k) l[k] = __shfl_sync(0xffffffffu, s, base + k);
   if (valid && q == 0) {
     double tail = 0.0;
-    for (int64_t i = H8; i < H; ++i) tail = __dadd_rn(tail, __dmul_rn((double)x[i], (double)y[i]));
+    for (int64_t i = H8; i < H; ++i)
+      tail = __dadd_rn(tail, __dmul_rn((double)x[i], (double)ld_f(y + i)));
     const double tot = __dadd_rn(__dadd_rn(__dadd_rn(l[0], l[1]), __dadd_rn(l[2], l[3])),
                                  __dadd_rn(__dadd_rn(l[4], l[5]), __dadd_rn(l[6], l[7])));
     score[r] = (float)__dadd_rn(tot, tail);
@@ -69,34 +85,80 @@ __device__ __forceinline__ double softplus_d(double x) {
 }
 __device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + exp(-x)); }
 
+// a warp per position: the records' terms in parallel (lane = record within
+// a 32-record chunk), their sum in the reference's record order by lane 0
+// (backprop.hpp:136-150: L += scale softplus(..) in j order)
 __global__ void k_nce_loss(const float* __restrict__ score, const uint32_t* __restrict__ rec_word,
                            const double* __restrict__ ln_kq, int64_t P, int K1, double scale,
                            double* __restrict__ loss_pos, float* __restrict__ ds) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= P) return;
+  const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (p >= P) return;  // (whole warps)
   const int64_t r0 = p * K1;
-  const double at = (double)score[r0] - ln_kq[rec_word[r0]];
-  double L = scale * softplus_d(-at);
-  ds[r0] = (float)(-scale * sigmoid_d(-at));
-  for (int j = 1; j < K1; ++j) {
-    const double a = (double)score[r0 + j] - ln_kq[rec_word[r0 + j]];
-    L += scale * softplus_d(a);
-    ds[r0 + j] = (float)(scale * sigmoid_d(a));
+  double L = 0.0;
+  for (int j0 = 0; j0 < K1; j0 += 32) {
+    const int j = j0 + lane;
+    double t = 0.0;
+    if (j < K1) {
+      const double a = (double)score[r0 + j] - ln_kq[rec_word[r0 + j]];
+      if (j == 0) {  // the target record
+        t = scale * softplus_d(-a);
+        ds[r0] = (float)(-scale * sigmoid_d(-a));
+      } else {
+        t = scale * softplus_d(a);
+        ds[r0 + j] = (float)(scale * sigmoid_d(a));
+      }
+    }
+    const int n = min(32, K1 - j0);
+    for (int i = 0; i < n; ++i) {
+      const double ti = __shfl_sync(0xffffffffu, t, i);
+      L = (j0 == 0 && i == 0) ? ti : L + ti;
+    }
   }
-  loss_pos[p] = L;
+  if (lane == 0) loss_pos[p] = L;
 }
 
 // dh[row] = sum_j ds_j * W_out[w_j] in record order (float, two roundings)
-__global__ void k_nce_dh(const float* __restrict__ w_out, int64_t H,
+template <typename W>
+__global__ void k_nce_dh(const W* __restrict__ w_out, int64_t H,
                          const uint32_t* __restrict__ rec_word, const uint32_t* __restrict__ rec_row,
                          const float* __restrict__ ds, int K1, float* __restrict__ dh) {
   const int64_t p = blockIdx.x;
   const int64_t r0 = p * K1;
   float* out = dh + (int64_t)rec_row[r0] * H;
+  if ((H % 4) == 0) {
+    // float4 columns; eight records' rows in flight before their adds
+    const int64_t H4 = H / 4;
+    for (int64_t i4 = threadIdx.x; i4 < H4; i4 += blockDim.x) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      auto add = [&](float d, float4 w) {
+        acc.x = __fadd_rn(acc.x, __fmul_rn(d, w.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(d, w.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(d, w.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(d, w.w));
+      };
+      int j = 0;
+      for (; j + 8 <= K1; j += 8) {
+        float4 w[8];
+        float d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          d[u] = __ldg(ds + r0 + j + u);
+          w[u] = ld_f4(w_out + (int64_t)__ldg(rec_word + r0 + j + u) * H, i4);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) add(d[u], w[u]);
+      }
+      for (; j < K1; ++j)
+        add(__ldg(ds + r0 + j), ld_f4(w_out + (int64_t)__ldg(rec_word + r0 + j) * H, i4));
+      reinterpret_cast<float4*>(out)[i4] = acc;
+    }
+    return;
+  }
   for (int64_t i = threadIdx.x; i < H; i += blockDim.x) {
     float acc = 0.f;
     for (int j = 0; j < K1; ++j)
-      acc = __fadd_rn(acc, __fmul_rn(ds[r0 + j], w_out[(int64_t)rec_word[r0 + j] * H + i]));
+      acc = __fadd_rn(acc, __fmul_rn(ds[r0 + j], ld_f(w_out + (int64_t)rec_word[r0 + j] * H + i)));
     out[i] = acc;
   }
 }
@@ -242,24 +304,31 @@ void nce_records(const uint8_t* w, const uint32_t* y, int64_t T, int64_t B, int6
 }
 
 void nce_scores(const float* h, const float* w_out, int64_t H, const uint32_t* rec_word,
-                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st) {
+                const uint32_t* rec_row, int64_t N, float* score, cudaStream_t st,
+                const bf16* w_bf) {
   if (N <= 0) return;
   const int64_t threads = N * 8;
-  k_nce_scores<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(h, w_out, H, rec_word, rec_row,
-                                                                  N, score);
+  const unsigned g = (unsigned)((threads + 255) / 256);
+  if (w_bf)
+    k_nce_scores<<<g, 256, 0, st>>>(h, w_bf, H, rec_word, rec_row, N, score);
+  else
+    k_nce_scores<<<g, 256, 0, st>>>(h, w_out, H, rec_word, rec_row, N, score);
 }
 
 void nce_loss(const float* score, const uint32_t* rec_word, const double* ln_kq, int64_t P,
               int K1, double scale, double* loss_pos, float* ds, cudaStream_t st) {
   if (P <= 0) return;
-  k_nce_loss<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(score, rec_word, ln_kq, P, K1, scale,
-                                                          loss_pos, ds);
+  k_nce_loss<<<(unsigned)((P * 32 + 127) / 128), 128, 0, st>>>(score, rec_word, ln_kq, P, K1,
+                                                               scale, loss_pos, ds);
 }
 
 void nce_dh(const float* w_out, int64_t H, const uint32_t* rec_word, const uint32_t* rec_row,
-            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st) {
+            const float* ds, int64_t P, int K1, float* dh, cudaStream_t st, const bf16* w_bf) {
   if (P <= 0) return;
-  k_nce_dh<<<(unsigned)P, 256, 0, st>>>(w_out, H, rec_word, rec_row, ds, K1, dh);
+  if (w_bf)
+    k_nce_dh<<<(unsigned)P, 256, 0, st>>>(w_bf, H, rec_word, rec_row, ds, K1, dh);
+  else
+    k_nce_dh<<<(unsigned)P, 256, 0, st>>>(w_out, H, rec_word, rec_row, ds, K1, dh);
 }
 
 size_t nce_sort_temp_bytes(int64_t N) {

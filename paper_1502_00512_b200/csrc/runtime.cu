@@ -978,7 +978,9 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
                 c->rec_word_d, c->rec_row_d, c->proc_r_d, st);
     c->nce_pending = false;
     c->launches += 2;
-    nce_scores(Hn, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st);
+    nce_scores(Hn, c->w_out, H, c->rec_word_d, c->rec_row_d, c->nce_N, c->score_d, st,
+               tc(c) ? c->w_out_bf : nullptr);
+    c->launches++;
     nce_loss(c->score_d, c->rec_word_d, c->ln_kq_d, c->nce_P, K1, scale, c->loss_pos_d, c->ds_d,
              st);
     sum_rows(c->loss_pos_d, nullptr, c->nce_P, c->d_loss, c->d_pos, st);
@@ -1153,7 +1155,8 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     Phase p(c, "nce_dh");
     float* dhn = nce_dp ? c->ng_dh : c->dh_out;
     DL_CUDA(cudaMemsetAsync(dhn, 0, T * Bn * H * sizeof(float), st));
-    nce_dh(c->w_out, H, c->rec_word_d, c->rec_row_d, c->ds_d, c->nce_P, c->nce_k + 1, dhn, st);
+    nce_dh(c->w_out, H, c->rec_word_d, c->rec_row_d, c->ds_d, c->nce_P, c->nce_k + 1, dhn, st,
+           tc(c) ? c->w_out_bf : nullptr);
     c->launches++;
     if (nce_dp)  // this rank's rows of the global window
       DL_CUDA(cudaMemcpy2DAsync(c->dh_out, B * H * 4, c->ng_dh + c->rank * B * H, Bn * H * 4,
