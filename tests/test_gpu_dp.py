@@ -34,6 +34,41 @@ def test_gathered_embed_follows_global_processing_order():
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("H", [100, 256, 2048])
+def test_embed_rows_all_segment_lengths_bitexact(H):
+    """W_in gradient rows for segments of every length class (kernels.cu):
+    1-64 rows on the warp kernel (next row's loads in flight), 65-168 rows
+    (one staged pass of k_embed_long) and ~500 rows (double-buffered
+    passes): each word's rows summed in the reference's processing order,
+    bit-exact; H = 100 takes the unaligned scalar paths."""
+    import paper_1502_00512_b200 as dl
+    from paper_1502_00512_b200._lib import check, load
+    G, T, B, V = 1, 16, 64, 400
+    rng = np.random.default_rng(H)
+    x = rng.integers(20, V, (G, T, B)).astype(np.uint32)
+    flat = x.reshape(-1)
+    pos = rng.permutation(flat.size)
+    flat[pos[:500]] = 1      # ~500-row segment
+    flat[pos[500:600]] = 2   # 100 rows
+    for k, n in enumerate((64, 65, 40, 9, 8)):
+        off = 600 + sum((64, 65, 40, 9, 8)[:k])
+        flat[pos[off:off + n]] = 3 + k
+    d = rng.standard_normal((G, T, B, H)).astype(np.float32)
+    clip = np.float32(40.0)
+    want = np.zeros((V, H), np.float32)
+    for t in range(T - 1, -1, -1):
+        for b in range(B):
+            want[x[0, t, b]] += d[0, t, b]
+    touched = np.zeros(V, bool)
+    touched[np.unique(x)] = True
+    want[touched] = np.minimum(clip, np.maximum(-clip, want[touched]))
+    m = dl.GpuRnn(V, H, 0, "fp32")
+    got = np.empty((V, H), np.float32)
+    check(load().dl_test_embed(m.handle, G, T, B, x.ctypes.data, d.ctypes.data, float(clip),
+                               got.ctypes.data), m.handle)
+    assert np.array_equal(got, want)
+
+
 def test_concurrent_wout_update_is_bitexact(orc):
     import paper_1502_00512_b200 as dl
     V, H = 4096, 1024

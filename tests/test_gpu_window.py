@@ -109,10 +109,13 @@ def test_loss_only_window(orc):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_rmsprop_bitexact_given_identical_grads(orc, precision):
-    """rmsprop_update on injected oracle gradients: W and m bit-exact."""
+@pytest.mark.parametrize("V,H", [(64, 32), (304, 512), (200, 2048)])
+def test_rmsprop_bitexact_given_identical_grads(orc, precision, V, H):
+    """rmsprop_update on injected oracle gradients: W and m bit-exact.  H >=
+    512 runs the block-per-row kernel (kernels.cu k_rms_rows_blk) for the
+    sparse W_in rows and the dense W_out rows."""
     import paper_1502_00512_b200 as dl
-    V, H, T, B = 64, 32, 5, 3
+    T, B = 5, 3
     rng = np.random.default_rng(157)
     params = orc.init_uniform(V, H, 97)
     x, y, w = rand_window(rng, T, B, V, 0.1)
