@@ -263,6 +263,10 @@ struct dl_ctx {
   int64_t pre_n = 0;
   int pre_slot = 0;
   int64_t pre_used = 0;  // outputs of the queue the last prepared window took
+  // a caller that sets the generator's state before every window (the C++
+  // Traits drop-in: BpttOptions::rng) would have every queue dropped unused:
+  // no pre-drawing until a window comes without a dl_set_rng_state first
+  bool rng_set = false, predraw_off = false;
   bool nce_pending = false;       // records of the prepared window not built yet
   double nce_wait_s = 0.0, nce_gen_s = 0.0, nce_res_s = 0.0, nce_copy_s = 0.0;  // (DL_DEBUG)
   std::vector<uint32_t> h_ids;  // trainer: host copy of the stream (NCE draws)
@@ -795,6 +799,10 @@ void nce_prepare(dl_ctx* c, int64_t T, int64_t B, const uint8_t* weights, bool p
     c->first_d = dalloc<int>(std::max(c->capT, T) + 1);
     c->raw_cap = cap;
   }
+  if (predraw) {
+    if (!c->rng_set) c->predraw_off = false;
+    c->rng_set = false;
+  }
   if (c->pre_used > 0) {  // (a window that failed after taking its draws)
     c->rng.discard(c->pre_used);
     c->pre_n = 0;
@@ -843,7 +851,7 @@ void nce_predraw(dl_ctx* c, int64_t T, int64_t B) {
   const int cur = c->raw_last, nxt = cur ^ 1;
   int64_t have = 0;
   unsigned long long* dst = static_cast<unsigned long long*>(c->raw_pin[nxt]);
-  if (cap_n > c->raw_cap) {
+  if (cap_n > c->raw_cap || c->predraw_off) {
     if (c->pre_used > 0) c->rng.discard(c->pre_used);
     c->pre_n = 0;
     c->pre_used = 0;
@@ -2649,7 +2657,9 @@ int dl_set_rng_state(dl_ctx* c, const uint64_t state[313]) {
   for (int i = 0; i < 313; ++i) ss << state[i] << ' ';
   ss >> c->rng;
   if (!ss) return fail(c, DL_EINVAL, "dl_set_rng_state: bad state");
+  if (c->pre_n > 0) c->predraw_off = true;  // (that queue was drawn for nothing)
   c->pre_n = 0;
+  c->rng_set = true;
   drop_graphs(c);
   return DL_OK;
 }
