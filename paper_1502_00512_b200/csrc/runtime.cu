@@ -86,7 +86,6 @@ struct dl_ctx {
   cudaStream_t st2 = nullptr;  // side stream (W_out update during backward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sort_fork = nullptr, ev_sort_join = nullptr;  // W_in id sort on st2
-  cudaEvent_t ev_dh_fork = nullptr;  // the m_in decay on st2 beside the dh GEMM
   cudaEvent_t ev_hfinal = nullptr;  // forward recurrence done (h_final readable)
   // data-parallel + vocabulary-parallel: dh partials ready / dh reduce-scattered
   cudaEvent_t ev_dh = nullptr, ev_rs = nullptr;
@@ -122,8 +121,7 @@ struct dl_ctx {
   bool pfac = true;
   bool pf_on = false;
   bool rec_fused = false;  // this window's W_rec step ran in the dW_rec reduction
-  bool in_decay_want = false;  // run_window: issue the m_in decay beside dh
-  bool in_decayed = false;     // this window's m_in decay ran on the side stream (run_window)
+  bool in_decayed = false;  // this window's m_in decay ran on the side stream (run_window)
   float *pf_shift = nullptr, *pf_sigma = nullptr, *pf_resid = nullptr;
   const uint32_t* pf_tgt = nullptr;  // this window's output-row targets
   bf16* pf_hs = nullptr;     // diag(sigma) Hs in bf16 [MO x H] (dW_out's B operand)
@@ -896,8 +894,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   const int64_t MO = dpv ? c->nranks * TB : TB;  // output-layer rows
   c->pf_on = false;  // (set by output_layer for this window)
   c->rec_fused = false;
-  c->in_decay_want = false;
-  c->in_decayed = false;
   if (grads && !dprec) {
     // the W_in gradient's id sort depends on x only: run it on the side
     // stream under the forward recurrence (which leaves SMs free) (joined before embed_rows)
@@ -905,12 +901,15 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
     DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_sort_fork, 0));
     embed_sort(c->x_d, T, B, 1, V, c->ews, c->g_in_words, c->g_in_n, c->st2);
     c->launches++;
+    if (fuse_eta > 0.0 && std::isfinite(clip)) {
+      // this window's update cannot be rejected (a finite clip maps every
+      // gradient element to a finite value): every W_in accumulator's decay
+      // (rmsprop.hpp:84) runs here too, instead of after the backward pass
+      rms_decay(c->m_in, c->V, c->rho, nullptr, c->st2);
+      c->launches++;
+      c->in_decayed = true;
+    }
     DL_CUDA(cudaEventRecord(c->ev_sort_join, c->st2));
-    // this window's update cannot be rejected (a finite clip maps every
-    // gradient element to a finite value): every W_in accumulator's decay
-    // (rmsprop.hpp:84) runs on the side stream beside the dh GEMM (64 of the
-    // 74 SM pairs busy) instead of after the backward pass
-    c->in_decay_want = fuse_eta > 0.0 && std::isfinite(clip);
   }
   if (tc(c) && !c->h0_bf_ready) {
     f32_to_bf16(c->htape, c->htape_bf, BH, st);
@@ -1212,15 +1211,6 @@ void run_window(dl_ctx* c, int64_t T, int64_t B, double scale, float clip, bool 
   }
   // dh_out = dS . W_out   [TB x H]  (rnn.hpp:257 matmul_nn)
   auto dh = [&] {
-    if (c->in_decay_want) {
-      c->in_decay_want = false;
-      c->in_decayed = true;
-      DL_CUDA(cudaEventRecord(c->ev_dh_fork, st));
-      DL_CUDA(cudaStreamWaitEvent(c->st2, c->ev_dh_fork, 0));
-      rms_decay(c->m_in, c->V, c->rho, nullptr, c->st2);
-      c->launches++;
-      DL_CUDA(cudaEventRecord(c->ev_sort_join, c->st2));  // (joined before the W_in rows)
-    }
     Phase p(c, "dh");
     float* dst = dpv ? c->dh_all : c->dh_out;
     const int s = pick_splits(c, (int)MO, (int)H, (int)Vo, 8);
@@ -1531,7 +1521,6 @@ int dl_create(dl_ctx** out, int device, int64_t V, int64_t H, int act, int preci
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_sort_join, cudaEventDisableTiming));
-    DL_CUDA(cudaEventCreateWithFlags(&c->ev_dh_fork, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_hfinal, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_dh, cudaEventDisableTiming));
     DL_CUDA(cudaEventCreateWithFlags(&c->ev_rs, cudaEventDisableTiming));
@@ -1611,7 +1600,6 @@ int dl_destroy(dl_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->ev_sort_fork) cudaEventDestroy(c->ev_sort_fork);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
-  if (c->ev_dh_fork) cudaEventDestroy(c->ev_dh_fork);
   if (c->ev_hfinal) cudaEventDestroy(c->ev_hfinal);
   if (c->ev_dh) cudaEventDestroy(c->ev_dh);
   if (c->ev_rs) cudaEventDestroy(c->ev_rs);
